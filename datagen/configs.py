@@ -1,0 +1,84 @@
+"""Workload configurations C1..C5 (BASELINE.json `configs[0..4]`) and scaled test variants.
+
+This module is part of the seeded-input layer (`datagen/`): it holds shapes, seeds and
+search parameters only -- none of the method's arithmetic.  Both the oracle (`oracle/`)
+and the CUDA path (`paper_2604_01960_b200/`) consume what `datagen` produces.
+
+Sources
+  * BASELINE.json configs[0..4]  -> C1..C5 (N, d, storage, quantizer, nlist, nq, k, nprobe,
+    budget multiplier).
+  * SURVEY.md section 8(d) "Synthetic inputs" -> generator recipes (see `synth.py`).
+  * Seeds: base 260401960 + config index (1..5), SURVEY.md 8(d).
+"""
+from __future__ import annotations
+
+import dataclasses
+from dataclasses import dataclass, field
+
+SEED_BASE = 260401960
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str            # "C1" ... "C5" or a scaled variant such as "C2s"
+    gen: str             # generator id: "C1".."C5" (the recipe in synth.py)
+    N: int               # database size
+    d: int               # dimensionality
+    raw_dtype: str       # "f32" or "u8" (storage of raw vectors)
+    kind: str            # "pq" or "rabitq"
+    nlist: int           # IVF lists
+    M: int               # PQ sub-quantizers (0 for RaBitQ)
+    nq: int              # queries per batch
+    k: int               # top-k
+    nprobe: int          # lists probed per query
+    budget: int          # candidate budget (n_cand in the paper)
+    seed: int            # base seed of the generator
+    # index-build knobs (deterministic; the serialized file is the contract)
+    kmeans_iters: int = 10
+    kmeans_train_per_list: int = 64
+    pq_train: int = 65536
+    pq_iters: int = 12
+    extra: dict = field(default_factory=dict, compare=False, hash=False)
+
+    @property
+    def dsub(self) -> int:
+        return self.d // self.M if self.M else 0
+
+    def replace(self, **kw) -> "Config":
+        return dataclasses.replace(self, **kw)
+
+
+# BASELINE.json configs, verbatim shapes.
+C1 = Config("C1", "C1", 100_000, 128, "f32", "pq", 256, 16, 100, 5_000, 32, 10_000, SEED_BASE + 1,
+            kmeans_iters=20)
+C2 = Config("C2", "C2", 1_000_000, 128, "f32", "pq", 4_096, 32, 1_000, 10_000, 128, 20_000,
+            SEED_BASE + 2)
+C3 = Config("C3", "C3", 1_000_000, 960, "f32", "rabitq", 4_096, 0, 1_000, 5_000, 256, 15_000,
+            SEED_BASE + 3)
+C4 = Config("C4", "C4", 10_000_000, 96, "f32", "pq", 16_384, 48, 10_000, 50_000, 512, 75_000,
+            SEED_BASE + 4)
+C5 = Config("C5", "C5", 100_000_000, 128, "u8", "pq", 65_536, 32, 10_000, 20_000, 1_024, 40_000,
+            SEED_BASE + 5)
+
+FULL = {c.name: c for c in (C1, C2, C3, C4, C5)}
+
+# Scaled variants used by the parity tests: same generators and structure, sizes the CPU oracle
+# finishes in seconds while still spanning many tiles and ragged list tails.
+SMALL = {
+    "C1t": C1.replace(name="C1t", N=6_000, nlist=32, nq=12, k=300, nprobe=6, budget=600),
+    "C1s": C1.replace(name="C1s", nq=24),
+    "C2s": C2.replace(name="C2s", N=120_000, nlist=512, nq=24, k=1_500, nprobe=24, budget=3_000,
+                      kmeans_iters=8),
+    "C3s": C3.replace(name="C3s", N=40_000, nlist=128, nq=12, k=500, nprobe=12, budget=1_500,
+                      kmeans_iters=8),
+    "C4s": C4.replace(name="C4s", N=200_000, nlist=512, nq=24, k=2_000, nprobe=32, budget=3_000,
+                      kmeans_iters=6),
+    "C5s": C5.replace(name="C5s", N=200_000, nlist=512, nq=24, k=1_500, nprobe=32, budget=3_000,
+                      kmeans_iters=6),
+}
+
+ALL = {**FULL, **SMALL}
+
+
+def get(name: str) -> Config:
+    return ALL[name]

@@ -1,0 +1,346 @@
+"""CPU oracle of the BBC large-k IVF query path -- TEST INFRASTRUCTURE ONLY.
+
+Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s cpu_baseline / `--impl reference` leg
+may import this module.  The product path (`paper_2604_01960_b200`) never imports it, and this
+module imports nothing from the product.  It shares no code with the CUDA path: the only common
+dependency is the seeded-input layer `datagen/` (generators, index file), which holds none of the
+method's arithmetic.
+
+What it computes (steps O1-O9; "P:Lnnn" = line of PAPER.md):
+
+  O1 coarse probe      d^2(q, c_j) for all lists, keep the nprobe smallest by (d^2, j)
+                       (route; nearest-first order)
+  O2 query tables      PQ: LUT[m][c] = sum_t (q_t - C[m][c][t])^2   ("pre-compute distances
+                       between the query and the codebook vectors")
+                       RaBitQ: u = P^T q, per probed list the 4-bit query code (B_q = 4)
+  O3 estimate          PQ: est = sum_m LUT[m][code_m] ("use these pre-computed distances to
+                       efficiently estimate"); RaBitQ: unbiased inner-product estimator
+  O4 sample            codebook generation from the nearest clusters
+  O5 edges             d_min = smallest, d_max = budget-th smallest estimate of the sample
+                       ("partial sort ... derive d_min and d_max from the local top-k")
+                       equal-width cells, Eq. 6 with an explicit overflow cell
+  O6 histogram         Push: bucket id of every probed object (Alg. 1 l.1-4)
+  O7 threshold         Update: first bucket whose cumulative count reaches the budget
+                       (Alg. 1 l.5-11; ">=" per Fig. 3)
+  O8 superset          Collect l.19-21: all objects in buckets <= tau (superset P:L209)
+  O9 re-rank, select   exact distance of every superset object and the k
+                       smallest by (d^2, id)
+
+Floating-point conventions.  Every quantity that feeds a discrete
+decision (probe order, LUT, estimate, bucket) is evaluated in fp32 in the fixed order written
+below, with each +,-,*,/ rounded separately (no fused multiply-add): that is the kernel's
+precision, and both sides take the decision in it.  Exact re-rank distances are accumulated in
+fp64 and rounded to fp32 once.
+
+Parity pins (tests/test_oracle.py): brute force on tiny inputs, the LUT identity, the closed form
+tau = cell(budget-th smallest estimate), the superset invariants, Fig. 3 of the paper, Eq. 3, the
+RaBitQ closed forms and error bound, and full-probe/unlimited-budget == brute force.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+F32 = np.float32
+TAU_INF = 1 << 30          # "tau = infinity" (Alg. 1 l.11): every probed object is a candidate
+NCELL = 256                # 255 regular equal-width cells + 1 overflow cell (reading R3)
+SAMPLE_MIN_LISTS = 8       # "5-10 nearest clusters", reading R5
+
+
+# ----------------------------------------------------------------------------------------------
+# O1  coarse probe
+# ----------------------------------------------------------------------------------------------
+def coarse_d2(Q: np.ndarray, C: np.ndarray) -> np.ndarray:
+    """d^2(q, c_j) [nq x nlist]: acc = 0; for t ascending: diff = q_t - c_t; acc = acc + diff*diff."""
+    Q = np.asarray(Q, dtype=F32)
+    C = np.asarray(C, dtype=F32)
+    acc = np.zeros((len(Q), len(C)), dtype=F32)
+    for t in range(Q.shape[1]):
+        diff = Q[:, t, None] - C[None, :, t]
+        acc = acc + diff * diff
+    return acc
+
+
+def probe(Q: np.ndarray, C: np.ndarray, nprobe: int):
+    """The nprobe nearest lists per query, nearest first, ties by list id.  -> (probe i32, rq2 f32)."""
+    d2 = coarse_d2(Q, C)
+    nq, nlist = d2.shape
+    pr = np.empty((nq, nprobe), dtype=np.int32)
+    rq = np.empty((nq, nprobe), dtype=F32)
+    j = np.arange(nlist)
+    for i in range(nq):
+        order = np.lexsort((j, d2[i]))[:nprobe]
+        pr[i] = order
+        rq[i] = d2[i][order]
+    return pr, rq
+
+
+# ----------------------------------------------------------------------------------------------
+# O2/O3  PQ
+# ----------------------------------------------------------------------------------------------
+def pq_lut(q: np.ndarray, books: np.ndarray) -> np.ndarray:
+    """LUT[m][c] = sum_{t < dsub} (q[m*dsub + t] - C[m][c][t])^2, t ascending, fp32 [M x 256]."""
+    M, K, ds = books.shape
+    qs = np.asarray(q, dtype=F32).reshape(M, ds)
+    acc = np.zeros((M, K), dtype=F32)
+    for t in range(ds):
+        diff = qs[:, t, None] - books[:, :, t]
+        acc = acc + diff * diff
+    return acc
+
+
+def pq_est(lut: np.ndarray, codes: np.ndarray) -> np.ndarray:
+    """est = LUT[0][c_0] + LUT[1][c_1] + ... + LUT[M-1][c_{M-1}], left to right, fp32."""
+    acc = lut[0][codes[:, 0]]
+    for m in range(1, lut.shape[0]):
+        acc = acc + lut[m][codes[:, m]]
+    return acc
+
+
+# ----------------------------------------------------------------------------------------------
+# O2/O3  RaBitQ (1-bit codes, B_q = 4-bit query, estimator of gao2024rabitq)
+# ----------------------------------------------------------------------------------------------
+def rabitq_rotate(q: np.ndarray, P: np.ndarray) -> np.ndarray:
+    """u = P^T q: u_i = sum_t P[t][i] q_t, t ascending over the d real dims (the zero padding
+    up to D adds +-0 and cannot change a sum), fp32."""
+    q = np.asarray(q, dtype=F32)
+    acc = np.zeros(P.shape[1], dtype=F32)
+    for t in range(len(q)):
+        acc = acc + P[t] * q[t]
+    return acc
+
+
+def rabitq_query_code(u: np.ndarray, wL: np.ndarray, rq2: F32):
+    """Per (query, list): q' = (u - w_L)/r, 4-bit scalar quantisation of q' (round half up).
+
+    Returns (qbar int [D], consts (c1, c2, c3) fp32, r fp32).  With D the padded dimension,
+    <x_bar, q'> ~= c1 * <b, qbar> + c2 * popcount(b) + c3 where x_bar = (2b - 1)/sqrt(D):
+      c1 = (2 delta)/sqrt(D), c2 = (2 v_l)/sqrt(D), c3 = -((delta * sum qbar)/sqrt(D)) - sqrt(D) v_l.
+    """
+    D = len(u)
+    r = np.sqrt(F32(rq2))
+    if r > 0:
+        qp = (u - wL) / r
+    else:
+        qp = np.zeros(D, dtype=F32)
+    vl = qp.min()
+    vr = qp.max()
+    delta = (vr - vl) / F32(15.0)
+    if delta > 0:
+        qbar = np.floor((qp - vl) / delta + F32(0.5))
+        qbar = np.clip(qbar, 0, 15).astype(np.int64)
+    else:
+        qbar = np.zeros(D, dtype=np.int64)
+    sq = F32(int(qbar.sum()))
+    sD = np.sqrt(F32(D))
+    c1 = (F32(2.0) * delta) / sD
+    c2 = (F32(2.0) * vl) / sD
+    c3 = (-((delta * sq) / sD)) - sD * vl
+    return qbar, (F32(c1), F32(c2), F32(c3)), F32(r)
+
+
+def rabitq_est(bits: np.ndarray, fac: np.ndarray, qbar: np.ndarray, consts, r: F32,
+               rq2: F32) -> np.ndarray:
+    """est d^2 = r_o^2 + r_q^2 - 2 r_o r_q <o,q>_est, <o,q>_est = <x_bar,q'>_est / g_o.
+
+    Evaluation order (fp32, each op rounded): t1 = c2*p; t2 = t1 + c3; t3 = c1*ip; oq = t3 + t2;
+    e = oq / g_o; a = r_o*r_o; s = a + rq2; f = (2*r_o)*r; est = s - f*e.
+    """
+    c1, c2, c3 = consts
+    b = np.unpackbits(bits, axis=1, bitorder="little").astype(np.int64)
+    ip = (b * qbar[None, :]).sum(1)
+    p = b.sum(1)
+    t1 = c2 * p.astype(F32)
+    t2 = t1 + c3
+    t3 = c1 * ip.astype(F32)
+    oq = t3 + t2
+    e = oq / fac[:, 1]
+    ro = fac[:, 0]
+    a = ro * ro
+    s = a + F32(rq2)
+    f = (F32(2.0) * ro) * F32(r)
+    return (s - f * e).astype(F32)
+
+
+# ----------------------------------------------------------------------------------------------
+# O4-O8  the bucket-based result buffer
+# ----------------------------------------------------------------------------------------------
+def sample_lists(sizes_in_probe_order: np.ndarray, budget: int) -> int:
+    """Number s of probe-order lists forming D_sample: the smallest s >= min(8, nprobe) whose
+    lists hold >= budget objects (reading R5).  Returns 0 when n_o <= budget (tau = infinity)."""
+    cum = np.cumsum(sizes_in_probe_order)
+    if cum[-1] <= budget:
+        return 0
+    s0 = min(SAMPLE_MIN_LISTS, len(sizes_in_probe_order))
+    s = int(np.searchsorted(cum, budget, side="left")) + 1     # first prefix with cum >= budget
+    return max(s, s0)
+
+
+def edges(sample_est: np.ndarray, budget: int):
+    """(d_min, d_max): smallest and budget-th smallest estimate of the sample."""
+    v = np.asarray(sample_est, dtype=F32)
+    return F32(v.min()), F32(np.partition(v, budget - 1)[budget - 1])
+
+
+def cells(x: np.ndarray, d_min: F32, d_max: F32) -> np.ndarray:
+    """Bucket id (Eq. 6, reading R3): 255 for x > d_max; otherwise
+    clamp(floor((x - d_min) * inv), 0, 254) with inv = 255/(d_max - d_min) in fp32;
+    0 when d_max == d_min (or inv is not finite)."""
+    x = np.asarray(x, dtype=F32)
+    out = np.full(len(x), 255, dtype=np.int64)
+    inb = ~(x > d_max)
+    width = F32(d_max - d_min)
+    inv = F32(255.0) / width if width > 0 else F32(np.inf)
+    if not np.isfinite(inv):
+        out[inb] = 0
+        return out
+    t = (x[inb] - d_min) * inv
+    out[inb] = np.clip(np.floor(t), 0, 254).astype(np.int64)
+    return out
+
+
+def threshold(H: np.ndarray, budget: int) -> int:
+    """Update (Alg. 1 l.5-11): the first bucket whose cumulative count reaches the budget."""
+    cum = np.cumsum(H)
+    hit = np.flatnonzero(cum >= budget)
+    return int(hit[0]) if len(hit) else TAU_INF
+
+
+# ----------------------------------------------------------------------------------------------
+# O9  exact re-rank and final selection
+# ----------------------------------------------------------------------------------------------
+def exact_d2(q: np.ndarray, rows: np.ndarray) -> np.ndarray:
+    """||q - x||^2 accumulated in fp64, rounded to fp32 once."""
+    diff = rows.astype(np.float64) - np.asarray(q, dtype=np.float64)[None, :]
+    return (diff * diff).sum(1).astype(F32)
+
+
+def select_topk(d2: np.ndarray, ids: np.ndarray, k: int):
+    """The k smallest by (d^2, id); pads with (-1, +inf) when fewer than k exist."""
+    order = np.lexsort((ids, d2))[:k]
+    out_ids = np.full(k, -1, dtype=np.int64)
+    out_d2 = np.full(k, np.inf, dtype=F32)
+    out_ids[:len(order)] = ids[order]
+    out_d2[:len(order)] = d2[order]
+    return out_ids, out_d2
+
+
+# ----------------------------------------------------------------------------------------------
+# the whole path
+# ----------------------------------------------------------------------------------------------
+def search(ix: dict, Q: np.ndarray, k: int, nprobe: int, budget: int, want_debug: bool = False,
+           probe_result=None):
+    """BBC search of every query in Q over the index dict `ix` (datagen.index_file.read).
+
+    Returns (ids int64 [nq x k], d2 fp32 [nq x k]) -- rows sorted by (d^2, id) -- and, when
+    want_debug, a list of per-query dicts with every intermediate of O1-O9.
+    """
+    if not (1 <= k <= ix["N"]):
+        raise ValueError("k out of range")
+    if not (1 <= nprobe <= ix["nlist"]):
+        raise ValueError("nprobe out of range")
+    if budget < k:
+        raise ValueError("budget < k")
+    Q = np.asarray(Q, dtype=F32)
+    nq = len(Q)
+    off = np.asarray(ix["list_offsets"])
+    ids_all = ix["ids"]
+    raw = ix["raw"]
+    pr, rq = probe(Q, ix["centroids"], nprobe) if probe_result is None else probe_result
+    out_ids = np.empty((nq, k), dtype=np.int64)
+    out_d2 = np.empty((nq, k), dtype=F32)
+    dbg = []
+    for i in range(nq):
+        lists = pr[i]
+        sizes = off[lists + 1] - off[lists]
+        pos = np.concatenate([np.arange(off[L], off[L + 1]) for L in lists])  # probe order
+        if ix["kind"] == "pq":
+            lut = pq_lut(Q[i], ix["codebooks"])
+            est = pq_est(lut, np.asarray(ix["codes"][pos]))
+        else:
+            u = rabitq_rotate(Q[i], ix["P"])
+            parts = []
+            for j, L in enumerate(lists):
+                qbar, cs, r = rabitq_query_code(u, ix["wL"][L], rq[i, j])
+                sl = slice(off[L], off[L + 1])
+                parts.append(rabitq_est(np.asarray(ix["bits"][sl]), np.asarray(ix["factors"][sl]),
+                                        qbar, cs, r, rq[i, j]))
+            est = np.concatenate(parts) if parts else np.zeros(0, F32)
+        n_o = len(pos)
+        s = sample_lists(sizes, budget)
+        if s == 0:
+            tau = TAU_INF
+            dmin = dmax = F32(np.nan)
+            cell = np.zeros(n_o, dtype=np.int64)       # no buckets are formed (Alg. 1 l.11)
+            H = np.zeros(NCELL, dtype=np.int64)
+            sup = np.arange(n_o)
+        else:
+            ns = int(sizes[:s].sum())
+            dmin, dmax = edges(est[:ns], budget)
+            cell = cells(est, dmin, dmax)
+            H = np.bincount(cell, minlength=NCELL)
+            tau = threshold(H, budget)
+            sup = np.flatnonzero(cell <= tau)
+        spos = pos[sup]
+        sid = np.asarray(ids_all[spos])
+        d2 = exact_d2(Q[i], np.asarray(raw[spos]))
+        out_ids[i], out_d2[i] = select_topk(d2, sid, k)
+        if want_debug:
+            dbg.append(dict(probe=lists, rq2=rq[i], n_o=n_o, s=s, d_min=dmin, d_max=dmax, H=H,
+                            tau=tau, est=est, cell=cell, pos=pos, sup_pos=spos, sup_ids=sid,
+                            sup_d2=d2))
+    return (out_ids, out_d2, dbg) if want_debug else (out_ids, out_d2)
+
+
+# ----------------------------------------------------------------------------------------------
+# paper-literal pieces used as pins
+# ----------------------------------------------------------------------------------------------
+class ResultBuffer:
+    """Algorithm 1 written out literally over an explicit codebook C (Eq. 1-2):
+    bucket B[i] = [c_i, c_{i+1}), i = 1..m; Push appends when j <= tau; Update returns the first
+    bucket whose cumulative size reaches k (">=", reading R1); Collect returns B[1..tau-1] plus
+    the top-s of B[tau].  Buckets are numbered from 1 as in Eq. 2."""
+
+    def __init__(self, codebook):
+        self.c = [float(v) for v in codebook]          # c_1 .. c_{m+1}
+        self.m = len(self.c) - 1
+        self.B = {i: [] for i in range(1, self.m + 1)}
+        self.tau = float("inf")
+
+    def bucket(self, dist: float) -> int:
+        for i in range(1, self.m + 1):
+            if self.c[i - 1] <= dist < self.c[i]:
+                return i
+        return 1 if dist < self.c[0] else self.m       # Eq. 6 clamp at both ends
+
+    def push(self, oid, dist: float) -> None:
+        j = self.bucket(dist)
+        if j <= self.tau:
+            self.B[j].append((dist, oid))
+
+    def update(self, k: int):
+        s = 0
+        for i in range(1, self.m + 1):
+            s += len(self.B[i])
+            if s >= k:
+                return i
+        return float("inf")
+
+    def relaxed_threshold(self) -> float:
+        return self.c[self.tau] if self.tau != float("inf") else float("inf")
+
+    def collect(self, k: int):
+        res = []
+        last = self.m if self.tau == float("inf") else self.tau
+        for i in range(1, last):
+            res.extend(self.B[i])
+        s = k - len(res)
+        res.extend(sorted(self.B[last], key=lambda p: (p[0], p[1]))[:max(s, 0)])
+        return res
+
+
+def eq3_num_buckets(d: int, n_sub: int, bits: int, l1_bytes: int = 32768) -> float:
+    """Eq. 3: m = (C_L1 - C_quant - C_lut)/256 with C_quant = 2*32*n_sub*(B/8) and
+    C_lut = n_sub * 2^B bytes, where n_sub (the paper's "d/M") is the number of sub-vectors."""
+    c_quant = 2 * 32 * n_sub * bits / 8
+    c_lut = n_sub * (2 ** bits)
+    return (l1_bytes - c_quant - c_lut) / 256

@@ -1,0 +1,370 @@
+"""Pins of the CPU oracle against the paper and against mathematics (not against itself).
+
+Each test names what fixes the expected value: a value printed in PAPER.md (golden fixture), a
+closed form, an invariant the paper states, a textbook routine, or brute force on tiny inputs.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import bbc_oracle as O
+from oracle import bruteforce as BF
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+F32 = np.float32
+
+
+def _gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+# ---------------------------------------------------------------- values printed in the paper
+def test_fig3_walkthrough():
+    """tau 5 -> 4 and relaxed threshold 6 -> 5 when object 9 (4.9) arrives.
+    Also pins the Update comparison as '>=' (Alg. 1 l.9 prints 's > k', reading R1)."""
+    g = _gold("fig3_walkthrough.json")
+    rb = O.ResultBuffer(g["codebook"])
+    for oid, dist in g["objects"]:
+        rb.push(oid, dist)
+    rb.tau = rb.update(g["k"])
+    assert rb.tau == g["expect_tau_before"]
+    assert rb.relaxed_threshold() == g["expect_relaxed_threshold_before"]
+    oid, dist = g["insert"]
+    assert rb.bucket(dist) == g["expect_bucket_of_insert"]
+    rb.push(oid, dist)
+    rb.tau = rb.update(g["k"])
+    assert rb.tau == g["expect_tau_after"]
+    assert rb.relaxed_threshold() == g["expect_relaxed_threshold_after"]
+    # Collect returns the exact top-k of what was pushed
+    allp = sorted([(d, i) for i, d in g["objects"]] + [(dist, oid)])
+    assert sorted(rb.collect(g["k"])) == allp[: g["k"]]
+
+
+def test_fig3_strict_reading_contradicts_text():
+    """Under the literal 's > k' the threshold before the insert would be infinity, which the
+    text (bucket 5 is the threshold bucket) rules out -- the reason for reading R1."""
+    g = _gold("fig3_walkthrough.json")
+    counts = np.zeros(9, int)
+    for _, dist in g["objects"]:
+        counts[int(dist)] += 1
+    cum = np.cumsum(counts)
+    assert not np.any(cum > g["k"])                       # '>' never fires: tau = inf
+    assert int(np.flatnonzero(cum >= g["k"])[0]) == g["expect_tau_before"]
+
+
+def test_eq3_bucket_counts():
+    g = _gold("eq3_num_buckets.json")
+    for c in g["cases"]:
+        m = O.eq3_num_buckets(c["d"], c["d"] // 4, g["bits"], g["l1_bytes"])
+        assert m == c["m"], c
+    nd = g["not_pinned"]
+    assert O.eq3_num_buckets(nd["d"], nd["d"] // 4, g["bits"], g["l1_bytes"]) == nd["eq3_gives"]
+
+
+# ---------------------------------------------------------------- O1 coarse probe
+def test_coarse_d2_matches_fp64(rng):
+    Q = rng.standard_normal((7, 33)).astype(F32)
+    C = rng.standard_normal((50, 33)).astype(F32)
+    d = O.coarse_d2(Q, C)
+    ref = ((Q[:, None, :].astype(np.float64) - C[None].astype(np.float64)) ** 2).sum(2)
+    np.testing.assert_allclose(d, ref, rtol=1e-5)
+
+
+def test_probe_is_textbook_sort_and_prefix_monotone(rng):
+    Q = rng.standard_normal((5, 16)).astype(F32)
+    C = rng.standard_normal((40, 16)).astype(F32)
+    C[7] = C[3]                                         # exact tie: smaller id first
+    d = O.coarse_d2(Q, C)
+    pr, rq = O.probe(Q, C, 40)
+    for i in range(5):
+        ref = sorted(range(40), key=lambda j: (float(d[i, j]), j))
+        assert list(pr[i]) == ref
+        assert np.all(np.diff(rq[i]) >= 0)
+    p10, _ = O.probe(Q, C, 10)
+    assert np.array_equal(p10, pr[:, :10])
+
+
+# ---------------------------------------------------------------- O2/O3 PQ
+def test_lut_identity(c1t):
+    """sum_m LUT[m][code_m] == ||q - decode(code)||^2."""
+    cfg, ix, Q, _ = c1t
+    books = np.asarray(ix["codebooks"])
+    codes = np.asarray(ix["codes"][:500])
+    for q in Q[:3]:
+        est = O.pq_est(O.pq_lut(q, books), codes)
+        dec = np.concatenate([books[m][codes[:, m]] for m in range(books.shape[0])], axis=1)
+        ref = ((dec.astype(np.float64) - q.astype(np.float64)) ** 2).sum(1)
+        np.testing.assert_allclose(est, ref, rtol=1e-5)
+
+
+def test_pq_est_zero_at_decoded_query(c1t):
+    """q = decode(c) makes every LUT term (q_t - C_t)^2 exactly 0."""
+    cfg, ix, Q, _ = c1t
+    books = np.asarray(ix["codebooks"])
+    code = np.asarray(ix["codes"][17:18])
+    q = np.concatenate([books[m][code[0, m]] for m in range(books.shape[0])])
+    assert O.pq_est(O.pq_lut(q, books), code)[0] == 0.0
+
+
+# ---------------------------------------------------------------- O4-O8 result buffer
+def _probed_est(ix, q, nprobe):
+    pr, rq = O.probe(q[None], ix["centroids"], nprobe)
+    off = np.asarray(ix["list_offsets"])
+    lut = O.pq_lut(q, np.asarray(ix["codebooks"]))
+    sizes = off[pr[0] + 1] - off[pr[0]]
+    pos = np.concatenate([np.arange(off[L], off[L + 1]) for L in pr[0]])
+    return O.pq_est(lut, np.asarray(ix["codes"][pos])), sizes, pos
+
+
+def test_cells_monotone_and_clamped(rng):
+    x = np.sort(rng.uniform(-1, 12, 200_000).astype(F32))
+    c = O.cells(x, F32(0.5), F32(9.25))
+    assert np.all(np.diff(c) >= 0)
+    assert c.min() == 0 and c.max() == 255
+    assert np.all(c[x > F32(9.25)] == 255) and np.all(c[x <= F32(9.25)] <= 254)
+    assert np.all(c[x < F32(0.5)] == 0)
+    assert np.all(O.cells(x, F32(3.0), F32(3.0))[x <= 3.0] == 0)
+
+
+def test_threshold_invariants(c1t):
+    """tau = cell(budget-th smallest estimate) (closed form; cell() is monotone), and
+    sum_{c<tau} H < budget <= sum_{c<=tau} H (Alg. 1 Update)."""
+    cfg, ix, Q, _ = c1t
+    for q in Q[:4]:
+        est, sizes, _ = _probed_est(ix, q, cfg.nprobe)
+        budget = cfg.budget
+        s = O.sample_lists(sizes, budget)
+        ns = int(sizes[:s].sum())
+        dmin, dmax = O.edges(est[:ns], budget)
+        c = O.cells(est, dmin, dmax)
+        H = np.bincount(c, minlength=256)
+        tau = O.threshold(H, budget)
+        kth = np.sort(est)[budget - 1]
+        assert tau == O.cells(np.array([kth]), dmin, dmax)[0]
+        assert H[:tau].sum() < budget <= H[: tau + 1].sum()
+        assert tau <= 254
+
+
+def test_sample_and_edges(c1t):
+    """d_max >= the budget-th smallest estimate over everything probed (P:L899's claim), d_min is
+    the sample minimum, and the sample is the shortest probe-order prefix of >= min(8, nprobe)
+    lists holding >= budget objects (reading R5)."""
+    cfg, ix, Q, _ = c1t
+    for q in Q[:4]:
+        for nprobe, budget in ((cfg.nprobe, cfg.budget), (cfg.nlist, 2 * cfg.budget), (12, 350)):
+            est, sizes, _ = _probed_est(ix, q, nprobe)
+            s = O.sample_lists(sizes, budget)
+            if sizes.sum() <= budget:
+                assert s == 0
+                continue
+            assert s >= min(8, nprobe) and sizes[:s].sum() >= budget
+            if s > min(8, nprobe):
+                assert sizes[: s - 1].sum() < budget
+            ns = int(sizes[:s].sum())
+            dmin, dmax = O.edges(est[:ns], budget)
+            assert dmin == est[:ns].min()
+            assert dmax >= np.sort(est)[budget - 1]
+            assert dmax == np.sort(est[:ns])[budget - 1]
+
+
+def test_superset_invariants(c1t):
+    """|S*| >= budget; S* contains the top-budget by estimate; every member lies at or below the
+    threshold bucket's upper edge (BASELINE.json north_star invariants); threshold gap small
+    (Exp-4: 'on the order of 1e-2 or smaller')."""
+    cfg, ix, Q, _ = c1t
+    for q in Q:
+        est, sizes, _ = _probed_est(ix, q, 16)
+        budget = cfg.budget
+        s = O.sample_lists(sizes, budget)
+        ns = int(sizes[:s].sum())
+        dmin, dmax = O.edges(est[:ns], budget)
+        c = O.cells(est, dmin, dmax)
+        tau = O.threshold(np.bincount(c, minlength=256), budget)
+        sup = np.flatnonzero(c <= tau)
+        assert len(sup) >= budget
+        top = np.lexsort((np.arange(len(est)), est))[:budget]
+        assert set(top) <= set(sup)
+        upper = float(dmin) + (tau + 1) * (float(dmax) - float(dmin)) / 255.0
+        assert np.all(est[sup].astype(np.float64) <= upper * (1 + 1e-6))
+        kth = float(np.sort(est)[budget - 1])
+        assert (upper - kth) / kth <= 5e-2
+
+
+def test_alg1_literal_equals_one_shot(c1t):
+    """Alg. 1 run cluster by cluster (Push drops j > tau, Update after every cluster) keeps
+    exactly the one-shot superset {cell <= tau_final} (reading R17)."""
+    cfg, ix, Q, _ = c1t
+    est, sizes, _ = _probed_est(ix, Q[0], 16)
+    budget = 900
+    s = O.sample_lists(sizes, budget)
+    dmin, dmax = O.edges(est[: int(sizes[:s].sum())], budget)
+    c = O.cells(est, dmin, dmax)
+    tau = O.threshold(np.bincount(c, minlength=256), budget)
+    rb = O.ResultBuffer(np.arange(1, 258))            # bucket j = [j, j+1) holds cell j-1
+    pos = 0
+    for n in sizes:
+        for i in range(pos, pos + n):
+            rb.push(i, float(c[i]) + 1.5)
+        rb.tau = rb.update(budget)
+        pos += n
+    assert rb.tau - 1 == tau
+    kept = {oid for j in range(1, rb.tau + 1) for _, oid in rb.B[j]}
+    assert kept == set(np.flatnonzero(c <= tau))
+
+
+# ---------------------------------------------------------------- O9
+def test_exact_d2_and_select_textbook(rng):
+    q = rng.standard_normal(40).astype(F32)
+    X = rng.standard_normal((300, 40)).astype(F32)
+    d = O.exact_d2(q, X)
+    ref = np.linalg.norm(X.astype(np.float64) - q.astype(np.float64), axis=1) ** 2
+    np.testing.assert_allclose(d, ref, rtol=1e-6)
+    ids = rng.permutation(1000)[:300].astype(np.int64)
+    d[5] = d[9]                                           # a tie: smaller id first
+    oi, od = O.select_topk(d, ids, 50)
+    ref = sorted(zip(d.tolist(), ids.tolist()))[:50]
+    assert list(oi) == [r[1] for r in ref]
+    oi, od = O.select_topk(d[:3], ids[:3], 5)             # short: padded
+    assert list(oi[3:]) == [-1, -1] and np.all(np.isinf(od[3:]))
+
+
+def test_u8_exact_distances_are_integers(rng):
+    q = rng.integers(0, 256, 128).astype(F32)
+    X = rng.integers(0, 256, (100, 128)).astype(np.uint8)
+    d = O.exact_d2(q, X)
+    ref = ((X.astype(np.int64) - q.astype(np.int64)) ** 2).sum(1)
+    assert np.array_equal(d.astype(np.int64), ref)
+
+
+# ---------------------------------------------------------------- end to end
+def test_full_probe_unlimited_budget_is_brute_force(c1t):
+    """nprobe = nlist and budget >= N reproduce brute force exactly (BASELINE.json north_star)."""
+    cfg, ix, Q, _ = c1t
+    raw = np.asarray(ix["raw"])
+    X = np.empty_like(raw)
+    X[np.asarray(ix["ids"])] = raw
+    ids, d2 = O.search(ix, Q[:4], cfg.k, cfg.nlist, cfg.N)
+    gi, gd = BF.ground_truth(Q[:4], X, cfg.k)
+    assert np.array_equal(ids, gi)
+    np.testing.assert_allclose(d2, gd, rtol=1e-6)
+
+
+def test_tiny_brute_force_all_parameters(rng):
+    """Tiny index built by the builder: with every list probed and budget >= N the result is the
+    brute-force top-k for every k."""
+    import datagen
+    from datagen import build_index, configs
+    cfg = configs.get("C1t").replace(name="tiny", N=700, nlist=8, nq=3, k=20, nprobe=8, budget=700,
+                                     M=8, kmeans_iters=3, pq_train=700, pq_iters=3)
+    from datagen import synth
+    X = synth.generate_data(cfg)
+    ix = build_index.build(cfg, X=X)
+    Q = synth.generate_queries(cfg)
+    for k in (1, 7, 20, 700):
+        ids, d2 = O.search(ix, Q, k, cfg.nlist, max(k, cfg.N))
+        gi, gd = BF.ground_truth(Q, X, k)
+        assert np.array_equal(ids, gi)
+
+
+def test_short_results_padded(c1t):
+    cfg, ix, Q, _ = c1t
+    off = np.asarray(ix["list_offsets"])
+    ids, d2, dbg = O.search(ix, Q[:2], 5000, 1, 5000, want_debug=True)
+    for i in range(2):
+        n_o = dbg[i]["n_o"]
+        assert dbg[i]["tau"] == O.TAU_INF and n_o < 5000
+        assert np.all(ids[i, n_o:] == -1) and np.all(np.isinf(d2[i, n_o:]))
+        assert len(set(ids[i, :n_o])) == n_o
+
+
+def test_recall_and_relative_error_hand_examples():
+    gt = np.array([[1, 2, 3, 4]])
+    gd = np.array([[1.0, 4.0, 9.0, 16.0]])
+    res = np.array([[1, 2, 9, 8]])
+    rd = np.array([[1.0, 4.0, 16.0, 25.0]])
+    assert BF.recall(res, rd, gt, gd) == 0.75              # id 9 ties the 4th GT distance
+    assert abs(BF.relative_error(np.array([[1.0, 4.0, 9.0, 16.0 * 1.1025]]), gd) - 0.0125) < 1e-12
+
+
+# ---------------------------------------------------------------- RaBitQ
+def test_rabitq_estimator_bound_and_closed_form(c3s):
+    """<x_bar, q'> from (c1, c2, c3) equals sum_i x_bar_i * (v_l + delta * qbar_i) exactly (up to
+    fp32 rounding), and differs from <x_bar, q'> by at most sqrt(D)*delta/2 (the 4-bit query
+    quantisation bound); q = a database vector gives est d^2 within that bound of 0."""
+    cfg, ix, Q, _ = c3s
+    off = np.asarray(ix["list_offsets"])
+    P = np.asarray(ix["P"])
+    D = P.shape[0]
+    L = 5
+    sl = slice(off[L], off[L + 1])
+    bits = np.asarray(ix["bits"][sl])
+    fac = np.asarray(ix["factors"][sl])
+    raw = np.asarray(ix["raw"][sl])
+    b = np.unpackbits(bits, axis=1, bitorder="little").astype(np.float64)
+    xbar = (2 * b - 1) / np.sqrt(D)
+    for q in (Q[0], raw[3]):
+        rq2 = O.coarse_d2(q[None], np.asarray(ix["centroids"][L:L + 1]))[0, 0]
+        u = O.rabitq_rotate(q, P)
+        qbar, (c1, c2, c3), r = O.rabitq_query_code(u, np.asarray(ix["wL"][L]), rq2)
+        qp = (u.astype(np.float64) - ix["wL"][L]) / float(r)
+        vl = qp.min()
+        delta = (qp.max() - vl) / 15
+        ip = (b * qbar).sum(1)
+        est_ip = c1 * ip + c2 * b.sum(1) + c3
+        deq = (xbar * (vl + delta * qbar)).sum(1)
+        np.testing.assert_allclose(est_ip, deq, atol=1e-4)
+        exact_ip = xbar @ qp
+        assert np.all(np.abs(est_ip - exact_ip) <= np.sqrt(D) * delta / 2 + 1e-5)
+    # q = raw[3]: true d^2 = 0 for that object
+    est = O.rabitq_est(bits, fac, qbar, (c1, c2, c3), r, rq2)
+    ro, go = float(fac[3, 0]), float(fac[3, 1])
+    bound = 2 * ro * float(r) * (np.sqrt(D) * delta / 2 + 1e-5) / go
+    assert abs(float(est[3])) <= bound + 1e-3
+
+
+def test_rabitq_factors_and_unbiased(c3s):
+    """g_o in (0, 1], mean ~ sqrt(2/pi) (RaBitQ), rotation orthogonal; the estimator of <o, q>
+    is unbiased and its error is covered by eps0 * sqrt((1-g^2)/g^2)/sqrt(D-1) for most pairs
+    with eps0 = 1.9."""
+    cfg, ix, Q, _ = c3s
+    P = np.asarray(ix["P"]).astype(np.float64)
+    assert np.abs(P.T @ P - np.eye(len(P))).max() < 1e-5
+    fac = np.asarray(ix["factors"])
+    assert np.all(fac[:, 1] > 0) and np.all(fac[:, 1] <= 1.0 + 1e-6)
+    assert abs(fac[:, 1].mean() - np.sqrt(2 / np.pi)) < 0.02
+    off = np.asarray(ix["list_offsets"])
+    D = P.shape[0]
+    errs, cover = [], []
+    for qi in range(6):
+        q = Q[qi]
+        for L in range(0, 40, 3):
+            sl = slice(off[L], off[L + 1])
+            c = np.asarray(ix["centroids"][L])
+            rq2 = O.coarse_d2(q[None], c[None])[0, 0]
+            u = O.rabitq_rotate(q, np.asarray(ix["P"]))
+            qbar, cs, r = O.rabitq_query_code(u, np.asarray(ix["wL"][L]), rq2)
+            est = O.rabitq_est(np.asarray(ix["bits"][sl]), np.asarray(ix["factors"][sl]), qbar, cs,
+                               r, rq2).astype(np.float64)
+            raw = np.asarray(ix["raw"][sl]).astype(np.float64)
+            ro = fac[sl, 0].astype(np.float64)
+            g = fac[sl, 1].astype(np.float64)
+            true_ip = ((raw - c) @ (q - c)) / (ro * np.sqrt(rq2))
+            est_ip = (ro ** 2 + rq2 - est) / (2 * ro * np.sqrt(rq2))
+            errs.append(est_ip - true_ip)
+            cover.append(np.abs(est_ip - true_ip) <= 1.9 * np.sqrt((1 - g * g) / (g * g)) / np.sqrt(D - 1))
+    e = np.concatenate(errs)
+    assert abs(e.mean()) < 3 * e.std() / np.sqrt(len(e)) + 2e-3
+    assert np.concatenate(cover).mean() > 0.85
+
+
+def test_rabitq_full_probe_is_brute_force(c3s):
+    cfg, ix, Q, _ = c3s
+    raw = np.asarray(ix["raw"])
+    X = np.empty_like(raw)
+    X[np.asarray(ix["ids"])] = raw
+    ids, d2 = O.search(ix, Q[:2], 50, cfg.nlist, cfg.N)
+    gi, gd = BF.ground_truth(Q[:2], X, 50)
+    assert np.array_equal(ids, gi)
