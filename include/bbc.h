@@ -1,0 +1,201 @@
+/*
+ * bbc.h -- C ABI of libbbc.so: the B200 query hot path of BBC, the bucket-based result
+ * collector for large-k ANN search over quantized IVF indexes (arXiv 2604.01960).
+ *
+ * "P:Lnnn" cites a line of the paper text; DESIGN.md section 2 lists the readings.
+ *
+ * One call, bbc_search(), runs the whole path for a batch of queries (BASELINE.json north_star):
+ *   a1 coarse probe -- the nprobe nearest IVF lists, nearest first
+ *   a2 query tables -- PQ LUT / RaBitQ rotated + 4-bit query code
+ *   a3 sample       -- estimates of the nearest lists; d_min, d_max
+ *   a4 Push         -- estimate + bucket id of every probed object, histogram (Alg. 1 l.1-4,
+ *                      Eq. 6)
+ *   a5 Update       -- threshold bucket tau: first cumulative count >= budget (Alg. 1 l.5-11)
+ *   a6 Collect      -- candidate superset S* = objects in buckets <= tau
+ *   a7 re-rank      -- exact squared L2 of every candidate against raw vectors
+ *   a8 select       -- the k candidates with the smallest (exact d^2, id)
+ *
+ * Conventions
+ *   - All "device" pointers are CUDA device memory of the device the index was loaded on; all
+ *     "host" pointers are ordinary (or pinned) host memory.  No function allocates device memory
+ *     except ivf_load (index arrays, freed by ivf_free).  Scratch lives in the caller's workspace.
+ *   - Work is enqueued on `stream` (a cudaStream_t; NULL = legacy default stream) and the search
+ *     functions return after enqueueing (bbc_search_host synchronises the stream before it
+ *     returns).  One search may be in flight per workspace.
+ *   - Distances are squared Euclidean.  Output ids are the original row ids of the database.
+ *   - Errors: every function returns BBC_OK or an error code and then nothing was enqueued
+ *     (argument errors) or the stream state is unspecified (CUDA errors; the index handle
+ *     becomes unusable: later calls return BBC_ERR_STATE).  bbc_last_error() gives a message.
+ */
+#ifndef BBC_H_
+#define BBC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bbc_index_s* bbc_index;
+
+typedef enum {
+  BBC_OK = 0,
+  BBC_ERR_ARG = 1,     /* invalid argument (k, nprobe, budget, nq, null pointer, workspace size) */
+  BBC_ERR_IO = 2,      /* index file cannot be opened or read                                    */
+  BBC_ERR_FORMAT = 3,  /* index file malformed (magic, version, section sizes)                    */
+  BBC_ERR_CUDA = 4,    /* a CUDA runtime error (message in bbc_last_error)                        */
+  BBC_ERR_NCCL = 5,    /* a collective failed (multi-GPU)                                         */
+  BBC_ERR_OOM = 6,     /* device allocation in ivf_load failed                                    */
+  BBC_ERR_STATE = 7    /* handle unusable after an earlier CUDA/NCCL error                        */
+} bbc_status;
+
+/* Index kinds (file header field `kind`). */
+#define BBC_KIND_PQ 1      /* 8-bit product quantization, M sub-quantizers of 256 codewords   */
+#define BBC_KIND_RABITQ 2  /* 1-bit RaBitQ codes over a random rotation, factors (r_o, g_o)  */
+
+/*
+ * ivf_load -- read a BBCIVF01 index file (layout: DESIGN.md section 4 / datagen/index_file.py):
+ *   bytes [0,8) magic "BBCIVF01"; [8,256) 31 x int64 header {version=1, kind, raw_dtype(0 f32,
+ *   1 u8), N, d, nlist, M, nbits, D, seed, n_sections=10}; [256,416) section table of
+ *   (int64 offset, int64 nbytes); sections centroids f32[nlist*d], list_offsets i64[nlist+1],
+ *   ids i64[N], codebooks f32[M*256*(d/M)], codes u8[N*M], P f32[D*D], wL f32[nlist*D],
+ *   bits u8[N*D/8], factors f32[N*2], raw f32|u8[N*d]; per-object arrays in list order.
+ * and upload it to `cuda_device`.  With world > 1 only the lists assigned to `rank` are kept
+ * (lists sorted by (size desc, id asc) and given greedily to the least-loaded rank); centroids,
+ * codebooks, rotation and every list's size are replicated.  On success *out owns the device
+ * arrays until ivf_free.
+ */
+bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_index* out);
+void ivf_free(bbc_index index);
+
+typedef struct {
+  int64_t n;           /* database size N (all ranks)                  */
+  int32_t d;           /* dimensionality                               */
+  int32_t nlist;       /* IVF lists                                    */
+  int32_t kind;        /* BBC_KIND_PQ or BBC_KIND_RABITQ               */
+  int32_t m;           /* PQ sub-quantizers (0 for RaBitQ)             */
+  int32_t dpad;        /* RaBitQ padded dimension D (0 for PQ)         */
+  int32_t raw_u8;      /* 1 if raw vectors are uint8, 0 if fp32         */
+  int64_t n_local;     /* objects held by this rank                    */
+  int32_t max_list;    /* largest list size                            */
+  int32_t rank, world; /* shard of this handle                         */
+} bbc_index_info_t;
+
+bbc_status bbc_index_info(bbc_index index, bbc_index_info_t* info);
+
+/*
+ * bbc_workspace_size -- bytes of device workspace bbc_search needs for (nq, k, nprobe, budget).
+ * The workspace holds per-query scratch sized for the nprobe largest lists (cell ids, candidate
+ * rows and distances) plus query/output staging used by bbc_search_host.  Queries are processed
+ * in micro-batches that fit; a larger workspace means larger micro-batches.  `min_bytes` (may be
+ * NULL) receives the smallest workspace that still works (one query per micro-batch).
+ */
+bbc_status bbc_workspace_size(bbc_index index, int64_t nq, int32_t k, int32_t nprobe,
+                              int64_t budget, size_t* bytes, size_t* min_bytes);
+
+/*
+ * bbc_query_capacity -- upper bound on the objects one query probes on this shard (and hence on
+ * |S*|): the sum of the nprobe largest local lists.  Sizes the per-query debug buffers.
+ */
+bbc_status bbc_query_capacity(bbc_index index, int32_t nprobe, int64_t* cap);
+
+/*
+ * bbc_search -- top-k of every query (device pointers).
+ *   queries  device f32 [nq x d], row-major (uint8-valued queries for a uint8 index are passed
+ *            as fp32)
+ *   k        1 <= k <= N                        (else BBC_ERR_ARG)
+ *   nprobe   1 <= nprobe <= nlist               (else BBC_ERR_ARG)
+ *   budget   candidate budget, budget >= k      (else BBC_ERR_ARG); budget >= probed count means
+ *            every probed object is re-ranked (tau = infinity, Alg. 1 l.11)
+ *   out_ids  device i64 [nq x k]; out_d2 device f32 [nq x k].  Row i holds the k probed
+ *            candidates with the smallest (exact d^2, id), in candidate (probe) order, not sorted.
+ *            When fewer than k objects are probed the row is padded with (id -1, d^2 +inf).
+ *   workspace/workspace_bytes: device scratch of at least the `min_bytes` of bbc_workspace_size.
+ *   stream   cudaStream_t (void*), NULL = default stream.
+ */
+bbc_status bbc_search(bbc_index index, const float* queries, int64_t nq, int32_t k,
+                      int32_t nprobe, int64_t budget, int64_t* out_ids, float* out_d2,
+                      void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * bbc_search_host -- same as bbc_search, but queries/out_ids/out_d2 are HOST pointers.  The
+ * host->device copy of the queries, the search and the device->host copy of the results are
+ * enqueued on `stream` (staging buffers come from the workspace, which must be at least the
+ * `bytes` of bbc_workspace_size for this nq), then the stream is synchronised.
+ */
+bbc_status bbc_search_host(bbc_index index, const float* queries_host, int64_t nq, int32_t k,
+                           int32_t nprobe, int64_t budget, int64_t* out_ids_host,
+                           float* out_d2_host, void* workspace, size_t workspace_bytes,
+                           void* stream);
+
+/*
+ * Intermediates for parity tests.  Device pointers, any may be NULL; per-query strides are the
+ * `*_stride` values the caller passes (elements).  Requires a workspace in which all nq queries
+ * fit in one micro-batch (workspace_bytes >= bbc_workspace_size(...).bytes).
+ *   probe   i32 [nq x nprobe]  lists, nearest first          rq2    f32 [nq x nprobe]
+ *   nsample i32 [nq]           sample lists s (0 = tau inf)  edges  f32 [nq x 2] (d_min, d_max)
+ *   hist    i32 [nq x 256]     bucket histogram (255 = overflow, not counted)
+ *   tau     i32 [nq]           threshold bucket (1<<30 = infinity)
+ *   n_probed i32 [nq]          objects probed (n_o)
+ *   est     f32 [nq x est_stride]  estimated distances in probe order (only when non-NULL;
+ *                                  costs an extra pass)
+ *   n_cand  i32 [nq]           |S*|
+ *   cand_ids i64 [nq x cand_stride]  ids of S* in probe order
+ *   cand_d2  f32 [nq x cand_stride]  exact d^2 of S*
+ */
+typedef struct {
+  int32_t* probe;
+  float* rq2;
+  int32_t* nsample;
+  float* edges;
+  int32_t* hist;
+  int32_t* tau;
+  int32_t* n_probed;
+  float* est;
+  int64_t est_stride;
+  int32_t* n_cand;
+  int64_t* cand_ids;
+  float* cand_d2;
+  int64_t cand_stride;
+} bbc_debug_bufs;
+
+bbc_status bbc_search_debug(bbc_index index, const float* queries, int64_t nq, int32_t k,
+                            int32_t nprobe, int64_t budget, int64_t* out_ids, float* out_d2,
+                            void* workspace, size_t workspace_bytes, void* stream,
+                            const bbc_debug_bufs* dbg);
+
+/*
+ * Stage timing: when enabled, bbc_search records CUDA events on `stream` around each kernel of
+ * the path; bbc_get_timing returns the summed milliseconds per stage of the searches since the
+ * last call (and resets them).  Stages: BBC_STAGE_* below.  Synchronises the stream.
+ */
+enum {
+  BBC_STAGE_PROBE = 0,   /* a1: coarse distances + nprobe selection */
+  BBC_STAGE_TABLES = 1,  /* a2: LUT / rotation                      */
+  BBC_STAGE_SAMPLE = 2,  /* a3: sample estimates + edge selection   */
+  BBC_STAGE_SCAN = 3,    /* a4: Push (code scan + histogram)        */
+  BBC_STAGE_COMPACT = 4, /* a5+a6: threshold + superset compaction  */
+  BBC_STAGE_RERANK = 5,  /* a7: exact re-rank gather                */
+  BBC_STAGE_SELECT = 6,  /* a8: final top-k                         */
+  BBC_STAGE_COMM = 7,    /* a9: collectives (world > 1)             */
+  BBC_NUM_STAGES = 8
+};
+bbc_status bbc_set_timing(bbc_index index, int enable);
+bbc_status bbc_get_timing(bbc_index index, float* ms, int n, int64_t* calls);
+
+/* Per-search counters of the last bbc_search on this handle (host copy; synchronises the
+ * stream): total probed objects (sum of n_o), total candidates (sum of |S*|), micro-batches. */
+bbc_status bbc_last_stats(bbc_index index, int64_t* probed, int64_t* candidates,
+                          int64_t* microbatches);
+
+/* Number of CUDA kernels this library has launched in this process. */
+int64_t bbc_launch_count(void);
+
+/* Message for the last non-OK status returned on the calling thread. */
+const char* bbc_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BBC_H_ */

@@ -1,0 +1,237 @@
+"""Python binding of libbbc.so (include/bbc.h): argument marshalling only.
+
+Every step of the query path runs in the library's CUDA kernels.  There is no CPU fallback:
+if the library cannot be loaded, or no CUDA device is present, the calls raise.
+
+    idx = Index(path)                                   # ivf_load
+    ids, d2 = idx.search(q, k, nprobe, budget)          # bbc_search (q: cuda fp32 [nq, d])
+    ids, d2 = idx.search_host(q_np, k, nprobe, budget)  # bbc_search_host (numpy in, numpy out)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbbc.so")
+
+# names exported by include/bbc.h (checked by tests/test_lib_exports.py)
+EXPORTS = ("ivf_load", "ivf_free", "bbc_index_info", "bbc_workspace_size", "bbc_query_capacity",
+           "bbc_search",
+           "bbc_search_host", "bbc_search_debug", "bbc_set_timing", "bbc_get_timing",
+           "bbc_last_stats", "bbc_launch_count", "bbc_last_error")
+
+STAGES = ("probe", "tables", "sample", "scan", "compact", "rerank", "select", "comm")
+TAU_INF = 1 << 30
+KIND_PQ, KIND_RABITQ = 1, 2
+
+
+class BBCError(RuntimeError):
+    pass
+
+
+class IndexInfo(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("d", ctypes.c_int32), ("nlist", ctypes.c_int32),
+                ("kind", ctypes.c_int32), ("m", ctypes.c_int32), ("dpad", ctypes.c_int32),
+                ("raw_u8", ctypes.c_int32), ("n_local", ctypes.c_int64),
+                ("max_list", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32)]
+
+
+class DebugBufs(ctypes.Structure):
+    _fields_ = [("probe", ctypes.c_void_p), ("rq2", ctypes.c_void_p),
+                ("nsample", ctypes.c_void_p), ("edges", ctypes.c_void_p),
+                ("hist", ctypes.c_void_p), ("tau", ctypes.c_void_p),
+                ("n_probed", ctypes.c_void_p), ("est", ctypes.c_void_p),
+                ("est_stride", ctypes.c_int64), ("n_cand", ctypes.c_void_p),
+                ("cand_ids", ctypes.c_void_p), ("cand_d2", ctypes.c_void_p),
+                ("cand_stride", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """The loaded libbbc.so (raises if it is missing: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise BBCError(f"{LIB_PATH} not built (run paper_2604_01960_b200/build.py)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
+        L.ivf_load.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                               ctypes.POINTER(vp)]
+        L.ivf_free.argtypes = [vp]
+        L.ivf_free.restype = None
+        L.bbc_index_info.argtypes = [vp, ctypes.POINTER(IndexInfo)]
+        L.bbc_workspace_size.argtypes = [vp, i64, i32, i32, i64, ctypes.POINTER(ctypes.c_size_t),
+                                         ctypes.POINTER(ctypes.c_size_t)]
+        L.bbc_search.argtypes = [vp, vp, i64, i32, i32, i64, vp, vp, vp, ctypes.c_size_t, vp]
+        L.bbc_search_host.argtypes = [vp, vp, i64, i32, i32, i64, vp, vp, vp, ctypes.c_size_t, vp]
+        L.bbc_search_debug.argtypes = [vp, vp, i64, i32, i32, i64, vp, vp, vp, ctypes.c_size_t, vp,
+                                       ctypes.POINTER(DebugBufs)]
+        L.bbc_query_capacity.argtypes = [vp, i32, ctypes.POINTER(i64)]
+        L.bbc_set_timing.argtypes = [vp, ctypes.c_int]
+        L.bbc_get_timing.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int,
+                                     ctypes.POINTER(ctypes.c_int64)]
+        L.bbc_last_stats.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64),
+                                     ctypes.POINTER(i64)]
+        L.bbc_launch_count.argtypes = []
+        L.bbc_launch_count.restype = i64
+        L.bbc_last_error.argtypes = []
+        L.bbc_last_error.restype = ctypes.c_char_p
+        for fn in ("ivf_load", "bbc_index_info", "bbc_workspace_size", "bbc_search",
+                   "bbc_search_host", "bbc_search_debug", "bbc_set_timing", "bbc_get_timing",
+                   "bbc_last_stats", "bbc_query_capacity"):
+            getattr(L, fn).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        raise BBCError(f"bbc status {status}: {lib().bbc_last_error().decode()}")
+
+
+def launch_count() -> int:
+    return int(lib().bbc_launch_count())
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise BBCError("no CUDA device: the BBC path has no CPU fallback")
+    return torch
+
+
+class Index:
+    """A loaded (shard of an) IVF index on one GPU (ivf_load / ivf_free)."""
+
+    def __init__(self, path: str, rank: int = 0, world: int = 1, device: int | None = None):
+        torch = _torch()
+        dev = torch.cuda.current_device() if device is None else device
+        self.device = dev
+        h = ctypes.c_void_p()
+        with torch.cuda.device(dev):
+            _check(lib().ivf_load(path.encode(), rank, world, dev, ctypes.byref(h)))
+        self._h = h
+        info = IndexInfo()
+        _check(lib().bbc_index_info(h, ctypes.byref(info)))
+        self.info = info
+        self._ws = None
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().ivf_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ workspace
+    def workspace_size(self, nq: int, k: int, nprobe: int, budget: int):
+        b, m = ctypes.c_size_t(), ctypes.c_size_t()
+        _check(lib().bbc_workspace_size(self._h, nq, k, nprobe, budget, ctypes.byref(b),
+                                        ctypes.byref(m)))
+        return b.value, m.value
+
+    def workspace(self, nq: int, k: int, nprobe: int, budget: int, max_bytes: int | None = None):
+        """A cached device workspace (uint8 tensor) big enough for nq queries in one micro-batch
+        (capped at max_bytes, never below the minimum)."""
+        torch = _torch()
+        want, mn = self.workspace_size(nq, k, nprobe, budget)
+        if max_bytes is not None:
+            want = max(mn, min(want, max_bytes))
+        if self._ws is None or self._ws.numel() < want:
+            self._ws = None
+            self._ws = torch.empty(want, dtype=torch.uint8, device=f"cuda:{self.device}")
+        return self._ws
+
+    # ------------------------------------------------------------------ search
+    def search(self, q, k: int, nprobe: int, budget: int, out=None, workspace=None, stream=None):
+        """q: cuda fp32 [nq, d] -> (ids int64 [nq, k], d2 fp32 [nq, k]) on the same device."""
+        torch = _torch()
+        assert q.is_cuda and q.dtype == torch.float32 and q.is_contiguous()
+        nq = q.shape[0]
+        if out is None:
+            out = (torch.empty((nq, k), dtype=torch.int64, device=q.device),
+                   torch.empty((nq, k), dtype=torch.float32, device=q.device))
+        ws = self.workspace(nq, k, nprobe, budget) if workspace is None else workspace
+        st = torch.cuda.current_stream(q.device).cuda_stream if stream is None else stream
+        _check(lib().bbc_search(self._h, q.data_ptr(), nq, k, nprobe, budget, out[0].data_ptr(),
+                                out[1].data_ptr(), ws.data_ptr(), ws.numel(), st))
+        return out
+
+    def search_host(self, q: np.ndarray, k: int, nprobe: int, budget: int, out=None,
+                    workspace=None, stream=None):
+        """Host arrays in and out (bbc_search_host); pinned numpy views are fastest."""
+        torch = _torch()
+        q = np.ascontiguousarray(q, dtype=np.float32)
+        nq = q.shape[0]
+        if out is None:
+            out = (np.empty((nq, k), dtype=np.int64), np.empty((nq, k), dtype=np.float32))
+        ws = self.workspace(nq, k, nprobe, budget) if workspace is None else workspace
+        st = torch.cuda.current_stream(self.device).cuda_stream if stream is None else stream
+        _check(lib().bbc_search_host(self._h, q.ctypes.data, nq, k, nprobe, budget,
+                                     out[0].ctypes.data, out[1].ctypes.data, ws.data_ptr(),
+                                     ws.numel(), st))
+        return out
+
+    def search_debug(self, q, k: int, nprobe: int, budget: int, want_est: bool = False):
+        """Search plus every intermediate (parity tests).  Returns (ids, d2, dict of tensors)."""
+        torch = _torch()
+        nq = q.shape[0]
+        dev = q.device
+        ws = self.workspace(nq, k, nprobe, budget)
+        cap = int(self.cap(nprobe))
+        t = dict(
+            probe=torch.empty((nq, nprobe), dtype=torch.int32, device=dev),
+            rq2=torch.empty((nq, nprobe), dtype=torch.float32, device=dev),
+            nsample=torch.empty(nq, dtype=torch.int32, device=dev),
+            edges=torch.empty((nq, 2), dtype=torch.float32, device=dev),
+            hist=torch.empty((nq, 256), dtype=torch.int32, device=dev),
+            tau=torch.empty(nq, dtype=torch.int32, device=dev),
+            n_probed=torch.empty(nq, dtype=torch.int32, device=dev),
+            n_cand=torch.empty(nq, dtype=torch.int32, device=dev),
+            cand_ids=torch.full((nq, cap), -1, dtype=torch.int64, device=dev),
+            cand_d2=torch.empty((nq, cap), dtype=torch.float32, device=dev),
+        )
+        if want_est:
+            t["est"] = torch.empty((nq, cap), dtype=torch.float32, device=dev)
+        db = DebugBufs(t["probe"].data_ptr(), t["rq2"].data_ptr(), t["nsample"].data_ptr(),
+                       t["edges"].data_ptr(), t["hist"].data_ptr(), t["tau"].data_ptr(),
+                       t["n_probed"].data_ptr(), t["est"].data_ptr() if want_est else None, cap,
+                       t["n_cand"].data_ptr(), t["cand_ids"].data_ptr(), t["cand_d2"].data_ptr(),
+                       cap)
+        ids = torch.empty((nq, k), dtype=torch.int64, device=dev)
+        d2 = torch.empty((nq, k), dtype=torch.float32, device=dev)
+        st = torch.cuda.current_stream(dev).cuda_stream
+        _check(lib().bbc_search_debug(self._h, q.data_ptr(), nq, k, nprobe, budget,
+                                      ids.data_ptr(), d2.data_ptr(), ws.data_ptr(), ws.numel(),
+                                      st, ctypes.byref(db)))
+        return ids, d2, t
+
+    def cap(self, nprobe: int) -> int:
+        """Per-query element capacity (bbc_query_capacity)."""
+        c = ctypes.c_int64()
+        _check(lib().bbc_query_capacity(self._h, nprobe, ctypes.byref(c)))
+        return c.value
+
+    # ------------------------------------------------------------------ instrumentation
+    def set_timing(self, on: bool) -> None:
+        _check(lib().bbc_set_timing(self._h, int(on)))
+
+    def get_timing(self):
+        arr = (ctypes.c_float * 8)()
+        calls = ctypes.c_int64()
+        _check(lib().bbc_get_timing(self._h, arr, 8, ctypes.byref(calls)))
+        return dict(zip(STAGES, [float(x) for x in arr])), calls.value
+
+    def last_stats(self):
+        a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().bbc_last_stats(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return dict(probed=a.value, candidates=b.value, microbatches=c.value)

@@ -1,0 +1,635 @@
+// Host side of libbbc.so: index loading (ivf_load), workspace planning, and the launch sequence
+// of the query path (bbc_search).  C ABI declared in include/bbc.h.
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "bbc.h"
+#include "bbc_kernels.cuh"
+
+using namespace bbc;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+
+bbc_status fail(bbc_status s, const std::string& m) {
+  g_err = m;
+  return s;
+}
+
+struct Timer {
+  int stage;
+  cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct bbc_index_s {
+  int device = 0;
+  int rank = 0, world = 1;
+  int kind = 0, d = 0, nlist = 0, M = 0, D = 0, raw_u8 = 0;
+  long long N = 0, n_local = 0;
+  int max_list = 0;
+  std::vector<int> lsize;               // local list sizes
+  std::vector<int> gsize;               // global list sizes
+  std::vector<long long> desc_prefix;   // prefix sums of local sizes sorted descending
+  // device arrays
+  float* centroids = nullptr;
+  long long* loff = nullptr;
+  int* gsize_d = nullptr;
+  long long* ids = nullptr;
+  float* books = nullptr;
+  uint8_t* codes = nullptr;
+  float* P = nullptr;
+  float* wL = nullptr;
+  uint8_t* bits = nullptr;
+  float* factors = nullptr;
+  void* raw = nullptr;
+  long long* stats = nullptr;           // [4]
+  bool broken = false;
+  bool timing = false;
+  std::vector<Timer> timers;
+  std::vector<cudaEvent_t> pool;
+  double stage_ms[BBC_NUM_STAGES] = {0};
+  long long timed_calls = 0;
+  long long microbatches = 0;
+};
+
+namespace {
+
+#define CU(expr)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (expr);                                                       \
+    if (e_ != cudaSuccess) {                                                       \
+      if (ix) ix->broken = true;                                                   \
+      return fail(BBC_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    }                                                                              \
+  } while (0)
+
+Dev dev_view(const bbc_index_s* ix) {
+  Dev v;
+  v.kind = ix->kind; v.d = ix->d; v.nlist = ix->nlist; v.M = ix->M; v.D = ix->D;
+  v.raw_u8 = ix->raw_u8; v.n_local = ix->n_local;
+  v.centroids = ix->centroids; v.loff = ix->loff; v.gsize = ix->gsize_d; v.ids = ix->ids;
+  v.books = ix->books; v.codes = ix->codes; v.P = ix->P; v.wL = ix->wL; v.bits = ix->bits;
+  v.factors = ix->factors; v.raw = ix->raw;
+  return v;
+}
+
+cudaEvent_t take_event(bbc_index_s* ix) {
+  if (!ix->pool.empty()) {
+    cudaEvent_t e = ix->pool.back();
+    ix->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct StageScope {
+  bbc_index_s* ix;
+  cudaStream_t st;
+  Timer t;
+  bool on;
+  StageScope(bbc_index_s* i, cudaStream_t s, int stage) : ix(i), st(s), on(i->timing) {
+    if (on) {
+      t.stage = stage;
+      t.a = take_event(ix);
+      t.b = take_event(ix);
+      cudaEventRecord(t.a, st);
+    }
+  }
+  ~StageScope() {
+    if (on) {
+      cudaEventRecord(t.b, st);
+      ix->timers.push_back(t);
+    }
+  }
+};
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Plan {
+  long long cap;      // per-query element capacity
+  size_t per_query;   // bytes per query
+  size_t fixed;       // alignment slack
+};
+
+Plan make_plan(const bbc_index_s* ix, int nprobe, int k) {
+  Plan p;
+  long long cap = ix->desc_prefix[std::min<size_t>(nprobe, ix->desc_prefix.size() - 1)];
+  cap = (cap + 15) / 16 * 16;
+  if (cap < 16) cap = 16;
+  p.cap = cap;
+  size_t table = ix->kind == BBC_KIND_PQ ? (size_t)ix->M * 256 * 4 : (size_t)ix->D * 4;
+  p.per_query = (size_t)ix->nlist * 4 + (size_t)nprobe * 12 + 4 + 4 + 8 + kCells * 4 + 4 + 4 +
+                table + (size_t)cap * 9 + (size_t)ix->d * 4 + (size_t)k * 12 + 64;
+  p.fixed = 32 * 256;
+  return p;
+}
+
+// Carve the micro-batch arrays out of the workspace.
+void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, Batch& b,
+           float** qstage, long long** ostage_ids, float** ostage_d2, int k) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char* r = ws + off;
+    off = align256(off + bytes);
+    return r;
+  };
+  size_t table = ix->kind == BBC_KIND_PQ ? (size_t)ix->M * 256 : (size_t)ix->D;
+  b.coarse = (float*)take((size_t)nqb * ix->nlist * 4);
+  b.probe = (int*)take((size_t)nqb * nprobe * 4);
+  b.rq2 = (float*)take((size_t)nqb * nprobe * 4);
+  b.poff = (int*)take((size_t)nqb * (nprobe + 1) * 4);
+  b.nsamp = (int*)take((size_t)nqb * 4);
+  b.edges = (float*)take((size_t)nqb * 8);
+  b.hist = (int*)take((size_t)nqb * kCells * 4);
+  b.tau = (int*)take((size_t)nqb * 4);
+  b.ncand = (int*)take((size_t)nqb * 4);
+  b.table = (float*)take((size_t)nqb * table * 4);
+  b.cells = (uint8_t*)take((size_t)nqb * p.cap);
+  b.cpos = (int*)take((size_t)nqb * p.cap * 4);
+  b.val = (float*)take((size_t)nqb * p.cap * 4);
+  *qstage = (float*)take((size_t)nqb * ix->d * 4);
+  *ostage_ids = (long long*)take((size_t)nqb * k * 8);
+  *ostage_d2 = (float*)take((size_t)nqb * k * 4);
+}
+
+template <typename Kern>
+void set_smem(Kern kern, size_t bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+__global__ void k_debug_cands(const int* cpos, const float* val, const int* ncand, long long cap,
+                              long long* out_ids, float* out_d2, long long stride) {
+  const int q = blockIdx.y;
+  const int n = ncand[q];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n && i < stride;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (out_ids) out_ids[q * stride + i] = cpos[q * cap + i];
+    if (out_d2) out_d2[q * stride + i] = val[q * cap + i];
+  }
+}
+
+template <int M>
+void launch_pq_scan(bool sample, dim3 grid, size_t smem, cudaStream_t st, const Batch& b,
+                    const Dev& dv, int G) {
+  if (sample) {
+    set_smem(k_pq_scan<M, true>, smem);
+    k_pq_scan<M, true><<<grid, kScanNT, smem, st>>>(b, dv, G);
+  } else {
+    set_smem(k_pq_scan<M, false>, smem);
+    k_pq_scan<M, false><<<grid, kScanNT, smem, st>>>(b, dv, G);
+  }
+}
+
+bool pq_scan(int M, bool sample, dim3 grid, cudaStream_t st, const Batch& b, const Dev& dv, int G) {
+  size_t smem = (size_t)M * 256 * 4;
+  switch (M) {
+    case 8: launch_pq_scan<8>(sample, grid, smem, st, b, dv, G); return true;
+    case 16: launch_pq_scan<16>(sample, grid, smem, st, b, dv, G); return true;
+    case 24: launch_pq_scan<24>(sample, grid, smem, st, b, dv, G); return true;
+    case 32: launch_pq_scan<32>(sample, grid, smem, st, b, dv, G); return true;
+    case 48: launch_pq_scan<48>(sample, grid, smem, st, b, dv, G); return true;
+    case 64: launch_pq_scan<64>(sample, grid, smem, st, b, dv, G); return true;
+    default: return false;
+  }
+}
+
+bbc_status check_args(bbc_index ix, const void* q, int64_t nq, int32_t k, int32_t nprobe,
+                      int64_t budget, const void* oi, const void* od, const void* ws) {
+  if (!ix) return fail(BBC_ERR_ARG, "null index");
+  if (ix->broken) return fail(BBC_ERR_STATE, "index handle unusable after an earlier CUDA error");
+  if (nq < 0) return fail(BBC_ERR_ARG, "nq < 0");
+  if (k < 1 || k > ix->N) return fail(BBC_ERR_ARG, "k must satisfy 1 <= k <= N");
+  if (nprobe < 1 || nprobe > ix->nlist) return fail(BBC_ERR_ARG, "nprobe must satisfy 1 <= nprobe <= nlist");
+  if (nprobe > kMaxProbe) return fail(BBC_ERR_ARG, "nprobe > 2048 is not supported");
+  if (budget < k) return fail(BBC_ERR_ARG, "budget must be >= k");
+  if (nq > 0 && (!q || !oi || !od || !ws)) return fail(BBC_ERR_ARG, "null pointer");
+  return BBC_OK;
+}
+
+bbc_status run_search(bbc_index ix, const float* queries, int64_t nq, int32_t k, int32_t nprobe,
+                      int64_t budget, int64_t* out_ids, float* out_d2, void* workspace,
+                      size_t ws_bytes, void* stream, bool host, const bbc_debug_bufs* dbg) {
+  bbc_status s = check_args(ix, queries, nq, k, nprobe, budget, out_ids, out_d2, workspace);
+  if (s != BBC_OK) return s;
+  if (nq == 0) return BBC_OK;
+  CU(cudaSetDevice(ix->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  Plan p = make_plan(ix, nprobe, k);
+  if (ws_bytes < p.fixed + p.per_query)
+    return fail(BBC_ERR_ARG, "workspace smaller than bbc_workspace_size min_bytes");
+  long long nqb = std::min<long long>(nq, (long long)((ws_bytes - p.fixed) / p.per_query));
+  if (dbg && nqb < nq) return fail(BBC_ERR_ARG, "debug search needs all queries in one micro-batch");
+  const long long budget_c = std::min<long long>(budget, (long long)1 << 40);
+  CU(cudaMemsetAsync(ix->stats, 0, 4 * sizeof(long long), st));
+  ix->microbatches = 0;
+  if (ix->timing) ix->timed_calls++;
+  Dev dv = dev_view(ix);
+  for (long long q0 = 0; q0 < nq; q0 += nqb) {
+    const int nb = (int)std::min<long long>(nqb, nq - q0);
+    Batch b;
+    float* qstage;
+    long long* oids;
+    float* od2;
+    carve(ix, p, nb, nprobe, (char*)workspace, b, &qstage, &oids, &od2, k);
+    b.nq = nb; b.nprobe = nprobe; b.k = k; b.budget = budget_c; b.cap = p.cap;
+    b.stats = ix->stats;
+    if (host) {
+      CU(cudaMemcpyAsync(qstage, queries + q0 * ix->d, (size_t)nb * ix->d * 4,
+                         cudaMemcpyHostToDevice, st));
+      b.Q = qstage;
+    } else {
+      b.Q = queries + q0 * ix->d;
+      oids = (long long*)out_ids + q0 * k;
+      od2 = out_d2 + q0 * k;
+    }
+    CU(cudaMemsetAsync(b.hist, 0, (size_t)nb * kCells * 4, st));
+    {
+      StageScope sc(ix, st, BBC_STAGE_PROBE);
+      dim3 g1((ix->nlist + kPT - 1) / kPT, (nb + kPT - 1) / kPT);
+      k_probe_d2<<<g1, 256, 0, st>>>(b.Q, ix->centroids, b.coarse, nb, ix->nlist, ix->d);
+      k_probe_select<<<nb, kSelNT, 0, st>>>(b, dv);
+      g_launches += 2;
+    }
+    {
+      StageScope sc(ix, st, BBC_STAGE_TABLES);
+      if (ix->kind == BBC_KIND_PQ) {
+        k_pq_lut<<<dim3(ix->M, nb), 256, 0, st>>>(b, dv);
+      } else {
+        k_rbq_rotate<<<dim3((ix->D + 255) / 256, nb), 256, (size_t)ix->d * 4, st>>>(b, dv);
+      }
+      g_launches += 1;
+    }
+    const int Gs = 1, Gf = 8;
+    const int sample_grid = std::min(nprobe, 16);
+    {
+      StageScope sc(ix, st, BBC_STAGE_SAMPLE);
+      if (ix->kind == BBC_KIND_PQ) {
+        pq_scan(ix->M, true, dim3(sample_grid, nb), st, b, dv, Gs);
+      } else {
+        size_t sm = (size_t)ix->D * 4 + 4 * (ix->D / 32) * 4;
+        set_smem(k_rbq_scan<true>, sm);
+        k_rbq_scan<true><<<dim3(sample_grid, nb), kScanNT, sm, st>>>(b, dv, Gs);
+      }
+      k_select_edges<<<nb, kSelNT, 0, st>>>(b, dv);
+      g_launches += 2;
+    }
+    {
+      StageScope sc(ix, st, BBC_STAGE_SCAN);
+      dim3 g((nprobe + Gf - 1) / Gf, nb);
+      if (ix->kind == BBC_KIND_PQ) {
+        pq_scan(ix->M, false, g, st, b, dv, Gf);
+      } else {
+        size_t sm = (size_t)ix->D * 4 + 4 * (ix->D / 32) * 4;
+        set_smem(k_rbq_scan<false>, sm);
+        k_rbq_scan<false><<<g, kScanNT, sm, st>>>(b, dv, Gf);
+      }
+      g_launches += 1;
+    }
+    {
+      StageScope sc(ix, st, BBC_STAGE_COMPACT);
+      k_compact<<<nb, kCompNT, 0, st>>>(b, dv);
+      g_launches += 1;
+    }
+    {
+      StageScope sc(ix, st, BBC_STAGE_RERANK);
+      const int gy = 16;
+      size_t sm = (size_t)ix->d * 4;
+      if (ix->raw_u8) k_rerank<true><<<dim3(gy, nb), kRrNT, sm, st>>>(b, dv);
+      else k_rerank<false><<<dim3(gy, nb), kRrNT, sm, st>>>(b, dv);
+      g_launches += 1;
+    }
+    {
+      StageScope sc(ix, st, BBC_STAGE_SELECT);
+      k_final_select<<<nb, kSelNT, 0, st>>>(b, dv, oids, od2);
+      g_launches += 1;
+    }
+    CU(cudaGetLastError());
+    if (dbg) {
+      auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+        return dst ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st) : cudaSuccess;
+      };
+      CU(cp(dbg->probe, b.probe, (size_t)nb * nprobe * 4));
+      CU(cp(dbg->rq2, b.rq2, (size_t)nb * nprobe * 4));
+      CU(cp(dbg->nsample, b.nsamp, (size_t)nb * 4));
+      CU(cp(dbg->edges, b.edges, (size_t)nb * 8));
+      CU(cp(dbg->hist, b.hist, (size_t)nb * kCells * 4));
+      CU(cp(dbg->tau, b.tau, (size_t)nb * 4));
+      CU(cp(dbg->n_cand, b.ncand, (size_t)nb * 4));
+      if (dbg->n_probed)
+        CU(cudaMemcpy2DAsync(dbg->n_probed, 4, b.poff + nprobe, (size_t)(nprobe + 1) * 4, 4, nb,
+                             cudaMemcpyDeviceToDevice, st));
+      if (dbg->cand_ids || dbg->cand_d2) {
+        k_debug_cands<<<dim3(64, nb), 256, 0, st>>>(b.cpos, b.val, b.ncand, p.cap, (long long*)dbg->cand_ids,
+                                                    dbg->cand_d2, dbg->cand_stride);
+        g_launches += 1;
+      }
+      if (dbg->est) {
+        // all estimates in probe order: rerun the estimate pass over every probed list into
+        // the caller's buffer (debug only)
+        Batch b2 = b;
+        b2.val = dbg->est;
+        b2.cap = dbg->est_stride;
+        std::vector<int> ones(nb, nprobe);
+        // temporarily mark every list as "sample" so the sample kernel covers all of them
+        int* ns_all = b.tau;  // reuse: tau already copied out above
+        CU(cudaMemcpyAsync(ns_all, ones.data(), (size_t)nb * 4, cudaMemcpyHostToDevice, st));
+        CU(cudaStreamSynchronize(st));
+        b2.nsamp = ns_all;
+        if (ix->kind == BBC_KIND_PQ) {
+          pq_scan(ix->M, true, dim3(std::min(nprobe, 64), nb), st, b2, dv, Gs);
+        } else {
+          size_t sm = (size_t)ix->D * 4 + 4 * (ix->D / 32) * 4;
+          k_rbq_scan<true><<<dim3(std::min(nprobe, 64), nb), kScanNT, sm, st>>>(b2, dv, Gs);
+        }
+        g_launches += 1;
+        CU(cudaGetLastError());
+      }
+    }
+    if (host) {
+      CU(cudaMemcpyAsync(out_ids + q0 * k, oids, (size_t)nb * k * 8, cudaMemcpyDeviceToHost, st));
+      CU(cudaMemcpyAsync(out_d2 + q0 * k, od2, (size_t)nb * k * 4, cudaMemcpyDeviceToHost, st));
+    }
+    ix->microbatches++;
+  }
+  if (host || dbg) CU(cudaStreamSynchronize(st));
+  return BBC_OK;
+}
+
+}  // namespace
+
+// ============================================================================================
+// C ABI
+// ============================================================================================
+extern "C" {
+
+const char* bbc_last_error(void) { return g_err.c_str(); }
+int64_t bbc_launch_count(void) { return g_launches.load(); }
+
+bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_index* out) {
+  bbc_index_s* ix = nullptr;
+  if (!path || !out) return fail(BBC_ERR_ARG, "null argument");
+  if (world < 1 || rank < 0 || rank >= world) return fail(BBC_ERR_ARG, "bad rank/world");
+  FILE* f = fopen(path, "rb");
+  if (!f) return fail(BBC_ERR_IO, std::string("cannot open ") + path);
+  char head[512];
+  if (fread(head, 1, 512, f) != 512) { fclose(f); return fail(BBC_ERR_FORMAT, "short header"); }
+  if (memcmp(head, "BBCIVF01", 8) != 0) { fclose(f); return fail(BBC_ERR_FORMAT, "bad magic"); }
+  long long hdr[31], table[10][2];
+  memcpy(hdr, head + 8, sizeof(hdr));
+  memcpy(table, head + 256, sizeof(table));
+  if (hdr[0] != 1) { fclose(f); return fail(BBC_ERR_FORMAT, "unsupported version"); }
+  const int kind = (int)hdr[1], raw_u8 = (int)hdr[2];
+  const long long N = hdr[3];
+  const int d = (int)hdr[4], nlist = (int)hdr[5], M = (int)hdr[6], D = (int)hdr[8];
+  if ((kind != BBC_KIND_PQ && kind != BBC_KIND_RABITQ) || N <= 0 || d <= 0 || nlist <= 0 ||
+      N >= (1ll << 31)) {
+    fclose(f);
+    return fail(BBC_ERR_FORMAT, "bad header fields");
+  }
+  if (kind == BBC_KIND_PQ && (M <= 0 || d % M != 0 || M % 8 != 0 || M > 64 || hdr[7] != 8)) {
+    fclose(f);
+    return fail(BBC_ERR_FORMAT, "PQ needs 8-bit codes, M in {8,16,24,32,48,64}, M | d");
+  }
+  if (kind == BBC_KIND_RABITQ && (D % 64 != 0 || D < d)) {
+    fclose(f);
+    return fail(BBC_ERR_FORMAT, "RaBitQ needs D a multiple of 64, D >= d");
+  }
+  if (raw_u8 ? (d % 16 != 0) : (d % 4 != 0)) {
+    fclose(f);
+    return fail(BBC_ERR_FORMAT, "d must be a multiple of 4 (f32) or 16 (u8)");
+  }
+  const size_t rowraw = (size_t)d * (raw_u8 ? 1 : 4);
+  const size_t dsub = kind == BBC_KIND_PQ ? d / M : 0;
+  const size_t expect[10] = {(size_t)nlist * d * 4, (size_t)(nlist + 1) * 8, (size_t)N * 8,
+                             kind == BBC_KIND_PQ ? (size_t)M * 256 * dsub * 4 : 0,
+                             kind == BBC_KIND_PQ ? (size_t)N * M : 0,
+                             kind == BBC_KIND_RABITQ ? (size_t)D * D * 4 : 0,
+                             kind == BBC_KIND_RABITQ ? (size_t)nlist * D * 4 : 0,
+                             kind == BBC_KIND_RABITQ ? (size_t)N * D / 8 : 0,
+                             kind == BBC_KIND_RABITQ ? (size_t)N * 8 : 0, (size_t)N * rowraw};
+  for (int s = 0; s < 10; ++s) {
+    if (expect[s] && (size_t)table[s][1] != expect[s]) {
+      fclose(f);
+      return fail(BBC_ERR_FORMAT, "section " + std::to_string(s) + " has the wrong size");
+    }
+  }
+  auto rd = [&](int s, void* dst, size_t off, size_t bytes) -> bool {
+    if (fseeko(f, (off_t)(table[s][0] + off), SEEK_SET) != 0) return false;
+    return fread(dst, 1, bytes, f) == bytes;
+  };
+  std::vector<long long> goff(nlist + 1);
+  if (!rd(1, goff.data(), 0, goff.size() * 8)) { fclose(f); return fail(BBC_ERR_IO, "read offsets"); }
+  if (goff[0] != 0 || goff[nlist] != N) { fclose(f); return fail(BBC_ERR_FORMAT, "bad list offsets"); }
+  ix = new bbc_index_s();
+  ix->device = cuda_device; ix->rank = rank; ix->world = world;
+  ix->kind = kind; ix->d = d; ix->nlist = nlist; ix->M = M; ix->D = D; ix->raw_u8 = raw_u8;
+  ix->N = N;
+  ix->gsize.resize(nlist);
+  for (int L = 0; L < nlist; ++L) ix->gsize[L] = (int)(goff[L + 1] - goff[L]);
+  // shard assignment: lists by (size desc, id asc), each to the least-loaded rank (ties: lowest)
+  std::vector<int> owner(nlist, 0);
+  if (world > 1) {
+    std::vector<int> order(nlist);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int a, int b) { return ix->gsize[a] > ix->gsize[b]; });
+    std::vector<long long> load(world, 0);
+    for (int L : order) {
+      int r = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+      owner[L] = r;
+      load[r] += ix->gsize[L];
+    }
+  }
+  ix->lsize.assign(nlist, 0);
+  std::vector<long long> loff(nlist + 1, 0);
+  for (int L = 0; L < nlist; ++L) {
+    ix->lsize[L] = owner[L] == rank ? ix->gsize[L] : 0;
+    loff[L + 1] = loff[L] + ix->lsize[L];
+  }
+  ix->n_local = loff[nlist];
+  ix->max_list = *std::max_element(ix->gsize.begin(), ix->gsize.end());
+  std::vector<int> sorted = ix->lsize;
+  std::sort(sorted.begin(), sorted.end(), std::greater<int>());
+  ix->desc_prefix.assign(nlist + 1, 0);
+  for (int i = 0; i < nlist; ++i) ix->desc_prefix[i + 1] = ix->desc_prefix[i] + sorted[i];
+
+  auto fail_load = [&](bbc_status s, const std::string& m) {
+    fclose(f);
+    ivf_free(ix);
+    return fail(s, m);
+  };
+  if (cudaSetDevice(cuda_device) != cudaSuccess) return fail_load(BBC_ERR_CUDA, "cudaSetDevice");
+  auto dalloc = [&](void** p, size_t bytes) -> bool {
+    if (bytes == 0) bytes = 256;
+    return cudaMalloc(p, bytes) == cudaSuccess;
+  };
+  // replicated arrays
+  std::vector<char> buf;
+  auto upload_full = [&](int s, void** dst) -> bool {
+    size_t bytes = (size_t)table[s][1];
+    buf.resize(bytes);
+    if (!rd(s, buf.data(), 0, bytes)) return false;
+    if (!dalloc(dst, bytes)) return false;
+    return cudaMemcpy(*dst, buf.data(), bytes, cudaMemcpyHostToDevice) == cudaSuccess;
+  };
+  // per-object arrays: rows of owned lists, concatenated in list order
+  auto upload_rows = [&](int s, size_t rowbytes, void** dst) -> bool {
+    size_t bytes = (size_t)ix->n_local * rowbytes;
+    if (!dalloc(dst, bytes)) return false;
+    if (world == 1) {
+      // stream in 256 MB chunks
+      const size_t chunk = 256u << 20;
+      buf.resize(std::min(bytes, chunk));
+      for (size_t o = 0; o < bytes; o += chunk) {
+        size_t nb = std::min(chunk, bytes - o);
+        if (!rd(s, buf.data(), o, nb)) return false;
+        if (cudaMemcpy((char*)*dst + o, buf.data(), nb, cudaMemcpyHostToDevice) != cudaSuccess) return false;
+      }
+      return true;
+    }
+    for (int L = 0; L < nlist; ++L) {
+      if (!ix->lsize[L]) continue;
+      size_t nb = (size_t)ix->lsize[L] * rowbytes;
+      buf.resize(nb);
+      if (!rd(s, buf.data(), (size_t)goff[L] * rowbytes, nb)) return false;
+      if (cudaMemcpy((char*)*dst + (size_t)loff[L] * rowbytes, buf.data(), nb,
+                     cudaMemcpyHostToDevice) != cudaSuccess)
+        return false;
+    }
+    return true;
+  };
+  bool ok = upload_full(0, (void**)&ix->centroids);
+  ok = ok && dalloc((void**)&ix->loff, (nlist + 1) * 8) &&
+       cudaMemcpy(ix->loff, loff.data(), (nlist + 1) * 8, cudaMemcpyHostToDevice) == cudaSuccess;
+  ok = ok && dalloc((void**)&ix->gsize_d, nlist * 4) &&
+       cudaMemcpy(ix->gsize_d, ix->gsize.data(), nlist * 4, cudaMemcpyHostToDevice) == cudaSuccess;
+  ok = ok && upload_rows(2, 8, (void**)&ix->ids);
+  if (kind == BBC_KIND_PQ) {
+    ok = ok && upload_full(3, (void**)&ix->books);
+    ok = ok && upload_rows(4, (size_t)M, (void**)&ix->codes);
+  } else {
+    ok = ok && upload_full(5, (void**)&ix->P);
+    ok = ok && upload_full(6, (void**)&ix->wL);
+    ok = ok && upload_rows(7, (size_t)D / 8, (void**)&ix->bits);
+    ok = ok && upload_rows(8, 8, (void**)&ix->factors);
+  }
+  ok = ok && upload_rows(9, rowraw, &ix->raw);
+  ok = ok && dalloc((void**)&ix->stats, 4 * sizeof(long long));
+  if (!ok) {
+    cudaError_t e = cudaGetLastError();
+    return fail_load(e == cudaErrorMemoryAllocation ? BBC_ERR_OOM : BBC_ERR_IO,
+                     std::string("load failed: ") + cudaGetErrorString(e));
+  }
+  fclose(f);
+  *out = ix;
+  return BBC_OK;
+}
+
+void ivf_free(bbc_index ix) {
+  if (!ix) return;
+  cudaSetDevice(ix->device);
+  void* ptrs[] = {ix->centroids, ix->loff, ix->gsize_d, ix->ids, ix->books, ix->codes, ix->P,
+                  ix->wL, ix->bits, ix->factors, ix->raw, ix->stats};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (auto& t : ix->timers) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
+  for (auto e : ix->pool) cudaEventDestroy(e);
+  delete ix;
+}
+
+bbc_status bbc_index_info(bbc_index ix, bbc_index_info_t* info) {
+  if (!ix || !info) return fail(BBC_ERR_ARG, "null argument");
+  info->n = ix->N; info->d = ix->d; info->nlist = ix->nlist; info->kind = ix->kind;
+  info->m = ix->M; info->dpad = ix->D; info->raw_u8 = ix->raw_u8; info->n_local = ix->n_local;
+  info->max_list = ix->max_list; info->rank = ix->rank; info->world = ix->world;
+  return BBC_OK;
+}
+
+bbc_status bbc_workspace_size(bbc_index ix, int64_t nq, int32_t k, int32_t nprobe, int64_t budget,
+                              size_t* bytes, size_t* min_bytes) {
+  if (!ix || !bytes) return fail(BBC_ERR_ARG, "null argument");
+  if (nprobe < 1 || nprobe > ix->nlist || k < 1 || nq < 0 || budget < k)
+    return fail(BBC_ERR_ARG, "bad arguments");
+  Plan p = make_plan(ix, nprobe, k);
+  *bytes = p.fixed + (size_t)std::max<int64_t>(nq, 1) * p.per_query;
+  if (min_bytes) *min_bytes = p.fixed + p.per_query;
+  return BBC_OK;
+}
+
+bbc_status bbc_query_capacity(bbc_index ix, int32_t nprobe, int64_t* cap) {
+  if (!ix || !cap) return fail(BBC_ERR_ARG, "null argument");
+  if (nprobe < 1 || nprobe > ix->nlist) return fail(BBC_ERR_ARG, "bad nprobe");
+  *cap = make_plan(ix, nprobe, 1).cap;
+  return BBC_OK;
+}
+
+bbc_status bbc_search(bbc_index ix, const float* queries, int64_t nq, int32_t k, int32_t nprobe,
+                      int64_t budget, int64_t* out_ids, float* out_d2, void* workspace,
+                      size_t workspace_bytes, void* stream) {
+  return run_search(ix, queries, nq, k, nprobe, budget, out_ids, out_d2, workspace,
+                    workspace_bytes, stream, false, nullptr);
+}
+
+bbc_status bbc_search_host(bbc_index ix, const float* queries_host, int64_t nq, int32_t k,
+                           int32_t nprobe, int64_t budget, int64_t* out_ids_host,
+                           float* out_d2_host, void* workspace, size_t workspace_bytes,
+                           void* stream) {
+  return run_search(ix, queries_host, nq, k, nprobe, budget, out_ids_host, out_d2_host, workspace,
+                    workspace_bytes, stream, true, nullptr);
+}
+
+bbc_status bbc_search_debug(bbc_index ix, const float* queries, int64_t nq, int32_t k,
+                            int32_t nprobe, int64_t budget, int64_t* out_ids, float* out_d2,
+                            void* workspace, size_t workspace_bytes, void* stream,
+                            const bbc_debug_bufs* dbg) {
+  if (!dbg) return fail(BBC_ERR_ARG, "null debug buffers");
+  return run_search(ix, queries, nq, k, nprobe, budget, out_ids, out_d2, workspace,
+                    workspace_bytes, stream, false, dbg);
+}
+
+bbc_status bbc_set_timing(bbc_index ix, int enable) {
+  if (!ix) return fail(BBC_ERR_ARG, "null index");
+  ix->timing = enable != 0;
+  return BBC_OK;
+}
+
+bbc_status bbc_get_timing(bbc_index ix, float* ms, int n, int64_t* calls) {
+  if (!ix) return fail(BBC_ERR_ARG, "null index");
+  for (auto& t : ix->timers) {
+    cudaEventSynchronize(t.b);
+    float e = 0.f;
+    cudaEventElapsedTime(&e, t.a, t.b);
+    ix->stage_ms[t.stage] += e;
+    ix->pool.push_back(t.a);
+    ix->pool.push_back(t.b);
+  }
+  ix->timers.clear();
+  for (int i = 0; i < n && i < BBC_NUM_STAGES; ++i) ms[i] = (float)ix->stage_ms[i];
+  if (calls) *calls = ix->timed_calls;
+  for (double& v : ix->stage_ms) v = 0;
+  ix->timed_calls = 0;
+  return BBC_OK;
+}
+
+bbc_status bbc_last_stats(bbc_index ix, int64_t* probed, int64_t* candidates, int64_t* micro) {
+  if (!ix) return fail(BBC_ERR_ARG, "null index");
+  long long h[4];
+  CU(cudaMemcpy(h, ix->stats, sizeof(h), cudaMemcpyDeviceToHost));
+  if (probed) *probed = h[0];
+  if (candidates) *candidates = h[1];
+  if (micro) *micro = ix->microbatches;
+  return BBC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,683 @@
+// Kernels of the BBC query hot path (sm_100a).  Steps a1..a8 of DESIGN.md section 1.
+//
+// Canonical arithmetic: every value that decides an integer (probe order,
+// LUT entries, estimates, bucket ids) is computed with explicitly rounded intrinsics
+// (__fadd_rn/__fsub_rn/__fmul_rn/__fdiv_rn/__fsqrt_rn) in a fixed order, so no FMA contraction
+// can change a rounding; the CPU oracle evaluates the same expression tree.
+#pragma once
+#include "bbc_device.cuh"
+
+namespace bbc {
+
+// Per-micro-batch pointers (device), all per-query arrays indexed by the query's slot in the
+// micro-batch.
+struct Batch {
+  int nq;             // queries in this micro-batch
+  int nprobe;
+  int k;
+  long long budget;
+  long long cap;      // per-query element capacity (sum of the nprobe largest local lists)
+  const float* Q;     // [nq x d]
+  float* coarse;      // [nq x nlist]        coarse d^2 scratch
+  int* probe;         // [nq x nprobe]
+  float* rq2;         // [nq x nprobe]
+  int* poff;          // [nq x (nprobe+1)]   element offset of each probed list (local)
+  int* nsamp;         // [nq]                sample lists s (0 = tau infinity)
+  float* edges;       // [nq x 2]            (d_min, d_max)
+  int* hist;          // [nq x 256]
+  int* tau;           // [nq]
+  int* ncand;         // [nq]
+  float* table;       // PQ LUT [nq x M x 256] | RaBitQ u [nq x D]
+  uint8_t* cells;     // [nq x cap]
+  int* cpos;          // [nq x cap]  candidate rows, then (after re-rank) original ids
+  float* val;         // [nq x cap]  sample estimates, then exact d^2 of candidates
+  long long* stats;   // [2] sum n_o, sum |S*|
+};
+
+// Index arrays on the device.
+struct Dev {
+  int kind, d, nlist, M, D, raw_u8;
+  long long n_local;
+  const float* centroids;        // [nlist x d]
+  const long long* loff;         // [nlist + 1] local list offsets (rows of this shard)
+  const int* gsize;              // [nlist] global list sizes (all shards)
+  const long long* ids;          // [n_local]
+  const float* books;            // [M x 256 x dsub]
+  const uint8_t* codes;          // [n_local x M]
+  const float* P;                // [D x D]
+  const float* wL;               // [nlist x D]
+  const uint8_t* bits;           // [n_local x D/8]
+  const float* factors;          // [n_local x 2]
+  const void* raw;               // [n_local x d] f32 | u8
+};
+
+// ------------------------------------------------------------------------------------------
+// a1  coarse probe: canonical d^2 of every (query, centroid), 64 x 64 tiles, 4 x 4 per thread.
+// ------------------------------------------------------------------------------------------
+constexpr int kPT = 64, kPK = 16;
+__global__ void __launch_bounds__(256) k_probe_d2(const float* __restrict__ Q,
+                                                  const float* __restrict__ C, float* __restrict__ out,
+                                                  int nq, int nlist, int d) {
+  __shared__ float sQ[kPK][kPT + 1];
+  __shared__ float sC[kPK][kPT + 1];
+  const int q0 = blockIdx.y * kPT, c0 = blockIdx.x * kPT;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  for (int t0 = 0; t0 < d; t0 += kPK) {
+    for (int e = threadIdx.x; e < kPT * kPK; e += 256) {
+      int r = e / kPK, t = e % kPK;
+      int qq = q0 + r, cc = c0 + r, tt = t0 + t;
+      sQ[t][r] = (qq < nq && tt < d) ? Q[(size_t)qq * d + tt] : 0.f;
+      sC[t][r] = (cc < nlist && tt < d) ? C[(size_t)cc * d + tt] : 0.f;
+    }
+    __syncthreads();
+    const int tmax = min(kPK, d - t0);
+    for (int t = 0; t < tmax; ++t) {
+      float qv[4], cv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) qv[i] = sQ[t][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) cv[j] = sC[t][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float df = __fsub_rn(qv[i], cv[j]);
+          acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(df, df));
+        }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int qq = q0 + ty * 4 + i;
+    if (qq >= nq) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int cc = c0 + tx + 16 * j;
+      if (cc < nlist) out[(size_t)qq * nlist + cc] = acc[i][j];
+    }
+  }
+}
+
+// Per query: the nprobe smallest (d^2, list) keys, sorted; list offsets and the sample rule.
+constexpr int kSelNT = 1024;
+constexpr int kMaxProbe = 2048;
+__global__ void __launch_bounds__(kSelNT) k_probe_select(Batch b, Dev ix) {
+  __shared__ SelectSmem sm;
+  __shared__ uint64_t keys[kMaxProbe];
+  __shared__ int wcnt[kSelNT / 32 + 1];
+  __shared__ int s_count;
+  const int q = blockIdx.x;
+  const int nlist = ix.nlist, nprobe = b.nprobe;
+  const float* d2 = b.coarse + (size_t)q * nlist;
+  auto load = [&](int64_t i) -> uint64_t {
+    return ((uint64_t)f2key(d2[i]) << 32) | (uint32_t)i;
+  };
+  int pshift;
+  uint64_t pref = cta_select<kSelNT>(nlist, nprobe, load, false, &pshift, sm);
+  if (threadIdx.x == 0) s_count = 0;
+  int P2 = 1;
+  while (P2 < nprobe) P2 <<= 1;
+  for (int i = threadIdx.x; i < P2; i += kSelNT) keys[i] = ~0ull;
+  __syncthreads();
+  for (int i = threadIdx.x; i < nlist; i += kSelNT) {
+    uint64_t k = load(i);
+    if (shr64(k, pshift) <= pref) keys[atomicAdd(&s_count, 1)] = k;
+  }
+  __syncthreads();
+  // bitonic sort of P2 keys
+  for (int size = 2; size <= P2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < P2 / 2; i += kSelNT) {
+        int lo = 2 * stride * (i / stride) + (i % stride);
+        int hi = lo + stride;
+        bool up = ((lo & size) == 0);
+        uint64_t a = keys[lo], c = keys[hi];
+        if ((a > c) == up) { keys[lo] = c; keys[hi] = a; }
+      }
+      __syncthreads();
+    }
+  }
+  // write probes; prefix over local and global sizes
+  int* pr = b.probe + (size_t)q * nprobe;
+  float* rq = b.rq2 + (size_t)q * nprobe;
+  int* po = b.poff + (size_t)q * (nprobe + 1);
+  long long lrun = 0, grun = 0;
+  int s = -1;
+  for (int base = 0; base < nprobe; base += kSelNT) {
+    const int j = base + threadIdx.x;
+    int lsz = 0, gsz = 0;
+    if (j < nprobe) {
+      uint64_t k = keys[j];
+      int L = (int)(k & 0xffffffffu);
+      pr[j] = L;
+      rq[j] = key2f((uint32_t)(k >> 32));
+      lsz = (int)(ix.loff[L + 1] - ix.loff[L]);
+      gsz = ix.gsize[L];
+    }
+    // inclusive scans of lsz and gsz across the block (two ranks via block_rank is not enough:
+    // use warp scans + smem)
+    __shared__ long long wl[kSelNT / 32], wg[kSelNT / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    long long il = lsz, ig = gsz;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      long long tl = __shfl_up_sync(0xffffffffu, il, o);
+      long long tg = __shfl_up_sync(0xffffffffu, ig, o);
+      if (lane >= o) { il += tl; ig += tg; }
+    }
+    if (lane == 31) { wl[wid] = il; wg[wid] = ig; }
+    __syncthreads();
+    if (wid == 0) {
+      long long vl = wl[lane], vg = wg[lane];
+      long long sl = vl, sg = vg;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        long long tl = __shfl_up_sync(0xffffffffu, sl, o);
+        long long tg = __shfl_up_sync(0xffffffffu, sg, o);
+        if (lane >= o) { sl += tl; sg += tg; }
+      }
+      wl[lane] = sl - vl;
+      wg[lane] = sg - vg;
+    }
+    __syncthreads();
+    const long long excl_l = lrun + wl[wid] + il - lsz;
+    const long long incl_g = grun + wg[wid] + ig;
+    if (j < nprobe) po[j] = (int)excl_l;
+    // sample rule: first j with cumulative global size >= budget
+    int cand = (j < nprobe && incl_g >= b.budget && incl_g - gsz < b.budget) ? j : -1;
+    __shared__ int s_first;
+    if (threadIdx.x == 0) s_first = -1;
+    __syncthreads();
+    if (cand >= 0) s_first = cand;
+    __syncthreads();
+    if (s < 0 && s_first >= 0) s = s_first;
+    // block totals
+    __shared__ long long tot_l, tot_g;
+    if (threadIdx.x == kSelNT - 1) { tot_l = wl[wid] + il; tot_g = wg[wid] + ig; }
+    __syncthreads();
+    lrun += tot_l;
+    grun += tot_g;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    po[nprobe] = (int)lrun;
+    int ns;
+    if (grun <= b.budget) ns = 0;
+    else {
+      int s0 = nprobe < kSampleMinLists ? nprobe : kSampleMinLists;
+      ns = s + 1 > s0 ? s + 1 : s0;
+    }
+    b.nsamp[q] = ns;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// a2  PQ lookup table: LUT[q][m][c] = sum_t (q_t - C[m][c][t])^2, t ascending (canonical)
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_pq_lut(Batch b, Dev ix) {
+  const int m = blockIdx.x, q = blockIdx.y, c = threadIdx.x;
+  const int ds = ix.d / ix.M;
+  const float* qv = b.Q + (size_t)q * ix.d + m * ds;
+  const float* cb = ix.books + ((size_t)m * 256 + c) * ds;
+  float acc = 0.f;
+  for (int t = 0; t < ds; ++t) {
+    float df = __fsub_rn(qv[t], cb[t]);
+    acc = __fadd_rn(acc, __fmul_rn(df, df));
+  }
+  b.table[((size_t)q * ix.M + m) * 256 + c] = acc;
+}
+
+// RaBitQ rotated query u = P^T q: u_i = sum_{t<d} P[t][i] q_t, t ascending (canonical).
+__global__ void __launch_bounds__(256) k_rbq_rotate(Batch b, Dev ix) {
+  extern __shared__ float sq[];
+  const int q = blockIdx.y, i = blockIdx.x * 256 + threadIdx.x;
+  for (int t = threadIdx.x; t < ix.d; t += 256) sq[t] = b.Q[(size_t)q * ix.d + t];
+  __syncthreads();
+  if (i >= ix.D) return;
+  float acc = 0.f;
+  for (int t = 0; t < ix.d; ++t) acc = __fadd_rn(acc, __fmul_rn(ix.P[(size_t)t * ix.D + i], sq[t]));
+  b.table[(size_t)q * ix.D + i] = acc;
+}
+
+// ------------------------------------------------------------------------------------------
+// bucket id (Eq. 6 with DESIGN R3): precomputed per query
+// ------------------------------------------------------------------------------------------
+struct CellFn {
+  float dmin, dmax, inv;
+  bool degen;
+  __device__ __forceinline__ void init(float lo, float hi) {
+    dmin = lo;
+    dmax = hi;
+    float w = __fsub_rn(hi, lo);
+    degen = !(w > 0.f);
+    inv = degen ? 0.f : __fdiv_rn(255.0f, w);
+    if (!degen && isinf(inv)) degen = true;
+  }
+  __device__ __forceinline__ int operator()(float x) const {
+    if (x > dmax) return 255;
+    if (degen) return 0;
+    float t = __fmul_rn(__fsub_rn(x, dmin), inv);
+    float f = floorf(t);
+    return f < 0.f ? 0 : (f > 254.f ? 254 : (int)f);
+  }
+};
+
+// ------------------------------------------------------------------------------------------
+// a3/a4  PQ code scan.  CTA = (group of G probed lists, query).  The query's LUT lives in shared
+// memory; each thread estimates whole objects: est = LUT[0][c0] + ... + LUT[M-1][c_{M-1}].
+//   SAMPLE: lists j < nsamp[q] -> est written to val (the sample)
+//   FULL:   every probed list  -> bucket id to cells, histogram of ids < 255 (Push, Alg. 1 l.1-4)
+// ------------------------------------------------------------------------------------------
+constexpr int kScanNT = 256;
+template <int M, bool SAMPLE>
+__global__ void __launch_bounds__(kScanNT) k_pq_scan(Batch b, Dev ix, int G) {
+  extern __shared__ float lut[];            // [M x 256]
+  __shared__ int hist[kCells];
+  const int q = blockIdx.y;
+  const int ns = b.nsamp[q];
+  if (ns == 0) return;                      // tau = infinity: no buckets (Alg. 1 l.11)
+  const int jlim = SAMPLE ? ns : b.nprobe;
+  if (blockIdx.x * G >= jlim) return;
+  const float* gl = b.table + (size_t)q * M * 256;
+  for (int i = threadIdx.x; i < M * 64; i += kScanNT)
+    reinterpret_cast<float4*>(lut)[i] = reinterpret_cast<const float4*>(gl)[i];
+  CellFn cf;
+  if (!SAMPLE) {
+    for (int i = threadIdx.x; i < kCells; i += kScanNT) hist[i] = 0;
+    cf.init(b.edges[2 * q], b.edges[2 * q + 1]);
+  }
+  __syncthreads();
+  const int* po = b.poff + (size_t)q * (b.nprobe + 1);
+  const int* pr = b.probe + (size_t)q * b.nprobe;
+  for (int g0 = blockIdx.x * G; g0 < jlim; g0 += gridDim.x * G)
+  for (int j = g0; j < min(g0 + G, jlim); ++j) {
+    const int L = pr[j];
+    const long long row0 = ix.loff[L];
+    const int n = (int)(ix.loff[L + 1] - row0);
+    const long long e0 = (long long)q * b.cap + po[j];
+    for (int i = threadIdx.x; i < n; i += kScanNT) {
+      const uint8_t* cp = ix.codes + (size_t)(row0 + i) * M;
+      uint32_t w[M / 4];
+      if constexpr (M % 16 == 0) {
+#pragma unroll
+        for (int v = 0; v < M / 16; ++v) {
+          uint4 x = __ldg(reinterpret_cast<const uint4*>(cp) + v);
+          w[4 * v] = x.x; w[4 * v + 1] = x.y; w[4 * v + 2] = x.z; w[4 * v + 3] = x.w;
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < M / 8; ++v) {
+          uint2 x = __ldg(reinterpret_cast<const uint2*>(cp) + v);
+          w[2 * v] = x.x; w[2 * v + 1] = x.y;
+        }
+      }
+      float acc = lut[w[0] & 255u];
+#pragma unroll
+      for (int m = 1; m < M; ++m) {
+        const uint32_t c = (w[m >> 2] >> (8 * (m & 3))) & 255u;
+        acc = __fadd_rn(acc, lut[m * 256 + c]);
+      }
+      if (SAMPLE) {
+        b.val[e0 + i] = acc;
+      } else {
+        const int cell = cf(acc);
+        b.cells[e0 + i] = (uint8_t)cell;
+        if (cell < 255) atomicAdd(&hist[cell], 1);
+      }
+    }
+  }
+  if (!SAMPLE) {
+    __syncthreads();
+    int* gh = b.hist + (size_t)q * kCells;
+    for (int i = threadIdx.x; i < kCells; i += kScanNT)
+      if (hist[i]) atomicAdd(&gh[i], hist[i]);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// a3/a4  RaBitQ scan: per (query, list) 4-bit query code as 4 bit planes in shared memory, then
+// ip = <bits, qbar> = sum_p 2^p popc(bits & plane_p) per object (B_q = 4).
+// ------------------------------------------------------------------------------------------
+template <bool SAMPLE>
+__global__ void __launch_bounds__(kScanNT) k_rbq_scan(Batch b, Dev ix, int G) {
+  extern __shared__ float smem[];
+  const int D = ix.D, W = D / 32;
+  float* qp = smem;                                       // [D]
+  uint32_t* planes = reinterpret_cast<uint32_t*>(smem + D); // [4 x W]
+  __shared__ int hist[kCells];
+  __shared__ float red_mn[kScanNT / 32], red_mx[kScanNT / 32];
+  __shared__ int red_s[kScanNT / 32];
+  __shared__ float s_c[4];
+  const int q = blockIdx.y;
+  const int ns = b.nsamp[q];
+  if (ns == 0) return;
+  const int jlim = SAMPLE ? ns : b.nprobe;
+  if (blockIdx.x * G >= jlim) return;
+  CellFn cf;
+  if (!SAMPLE) {
+    for (int i = threadIdx.x; i < kCells; i += kScanNT) hist[i] = 0;
+    cf.init(b.edges[2 * q], b.edges[2 * q + 1]);
+  }
+  const float* u = b.table + (size_t)q * D;
+  const int* po = b.poff + (size_t)q * (b.nprobe + 1);
+  const int* pr = b.probe + (size_t)q * b.nprobe;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int g0 = blockIdx.x * G; g0 < jlim; g0 += gridDim.x * G)
+  for (int j = g0; j < min(g0 + G, jlim); ++j) {
+    const int L = pr[j];
+    const float rq2 = b.rq2[(size_t)q * b.nprobe + j];
+    const float r = __fsqrt_rn(rq2);
+    const float* w = ix.wL + (size_t)L * D;
+    float mn = INFINITY, mx = -INFINITY;
+    for (int i = threadIdx.x; i < D; i += kScanNT) {
+      float v = r > 0.f ? __fdiv_rn(__fsub_rn(u[i], w[i]), r) : 0.f;
+      qp[i] = v;
+      mn = fminf(mn, v);
+      mx = fmaxf(mx, v);
+    }
+    mn = warp_min(mn);
+    mx = warp_max(mx);
+    if (lane == 0) { red_mn[wid] = mn; red_mx[wid] = mx; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float a = red_mn[0], c = red_mx[0];
+      for (int t = 1; t < kScanNT / 32; ++t) { a = fminf(a, red_mn[t]); c = fmaxf(c, red_mx[t]); }
+      s_c[0] = a;
+      s_c[1] = __fdiv_rn(__fsub_rn(c, a), 15.0f);
+    }
+    __syncthreads();
+    const float vl = s_c[0], delta = s_c[1];
+    int sq = 0;
+    for (int base = 0; base < D; base += kScanNT) {      // D is a multiple of 64
+      const int i = base + threadIdx.x;
+      int qb = 0;
+      if (i < D && delta > 0.f) {
+        float t = floorf(__fadd_rn(__fdiv_rn(__fsub_rn(qp[i], vl), delta), 0.5f));
+        qb = t < 0.f ? 0 : (t > 15.f ? 15 : (int)t);
+      }
+      sq += qb;
+      const bool act = (base + wid * 32) < D;
+      if (act) {
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          unsigned m = __ballot_sync(0xffffffffu, (qb >> p) & 1);
+          if (lane == 0) planes[p * W + (i >> 5)] = m;
+        }
+      }
+    }
+    sq = warp_sum(sq);
+    if (lane == 0) red_s[wid] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int s = 0;
+      for (int t = 0; t < kScanNT / 32; ++t) s += red_s[t];
+      const float sD = __fsqrt_rn((float)D);
+      s_c[0] = __fdiv_rn(__fmul_rn(2.0f, delta), sD);                               // c1
+      s_c[1] = __fdiv_rn(__fmul_rn(2.0f, vl), sD);                                  // c2
+      s_c[2] = __fsub_rn(-__fdiv_rn(__fmul_rn(delta, (float)s), sD), __fmul_rn(sD, vl)); // c3
+    }
+    __syncthreads();
+    const float c1 = s_c[0], c2 = s_c[1], c3 = s_c[2];
+    const long long row0 = ix.loff[L];
+    const int n = (int)(ix.loff[L + 1] - row0);
+    const long long e0 = (long long)q * b.cap + po[j];
+    for (int i = threadIdx.x; i < n; i += kScanNT) {
+      const uint2* bp = reinterpret_cast<const uint2*>(ix.bits + (size_t)(row0 + i) * (D / 8));
+      int ip = 0, pc = 0;
+      for (int v = 0; v < W / 2; ++v) {
+        uint2 x = __ldg(bp + v);
+        const int w0 = 2 * v;
+        pc += __popc(x.x) + __popc(x.y);
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+          ip += (__popc(x.x & planes[p * W + w0]) + __popc(x.y & planes[p * W + w0 + 1])) << p;
+      }
+      const float2 f = __ldg(reinterpret_cast<const float2*>(ix.factors) + row0 + i);
+      const float t1 = __fmul_rn(c2, (float)pc);
+      const float t2 = __fadd_rn(t1, c3);
+      const float t3 = __fmul_rn(c1, (float)ip);
+      const float oq = __fadd_rn(t3, t2);
+      const float e = __fdiv_rn(oq, f.y);
+      const float a = __fmul_rn(f.x, f.x);
+      const float s = __fadd_rn(a, rq2);
+      const float ff = __fmul_rn(__fmul_rn(2.0f, f.x), r);
+      const float est = __fsub_rn(s, __fmul_rn(ff, e));
+      if (SAMPLE) {
+        b.val[e0 + i] = est;
+      } else {
+        const int cell = cf(est);
+        b.cells[e0 + i] = (uint8_t)cell;
+        if (cell < 255) atomicAdd(&hist[cell], 1);
+      }
+    }
+    __syncthreads();
+  }
+  if (!SAMPLE) {
+    int* gh = b.hist + (size_t)q * kCells;
+    for (int i = threadIdx.x; i < kCells; i += kScanNT)
+      if (hist[i]) atomicAdd(&gh[i], hist[i]);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// a3  edges: d_min = min of the sample estimates, d_max = budget-th smallest
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSelNT) k_select_edges(Batch b, Dev ix) {
+  __shared__ SelectSmem sm;
+  const int q = blockIdx.x;
+  const int ns = b.nsamp[q];
+  if (ns == 0) return;
+  const int n = b.poff[(size_t)q * (b.nprobe + 1) + ns];
+  const float* v = b.val + (size_t)q * b.cap;
+  auto load = [&](int64_t i) -> uint64_t { return (uint64_t)f2key(v[i]); };
+  int ps;
+  uint64_t kmin = cta_select<kSelNT>(n, 1, load, true, &ps, sm);
+  uint64_t kmax = cta_select<kSelNT>(n, b.budget, load, true, &ps, sm);
+  if (threadIdx.x == 0) {
+    b.edges[2 * q] = key2f((uint32_t)kmin);
+    b.edges[2 * q + 1] = key2f((uint32_t)kmax);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// a5+a6  threshold bucket and superset compaction (deterministic: probe order)
+// ------------------------------------------------------------------------------------------
+constexpr int kCompNT = 1024;
+__global__ void __launch_bounds__(kCompNT) k_compact(Batch b, Dev ix) {
+  __shared__ int s_poff[kMaxProbe + 1];
+  __shared__ int wcnt[kCompNT / 32 + 1];
+  __shared__ int s_tau;
+  const int q = blockIdx.x;
+  const int nprobe = b.nprobe;
+  const int* po = b.poff + (size_t)q * (nprobe + 1);
+  for (int j = threadIdx.x; j <= nprobe; j += kCompNT) s_poff[j] = po[j];
+  const int ns = b.nsamp[q];
+  if (threadIdx.x < 32) {
+    int tau = kTauInf;
+    if (ns > 0) {
+      // Update: first cell whose cumulative count reaches the budget (8 cells per lane)
+      const int* H = b.hist + (size_t)q * kCells;
+      const int lane = threadIdx.x;
+      long long v[8], s = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) { v[j] = H[lane * 8 + j]; s += v[j]; }
+      long long incl = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        long long t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      long long c = incl - s;
+      int found = 1 << 30;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        c += v[j];
+        if (c >= b.budget && found == (1 << 30)) found = lane * 8 + j;
+      }
+      found = warp_min(found);
+      tau = found;            // < 255 guaranteed by the sample rule (DESIGN R5)
+    }
+    if (threadIdx.x == 0) s_tau = tau;
+  }
+  __syncthreads();
+  const int tau = s_tau;
+  const int n = s_poff[nprobe];
+  const uint8_t* cl = b.cells + (size_t)q * b.cap;
+  int* out = b.cpos + (size_t)q * b.cap;
+  const int* pr = b.probe + (size_t)q * nprobe;
+  int base = 0;
+  for (int t0 = 0; t0 < n; t0 += kCompNT) {
+    const int i = t0 + threadIdx.x;
+    bool f = false;
+    if (i < n) f = (tau == kTauInf) || ((int)cl[i] <= tau);
+    int total;
+    int r = block_rank<kCompNT>(f, wcnt, &total);
+    if (f) {
+      int lo = 0, hi = nprobe - 1;                // last j with s_poff[j] <= i
+      while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (s_poff[mid] <= i) lo = mid; else hi = mid - 1;
+      }
+      out[base + r] = (int)(ix.loff[pr[lo]] + (i - s_poff[lo]));
+    }
+    base += total;
+  }
+  if (threadIdx.x == 0) {
+    b.ncand[q] = base;
+    b.tau[q] = tau;
+    atomicAdd((unsigned long long*)&b.stats[0], (unsigned long long)n);
+    atomicAdd((unsigned long long*)&b.stats[1], (unsigned long long)base);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// a7  exact re-rank: one warp per candidate row, 16-byte loads, shuffle reduction.
+//     After it, cpos holds the candidate's original id and val its exact d^2.
+// ------------------------------------------------------------------------------------------
+constexpr int kRrNT = 256;
+constexpr int kRrUnroll = 4;
+template <bool U8>
+__global__ void __launch_bounds__(kRrNT) k_rerank(Batch b, Dev ix) {
+  extern __shared__ float sq[];
+  const int q = blockIdx.y;
+  const int d = ix.d;
+  for (int t = threadIdx.x; t < d; t += kRrNT) sq[t] = b.Q[(size_t)q * d + t];
+  __syncthreads();
+  const int nc = b.ncand[q];
+  int* cp = b.cpos + (size_t)q * b.cap;
+  float* vv = b.val + (size_t)q * b.cap;
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * (kRrNT / 32) + (threadIdx.x >> 5);
+  const int nw = gridDim.x * (kRrNT / 32);
+  for (int c0 = gw * kRrUnroll; c0 < nc; c0 += nw * kRrUnroll) {
+    int row[kRrUnroll];
+    float acc[kRrUnroll];
+#pragma unroll
+    for (int u = 0; u < kRrUnroll; ++u) {
+      row[u] = (c0 + u < nc) ? cp[c0 + u] : -1;
+      acc[u] = 0.f;
+    }
+    if constexpr (!U8) {
+      const int nv = d / 4;
+      for (int t = lane; t < nv; t += 32) {
+        float4 x[kRrUnroll];
+#pragma unroll
+        for (int u = 0; u < kRrUnroll; ++u)
+          if (row[u] >= 0)
+            x[u] = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(ix.raw) + (size_t)row[u] * d) + t);
+        const float4 qq = reinterpret_cast<const float4*>(sq)[t];
+#pragma unroll
+        for (int u = 0; u < kRrUnroll; ++u)
+          if (row[u] >= 0) {
+            float a = x[u].x - qq.x, bb = x[u].y - qq.y, c = x[u].z - qq.z, e = x[u].w - qq.w;
+            acc[u] = fmaf(a, a, acc[u]);
+            acc[u] = fmaf(bb, bb, acc[u]);
+            acc[u] = fmaf(c, c, acc[u]);
+            acc[u] = fmaf(e, e, acc[u]);
+          }
+      }
+    } else {
+      const int nv = d / 16;
+      for (int t = lane; t < nv; t += 32) {
+        uint4 x[kRrUnroll];
+#pragma unroll
+        for (int u = 0; u < kRrUnroll; ++u)
+          if (row[u] >= 0)
+            x[u] = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(ix.raw) + (size_t)row[u] * d) + t);
+#pragma unroll
+        for (int u = 0; u < kRrUnroll; ++u)
+          if (row[u] >= 0) {
+            const uint32_t wv[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h)
+#pragma unroll
+              for (int by = 0; by < 4; ++by) {
+                float xv = (float)((wv[h] >> (8 * by)) & 255u);
+                float df = xv - sq[t * 16 + h * 4 + by];
+                acc[u] = fmaf(df, df, acc[u]);
+              }
+          }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kRrUnroll; ++u) acc[u] = warp_sum(acc[u]);
+    if (lane < kRrUnroll && c0 + lane < nc) {
+      float a = acc[0];
+#pragma unroll
+      for (int u = 1; u < kRrUnroll; ++u) if (lane == u) a = acc[u];
+      vv[c0 + lane] = a;
+      cp[c0 + lane] = (int)ix.ids[row[lane] >= 0 ? row[lane] : 0];
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// a8  final top-k by (exact d^2, id): CTA radix select, then order-preserving write-out.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSelNT) k_final_select(Batch b, Dev ix, long long* out_ids,
+                                                         float* out_d2) {
+  __shared__ SelectSmem sm;
+  __shared__ int wcnt[kSelNT / 32 + 1];
+  const int q = blockIdx.x;
+  const int nc = b.ncand[q];
+  const int k = b.k;
+  const int* cp = b.cpos + (size_t)q * b.cap;
+  const float* vv = b.val + (size_t)q * b.cap;
+  long long* oi = out_ids + (size_t)q * k;
+  float* od = out_d2 + (size_t)q * k;
+  auto load = [&](int64_t i) -> uint64_t {
+    return ((uint64_t)f2key(vv[i]) << 32) | (uint32_t)cp[i];
+  };
+  uint64_t pref = ~0ull;
+  int pshift = 0;
+  if (nc > k) pref = cta_select<kSelNT>(nc, k, load, false, &pshift, sm);
+  int base = 0;
+  for (int t0 = 0; t0 < nc; t0 += kSelNT) {
+    const int i = t0 + threadIdx.x;
+    uint64_t key = 0;
+    bool f = false;
+    if (i < nc) {
+      key = load(i);
+      f = shr64(key, pshift) <= pref;
+    }
+    int total;
+    int r = block_rank<kSelNT>(f, wcnt, &total);
+    if (f && base + r < k) {
+      oi[base + r] = (long long)(uint32_t)key;
+      od[base + r] = vv[i];
+    }
+    base += total;
+  }
+  for (int i = base + threadIdx.x; i < k; i += kSelNT) {
+    oi[i] = -1;
+    od[i] = INFINITY;
+  }
+}
+
+}  // namespace bbc

@@ -31,6 +31,11 @@ def load_cfg(name):
 
 
 @pytest.fixture(scope="session")
+def load():
+    return load_cfg
+
+
+@pytest.fixture(scope="session")
 def c1t():
     return load_cfg("C1t")
 

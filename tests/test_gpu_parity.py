@@ -1,0 +1,208 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle, element by element.
+
+Tolerances (BASELINE.json north_star): probe lists, sample counts, edges,
+estimates, histograms, thresholds and superset ids bit-exact (canonical fp32 order on both
+sides); exact d^2 within 1e-5 relative; final id sets identical except ids whose oracle d^2 is
+within 1e-5 relative of the oracle's k-th d^2; recall equal within 0.001.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _index(path):
+    from paper_2604_01960_b200 import Index
+    return Index(path)
+
+
+_IDX = {}
+_LOAD = {}
+
+
+@pytest.fixture(autouse=True)
+def _bind_loader(load):
+    _LOAD["f"] = load
+
+
+def gpu_index(name):
+    cfg, ix, Q, path = _LOAD["f"](name)
+    if name not in _IDX:
+        _IDX[name] = _index(path)
+    return cfg, ix, Q, _IDX[name]
+
+
+def compare(cfg, ix, Q, gidx, k, nprobe, budget, want_est=True, check_final=True):
+    from oracle import bbc_oracle as O
+    q = torch.from_numpy(Q).cuda()
+    ids, d2, t = gidx.search_debug(q, k, nprobe, budget, want_est=want_est)
+    torch.cuda.synchronize()
+    t = {a: b.cpu().numpy() for a, b in t.items()}
+    ids, d2 = ids.cpu().numpy(), d2.cpu().numpy()
+    oi, od, dbg = O.search(ix, Q, k, nprobe, budget, want_debug=True)
+    for i, g in enumerate(dbg):
+        assert np.array_equal(t["probe"][i], g["probe"]), f"q{i} probe"
+        assert np.array_equal(t["rq2"][i].view(np.uint32), g["rq2"].view(np.uint32)), f"q{i} rq2"
+        assert t["n_probed"][i] == g["n_o"], f"q{i} n_o"
+        assert t["nsample"][i] == g["s"], f"q{i} sample lists"
+        if want_est:
+            ge = t["est"][i][: g["n_o"]]
+            assert np.array_equal(ge.view(np.uint32), g["est"].view(np.uint32)), \
+                f"q{i} est: {np.count_nonzero(ge != g['est'])} differ"
+        if g["s"] > 0:
+            assert t["edges"][i][0] == g["d_min"] and t["edges"][i][1] == g["d_max"], f"q{i} edges"
+            assert np.array_equal(t["hist"][i][:255], g["H"][:255]), f"q{i} hist"
+            assert t["tau"][i] == g["tau"], f"q{i} tau"
+        else:
+            assert t["tau"][i] == O.TAU_INF
+        nc = t["n_cand"][i]
+        assert nc == len(g["sup_ids"]), f"q{i} |S*|"
+        assert np.array_equal(t["cand_ids"][i][:nc], g["sup_ids"]), f"q{i} superset ids"
+        np.testing.assert_allclose(t["cand_d2"][i][:nc], g["sup_d2"], rtol=1e-5, atol=1e-6)
+        if check_final:
+            check_final_ids(ids[i], d2[i], oi[i], od[i], k)
+    return ids, d2, t
+
+
+def check_final_ids(gi, gd, oi, od, k):
+    """Same id set except at ties of the k-th distance (within 1e-5 relative)."""
+    valid = oi >= 0
+    assert np.count_nonzero(gi >= 0) == np.count_nonzero(valid)
+    if not valid.any():
+        return
+    kth = od[valid].max()
+    tol = 1e-5 * max(abs(kth), 1e-30)
+    go, oo = set(gi[gi >= 0].tolist()), set(oi[valid].tolist())
+    for x in go ^ oo:
+        # the differing id must sit at the boundary distance
+        if x in oo:
+            dx = od[oi == x][0]
+        else:
+            dx = gd[gi == x][0]
+        assert abs(dx - kth) <= tol, f"id {x} d2 {dx} vs kth {kth}"
+    assert len(go) == len(gi[gi >= 0])                   # no duplicates
+
+
+@pytest.mark.parametrize("name", ["C1t", "C1s", "C2s", "C3s"])
+def test_parity_config_point(name):
+    cfg, ix, Q, g = gpu_index(name)
+    compare(cfg, ix, Q, g, cfg.k, cfg.nprobe, cfg.budget)
+
+
+@pytest.mark.parametrize("name", ["C1t", "C2s", "C3s"])
+def test_parity_parameter_grid(name):
+    cfg, ix, Q, g = gpu_index(name)
+    for nprobe, bm in ((1, 1), (3, 2), (cfg.nprobe * 2, 1), (min(cfg.nlist, 64), 3)):
+        nprobe = min(nprobe, cfg.nlist)
+        for k in (1, 17, cfg.k):
+            compare(cfg, ix, Q[:6], g, k, nprobe, max(k, int(bm * k)), want_est=False)
+
+
+def test_full_probe_unlimited_budget_is_brute_force():
+    from oracle import bruteforce as BF
+    cfg, ix, Q, g = gpu_index("C1t")
+    raw = np.asarray(ix["raw"])
+    X = np.empty_like(raw)
+    X[np.asarray(ix["ids"])] = raw
+    q = torch.from_numpy(Q).cuda()
+    ids, d2 = g.search(q, cfg.k, cfg.nlist, cfg.N)
+    gi, gd = BF.ground_truth(Q, X, cfg.k)
+    ids = ids.cpu().numpy()
+    d2 = d2.cpu().numpy()
+    for i in range(len(Q)):
+        check_final_ids(ids[i], d2[i], gi[i], gd[i].astype(np.float32), cfg.k)
+
+
+def test_edge_cases():
+    from paper_2604_01960_b200.bbc import BBCError
+    cfg, ix, Q, g = gpu_index("C1t")
+    q = torch.from_numpy(Q).cuda()
+    # n_o < k: padded rows (tau = infinity)
+    ids, d2, t = compare(cfg, ix, Q[:3], g, 5000, 1, 5000)
+    assert (ids[:, -1] == -1).all() and np.isinf(d2[:, -1]).all()
+    # budget == k, k == 1, single query, empty batch
+    compare(cfg, ix, Q[:1], g, 1, 4, 1)
+    compare(cfg, ix, Q[:2], g, 250, 6, 250)
+    e = torch.empty((0, cfg.d), dtype=torch.float32, device="cuda")
+    g.search(e, 10, 4, 20)
+    # errors
+    for k, nprobe, budget in ((0, 4, 10), (10, 0, 10), (10, cfg.nlist + 1, 10), (10, 4, 9),
+                              (cfg.N + 1, 4, cfg.N + 1)):
+        with pytest.raises(BBCError):
+            g.search(q, k, nprobe, budget)
+
+
+def test_degenerate_identical_vectors(tmp_path):
+    """All database vectors equal: every estimate is equal, d_max == d_min, every object lands in
+    cell 0 and the final selection is decided by id alone."""
+    from datagen import build_index, configs, index_file, synth
+    cfg = configs.get("C1t").replace(name="degen", N=1500, nlist=8, M=16, kmeans_iters=2,
+                                     pq_train=1500, pq_iters=2)
+    X = np.repeat(synth.generate_data(cfg)[:1], cfg.N, axis=0)
+    idx = build_index.build(cfg, X=X)
+    p = str(tmp_path / "degen.bbcivf")
+    index_file.write(p, idx)
+    ix = index_file.read(p)
+    g = _index(p)
+    Q = synth.generate_queries(cfg)[:3]
+    ids, d2, t = compare(cfg, ix, Q, g, 100, 8, 300)
+    for i in range(3):
+        assert sorted(ids[i].tolist()) == list(range(100))
+
+
+def test_microbatching_matches_one_batch():
+    cfg, ix, Q, g = gpu_index("C2s")
+    q = torch.from_numpy(Q).cuda()
+    a_ids, a_d2 = g.search(q, cfg.k, cfg.nprobe, cfg.budget)
+    _, mn = g.workspace_size(len(Q), cfg.k, cfg.nprobe, cfg.budget)
+    ws = torch.empty(mn + (mn // 3), dtype=torch.uint8, device="cuda")   # one query per batch
+    b_ids, b_d2 = g.search(q, cfg.k, cfg.nprobe, cfg.budget, workspace=ws)
+    assert torch.equal(a_ids, b_ids) and torch.equal(a_d2, b_d2)
+    assert g.last_stats()["microbatches"] == len(Q)
+
+
+def test_host_api_matches_device_api():
+    cfg, ix, Q, g = gpu_index("C2s")
+    q = torch.from_numpy(Q).cuda()
+    a_ids, a_d2 = g.search(q, cfg.k, cfg.nprobe, cfg.budget)
+    h_ids, h_d2 = g.search_host(Q, cfg.k, cfg.nprobe, cfg.budget)
+    assert np.array_equal(a_ids.cpu().numpy(), h_ids)
+    assert np.array_equal(a_d2.cpu().numpy(), h_d2)
+
+
+def test_recall_matches_oracle():
+    from oracle import bbc_oracle as O
+    from oracle import bruteforce as BF
+    cfg, ix, Q, g = gpu_index("C1s")
+    raw = np.asarray(ix["raw"])
+    X = np.empty_like(raw)
+    X[np.asarray(ix["ids"])] = raw
+    q = torch.from_numpy(Q).cuda()
+    ids, d2 = g.search(q, cfg.k, cfg.nprobe, cfg.budget)
+    ids = ids.cpu().numpy()
+    oi, od = O.search(ix, Q, cfg.k, cfg.nprobe, cfg.budget)
+    gi, gd = BF.ground_truth(Q, X, cfg.k)
+    ex = lambda R: np.stack([BF.exact_all(Q[i], X)[np.maximum(R[i], 0)] for i in range(len(Q))])
+    r_gpu = BF.recall(ids, ex(ids), gi, gd)
+    r_orc = BF.recall(oi, ex(oi), gi, gd)
+    assert abs(r_gpu - r_orc) <= 1e-3
+
+
+@pytest.mark.slow
+def test_full_size_c2_sampled_queries():
+    """BASELINE.json configs[1] at full size, in the launch configuration bench.py times (all 1,000
+    queries in one call); 24 sampled queries compared with the oracle one by one."""
+    from oracle import bbc_oracle as O
+    cfg, ix, Q, g = gpu_index("C2")
+    q = torch.from_numpy(Q).cuda()
+    ids, d2 = g.search(q, cfg.k, cfg.nprobe, cfg.budget)
+    ids, d2 = ids.cpu().numpy(), d2.cpu().numpy()
+    sample = np.random.default_rng(7).choice(len(Q), 24, replace=False)
+    oi, od = O.search(ix, Q[sample], cfg.k, cfg.nprobe, cfg.budget)
+    for j, i in enumerate(sample):
+        check_final_ids(ids[i], d2[i], oi[j], od[j], cfg.k)
+    # invariants over every query: k distinct ids, distances ascending in no particular order
+    for i in range(len(Q)):
+        assert len(set(ids[i].tolist())) == cfg.k

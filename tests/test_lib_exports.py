@@ -1,0 +1,54 @@
+"""The C-ABI library builds for sm_100a, loads, and exports every function include/bbc.h declares
+(no compute calls: this runs without a GPU)."""
+import ctypes
+import os
+import re
+import subprocess
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    with open(os.path.join(ROOT, "include", "bbc.h")) as f:
+        src = f.read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"^\s*(?:bbc_status|void|int64_t|const char\*)\s+(\w+)\s*\(", src, flags=re.M)
+    return sorted(set(names))
+
+
+def test_header_declares_the_boundary():
+    names = _declared()
+    for must in ("ivf_load", "ivf_free", "bbc_search", "bbc_search_host", "bbc_workspace_size"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2604_01960_b200 import build
+    lib_path = build.build()
+    L = ctypes.CDLL(lib_path)
+    for name in _declared():
+        assert hasattr(L, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", lib_path], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (\w+)$", out, flags=re.M))
+    assert set(_declared()) <= exported
+    from paper_2604_01960_b200 import bbc
+    assert set(bbc.EXPORTS) == set(_declared())
+
+
+def test_sass_is_sm100a():
+    from paper_2604_01960_b200 import build
+    lib_path = build.build()
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", lib_path],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_argument_errors_without_gpu():
+    """Argument validation happens before any device work: a null index is rejected."""
+    from paper_2604_01960_b200 import bbc
+    L = bbc.lib()
+    size = ctypes.c_size_t()
+    assert L.bbc_workspace_size(None, 1, 1, 1, 1, ctypes.byref(size), None) == 1
+    assert b"null" in L.bbc_last_error()
+    h = ctypes.c_void_p()
+    assert L.ivf_load(b"/nonexistent/index", 0, 1, 0, ctypes.byref(h)) == 2
