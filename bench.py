@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 BBC query path (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2] [--impl bbc|reference]
+
+A step = one bbc_search over the workload's whole query batch (all steps a1-a8 of DESIGN.md
+section 1) with queries already resident in HBM; L2 is flushed (256 MB write) between timed steps,
+outside the timed events.  `value` = queries/s of the whole job (all ranks), timed with CUDA
+events on the search stream, max over ranks.  `e2e` = the same through bbc_search_host with the
+host->device query copy and the device->host result copy inside the timed region.
+
+Multi-GPU (torchrun): the batch of queries is sharded across ranks (each rank runs its own
+batch of `nq` queries on a replicated index: independent problems, no data-path collective,
+"scaling": "weak").
+
+--impl reference times the CPU oracle (oracle/, test infrastructure) on a bounded sample of the
+same workload, on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import datagen  # noqa: E402
+from datagen import configs, groundtruth, index_file, synth  # noqa: E402
+
+# Operating points (nprobe, budget) per workload where GPU recall@k >= 0.95 on the first 100
+# queries (sweep: `python bench.py --sweep`).  None = use the config point.
+RECALL95 = {"C2": (768, 20000)}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="bbc", choices=["bbc", "reference"])
+    p.add_argument("--workload", default="C2")
+    p.add_argument("--nprobe", type=int, default=None)
+    p.add_argument("--budget", type=int, default=None)
+    p.add_argument("--recall-queries", type=int, default=100)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=15.0)
+    p.add_argument("--sweep", action="store_true", help="recall/QPS over an (nprobe, budget) grid")
+    p.add_argument("--profile-steps", action="store_true", help="no warm-up/recall/cpu (ncu runs)")
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return float(m["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, dev: int):
+        self.dev = dev
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def operating_point(cfg, args):
+    op = RECALL95.get(cfg.name)
+    nprobe = args.nprobe or (op[0] if op else cfg.nprobe)
+    budget = args.budget or (op[1] if op else cfg.budget)
+    return nprobe, budget
+
+
+def load_workload(name: str):
+    cfg = configs.get(name)
+    path = datagen.ensure_index(cfg)
+    return cfg, path
+
+
+def database_in_id_order(path):
+    ix = index_file.read(path)
+    raw = np.asarray(ix["raw"])
+    X = np.empty_like(raw)
+    X[np.asarray(ix["ids"])] = raw
+    return X
+
+
+# ------------------------------------------------------------------------------------ reference
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import bbc_oracle as O
+    cfg, path = load_workload(args.workload)
+    nprobe, budget = operating_point(cfg, args)
+    ix = index_file.read(path)
+    Q = synth.generate_queries(cfg)
+    t0 = time.perf_counter()
+    O.search(ix, Q[:2], cfg.k, nprobe, budget)
+    per_q = max(1e-3, (time.perf_counter() - t0) / 2)
+    # each step a bounded sample: the whole run stays within a few minutes
+    budget_s = 120.0 / max(1, args.steps + args.warmup)
+    ns = int(max(1, min(cfg.nq, budget_s / per_q)))
+    for w in range(args.warmup):
+        O.search(ix, Q[:ns], cfg.k, nprobe, budget)
+    tot = 0.0
+    for s in range(args.steps):
+        sl = Q[(s * ns) % cfg.nq:][:ns]
+        t0 = time.perf_counter()
+        O.search(ix, sl, cfg.k, nprobe, budget)
+        tot += time.perf_counter() - t0
+    qps = ns * args.steps / tot
+    line = {"impl": "reference", "metric": "queries/sec at recall@k (BBC query path)",
+            "value": qps, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": cfg.name, "nq": cfg.nq, "k": cfg.k, "nprobe": nprobe,
+                       "budget": budget},
+            "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{ns} of {cfg.nq} {cfg.name} queries per step"},
+            "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg, path, nprobe, budget, seconds):
+    from oracle import bbc_oracle as O
+    ix = index_file.read(path)
+    Q = synth.generate_queries(cfg)
+    t0 = time.perf_counter()
+    O.search(ix, Q[:2], cfg.k, nprobe, budget)
+    per_q = max(1e-3, (time.perf_counter() - t0) / 2)
+    ns = int(max(2, min(cfg.nq, seconds / per_q)))
+    t0 = time.perf_counter()
+    O.search(ix, Q[:ns], cfg.k, nprobe, budget)
+    el = time.perf_counter() - t0
+    return {"value": ns / el, "unit": "queries/s", "cores": 1, "kind": "oracle",
+            "sample": f"first {ns} of {cfg.nq} {cfg.name} queries (nprobe={nprobe}, "
+                      f"budget={budget}), single-threaded numpy oracle, {el:.1f} s"}
+
+
+# ------------------------------------------------------------------------------------ GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+    from paper_2604_01960_b200 import Index, launch_count
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = configs.get(args.workload)
+    if rank == 0:
+        path = datagen.ensure_index(cfg, verbose=True)
+    if world > 1:
+        dist.barrier()
+    path = datagen.index_path(cfg)
+    nprobe, budget = operating_point(cfg, args)
+    k = cfg.k
+
+    g = Index(path, device=local)
+    if args.sweep:
+        return sweep(cfg, path, g, rank)
+    Qall = synth.generate_queries(cfg, cfg.nq * world)
+    Qh = np.ascontiguousarray(Qall[rank * cfg.nq:(rank + 1) * cfg.nq])
+    nq = len(Qh)
+    q = torch.from_numpy(Qh).cuda()
+    ws = g.workspace(nq, k, nprobe, budget)
+    out = (torch.empty((nq, k), dtype=torch.int64, device="cuda"),
+           torch.empty((nq, k), dtype=torch.float32, device="cuda"))
+    st = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    for _ in range(max(args.warmup, 0 if args.profile_steps else 3)):
+        g.search(q, k, nprobe, budget, out=out, workspace=ws)
+    torch.cuda.synchronize()
+
+    # ---------------- timed region: K steps, device time per step, L2 flushed between steps
+    g.get_timing()
+    g.set_timing(True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = launch_count()
+    with Clocks(local) as clk:
+        for s in range(args.steps):
+            flush.zero_()
+            evs[s][0].record(st)
+            g.search(q, k, nprobe, budget, out=out, workspace=ws)
+            evs[s][1].record(st)
+        torch.cuda.synchronize()
+    launches = launch_count() - l0
+    if world > 1:
+        dist.barrier()
+    g.set_timing(False)
+    stage_ms, calls = g.get_timing()
+    stats = g.last_stats()
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * nq * args.steps / (ms_max / 1e3)
+
+    # ---------------- e2e through the host API (pinned host buffers)
+    qh = torch.from_numpy(Qh).pin_memory()
+    oh = (torch.empty((nq, k), dtype=torch.int64).pin_memory(),
+          torch.empty((nq, k), dtype=torch.float32).pin_memory())
+    qn, on = qh.numpy(), (oh[0].numpy(), oh[1].numpy())
+    g.search_host(qn, k, nprobe, budget, out=on, workspace=ws)
+    e2e_ms = 0.0
+    for s in range(args.steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        g.search_host(qn, k, nprobe, budget, out=on, workspace=ws)
+        b.record(st)
+        torch.cuda.synchronize()
+        e2e_ms += a.elapsed_time(b)
+    te = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * nq * args.steps / (float(te.item()) / 1e3)
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---------------- roofline of the dominant kernel (algorithmic bytes / event-timed duration)
+    info = g.info
+    code_bytes = info.m if info.kind == 1 else info.dpad // 8 + 8
+    row_bytes = info.d * (1 if info.raw_u8 else 4)
+    scan_bytes = stats["probed"] * code_bytes            # per step (the last step's counters)
+    rr_bytes = stats["candidates"] * row_bytes
+    peak, peak_src = peaks()
+    per = {
+        "scan": {"ms": stage_ms["scan"] / args.steps, "bytes": scan_bytes},
+        "rerank": {"ms": stage_ms["rerank"] / args.steps, "bytes": rr_bytes},
+    }
+    for v in per.values():
+        v["GBs"] = v["bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] > 0 else None
+        v["frac"] = v["GBs"] / peak if v["GBs"] else None
+    dom = max(per, key=lambda n: per[n]["ms"])
+    roof = {"bound": "hbm", "kernel": dom, "achieved": per[dom]["GBs"], "peak": peak,
+            "unit": "GB/s", "frac": per[dom]["frac"], "traffic": None,
+            "peak_source": peak_src, "per_kernel": per,
+            "stage_ms_per_step": {k_: v / args.steps for k_, v in stage_ms.items()}}
+
+    # ---------------- recall on sampled queries (fp64 brute-force ground truth)
+    rq = min(args.recall_queries, nq)
+    rec = None
+    if rq > 0 and not args.profile_steps:
+        X = database_in_id_order(path)
+        gi, gd = groundtruth.cached_topk(f"{cfg.name}_{os.path.basename(path)}", Qh[:rq], X, k,
+                                         datagen.cache_dir())
+        ids = out[0][:rq].cpu().numpy()
+        ex = groundtruth.exact_of(Qh[:rq], X, ids)
+        rec = {"recall": groundtruth.recall(ids, ex, gi, gd),
+               "relative_error": groundtruth.relative_error(out[1][:rq].cpu().numpy(), gd),
+               "queries": rq}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline and not args.profile_steps:
+        cpu = cpu_baseline(cfg, path, nprobe, budget, args.cpu_seconds)
+
+    line = {
+        "metric": "queries/sec at recall@k (BBC large-k IVF query path)",
+        "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg.name, "N": cfg.N, "d": cfg.d, "quantizer": cfg.kind,
+                   "M": cfg.M, "nlist": cfg.nlist, "nq_per_gpu": nq, "k": k, "nprobe": nprobe,
+                   "budget": budget, "parallelism": f"query-sharded x{world}",
+                   "l2": "flushed (256 MB write) between timed steps",
+                   "probed_per_query": stats["probed"] / nq,
+                   "candidates_per_query": stats["candidates"] / nq,
+                   "microbatches": stats["microbatches"],
+                   **({} if rec is None else rec)},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": nq * cfg.d * 4,
+                "d2h_bytes_per_step": nq * k * 12},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def sweep(cfg, path, g, rank):
+    import torch
+    X = database_in_id_order(path)
+    Q = synth.generate_queries(cfg)
+    q = torch.from_numpy(Q).cuda()
+    rq = 100
+    gi, gd = groundtruth.cached_topk(f"{cfg.name}_{os.path.basename(path)}", Q[:rq], X, cfg.k,
+                                     datagen.cache_dir())
+    st = torch.cuda.current_stream()
+    for nprobe in sorted({cfg.nprobe, 2 * cfg.nprobe, 3 * cfg.nprobe, 4 * cfg.nprobe,
+                          6 * cfg.nprobe, 8 * cfg.nprobe}):
+        if nprobe > cfg.nlist or nprobe > 2048:
+            continue
+        for bm in (1.0, 1.5, 2.0, 3.0, 4.0):
+            budget = int(bm * cfg.k)
+            ws = g.workspace(len(Q), cfg.k, nprobe, budget, max_bytes=60 << 30)
+            g.search(q, cfg.k, nprobe, budget, workspace=ws)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            ids, d2 = g.search(q, cfg.k, nprobe, budget, workspace=ws)
+            b.record(st)
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(b)
+            idn = ids[:rq].cpu().numpy()
+            r = groundtruth.recall(idn, groundtruth.exact_of(Q[:rq], X, idn), gi, gd)
+            s = g.last_stats()
+            print(json.dumps({"sweep": cfg.name, "nprobe": nprobe, "budget": budget,
+                              "recall": round(r, 4), "qps": len(Q) / (ms / 1e3), "ms": ms,
+                              "probed_per_q": s["probed"] / len(Q),
+                              "cand_per_q": s["candidates"] / len(Q)}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,78 @@
+"""Ground truth and accuracy metrics of a workload (measurement side of the seeded-input layer).
+
+Used by bench.py to report recall@k of the GPU results; it is not part of the query path and
+holds none of its arithmetic.  Definitions (section 4.1):
+  * ground truth = brute-force exact top-k (fp64 squared L2, ties by id);
+  * recall@k = |R ∩ R~| / k, tie-tolerant (an id also counts when its exact distance is <= the
+    k-th ground-truth distance; reading R14);
+  * relative error = mean over ranks 1..k of Dist(R[i]) / Dist(R~[i]) - 1 (Euclidean, sorted).
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+
+
+def _sqdist(Q: np.ndarray, X: np.ndarray, chunk: int = 1 << 17) -> np.ndarray:
+    Q64 = np.asarray(Q, dtype=np.float64)
+    qn = (Q64 * Q64).sum(1)
+    out = np.empty((len(Q), len(X)), dtype=np.float64)
+    for lo in range(0, len(X), chunk):
+        xb = np.asarray(X[lo:lo + chunk], dtype=np.float64)
+        out[:, lo:lo + len(xb)] = np.maximum(0.0, qn[:, None] + (xb * xb).sum(1)[None] - 2.0 * (Q64 @ xb.T))
+    return out
+
+
+def topk(Q: np.ndarray, X: np.ndarray, k: int, block: int = 16):
+    """(ids int64 [nq x k], d2 fp64 [nq x k]) exact, ordered by (d2, id)."""
+    nq = len(Q)
+    gi = np.empty((nq, k), dtype=np.int64)
+    gd = np.empty((nq, k), dtype=np.float64)
+    for lo in range(0, nq, block):
+        D = _sqdist(Q[lo:lo + block], X)
+        for r in range(len(D)):
+            d = D[r]
+            cand = np.argpartition(d, k - 1)[:k] if k < len(d) else np.arange(len(d))
+            kth = d[cand].max()
+            cand = np.flatnonzero(d <= kth)
+            order = cand[np.lexsort((cand, d[cand]))][:k]
+            gi[lo + r] = order
+            gd[lo + r] = d[order]
+    return gi, gd
+
+
+def cached_topk(tag: str, Q: np.ndarray, X: np.ndarray, k: int, cache_dir: str):
+    path = os.path.join(cache_dir, f"gt_{tag}_{len(Q)}_{k}.npz")
+    if os.path.exists(path):
+        z = np.load(path)
+        return z["ids"], z["d2"]
+    gi, gd = topk(Q, X, k)
+    np.savez(path, ids=gi, d2=gd)
+    return gi, gd
+
+
+def exact_of(Q: np.ndarray, X: np.ndarray, ids: np.ndarray) -> np.ndarray:
+    """fp64 exact d^2 of the returned ids (inf for padding ids < 0)."""
+    out = np.full(ids.shape, np.inf)
+    for i in range(len(Q)):
+        ok = ids[i] >= 0
+        rows = np.asarray(X[ids[i][ok]], dtype=np.float64)
+        out[i][ok] = ((rows - Q[i].astype(np.float64)) ** 2).sum(1)
+    return out
+
+
+def recall(ids: np.ndarray, d2_exact: np.ndarray, gt_ids: np.ndarray, gt_d2: np.ndarray) -> float:
+    nq, k = gt_ids.shape
+    hit = 0
+    for i in range(nq):
+        ok = ids[i] >= 0
+        hit += int(np.count_nonzero(ok & (np.isin(ids[i], gt_ids[i]) | (d2_exact[i] <= gt_d2[i, -1]))))
+    return hit / (nq * k)
+
+
+def relative_error(d2: np.ndarray, gt_d2: np.ndarray) -> float:
+    r = np.sqrt(np.sort(np.asarray(d2, dtype=np.float64), axis=1))
+    g = np.sqrt(np.sort(np.asarray(gt_d2, dtype=np.float64), axis=1))
+    m = (g > 0) & np.isfinite(r)
+    return float(np.mean(r[m] / g[m] - 1.0))

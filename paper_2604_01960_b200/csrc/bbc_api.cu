@@ -130,7 +130,8 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k) {
   p.cap = cap;
   size_t table = ix->kind == BBC_KIND_PQ ? (size_t)ix->M * 256 * 4 : (size_t)ix->D * 4;
   p.per_query = (size_t)ix->nlist * 4 + (size_t)nprobe * 12 + 4 + 4 + 8 + kCells * 4 + 4 + 4 +
-                table + (size_t)cap * 9 + (size_t)ix->d * 4 + (size_t)k * 12 + 64;
+                table + (size_t)cap * 9 + (size_t)ix->d * 4 + (size_t)k * 12 + 64 +
+                (size_t)((cap + kChunk - 1) / kChunk) * 4;
   p.fixed = 32 * 256;
   return p;
 }
@@ -158,6 +159,7 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, 
   b.cells = (uint8_t*)take((size_t)nqb * p.cap);
   b.cpos = (int*)take((size_t)nqb * p.cap * 4);
   b.val = (float*)take((size_t)nqb * p.cap * 4);
+  b.chunk = (int*)take((size_t)nqb * ((p.cap + kChunk - 1) / kChunk) * 4);
   *qstage = (float*)take((size_t)nqb * ix->d * 4);
   *ostage_ids = (long long*)take((size_t)nqb * k * 8);
   *ostage_d2 = (float*)take((size_t)nqb * k * 4);
@@ -270,8 +272,12 @@ bbc_status run_search(bbc_index ix, const float* queries, int64_t nq, int32_t k,
       }
       g_launches += 1;
     }
-    const int Gs = 1, Gf = 8;
-    const int sample_grid = std::min(nprobe, 16);
+    // lists per CTA: the query's LUT is staged once per CTA, so few CTAs per query; enough
+    // CTAs overall for >= 4 waves.
+    const int Gs = 1;
+    const int sample_grid = std::min(nprobe, 4);
+    const int cta_per_q = std::max(1, std::min(nprobe, (3 * 148 * 6 + nb - 1) / nb));
+    const int Gf = (nprobe + cta_per_q - 1) / cta_per_q;
     {
       StageScope sc(ix, st, BBC_STAGE_SAMPLE);
       if (ix->kind == BBC_KIND_PQ) {
@@ -298,8 +304,13 @@ bbc_status run_search(bbc_index ix, const float* queries, int64_t nq, int32_t k,
     }
     {
       StageScope sc(ix, st, BBC_STAGE_COMPACT);
-      k_compact<<<nb, kCompNT, 0, st>>>(b, dv);
-      g_launches += 1;
+      const int nchunk = (int)((p.cap + kChunk - 1) / kChunk);
+      const int gx = std::max(1, std::min(nchunk, (4 * 148 * 8 + nb - 1) / nb));
+      k_tau<<<nb, 32, 0, st>>>(b);
+      k_count<<<dim3(gx, nb), kCmpNT, 0, st>>>(b, b.chunk, nchunk);
+      k_chunk_offsets<<<nb, 256, 0, st>>>(b, b.chunk, nchunk);
+      k_emit<<<dim3(gx, nb), kCmpNT, 0, st>>>(b, dv, b.chunk, nchunk);
+      g_launches += 4;
     }
     {
       StageScope sc(ix, st, BBC_STAGE_RERANK);

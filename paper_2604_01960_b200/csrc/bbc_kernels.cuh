@@ -32,6 +32,7 @@ struct Batch {
   int* cpos;          // [nq x cap]  candidate rows, then (after re-rank) original ids
   float* val;         // [nq x cap]  sample estimates, then exact d^2 of candidates
   long long* stats;   // [2] sum n_o, sum |S*|
+  int* chunk;         // [nq x nchunk]  per-chunk candidate counts -> offsets (compaction)
 };
 
 // Index arrays on the device.
@@ -110,7 +111,6 @@ constexpr int kMaxProbe = 2048;
 __global__ void __launch_bounds__(kSelNT) k_probe_select(Batch b, Dev ix) {
   __shared__ SelectSmem sm;
   __shared__ uint64_t keys[kMaxProbe];
-  __shared__ int wcnt[kSelNT / 32 + 1];
   __shared__ int s_count;
   const int q = blockIdx.x;
   const int nlist = ix.nlist, nprobe = b.nprobe;
@@ -486,73 +486,164 @@ __global__ void __launch_bounds__(kSelNT) k_select_edges(Batch b, Dev ix) {
 }
 
 // ------------------------------------------------------------------------------------------
-// a5+a6  threshold bucket and superset compaction (deterministic: probe order)
+// a5  Update: tau = first cell whose cumulative count reaches the budget (Alg. 1 l.5-11).
+//     One warp per query, 8 cells per lane, inclusive scan.  tau = infinity when no sample.
 // ------------------------------------------------------------------------------------------
-constexpr int kCompNT = 1024;
-__global__ void __launch_bounds__(kCompNT) k_compact(Batch b, Dev ix) {
-  __shared__ int s_poff[kMaxProbe + 1];
-  __shared__ int wcnt[kCompNT / 32 + 1];
-  __shared__ int s_tau;
-  const int q = blockIdx.x;
-  const int nprobe = b.nprobe;
-  const int* po = b.poff + (size_t)q * (nprobe + 1);
-  for (int j = threadIdx.x; j <= nprobe; j += kCompNT) s_poff[j] = po[j];
-  const int ns = b.nsamp[q];
-  if (threadIdx.x < 32) {
-    int tau = kTauInf;
-    if (ns > 0) {
-      // Update: first cell whose cumulative count reaches the budget (8 cells per lane)
-      const int* H = b.hist + (size_t)q * kCells;
-      const int lane = threadIdx.x;
-      long long v[8], s = 0;
+__global__ void __launch_bounds__(32) k_tau(Batch b) {
+  const int q = blockIdx.x, lane = threadIdx.x;
+  int tau = kTauInf;
+  if (b.nsamp[q] > 0) {
+    const int* H = b.hist + (size_t)q * kCells;
+    long long v[8], s = 0;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) { v[j] = H[lane * 8 + j]; s += v[j]; }
-      long long incl = s;
+    for (int j = 0; j < 8; ++j) { v[j] = H[lane * 8 + j]; s += v[j]; }
+    long long incl = s;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        long long t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      long long c = incl - s;
-      int found = 1 << 30;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        c += v[j];
-        if (c >= b.budget && found == (1 << 30)) found = lane * 8 + j;
-      }
-      found = warp_min(found);
-      tau = found;            // < 255 guaranteed by the sample rule (DESIGN R5)
+    for (int o = 1; o < 32; o <<= 1) {
+      long long t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
     }
-    if (threadIdx.x == 0) s_tau = tau;
+    long long c = incl - s;
+    int found = kTauInf;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      c += v[j];
+      if (c >= b.budget && found == kTauInf) found = lane * 8 + j;
+    }
+    tau = warp_min(found);    // <= 254 by the sample rule (DESIGN R5)
   }
-  __syncthreads();
-  const int tau = s_tau;
-  const int n = s_poff[nprobe];
-  const uint8_t* cl = b.cells + (size_t)q * b.cap;
-  int* out = b.cpos + (size_t)q * b.cap;
-  const int* pr = b.probe + (size_t)q * nprobe;
-  int base = 0;
-  for (int t0 = 0; t0 < n; t0 += kCompNT) {
-    const int i = t0 + threadIdx.x;
-    bool f = false;
-    if (i < n) f = (tau == kTauInf) || ((int)cl[i] <= tau);
-    int total;
-    int r = block_rank<kCompNT>(f, wcnt, &total);
-    if (f) {
-      int lo = 0, hi = nprobe - 1;                // last j with s_poff[j] <= i
-      while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (s_poff[mid] <= i) lo = mid; else hi = mid - 1;
-      }
-      out[base + r] = (int)(ix.loff[pr[lo]] + (i - s_poff[lo]));
+  if (lane == 0) b.tau[q] = tau;
+}
+
+// ------------------------------------------------------------------------------------------
+// a6  Collect l.19-21: superset S* = {cell <= tau}, compacted in probe order (deterministic).
+//     Chunks of kChunk objects per CTA, 16 per thread (one 16-byte load of cell ids):
+//     k_count -> per-chunk counts, k_chunk_offsets -> per-query exclusive scan, k_emit -> rows.
+// ------------------------------------------------------------------------------------------
+constexpr int kCmpNT = 256, kPerThr = 16, kChunk = kCmpNT * kPerThr;
+
+__device__ __forceinline__ unsigned chunk_flags(const Batch& b, int q, int i0, int n, int tau) {
+  // bit e set <=> element i0 + e (e < 16) is a candidate
+  unsigned f = 0;
+  if (i0 >= n) return 0;
+  const int m = min(kPerThr, n - i0);
+  if (tau == kTauInf) return m == 32 ? 0xffffffffu : ((1u << m) - 1u);
+  const uint8_t* cl = b.cells + (size_t)q * b.cap + i0;
+  uint32_t w[4];
+  if (m == kPerThr) {
+    uint4 x = *reinterpret_cast<const uint4*>(cl);
+    w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
+  } else {
+    for (int e = 0; e < 4; ++e) w[e] = 0xffffffffu;
+    for (int e = 0; e < m; ++e) reinterpret_cast<uint8_t*>(w)[e] = cl[e];
+  }
+#pragma unroll
+  for (int e = 0; e < kPerThr; ++e)
+    if ((int)((w[e >> 2] >> (8 * (e & 3))) & 255u) <= tau) f |= 1u << e;
+  return f;
+}
+
+__global__ void __launch_bounds__(kCmpNT) k_count(Batch b, int* chunk_cnt, int nchunk) {
+  __shared__ int red[kCmpNT / 32];
+  const int q = blockIdx.y;
+  const int n = b.poff[(size_t)q * (b.nprobe + 1) + b.nprobe];
+  const int tau = b.tau[q];
+  const int need = (n + kChunk - 1) / kChunk;
+  for (int c = blockIdx.x; c < need; c += gridDim.x) {
+    const int i0 = c * kChunk + threadIdx.x * kPerThr;
+    int cnt = __popc(chunk_flags(b, q, i0, n, tau));
+    cnt = warp_sum(cnt);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int w = 0; w < kCmpNT / 32; ++w) t += red[w];
+      chunk_cnt[(size_t)q * nchunk + c] = t;
     }
-    base += total;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_chunk_offsets(Batch b, int* chunk_cnt, int nchunk) {
+  __shared__ int wsum[8];
+  const int q = blockIdx.x;
+  int* cc = chunk_cnt + (size_t)q * nchunk;
+  const int need = (b.poff[(size_t)q * (b.nprobe + 1) + b.nprobe] + kChunk - 1) / kChunk;
+  int run = 0;
+  for (int base = 0; base < need; base += 256) {
+    const int c = base + threadIdx.x;
+    const int v = c < need ? cc[c] : 0;
+    int incl = v;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    int pre = 0, tot = 0;
+    for (int w = 0; w < 8; ++w) { if (w < wid) pre += wsum[w]; tot += wsum[w]; }
+    if (c < need) cc[c] = run + pre + incl - v;
+    run += tot;
+    __syncthreads();
   }
   if (threadIdx.x == 0) {
-    b.ncand[q] = base;
-    b.tau[q] = tau;
+    const int n = b.poff[(size_t)q * (b.nprobe + 1) + b.nprobe];
+    b.ncand[q] = run;
     atomicAdd((unsigned long long*)&b.stats[0], (unsigned long long)n);
-    atomicAdd((unsigned long long*)&b.stats[1], (unsigned long long)base);
+    atomicAdd((unsigned long long*)&b.stats[1], (unsigned long long)run);
+  }
+}
+
+__global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chunk_off, int nchunk) {
+  __shared__ int wcnt[kCmpNT / 32 + 1];
+  const int q = blockIdx.y;
+  const int nprobe = b.nprobe;
+  const int* po = b.poff + (size_t)q * (nprobe + 1);
+  const int n = po[nprobe];
+  const int tau = b.tau[q];
+  const int need = (n + kChunk - 1) / kChunk;
+  for (int c = blockIdx.x; c < need; c += gridDim.x) {
+  const int i0 = c * kChunk + threadIdx.x * kPerThr;
+  const unsigned f = chunk_flags(b, q, i0, n, tau);
+  // exclusive prefix of per-thread counts across the block
+  const int mine = __popc(f);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) wcnt[wid] = incl;
+  __syncthreads();
+  int pre = 0;
+  for (int w = 0; w < wid; ++w) pre += wcnt[w];
+  int pos = chunk_off[(size_t)q * nchunk + c] + pre + incl - mine;
+  __syncthreads();
+  if (!f) continue;
+  // list of the first candidate: last j with po[j] <= i (binary search), then walk forward
+  const int* pr = b.probe + (size_t)q * nprobe;
+  int* out = b.cpos + (size_t)q * b.cap;
+  int ifirst = i0 + __ffs(f) - 1;
+  int lo = 0, hi = nprobe - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (po[mid] <= ifirst) lo = mid; else hi = mid - 1;
+  }
+  int j = lo;
+  int jend = po[j + 1];
+  long long rbase = ix.loff[pr[j]] - po[j];
+  for (unsigned r = f; r; r &= r - 1) {
+    const int i = i0 + __ffs(r) - 1;
+    while (i >= jend) {            // next non-empty list containing i
+      ++j;
+      jend = po[j + 1];
+      rbase = ix.loff[pr[j]] - po[j];
+    }
+    out[pos++] = (int)(rbase + i);
+  }
   }
 }
 
