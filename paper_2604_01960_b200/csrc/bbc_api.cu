@@ -52,6 +52,8 @@ struct bbc_index_s {
   float* factors = nullptr;
   void* raw = nullptr;
   long long* stats = nullptr;           // [4]
+  uint8_t* codes_t = nullptr;           // PQ codes, per-list chunk-major (replicated-LUT scan)
+  long long* tbase = nullptr;           // [nlist] byte offset of each list in codes_t
   bool broken = false;
   bool timing = false;
   std::vector<Timer> timers;
@@ -59,6 +61,7 @@ struct bbc_index_s {
   double stage_ms[BBC_NUM_STAGES] = {0};
   long long timed_calls = 0;
   long long microbatches = 0;
+  int num_sms = 148;
 };
 
 namespace {
@@ -131,7 +134,7 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k) {
   size_t table = ix->kind == BBC_KIND_PQ ? (size_t)ix->M * 256 * 4 : (size_t)ix->D * 4;
   p.per_query = (size_t)ix->nlist * 4 + (size_t)nprobe * 12 + 4 + 4 + 8 + kCells * 4 + 4 + 4 +
                 table + (size_t)cap * 9 + (size_t)ix->d * 4 + (size_t)k * 12 + 64 +
-                (size_t)((cap + kChunk - 1) / kChunk) * 4;
+                (size_t)((cap + kChunk - 1) / kChunk) * 4 + (size_t)(nprobe + 1) * 4;
   p.fixed = 32 * 256;
   return p;
 }
@@ -150,6 +153,7 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, 
   b.probe = (int*)take((size_t)nqb * nprobe * 4);
   b.rq2 = (float*)take((size_t)nqb * nprobe * 4);
   b.poff = (int*)take((size_t)nqb * (nprobe + 1) * 4);
+  b.popad = (int*)take((size_t)nqb * (nprobe + 1) * 4);
   b.nsamp = (int*)take((size_t)nqb * 4);
   b.edges = (float*)take((size_t)nqb * 8);
   b.hist = (int*)take((size_t)nqb * kCells * 4);
@@ -182,27 +186,26 @@ __global__ void k_debug_cands(const int* cpos, const float* val, const int* ncan
 }
 
 template <int M>
-void launch_pq_scan(bool sample, dim3 grid, size_t smem, cudaStream_t st, const Batch& b,
-                    const Dev& dv, int G) {
-  if (sample) {
-    set_smem(k_pq_scan<M, true>, smem);
-    k_pq_scan<M, true><<<grid, kScanNT, smem, st>>>(b, dv, G);
+void launch_rq(bool est, dim3 grid, cudaStream_t st, const Batch& b, const Dev& dv,
+               const uint8_t* ct, const long long* tb, float* out, long long stride, int mode) {
+  if (est) {
+    set_smem(k_pq_scan_rq<M, true>, kRqSmem);
+    k_pq_scan_rq<M, true><<<grid, kRqNT, kRqSmem, st>>>(b, dv, ct, tb, out, stride, mode);
   } else {
-    set_smem(k_pq_scan<M, false>, smem);
-    k_pq_scan<M, false><<<grid, kScanNT, smem, st>>>(b, dv, G);
+    set_smem(k_pq_scan_rq<M, false>, kRqSmem);
+    k_pq_scan_rq<M, false><<<grid, kRqNT, kRqSmem, st>>>(b, dv, ct, tb, out, stride, mode);
   }
 }
 
-bool pq_scan(int M, bool sample, dim3 grid, cudaStream_t st, const Batch& b, const Dev& dv, int G) {
-  size_t smem = (size_t)M * 256 * 4;
+void rq_scan(int M, bool est, dim3 grid, cudaStream_t st, const Batch& b, const Dev& dv,
+             const uint8_t* ct, const long long* tb, float* out, long long stride, int mode) {
   switch (M) {
-    case 8: launch_pq_scan<8>(sample, grid, smem, st, b, dv, G); return true;
-    case 16: launch_pq_scan<16>(sample, grid, smem, st, b, dv, G); return true;
-    case 24: launch_pq_scan<24>(sample, grid, smem, st, b, dv, G); return true;
-    case 32: launch_pq_scan<32>(sample, grid, smem, st, b, dv, G); return true;
-    case 48: launch_pq_scan<48>(sample, grid, smem, st, b, dv, G); return true;
-    case 64: launch_pq_scan<64>(sample, grid, smem, st, b, dv, G); return true;
-    default: return false;
+    case 8: launch_rq<8>(est, grid, st, b, dv, ct, tb, out, stride, mode); break;
+    case 16: launch_rq<16>(est, grid, st, b, dv, ct, tb, out, stride, mode); break;
+    case 24: launch_rq<24>(est, grid, st, b, dv, ct, tb, out, stride, mode); break;
+    case 32: launch_rq<32>(est, grid, st, b, dv, ct, tb, out, stride, mode); break;
+    case 48: launch_rq<48>(est, grid, st, b, dv, ct, tb, out, stride, mode); break;
+    case 64: launch_rq<64>(est, grid, st, b, dv, ct, tb, out, stride, mode); break;
   }
 }
 
@@ -278,29 +281,37 @@ bbc_status run_search(bbc_index ix, const float* queries, int64_t nq, int32_t k,
     const int sample_grid = std::min(nprobe, 4);
     const int cta_per_q = std::max(1, std::min(nprobe, (3 * 148 * 6 + nb - 1) / nb));
     const int Gf = (nprobe + cta_per_q - 1) / cta_per_q;
-    {
-      StageScope sc(ix, st, BBC_STAGE_SAMPLE);
-      if (ix->kind == BBC_KIND_PQ) {
-        pq_scan(ix->M, true, dim3(sample_grid, nb), st, b, dv, Gs);
-      } else {
+    if (ix->kind == BBC_KIND_PQ) {
+      const int gx = (int)((p.cap + 32LL * nprobe + kRqE - 1) / kRqE);
+      {
+        StageScope sc(ix, st, BBC_STAGE_SAMPLE);
+        rq_scan(ix->M, true, dim3(gx, nb), st, b, dv, ix->codes_t, ix->tbase, b.val, p.cap, 0);
+        k_select_edges<<<nb, kSelNT, 0, st>>>(b, dv);
+        k_sample_cells<<<dim3(8, nb), 256, 0, st>>>(b);
+        g_launches += 3;
+      }
+      {
+        StageScope sc(ix, st, BBC_STAGE_SCAN);
+        rq_scan(ix->M, false, dim3(gx, nb), st, b, dv, ix->codes_t, ix->tbase, nullptr, 0, 1);
+        g_launches += 1;
+      }
+    } else {
+      {
+        StageScope sc(ix, st, BBC_STAGE_SAMPLE);
         size_t sm = (size_t)ix->D * 4 + 4 * (ix->D / 32) * 4;
         set_smem(k_rbq_scan<true>, sm);
         k_rbq_scan<true><<<dim3(sample_grid, nb), kScanNT, sm, st>>>(b, dv, Gs);
+        k_select_edges<<<nb, kSelNT, 0, st>>>(b, dv);
+        g_launches += 2;
       }
-      k_select_edges<<<nb, kSelNT, 0, st>>>(b, dv);
-      g_launches += 2;
-    }
-    {
-      StageScope sc(ix, st, BBC_STAGE_SCAN);
-      dim3 g((nprobe + Gf - 1) / Gf, nb);
-      if (ix->kind == BBC_KIND_PQ) {
-        pq_scan(ix->M, false, g, st, b, dv, Gf);
-      } else {
+      {
+        StageScope sc(ix, st, BBC_STAGE_SCAN);
+        dim3 g((nprobe + Gf - 1) / Gf, nb);
         size_t sm = (size_t)ix->D * 4 + 4 * (ix->D / 32) * 4;
         set_smem(k_rbq_scan<false>, sm);
         k_rbq_scan<false><<<g, kScanNT, sm, st>>>(b, dv, Gf);
+        g_launches += 1;
       }
-      g_launches += 1;
     }
     {
       StageScope sc(ix, st, BBC_STAGE_COMPACT);
@@ -346,22 +357,22 @@ bbc_status run_search(bbc_index ix, const float* queries, int64_t nq, int32_t k,
         g_launches += 1;
       }
       if (dbg->est) {
-        // all estimates in probe order: rerun the estimate pass over every probed list into
-        // the caller's buffer (debug only)
-        Batch b2 = b;
-        b2.val = dbg->est;
-        b2.cap = dbg->est_stride;
-        std::vector<int> ones(nb, nprobe);
-        // temporarily mark every list as "sample" so the sample kernel covers all of them
-        int* ns_all = b.tau;  // reuse: tau already copied out above
-        CU(cudaMemcpyAsync(ns_all, ones.data(), (size_t)nb * 4, cudaMemcpyHostToDevice, st));
-        CU(cudaStreamSynchronize(st));
-        b2.nsamp = ns_all;
+        // every estimate in probe order, written to the caller's buffer (debug only)
         if (ix->kind == BBC_KIND_PQ) {
-          pq_scan(ix->M, true, dim3(std::min(nprobe, 64), nb), st, b2, dv, Gs);
+          const int gx = (int)((p.cap + 32LL * nprobe + kRqE - 1) / kRqE);
+          rq_scan(ix->M, true, dim3(gx, nb), st, b, dv, ix->codes_t, ix->tbase, dbg->est,
+                  dbg->est_stride, 2);
         } else {
+          Batch b2 = b;
+          b2.val = dbg->est;
+          b2.cap = dbg->est_stride;
+          std::vector<int> all(nb, nprobe);
+          int* ns_all = b.tau;  // scratch: tau was copied out above
+          CU(cudaMemcpyAsync(ns_all, all.data(), (size_t)nb * 4, cudaMemcpyHostToDevice, st));
+          CU(cudaStreamSynchronize(st));
+          b2.nsamp = ns_all;
           size_t sm = (size_t)ix->D * 4 + 4 * (ix->D / 32) * 4;
-          k_rbq_scan<true><<<dim3(std::min(nprobe, 64), nb), kScanNT, sm, st>>>(b2, dv, Gs);
+          k_rbq_scan<true><<<dim3(std::min(nprobe, 64), nb), kScanNT, sm, st>>>(b2, dv, 1);
         }
         g_launches += 1;
         CU(cudaGetLastError());
@@ -537,6 +548,25 @@ bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_
   }
   ok = ok && upload_rows(9, rowraw, &ix->raw);
   ok = ok && dalloc((void**)&ix->stats, 4 * sizeof(long long));
+  cudaDeviceGetAttribute(&ix->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
+  if (ok && kind == BBC_KIND_PQ) {
+    // chunk-major copy of the codes for the replicated-LUT scan (layout: k_transpose_codes)
+    std::vector<long long> tb(nlist, 0);
+    long long tot = 0;
+    for (int L = 0; L < nlist; ++L) {
+      tb[L] = tot;
+      tot += (long long)((ix->lsize[L] + 31) / 32) * M * 32;
+    }
+    ok = dalloc((void**)&ix->codes_t, (size_t)tot + kCodesTailPad) &&
+         dalloc((void**)&ix->tbase, (size_t)nlist * 8) &&
+         cudaMemcpy(ix->tbase, tb.data(), (size_t)nlist * 8, cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemset(ix->codes_t, 0, (size_t)tot + kCodesTailPad) == cudaSuccess;
+    if (ok && ix->n_local > 0) {
+      k_transpose_codes<<<(unsigned)((ix->n_local + 255) / 256), 256>>>(
+          ix->codes, ix->loff, ix->tbase, nlist, ix->n_local, M, ix->codes_t);
+      ok = cudaDeviceSynchronize() == cudaSuccess;
+    }
+  }
   if (!ok) {
     cudaError_t e = cudaGetLastError();
     return fail_load(e == cudaErrorMemoryAllocation ? BBC_ERR_OOM : BBC_ERR_IO,
@@ -551,7 +581,7 @@ void ivf_free(bbc_index ix) {
   if (!ix) return;
   cudaSetDevice(ix->device);
   void* ptrs[] = {ix->centroids, ix->loff, ix->gsize_d, ix->ids, ix->books, ix->codes, ix->P,
-                  ix->wL, ix->bits, ix->factors, ix->raw, ix->stats};
+                  ix->wL, ix->bits, ix->factors, ix->raw, ix->stats, ix->codes_t, ix->tbase};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& t : ix->timers) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }

@@ -22,6 +22,7 @@ struct Batch {
   int* probe;         // [nq x nprobe]
   float* rq2;         // [nq x nprobe]
   int* poff;          // [nq x (nprobe+1)]   element offset of each probed list (local)
+  int* popad;         // [nq x (nprobe+1)]   same with every list rounded up to 32 objects
   int* nsamp;         // [nq]                sample lists s (0 = tau infinity)
   float* edges;       // [nq x 2]            (d_min, d_max)
   int* hist;          // [nq x 256]
@@ -147,7 +148,8 @@ __global__ void __launch_bounds__(kSelNT) k_probe_select(Batch b, Dev ix) {
   int* pr = b.probe + (size_t)q * nprobe;
   float* rq = b.rq2 + (size_t)q * nprobe;
   int* po = b.poff + (size_t)q * (nprobe + 1);
-  long long lrun = 0, grun = 0;
+  int* pp = b.popad + (size_t)q * (nprobe + 1);
+  long long lrun = 0, grun = 0, prun = 0;
   int s = -1;
   for (int base = 0; base < nprobe; base += kSelNT) {
     const int j = base + threadIdx.x;
@@ -162,33 +164,39 @@ __global__ void __launch_bounds__(kSelNT) k_probe_select(Batch b, Dev ix) {
     }
     // inclusive scans of lsz and gsz across the block (two ranks via block_rank is not enough:
     // use warp scans + smem)
-    __shared__ long long wl[kSelNT / 32], wg[kSelNT / 32];
+    __shared__ long long wl[kSelNT / 32], wg[kSelNT / 32], wpd[kSelNT / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    long long il = lsz, ig = gsz;
+    long long il = lsz, ig = gsz, ipd = (lsz + 31) & ~31;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       long long tl = __shfl_up_sync(0xffffffffu, il, o);
       long long tg = __shfl_up_sync(0xffffffffu, ig, o);
-      if (lane >= o) { il += tl; ig += tg; }
+      long long tp = __shfl_up_sync(0xffffffffu, ipd, o);
+      if (lane >= o) { il += tl; ig += tg; ipd += tp; }
     }
-    if (lane == 31) { wl[wid] = il; wg[wid] = ig; }
+    if (lane == 31) { wl[wid] = il; wg[wid] = ig; wpd[wid] = ipd; }
     __syncthreads();
     if (wid == 0) {
-      long long vl = wl[lane], vg = wg[lane];
-      long long sl = vl, sg = vg;
+      long long vl = wl[lane], vg = wg[lane], vp = wpd[lane];
+      long long sl = vl, sg = vg, sp = vp;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         long long tl = __shfl_up_sync(0xffffffffu, sl, o);
         long long tg = __shfl_up_sync(0xffffffffu, sg, o);
-        if (lane >= o) { sl += tl; sg += tg; }
+        long long tp = __shfl_up_sync(0xffffffffu, sp, o);
+        if (lane >= o) { sl += tl; sg += tg; sp += tp; }
       }
       wl[lane] = sl - vl;
       wg[lane] = sg - vg;
+      wpd[lane] = sp - vp;
     }
     __syncthreads();
     const long long excl_l = lrun + wl[wid] + il - lsz;
     const long long incl_g = grun + wg[wid] + ig;
-    if (j < nprobe) po[j] = (int)excl_l;
+    if (j < nprobe) {
+      po[j] = (int)excl_l;
+      pp[j] = (int)(prun + wpd[wid] + ipd - ((lsz + 31) & ~31));
+    }
     // sample rule: first j with cumulative global size >= budget
     int cand = (j < nprobe && incl_g >= b.budget && incl_g - gsz < b.budget) ? j : -1;
     __shared__ int s_first;
@@ -198,15 +206,17 @@ __global__ void __launch_bounds__(kSelNT) k_probe_select(Batch b, Dev ix) {
     __syncthreads();
     if (s < 0 && s_first >= 0) s = s_first;
     // block totals
-    __shared__ long long tot_l, tot_g;
-    if (threadIdx.x == kSelNT - 1) { tot_l = wl[wid] + il; tot_g = wg[wid] + ig; }
+    __shared__ long long tot_l, tot_g, tot_p;
+    if (threadIdx.x == kSelNT - 1) { tot_l = wl[wid] + il; tot_g = wg[wid] + ig; tot_p = wpd[wid] + ipd; }
     __syncthreads();
     lrun += tot_l;
     grun += tot_g;
+    prun += tot_p;
     __syncthreads();
   }
   if (threadIdx.x == 0) {
     po[nprobe] = (int)lrun;
+    pp[nprobe] = (int)prun;
     int ns;
     if (grun <= b.budget) ns = 0;
     else {
@@ -268,76 +278,229 @@ struct CellFn {
   }
 };
 
+constexpr int kScanNT = 256;   // RaBitQ scan CTA size
+
 // ------------------------------------------------------------------------------------------
-// a3/a4  PQ code scan.  CTA = (group of G probed lists, query).  The query's LUT lives in shared
-// memory; each thread estimates whole objects: est = LUT[0][c0] + ... + LUT[M-1][c_{M-1}].
-//   SAMPLE: lists j < nsamp[q] -> est written to val (the sample)
-//   FULL:   every probed list  -> bucket id to cells, histogram of ids < 255 (Push, Alg. 1 l.1-4)
+// a3/a4  PQ code scan with a replicated LUT (query-major, conflict-free).
+//
+// CTA = (query q, pass P): objects [P*kRqE, (P+1)*kRqE) of q's probed objects in probe order,
+// where every probed list starts on a multiple of 32 (padded order, popad).  Warp w owns 64
+// groups of 32 consecutive objects; a group never straddles two lists, so lane l of the warp
+// handles object i0 + l of one list.  Each lane keeps the 64 running estimates of its objects in
+// registers; the M sub-quantizers are visited in chunks of 4 (canonical order m = 0..M-1).
+//
+// The chunk's 4 x 256 LUT entries are replicated 32 times in shared memory so that lane l
+// always reads bank l, whatever the code: no bank conflicts (a single LUT copy costs ~3.5
+// wavefronts per lookup with random codes).  The replica layout [mm>>1][c][mm&1][lane] makes
+// the byte address of entry (mm, c) for lane l equal (c << 8) | 4l plus an immediate, so one
+// byte permute of the code word gives the address: PRMT + LDS + FADD per lookup.
+// Codes are read from a group-major copy (codes_t): a group's 32 code words of one chunk are
+// 128 consecutive bytes.
+//   EST : estimate written to out_est[q * est_stride + probe-order position] (sample/debug)
+//   !EST: bucket id to cells, histogram of ids < 255 (Push, Alg. 1 l.1-4)
 // ------------------------------------------------------------------------------------------
-constexpr int kScanNT = 256;
-template <int M, bool SAMPLE>
-__global__ void __launch_bounds__(kScanNT) k_pq_scan(Batch b, Dev ix, int G) {
-  extern __shared__ float lut[];            // [M x 256]
-  __shared__ int hist[kCells];
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+
+constexpr int kRqWarps = 16, kRqNT = kRqWarps * 32, kRqEW = 64;
+constexpr int kRqE = kRqNT * kRqEW;                      // objects per CTA (32768)
+constexpr int kRqMC = 4;                                 // sub-quantizers per chunk
+constexpr int kRqBatch = 8;                              // code loads in flight per lane
+constexpr int kRqGroups = kRqWarps * kRqEW;              // 32-object groups per CTA
+constexpr int kRqLutBytes = kRqMC * 256 * 32 * 4;        // 131072
+// dynamic shared memory: [LUT chunk][group code pointers][group output offsets][group counts]
+//                        [histogram][padded probe offsets]
+constexpr int kRqOffPtr = kRqLutBytes;
+constexpr int kRqOffOut = kRqOffPtr + kRqGroups * 8;
+constexpr int kRqOffCnt = kRqOffOut + kRqGroups * 8;
+constexpr int kRqOffHist = kRqOffCnt + kRqGroups * 4;
+constexpr int kRqOffPo = kRqOffHist + kCells * 4;
+constexpr size_t kRqSmem = kRqOffPo + (kMaxProbe + 1) * 4;
+// The kernel has no static shared memory, so its dynamic buffer starts right after the 1 KB
+// the driver reserves per CTA; the LUT lookups use that offset as an immediate (checked).
+constexpr unsigned kRqSmemBase = 1024;
+
+// Codes in group-major order for this scan: list L is cut into groups of 32 objects; group g,
+// chunk p (sub-quantizers 4p..4p+3), object lane l at byte tbase[L] + (g*(M/4) + p)*128 + 4l.
+__device__ __forceinline__ long long rq_list_bytes(int n, int M) { return (long long)((n + 31) >> 5) * M * 32; }
+constexpr int kCodesTailPad = 128;
+
+template <int IMM>
+__device__ __forceinline__ float lds_imm(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(a), "n"(IMM));
+  return v;
+}
+
+// mode 0: sample lists [0, nsamp) -> estimates; 1: lists [nsamp, nprobe) -> bucket ids;
+// 2: all lists -> estimates (debug)
+template <int M, bool EST>
+__global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const uint8_t* __restrict__ codes_t,
+                                                         const long long* __restrict__ tbase,
+                                                         float* out_est, long long est_stride,
+                                                         int mode) {
+  extern __shared__ __align__(16) uint8_t rsm[];
+  float* lut = reinterpret_cast<float*>(rsm);
+  const uint8_t** gptr = reinterpret_cast<const uint8_t**>(rsm + kRqOffPtr);
+  long long* gout = reinterpret_cast<long long*>(rsm + kRqOffOut);
+  int* gcnt = reinterpret_cast<int*>(rsm + kRqOffCnt);
+  int* hist = reinterpret_cast<int*>(rsm + kRqOffHist);
+  int* s_popad = reinterpret_cast<int*>(rsm + kRqOffPo);
   const int q = blockIdx.y;
   const int ns = b.nsamp[q];
-  if (ns == 0) return;                      // tau = infinity: no buckets (Alg. 1 l.11)
-  const int jlim = SAMPLE ? ns : b.nprobe;
-  if (blockIdx.x * G >= jlim) return;
-  const float* gl = b.table + (size_t)q * M * 256;
-  for (int i = threadIdx.x; i < M * 64; i += kScanNT)
-    reinterpret_cast<float4*>(lut)[i] = reinterpret_cast<const float4*>(gl)[i];
-  CellFn cf;
-  if (!SAMPLE) {
-    for (int i = threadIdx.x; i < kCells; i += kScanNT) hist[i] = 0;
-    cf.init(b.edges[2 * q], b.edges[2 * q + 1]);
-  }
+  if (mode != 2 && ns == 0) return;                  // tau = infinity: nothing to bucket
+  const int first = mode == 1 ? ns : 0;
+  const int lim = mode == 0 ? ns : b.nprobe;
+  const int* popad = b.popad + (size_t)q * (b.nprobe + 1);
+  const int nflat = popad[lim];
+  const int x0 = popad[first] + blockIdx.x * kRqE;
+  if (x0 >= nflat) return;
+  if (smem_u32(rsm) != kRqSmemBase) __trap();        // layout assumption of lds_imm
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int j = threadIdx.x; j <= lim; j += kRqNT) s_popad[j] = popad[j];
+  if (!EST)
+    for (int i = threadIdx.x; i < kCells; i += kRqNT) hist[i] = 0;
+  const float* glut = b.table + (size_t)q * M * 256;
+  float nv0 = __ldg(glut + threadIdx.x), nv1 = __ldg(glut + threadIdx.x + kRqNT);  // chunk 0
   __syncthreads();
+  // group table: group G = 32 objects starting at flat x0 + 32 G (never straddles a list)
   const int* po = b.poff + (size_t)q * (b.nprobe + 1);
   const int* pr = b.probe + (size_t)q * b.nprobe;
-  for (int g0 = blockIdx.x * G; g0 < jlim; g0 += gridDim.x * G)
-  for (int j = g0; j < min(g0 + G, jlim); ++j) {
-    const int L = pr[j];
-    const long long row0 = ix.loff[L];
-    const int n = (int)(ix.loff[L + 1] - row0);
-    const long long e0 = (long long)q * b.cap + po[j];
-    for (int i = threadIdx.x; i < n; i += kScanNT) {
-      const uint8_t* cp = ix.codes + (size_t)(row0 + i) * M;
-      uint32_t w[M / 4];
-      if constexpr (M % 16 == 0) {
-#pragma unroll
-        for (int v = 0; v < M / 16; ++v) {
-          uint4 x = __ldg(reinterpret_cast<const uint4*>(cp) + v);
-          w[4 * v] = x.x; w[4 * v + 1] = x.y; w[4 * v + 2] = x.z; w[4 * v + 3] = x.w;
-        }
-      } else {
-#pragma unroll
-        for (int v = 0; v < M / 8; ++v) {
-          uint2 x = __ldg(reinterpret_cast<const uint2*>(cp) + v);
-          w[2 * v] = x.x; w[2 * v + 1] = x.y;
-        }
+  const long long obase = EST ? (long long)q * est_stride : (long long)q * b.cap;
+  for (int G = threadIdx.x; G < kRqGroups; G += kRqNT) {
+    const uint8_t* cp = codes_t;                      // invalid groups read (masked) garbage
+    long long oo = 0;
+    int cnt = 0;
+    const int xg = x0 + 32 * G;
+    if (xg < nflat) {
+      int lo = first, hi = lim - 1;                   // last j with popad[j] <= xg
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_popad[mid] <= xg) lo = mid; else hi = mid - 1;
       }
-      float acc = lut[w[0] & 255u];
+      const int L = pr[lo];
+      const int nL = (int)(ix.loff[L + 1] - ix.loff[L]);
+      const int i0 = xg - s_popad[lo];
+      cnt = min(32, nL - i0);
+      cp = codes_t + tbase[L] + (long long)(i0 >> 5) * M * 32;
+      oo = obase + po[lo] + i0;
+    }
+    gptr[G] = cp;
+    gout[G] = oo;
+    gcnt[G] = cnt;
+  }
+  CellFn cf;
+  if (!EST) cf.init(b.edges[2 * q], b.edges[2 * q + 1]);
+  float acc[kRqEW];
 #pragma unroll
-      for (int m = 1; m < M; ++m) {
-        const uint32_t c = (w[m >> 2] >> (8 * (m & 3))) & 255u;
-        acc = __fadd_rn(acc, lut[m * 256 + c]);
+  for (int e = 0; e < kRqEW; ++e) acc[e] = 0.f;
+  const uint8_t* const* mg = gptr + wid * kRqEW;
+  const uint32_t lane4 = (uint32_t)lane * 4u;
+#pragma unroll 1
+  for (int p = 0; p < M / kRqMC; ++p) {
+    __syncthreads();                                  // previous chunk fully consumed
+    // stage chunk p: entry (mm, c) replicated 32x at words ((mm>>1)*256 + c)*64 + (mm&1)*32 +
+    // [0, 32): lane l reads bank l.  Thread t writes entries t and t + 512 as 8 rotated
+    // 16-byte stores each (a quarter-warp covers all 32 banks).
+    {
+      const float4 a4 = make_float4(nv0, nv0, nv0, nv0), b4 = make_float4(nv1, nv1, nv1, nv1);
+      const int ea = threadIdx.x, eb = threadIdx.x + kRqNT;
+      float4* ra = reinterpret_cast<float4*>(lut + (size_t)((ea >> 9) * 256 + (ea & 255)) * 64 + ((ea >> 8) & 1) * 32);
+      float4* rb = reinterpret_cast<float4*>(lut + (size_t)((eb >> 9) * 256 + (eb & 255)) * 64 + ((eb >> 8) & 1) * 32);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        ra[(r + lane) & 7] = a4;
+        rb[(r + lane) & 7] = b4;
       }
-      if (SAMPLE) {
-        b.val[e0 + i] = acc;
+    }
+    if (p + 1 < M / kRqMC) {                          // prefetch chunk p+1's entries
+      nv0 = __ldg(glut + (p + 1) * kRqMC * 256 + threadIdx.x);
+      nv1 = __ldg(glut + (p + 1) * kRqMC * 256 + threadIdx.x + kRqNT);
+    }
+    __syncthreads();
+    const uint32_t plane = (uint32_t)p * 128u + lane4;
+#pragma unroll
+    for (int g0 = 0; g0 < kRqEW; g0 += kRqBatch) {
+      uint32_t w[kRqBatch];
+#pragma unroll
+      for (int u = 0; u < kRqBatch; ++u)             // lanes past cnt read padding: masked later
+        w[u] = __ldg(reinterpret_cast<const uint32_t*>(mg[g0 + u] + plane));
+#pragma unroll
+      for (int u = 0; u < kRqBatch; ++u) {
+        // address = (c << 8) | 4*lane from one byte permute; sub-quantizer offset is immediate
+        float a = acc[g0 + u];
+        a = __fadd_rn(a, lds_imm<kRqSmemBase + 0>(__byte_perm(w[u], lane4, 0x7604)));
+        a = __fadd_rn(a, lds_imm<kRqSmemBase + 128>(__byte_perm(w[u], lane4, 0x7614)));
+        a = __fadd_rn(a, lds_imm<kRqSmemBase + 65536>(__byte_perm(w[u], lane4, 0x7624)));
+        a = __fadd_rn(a, lds_imm<kRqSmemBase + 65536 + 128>(__byte_perm(w[u], lane4, 0x7634)));
+        acc[g0 + u] = a;
+      }
+    }
+  }
+  // epilogue
+#pragma unroll
+  for (int g = 0; g < kRqEW; ++g) {
+    const int cnt = gcnt[wid * kRqEW + g];
+    if (lane < cnt) {
+      const long long oo = gout[wid * kRqEW + g] + lane;
+      if (EST) {
+        out_est[oo] = acc[g];
       } else {
-        const int cell = cf(acc);
-        b.cells[e0 + i] = (uint8_t)cell;
+        const int cell = cf(acc[g]);
+        b.cells[oo] = (uint8_t)cell;
         if (cell < 255) atomicAdd(&hist[cell], 1);
       }
     }
   }
-  if (!SAMPLE) {
+  if (!EST) {
     __syncthreads();
-    int* gh = b.hist + (size_t)q * kCells;
-    for (int i = threadIdx.x; i < kCells; i += kScanNT)
-      if (hist[i]) atomicAdd(&gh[i], hist[i]);
+    for (int i = threadIdx.x; i < kCells; i += kRqNT)
+      if (hist[i]) atomicAdd(&b.hist[(size_t)q * kCells + i], hist[i]);
   }
+}
+
+// Index-load-time copy of the PQ codes in the group-major order of k_pq_scan_rq.
+__global__ void k_transpose_codes(const uint8_t* codes, const long long* loff,
+                                  const long long* tbase, int nlist, long long n, int M,
+                                  uint8_t* codes_t) {
+  const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int lo = 0, hi = nlist - 1;                         // last list with loff[L] <= r
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (loff[mid] <= r) lo = mid; else hi = mid - 1;
+  }
+  const int L = lo;
+  const long long x = r - loff[L];
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(codes + r * M);
+  uint8_t* dst = codes_t + tbase[L] + (x >> 5) * M * 32 + (x & 31) * 4;
+  for (int p = 0; p < M / 4; ++p) *reinterpret_cast<uint32_t*>(dst + p * 128) = src[p];
+}
+
+// Bucket ids (and histogram) of the sample objects from their stored estimates, once the edges
+// are known (the list-major main scan skips the sample pairs).
+__global__ void __launch_bounds__(256) k_sample_cells(Batch b) {
+  __shared__ int hist[kCells];
+  const int q = blockIdx.y;
+  const int ns = b.nsamp[q];
+  if (ns == 0) return;
+  const int n = b.poff[(size_t)q * (b.nprobe + 1) + ns];
+  if (blockIdx.x * 256 >= n) return;
+  for (int i = threadIdx.x; i < kCells; i += 256) hist[i] = 0;
+  CellFn cf;
+  cf.init(b.edges[2 * q], b.edges[2 * q + 1]);
+  __syncthreads();
+  const float* v = b.val + (size_t)q * b.cap;
+  uint8_t* cl = b.cells + (size_t)q * b.cap;
+  for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
+    const int c = cf(v[i]);
+    cl[i] = (uint8_t)c;
+    if (c < 255) atomicAdd(&hist[c], 1);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kCells; i += 256)
+    if (hist[i]) atomicAdd(&b.hist[(size_t)q * kCells + i], hist[i]);
 }
 
 // ------------------------------------------------------------------------------------------
