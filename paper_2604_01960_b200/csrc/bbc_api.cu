@@ -133,9 +133,9 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k) {
   p.cap = cap;
   size_t table = ix->kind == BBC_KIND_PQ ? (size_t)ix->M * 256 * 4 : (size_t)ix->D * 4;
   p.per_query = (size_t)ix->nlist * 4 + (size_t)nprobe * 12 + 4 + 4 + 8 + kCells * 4 + 4 + 4 +
-                table + (size_t)cap * 9 + (size_t)ix->d * 4 + (size_t)k * 12 + 64 +
+                table + (size_t)cap * 13 + (size_t)ix->d * 4 + (size_t)k * 12 + 64 +
                 (size_t)((cap + kChunk - 1) / kChunk) * 4 + (size_t)(nprobe + 1) * 4;
-  p.fixed = 32 * 256;
+  p.fixed = 64 * 256;
   return p;
 }
 
@@ -162,8 +162,10 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, 
   b.table = (float*)take((size_t)nqb * table * 4);
   b.cells = (uint8_t*)take((size_t)nqb * p.cap);
   b.cpos = (int*)take((size_t)nqb * p.cap * 4);
+  b.cid = (int*)take((size_t)nqb * p.cap * 4);
   b.val = (float*)take((size_t)nqb * p.cap * 4);
   b.chunk = (int*)take((size_t)nqb * ((p.cap + kChunk - 1) / kChunk) * 4);
+
   *qstage = (float*)take((size_t)nqb * ix->d * 4);
   *ostage_ids = (long long*)take((size_t)nqb * k * 8);
   *ostage_d2 = (float*)take((size_t)nqb * k * 4);
@@ -325,10 +327,21 @@ bbc_status run_search(bbc_index ix, const float* queries, int64_t nq, int32_t k,
     }
     {
       StageScope sc(ix, st, BBC_STAGE_RERANK);
-      const int gy = 16;
-      size_t sm = (size_t)ix->d * 4;
-      if (ix->raw_u8) k_rerank<true><<<dim3(gy, nb), kRrNT, sm, st>>>(b, dv);
-      else k_rerank<false><<<dim3(gy, nb), kRrNT, sm, st>>>(b, dv);
+      const int gy = std::max(1, (8 * ix->num_sms + nb - 1) / nb);
+      const int rowb = ix->raw_u8 ? ix->d : ix->d * 4;
+      // lanes per candidate and 16-byte chunks per lane by row size
+      const dim3 g(gy, nb);
+      if (rowb <= 128) {
+        if (ix->raw_u8) k_rerank<true, 8, 1, 4><<<g, kRrNT, 0, st>>>(b, dv);
+        else k_rerank<false, 8, 1, 4><<<g, kRrNT, 0, st>>>(b, dv);
+      } else if (rowb <= 512) {
+        if (ix->raw_u8) k_rerank<true, 8, 4, 2><<<g, kRrNT, 0, st>>>(b, dv);
+        else k_rerank<false, 8, 4, 2><<<g, kRrNT, 0, st>>>(b, dv);
+      } else if (rowb <= 1024) {
+        k_rerank<false, 8, 8, 1><<<g, kRrNT, 0, st>>>(b, dv);
+      } else {
+        k_rerank<false, 32, 8, 1><<<g, kRrNT, 0, st>>>(b, dv);
+      }
       g_launches += 1;
     }
     {
@@ -352,7 +365,7 @@ bbc_status run_search(bbc_index ix, const float* queries, int64_t nq, int32_t k,
         CU(cudaMemcpy2DAsync(dbg->n_probed, 4, b.poff + nprobe, (size_t)(nprobe + 1) * 4, 4, nb,
                              cudaMemcpyDeviceToDevice, st));
       if (dbg->cand_ids || dbg->cand_d2) {
-        k_debug_cands<<<dim3(64, nb), 256, 0, st>>>(b.cpos, b.val, b.ncand, p.cap, (long long*)dbg->cand_ids,
+        k_debug_cands<<<dim3(64, nb), 256, 0, st>>>(b.cid, b.val, b.ncand, p.cap, (long long*)dbg->cand_ids,
                                                     dbg->cand_d2, dbg->cand_stride);
         g_launches += 1;
       }
@@ -427,9 +440,9 @@ bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_
     fclose(f);
     return fail(BBC_ERR_FORMAT, "RaBitQ needs D a multiple of 64, D >= d");
   }
-  if (raw_u8 ? (d % 16 != 0) : (d % 4 != 0)) {
+  if (raw_u8 ? (d % 16 != 0 || d > 512) : (d % 4 != 0 || d > 1024)) {
     fclose(f);
-    return fail(BBC_ERR_FORMAT, "d must be a multiple of 4 (f32) or 16 (u8)");
+    return fail(BBC_ERR_FORMAT, "d must be a multiple of 4 and <= 1024 (f32) or of 16 and <= 512 (u8)");
   }
   const size_t rowraw = (size_t)d * (raw_u8 ? 1 : 4);
   const size_t dsub = kind == BBC_KIND_PQ ? d / M : 0;

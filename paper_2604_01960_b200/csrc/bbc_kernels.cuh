@@ -30,7 +30,8 @@ struct Batch {
   int* ncand;         // [nq]
   float* table;       // PQ LUT [nq x M x 256] | RaBitQ u [nq x D]
   uint8_t* cells;     // [nq x cap]
-  int* cpos;          // [nq x cap]  candidate rows, then (after re-rank) original ids
+  int* cpos;          // [nq x cap]  candidate rows (list-ordered index of this shard)
+  int* cid;           // [nq x cap]  candidate original ids
   float* val;         // [nq x cap]  sample estimates, then exact d^2 of candidates
   long long* stats;   // [2] sum n_o, sum |S*|
   int* chunk;         // [nq x nchunk]  per-chunk candidate counts -> offsets (compaction)
@@ -805,88 +806,94 @@ __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chu
       jend = po[j + 1];
       rbase = ix.loff[pr[j]] - po[j];
     }
-    out[pos++] = (int)(rbase + i);
+    const long long row = rbase + i;
+    b.cid[(size_t)q * b.cap + pos] = (int)ix.ids[row];
+    out[pos++] = (int)row;
   }
   }
 }
 
 // ------------------------------------------------------------------------------------------
-// a7  exact re-rank: one warp per candidate row, 16-byte loads, shuffle reduction.
-//     After it, cpos holds the candidate's original id and val its exact d^2.
+// a7  exact re-rank.  CTA = (query q, slice of its candidates).  LPC lanes cooperate on one
+// candidate row (LPC = 8 for rows <= 1 KB, else 32): each lane holds its share of the query in
+// registers and loads its share of the row with 16-byte loads; several warp-steps are unrolled
+// so that 8 x 16-byte loads per lane are in flight.  Candidate rows are fetched 32 at a time
+// with one coalesced load and broadcast by shuffle.  Writes exact d^2 to val (fp32, FMA order
+// of the lane split; tolerance 1e-5 relative to the oracle's fp64).
 // ------------------------------------------------------------------------------------------
 constexpr int kRrNT = 256;
-constexpr int kRrUnroll = 4;
-template <bool U8>
+template <bool U8, int LPC, int MAXV, int STEPS>
 __global__ void __launch_bounds__(kRrNT) k_rerank(Batch b, Dev ix) {
-  extern __shared__ float sq[];
+  constexpr int CPW = 32 / LPC;                       // candidates per warp step
   const int q = blockIdx.y;
+  const int lane = threadIdx.x & 31, sub = lane / LPC, sl = lane % LPC;
   const int d = ix.d;
-  for (int t = threadIdx.x; t < d; t += kRrNT) sq[t] = b.Q[(size_t)q * d + t];
-  __syncthreads();
+  const int rowb = U8 ? d : d * 4;
+  const int nv = rowb / 16;
+  const int per = (nv + LPC - 1) / LPC;               // <= MAXV (checked by the launcher)
   const int nc = b.ncand[q];
-  int* cp = b.cpos + (size_t)q * b.cap;
+  const int* cp = b.cpos + (size_t)q * b.cap;
   float* vv = b.val + (size_t)q * b.cap;
-  const int lane = threadIdx.x & 31;
+  float qr[MAXV][4];
+  const float* qv = b.Q + (size_t)q * d;
+#pragma unroll
+  for (int v = 0; v < MAXV; ++v) {
+    const int t = sl + LPC * v;
+    if (v < per && t < nv && !U8) {
+      const float4 x = reinterpret_cast<const float4*>(qv)[t];
+      qr[v][0] = x.x; qr[v][1] = x.y; qr[v][2] = x.z; qr[v][3] = x.w;
+    }
+  }
+  const uint8_t* raw = static_cast<const uint8_t*>(ix.raw);
   const int gw = blockIdx.x * (kRrNT / 32) + (threadIdx.x >> 5);
   const int nw = gridDim.x * (kRrNT / 32);
-  for (int c0 = gw * kRrUnroll; c0 < nc; c0 += nw * kRrUnroll) {
-    int row[kRrUnroll];
-    float acc[kRrUnroll];
+  for (int cb = gw * 32; cb < nc; cb += nw * 32) {    // 32 candidates per warp round
+    const int myrow = cb + lane < nc ? cp[cb + lane] : 0;
+    const int n32 = min(32, nc - cb);
+    for (int k0 = 0; k0 < n32; k0 += CPW * STEPS) {
+      uint4 x[STEPS][MAXV];
+      int kk[STEPS];
 #pragma unroll
-    for (int u = 0; u < kRrUnroll; ++u) {
-      row[u] = (c0 + u < nc) ? cp[c0 + u] : -1;
-      acc[u] = 0.f;
-    }
-    if constexpr (!U8) {
-      const int nv = d / 4;
-      for (int t = lane; t < nv; t += 32) {
-        float4 x[kRrUnroll];
+      for (int s = 0; s < STEPS; ++s) {
+        kk[s] = k0 + s * CPW + sub;
+        const int r = __shfl_sync(0xffffffffu, myrow, kk[s] & 31);
+        const uint4* rp = reinterpret_cast<const uint4*>(raw + (size_t)r * rowb);
 #pragma unroll
-        for (int u = 0; u < kRrUnroll; ++u)
-          if (row[u] >= 0)
-            x[u] = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(ix.raw) + (size_t)row[u] * d) + t);
-        const float4 qq = reinterpret_cast<const float4*>(sq)[t];
-#pragma unroll
-        for (int u = 0; u < kRrUnroll; ++u)
-          if (row[u] >= 0) {
-            float a = x[u].x - qq.x, bb = x[u].y - qq.y, c = x[u].z - qq.z, e = x[u].w - qq.w;
-            acc[u] = fmaf(a, a, acc[u]);
-            acc[u] = fmaf(bb, bb, acc[u]);
-            acc[u] = fmaf(c, c, acc[u]);
-            acc[u] = fmaf(e, e, acc[u]);
-          }
+        for (int v = 0; v < MAXV; ++v) {
+          const int t = sl + LPC * v;
+          if (v < per && t < nv) x[s][v] = __ldg(rp + t);
+        }
       }
-    } else {
-      const int nv = d / 16;
-      for (int t = lane; t < nv; t += 32) {
-        uint4 x[kRrUnroll];
 #pragma unroll
-        for (int u = 0; u < kRrUnroll; ++u)
-          if (row[u] >= 0)
-            x[u] = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(ix.raw) + (size_t)row[u] * d) + t);
+      for (int s = 0; s < STEPS; ++s) {
+        float acc = 0.f;
 #pragma unroll
-        for (int u = 0; u < kRrUnroll; ++u)
-          if (row[u] >= 0) {
-            const uint32_t wv[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+        for (int v = 0; v < MAXV; ++v) {
+          const int t = sl + LPC * v;
+          if (v < per && t < nv) {
+            if (U8) {
+              const uint32_t wv[4] = {x[s][v].x, x[s][v].y, x[s][v].z, x[s][v].w};
 #pragma unroll
-            for (int h = 0; h < 4; ++h)
+              for (int h = 0; h < 4; ++h)
 #pragma unroll
-              for (int by = 0; by < 4; ++by) {
-                float xv = (float)((wv[h] >> (8 * by)) & 255u);
-                float df = xv - sq[t * 16 + h * 4 + by];
-                acc[u] = fmaf(df, df, acc[u]);
-              }
+                for (int by = 0; by < 4; ++by) {
+                  const float df = (float)((wv[h] >> (8 * by)) & 255u) - __ldg(qv + t * 16 + h * 4 + by);
+                  acc = fmaf(df, df, acc);
+                }
+            } else {
+              const float a0 = __uint_as_float(x[s][v].x) - qr[v][0], a1 = __uint_as_float(x[s][v].y) - qr[v][1];
+              const float a2 = __uint_as_float(x[s][v].z) - qr[v][2], a3 = __uint_as_float(x[s][v].w) - qr[v][3];
+              acc = fmaf(a0, a0, acc);
+              acc = fmaf(a1, a1, acc);
+              acc = fmaf(a2, a2, acc);
+              acc = fmaf(a3, a3, acc);
+            }
           }
+        }
+#pragma unroll
+        for (int o = LPC / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (sl == 0 && kk[s] < n32) vv[cb + kk[s]] = acc;
       }
-    }
-#pragma unroll
-    for (int u = 0; u < kRrUnroll; ++u) acc[u] = warp_sum(acc[u]);
-    if (lane < kRrUnroll && c0 + lane < nc) {
-      float a = acc[0];
-#pragma unroll
-      for (int u = 1; u < kRrUnroll; ++u) if (lane == u) a = acc[u];
-      vv[c0 + lane] = a;
-      cp[c0 + lane] = (int)ix.ids[row[lane] >= 0 ? row[lane] : 0];
     }
   }
 }
@@ -901,7 +908,7 @@ __global__ void __launch_bounds__(kSelNT) k_final_select(Batch b, Dev ix, long l
   const int q = blockIdx.x;
   const int nc = b.ncand[q];
   const int k = b.k;
-  const int* cp = b.cpos + (size_t)q * b.cap;
+  const int* cp = b.cid + (size_t)q * b.cap;
   const float* vv = b.val + (size_t)q * b.cap;
   long long* oi = out_ids + (size_t)q * k;
   float* od = out_d2 + (size_t)q * k;
