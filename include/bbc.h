@@ -166,6 +166,31 @@ bbc_status bbc_search_debug(bbc_index index, const float* queries, int64_t nq, i
                             const bbc_debug_bufs* dbg);
 
 /*
+ * Multi-GPU (database sharded by IVF list).  Each rank loads its shard with
+ * ivf_load(path, rank, world, device), rank 0 creates an NCCL id with bbc_nccl_unique_id and
+ * broadcasts the 128 bytes (e.g. through torch.distributed), every rank calls bbc_comm_init, then
+ * every rank calls bbc_search with the SAME queries and parameters (SPMD).  The exchange steps
+ * (sample minimum and budget-th estimate, bucket histogram, final top-k) are NCCL all-reduces
+ * enqueued on the search stream; every rank receives the full result (replicated).  Results are
+ * identical for every world size.  Calling bbc_comm_init on a world-1 index makes bbc_search
+ * take the same sharded code path with a 1-rank communicator (used by tests).
+ */
+bbc_status bbc_nccl_unique_id(void* id128);
+bbc_status bbc_comm_init(bbc_index index, const void* id128, int rank, int world);
+
+/*
+ * bbc_search_group -- the sharded search for nshards (<= 8) shards held by ONE process on one
+ * device: shard i loaded with ivf_load(path, i, nshards, device).  The exchange steps are
+ * element-wise reductions across the shards' workspaces on `stream` (no NCCL); used to test the
+ * sharded algebra on a single GPU.  workspaces[i] / workspace_bytes[i]: per-shard device scratch
+ * (bbc_workspace_size of shard i).  out_ids/out_d2: device, [nq x k].
+ */
+bbc_status bbc_search_group(const bbc_index* shards, int nshards, const float* queries, int64_t nq,
+                            int32_t k, int32_t nprobe, int64_t budget, int64_t* out_ids,
+                            float* out_d2, void* const* workspaces, const size_t* workspace_bytes,
+                            void* stream);
+
+/*
  * Stage timing: when enabled, bbc_search records CUDA events on `stream` around each kernel of
  * the path; bbc_get_timing returns the summed milliseconds per stage of the searches since the
  * last call (and resets them).  Stages: BBC_STAGE_* below.  Synchronises the stream.

@@ -21,7 +21,8 @@ LIB_PATH = os.path.join(_HERE, "libbbc.so")
 EXPORTS = ("ivf_load", "ivf_free", "bbc_index_info", "bbc_workspace_size", "bbc_query_capacity",
            "bbc_search",
            "bbc_search_host", "bbc_search_debug", "bbc_set_timing", "bbc_get_timing",
-           "bbc_last_stats", "bbc_launch_count", "bbc_last_error")
+           "bbc_last_stats", "bbc_launch_count", "bbc_last_error", "bbc_nccl_unique_id",
+           "bbc_comm_init", "bbc_search_group")
 
 STAGES = ("probe", "tables", "sample", "scan", "compact", "rerank", "select", "comm")
 TAU_INF = 1 << 30
@@ -72,6 +73,10 @@ def lib() -> ctypes.CDLL:
         L.bbc_search_debug.argtypes = [vp, vp, i64, i32, i32, i64, vp, vp, vp, ctypes.c_size_t, vp,
                                        ctypes.POINTER(DebugBufs)]
         L.bbc_query_capacity.argtypes = [vp, i32, ctypes.POINTER(i64)]
+        L.bbc_nccl_unique_id.argtypes = [vp]
+        L.bbc_comm_init.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int]
+        L.bbc_search_group.argtypes = [ctypes.POINTER(vp), ctypes.c_int, vp, i64, i32, i32, i64, vp,
+                                       vp, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_size_t), vp]
         L.bbc_set_timing.argtypes = [vp, ctypes.c_int]
         L.bbc_get_timing.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int,
                                      ctypes.POINTER(ctypes.c_int64)]
@@ -83,7 +88,8 @@ def lib() -> ctypes.CDLL:
         L.bbc_last_error.restype = ctypes.c_char_p
         for fn in ("ivf_load", "bbc_index_info", "bbc_workspace_size", "bbc_search",
                    "bbc_search_host", "bbc_search_debug", "bbc_set_timing", "bbc_get_timing",
-                   "bbc_last_stats", "bbc_query_capacity"):
+                   "bbc_last_stats", "bbc_query_capacity", "bbc_nccl_unique_id",
+                   "bbc_comm_init", "bbc_search_group"):
             getattr(L, fn).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -103,6 +109,31 @@ def _torch():
     if not torch.cuda.is_available():
         raise BBCError("no CUDA device: the BBC path has no CPU fallback")
     return torch
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().bbc_nccl_unique_id(buf))
+    return buf.raw
+
+
+def search_group(shards, q, k: int, nprobe: int, budget: int, out=None, stream=None):
+    """Sharded search over shards (Index objects loaded with rank i, world len(shards)) held by
+    this process on one device: exchange steps are device reductions (bbc_search_group)."""
+    torch = _torch()
+    nq = q.shape[0]
+    G = len(shards)
+    if out is None:
+        out = (torch.empty((nq, k), dtype=torch.int64, device=q.device),
+               torch.empty((nq, k), dtype=torch.float32, device=q.device))
+    wss = [s.workspace(nq, k, nprobe, budget) for s in shards]
+    hs = (ctypes.c_void_p * G)(*[s._h.value for s in shards])
+    wp = (ctypes.c_void_p * G)(*[w.data_ptr() for w in wss])
+    wb = (ctypes.c_size_t * G)(*[w.numel() for w in wss])
+    st = torch.cuda.current_stream(q.device).cuda_stream if stream is None else stream
+    _check(lib().bbc_search_group(hs, G, q.data_ptr(), nq, k, nprobe, budget, out[0].data_ptr(),
+                                  out[1].data_ptr(), wp, wb, st))
+    return out
 
 
 class Index:
@@ -220,6 +251,12 @@ class Index:
         c = ctypes.c_int64()
         _check(lib().bbc_query_capacity(self._h, nprobe, ctypes.byref(c)))
         return c.value
+
+    # ------------------------------------------------------------------ multi-GPU
+    def comm_init(self, nccl_id: bytes, rank: int, world: int) -> None:
+        """Attach an NCCL communicator (SPMD sharded search; see include/bbc.h)."""
+        buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        _check(lib().bbc_comm_init(self._h, buf, rank, world))
 
     # ------------------------------------------------------------------ instrumentation
     def set_timing(self, on: bool) -> None:

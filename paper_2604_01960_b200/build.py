@@ -9,9 +9,19 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libbbc.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in ("bbc_api.cu",)]
-DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("bbc_kernels.cuh", "bbc_device.cuh")] + [
+DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("bbc_kernels.cuh", "bbc_device.cuh",
+                                                          "bbc_dist.cuh")] + [
     os.path.join(ROOT, "include", "bbc.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _nccl_dir() -> str:
+    """NCCL shipped with PyTorch's nvidia-nccl wheel (the library torch itself loads)."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec and spec.submodule_search_locations:
+        return list(spec.submodule_search_locations)[0]
+    return "/usr"
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
 
@@ -25,8 +35,10 @@ def stale() -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or stale():
-        cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), *SOURCES, "-o", LIB + ".tmp",
-               "-lcudart"]
+        nccl = _nccl_dir()
+        cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nccl, "include"),
+               *SOURCES, "-o", LIB + ".tmp", "-lcudart", "-L", os.path.join(nccl, "lib"),
+               "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(nccl, "lib")]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

@@ -4,12 +4,15 @@
 #include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <numeric>
 #include <string>
 #include <vector>
 
 #include "bbc.h"
-#include "bbc_kernels.cuh"
+#include <nccl.h>
+
+#include "bbc_dist.cuh"
 
 using namespace bbc;
 
@@ -62,6 +65,8 @@ struct bbc_index_s {
   long long timed_calls = 0;
   long long microbatches = 0;
   int num_sms = 148;
+  void* nccl = nullptr;                 // ncclComm_t of this rank (bbc_comm_init)
+  int force_dist = 0;                   // run the sharded code path even at world 1 (tests)
 };
 
 namespace {
@@ -73,6 +78,12 @@ namespace {
       if (ix) ix->broken = true;                                                   \
       return fail(BBC_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
     }                                                                              \
+  } while (0)
+
+#define CU_NOIX(expr)                                                              \
+  do {                                                                             \
+    cudaError_t e_ = (expr);                                                       \
+    if (e_ != cudaSuccess) return fail(BBC_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
 Dev dev_view(const bbc_index_s* ix) {
@@ -125,7 +136,7 @@ struct Plan {
   size_t fixed;       // alignment slack
 };
 
-Plan make_plan(const bbc_index_s* ix, int nprobe, int k) {
+Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1) {
   Plan p;
   long long cap = ix->desc_prefix[std::min<size_t>(nprobe, ix->desc_prefix.size() - 1)];
   cap = (cap + 15) / 16 * 16;
@@ -135,13 +146,14 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k) {
   p.per_query = (size_t)ix->nlist * 4 + (size_t)nprobe * 12 + 4 + 4 + 8 + kCells * 4 + 4 + 4 +
                 table + (size_t)cap * 13 + (size_t)ix->d * 4 + (size_t)k * 12 + 64 +
                 (size_t)((cap + kChunk - 1) / kChunk) * 4 + (size_t)(nprobe + 1) * 4;
+  p.per_query += 8 + 8 + kCells * 4 + 4 + 4 + (size_t)4 * world;   // DistBuf
   p.fixed = 64 * 256;
   return p;
 }
 
 // Carve the micro-batch arrays out of the workspace.
 void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, Batch& b,
-           float** qstage, long long** ostage_ids, float** ostage_d2, int k) {
+           float** qstage, long long** ostage_ids, float** ostage_d2, int k, DistBuf* db, int world) {
   size_t off = 0;
   auto take = [&](size_t bytes) {
     char* r = ws + off;
@@ -169,6 +181,12 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, 
   *qstage = (float*)take((size_t)nqb * ix->d * 4);
   *ostage_ids = (long long*)take((size_t)nqb * k * 8);
   *ostage_d2 = (float*)take((size_t)nqb * k * 4);
+  db->prefix = (unsigned long long*)take((size_t)nqb * 8);
+  db->need = (long long*)take((size_t)nqb * 8);
+  db->dh = (int*)take((size_t)nqb * kCells * 4);
+  db->umin = (unsigned*)take((size_t)nqb * 4);
+  db->tot = (int*)take((size_t)nqb * 4);
+  db->cnt = (int*)take((size_t)nqb * world * 4);
 }
 
 template <typename Kern>
@@ -224,133 +242,338 @@ bbc_status check_args(bbc_index ix, const void* q, int64_t nq, int32_t k, int32_
   return BBC_OK;
 }
 
-bbc_status run_search(bbc_index ix, const float* queries, int64_t nq, int32_t k, int32_t nprobe,
-                      int64_t budget, int64_t* out_ids, float* out_d2, void* workspace,
-                      size_t ws_bytes, void* stream, bool host, const bbc_debug_bufs* dbg) {
-  bbc_status s = check_args(ix, queries, nq, k, nprobe, budget, out_ids, out_d2, workspace);
-  if (s != BBC_OK) return s;
-  if (nq == 0) return BBC_OK;
-  CU(cudaSetDevice(ix->device));
-  cudaStream_t st = (cudaStream_t)stream;
-  Plan p = make_plan(ix, nprobe, k);
-  if (ws_bytes < p.fixed + p.per_query)
-    return fail(BBC_ERR_ARG, "workspace smaller than bbc_workspace_size min_bytes");
-  long long nqb = std::min<long long>(nq, (long long)((ws_bytes - p.fixed) / p.per_query));
-  if (dbg && nqb < nq) return fail(BBC_ERR_ARG, "debug search needs all queries in one micro-batch");
-  const long long budget_c = std::min<long long>(budget, (long long)1 << 40);
-  CU(cudaMemsetAsync(ix->stats, 0, 4 * sizeof(long long), st));
-  ix->microbatches = 0;
-  if (ix->timing) ix->timed_calls++;
-  Dev dv = dev_view(ix);
-  for (long long q0 = 0; q0 < nq; q0 += nqb) {
-    const int nb = (int)std::min<long long>(nqb, nq - q0);
-    Batch b;
-    float* qstage;
-    long long* oids;
-    float* od2;
-    carve(ix, p, nb, nprobe, (char*)workspace, b, &qstage, &oids, &od2, k);
-    b.nq = nb; b.nprobe = nprobe; b.k = k; b.budget = budget_c; b.cap = p.cap;
-    b.stats = ix->stats;
-    if (host) {
-      CU(cudaMemcpyAsync(qstage, queries + q0 * ix->d, (size_t)nb * ix->d * 4,
-                         cudaMemcpyHostToDevice, st));
-      b.Q = qstage;
-    } else {
-      b.Q = queries + q0 * ix->d;
-      oids = (long long*)out_ids + q0 * k;
-      od2 = out_d2 + q0 * k;
+// ---------------------------------------------------------------------------------------------
+// Collectives.  A search runs over one or more local shards; exchange steps call Comm.
+//   GroupComm: G shards of one process on one device (element-wise reduction kernel)
+//   NcclComm : one shard per process, ncclAllReduce on the search stream (NVLink/NVSwitch)
+// ---------------------------------------------------------------------------------------------
+enum class Dt { I32, U32, I64, F32 };
+enum class Op { Sum, Min };
+
+struct Comm {
+  virtual ~Comm() {}
+  virtual int world() const = 0;
+  virtual bool allreduce(const std::vector<void*>& bufs, size_t n, Dt dt, Op op, cudaStream_t st) = 0;
+};
+
+struct GroupComm : Comm {
+  int G;
+  explicit GroupComm(int g) : G(g) {}
+  int world() const override { return G; }
+  bool allreduce(const std::vector<void*>& bufs, size_t n, Dt dt, Op op, cudaStream_t st) override {
+    if (n == 0) return true;
+    GroupPtrs gp;
+    for (int g = 0; g < G; ++g) gp.p[g] = bufs[g];
+    const int blocks = (int)std::min<size_t>(4096, (n + 255) / 256);
+    const int o = op == Op::Sum ? 0 : 1;
+    switch (dt) {
+      case Dt::I32: k_group_allreduce<int><<<blocks, 256, 0, st>>>(gp, G, (long long)n, o); break;
+      case Dt::U32: k_group_allreduce<unsigned><<<blocks, 256, 0, st>>>(gp, G, (long long)n, o); break;
+      case Dt::I64: k_group_allreduce<long long><<<blocks, 256, 0, st>>>(gp, G, (long long)n, o); break;
+      case Dt::F32: k_group_allreduce<float><<<blocks, 256, 0, st>>>(gp, G, (long long)n, o); break;
     }
-    CU(cudaMemsetAsync(b.hist, 0, (size_t)nb * kCells * 4, st));
-    {
-      StageScope sc(ix, st, BBC_STAGE_PROBE);
-      dim3 g1((ix->nlist + kPT - 1) / kPT, (nb + kPT - 1) / kPT);
-      k_probe_d2<<<g1, 256, 0, st>>>(b.Q, ix->centroids, b.coarse, nb, ix->nlist, ix->d);
-      k_probe_select<<<nb, kSelNT, 0, st>>>(b, dv);
-      g_launches += 2;
-    }
-    {
-      StageScope sc(ix, st, BBC_STAGE_TABLES);
-      if (ix->kind == BBC_KIND_PQ) {
-        k_pq_lut<<<dim3(ix->M, nb), 256, 0, st>>>(b, dv);
-      } else {
-        k_rbq_rotate<<<dim3((ix->D + 255) / 256, nb), 256, (size_t)ix->d * 4, st>>>(b, dv);
-      }
-      g_launches += 1;
-    }
-    // lists per CTA: the query's LUT is staged once per CTA, so few CTAs per query; enough
-    // CTAs overall for >= 4 waves.
-    const int Gs = 1;
-    const int sample_grid = std::min(nprobe, 4);
+    g_launches += 1;
+    return cudaGetLastError() == cudaSuccess;
+  }
+};
+
+struct NcclComm : Comm {
+  ncclComm_t c;
+  int W;
+  NcclComm(ncclComm_t comm, int w) : c(comm), W(w) {}
+  int world() const override { return W; }
+  bool allreduce(const std::vector<void*>& bufs, size_t n, Dt dt, Op op, cudaStream_t st) override {
+    if (n == 0) return true;
+    ncclDataType_t t = dt == Dt::I32 ? ncclInt32 : dt == Dt::U32 ? ncclUint32 : dt == Dt::I64 ? ncclInt64 : ncclFloat32;
+    return ncclAllReduce(bufs[0], bufs[0], n, t, op == Op::Sum ? ncclSum : ncclMin, c, st) == ncclSuccess;
+  }
+};
+
+struct Shard {
+  bbc_index_s* ix;
+  char* ws;
+  size_t ws_bytes;
+  Plan p;
+  Dev dv;
+  Batch b;
+  DistBuf db;
+  float* qstage;
+  long long* oids;
+  float* od2;
+  int rank;
+};
+
+// ------------------------------------------------------------------ stage launchers (one shard)
+void stage_probe(Shard& s, cudaStream_t st) {
+  bbc_index_s* ix = s.ix;
+  StageScope sc(ix, st, BBC_STAGE_PROBE);
+  dim3 g1((ix->nlist + kPT - 1) / kPT, (s.b.nq + kPT - 1) / kPT);
+  k_probe_d2<<<g1, 256, 0, st>>>(s.b.Q, ix->centroids, s.b.coarse, s.b.nq, ix->nlist, ix->d);
+  k_probe_select<<<s.b.nq, kSelNT, 0, st>>>(s.b, s.dv);
+  g_launches += 2;
+}
+
+void stage_tables(Shard& s, cudaStream_t st) {
+  bbc_index_s* ix = s.ix;
+  StageScope sc(ix, st, BBC_STAGE_TABLES);
+  if (ix->kind == BBC_KIND_PQ)
+    k_pq_lut<<<dim3(ix->M, s.b.nq), 256, 0, st>>>(s.b, s.dv);
+  else
+    k_rbq_rotate<<<dim3((ix->D + 255) / 256, s.b.nq), 256, (size_t)ix->d * 4, st>>>(s.b, s.dv);
+  g_launches += 1;
+}
+
+int rq_grid(const Shard& s) { return (int)((s.p.cap + 32LL * s.b.nprobe + kRqE - 1) / kRqE); }
+
+// a3: estimates of the (local) sample objects -> val
+void stage_sample_est(Shard& s, cudaStream_t st) {
+  bbc_index_s* ix = s.ix;
+  StageScope sc(ix, st, BBC_STAGE_SAMPLE);
+  if (ix->kind == BBC_KIND_PQ) {
+    rq_scan(ix->M, true, dim3(rq_grid(s), s.b.nq), st, s.b, s.dv, ix->codes_t, ix->tbase, s.b.val, s.p.cap, 0);
+  } else {
+    const size_t sm = (size_t)ix->D * 4 + 4 * (ix->D / 32) * 4;
+    set_smem(k_rbq_scan<true>, sm);
+    k_rbq_scan<true><<<dim3(std::min(s.b.nprobe, 4), s.b.nq), kScanNT, sm, st>>>(s.b, s.dv, 1);
+  }
+  g_launches += 1;
+}
+
+// a4: bucket ids + local histogram of every probed object (sample ids from stored estimates)
+void stage_scan(Shard& s, cudaStream_t st) {
+  bbc_index_s* ix = s.ix;
+  StageScope sc(ix, st, BBC_STAGE_SCAN);
+  const int nb = s.b.nq, nprobe = s.b.nprobe;
+  if (ix->kind == BBC_KIND_PQ) {
+    k_sample_cells<<<dim3(8, nb), 256, 0, st>>>(s.b);
+    rq_scan(ix->M, false, dim3(rq_grid(s), nb), st, s.b, s.dv, ix->codes_t, ix->tbase, nullptr, 0, 1);
+    g_launches += 2;
+  } else {
     const int cta_per_q = std::max(1, std::min(nprobe, (3 * 148 * 6 + nb - 1) / nb));
     const int Gf = (nprobe + cta_per_q - 1) / cta_per_q;
-    if (ix->kind == BBC_KIND_PQ) {
-      const int gx = (int)((p.cap + 32LL * nprobe + kRqE - 1) / kRqE);
-      {
-        StageScope sc(ix, st, BBC_STAGE_SAMPLE);
-        rq_scan(ix->M, true, dim3(gx, nb), st, b, dv, ix->codes_t, ix->tbase, b.val, p.cap, 0);
-        k_select_edges<<<nb, kSelNT, 0, st>>>(b, dv);
-        k_sample_cells<<<dim3(8, nb), 256, 0, st>>>(b);
-        g_launches += 3;
+    const size_t sm = (size_t)ix->D * 4 + 4 * (ix->D / 32) * 4;
+    set_smem(k_rbq_scan<false>, sm);
+    k_rbq_scan<false><<<dim3((nprobe + Gf - 1) / Gf, nb), kScanNT, sm, st>>>(s.b, s.dv, Gf);
+    g_launches += 1;
+  }
+}
+
+void stage_compact(Shard& s, cudaStream_t st) {
+  StageScope sc(s.ix, st, BBC_STAGE_COMPACT);
+  const int nb = s.b.nq;
+  const int nchunk = (int)((s.p.cap + kChunk - 1) / kChunk);
+  const int gx = std::max(1, std::min(nchunk, (4 * 148 * 8 + nb - 1) / nb));
+  k_tau<<<nb, 32, 0, st>>>(s.b);
+  k_count<<<dim3(gx, nb), kCmpNT, 0, st>>>(s.b, s.b.chunk, nchunk);
+  k_chunk_offsets<<<nb, 256, 0, st>>>(s.b, s.b.chunk, nchunk);
+  k_emit<<<dim3(gx, nb), kCmpNT, 0, st>>>(s.b, s.dv, s.b.chunk, nchunk);
+  g_launches += 4;
+}
+
+void stage_rerank(Shard& s, cudaStream_t st) {
+  bbc_index_s* ix = s.ix;
+  StageScope sc(ix, st, BBC_STAGE_RERANK);
+  const int nb = s.b.nq;
+  const int gy = std::max(1, (8 * ix->num_sms + nb - 1) / nb);
+  const int rowb = ix->raw_u8 ? ix->d : ix->d * 4;
+  // lanes per candidate and 16-byte chunks per lane by row size
+  const dim3 g(gy, nb);
+  if (rowb <= 128) {
+    if (ix->raw_u8) k_rerank<true, 8, 1, 4><<<g, kRrNT, 0, st>>>(s.b, s.dv);
+    else k_rerank<false, 8, 1, 4><<<g, kRrNT, 0, st>>>(s.b, s.dv);
+  } else if (rowb <= 512) {
+    if (ix->raw_u8) k_rerank<true, 8, 4, 2><<<g, kRrNT, 0, st>>>(s.b, s.dv);
+    else k_rerank<false, 8, 4, 2><<<g, kRrNT, 0, st>>>(s.b, s.dv);
+  } else if (rowb <= 1024) {
+    k_rerank<false, 8, 8, 1><<<g, kRrNT, 0, st>>>(s.b, s.dv);
+  } else {
+    k_rerank<false, 32, 8, 1><<<g, kRrNT, 0, st>>>(s.b, s.dv);
+  }
+  g_launches += 1;
+}
+
+// ------------------------------------------------------------------ sharded exchange steps
+bool all_reduce(Comm* comm, std::vector<Shard>& sh, void* Shard::*unused, size_t n, Dt dt, Op op,
+                cudaStream_t st, const std::function<void*(Shard&)>& ptr) {
+  std::vector<void*> bufs;
+  for (auto& s : sh) bufs.push_back(ptr(s));
+  return comm->allreduce(bufs, n, dt, op, st);
+}
+
+bbc_status dist_edges(std::vector<Shard>& sh, Comm* comm, cudaStream_t st) {
+  bbc_index_s* ix = sh[0].ix;
+  const int nb = sh[0].b.nq;
+  StageScope sc(ix, st, BBC_STAGE_COMM);
+  for (auto& s : sh) {
+    k_ds_edges_init<<<(nb + 255) / 256, 256, 0, st>>>(s.b, s.db);
+    k_ds_localmin<<<nb, 256, 0, st>>>(s.b, s.db);
+    g_launches += 2;
+  }
+  if (!all_reduce(comm, sh, nullptr, (size_t)nb, Dt::U32, Op::Min, st, [](Shard& s) { return (void*)s.db.umin; }))
+    return fail(BBC_ERR_NCCL, "all-reduce (sample minimum) failed");
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (auto& s : sh) {
+      CU_NOIX(cudaMemsetAsync(s.db.dh, 0, (size_t)nb * kCells * 4, st));
+      k_ds_hist<false><<<dim3(8, nb), 256, 0, st>>>(s.b, s.db, shift);
+      g_launches += 1;
+    }
+    if (!all_reduce(comm, sh, nullptr, (size_t)nb * kCells, Dt::I32, Op::Sum, st, [](Shard& s) { return (void*)s.db.dh; }))
+      return fail(BBC_ERR_NCCL, "all-reduce (sample histogram) failed");
+    for (auto& s : sh) {
+      k_ds_pick<<<nb, 32, 0, st>>>(s.b, s.db, shift);
+      g_launches += 1;
+    }
+  }
+  for (auto& s : sh) {
+    k_ds_edges_finish<<<(nb + 255) / 256, 256, 0, st>>>(s.b, s.db);
+    g_launches += 1;
+  }
+  return BBC_OK;
+}
+
+bbc_status dist_hist(std::vector<Shard>& sh, Comm* comm, cudaStream_t st) {
+  StageScope sc(sh[0].ix, st, BBC_STAGE_COMM);
+  if (!all_reduce(comm, sh, nullptr, (size_t)sh[0].b.nq * kCells, Dt::I32, Op::Sum, st, [](Shard& s) { return (void*)s.b.hist; }))
+    return fail(BBC_ERR_NCCL, "all-reduce (bucket histogram) failed");
+  return BBC_OK;
+}
+
+bbc_status dist_select(std::vector<Shard>& sh, Comm* comm, cudaStream_t st) {
+  bbc_index_s* ix = sh[0].ix;
+  const int nb = sh[0].b.nq, k = sh[0].b.k, W = comm->world();
+  StageScope sc(ix, st, BBC_STAGE_SELECT);
+  for (auto& s : sh) {
+    k_ds_ncand<<<(nb + 255) / 256, 256, 0, st>>>(s.b, s.db);
+    g_launches += 1;
+  }
+  if (!all_reduce(comm, sh, nullptr, (size_t)nb, Dt::I32, Op::Sum, st, [](Shard& s) { return (void*)s.db.tot; }))
+    return fail(BBC_ERR_NCCL, "all-reduce (candidate count) failed");
+  for (auto& s : sh) {
+    k_ds_final_init<<<(nb + 255) / 256, 256, 0, st>>>(s.b, s.db);
+    g_launches += 1;
+  }
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (auto& s : sh) {
+      CU_NOIX(cudaMemsetAsync(s.db.dh, 0, (size_t)nb * kCells * 4, st));
+      k_ds_hist<true><<<dim3(8, nb), 256, 0, st>>>(s.b, s.db, shift);
+      g_launches += 1;
+    }
+    if (!all_reduce(comm, sh, nullptr, (size_t)nb * kCells, Dt::I32, Op::Sum, st, [](Shard& s) { return (void*)s.db.dh; }))
+      return fail(BBC_ERR_NCCL, "all-reduce (selection histogram) failed");
+    for (auto& s : sh) {
+      k_ds_pick<<<nb, 32, 0, st>>>(s.b, s.db, shift);
+      g_launches += 1;
+    }
+  }
+  for (auto& s : sh) {
+    CU_NOIX(cudaMemsetAsync(s.db.cnt, 0, (size_t)W * nb * 4, st));
+    k_ds_select<false><<<nb, kSelNT, 0, st>>>(s.b, s.db, s.rank, W, nullptr, nullptr);
+    g_launches += 1;
+  }
+  if (!all_reduce(comm, sh, nullptr, (size_t)W * nb, Dt::I32, Op::Sum, st, [](Shard& s) { return (void*)s.db.cnt; }))
+    return fail(BBC_ERR_NCCL, "all-reduce (selected counts) failed");
+  for (auto& s : sh) {
+    CU_NOIX(cudaMemsetAsync(s.oids, 0, (size_t)nb * k * 8, st));
+    CU_NOIX(cudaMemsetAsync(s.od2, 0, (size_t)nb * k * 4, st));
+    k_ds_select<true><<<nb, kSelNT, 0, st>>>(s.b, s.db, s.rank, W, s.oids, s.od2);
+    g_launches += 1;
+  }
+  if (!all_reduce(comm, sh, nullptr, (size_t)nb * k, Dt::I64, Op::Sum, st, [](Shard& s) { return (void*)s.oids; }) ||
+      !all_reduce(comm, sh, nullptr, (size_t)nb * k, Dt::F32, Op::Sum, st, [](Shard& s) { return (void*)s.od2; }))
+    return fail(BBC_ERR_NCCL, "all-reduce (results) failed");
+  for (auto& s : sh) {
+    k_ds_pad<<<dim3(4, nb), 256, 0, st>>>(s.b, s.db, W, s.oids, s.od2);
+    g_launches += 1;
+  }
+  return BBC_OK;
+}
+
+// ------------------------------------------------------------------ one search over local shards
+bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t nq, int32_t k,
+               int32_t nprobe, int64_t budget, int64_t* out_ids, float* out_d2, void* stream,
+               bool host, const bbc_debug_bufs* dbg) {
+  for (auto& s : sh) {
+    bbc_status st0 = check_args(s.ix, queries, nq, k, nprobe, budget, out_ids, out_d2, s.ws);
+    if (st0 != BBC_OK) return st0;
+  }
+  if (nq == 0) return BBC_OK;
+  bbc_index_s* ix = sh[0].ix;                       // for CU() error marking
+  CU(cudaSetDevice(ix->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool dist = comm != nullptr;
+  const int W = dist ? comm->world() : 1;
+  long long nqb = nq;
+  for (auto& s : sh) {
+    s.p = make_plan(s.ix, nprobe, k, W);
+    if (s.ws_bytes < s.p.fixed + s.p.per_query)
+      return fail(BBC_ERR_ARG, "workspace smaller than bbc_workspace_size min_bytes");
+    nqb = std::min<long long>(nqb, (long long)((s.ws_bytes - s.p.fixed) / s.p.per_query));
+  }
+  if (dbg && nqb < nq) return fail(BBC_ERR_ARG, "debug search needs all queries in one micro-batch");
+  const long long budget_c = std::min<long long>(budget, (long long)1 << 40);
+  for (auto& s : sh) {
+    CU(cudaMemsetAsync(s.ix->stats, 0, 4 * sizeof(long long), st));
+    s.ix->microbatches = 0;
+    if (s.ix->timing) s.ix->timed_calls++;
+    s.dv = dev_view(s.ix);
+  }
+  for (long long q0 = 0; q0 < nq; q0 += nqb) {
+    const int nb = (int)std::min<long long>(nqb, nq - q0);
+    for (auto& s : sh) {
+      carve(s.ix, s.p, nb, nprobe, s.ws, s.b, &s.qstage, &s.oids, &s.od2, k, &s.db, W);
+      Batch& b = s.b;
+      b.nq = nb; b.nprobe = nprobe; b.k = k; b.budget = budget_c; b.cap = s.p.cap;
+      b.stats = s.ix->stats;
+      if (host) {
+        CU(cudaMemcpyAsync(s.qstage, queries + q0 * ix->d, (size_t)nb * ix->d * 4,
+                           cudaMemcpyHostToDevice, st));
+        b.Q = s.qstage;
+      } else {
+        b.Q = queries + q0 * ix->d;
+        if (!dist) {
+          s.oids = (long long*)out_ids + q0 * k;
+          s.od2 = out_d2 + q0 * k;
+        }
       }
+      CU(cudaMemsetAsync(b.hist, 0, (size_t)nb * kCells * 4, st));
+      stage_probe(s, st);
+      stage_tables(s, st);
+      stage_sample_est(s, st);
+    }
+    if (!dist) {
+      Shard& s = sh[0];
       {
-        StageScope sc(ix, st, BBC_STAGE_SCAN);
-        rq_scan(ix->M, false, dim3(gx, nb), st, b, dv, ix->codes_t, ix->tbase, nullptr, 0, 1);
+        StageScope sc(s.ix, st, BBC_STAGE_SAMPLE);
+        k_select_edges<<<nb, kSelNT, 0, st>>>(s.b, s.dv);
+        g_launches += 1;
+      }
+      stage_scan(s, st);
+      stage_compact(s, st);
+      stage_rerank(s, st);
+      {
+        StageScope sc(s.ix, st, BBC_STAGE_SELECT);
+        k_final_select<<<nb, kSelNT, 0, st>>>(s.b, s.dv, s.oids, s.od2);
         g_launches += 1;
       }
     } else {
-      {
-        StageScope sc(ix, st, BBC_STAGE_SAMPLE);
-        size_t sm = (size_t)ix->D * 4 + 4 * (ix->D / 32) * 4;
-        set_smem(k_rbq_scan<true>, sm);
-        k_rbq_scan<true><<<dim3(sample_grid, nb), kScanNT, sm, st>>>(b, dv, Gs);
-        k_select_edges<<<nb, kSelNT, 0, st>>>(b, dv);
-        g_launches += 2;
+      bbc_status e = dist_edges(sh, comm, st);
+      if (e != BBC_OK) return e;
+      for (auto& s : sh) stage_scan(s, st);
+      if ((e = dist_hist(sh, comm, st)) != BBC_OK) return e;
+      for (auto& s : sh) {
+        stage_compact(s, st);
+        stage_rerank(s, st);
       }
-      {
-        StageScope sc(ix, st, BBC_STAGE_SCAN);
-        dim3 g((nprobe + Gf - 1) / Gf, nb);
-        size_t sm = (size_t)ix->D * 4 + 4 * (ix->D / 32) * 4;
-        set_smem(k_rbq_scan<false>, sm);
-        k_rbq_scan<false><<<g, kScanNT, sm, st>>>(b, dv, Gf);
-        g_launches += 1;
+      if ((e = dist_select(sh, comm, st)) != BBC_OK) return e;
+      if (!host) {                                     // results are replicated: shard 0's copy
+        CU(cudaMemcpyAsync(out_ids + q0 * k, sh[0].oids, (size_t)nb * k * 8, cudaMemcpyDeviceToDevice, st));
+        CU(cudaMemcpyAsync(out_d2 + q0 * k, sh[0].od2, (size_t)nb * k * 4, cudaMemcpyDeviceToDevice, st));
       }
-    }
-    {
-      StageScope sc(ix, st, BBC_STAGE_COMPACT);
-      const int nchunk = (int)((p.cap + kChunk - 1) / kChunk);
-      const int gx = std::max(1, std::min(nchunk, (4 * 148 * 8 + nb - 1) / nb));
-      k_tau<<<nb, 32, 0, st>>>(b);
-      k_count<<<dim3(gx, nb), kCmpNT, 0, st>>>(b, b.chunk, nchunk);
-      k_chunk_offsets<<<nb, 256, 0, st>>>(b, b.chunk, nchunk);
-      k_emit<<<dim3(gx, nb), kCmpNT, 0, st>>>(b, dv, b.chunk, nchunk);
-      g_launches += 4;
-    }
-    {
-      StageScope sc(ix, st, BBC_STAGE_RERANK);
-      const int gy = std::max(1, (8 * ix->num_sms + nb - 1) / nb);
-      const int rowb = ix->raw_u8 ? ix->d : ix->d * 4;
-      // lanes per candidate and 16-byte chunks per lane by row size
-      const dim3 g(gy, nb);
-      if (rowb <= 128) {
-        if (ix->raw_u8) k_rerank<true, 8, 1, 4><<<g, kRrNT, 0, st>>>(b, dv);
-        else k_rerank<false, 8, 1, 4><<<g, kRrNT, 0, st>>>(b, dv);
-      } else if (rowb <= 512) {
-        if (ix->raw_u8) k_rerank<true, 8, 4, 2><<<g, kRrNT, 0, st>>>(b, dv);
-        else k_rerank<false, 8, 4, 2><<<g, kRrNT, 0, st>>>(b, dv);
-      } else if (rowb <= 1024) {
-        k_rerank<false, 8, 8, 1><<<g, kRrNT, 0, st>>>(b, dv);
-      } else {
-        k_rerank<false, 32, 8, 1><<<g, kRrNT, 0, st>>>(b, dv);
-      }
-      g_launches += 1;
-    }
-    {
-      StageScope sc(ix, st, BBC_STAGE_SELECT);
-      k_final_select<<<nb, kSelNT, 0, st>>>(b, dv, oids, od2);
-      g_launches += 1;
     }
     CU(cudaGetLastError());
+    Shard& s0 = sh[0];
     if (dbg) {
+      const Batch& b = s0.b;
       auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
         return dst ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st) : cudaSuccess;
       };
@@ -365,15 +588,14 @@ bbc_status run_search(bbc_index ix, const float* queries, int64_t nq, int32_t k,
         CU(cudaMemcpy2DAsync(dbg->n_probed, 4, b.poff + nprobe, (size_t)(nprobe + 1) * 4, 4, nb,
                              cudaMemcpyDeviceToDevice, st));
       if (dbg->cand_ids || dbg->cand_d2) {
-        k_debug_cands<<<dim3(64, nb), 256, 0, st>>>(b.cid, b.val, b.ncand, p.cap, (long long*)dbg->cand_ids,
-                                                    dbg->cand_d2, dbg->cand_stride);
+        k_debug_cands<<<dim3(64, nb), 256, 0, st>>>(b.cid, b.val, b.ncand, s0.p.cap,
+                                                    (long long*)dbg->cand_ids, dbg->cand_d2, dbg->cand_stride);
         g_launches += 1;
       }
       if (dbg->est) {
         // every estimate in probe order, written to the caller's buffer (debug only)
         if (ix->kind == BBC_KIND_PQ) {
-          const int gx = (int)((p.cap + 32LL * nprobe + kRqE - 1) / kRqE);
-          rq_scan(ix->M, true, dim3(gx, nb), st, b, dv, ix->codes_t, ix->tbase, dbg->est,
+          rq_scan(ix->M, true, dim3(rq_grid(s0), nb), st, b, s0.dv, ix->codes_t, ix->tbase, dbg->est,
                   dbg->est_stride, 2);
         } else {
           Batch b2 = b;
@@ -384,21 +606,43 @@ bbc_status run_search(bbc_index ix, const float* queries, int64_t nq, int32_t k,
           CU(cudaMemcpyAsync(ns_all, all.data(), (size_t)nb * 4, cudaMemcpyHostToDevice, st));
           CU(cudaStreamSynchronize(st));
           b2.nsamp = ns_all;
-          size_t sm = (size_t)ix->D * 4 + 4 * (ix->D / 32) * 4;
-          k_rbq_scan<true><<<dim3(std::min(nprobe, 64), nb), kScanNT, sm, st>>>(b2, dv, 1);
+          const size_t sm = (size_t)ix->D * 4 + 4 * (ix->D / 32) * 4;
+          k_rbq_scan<true><<<dim3(std::min(nprobe, 64), nb), kScanNT, sm, st>>>(b2, s0.dv, 1);
         }
         g_launches += 1;
         CU(cudaGetLastError());
       }
     }
     if (host) {
-      CU(cudaMemcpyAsync(out_ids + q0 * k, oids, (size_t)nb * k * 8, cudaMemcpyDeviceToHost, st));
-      CU(cudaMemcpyAsync(out_d2 + q0 * k, od2, (size_t)nb * k * 4, cudaMemcpyDeviceToHost, st));
+      CU(cudaMemcpyAsync(out_ids + q0 * k, s0.oids, (size_t)nb * k * 8, cudaMemcpyDeviceToHost, st));
+      CU(cudaMemcpyAsync(out_d2 + q0 * k, s0.od2, (size_t)nb * k * 4, cudaMemcpyDeviceToHost, st));
     }
-    ix->microbatches++;
+    for (auto& s : sh) s.ix->microbatches++;
   }
   if (host || dbg) CU(cudaStreamSynchronize(st));
   return BBC_OK;
+}
+
+bbc_status run_one(bbc_index ix, const float* queries, int64_t nq, int32_t k, int32_t nprobe,
+                   int64_t budget, int64_t* out_ids, float* out_d2, void* workspace,
+                   size_t ws_bytes, void* stream, bool host, const bbc_debug_bufs* dbg) {
+  if (!ix) return fail(BBC_ERR_ARG, "null index");
+  std::vector<Shard> sh(1);
+  sh[0].ix = ix;
+  sh[0].ws = (char*)workspace;
+  sh[0].ws_bytes = ws_bytes;
+  sh[0].rank = ix->rank;
+  if (ix->world > 1) {
+    if (!ix->nccl) return fail(BBC_ERR_STATE, "sharded index: call bbc_comm_init first");
+    NcclComm c((ncclComm_t)ix->nccl, ix->world);
+    return run(sh, &c, queries, nq, k, nprobe, budget, out_ids, out_d2, stream, host, dbg);
+  }
+  if (ix->force_dist) {                            // world-1 NCCL communicator (tests)
+    if (!ix->nccl) return fail(BBC_ERR_STATE, "call bbc_comm_init first");
+    NcclComm c((ncclComm_t)ix->nccl, 1);
+    return run(sh, &c, queries, nq, k, nprobe, budget, out_ids, out_d2, stream, host, dbg);
+  }
+  return run(sh, nullptr, queries, nq, k, nprobe, budget, out_ids, out_d2, stream, host, dbg);
 }
 
 }  // namespace
@@ -598,6 +842,7 @@ void ivf_free(bbc_index ix) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& t : ix->timers) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
+  if (ix->nccl) ncclCommDestroy((ncclComm_t)ix->nccl);
   for (auto e : ix->pool) cudaEventDestroy(e);
   delete ix;
 }
@@ -615,7 +860,7 @@ bbc_status bbc_workspace_size(bbc_index ix, int64_t nq, int32_t k, int32_t nprob
   if (!ix || !bytes) return fail(BBC_ERR_ARG, "null argument");
   if (nprobe < 1 || nprobe > ix->nlist || k < 1 || nq < 0 || budget < k)
     return fail(BBC_ERR_ARG, "bad arguments");
-  Plan p = make_plan(ix, nprobe, k);
+  Plan p = make_plan(ix, nprobe, k, ix->world);
   *bytes = p.fixed + (size_t)std::max<int64_t>(nq, 1) * p.per_query;
   if (min_bytes) *min_bytes = p.fixed + p.per_query;
   return BBC_OK;
@@ -631,16 +876,16 @@ bbc_status bbc_query_capacity(bbc_index ix, int32_t nprobe, int64_t* cap) {
 bbc_status bbc_search(bbc_index ix, const float* queries, int64_t nq, int32_t k, int32_t nprobe,
                       int64_t budget, int64_t* out_ids, float* out_d2, void* workspace,
                       size_t workspace_bytes, void* stream) {
-  return run_search(ix, queries, nq, k, nprobe, budget, out_ids, out_d2, workspace,
-                    workspace_bytes, stream, false, nullptr);
+  return run_one(ix, queries, nq, k, nprobe, budget, out_ids, out_d2, workspace,
+                 workspace_bytes, stream, false, nullptr);
 }
 
 bbc_status bbc_search_host(bbc_index ix, const float* queries_host, int64_t nq, int32_t k,
                            int32_t nprobe, int64_t budget, int64_t* out_ids_host,
                            float* out_d2_host, void* workspace, size_t workspace_bytes,
                            void* stream) {
-  return run_search(ix, queries_host, nq, k, nprobe, budget, out_ids_host, out_d2_host, workspace,
-                    workspace_bytes, stream, true, nullptr);
+  return run_one(ix, queries_host, nq, k, nprobe, budget, out_ids_host, out_d2_host, workspace,
+                 workspace_bytes, stream, true, nullptr);
 }
 
 bbc_status bbc_search_debug(bbc_index ix, const float* queries, int64_t nq, int32_t k,
@@ -648,8 +893,53 @@ bbc_status bbc_search_debug(bbc_index ix, const float* queries, int64_t nq, int3
                             void* workspace, size_t workspace_bytes, void* stream,
                             const bbc_debug_bufs* dbg) {
   if (!dbg) return fail(BBC_ERR_ARG, "null debug buffers");
-  return run_search(ix, queries, nq, k, nprobe, budget, out_ids, out_d2, workspace,
-                    workspace_bytes, stream, false, dbg);
+  return run_one(ix, queries, nq, k, nprobe, budget, out_ids, out_d2, workspace,
+                 workspace_bytes, stream, false, dbg);
+}
+
+bbc_status bbc_search_group(const bbc_index* shards, int nshards, const float* queries, int64_t nq,
+                            int32_t k, int32_t nprobe, int64_t budget, int64_t* out_ids,
+                            float* out_d2, void* const* workspaces, const size_t* workspace_bytes,
+                            void* stream) {
+  if (!shards || !workspaces || !workspace_bytes || nshards < 1 || nshards > 8)
+    return fail(BBC_ERR_ARG, "bbc_search_group: 1..8 shards with workspaces");
+  std::vector<Shard> sh(nshards);
+  for (int i = 0; i < nshards; ++i) {
+    bbc_index_s* ix = shards[i];
+    if (!ix) return fail(BBC_ERR_ARG, "null shard");
+    if (ix->world != nshards || ix->rank != i || ix->device != shards[0]->device)
+      return fail(BBC_ERR_ARG, "shard i must be loaded with rank i, world nshards, same device");
+    sh[i].ix = ix;
+    sh[i].ws = (char*)workspaces[i];
+    sh[i].ws_bytes = workspace_bytes[i];
+    sh[i].rank = i;
+  }
+  GroupComm c(nshards);
+  return run(sh, &c, queries, nq, k, nprobe, budget, out_ids, out_d2, stream, false, nullptr);
+}
+
+bbc_status bbc_nccl_unique_id(void* id128) {
+  if (!id128) return fail(BBC_ERR_ARG, "null argument");
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return fail(BBC_ERR_NCCL, "ncclGetUniqueId failed");
+  memcpy(id128, &id, sizeof(id));
+  return BBC_OK;
+}
+
+bbc_status bbc_comm_init(bbc_index ix, const void* id128, int rank, int world) {
+  if (!ix || !id128) return fail(BBC_ERR_ARG, "null argument");
+  if (rank != ix->rank || world != ix->world)
+    return fail(BBC_ERR_ARG, "rank/world must match the shard the index was loaded as");
+  if (cudaSetDevice(ix->device) != cudaSuccess) return fail(BBC_ERR_CUDA, "cudaSetDevice");
+  ncclUniqueId id;
+  memcpy(&id, id128, sizeof(id));
+  ncclComm_t c;
+  const ncclResult_t r = ncclCommInitRank(&c, world, id, rank);
+  if (r != ncclSuccess) return fail(BBC_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  if (ix->nccl) ncclCommDestroy((ncclComm_t)ix->nccl);
+  ix->nccl = (void*)c;
+  ix->force_dist = world == 1;
+  return BBC_OK;
 }
 
 bbc_status bbc_set_timing(bbc_index ix, int enable) {

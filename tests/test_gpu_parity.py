@@ -206,3 +206,46 @@ def test_full_size_c2_sampled_queries():
     # invariants over every query: k distinct ids, distances ascending in no particular order
     for i in range(len(Q)):
         assert len(set(ids[i].tolist())) == cfg.k
+
+
+# ------------------------------------------------------------------ list-sharded path (8(e))
+def _sorted_by_id(ids, d2):
+    o = np.argsort(ids, axis=1, kind="stable")
+    return np.take_along_axis(ids, o, 1), np.take_along_axis(d2, o, 1)
+
+
+@pytest.mark.parametrize("name,G", [("C1t", 2), ("C2s", 3), ("C3s", 2), ("C5s", 4)])
+def test_sharded_group_equals_single(name, G):
+    """Lists sharded over G shards (greedy by size, as ivf_load does on G GPUs), the exchange
+    steps (MIN/histogram all-reduces, radix passes, result sum) done by the single-process group:
+    ids and exact d^2 identical to the unsharded search."""
+    from paper_2604_01960_b200 import Index
+    from paper_2604_01960_b200.bbc import search_group
+    cfg, ix, Q, g = gpu_index(name)
+    path = _LOAD["f"](name)[3]
+    shards = [Index(path, rank=r, world=G) for r in range(G)]
+    assert sum(s.info.n_local for s in shards) == cfg.N
+    q = torch.from_numpy(Q).cuda()
+    for k, nprobe, budget in ((cfg.k, cfg.nprobe, cfg.budget), (17, 3, 40), (cfg.k, 1, cfg.k)):
+        a_ids, a_d2 = g.search(q, k, nprobe, budget)
+        b_ids, b_d2 = search_group(shards, q, k, nprobe, budget)
+        a = _sorted_by_id(a_ids.cpu().numpy(), a_d2.cpu().numpy())
+        b = _sorted_by_id(b_ids.cpu().numpy(), b_d2.cpu().numpy())
+        assert np.array_equal(a[0], b[0])
+        assert np.array_equal(a[1].view(np.uint32), b[1].view(np.uint32))
+
+
+def test_nccl_path_world1_equals_single():
+    """bbc_search through the sharded code path with a real (1-rank) NCCL communicator."""
+    from paper_2604_01960_b200 import Index
+    from paper_2604_01960_b200.bbc import nccl_unique_id
+    cfg, ix, Q, g = gpu_index("C2s")
+    path = _LOAD["f"]("C2s")[3]
+    h = Index(path)
+    h.comm_init(nccl_unique_id(), 0, 1)
+    q = torch.from_numpy(Q).cuda()
+    a_ids, a_d2 = g.search(q, cfg.k, cfg.nprobe, cfg.budget)
+    b_ids, b_d2 = h.search(q, cfg.k, cfg.nprobe, cfg.budget)
+    a = _sorted_by_id(a_ids.cpu().numpy(), a_d2.cpu().numpy())
+    b = _sorted_by_id(b_ids.cpu().numpy(), b_d2.cpu().numpy())
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
