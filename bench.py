@@ -9,9 +9,10 @@ outside the timed events.  `value` = queries/s of the whole job (all ranks), tim
 events on the search stream, max over ranks.  `e2e` = the same through bbc_search_host with the
 host->device query copy and the device->host result copy inside the timed region.
 
-Multi-GPU (torchrun): the batch of queries is sharded across ranks (each rank runs its own
-batch of `nq` queries on a replicated index: independent problems, no data-path collective,
-"scaling": "weak").
+Multi-GPU (torchrun), --shard queries (default): each rank runs its own batch of `nq` queries
+on a replicated index (independent problems, no data-path collective, "scaling": "weak").
+--shard lists: the index is sharded by IVF list, every rank runs the same `nq` queries and the
+exchange steps are NCCL all-reduces inside libbbc.so ("scaling": "strong").
 
 --impl reference times the CPU oracle (oracle/, test infrastructure) on a bounded sample of the
 same workload, on rank 0 only.
@@ -53,6 +54,7 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=15.0)
     p.add_argument("--sweep", action="store_true", help="recall/QPS over an (nprobe, budget) grid")
     p.add_argument("--profile-steps", action="store_true", help="no warm-up/recall/cpu (ncu runs)")
+    p.add_argument("--shard", default="queries", choices=["queries", "lists"])
     return p.parse_args()
 
 
@@ -63,6 +65,29 @@ def peaks():
         return float(m["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def smem_lookup_peak_gbs():
+    """Shared-memory read peak: one 128-byte wavefront per clock per SM (32 conflict-free 4-byte
+    LUT lookups), 148 SMs, at the measured max SM clock."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz = float(json.load(f)["sm_max_mhz"])
+    except Exception:
+        mhz = 1965.0
+    return 148 * 128 * mhz * 1e6 / 1e9
+
+
+def measured_traffic(workload, nprobe, budget, kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture of the same workload and
+    operating point (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        e = t[f"{workload}/{nprobe}/{budget}"][kernel]
+        return {"dram_bytes_per_launch": e["dram_bytes"], "source": e["source"]}
+    except Exception:
+        return None
 
 
 class Clocks:
@@ -216,11 +241,22 @@ def main():
     nprobe, budget = operating_point(cfg, args)
     k = cfg.k
 
-    g = Index(path, device=local)
+    lists = args.shard == "lists" and world > 1
+    if lists:
+        from paper_2604_01960_b200.bbc import nccl_unique_id
+        g = Index(path, rank=rank, world=world, device=local)
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        g.comm_init(obj[0], rank, world)
+    else:
+        g = Index(path, device=local)
     if args.sweep:
         return sweep(cfg, path, g, rank)
-    Qall = synth.generate_queries(cfg, cfg.nq * world)
-    Qh = np.ascontiguousarray(Qall[rank * cfg.nq:(rank + 1) * cfg.nq])
+    if lists:                                            # same queries on every rank
+        Qh = np.ascontiguousarray(synth.generate_queries(cfg))
+    else:
+        Qall = synth.generate_queries(cfg, cfg.nq * world)
+        Qh = np.ascontiguousarray(Qall[rank * cfg.nq:(rank + 1) * cfg.nq])
     nq = len(Qh)
     q = torch.from_numpy(Qh).cuda()
     ws = g.workspace(nq, k, nprobe, budget)
@@ -260,7 +296,8 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    value = world * nq * args.steps / (ms_max / 1e3)
+    jobq = nq if lists else world * nq                   # queries answered by the whole job
+    value = jobq * args.steps / (ms_max / 1e3)
 
     # ---------------- e2e through the host API (pinned host buffers)
     qh = torch.from_numpy(Qh).pin_memory()
@@ -280,7 +317,7 @@ def main():
     te = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = world * nq * args.steps / (float(te.item()) / 1e3)
+    e2e_value = jobq * args.steps / (float(te.item()) / 1e3)
 
     if rank != 0:
         if world > 1:
@@ -288,24 +325,43 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ---------------- roofline of the dominant kernel (algorithmic bytes / event-timed duration)
+    # ---------------- roofline of the dominant kernel (algorithmic work / event-timed duration)
+    # Per step (the counters of the last timed search): the main scan estimates the probed
+    # objects outside the sample, M LUT lookups each (PQ); the re-rank gathers |S*| raw rows.
     info = g.info
     code_bytes = info.m if info.kind == 1 else info.dpad // 8 + 8
     row_bytes = info.d * (1 if info.raw_u8 else 4)
-    scan_bytes = stats["probed"] * code_bytes            # per step (the last step's counters)
-    rr_bytes = stats["candidates"] * row_bytes
+    main_objs = stats["probed"] - stats["sampled"]
     peak, peak_src = peaks()
+    smem_peak = smem_lookup_peak_gbs()
+    scan_ms = stage_ms["scan"] / args.steps
+    rr_ms = stage_ms["rerank"] / args.steps
     per = {
-        "scan": {"ms": stage_ms["scan"] / args.steps, "bytes": scan_bytes},
-        "rerank": {"ms": stage_ms["rerank"] / args.steps, "bytes": rr_bytes},
+        "scan": {"ms": scan_ms, "bound": "alu",
+                 "pipe": "shared-memory LUT lookups (one 4-byte LDS per code byte, conflict-free)",
+                 "bytes": main_objs * (info.m if info.kind == 1 else 0) * 4, "peak_GBs": smem_peak,
+                 "hbm_view": {"code_bytes": main_objs * code_bytes, "peak_GBs": peak}},
+        "rerank": {"ms": rr_ms, "bound": "hbm", "bytes": stats["candidates"] * row_bytes,
+                   "peak_GBs": peak},
     }
     for v in per.values():
         v["GBs"] = v["bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] > 0 else None
-        v["frac"] = v["GBs"] / peak if v["GBs"] else None
+        v["frac"] = v["GBs"] / v["peak_GBs"] if v["GBs"] else None
+        if "hbm_view" in v and v["ms"] > 0:
+            hv = v["hbm_view"]
+            hv["GBs"] = hv["code_bytes"] / (v["ms"] / 1e3) / 1e9
+            hv["frac"] = hv["GBs"] / peak
+    if info.kind != 1:                                  # RaBitQ scan: popcount, report HBM view
+        per["scan"].update(bound="hbm", bytes=main_objs * code_bytes, peak_GBs=peak)
+        per["scan"]["GBs"] = per["scan"]["bytes"] / (scan_ms / 1e3) / 1e9 if scan_ms > 0 else None
+        per["scan"]["frac"] = per["scan"]["GBs"] / peak if per["scan"]["GBs"] else None
     dom = max(per, key=lambda n: per[n]["ms"])
-    roof = {"bound": "hbm", "kernel": dom, "achieved": per[dom]["GBs"], "peak": peak,
-            "unit": "GB/s", "frac": per[dom]["frac"], "traffic": None,
-            "peak_source": peak_src, "per_kernel": per,
+    traffic = measured_traffic(cfg.name, nprobe, budget, dom)
+    roof = {"bound": per[dom]["bound"], "kernel": dom, "achieved": per[dom]["GBs"],
+            "peak": per[dom]["peak_GBs"], "unit": "GB/s", "frac": per[dom]["frac"],
+            "traffic": traffic, "peak_source": peak_src if per[dom]["bound"] == "hbm" else
+            "derived: 148 SMs x 128 B/clk shared-memory wavefronts x sm_max_mhz (DESIGN.md 5)",
+            "per_kernel": per,
             "stage_ms_per_step": {k_: v / args.steps for k_, v in stage_ms.items()}}
 
     # ---------------- recall on sampled queries (fp64 brute-force ground truth)
@@ -328,10 +384,12 @@ def main():
         "metric": "queries/sec at recall@k (BBC large-k IVF query path)",
         "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "strong" if lists else "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
         "config": {"workload": cfg.name, "N": cfg.N, "d": cfg.d, "quantizer": cfg.kind,
                    "M": cfg.M, "nlist": cfg.nlist, "nq_per_gpu": nq, "k": k, "nprobe": nprobe,
-                   "budget": budget, "parallelism": f"query-sharded x{world}",
+                   "budget": budget,
+                   "parallelism": (f"list-sharded x{world} (NCCL)" if lists else f"query-sharded x{world}"),
                    "l2": "flushed (256 MB write) between timed steps",
                    "probed_per_query": stats["probed"] / nq,
                    "candidates_per_query": stats["candidates"] / nq,

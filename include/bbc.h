@@ -213,6 +213,9 @@ bbc_status bbc_get_timing(bbc_index index, float* ms, int n, int64_t* calls);
  * stream): total probed objects (sum of n_o), total candidates (sum of |S*|), micro-batches. */
 bbc_status bbc_last_stats(bbc_index index, int64_t* probed, int64_t* candidates,
                           int64_t* microbatches);
+/* Same, plus the number of sample objects estimated in step a3 (summed over queries). */
+bbc_status bbc_last_stats2(bbc_index index, int64_t* probed, int64_t* candidates,
+                           int64_t* microbatches, int64_t* sampled);
 
 /* Number of CUDA kernels this library has launched in this process. */
 int64_t bbc_launch_count(void);

@@ -22,7 +22,7 @@ EXPORTS = ("ivf_load", "ivf_free", "bbc_index_info", "bbc_workspace_size", "bbc_
            "bbc_search",
            "bbc_search_host", "bbc_search_debug", "bbc_set_timing", "bbc_get_timing",
            "bbc_last_stats", "bbc_launch_count", "bbc_last_error", "bbc_nccl_unique_id",
-           "bbc_comm_init", "bbc_search_group")
+           "bbc_comm_init", "bbc_search_group", "bbc_last_stats2")
 
 STAGES = ("probe", "tables", "sample", "scan", "compact", "rerank", "select", "comm")
 TAU_INF = 1 << 30
@@ -82,6 +82,8 @@ def lib() -> ctypes.CDLL:
                                      ctypes.POINTER(ctypes.c_int64)]
         L.bbc_last_stats.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64),
                                      ctypes.POINTER(i64)]
+        L.bbc_last_stats2.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64),
+                                      ctypes.POINTER(i64), ctypes.POINTER(i64)]
         L.bbc_launch_count.argtypes = []
         L.bbc_launch_count.restype = i64
         L.bbc_last_error.argtypes = []
@@ -89,7 +91,7 @@ def lib() -> ctypes.CDLL:
         for fn in ("ivf_load", "bbc_index_info", "bbc_workspace_size", "bbc_search",
                    "bbc_search_host", "bbc_search_debug", "bbc_set_timing", "bbc_get_timing",
                    "bbc_last_stats", "bbc_query_capacity", "bbc_nccl_unique_id",
-                   "bbc_comm_init", "bbc_search_group"):
+                   "bbc_comm_init", "bbc_search_group", "bbc_last_stats2"):
             getattr(L, fn).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -269,6 +271,7 @@ class Index:
         return dict(zip(STAGES, [float(x) for x in arr])), calls.value
 
     def last_stats(self):
-        a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
-        _check(lib().bbc_last_stats(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
-        return dict(probed=a.value, candidates=b.value, microbatches=c.value)
+        a, b, c, d = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().bbc_last_stats2(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
+                                     ctypes.byref(d)))
+        return dict(probed=a.value, candidates=b.value, microbatches=c.value, sampled=d.value)

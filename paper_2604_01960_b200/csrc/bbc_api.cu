@@ -967,12 +967,18 @@ bbc_status bbc_get_timing(bbc_index ix, float* ms, int n, int64_t* calls) {
 }
 
 bbc_status bbc_last_stats(bbc_index ix, int64_t* probed, int64_t* candidates, int64_t* micro) {
+  return bbc_last_stats2(ix, probed, candidates, micro, nullptr);
+}
+
+bbc_status bbc_last_stats2(bbc_index ix, int64_t* probed, int64_t* candidates, int64_t* micro,
+                           int64_t* sampled) {
   if (!ix) return fail(BBC_ERR_ARG, "null index");
   long long h[4];
   CU(cudaMemcpy(h, ix->stats, sizeof(h), cudaMemcpyDeviceToHost));
   if (probed) *probed = h[0];
   if (candidates) *candidates = h[1];
   if (micro) *micro = ix->microbatches;
+  if (sampled) *sampled = h[2];
   return BBC_OK;
 }
 

@@ -114,6 +114,8 @@ __global__ void __launch_bounds__(256) k_ds_edges_finish(Batch b, DistBuf db) {
   if (q >= b.nq || b.nsamp[q] == 0) return;
   b.edges[2 * q] = key2f(db.umin[q]);
   b.edges[2 * q + 1] = key2f((unsigned)db.prefix[q]);
+  atomicAdd((unsigned long long*)&b.stats[2],
+            (unsigned long long)b.poff[(size_t)q * (b.nprobe + 1) + b.nsamp[q]]);
 }
 
 // ---------------------------------------------------------------- final selection (64-bit keys)

@@ -33,7 +33,7 @@ struct Batch {
   int* cpos;          // [nq x cap]  candidate rows (list-ordered index of this shard)
   int* cid;           // [nq x cap]  candidate original ids
   float* val;         // [nq x cap]  sample estimates, then exact d^2 of candidates
-  long long* stats;   // [2] sum n_o, sum |S*|
+  long long* stats;   // [3] sum n_o, sum |S*|, sum sample objects
   int* chunk;         // [nq x nchunk]  per-chunk candidate counts -> offsets (compaction)
 };
 
@@ -304,7 +304,7 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
 }
 
-constexpr int kRqWarps = 16, kRqNT = kRqWarps * 32, kRqEW = 64;
+constexpr int kRqWarps = 32, kRqNT = kRqWarps * 32, kRqEW = 32;
 constexpr int kRqE = kRqNT * kRqEW;                      // objects per CTA (32768)
 constexpr int kRqMC = 4;                                 // sub-quantizers per chunk
 constexpr int kRqBatch = 8;                              // code loads in flight per lane
@@ -363,7 +363,11 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
   if (!EST)
     for (int i = threadIdx.x; i < kCells; i += kRqNT) hist[i] = 0;
   const float* glut = b.table + (size_t)q * M * 256;
-  float nv0 = __ldg(glut + threadIdx.x), nv1 = __ldg(glut + threadIdx.x + kRqNT);  // chunk 0
+  constexpr int kStage = kRqMC * 256 / kRqNT;        // LUT entries staged per thread
+  static_assert(kStage * kRqNT == kRqMC * 256, "chunk entries must divide evenly");
+  float nv[kStage];
+#pragma unroll
+  for (int h = 0; h < kStage; ++h) nv[h] = __ldg(glut + threadIdx.x + h * kRqNT);   // chunk 0
   __syncthreads();
   // group table: group G = 32 objects starting at flat x0 + 32 G (never straddles a list)
   const int* po = b.poff + (size_t)q * (b.nprobe + 1);
@@ -402,22 +406,19 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
   for (int p = 0; p < M / kRqMC; ++p) {
     __syncthreads();                                  // previous chunk fully consumed
     // stage chunk p: entry (mm, c) replicated 32x at words ((mm>>1)*256 + c)*64 + (mm&1)*32 +
-    // [0, 32): lane l reads bank l.  Thread t writes entries t and t + 512 as 8 rotated
-    // 16-byte stores each (a quarter-warp covers all 32 banks).
-    {
-      const float4 a4 = make_float4(nv0, nv0, nv0, nv0), b4 = make_float4(nv1, nv1, nv1, nv1);
-      const int ea = threadIdx.x, eb = threadIdx.x + kRqNT;
-      float4* ra = reinterpret_cast<float4*>(lut + (size_t)((ea >> 9) * 256 + (ea & 255)) * 64 + ((ea >> 8) & 1) * 32);
-      float4* rb = reinterpret_cast<float4*>(lut + (size_t)((eb >> 9) * 256 + (eb & 255)) * 64 + ((eb >> 8) & 1) * 32);
+    // [0, 32): lane l reads bank l.  Each thread writes its entries as 8 rotated 16-byte
+    // stores each (a quarter-warp covers all 32 banks).
 #pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        ra[(r + lane) & 7] = a4;
-        rb[(r + lane) & 7] = b4;
-      }
+    for (int h = 0; h < kStage; ++h) {
+      const float4 a4 = make_float4(nv[h], nv[h], nv[h], nv[h]);
+      const int ea = threadIdx.x + h * kRqNT;
+      float4* ra = reinterpret_cast<float4*>(lut + (size_t)((ea >> 9) * 256 + (ea & 255)) * 64 + ((ea >> 8) & 1) * 32);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) ra[(r + lane) & 7] = a4;
     }
     if (p + 1 < M / kRqMC) {                          // prefetch chunk p+1's entries
-      nv0 = __ldg(glut + (p + 1) * kRqMC * 256 + threadIdx.x);
-      nv1 = __ldg(glut + (p + 1) * kRqMC * 256 + threadIdx.x + kRqNT);
+#pragma unroll
+      for (int h = 0; h < kStage; ++h) nv[h] = __ldg(glut + (p + 1) * kRqMC * 256 + threadIdx.x + h * kRqNT);
     }
     __syncthreads();
     const uint32_t plane = (uint32_t)p * 128u + lane4;
@@ -646,6 +647,7 @@ __global__ void __launch_bounds__(kSelNT) k_select_edges(Batch b, Dev ix) {
   if (threadIdx.x == 0) {
     b.edges[2 * q] = key2f((uint32_t)kmin);
     b.edges[2 * q + 1] = key2f((uint32_t)kmax);
+    atomicAdd((unsigned long long*)&b.stats[2], (unsigned long long)n);   // sample objects
   }
 }
 
