@@ -6,6 +6,7 @@
 // can change a rounding; the CPU oracle evaluates the same expression tree.
 #pragma once
 #include "bbc_device.cuh"
+#include <type_traits>
 
 namespace bbc {
 
@@ -285,18 +286,21 @@ constexpr int kScanNT = 256;   // RaBitQ scan CTA size
 // a3/a4  PQ code scan with a replicated LUT (query-major, conflict-free).
 //
 // CTA = (query q, pass P): objects [P*kRqE, (P+1)*kRqE) of q's probed objects in probe order,
-// where every probed list starts on a multiple of 32 (padded order, popad).  Warp w owns 64
-// groups of 32 consecutive objects; a group never straddles two lists, so lane l of the warp
-// handles object i0 + l of one list.  Each lane keeps the 64 running estimates of its objects in
-// registers; the M sub-quantizers are visited in chunks of 4 (canonical order m = 0..M-1).
+// where every probed list starts on a multiple of 32 (padded order, popad), so a 32-object
+// group never straddles two lists.  Warp w owns groups [32w, 32w + 32); lane l handles objects
+// 4(l&7) .. 4(l&7)+3 of groups 32w + (l>>3) + 4i, i = 0..7 (32 objects, 32 running estimates
+// in registers across all chunks).  The M sub-quantizers are visited in chunks of 4
+// (canonical order m = 0..M-1); a lane fetches the 4 objects' code words of one group and chunk
+// with one 16-byte load (8 lanes cover the group's 128 bytes: coalesced).
 //
 // The chunk's 4 x 256 LUT entries are replicated 32 times in shared memory so that lane l
-// always reads bank l, whatever the code: no bank conflicts (a single LUT copy costs ~3.5
-// wavefronts per lookup with random codes).  The replica layout [mm>>1][c][mm&1][lane] makes
-// the byte address of entry (mm, c) for lane l equal (c << 8) | 4l plus an immediate, so one
-// byte permute of the code word gives the address: PRMT + LDS + FADD per lookup.
-// Codes are read from a group-major copy (codes_t): a group's 32 code words of one chunk are
-// 128 consecutive bytes.
+// always reads bank l, whatever the code and whatever object it handles: no bank conflicts (a
+// single LUT copy costs ~3.5 wavefronts per lookup with random codes).  The replica layout
+// [mm>>1][c][mm&1][lane] makes the byte address of entry (mm, c) for lane l equal
+// (c << 8) | 4l plus an immediate, so one byte permute of the code word gives the address:
+// PRMT + LDS + FADD per lookup.  Group code offsets live in registers (no per-group pointer
+// reads), and the first code loads of chunk p+1 are issued before the chunk barrier so the L2
+// latency overlaps the LUT staging.
 //   EST : estimate written to out_est[q * est_stride + probe-order position] (sample/debug)
 //   !EST: bucket id to cells, histogram of ids < 255 (Push, Alg. 1 l.1-4)
 // ------------------------------------------------------------------------------------------
@@ -307,13 +311,14 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 constexpr int kRqWarps = 32, kRqNT = kRqWarps * 32, kRqEW = 32;
 constexpr int kRqE = kRqNT * kRqEW;                      // objects per CTA (32768)
 constexpr int kRqMC = 4;                                 // sub-quantizers per chunk
-constexpr int kRqBatch = 8;                              // code loads in flight per lane
-constexpr int kRqGroups = kRqWarps * kRqEW;              // 32-object groups per CTA
+constexpr int kRqGPL = kRqEW / 4;                        // groups per lane (8)
+constexpr int kRqDepth = 2;                              // 16-byte code loads in flight per lane
+constexpr int kRqGroups = kRqWarps * 32;                 // 32-object groups per CTA
 constexpr int kRqLutBytes = kRqMC * 256 * 32 * 4;        // 131072
-// dynamic shared memory: [LUT chunk][group code pointers][group output offsets][group counts]
+// dynamic shared memory: [LUT chunk][group code offsets][group output offsets][group counts]
 //                        [histogram][padded probe offsets]
-constexpr int kRqOffPtr = kRqLutBytes;
-constexpr int kRqOffOut = kRqOffPtr + kRqGroups * 8;
+constexpr int kRqOffGo = kRqLutBytes;
+constexpr int kRqOffOut = kRqOffGo + kRqGroups * 4;
 constexpr int kRqOffCnt = kRqOffOut + kRqGroups * 8;
 constexpr int kRqOffHist = kRqOffCnt + kRqGroups * 4;
 constexpr int kRqOffPo = kRqOffHist + kCells * 4;
@@ -324,6 +329,7 @@ constexpr unsigned kRqSmemBase = 1024;
 
 // Codes in group-major order for this scan: list L is cut into groups of 32 objects; group g,
 // chunk p (sub-quantizers 4p..4p+3), object lane l at byte tbase[L] + (g*(M/4) + p)*128 + 4l.
+// Every list's byte size is a multiple of 128 (M % 4 == 0), so offsets are kept in 128-byte units.
 __device__ __forceinline__ long long rq_list_bytes(int n, int M) { return (long long)((n + 31) >> 5) * M * 32; }
 constexpr int kCodesTailPad = 128;
 
@@ -334,6 +340,23 @@ __device__ __forceinline__ float lds_imm(uint32_t a) {
   return v;
 }
 
+template <int N, typename F, int I = 0>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (I < N) {
+    f(std::integral_constant<int, I>{});
+    static_for<N, F, I + 1>(static_cast<F&&>(f));
+  }
+}
+
+// acc += the 4 LUT entries selected by code word w (sub-quantizers 4p..4p+3, canonical order)
+__device__ __forceinline__ float rq_lookup4(float a, uint32_t w, uint32_t lane4) {
+  a = __fadd_rn(a, lds_imm<kRqSmemBase + 0>(__byte_perm(w, lane4, 0x7604)));
+  a = __fadd_rn(a, lds_imm<kRqSmemBase + 128>(__byte_perm(w, lane4, 0x7614)));
+  a = __fadd_rn(a, lds_imm<kRqSmemBase + 65536>(__byte_perm(w, lane4, 0x7624)));
+  a = __fadd_rn(a, lds_imm<kRqSmemBase + 65536 + 128>(__byte_perm(w, lane4, 0x7634)));
+  return a;
+}
+
 // mode 0: sample lists [0, nsamp) -> estimates; 1: lists [nsamp, nprobe) -> bucket ids;
 // 2: all lists -> estimates (debug)
 template <int M, bool EST>
@@ -341,9 +364,10 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
                                                          const long long* __restrict__ tbase,
                                                          float* out_est, long long est_stride,
                                                          int mode) {
+  constexpr int P = M / kRqMC;                       // chunks
   extern __shared__ __align__(16) uint8_t rsm[];
   float* lut = reinterpret_cast<float*>(rsm);
-  const uint8_t** gptr = reinterpret_cast<const uint8_t**>(rsm + kRqOffPtr);
+  uint32_t* gofs = reinterpret_cast<uint32_t*>(rsm + kRqOffGo);
   long long* gout = reinterpret_cast<long long*>(rsm + kRqOffOut);
   int* gcnt = reinterpret_cast<int*>(rsm + kRqOffCnt);
   int* hist = reinterpret_cast<int*>(rsm + kRqOffHist);
@@ -374,7 +398,7 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
   const int* pr = b.probe + (size_t)q * b.nprobe;
   const long long obase = EST ? (long long)q * est_stride : (long long)q * b.cap;
   for (int G = threadIdx.x; G < kRqGroups; G += kRqNT) {
-    const uint8_t* cp = codes_t;                      // invalid groups read (masked) garbage
+    uint32_t go = 0;                                  // invalid groups read (masked) list 0
     long long oo = 0;
     int cnt = 0;
     const int xg = x0 + 32 * G;
@@ -388,22 +412,35 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
       const int nL = (int)(ix.loff[L + 1] - ix.loff[L]);
       const int i0 = xg - s_popad[lo];
       cnt = min(32, nL - i0);
-      cp = codes_t + tbase[L] + (long long)(i0 >> 5) * M * 32;
+      go = (uint32_t)((tbase[L] + (long long)(i0 >> 5) * M * 32) >> 7);
       oo = obase + po[lo] + i0;
     }
-    gptr[G] = cp;
+    gofs[G] = go;
     gout[G] = oo;
     gcnt[G] = cnt;
   }
-  CellFn cf;
-  if (!EST) cf.init(b.edges[2 * q], b.edges[2 * q + 1]);
+  __syncthreads();
+  const int gl0 = wid * 32 + (lane >> 3);            // the lane's groups: gl0 + 4 i
+  // 16-byte index of the lane's slice of group gl0 + 4i, chunk p: gofs*8 + (lane&7) + 8p.  The
+  // group offsets are re-read from shared memory per load (4 distinct words per warp: one
+  // wavefront per 16 lookups) rather than held in 8 registers, which would spill.
+  for (int G = threadIdx.x; G < kRqGroups; G += kRqNT) gofs[G] = gofs[G] * 8u;
+  __syncthreads();
+  const uint32_t gaddr = smem_u32(gofs + gl0);
+  const uint4* __restrict__ c16 = reinterpret_cast<const uint4*>(codes_t) + (lane & 7);
+  auto ldc = [&](auto ic, int p) -> uint4 {
+    uint32_t g;
+    asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(g) : "r"(gaddr), "n"(16 * decltype(ic)::value));
+    return __ldg(c16 + (g + 8u * (uint32_t)p));
+  };
   float acc[kRqEW];
 #pragma unroll
   for (int e = 0; e < kRqEW; ++e) acc[e] = 0.f;
-  const uint8_t* const* mg = gptr + wid * kRqEW;
   const uint32_t lane4 = (uint32_t)lane * 4u;
+  uint4 cw[kRqDepth];
+  static_for<kRqDepth>([&](auto ic) { cw[decltype(ic)::value] = ldc(ic, 0); });
 #pragma unroll 1
-  for (int p = 0; p < M / kRqMC; ++p) {
+  for (int p = 0; p < P; ++p) {
     __syncthreads();                                  // previous chunk fully consumed
     // stage chunk p: entry (mm, c) replicated 32x at words ((mm>>1)*256 + c)*64 + (mm&1)*32 +
     // [0, 32): lane l reads bank l.  Each thread writes its entries as 8 rotated 16-byte
@@ -416,42 +453,43 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
 #pragma unroll
       for (int r = 0; r < 8; ++r) ra[(r + lane) & 7] = a4;
     }
-    if (p + 1 < M / kRqMC) {                          // prefetch chunk p+1's entries
+    if (p + 1 < P) {                                  // prefetch chunk p+1's entries
 #pragma unroll
       for (int h = 0; h < kStage; ++h) nv[h] = __ldg(glut + (p + 1) * kRqMC * 256 + threadIdx.x + h * kRqNT);
     }
     __syncthreads();
-    const uint32_t plane = (uint32_t)p * 128u + lane4;
-#pragma unroll
-    for (int g0 = 0; g0 < kRqEW; g0 += kRqBatch) {
-      uint32_t w[kRqBatch];
-#pragma unroll
-      for (int u = 0; u < kRqBatch; ++u)             // lanes past cnt read padding: masked later
-        w[u] = __ldg(reinterpret_cast<const uint32_t*>(mg[g0 + u] + plane));
-#pragma unroll
-      for (int u = 0; u < kRqBatch; ++u) {
-        // address = (c << 8) | 4*lane from one byte permute; sub-quantizer offset is immediate
-        float a = acc[g0 + u];
-        a = __fadd_rn(a, lds_imm<kRqSmemBase + 0>(__byte_perm(w[u], lane4, 0x7604)));
-        a = __fadd_rn(a, lds_imm<kRqSmemBase + 128>(__byte_perm(w[u], lane4, 0x7614)));
-        a = __fadd_rn(a, lds_imm<kRqSmemBase + 65536>(__byte_perm(w[u], lane4, 0x7624)));
-        a = __fadd_rn(a, lds_imm<kRqSmemBase + 65536 + 128>(__byte_perm(w[u], lane4, 0x7634)));
-        acc[g0 + u] = a;
-      }
-    }
+    const int pn = p + 1 < P ? p + 1 : p;            // code loads run one chunk ahead at the tail
+    static_for<kRqGPL>([&](auto ic) {
+      constexpr int i = decltype(ic)::value;
+      const uint4 c = cw[i % kRqDepth];
+      if constexpr (i + kRqDepth < kRqGPL)
+        cw[i % kRqDepth] = ldc(std::integral_constant<int, i + kRqDepth>{}, p);
+      else
+        cw[i % kRqDepth] = ldc(std::integral_constant<int, i + kRqDepth - kRqGPL>{}, pn);
+      acc[4 * i + 0] = rq_lookup4(acc[4 * i + 0], c.x, lane4);
+      acc[4 * i + 1] = rq_lookup4(acc[4 * i + 1], c.y, lane4);
+      acc[4 * i + 2] = rq_lookup4(acc[4 * i + 2], c.z, lane4);
+      acc[4 * i + 3] = rq_lookup4(acc[4 * i + 3], c.w, lane4);
+    });
   }
-  // epilogue
+  // epilogue: lane l holds objects 4(l&7)+j of its groups
+  CellFn cf;
+  if (!EST) cf.init(b.edges[2 * q], b.edges[2 * q + 1]);
 #pragma unroll
-  for (int g = 0; g < kRqEW; ++g) {
-    const int cnt = gcnt[wid * kRqEW + g];
-    if (lane < cnt) {
-      const long long oo = gout[wid * kRqEW + g] + lane;
-      if (EST) {
-        out_est[oo] = acc[g];
-      } else {
-        const int cell = cf(acc[g]);
-        b.cells[oo] = (uint8_t)cell;
-        if (cell < 255) atomicAdd(&hist[cell], 1);
+  for (int i = 0; i < kRqGPL; ++i) {
+    const int G = gl0 + 4 * i;
+    const int cnt = gcnt[G];
+    const long long oo = gout[G] + 4 * (lane & 7);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (4 * (lane & 7) + j < cnt) {
+        if (EST) {
+          out_est[oo + j] = acc[4 * i + j];
+        } else {
+          const int cell = cf(acc[4 * i + j]);
+          b.cells[oo + j] = (uint8_t)cell;
+          if (cell < 255) atomicAdd(&hist[cell], 1);
+        }
       }
     }
   }
