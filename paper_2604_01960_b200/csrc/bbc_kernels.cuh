@@ -800,56 +800,68 @@ __global__ void __launch_bounds__(256) k_chunk_offsets(Batch b, int* chunk_cnt, 
   }
 }
 
+// The query's probed-list boundaries (po) and row bases (loff[L] - po[j]) are staged in shared
+// memory once per CTA, so locating a candidate's list is a shared-memory binary search.
 __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chunk_off, int nchunk) {
   __shared__ int wcnt[kCmpNT / 32 + 1];
+  __shared__ int s_po[kMaxProbe + 1];
+  __shared__ long long s_rb[kMaxProbe];
   const int q = blockIdx.y;
   const int nprobe = b.nprobe;
   const int* po = b.poff + (size_t)q * (nprobe + 1);
   const int n = po[nprobe];
   const int tau = b.tau[q];
   const int need = (n + kChunk - 1) / kChunk;
-  for (int c = blockIdx.x; c < need; c += gridDim.x) {
-  const int i0 = c * kChunk + threadIdx.x * kPerThr;
-  const unsigned f = chunk_flags(b, q, i0, n, tau);
-  // exclusive prefix of per-thread counts across the block
-  const int mine = __popc(f);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int incl = mine;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int t = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += t;
-  }
-  if (lane == 31) wcnt[wid] = incl;
-  __syncthreads();
-  int pre = 0;
-  for (int w = 0; w < wid; ++w) pre += wcnt[w];
-  int pos = chunk_off[(size_t)q * nchunk + c] + pre + incl - mine;
-  __syncthreads();
-  if (!f) continue;
-  // list of the first candidate: last j with po[j] <= i (binary search), then walk forward
+  if ((int)blockIdx.x >= need) return;
   const int* pr = b.probe + (size_t)q * nprobe;
+  for (int j = threadIdx.x; j <= nprobe; j += kCmpNT) {
+    const int pj = po[j];
+    s_po[j] = pj;
+    if (j < nprobe) s_rb[j] = ix.loff[pr[j]] - pj;
+  }
+  __syncthreads();
   int* out = b.cpos + (size_t)q * b.cap;
-  int ifirst = i0 + __ffs(f) - 1;
-  int lo = 0, hi = nprobe - 1;
-  while (lo < hi) {
-    int mid = (lo + hi + 1) >> 1;
-    if (po[mid] <= ifirst) lo = mid; else hi = mid - 1;
-  }
-  int j = lo;
-  int jend = po[j + 1];
-  long long rbase = ix.loff[pr[j]] - po[j];
-  for (unsigned r = f; r; r &= r - 1) {
-    const int i = i0 + __ffs(r) - 1;
-    while (i >= jend) {            // next non-empty list containing i
-      ++j;
-      jend = po[j + 1];
-      rbase = ix.loff[pr[j]] - po[j];
+  int* oid = b.cid + (size_t)q * b.cap;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int c = blockIdx.x; c < need; c += gridDim.x) {
+    const int i0 = c * kChunk + threadIdx.x * kPerThr;
+    const unsigned f = chunk_flags(b, q, i0, n, tau);
+    // exclusive prefix of per-thread counts across the block
+    const int mine = __popc(f);
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
     }
-    const long long row = rbase + i;
-    b.cid[(size_t)q * b.cap + pos] = (int)ix.ids[row];
-    out[pos++] = (int)row;
-  }
+    if (lane == 31) wcnt[wid] = incl;
+    __syncthreads();
+    int pre = 0;
+    for (int w = 0; w < wid; ++w) pre += wcnt[w];
+    int pos = chunk_off[(size_t)q * nchunk + c] + pre + incl - mine;
+    __syncthreads();
+    if (!f) continue;
+    // list of the first candidate: last j with po[j] <= i, then walk forward
+    const int ifirst = i0 + __ffs(f) - 1;
+    int lo = 0, hi = nprobe - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_po[mid] <= ifirst) lo = mid; else hi = mid - 1;
+    }
+    int j = lo;
+    int jend = s_po[j + 1];
+    long long rbase = s_rb[j];
+    for (unsigned r = f; r; r &= r - 1) {
+      const int i = i0 + __ffs(r) - 1;
+      while (i >= jend) {            // next non-empty list containing i
+        ++j;
+        jend = s_po[j + 1];
+        rbase = s_rb[j];
+      }
+      const long long row = rbase + i;
+      oid[pos] = (int)ix.ids[row];
+      out[pos++] = (int)row;
+    }
   }
 }
 
@@ -862,8 +874,8 @@ __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chu
 // of the lane split; tolerance 1e-5 relative to the oracle's fp64).
 // ------------------------------------------------------------------------------------------
 constexpr int kRrNT = 256;
-template <bool U8, int LPC, int MAXV, int STEPS>
-__global__ void __launch_bounds__(kRrNT) k_rerank(Batch b, Dev ix) {
+template <bool U8, int LPC, int MAXV, int STEPS, int MINB = 1>
+__global__ void __launch_bounds__(kRrNT, MINB) k_rerank(Batch b, Dev ix) {
   constexpr int CPW = 32 / LPC;                       // candidates per warp step
   const int q = blockIdx.y;
   const int lane = threadIdx.x & 31, sub = lane / LPC, sl = lane % LPC;

@@ -1,0 +1,47 @@
+"""Per-stage device times of bbc_search on a workload (timed like bench.py: L2 flushed between
+steps), for kernel tuning runs."""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import datagen  # noqa: E402
+from datagen import configs, synth  # noqa: E402
+from paper_2604_01960_b200 import Index  # noqa: E402
+
+p = argparse.ArgumentParser()
+p.add_argument("--workload", default="C2")
+p.add_argument("--nprobe", type=int, default=768)
+p.add_argument("--budget", type=int, default=20000)
+p.add_argument("--steps", type=int, default=5)
+p.add_argument("--tag", default="")
+a = p.parse_args()
+cfg = configs.get(a.workload)
+path = datagen.ensure_index(cfg)
+g = Index(path)
+q = torch.from_numpy(synth.generate_queries(cfg)).cuda()
+ws = g.workspace(len(q), cfg.k, a.nprobe, a.budget)
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+for _ in range(3):
+    ids, d2 = g.search(q, cfg.k, a.nprobe, a.budget, workspace=ws)
+torch.cuda.synchronize()
+g.get_timing()
+g.set_timing(True)
+tot = 0.0
+for _ in range(a.steps):
+    flush.zero_()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.search(q, cfg.k, a.nprobe, a.budget, workspace=ws)
+    e1.record()
+    torch.cuda.synchronize()
+    tot += e0.elapsed_time(e1)
+g.set_timing(False)
+st, _ = g.get_timing()
+print(json.dumps({"tag": a.tag, "workload": a.workload, "ms_per_step": tot / a.steps,
+                  **{k: round(v / a.steps, 4) for k, v in st.items()}}), flush=True)
