@@ -362,9 +362,9 @@ void stage_compact(Shard& s, cudaStream_t st) {
   StageScope sc(s.ix, st, BBC_STAGE_COMPACT);
   const int nb = s.b.nq;
   const int nchunk = (int)((s.p.cap + kChunk - 1) / kChunk);
-  const int gx = std::max(1, std::min(nchunk, (4 * 148 * 8 + nb - 1) / nb));
+  const int gx = std::max(1, std::min(nchunk, (8 * s.ix->num_sms * 5 + nb - 1) / nb));
   k_tau<<<nb, 32, 0, st>>>(s.b);
-  k_count<<<dim3(gx, nb), kCmpNT, 0, st>>>(s.b, s.b.chunk, nchunk);
+  k_count<<<dim3((nchunk + kCntPer - 1) / kCntPer, nb), kCmpNT, 0, st>>>(s.b, s.b.chunk, nchunk);
   k_chunk_offsets<<<nb, 256, 0, st>>>(s.b, s.b.chunk, nchunk);
   k_emit<<<dim3(gx, nb), kCmpNT, 0, st>>>(s.b, s.dv, s.b.chunk, nchunk);
   g_launches += 4;

@@ -726,45 +726,63 @@ __global__ void __launch_bounds__(32) k_tau(Batch b) {
 // ------------------------------------------------------------------------------------------
 constexpr int kCmpNT = 256, kPerThr = 16, kChunk = kCmpNT * kPerThr;
 
-__device__ __forceinline__ unsigned chunk_flags(const Batch& b, int q, int i0, int n, int tau) {
-  // bit e set <=> element i0 + e (e < 16) is a candidate
-  unsigned f = 0;
-  if (i0 >= n) return 0;
-  const int m = min(kPerThr, n - i0);
-  if (tau == kTauInf) return m == 32 ? 0xffffffffu : ((1u << m) - 1u);
+// Cell ids of elements [i0, i0 + 16) of query q (ragged tail padded with 255 = never a candidate)
+__device__ __forceinline__ uint4 chunk_load(const Batch& b, int q, int i0, int n) {
+  uint4 x = make_uint4(~0u, ~0u, ~0u, ~0u);
+  if (i0 >= n) return x;
   const uint8_t* cl = b.cells + (size_t)q * b.cap + i0;
-  uint32_t w[4];
-  if (m == kPerThr) {
-    uint4 x = *reinterpret_cast<const uint4*>(cl);
-    w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
-  } else {
-    for (int e = 0; e < 4; ++e) w[e] = 0xffffffffu;
-    for (int e = 0; e < m; ++e) reinterpret_cast<uint8_t*>(w)[e] = cl[e];
-  }
+  const int m = min(kPerThr, n - i0);
+  if (m == kPerThr) return *reinterpret_cast<const uint4*>(cl);
+  uint32_t w[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
   for (int e = 0; e < kPerThr; ++e)
-    if ((int)((w[e >> 2] >> (8 * (e & 3))) & 255u) <= tau) f |= 1u << e;
-  return f;
+    w[e >> 2] |= (e < m ? (uint32_t)cl[e] : 255u) << (8 * (e & 3));
+  return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
+// bit e set <=> element i0 + e (e < 16) is a candidate (cell <= tau): four byte-wise SIMD
+// compares, the per-byte results gathered into 4-bit nibbles by one multiply each
+__device__ __forceinline__ unsigned chunk_flags(uint4 x, int i0, int n, int tau) {
+  if (i0 >= n) return 0;
+  const int m = min(kPerThr, n - i0);
+  const unsigned valid = m == 32 ? 0xffffffffu : ((1u << m) - 1u);
+  if (tau == kTauInf) return valid;
+  const unsigned t4 = (unsigned)tau * 0x01010101u;   // tau <= 254 here
+  const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+  unsigned f = 0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const unsigned le = (__vcmpleu4(w[e], t4) >> 7) & 0x01010101u;   // 1 per byte <= tau
+    f |= ((le * 0x01020408u) >> 24) << (4 * e);                      // bytes -> bits 0..3
+  }
+  return f & valid;
+}
+
+// Candidate count of kCntPer consecutive chunks per CTA (all loads issued up front).
+constexpr int kCntPer = 4;
 __global__ void __launch_bounds__(kCmpNT) k_count(Batch b, int* chunk_cnt, int nchunk) {
-  __shared__ int red[kCmpNT / 32];
+  __shared__ int red[kCntPer][kCmpNT / 32];
   const int q = blockIdx.y;
   const int n = b.poff[(size_t)q * (b.nprobe + 1) + b.nprobe];
   const int tau = b.tau[q];
   const int need = (n + kChunk - 1) / kChunk;
-  for (int c = blockIdx.x; c < need; c += gridDim.x) {
-    const int i0 = c * kChunk + threadIdx.x * kPerThr;
-    int cnt = __popc(chunk_flags(b, q, i0, n, tau));
+  const int c0 = blockIdx.x * kCntPer;
+  if (c0 >= need) return;
+  uint4 x[kCntPer];
+#pragma unroll
+  for (int u = 0; u < kCntPer; ++u)
+    x[u] = chunk_load(b, q, (c0 + u) * kChunk + threadIdx.x * kPerThr, tau == kTauInf ? 0 : n);
+#pragma unroll
+  for (int u = 0; u < kCntPer; ++u) {
+    int cnt = __popc(chunk_flags(x[u], (c0 + u) * kChunk + threadIdx.x * kPerThr, n, tau));
     cnt = warp_sum(cnt);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int t = 0;
-      for (int w = 0; w < kCmpNT / 32; ++w) t += red[w];
-      chunk_cnt[(size_t)q * nchunk + c] = t;
-    }
-    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[u][threadIdx.x >> 5] = cnt;
+  }
+  __syncthreads();
+  if (threadIdx.x < kCntPer && c0 + (int)threadIdx.x < need) {
+    int t = 0;
+    for (int w = 0; w < kCmpNT / 32; ++w) t += red[threadIdx.x][w];
+    chunk_cnt[(size_t)q * nchunk + c0 + threadIdx.x] = t;
   }
 }
 
@@ -801,11 +819,15 @@ __global__ void __launch_bounds__(256) k_chunk_offsets(Batch b, int* chunk_cnt, 
 }
 
 // The query's probed-list boundaries (po) and row bases (loff[L] - po[j]) are staged in shared
-// memory once per CTA, so locating a candidate's list is a shared-memory binary search.
+// memory once per CTA, so locating a candidate's list is a shared-memory binary search.  Each
+// chunk's candidate rows are first placed in shared memory at their block-scan rank, then
+// written out (rows and original ids) with coalesced stores; the next chunk's bucket ids are
+// loaded while the current one is processed.
 __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chunk_off, int nchunk) {
   __shared__ int wcnt[kCmpNT / 32 + 1];
   __shared__ int s_po[kMaxProbe + 1];
   __shared__ long long s_rb[kMaxProbe];
+  __shared__ int s_row[kChunk];
   const int q = blockIdx.y;
   const int nprobe = b.nprobe;
   const int* po = b.poff + (size_t)q * (nprobe + 1);
@@ -823,9 +845,12 @@ __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chu
   int* out = b.cpos + (size_t)q * b.cap;
   int* oid = b.cid + (size_t)q * b.cap;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nl = tau == kTauInf ? 0 : n;             // tau = infinity: no cell reads
+  uint4 xn = chunk_load(b, q, blockIdx.x * kChunk + threadIdx.x * kPerThr, nl);
   for (int c = blockIdx.x; c < need; c += gridDim.x) {
     const int i0 = c * kChunk + threadIdx.x * kPerThr;
-    const unsigned f = chunk_flags(b, q, i0, n, tau);
+    const unsigned f = chunk_flags(xn, i0, n, tau);
+    xn = chunk_load(b, q, (c + gridDim.x) * kChunk + threadIdx.x * kPerThr, nl);   // next chunk
     // exclusive prefix of per-thread counts across the block
     const int mine = __popc(f);
     int incl = mine;
@@ -836,32 +861,43 @@ __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chu
     }
     if (lane == 31) wcnt[wid] = incl;
     __syncthreads();
-    int pre = 0;
-    for (int w = 0; w < wid; ++w) pre += wcnt[w];
-    int pos = chunk_off[(size_t)q * nchunk + c] + pre + incl - mine;
-    __syncthreads();
-    if (!f) continue;
-    // list of the first candidate: last j with po[j] <= i, then walk forward
-    const int ifirst = i0 + __ffs(f) - 1;
-    int lo = 0, hi = nprobe - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (s_po[mid] <= ifirst) lo = mid; else hi = mid - 1;
+    int pre = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kCmpNT / 32; ++w) {
+      const int v = wcnt[w];
+      pre += w < wid ? v : 0;
+      tot += v;
     }
-    int j = lo;
-    int jend = s_po[j + 1];
-    long long rbase = s_rb[j];
-    for (unsigned r = f; r; r &= r - 1) {
-      const int i = i0 + __ffs(r) - 1;
-      while (i >= jend) {            // next non-empty list containing i
-        ++j;
-        jend = s_po[j + 1];
-        rbase = s_rb[j];
+    int pos = pre + incl - mine;
+    if (f) {
+      // list of the first candidate: last j with po[j] <= i, then walk forward
+      const int ifirst = i0 + __ffs(f) - 1;
+      int lo = 0, hi = nprobe - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_po[mid] <= ifirst) lo = mid; else hi = mid - 1;
       }
-      const long long row = rbase + i;
-      oid[pos] = (int)ix.ids[row];
-      out[pos++] = (int)row;
+      int j = lo;
+      int jend = s_po[j + 1];
+      long long rbase = s_rb[j];
+      for (unsigned r = f; r; r &= r - 1) {
+        const int i = i0 + __ffs(r) - 1;
+        while (i >= jend) {            // next non-empty list containing i
+          ++j;
+          jend = s_po[j + 1];
+          rbase = s_rb[j];
+        }
+        s_row[pos++] = (int)(rbase + i);
+      }
     }
+    __syncthreads();
+    const int base = chunk_off[(size_t)q * nchunk + c];
+    for (int t = threadIdx.x; t < tot; t += kCmpNT) {
+      const int row = s_row[t];
+      out[base + t] = row;
+      oid[base + t] = (int)ix.ids[row];
+    }
+    __syncthreads();
   }
 }
 
