@@ -191,7 +191,7 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, 
 
 template <typename Kern>
 void set_smem(Kern kern, size_t bytes) {
-  if (bytes > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (bytes > 0) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
 __global__ void k_debug_cands(const int* cpos, const float* val, const int* ncand, long long cap,
@@ -366,7 +366,8 @@ void stage_compact(Shard& s, cudaStream_t st) {
   k_tau<<<nb, 32, 0, st>>>(s.b);
   k_count<<<dim3((nchunk + kCntPer - 1) / kCntPer, nb), kCmpNT, 0, st>>>(s.b, s.b.chunk, nchunk);
   k_chunk_offsets<<<nb, 256, 0, st>>>(s.b, s.b.chunk, nchunk);
-  k_emit<<<dim3(gx, nb), kCmpNT, 0, st>>>(s.b, s.dv, s.b.chunk, nchunk);
+  set_smem(k_emit, (size_t)kChunk * 4);
+  k_emit<<<dim3(gx, nb), kCmpNT, (size_t)kChunk * 4, st>>>(s.b, s.dv, s.b.chunk, nchunk);
   g_launches += 4;
 }
 

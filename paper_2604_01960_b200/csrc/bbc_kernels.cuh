@@ -721,37 +721,45 @@ __global__ void __launch_bounds__(32) k_tau(Batch b) {
 
 // ------------------------------------------------------------------------------------------
 // a6  Collect l.19-21: superset S* = {cell <= tau}, compacted in probe order (deterministic).
-//     Chunks of kChunk objects per CTA, 16 per thread (one 16-byte load of cell ids):
+//     Chunks of kChunk objects per CTA, 32 per thread (two 16-byte loads of cell ids):
 //     k_count -> per-chunk counts, k_chunk_offsets -> per-query exclusive scan, k_emit -> rows.
 // ------------------------------------------------------------------------------------------
-constexpr int kCmpNT = 256, kPerThr = 16, kChunk = kCmpNT * kPerThr;
+constexpr int kCmpNT = 256, kPerThr = 32, kChunk = kCmpNT * kPerThr;
 
-// Cell ids of elements [i0, i0 + 16) of query q (ragged tail padded with 255 = never a candidate)
-__device__ __forceinline__ uint4 chunk_load(const Batch& b, int q, int i0, int n) {
-  uint4 x = make_uint4(~0u, ~0u, ~0u, ~0u);
+struct Cells32 { uint4 a, b; };                      // bucket ids of 32 consecutive elements
+
+// Cell ids of elements [i0, i0 + 32) of query q (ragged tail padded with 255 = never a candidate)
+__device__ __forceinline__ Cells32 chunk_load(const Batch& b, int q, int i0, int n) {
+  Cells32 x{make_uint4(~0u, ~0u, ~0u, ~0u), make_uint4(~0u, ~0u, ~0u, ~0u)};
   if (i0 >= n) return x;
   const uint8_t* cl = b.cells + (size_t)q * b.cap + i0;
   const int m = min(kPerThr, n - i0);
-  if (m == kPerThr) return *reinterpret_cast<const uint4*>(cl);
-  uint32_t w[4] = {0u, 0u, 0u, 0u};
+  if (m == kPerThr) {
+    x.a = reinterpret_cast<const uint4*>(cl)[0];
+    x.b = reinterpret_cast<const uint4*>(cl)[1];
+    return x;
+  }
+  uint32_t w[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
 #pragma unroll
   for (int e = 0; e < kPerThr; ++e)
     w[e >> 2] |= (e < m ? (uint32_t)cl[e] : 255u) << (8 * (e & 3));
-  return make_uint4(w[0], w[1], w[2], w[3]);
+  x.a = make_uint4(w[0], w[1], w[2], w[3]);
+  x.b = make_uint4(w[4], w[5], w[6], w[7]);
+  return x;
 }
 
-// bit e set <=> element i0 + e (e < 16) is a candidate (cell <= tau): four byte-wise SIMD
+// bit e set <=> element i0 + e (e < 32) is a candidate (cell <= tau): eight byte-wise SIMD
 // compares, the per-byte results gathered into 4-bit nibbles by one multiply each
-__device__ __forceinline__ unsigned chunk_flags(uint4 x, int i0, int n, int tau) {
+__device__ __forceinline__ unsigned chunk_flags(const Cells32& x, int i0, int n, int tau) {
   if (i0 >= n) return 0;
   const int m = min(kPerThr, n - i0);
   const unsigned valid = m == 32 ? 0xffffffffu : ((1u << m) - 1u);
   if (tau == kTauInf) return valid;
   const unsigned t4 = (unsigned)tau * 0x01010101u;   // tau <= 254 here
-  const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+  const uint32_t w[8] = {x.a.x, x.a.y, x.a.z, x.a.w, x.b.x, x.b.y, x.b.z, x.b.w};
   unsigned f = 0;
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
+  for (int e = 0; e < 8; ++e) {
     const unsigned le = (__vcmpleu4(w[e], t4) >> 7) & 0x01010101u;   // 1 per byte <= tau
     f |= ((le * 0x01020408u) >> 24) << (4 * e);                      // bytes -> bits 0..3
   }
@@ -768,7 +776,7 @@ __global__ void __launch_bounds__(kCmpNT) k_count(Batch b, int* chunk_cnt, int n
   const int need = (n + kChunk - 1) / kChunk;
   const int c0 = blockIdx.x * kCntPer;
   if (c0 >= need) return;
-  uint4 x[kCntPer];
+  Cells32 x[kCntPer];
 #pragma unroll
   for (int u = 0; u < kCntPer; ++u)
     x[u] = chunk_load(b, q, (c0 + u) * kChunk + threadIdx.x * kPerThr, tau == kTauInf ? 0 : n);
@@ -827,7 +835,7 @@ __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chu
   __shared__ int wcnt[kCmpNT / 32 + 1];
   __shared__ int s_po[kMaxProbe + 1];
   __shared__ long long s_rb[kMaxProbe];
-  __shared__ int s_row[kChunk];
+  extern __shared__ int s_row[];                     // [kChunk]
   const int q = blockIdx.y;
   const int nprobe = b.nprobe;
   const int* po = b.poff + (size_t)q * (nprobe + 1);
@@ -846,7 +854,7 @@ __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chu
   int* oid = b.cid + (size_t)q * b.cap;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int nl = tau == kTauInf ? 0 : n;             // tau = infinity: no cell reads
-  uint4 xn = chunk_load(b, q, blockIdx.x * kChunk + threadIdx.x * kPerThr, nl);
+  Cells32 xn = chunk_load(b, q, blockIdx.x * kChunk + threadIdx.x * kPerThr, nl);
   for (int c = blockIdx.x; c < need; c += gridDim.x) {
     const int i0 = c * kChunk + threadIdx.x * kPerThr;
     const unsigned f = chunk_flags(xn, i0, n, tau);
