@@ -143,9 +143,9 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1) {
   if (cap < 16) cap = 16;
   p.cap = cap;
   size_t table = ix->kind == BBC_KIND_PQ ? (size_t)ix->M * 256 * 4 : (size_t)ix->D * 4;
-  p.per_query = (size_t)ix->nlist * 4 + (size_t)nprobe * 12 + 4 + 4 + 8 + kCells * 4 + 4 + 4 +
+  p.per_query = (size_t)ix->nlist * 4 + (size_t)nprobe * 20 + 4 + 4 + 8 + kCells * 4 + 4 + 4 +
                 table + (size_t)cap * 13 + (size_t)ix->d * 4 + (size_t)k * 12 + 64 +
-                (size_t)((cap + kChunk - 1) / kChunk) * 4 + (size_t)(nprobe + 1) * 4;
+                (size_t)((cap + kChunk - 1) / kChunk) * 8 + (size_t)(nprobe + 1) * 4;
   p.per_query += 8 + 8 + kCells * 4 + 4 + 4 + (size_t)4 * world;   // DistBuf
   p.fixed = 64 * 256;
   return p;
@@ -166,6 +166,7 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, 
   b.rq2 = (float*)take((size_t)nqb * nprobe * 4);
   b.poff = (int*)take((size_t)nqb * (nprobe + 1) * 4);
   b.popad = (int*)take((size_t)nqb * (nprobe + 1) * 4);
+  b.rbase = (long long*)take((size_t)nqb * nprobe * 8);
   b.nsamp = (int*)take((size_t)nqb * 4);
   b.edges = (float*)take((size_t)nqb * 8);
   b.hist = (int*)take((size_t)nqb * kCells * 4);
@@ -177,6 +178,7 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, 
   b.cid = (int*)take((size_t)nqb * p.cap * 4);
   b.val = (float*)take((size_t)nqb * p.cap * 4);
   b.chunk = (int*)take((size_t)nqb * ((p.cap + kChunk - 1) / kChunk) * 4);
+  b.chunkj = (int*)take((size_t)nqb * ((p.cap + kChunk - 1) / kChunk) * 4);
 
   *qstage = (float*)take((size_t)nqb * ix->d * 4);
   *ostage_ids = (long long*)take((size_t)nqb * k * 8);
@@ -362,12 +364,11 @@ void stage_compact(Shard& s, cudaStream_t st) {
   StageScope sc(s.ix, st, BBC_STAGE_COMPACT);
   const int nb = s.b.nq;
   const int nchunk = (int)((s.p.cap + kChunk - 1) / kChunk);
-  const int gx = std::max(1, std::min(nchunk, (8 * s.ix->num_sms * 5 + nb - 1) / nb));
   k_tau<<<nb, 32, 0, st>>>(s.b);
   k_count<<<dim3((nchunk + kCntPer - 1) / kCntPer, nb), kCmpNT, 0, st>>>(s.b, s.b.chunk, nchunk);
   k_chunk_offsets<<<nb, 256, 0, st>>>(s.b, s.b.chunk, nchunk);
   set_smem(k_emit, (size_t)kChunk * 4);
-  k_emit<<<dim3(gx, nb), kCmpNT, (size_t)kChunk * 4, st>>>(s.b, s.dv, s.b.chunk, nchunk);
+  k_emit<<<dim3(nchunk, nb), kCmpNT, (size_t)kChunk * 4, st>>>(s.b, s.dv, s.b.chunk, nchunk);
   g_launches += 4;
 }
 

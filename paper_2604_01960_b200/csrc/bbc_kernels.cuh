@@ -24,6 +24,7 @@ struct Batch {
   float* rq2;         // [nq x nprobe]
   int* poff;          // [nq x (nprobe+1)]   element offset of each probed list (local)
   int* popad;         // [nq x (nprobe+1)]   same with every list rounded up to 32 objects
+  long long* rbase;   // [nq x nprobe]       loff[probe[j]] - poff[j]: row of element i = rbase[j] + i
   int* nsamp;         // [nq]                sample lists s (0 = tau infinity)
   float* edges;       // [nq x 2]            (d_min, d_max)
   int* hist;          // [nq x 256]
@@ -36,6 +37,7 @@ struct Batch {
   float* val;         // [nq x cap]  sample estimates, then exact d^2 of candidates
   long long* stats;   // [3] sum n_o, sum |S*|, sum sample objects
   int* chunk;         // [nq x nchunk]  per-chunk candidate counts -> offsets (compaction)
+  int* chunkj;        // [nq x nchunk]  probed list holding each chunk's first element
 };
 
 // Index arrays on the device.
@@ -197,6 +199,7 @@ __global__ void __launch_bounds__(kSelNT) k_probe_select(Batch b, Dev ix) {
     const long long incl_g = grun + wg[wid] + ig;
     if (j < nprobe) {
       po[j] = (int)excl_l;
+      b.rbase[(size_t)q * nprobe + j] = ix.loff[pr[j]] - excl_l;
       pp[j] = (int)(prun + wpd[wid] + ipd - ((lsz + 31) & ~31));
     }
     // sample rule: first j with cumulative global size >= budget
@@ -814,7 +817,17 @@ __global__ void __launch_bounds__(256) k_chunk_offsets(Batch b, int* chunk_cnt, 
     __syncthreads();
     int pre = 0, tot = 0;
     for (int w = 0; w < 8; ++w) { if (w < wid) pre += wsum[w]; tot += wsum[w]; }
-    if (c < need) cc[c] = run + pre + incl - v;
+    if (c < need) {
+      cc[c] = run + pre + incl - v;
+      const int* po = b.poff + (size_t)q * (b.nprobe + 1);
+      const int x = c * kChunk;                       // last j with po[j] <= x
+      int lo = 0, hi = b.nprobe - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (po[mid] <= x) lo = mid; else hi = mid - 1;
+      }
+      b.chunkj[(size_t)q * nchunk + c] = lo;
+    }
     run += tot;
     __syncthreads();
   }
@@ -826,86 +839,88 @@ __global__ void __launch_bounds__(256) k_chunk_offsets(Batch b, int* chunk_cnt, 
   }
 }
 
-// The query's probed-list boundaries (po) and row bases (loff[L] - po[j]) are staged in shared
-// memory once per CTA, so locating a candidate's list is a shared-memory binary search.  Each
-// chunk's candidate rows are first placed in shared memory at their block-scan rank, then
-// written out (rows and original ids) with coalesced stores; the next chunk's bucket ids are
-// loaded while the current one is processed.
+// One chunk per CTA.  The lists covering the chunk (from chunkj) have their offsets and row
+// bases staged in shared memory with one parallel load; a candidate's list is then a
+// shared-memory binary search and its row rbase[j] + i.  The chunk's candidate rows are placed
+// in shared memory at their block-scan rank, then written out (rows and original ids) with
+// coalesced stores.  Few dependent global accesses per CTA: the kernel is latency-bound.
+constexpr int kEmitWin = 1024;                       // lists staged per chunk (else global search)
 __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chunk_off, int nchunk) {
-  __shared__ int wcnt[kCmpNT / 32 + 1];
-  __shared__ int s_po[kMaxProbe + 1];
-  __shared__ long long s_rb[kMaxProbe];
+  __shared__ int wcnt[kCmpNT / 32];
+  __shared__ int s_po[kEmitWin + 1];
+  __shared__ long long s_rb[kEmitWin];
   extern __shared__ int s_row[];                     // [kChunk]
   const int q = blockIdx.y;
   const int nprobe = b.nprobe;
   const int* po = b.poff + (size_t)q * (nprobe + 1);
   const int n = po[nprobe];
   const int tau = b.tau[q];
-  const int need = (n + kChunk - 1) / kChunk;
-  if ((int)blockIdx.x >= need) return;
-  const int* pr = b.probe + (size_t)q * nprobe;
-  for (int j = threadIdx.x; j <= nprobe; j += kCmpNT) {
-    const int pj = po[j];
-    s_po[j] = pj;
-    if (j < nprobe) s_rb[j] = ix.loff[pr[j]] - pj;
+  const int c = blockIdx.x;
+  if (c * kChunk >= n) return;
+  const long long* rb = b.rbase + (size_t)q * nprobe;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int i0 = c * kChunk + threadIdx.x * kPerThr;
+  const Cells32 cx = chunk_load(b, q, i0, tau == kTauInf ? 0 : n);
+  const int jc = b.chunkj[(size_t)q * nchunk + c];
+  const int jn = (c + 1) * kChunk < n ? b.chunkj[(size_t)q * nchunk + c + 1] : nprobe - 1;
+  const int W = jn - jc + 1;                          // lists touching this chunk
+  const bool win = W <= kEmitWin;
+  if (win)
+    for (int t = threadIdx.x; t < W; t += kCmpNT) {
+      s_po[t] = po[jc + t];
+      s_rb[t] = rb[jc + t];
+      if (t == W - 1) s_po[W] = po[jc + W];
+    }
+  const unsigned f = chunk_flags(cx, i0, n, tau);
+  // exclusive prefix of per-thread counts across the block
+  const int mine = __popc(f);
+  int incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) wcnt[wid] = incl;
+  __syncthreads();
+  int pre = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < kCmpNT / 32; ++w) {
+    const int v = wcnt[w];
+    pre += w < wid ? v : 0;
+    tot += v;
+  }
+  int pos = pre + incl - mine;
+  if (f) {
+    // list of the first candidate: last j with po[j] <= i, then walk forward
+    const int ifirst = i0 + __ffs(f) - 1;
+    const int* sp = win ? s_po : po + jc;
+    const int top = win ? W - 1 : nprobe - 1 - jc;
+    int lo = 0, hi = top;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (sp[mid] <= ifirst) lo = mid; else hi = mid - 1;
+    }
+    int j = lo;
+    int jend = sp[j + 1];
+    long long rbase = win ? s_rb[j] : rb[jc + j];
+    for (unsigned r = f; r; r &= r - 1) {
+      const int i = i0 + __ffs(r) - 1;
+      while (i >= jend) {            // next non-empty list containing i
+        ++j;
+        jend = sp[j + 1];
+        rbase = win ? s_rb[j] : rb[jc + j];
+      }
+      s_row[pos++] = (int)(rbase + i);
+    }
   }
   __syncthreads();
-  int* out = b.cpos + (size_t)q * b.cap;
-  int* oid = b.cid + (size_t)q * b.cap;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int nl = tau == kTauInf ? 0 : n;             // tau = infinity: no cell reads
-  Cells32 xn = chunk_load(b, q, blockIdx.x * kChunk + threadIdx.x * kPerThr, nl);
-  for (int c = blockIdx.x; c < need; c += gridDim.x) {
-    const int i0 = c * kChunk + threadIdx.x * kPerThr;
-    const unsigned f = chunk_flags(xn, i0, n, tau);
-    xn = chunk_load(b, q, (c + gridDim.x) * kChunk + threadIdx.x * kPerThr, nl);   // next chunk
-    // exclusive prefix of per-thread counts across the block
-    const int mine = __popc(f);
-    int incl = mine;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    if (lane == 31) wcnt[wid] = incl;
-    __syncthreads();
-    int pre = 0, tot = 0;
-#pragma unroll
-    for (int w = 0; w < kCmpNT / 32; ++w) {
-      const int v = wcnt[w];
-      pre += w < wid ? v : 0;
-      tot += v;
-    }
-    int pos = pre + incl - mine;
-    if (f) {
-      // list of the first candidate: last j with po[j] <= i, then walk forward
-      const int ifirst = i0 + __ffs(f) - 1;
-      int lo = 0, hi = nprobe - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s_po[mid] <= ifirst) lo = mid; else hi = mid - 1;
-      }
-      int j = lo;
-      int jend = s_po[j + 1];
-      long long rbase = s_rb[j];
-      for (unsigned r = f; r; r &= r - 1) {
-        const int i = i0 + __ffs(r) - 1;
-        while (i >= jend) {            // next non-empty list containing i
-          ++j;
-          jend = s_po[j + 1];
-          rbase = s_rb[j];
-        }
-        s_row[pos++] = (int)(rbase + i);
-      }
-    }
-    __syncthreads();
-    const int base = chunk_off[(size_t)q * nchunk + c];
-    for (int t = threadIdx.x; t < tot; t += kCmpNT) {
-      const int row = s_row[t];
-      out[base + t] = row;
-      oid[base + t] = (int)ix.ids[row];
-    }
-    __syncthreads();
+  const int base = chunk_off[(size_t)q * nchunk + c];
+  int* out = b.cpos + (size_t)q * b.cap + base;
+  int* oid = b.cid + (size_t)q * b.cap + base;
+  for (int t = threadIdx.x; t < tot; t += kCmpNT) {
+    const int row = s_row[t];
+    out[t] = row;
+    oid[t] = (int)ix.ids[row];
   }
 }
 
