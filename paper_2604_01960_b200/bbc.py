@@ -78,6 +78,7 @@ def lib() -> ctypes.CDLL:
         L.bbc_search_group.argtypes = [ctypes.POINTER(vp), ctypes.c_int, vp, i64, i32, i32, i64, vp,
                                        vp, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_size_t), vp]
         L.bbc_set_timing.argtypes = [vp, ctypes.c_int]
+        L.bbc_set_probe_mode.argtypes = [vp, i32]
         L.bbc_get_timing.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int,
                                      ctypes.POINTER(ctypes.c_int64)]
         L.bbc_last_stats.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64),
@@ -261,6 +262,13 @@ class Index:
         _check(lib().bbc_comm_init(self._h, buf, rank, world))
 
     # ------------------------------------------------------------------ instrumentation
+    PROBE_SIMT, PROBE_TENSOR = 0, 1
+
+    def set_probe_mode(self, mode: int) -> None:
+        """Step a1 on the CUDA cores (canonical d^2 everywhere, PROBE_SIMT) or the tensor-core
+        shortlist + canonical re-score (PROBE_TENSOR, default for d <= 1024)."""
+        _check(lib().bbc_set_probe_mode(self._h, int(mode)))
+
     def set_timing(self, on: bool) -> None:
         _check(lib().bbc_set_timing(self._h, int(on)))
 

@@ -13,6 +13,7 @@
 #include <nccl.h>
 
 #include "bbc_dist.cuh"
+#include "bbc_probe_tc.cuh"
 
 using namespace bbc;
 
@@ -57,6 +58,10 @@ struct bbc_index_s {
   long long* stats = nullptr;           // [4]
   uint8_t* codes_t = nullptr;           // PQ codes, per-list chunk-major (replicated-LUT scan)
   long long* tbase = nullptr;           // [nlist] byte offset of each list in codes_t
+  float* cmu = nullptr;                 // [d] centroid mean (tensor-core probe)
+  float* cnorm = nullptr;               // [nlist] |c - mu|^2
+  float cmax = 0.f;                     // max |c - mu|, rounded up
+  int probe_tc = 0;                     // 1: tensor-core shortlist probe (bbc_probe_tc.cuh)
   bool broken = false;
   bool timing = false;
   std::vector<Timer> timers;
@@ -93,6 +98,7 @@ Dev dev_view(const bbc_index_s* ix) {
   v.centroids = ix->centroids; v.loff = ix->loff; v.gsize = ix->gsize_d; v.ids = ix->ids;
   v.books = ix->books; v.codes = ix->codes; v.P = ix->P; v.wL = ix->wL; v.bits = ix->bits;
   v.factors = ix->factors; v.raw = ix->raw;
+  v.cmu = ix->cmu; v.cnorm = ix->cnorm; v.cmax = ix->cmax; v.probe_tc = ix->probe_tc;
   return v;
 }
 
@@ -309,8 +315,15 @@ struct Shard {
 void stage_probe(Shard& s, cudaStream_t st) {
   bbc_index_s* ix = s.ix;
   StageScope sc(ix, st, BBC_STAGE_PROBE);
-  dim3 g1((ix->nlist + kPT - 1) / kPT, (s.b.nq + kPT - 1) / kPT);
-  k_probe_d2<<<g1, 256, 0, st>>>(s.b.Q, ix->centroids, s.b.coarse, s.b.nq, ix->nlist, ix->d);
+  if (ix->probe_tc) {
+    const dim3 gt((ix->nlist + kTcN - 1) / kTcN, (s.b.nq + kTcM - 1) / kTcM);
+    set_smem(k_probe_mma, kTcSmem);
+    k_probe_mma<<<gt, kTcNT, kTcSmem, st>>>(s.b.Q, ix->centroids, ix->cmu, ix->cnorm, s.b.coarse,
+                                            s.b.nq, ix->nlist, ix->d);
+  } else {
+    dim3 g1((ix->nlist + kPT - 1) / kPT, (s.b.nq + kPT - 1) / kPT);
+    k_probe_d2<<<g1, 256, 0, st>>>(s.b.Q, ix->centroids, s.b.coarse, s.b.nq, ix->nlist, ix->d);
+  }
   k_probe_select<<<s.b.nq, kSelNT, 0, st>>>(s.b, s.dv);
   g_launches += 2;
 }
@@ -810,6 +823,31 @@ bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_
   }
   ok = ok && upload_rows(9, rowraw, &ix->raw);
   ok = ok && dalloc((void**)&ix->stats, 4 * sizeof(long long));
+  if (ok) {
+    // centroid mean, |c - mu|^2 and max |c - mu| for the tensor-core probe's error bound
+    std::vector<float> C((size_t)nlist * d);
+    ok = cudaMemcpy(C.data(), ix->centroids, C.size() * 4, cudaMemcpyDeviceToHost) == cudaSuccess;
+    std::vector<double> mud(d, 0.0);
+    for (int c = 0; c < nlist; ++c)
+      for (int t = 0; t < d; ++t) mud[t] += C[(size_t)c * d + t];
+    std::vector<float> mu(d), cn(nlist);
+    for (int t = 0; t < d; ++t) mu[t] = (float)(mud[t] / nlist);
+    double mx = 0.0;
+    for (int c = 0; c < nlist; ++c) {
+      double a = 0.0;
+      for (int t = 0; t < d; ++t) {
+        const double y = (double)(C[(size_t)c * d + t] - mu[t]);
+        a += y * y;
+      }
+      cn[c] = (float)a;
+      mx = std::max(mx, a);
+    }
+    ix->cmax = (float)(std::sqrt(mx) * (1.0 + 1e-6));
+    ok = ok && dalloc((void**)&ix->cmu, (size_t)d * 4) && dalloc((void**)&ix->cnorm, (size_t)nlist * 4) &&
+         cudaMemcpy(ix->cmu, mu.data(), (size_t)d * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemcpy(ix->cnorm, cn.data(), (size_t)nlist * 4, cudaMemcpyHostToDevice) == cudaSuccess;
+    ix->probe_tc = d <= kMaxDimTc ? 1 : 0;
+  }
   cudaDeviceGetAttribute(&ix->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
   if (ok && kind == BBC_KIND_PQ) {
     // chunk-major copy of the codes for the replicated-LUT scan (layout: k_transpose_codes)
@@ -843,13 +881,22 @@ void ivf_free(bbc_index ix) {
   if (!ix) return;
   cudaSetDevice(ix->device);
   void* ptrs[] = {ix->centroids, ix->loff, ix->gsize_d, ix->ids, ix->books, ix->codes, ix->P,
-                  ix->wL, ix->bits, ix->factors, ix->raw, ix->stats, ix->codes_t, ix->tbase};
+                  ix->wL, ix->bits, ix->factors, ix->raw, ix->stats, ix->codes_t, ix->tbase,
+                  ix->cmu, ix->cnorm};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& t : ix->timers) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
   if (ix->nccl) ncclCommDestroy((ncclComm_t)ix->nccl);
   for (auto e : ix->pool) cudaEventDestroy(e);
   delete ix;
+}
+
+bbc_status bbc_set_probe_mode(bbc_index ix, int32_t mode) {
+  if (!ix) return fail(BBC_ERR_ARG, "null index");
+  if (mode != BBC_PROBE_SIMT && mode != BBC_PROBE_TENSOR) return fail(BBC_ERR_ARG, "unknown probe mode");
+  if (mode == BBC_PROBE_TENSOR && ix->d > kMaxDimTc) return fail(BBC_ERR_ARG, "d too large for the tensor-core probe");
+  ix->probe_tc = mode == BBC_PROBE_TENSOR ? 1 : 0;
+  return BBC_OK;
 }
 
 bbc_status bbc_index_info(bbc_index ix, bbc_index_info_t* info) {

@@ -55,6 +55,11 @@ struct Dev {
   const uint8_t* bits;           // [n_local x D/8]
   const float* factors;          // [n_local x 2]
   const void* raw;               // [n_local x d] f32 | u8
+  // tensor-core probe (bbc_probe_tc.cuh): centroid mean, |c - mu|^2, max |c - mu|
+  const float* cmu;              // [d]
+  const float* cnorm;            // [nlist]
+  float cmax;
+  int probe_tc;                  // 1: coarse holds d~ (shortlist mode of k_probe_select)
 };
 
 // ------------------------------------------------------------------------------------------
@@ -111,42 +116,119 @@ __global__ void __launch_bounds__(256) k_probe_d2(const float* __restrict__ Q,
 }
 
 // Per query: the nprobe smallest (d^2, list) keys, sorted; list offsets and the sample rule.
+//
+// ix.probe_tc == 0: coarse holds the canonical d^2 (k_probe_d2): radix select + sort.
+// ix.probe_tc == 1: coarse holds the tensor-core estimate d~ (k_probe_mma) with |d~ - d^2| <=
+//   E(q); the shortlist {d~ <= T~ + 2E} (T~ = nprobe-th smallest d~) provably holds the
+//   nprobe nearest lists (bbc_probe_tc.cuh); it is re-scored with the canonical d^2 and
+//   sorted, so the probe lists equal the SIMT path's.  A shortlist longer than kMaxShort falls
+//   back to canonical d^2 for every list.
 constexpr int kSelNT = 1024;
 constexpr int kMaxProbe = 2048;
-__global__ void __launch_bounds__(kSelNT) k_probe_select(Batch b, Dev ix) {
-  __shared__ SelectSmem sm;
-  __shared__ uint64_t keys[kMaxProbe];
-  __shared__ int s_count;
-  const int q = blockIdx.x;
-  const int nlist = ix.nlist, nprobe = b.nprobe;
-  const float* d2 = b.coarse + (size_t)q * nlist;
-  auto load = [&](int64_t i) -> uint64_t {
-    return ((uint64_t)f2key(d2[i]) << 32) | (uint32_t)i;
-  };
-  int pshift;
-  uint64_t pref = cta_select<kSelNT>(nlist, nprobe, load, false, &pshift, sm);
-  if (threadIdx.x == 0) s_count = 0;
-  int P2 = 1;
-  while (P2 < nprobe) P2 <<= 1;
-  for (int i = threadIdx.x; i < P2; i += kSelNT) keys[i] = ~0ull;
-  __syncthreads();
-  for (int i = threadIdx.x; i < nlist; i += kSelNT) {
-    uint64_t k = load(i);
-    if (shr64(k, pshift) <= pref) keys[atomicAdd(&s_count, 1)] = k;
+constexpr int kMaxShort = 4096;
+constexpr int kMaxDimTc = 1024;
+
+__device__ __forceinline__ float canonical_d2(const float* sq, const float* __restrict__ c, int d) {
+  float acc = 0.f;
+  for (int t = 0; t < d; ++t) {
+    const float df = __fsub_rn(sq[t], c[t]);
+    acc = __fadd_rn(acc, __fmul_rn(df, df));
   }
-  __syncthreads();
-  // bitonic sort of P2 keys
+  return acc;
+}
+
+__device__ __forceinline__ void bitonic_sort_keys(uint64_t* keys, int P2) {
   for (int size = 2; size <= P2; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       for (int i = threadIdx.x; i < P2 / 2; i += kSelNT) {
-        int lo = 2 * stride * (i / stride) + (i % stride);
-        int hi = lo + stride;
-        bool up = ((lo & size) == 0);
-        uint64_t a = keys[lo], c = keys[hi];
+        const int lo = 2 * stride * (i / stride) + (i % stride);
+        const int hi = lo + stride;
+        const bool up = ((lo & size) == 0);
+        const uint64_t a = keys[lo], c = keys[hi];
         if ((a > c) == up) { keys[lo] = c; keys[hi] = a; }
       }
       __syncthreads();
     }
+  }
+}
+
+__global__ void __launch_bounds__(kSelNT) k_probe_select(Batch b, Dev ix) {
+  __shared__ SelectSmem sm;
+  __shared__ uint64_t keys[kMaxShort];
+  __shared__ float s_q[kMaxDimTc];
+  __shared__ int s_count;
+  __shared__ float s_red[kSelNT / 32];
+  const int q = blockIdx.x;
+  const int nlist = ix.nlist, nprobe = b.nprobe, d = ix.d;
+  float* d2 = b.coarse + (size_t)q * nlist;
+  auto load = [&](int64_t i) -> uint64_t {
+    return ((uint64_t)f2key(d2[i]) << 32) | (uint32_t)i;
+  };
+  bool sorted = false;
+  if (ix.probe_tc) {
+    // |q - mu|^2 (any order: only the error bound uses it)
+    float part = 0.f;
+    for (int t = threadIdx.x; t < d; t += kSelNT) {
+      const float x = b.Q[(size_t)q * d + t];
+      s_q[t] = x;
+      const float y = x - ix.cmu[t];
+      part = fmaf(y, y, part);
+    }
+    part = warp_sum(part);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = part;
+    if (threadIdx.x == 0) s_count = 0;
+    __syncthreads();
+    float qn = 0.f;
+    for (int w = 0; w < kSelNT / 32; ++w) qn += s_red[w];
+    qn *= 1.0f + 0x1p-10f;                          // margin for this sum's own rounding
+    const float E = 0x1p-12f * sqrtf(qn) * ix.cmax + 0x1p-11f * (qn + ix.cmax * ix.cmax);
+    auto load32 = [&](int64_t i) -> uint64_t { return (uint64_t)f2key(d2[i]); };
+    int ps;
+    const float T = key2f((uint32_t)cta_select<kSelNT>(nlist, nprobe, load32, true, &ps, sm));
+    float thr = T + 2.0f * E;
+    thr = thr + fabsf(thr) * 0x1p-20f + 0x1p-100f;  // round the threshold up
+    for (int i = threadIdx.x; i < nlist; i += kSelNT)
+      if (d2[i] <= thr) {
+        const int at = atomicAdd(&s_count, 1);
+        if (at < kMaxShort) keys[at] = (uint64_t)i;
+      }
+    __syncthreads();
+    const int cnt = s_count;
+    if (cnt <= kMaxShort) {
+      int P2 = 1;
+      while (P2 < cnt) P2 <<= 1;
+      for (int i = threadIdx.x; i < P2; i += kSelNT) {
+        if (i < cnt) {
+          const int j = (int)keys[i];
+          const float e = canonical_d2(s_q, ix.centroids + (size_t)j * d, d);
+          keys[i] = ((uint64_t)f2key(e) << 32) | (uint32_t)j;
+        } else {
+          keys[i] = ~0ull;
+        }
+      }
+      __syncthreads();
+      bitonic_sort_keys(keys, P2);
+      sorted = true;
+    } else {
+      for (int i = threadIdx.x; i < nlist; i += kSelNT)   // fallback: canonical d^2 everywhere
+        d2[i] = canonical_d2(s_q, ix.centroids + (size_t)i * d, d);
+      __syncthreads();
+    }
+  }
+  if (!sorted) {
+    int pshift;
+    uint64_t pref = cta_select<kSelNT>(nlist, nprobe, load, false, &pshift, sm);
+    if (threadIdx.x == 0) s_count = 0;
+    int P2 = 1;
+    while (P2 < nprobe) P2 <<= 1;
+    for (int i = threadIdx.x; i < P2; i += kSelNT) keys[i] = ~0ull;
+    __syncthreads();
+    for (int i = threadIdx.x; i < nlist; i += kSelNT) {
+      uint64_t k = load(i);
+      if (shr64(k, pshift) <= pref) keys[atomicAdd(&s_count, 1)] = k;
+    }
+    __syncthreads();
+    bitonic_sort_keys(keys, P2);
   }
   // write probes; prefix over local and global sizes
   int* pr = b.probe + (size_t)q * nprobe;

@@ -249,3 +249,41 @@ def test_nccl_path_world1_equals_single():
     a = _sorted_by_id(a_ids.cpu().numpy(), a_d2.cpu().numpy())
     b = _sorted_by_id(b_ids.cpu().numpy(), b_d2.cpu().numpy())
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("name", ["C1t", "C2s", "C3s", "C4s", "C5s"])
+def test_probe_modes_identical(name):
+    """Tensor-core shortlist probe (default) and the SIMT canonical probe give the same probe
+    lists, rq2 and results, and both equal the oracle's probe (a1)."""
+    from oracle import bbc_oracle as O
+    cfg, ix, Q, g = gpu_index(name)
+    q = torch.from_numpy(Q).cuda()
+    outs = {}
+    for mode in (g.PROBE_SIMT, g.PROBE_TENSOR):
+        g.set_probe_mode(mode)
+        ids, d2, t = g.search_debug(q, cfg.k, cfg.nprobe, cfg.budget)
+        torch.cuda.synchronize()
+        outs[mode] = (ids.cpu().numpy(), d2.cpu().numpy(), t["probe"].cpu().numpy(),
+                      t["rq2"].cpu().numpy())
+    g.set_probe_mode(g.PROBE_TENSOR)
+    a, b = outs[g.PROBE_SIMT], outs[g.PROBE_TENSOR]
+    for x, y in zip(a, b):
+        assert np.array_equal(x.view(np.uint8), y.view(np.uint8))
+    lists, rq = O.probe(Q, np.asarray(ix["centroids"]), cfg.nprobe)
+    assert np.array_equal(b[2], lists)
+    assert np.array_equal(b[3].view(np.uint32), np.asarray(rq, dtype=np.float32).view(np.uint32))
+
+
+def test_probe_tensor_large_nprobe_and_ties():
+    """Tensor-core probe at nprobe = nlist (every list shortlisted) and with duplicated queries."""
+    cfg, ix, Q, g = gpu_index("C2s")
+    Q2 = np.ascontiguousarray(np.concatenate([Q[:4], Q[:4]]))
+    q = torch.from_numpy(Q2).cuda()
+    res = []
+    for mode in (g.PROBE_SIMT, g.PROBE_TENSOR):
+        g.set_probe_mode(mode)
+        _, _, t = g.search_debug(q, cfg.k, cfg.nlist, cfg.budget)
+        torch.cuda.synchronize()
+        res.append(t["probe"].cpu().numpy())
+    g.set_probe_mode(g.PROBE_TENSOR)
+    assert np.array_equal(res[0], res[1])
