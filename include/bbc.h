@@ -231,6 +231,10 @@ bbc_status bbc_last_stats(bbc_index index, int64_t* probed, int64_t* candidates,
 /* Same, plus the number of sample objects estimated in step a3 (summed over queries). */
 bbc_status bbc_last_stats2(bbc_index index, int64_t* probed, int64_t* candidates,
                            int64_t* microbatches, int64_t* sampled);
+/* Counters of the last search, in order: probed objects, candidates |S*|, sample objects,
+ * lists shortlisted by the tensor-core probe (0 in SIMT mode), micro-batches.  Copies the first
+ * n (<= 5) into out (host memory).  BBC_ERR_ARG for a null index or out with n > 0. */
+bbc_status bbc_stats_vector(bbc_index index, int64_t* out, int32_t n);
 
 /* Number of CUDA kernels this library has launched in this process. */
 int64_t bbc_launch_count(void);

@@ -79,6 +79,7 @@ def lib() -> ctypes.CDLL:
                                        vp, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_size_t), vp]
         L.bbc_set_timing.argtypes = [vp, ctypes.c_int]
         L.bbc_set_probe_mode.argtypes = [vp, i32]
+        L.bbc_stats_vector.argtypes = [vp, ctypes.POINTER(i64), i32]
         L.bbc_get_timing.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int,
                                      ctypes.POINTER(ctypes.c_int64)]
         L.bbc_last_stats.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64),
@@ -282,4 +283,7 @@ class Index:
         a, b, c, d = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         _check(lib().bbc_last_stats2(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
                                      ctypes.byref(d)))
-        return dict(probed=a.value, candidates=b.value, microbatches=c.value, sampled=d.value)
+        v = (ctypes.c_int64 * 5)()
+        _check(lib().bbc_stats_vector(self._h, v, 5))
+        return dict(probed=a.value, candidates=b.value, microbatches=c.value, sampled=d.value,
+                    shortlisted=v[3])

@@ -1034,4 +1034,13 @@ bbc_status bbc_last_stats2(bbc_index ix, int64_t* probed, int64_t* candidates, i
   return BBC_OK;
 }
 
+bbc_status bbc_stats_vector(bbc_index ix, int64_t* out, int32_t n) {
+  if (!ix || (!out && n > 0) || n < 0) return fail(BBC_ERR_ARG, "bad argument");
+  long long h[4];
+  CU(cudaMemcpy(h, ix->stats, sizeof(h), cudaMemcpyDeviceToHost));
+  const long long v[5] = {h[0], h[1], h[2], h[3], ix->microbatches};
+  for (int i = 0; i < n && i < 5; ++i) out[i] = v[i];
+  return BBC_OK;
+}
+
 }  // extern "C"

@@ -14,8 +14,8 @@
 //      canonical fp32 d^2 and the nprobe smallest (d^2, list) keys are selected exactly as the
 //      SIMT path does: the probe lists are identical by construction.
 //
-// Kernel shape: CTA = 128 queries x 256 centroids (one UMMA 128x256 accumulator, 256 TMEM
-// columns), K in chunks of 32 (tf32 MMA K = 8, four MMAs x three split products per chunk).
+// Kernel shape: CTA = 128 queries x 128 centroids (one UMMA 128x128 accumulator, 128 TMEM
+// columns; up to 3 CTAs per SM), K in chunks of 32 (tf32 MMA K = 8, four MMAs x three split products per chunk).
 // Operands are staged by the CTA's threads (split into hi/lo while staging) in the canonical
 // K-major no-swizzle layout: 8-row x 16-byte core matrices, LBO = 128 B between K-adjacent core
 // matrices, SBO = 1 KB between 8-row groups.  One elected thread issues the MMAs; completion is
@@ -25,7 +25,7 @@
 
 namespace bbc {
 
-constexpr int kTcM = 128, kTcN = 256, kTcKC = 32, kTcNT = 128;
+constexpr int kTcM = 128, kTcN = 128, kTcKC = 32, kTcNT = 128;
 constexpr int kTcSboBytes = (kTcKC / 4) * 128;                // 1 KB per 8-row group
 constexpr int kTcABytes = kTcM * kTcKC * 4;                     // 16 KB
 constexpr int kTcBBytes = kTcN * kTcKC * 4;                     // 32 KB
@@ -40,7 +40,7 @@ __device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr) {
   return d;                                                     // base offset 0, SWIZZLE_NONE
 }
 
-// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = 256
+// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = kTcN
 constexpr uint32_t kTcIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kTcN >> 3) << 17) |
                               ((uint32_t)(kTcM >> 4) << 24);
 
@@ -87,7 +87,7 @@ __device__ __forceinline__ void tc_stage(const float* __restrict__ X, int nrows,
   }
 }
 
-// coarse[q][c] = d~(q, c) for the CTA's 128 x 256 tile.  cnorm[c] = |c - mu|^2.
+// coarse[q][c] = d~(q, c) for the CTA's 128 x kTcN tile.  cnorm[c] = |c - mu|^2.
 __global__ void __launch_bounds__(kTcNT) k_probe_mma(const float* __restrict__ Q, const float* __restrict__ C,
                                                      const float* __restrict__ mu,
                                                      const float* __restrict__ cnorm,
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kTcNT) k_probe_mma(const float* __restrict__ Q
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 0) {                                              // 256 TMEM columns (fp32 128x256)
+  if (warp == 0) {                                              // kTcN TMEM columns (fp32 128 x kTcN)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                  ::"r"(smem_u32(tmem_slot)), "r"(kTcN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");

@@ -46,5 +46,7 @@ for _ in range(a.steps):
     tot += e0.elapsed_time(e1)
 g.set_timing(False)
 st, _ = g.get_timing()
+stats = g.last_stats()
 print(json.dumps({"tag": a.tag, "workload": a.workload, "ms_per_step": tot / a.steps,
-                  **{k: round(v / a.steps, 4) for k, v in st.items()}}), flush=True)
+                  **{k: round(v / a.steps, 4) for k, v in st.items()},
+                  **{k: v / len(q) for k, v in stats.items() if k != "microbatches"}}), flush=True)
