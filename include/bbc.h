@@ -100,6 +100,21 @@ bbc_status bbc_index_info(bbc_index index, bbc_index_info_t* info);
 bbc_status bbc_set_probe_mode(bbc_index index, int32_t mode);
 
 /*
+ * bbc_set_scan_mode -- how steps a3/a4 compute RaBitQ estimated distances (B_q = 4, P:L1440;
+ * estimator DESIGN.md 2.2).  Both modes give bit-identical estimates (the code/query inner
+ * product is an exact integer either way).  PQ indexes ignore the mode (replicated-LUT scan).
+ *   BBC_SCAN_SIMT   : per (query, list) CTA, 4 popcounts per 32 code bits.
+ *   BBC_SCAN_TENSOR : (default, D <= 1024) list-major: the codes of a list times the 4-bit
+ *                     query codes of every query probing it, one integer GEMM on the tensor
+ *                     cores (tcgen05 kind::i8) per 128-object tile.
+ * Errors: BBC_ERR_ARG for a null index, an unknown mode, or TENSOR on a RaBitQ index with
+ * D > 1024.  Must not change while a search on the handle is in flight.
+ */
+#define BBC_SCAN_SIMT 0
+#define BBC_SCAN_TENSOR 1
+bbc_status bbc_set_scan_mode(bbc_index index, int32_t mode);
+
+/*
  * bbc_workspace_size -- bytes of device workspace bbc_search needs for (nq, k, nprobe, budget).
  * The workspace holds per-query scratch sized for the nprobe largest lists (cell ids, candidate
  * rows and distances) plus query/output staging used by bbc_search_host.  Queries are processed

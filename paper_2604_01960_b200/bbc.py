@@ -79,6 +79,7 @@ def lib() -> ctypes.CDLL:
                                        vp, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_size_t), vp]
         L.bbc_set_timing.argtypes = [vp, ctypes.c_int]
         L.bbc_set_probe_mode.argtypes = [vp, i32]
+        L.bbc_set_scan_mode.argtypes = [vp, i32]
         L.bbc_stats_vector.argtypes = [vp, ctypes.POINTER(i64), i32]
         L.bbc_get_timing.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int,
                                      ctypes.POINTER(ctypes.c_int64)]
@@ -269,6 +270,13 @@ class Index:
         """Step a1 on the CUDA cores (canonical d^2 everywhere, PROBE_SIMT) or the tensor-core
         shortlist + canonical re-score (PROBE_TENSOR, default for d <= 1024)."""
         _check(lib().bbc_set_probe_mode(self._h, int(mode)))
+
+    SCAN_SIMT, SCAN_TENSOR = 0, 1
+
+    def set_scan_mode(self, mode: int) -> None:
+        """RaBitQ estimates with popcounts per (query, list) (SCAN_SIMT) or as list-major integer
+        GEMMs on the tensor cores (SCAN_TENSOR, default); PQ indexes ignore it."""
+        _check(lib().bbc_set_scan_mode(self._h, int(mode)))
 
     def set_timing(self, on: bool) -> None:
         _check(lib().bbc_set_timing(self._h, int(on)))

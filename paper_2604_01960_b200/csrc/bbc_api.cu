@@ -14,6 +14,7 @@
 
 #include "bbc_dist.cuh"
 #include "bbc_probe_tc.cuh"
+#include "bbc_rbq_tc.cuh"
 
 using namespace bbc;
 
@@ -62,6 +63,10 @@ struct bbc_index_s {
   float* cnorm = nullptr;               // [nlist] |c - mu|^2
   float cmax = 0.f;                     // max |c - mu|, rounded up
   int probe_tc = 0;                     // 1: tensor-core shortlist probe (bbc_probe_tc.cuh)
+  int rbq_tc = 0;                       // 1: RaBitQ estimates on the tensor cores (bbc_rbq_tc.cuh)
+  int2* rbq_tiles = nullptr;            // [rbq_ntiles] (list, first object) of 128-object tiles
+  int rbq_ntiles = 0;
+  int* rbq_pc = nullptr;                // [n_local] popcount of each code
   bool broken = false;
   bool timing = false;
   std::vector<Timer> timers;
@@ -134,6 +139,15 @@ struct StageScope {
   }
 };
 
+struct RbqBufs {
+  uint8_t* qbar = nullptr;
+  float4* pairc = nullptr;
+  int* inv = nullptr;
+  int* inv_cnt = nullptr;
+  int* inv_off = nullptr;
+  int* inv_cur = nullptr;
+};
+
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Plan {
@@ -154,12 +168,17 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1) {
                 (size_t)((cap + kChunk - 1) / kChunk) * 8 + (size_t)(nprobe + 1) * 4;
   p.per_query += 8 + 8 + kCells * 4 + 4 + 4 + (size_t)4 * world;   // DistBuf
   p.fixed = 64 * 256;
+  if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) {            // pair codes + inverted index
+    p.per_query += (size_t)nprobe * ((size_t)ix->D + 16 + 4) + 3 * 256;
+    p.fixed += (size_t)3 * (ix->nlist + 1) * 4 + 3 * 256;
+  }
   return p;
 }
 
 // Carve the micro-batch arrays out of the workspace.
 void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, Batch& b,
-           float** qstage, long long** ostage_ids, float** ostage_d2, int k, DistBuf* db, int world) {
+           float** qstage, long long** ostage_ids, float** ostage_d2, int k, DistBuf* db, int world,
+           RbqBufs* rb) {
   size_t off = 0;
   auto take = [&](size_t bytes) {
     char* r = ws + off;
@@ -195,6 +214,15 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, 
   db->umin = (unsigned*)take((size_t)nqb * 4);
   db->tot = (int*)take((size_t)nqb * 4);
   db->cnt = (int*)take((size_t)nqb * world * 4);
+  if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) {
+    const size_t pairs = (size_t)nqb * nprobe;
+    rb->qbar = (uint8_t*)take(pairs * ix->D);
+    rb->pairc = (float4*)take(pairs * 16);
+    rb->inv = (int*)take(pairs * 4);
+    rb->inv_cnt = (int*)take((size_t)(ix->nlist + 1) * 4);
+    rb->inv_off = (int*)take((size_t)(ix->nlist + 1) * 4);
+    rb->inv_cur = (int*)take((size_t)(ix->nlist + 1) * 4);
+  }
 }
 
 template <typename Kern>
@@ -298,6 +326,7 @@ struct NcclComm : Comm {
 };
 
 struct Shard {
+  RbqBufs rb;
   bbc_index_s* ix;
   char* ws;
   size_t ws_bytes;
@@ -336,6 +365,36 @@ void stage_tables(Shard& s, cudaStream_t st) {
   else
     k_rbq_rotate<<<dim3((ix->D + 255) / 256, s.b.nq), 256, (size_t)ix->d * 4, st>>>(s.b, s.dv);
   g_launches += 1;
+  if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) {
+    const long long pairs = (long long)s.b.nq * s.b.nprobe;
+    if (pairs > 0) {
+      k_rbq_pairs<<<(unsigned)((pairs + 7) / 8), 256, 0, st>>>(s.b, s.dv, s.rb.qbar, s.rb.pairc);
+      g_launches += 1;
+    }
+  }
+}
+
+// RaBitQ tensor-core pass over the selected (query, list) pairs: inverted index + list-major GEMM
+void rbq_tc_pass(Shard& s, const Batch& b, cudaStream_t st, bool sample) {
+  bbc_index_s* ix = s.ix;
+  const long long pairs = (long long)b.nq * b.nprobe;
+  if (pairs == 0 || ix->rbq_ntiles == 0) return;
+  const unsigned gp = (unsigned)((pairs + 255) / 256);
+  cudaMemsetAsync(s.rb.inv_cnt, 0, (size_t)(ix->nlist + 1) * 4, st);
+  k_inv_count<<<gp, 256, 0, st>>>(b, s.dv, s.rb.inv_cnt, sample ? 1 : 0);
+  k_inv_scan<<<1, 1024, 0, st>>>(s.rb.inv_cnt, s.rb.inv_off, s.rb.inv_cur, ix->nlist);
+  k_inv_fill<<<gp, 256, 0, st>>>(b, s.dv, s.rb.inv_cur, s.rb.inv, sample ? 1 : 0);
+  RbqTc t{s.rb.qbar, s.rb.pairc, s.rb.inv_off, s.rb.inv, ix->rbq_tiles, ix->rbq_pc};
+  const size_t sm = (size_t)(kRbM + kRbN) * ix->D + (size_t)kRbN * 64 * 4 + kRbN * sizeof(RbqPair) +
+                    3 * kRbM * 4 + 64;
+  if (sample) {
+    set_smem(k_rbq_mma<true>, sm);
+    k_rbq_mma<true><<<ix->rbq_ntiles, kRbNT, sm, st>>>(b, s.dv, t);
+  } else {
+    set_smem(k_rbq_mma<false>, sm);
+    k_rbq_mma<false><<<ix->rbq_ntiles, kRbNT, sm, st>>>(b, s.dv, t);
+  }
+  g_launches += 4;
 }
 
 int rq_grid(const Shard& s) { return (int)((s.p.cap + 32LL * s.b.nprobe + kRqE - 1) / kRqE); }
@@ -346,6 +405,8 @@ void stage_sample_est(Shard& s, cudaStream_t st) {
   StageScope sc(ix, st, BBC_STAGE_SAMPLE);
   if (ix->kind == BBC_KIND_PQ) {
     rq_scan(ix->M, true, dim3(rq_grid(s), s.b.nq), st, s.b, s.dv, ix->codes_t, ix->tbase, s.b.val, s.p.cap, 0);
+  } else if (ix->rbq_tc) {
+    rbq_tc_pass(s, s.b, st, true);
   } else {
     const size_t sm = (size_t)ix->D * 4 + 4 * (ix->D / 32) * 4;
     set_smem(k_rbq_scan<true>, sm);
@@ -363,6 +424,8 @@ void stage_scan(Shard& s, cudaStream_t st) {
     k_sample_cells<<<dim3(8, nb), 256, 0, st>>>(s.b);
     rq_scan(ix->M, false, dim3(rq_grid(s), nb), st, s.b, s.dv, ix->codes_t, ix->tbase, nullptr, 0, 1);
     g_launches += 2;
+  } else if (ix->rbq_tc) {
+    rbq_tc_pass(s, s.b, st, false);
   } else {
     const int cta_per_q = std::max(1, std::min(nprobe, (3 * 148 * 6 + nb - 1) / nb));
     const int Gf = (nprobe + cta_per_q - 1) / cta_per_q;
@@ -538,7 +601,7 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
   for (long long q0 = 0; q0 < nq; q0 += nqb) {
     const int nb = (int)std::min<long long>(nqb, nq - q0);
     for (auto& s : sh) {
-      carve(s.ix, s.p, nb, nprobe, s.ws, s.b, &s.qstage, &s.oids, &s.od2, k, &s.db, W);
+      carve(s.ix, s.p, nb, nprobe, s.ws, s.b, &s.qstage, &s.oids, &s.od2, k, &s.db, W, &s.rb);
       Batch& b = s.b;
       b.nq = nb; b.nprobe = nprobe; b.k = k; b.budget = budget_c; b.cap = s.p.cap;
       b.stats = s.ix->stats;
@@ -624,8 +687,12 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
           CU(cudaMemcpyAsync(ns_all, all.data(), (size_t)nb * 4, cudaMemcpyHostToDevice, st));
           CU(cudaStreamSynchronize(st));
           b2.nsamp = ns_all;
-          const size_t sm = (size_t)ix->D * 4 + 4 * (ix->D / 32) * 4;
-          k_rbq_scan<true><<<dim3(std::min(nprobe, 64), nb), kScanNT, sm, st>>>(b2, s0.dv, 1);
+          if (ix->rbq_tc) {
+            rbq_tc_pass(s0, b2, st, true);
+          } else {
+            const size_t sm = (size_t)ix->D * 4 + 4 * (ix->D / 32) * 4;
+            k_rbq_scan<true><<<dim3(std::min(nprobe, 64), nb), kScanNT, sm, st>>>(b2, s0.dv, 1);
+          }
         }
         g_launches += 1;
         CU(cudaGetLastError());
@@ -848,6 +915,20 @@ bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_
          cudaMemcpy(ix->cnorm, cn.data(), (size_t)nlist * 4, cudaMemcpyHostToDevice) == cudaSuccess;
     ix->probe_tc = d <= kMaxDimTc ? 1 : 0;
   }
+  if (ok && kind == BBC_KIND_RABITQ && D <= 1024 && D % 32 == 0) {
+    std::vector<int2> tiles;
+    for (int L = 0; L < nlist; ++L)
+      for (int o = 0; o < ix->lsize[L]; o += kRbM) tiles.push_back(make_int2(L, o));
+    ix->rbq_ntiles = (int)tiles.size();
+    ok = dalloc((void**)&ix->rbq_pc, (size_t)std::max<long long>(1, ix->n_local) * 4) &&
+         dalloc((void**)&ix->rbq_tiles, (size_t)std::max<size_t>(1, tiles.size()) * 8) &&
+         cudaMemcpy(ix->rbq_tiles, tiles.data(), tiles.size() * 8, cudaMemcpyHostToDevice) == cudaSuccess;
+    if (ok && ix->n_local > 0) {
+      k_rbq_popc<<<(unsigned)((ix->n_local + 255) / 256), 256>>>(ix->bits, ix->n_local, D, ix->rbq_pc);
+      ok = cudaDeviceSynchronize() == cudaSuccess;
+    }
+    ix->rbq_tc = ok ? 1 : 0;
+  }
   cudaDeviceGetAttribute(&ix->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
   if (ok && kind == BBC_KIND_PQ) {
     // chunk-major copy of the codes for the replicated-LUT scan (layout: k_transpose_codes)
@@ -882,7 +963,7 @@ void ivf_free(bbc_index ix) {
   cudaSetDevice(ix->device);
   void* ptrs[] = {ix->centroids, ix->loff, ix->gsize_d, ix->ids, ix->books, ix->codes, ix->P,
                   ix->wL, ix->bits, ix->factors, ix->raw, ix->stats, ix->codes_t, ix->tbase,
-                  ix->cmu, ix->cnorm};
+                  ix->cmu, ix->cnorm, ix->rbq_tiles, ix->rbq_pc};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& t : ix->timers) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
@@ -896,6 +977,15 @@ bbc_status bbc_set_probe_mode(bbc_index ix, int32_t mode) {
   if (mode != BBC_PROBE_SIMT && mode != BBC_PROBE_TENSOR) return fail(BBC_ERR_ARG, "unknown probe mode");
   if (mode == BBC_PROBE_TENSOR && ix->d > kMaxDimTc) return fail(BBC_ERR_ARG, "d too large for the tensor-core probe");
   ix->probe_tc = mode == BBC_PROBE_TENSOR ? 1 : 0;
+  return BBC_OK;
+}
+
+bbc_status bbc_set_scan_mode(bbc_index ix, int32_t mode) {
+  if (!ix) return fail(BBC_ERR_ARG, "null index");
+  if (mode != BBC_SCAN_SIMT && mode != BBC_SCAN_TENSOR) return fail(BBC_ERR_ARG, "unknown scan mode");
+  if (mode == BBC_SCAN_TENSOR && ix->kind == BBC_KIND_RABITQ && !ix->rbq_pc)
+    return fail(BBC_ERR_ARG, "tensor-core RaBitQ scan unavailable for this index (D > 1024)");
+  ix->rbq_tc = (mode == BBC_SCAN_TENSOR && ix->kind == BBC_KIND_RABITQ) ? 1 : 0;
   return BBC_OK;
 }
 

@@ -1,0 +1,372 @@
+// a3/a4 RaBitQ estimated distances on the 5th-generation tensor cores (tcgen05, kind::i8).
+//
+// The RaBitQ estimator of object x in list L for query q needs ip = <bits_x, qbar_{q,L}>, the
+// inner product of x's 1-bit code with the 4-bit query code of the pair (q, L) (B_q = 4,
+// P:L1440).  The SIMT kernel (k_rbq_scan) forms it with 4 popcounts per 32 code
+// bits per pair, which is popcount-bound.  Here the work is regrouped list-major: for list L,
+// every query that probes it is gathered (inverted probe index), and
+//      IP[objects x queries] = bits[objects x D] . qbar[queries x D]^T
+// is one integer GEMM on the tensor cores (A = code bits expanded to bytes 0/1, B = 4-bit query
+// codes as bytes 0..15, exact int32 accumulation in TMEM).  ip is exact, so every estimate is
+// bit-identical to the SIMT kernel's (same fp32 expression tree afterwards).
+//
+//   k_rbq_pairs   : per (query, probed list): q' = (u - w_L)/r, v_l, Delta, qbar (bytes), s_q,
+//                   and (c1, c2, c3, r) -- the canonical per-pair part of the estimator.
+//   k_inv_*       : inverted probe index (list -> pairs), for the sample pass (j < nsamp) or
+//                   the Push pass (all j).
+//   k_rbq_mma     : CTA = (list L, tile of 128 objects); A (128 x D bytes) staged once, then
+//                   for each tile of 64 pairs: B (64 x D bytes) staged, D/32 MMAs (M=128, N=64,
+//                   K=32), epilogue in registers: estimate -> estimate (sample) or bucket id +
+//                   per-pair histogram in shared memory (Push).
+// Operand layout: canonical K-major, no swizzle: 8-row x 16-byte core matrices, LBO = 128 B
+// (K-adjacent), SBO = (D/16) x 128 B (8-row groups).
+#pragma once
+#include "bbc_probe_tc.cuh"
+
+namespace bbc {
+
+constexpr int kRbM = 128, kRbN = 64, kRbNT = 256;
+
+// ------------------------------------------------------------------ per-pair query codes
+// One warp per pair p = q * nprobe + j; lane handles dims lane + 32 m.
+__global__ void __launch_bounds__(256) k_rbq_pairs(Batch b, Dev ix, uint8_t* __restrict__ qbar,
+                                                   float4* __restrict__ pairc) {
+  const int lane = threadIdx.x & 31;
+  const long long p = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (p >= (long long)b.nq * b.nprobe) return;
+  const int q = (int)(p / b.nprobe);
+  const int D = ix.D;
+  const int L = b.probe[p];
+  const float rq2 = b.rq2[p];
+  const float r = __fsqrt_rn(rq2);
+  const float* u = b.table + (size_t)q * D;
+  const float* w = ix.wL + (size_t)L * D;
+  constexpr int kMaxM = 32;                           // D <= 1024
+  float qp[kMaxM];
+  float mn = INFINITY, mx = -INFINITY;
+#pragma unroll
+  for (int m = 0; m < kMaxM; ++m) {
+    const int i = lane + 32 * m;
+    if (i < D) {
+      const float v = r > 0.f ? __fdiv_rn(__fsub_rn(u[i], w[i]), r) : 0.f;
+      qp[m] = v;
+      mn = fminf(mn, v);
+      mx = fmaxf(mx, v);
+    }
+  }
+  mn = warp_min(mn);
+  mx = warp_max(mx);
+  const float delta = __fdiv_rn(__fsub_rn(mx, mn), 15.0f);
+  int sq = 0;
+  uint8_t* qb = qbar + (size_t)p * D;
+#pragma unroll
+  for (int m = 0; m < kMaxM; ++m) {
+    const int i = lane + 32 * m;
+    if (i < D) {
+      int v = 0;
+      if (delta > 0.f) {
+        const float t = floorf(__fadd_rn(__fdiv_rn(__fsub_rn(qp[m], mn), delta), 0.5f));
+        v = t < 0.f ? 0 : (t > 15.f ? 15 : (int)t);
+      }
+      qb[i] = (uint8_t)v;
+      sq += v;
+    }
+  }
+  sq = warp_sum(sq);
+  if (lane == 0) {
+    const float sD = __fsqrt_rn((float)D);
+    float4 c;
+    c.x = __fdiv_rn(__fmul_rn(2.0f, delta), sD);                                        // c1
+    c.y = __fdiv_rn(__fmul_rn(2.0f, mn), sD);                                           // c2
+    c.z = __fsub_rn(-__fdiv_rn(__fmul_rn(delta, (float)sq), sD), __fmul_rn(sD, mn));     // c3
+    c.w = r;
+    pairc[p] = c;
+  }
+}
+
+// ------------------------------------------------------------------ inverted probe index
+// Pairs selected for a pass: queries with a sample (nsamp > 0; otherwise tau = infinity and no
+// estimate is needed) and j < nsamp (SAMPLE) or j < nprobe (Push); lists empty on this shard
+// are skipped.
+__device__ __forceinline__ bool inv_selected(const Batch& b, const Dev& ix, long long p, bool sample,
+                                             int* L_out) {
+  const int q = (int)(p / b.nprobe), j = (int)(p % b.nprobe);
+  const int ns = b.nsamp[q];
+  if (ns == 0 || (sample && j >= ns)) return false;
+  const int L = b.probe[p];
+  if (ix.loff[L + 1] == ix.loff[L]) return false;
+  *L_out = L;
+  return true;
+}
+
+__global__ void k_inv_count(Batch b, Dev ix, int* cnt, int sample) {
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= (long long)b.nq * b.nprobe) return;
+  int L;
+  if (inv_selected(b, ix, p, sample != 0, &L)) atomicAdd(&cnt[L], 1);
+}
+
+// exclusive scan of cnt[nlist] -> off[nlist + 1]; cur = off (one CTA of 1024 threads)
+__global__ void __launch_bounds__(1024) k_inv_scan(const int* cnt, int* off, int* cur, int nlist) {
+  __shared__ int ws[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int base = 0; base < nlist; base += 1024) {
+    const int i = base + threadIdx.x;
+    const int v = i < nlist ? cnt[i] : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += t;
+    }
+    if (lane == 31) ws[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      const int s = ws[lane];
+      int y = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= o) y += t;
+      }
+      ws[lane] = y - s;
+    }
+    __syncthreads();
+    const int c0 = carry;
+    if (i < nlist) {
+      off[i] = c0 + ws[wid] + x - v;
+      cur[i] = off[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = c0 + ws[wid] + x;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) off[nlist] = carry;
+}
+
+__global__ void k_inv_fill(Batch b, Dev ix, int* cur, int* inv, int sample) {
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= (long long)b.nq * b.nprobe) return;
+  int L;
+  if (inv_selected(b, ix, p, sample != 0, &L)) inv[atomicAdd(&cur[L], 1)] = (int)p;
+}
+
+// Index-load-time: popcount of every code and the (list, 128-object tile) work list.
+__global__ void k_rbq_popc(const uint8_t* bits, long long n, int D, int* pc) {
+  const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(bits + r * (D / 8));
+  int s = 0;
+  for (int t = 0; t < D / 32; ++t) s += __popc(w[t]);
+  pc[r] = s;
+}
+
+// ------------------------------------------------------------------ the list-major GEMM
+struct RbqTc {
+  const uint8_t* qbar;   // [pairs x D]
+  const float4* pairc;   // [pairs] (c1, c2, c3, r)
+  const int* inv_off;    // [nlist + 1]
+  const int* inv;        // pair ids grouped by list
+  const int2* tiles;     // [ntiles] (list, first object)
+  const int* pc;         // [n_local] popcount of each code
+};
+
+struct RbqPair {
+  float c1, c2, c3, r, rq2;
+  CellFn cf;
+  long long obase;       // q * cap + poff[q][j] + first object of the tile
+  int q;
+};
+
+constexpr int kRbqIdesc = (2 << 4) | ((kRbN >> 3) << 17) | ((kRbM >> 4) << 24);   // s32 += u8 x u8
+
+__device__ __forceinline__ uint64_t umma_desc_k(uint32_t saddr, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)(128u >> 4) << 16;                  // LBO: K-adjacent core matrices
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;       // SBO: 8-row groups
+  d |= (uint64_t)1 << 46;                            // descriptor version (sm_100)
+  return d;
+}
+
+__device__ __forceinline__ void i8_mma(uint32_t tmem_d, uint64_t a, uint64_t bdesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
+      ::"r"(tmem_d), "l"(a), "l"(bdesc), "r"((uint32_t)kRbqIdesc), "r"(acc));
+}
+
+__device__ __forceinline__ uint32_t nib_bytes(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
+
+template <bool SAMPLE>
+__global__ void __launch_bounds__(kRbNT, 1) k_rbq_mma(Batch b, Dev ix, RbqTc t) {
+  extern __shared__ __align__(1024) uint8_t rsm2[];
+  const int D = ix.D;
+  const int sbo = (D / 16) * 128;
+  uint8_t* sA = rsm2;                                             // [128 x D] bytes
+  uint8_t* sB = sA + kRbM * D;                                    // [64 x D] bytes
+  uint32_t* hist = reinterpret_cast<uint32_t*>(sB + kRbN * D);    // [64 x 64] packed 4 x u8
+  RbqPair* pi = reinterpret_cast<RbqPair*>(hist + kRbN * 64);     // [64]
+  float* o_r = reinterpret_cast<float*>(pi + kRbN);               // [128] r_o
+  float* o_g = o_r + kRbM;                                        // [128] g_o
+  float* o_pc = o_g + kRbM;                                       // [128] popcount (float)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(o_pc + kRbM);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+
+  const int2 tile = t.tiles[blockIdx.x];
+  const int L = tile.x, o0 = tile.y;
+  const int p0 = t.inv_off[L], np = t.inv_off[L + 1] - p0;
+  if (np == 0) return;
+  const long long row0 = ix.loff[L] + o0;
+  const int nobj = min(kRbM, (int)(ix.loff[L + 1] - row0));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t bar_a = smem_u32(bar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(smem_u32(tslot)), "r"(kRbN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // A: code bits of the tile's objects -> bytes 0/1 in the K-major core-matrix layout
+  const int W = D / 32;
+  for (int idx = threadIdx.x; idx < kRbM * W; idx += kRbNT) {
+    const int r = idx / W, wv = idx % W;
+    uint32_t x = 0;
+    if (r < nobj) x = reinterpret_cast<const uint32_t*>(ix.bits + (size_t)(row0 + r) * (D / 8))[wv];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {                     // 16 bits -> one 16-byte core-matrix row
+      const uint32_t s16 = (x >> (16 * h)) & 0xFFFFu;
+      const uint4 v = make_uint4(nib_bytes(s16 & 15u), nib_bytes((s16 >> 4) & 15u),
+                                 nib_bytes((s16 >> 8) & 15u), nib_bytes(s16 >> 12));
+      const int kc = 2 * wv + h;                      // 16-dim chunk index
+      *reinterpret_cast<uint4*>(sA + (r >> 3) * sbo + kc * 128 + (r & 7) * 16) = v;
+    }
+  }
+  for (int r = threadIdx.x; r < kRbM; r += kRbNT) {
+    float fr = 0.f, fg = 1.f, fp = 0.f;
+    if (r < nobj) {
+      const float2 f = reinterpret_cast<const float2*>(ix.factors)[row0 + r];
+      fr = f.x; fg = f.y; fp = (float)t.pc[row0 + r];
+    }
+    o_r[r] = fr; o_g[r] = fg; o_pc[r] = fp;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+  const uint32_t aA = smem_u32(sA), aB = smem_u32(sB);
+  uint32_t phase = 0;
+  for (int qt = 0; qt < np; qt += kRbN) {
+    const int nqt = min(kRbN, np - qt);
+    // pair info and B (4-bit query codes as bytes)
+    for (int s = threadIdx.x; s < kRbN; s += kRbNT) {
+      if (s < nqt) {
+        const int p = t.inv[p0 + qt + s];
+        const int q = p / b.nprobe, j = p % b.nprobe;
+        const float4 c = t.pairc[p];
+        RbqPair e;
+        e.c1 = c.x; e.c2 = c.y; e.c3 = c.z; e.r = c.w;
+        e.rq2 = b.rq2[p];
+        if (!SAMPLE) e.cf.init(b.edges[2 * q], b.edges[2 * q + 1]);
+        e.obase = (long long)q * b.cap + b.poff[(size_t)q * (b.nprobe + 1) + j] + o0;
+        e.q = q;
+        pi[s] = e;
+      }
+    }
+    for (int idx = threadIdx.x; idx < kRbN * (D / 16); idx += kRbNT) {
+      const int s = idx / (D / 16), kc = idx % (D / 16);
+      uint4 v = make_uint4(0u, 0u, 0u, 0u);
+      if (s < nqt) {
+        const int p = t.inv[p0 + qt + s];
+        v = reinterpret_cast<const uint4*>(t.qbar + (size_t)p * D)[kc];
+      }
+      *reinterpret_cast<uint4*>(sB + (s >> 3) * sbo + kc * 128 + (s & 7) * 16) = v;
+    }
+    if (!SAMPLE)
+      for (int i = threadIdx.x; i < kRbN * 64; i += kRbNT) hist[i] = 0u;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      for (int s = 0; s < D / 32; ++s) {              // K = 32 bytes per MMA: 2 core matrices
+        const uint32_t o = (uint32_t)s * 256u;
+        i8_mma(tmem, umma_desc_k(aA + o, (uint32_t)sbo), umma_desc_k(aB + o, (uint32_t)sbo), s ? 1u : 0u);
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                   ::"r"(bar_a) : "memory");
+    }
+    mbar_wait(bar_a, phase);
+    phase ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // epilogue: warp w -> object rows 32 (w % 4) + lane, pair columns 32 (w / 4) .. + 31
+    {
+      const int r = 32 * (warp & 3) + lane;
+      const int cbase = 32 * (warp >> 2);
+      uint32_t v[32];
+      const uint32_t taddr = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)cbase;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+          "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+            "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+            "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+            "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (r < nobj) {
+        const float ro = o_r[r], go = o_g[r], pc = o_pc[r];
+        const float a = __fmul_rn(ro, ro);
+        const float ro2 = __fmul_rn(2.0f, ro);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const int s = cbase + c;
+          if (s >= nqt) continue;
+          const RbqPair& e = pi[s];
+          // canonical estimator, identical to k_rbq_scan
+          const float t1 = __fmul_rn(e.c2, pc);
+          const float t2 = __fadd_rn(t1, e.c3);
+          const float t3 = __fmul_rn(e.c1, (float)(int)v[c]);
+          const float oq = __fadd_rn(t3, t2);
+          const float ee = __fdiv_rn(oq, go);
+          const float sum = __fadd_rn(a, e.rq2);
+          const float ff = __fmul_rn(ro2, e.r);
+          const float est = __fsub_rn(sum, __fmul_rn(ff, ee));
+          if (SAMPLE) {
+            b.val[e.obase + r] = est;
+          } else {
+            const int cell = e.cf(est);
+            b.cells[e.obase + r] = (uint8_t)cell;
+            if (cell < 255) atomicAdd(&hist[s * 64 + (cell >> 2)], 1u << (8 * (cell & 3)));
+          }
+        }
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();                                  // TMEM and smem free for the next tile
+    if (!SAMPLE) {
+      for (int i = threadIdx.x; i < nqt * 64; i += kRbNT) {
+        const uint32_t h = hist[i];
+        if (!h) continue;
+        const int s = i >> 6, c4 = (i & 63) * 4;
+        int* gh = b.hist + (size_t)pi[s].q * kCells + c4;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t cnt = (h >> (8 * u)) & 255u;
+          if (cnt) atomicAdd(gh + u, (int)cnt);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kRbN));
+}
+
+}  // namespace bbc

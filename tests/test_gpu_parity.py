@@ -287,3 +287,30 @@ def test_probe_tensor_large_nprobe_and_ties():
         res.append(t["probe"].cpu().numpy())
     g.set_probe_mode(g.PROBE_TENSOR)
     assert np.array_equal(res[0], res[1])
+
+
+@pytest.mark.parametrize("nprobe_mult", [1, 4])
+def test_rabitq_scan_modes_identical(nprobe_mult):
+    """RaBitQ estimates from the list-major tensor-core GEMM (default) and from the popcount
+    kernel are bit-identical (exact integer code/query inner products), and so are every
+    downstream intermediate and the results."""
+    cfg, ix, Q, g = gpu_index("C3s")
+    q = torch.from_numpy(Q).cuda()
+    nprobe = min(cfg.nlist, cfg.nprobe * nprobe_mult)
+    outs = []
+    for mode in (g.SCAN_SIMT, g.SCAN_TENSOR):
+        g.set_scan_mode(mode)
+        ids, d2, t = g.search_debug(q, cfg.k, nprobe, cfg.budget, want_est=True)
+        torch.cuda.synchronize()
+        outs.append({"ids": ids.cpu().numpy(), "d2": d2.cpu().numpy(),
+                     **{k_: v.cpu().numpy() for k_, v in t.items()}})
+    g.set_scan_mode(g.SCAN_TENSOR)
+    a, b = outs
+    valid = {"est": "n_probed", "cand_ids": "n_cand", "cand_d2": "n_cand"}
+    for key in a:
+        if key in valid:                               # rows are valid up to their count only
+            for i in range(len(Q)):
+                n = int(a[valid[key]][i])
+                assert np.array_equal(a[key][i][:n].view(np.uint8), b[key][i][:n].view(np.uint8)), key
+        else:
+            assert np.array_equal(a[key].view(np.uint8), b[key].view(np.uint8)), key
