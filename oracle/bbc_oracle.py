@@ -110,7 +110,9 @@ def rabitq_rotate(q: np.ndarray, P: np.ndarray) -> np.ndarray:
 
 
 def rabitq_query_code(u: np.ndarray, wL: np.ndarray, rq2: F32):
-    """Per (query, list): q' = (u - w_L)/r, 4-bit scalar quantisation of q' (round half up).
+    """Per (query, list): q' = (u - w_L) * (1/r), 4-bit scalar quantisation of q' (round half
+    up): qbar = clamp(floor((q' - v_l) * (1/delta) + 1/2), 0, 15).  The reciprocals 1/r and
+    1/delta are single fp32 divisions per pair (canonical arithmetic, R12).
 
     Returns (qbar int [D], consts (c1, c2, c3) fp32, r fp32).  With D the padded dimension,
     <x_bar, q'> ~= c1 * <b, qbar> + c2 * popcount(b) + c3 where x_bar = (2b - 1)/sqrt(D):
@@ -119,14 +121,16 @@ def rabitq_query_code(u: np.ndarray, wL: np.ndarray, rq2: F32):
     D = len(u)
     r = np.sqrt(F32(rq2))
     if r > 0:
-        qp = (u - wL) / r
+        rinv = F32(1.0) / r
+        qp = (u - wL) * rinv
     else:
         qp = np.zeros(D, dtype=F32)
     vl = qp.min()
     vr = qp.max()
     delta = (vr - vl) / F32(15.0)
     if delta > 0:
-        qbar = np.floor((qp - vl) / delta + F32(0.5))
+        dinv = F32(1.0) / delta
+        qbar = np.floor((qp - vl) * dinv + F32(0.5))
         qbar = np.clip(qbar, 0, 15).astype(np.int64)
     else:
         qbar = np.zeros(D, dtype=np.int64)
@@ -143,7 +147,8 @@ def rabitq_est(bits: np.ndarray, fac: np.ndarray, qbar: np.ndarray, consts, r: F
     """est d^2 = r_o^2 + r_q^2 - 2 r_o r_q <o,q>_est, <o,q>_est = <x_bar,q'>_est / g_o.
 
     Evaluation order (fp32, each op rounded): t1 = c2*p; t2 = t1 + c3; t3 = c1*ip; oq = t3 + t2;
-    e = oq / g_o; a = r_o*r_o; s = a + rq2; f = (2*r_o)*r; est = s - f*e.
+    e = oq * (1/g_o); a = r_o*r_o; s = a + rq2; f = (2*r_o)*r; est = s - f*e, with 1/g_o one fp32
+    division per object.
     """
     c1, c2, c3 = consts
     b = np.unpackbits(bits, axis=1, bitorder="little").astype(np.int64)
@@ -153,7 +158,8 @@ def rabitq_est(bits: np.ndarray, fac: np.ndarray, qbar: np.ndarray, consts, r: F
     t2 = t1 + c3
     t3 = c1 * ip.astype(F32)
     oq = t3 + t2
-    e = oq / fac[:, 1]
+    ginv = F32(1.0) / fac[:, 1]
+    e = oq * ginv
     ro = fac[:, 0]
     a = ro * ro
     s = a + F32(rq2)

@@ -368,7 +368,8 @@ void stage_tables(Shard& s, cudaStream_t st) {
   if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) {
     const long long pairs = (long long)s.b.nq * s.b.nprobe;
     if (pairs > 0) {
-      k_rbq_pairs<<<(unsigned)((pairs + 7) / 8), 256, 0, st>>>(s.b, s.dv, s.rb.qbar, s.rb.pairc);
+      const long long warps = (long long)s.b.nq * ((s.b.nprobe + kPairsPerWarp - 1) / kPairsPerWarp);
+      k_rbq_pairs<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(s.b, s.dv, s.rb.qbar, s.rb.pairc);
       g_launches += 1;
     }
   }
@@ -385,14 +386,15 @@ void rbq_tc_pass(Shard& s, const Batch& b, cudaStream_t st, bool sample) {
   k_inv_scan<<<1, 1024, 0, st>>>(s.rb.inv_cnt, s.rb.inv_off, s.rb.inv_cur, ix->nlist);
   k_inv_fill<<<gp, 256, 0, st>>>(b, s.dv, s.rb.inv_cur, s.rb.inv, sample ? 1 : 0);
   RbqTc t{s.rb.qbar, s.rb.pairc, s.rb.inv_off, s.rb.inv, ix->rbq_tiles, ix->rbq_pc};
-  const size_t sm = (size_t)(kRbM + kRbN) * ix->D + (size_t)kRbN * 64 * 4 + kRbN * sizeof(RbqPair) +
-                    3 * kRbM * 4 + 64;
+  const size_t sm = (size_t)(kRbM + 2 * kRbN) * ix->D + 2 * kRbN * sizeof(RbqPair) + 3 * kRbM * 4 + 64;
   if (sample) {
     set_smem(k_rbq_mma<true>, sm);
     k_rbq_mma<true><<<ix->rbq_ntiles, kRbNT, sm, st>>>(b, s.dv, t);
   } else {
     set_smem(k_rbq_mma<false>, sm);
     k_rbq_mma<false><<<ix->rbq_ntiles, kRbNT, sm, st>>>(b, s.dv, t);
+    k_cell_hist<<<dim3(std::max(1, (8 * ix->num_sms + b.nq - 1) / b.nq), b.nq), 256, 0, st>>>(b);
+    g_launches += 1;
   }
   g_launches += 4;
 }
@@ -915,7 +917,7 @@ bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_
          cudaMemcpy(ix->cnorm, cn.data(), (size_t)nlist * 4, cudaMemcpyHostToDevice) == cudaSuccess;
     ix->probe_tc = d <= kMaxDimTc ? 1 : 0;
   }
-  if (ok && kind == BBC_KIND_RABITQ && D <= 1024 && D % 32 == 0) {
+  if (ok && kind == BBC_KIND_RABITQ && D <= 1024 && D % 64 == 0) {
     std::vector<int2> tiles;
     for (int L = 0; L < nlist; ++L)
       for (int o = 0; o < ix->lsize[L]; o += kRbM) tiles.push_back(make_int2(L, o));

@@ -684,9 +684,10 @@ __global__ void __launch_bounds__(kScanNT) k_rbq_scan(Batch b, Dev ix, int G) {
     const float rq2 = b.rq2[(size_t)q * b.nprobe + j];
     const float r = __fsqrt_rn(rq2);
     const float* w = ix.wL + (size_t)L * D;
+    const float rinv = r > 0.f ? __fdiv_rn(1.0f, r) : 0.f;
     float mn = INFINITY, mx = -INFINITY;
     for (int i = threadIdx.x; i < D; i += kScanNT) {
-      float v = r > 0.f ? __fdiv_rn(__fsub_rn(u[i], w[i]), r) : 0.f;
+      float v = r > 0.f ? __fmul_rn(__fsub_rn(u[i], w[i]), rinv) : 0.f;
       qp[i] = v;
       mn = fminf(mn, v);
       mx = fmaxf(mx, v);
@@ -703,12 +704,13 @@ __global__ void __launch_bounds__(kScanNT) k_rbq_scan(Batch b, Dev ix, int G) {
     }
     __syncthreads();
     const float vl = s_c[0], delta = s_c[1];
+    const float dinv = delta > 0.f ? __fdiv_rn(1.0f, delta) : 0.f;
     int sq = 0;
     for (int base = 0; base < D; base += kScanNT) {      // D is a multiple of 64
       const int i = base + threadIdx.x;
       int qb = 0;
       if (i < D && delta > 0.f) {
-        float t = floorf(__fadd_rn(__fdiv_rn(__fsub_rn(qp[i], vl), delta), 0.5f));
+        float t = floorf(__fadd_rn(__fmul_rn(__fsub_rn(qp[i], vl), dinv), 0.5f));
         qb = t < 0.f ? 0 : (t > 15.f ? 15 : (int)t);
       }
       sq += qb;
@@ -753,7 +755,7 @@ __global__ void __launch_bounds__(kScanNT) k_rbq_scan(Batch b, Dev ix, int G) {
       const float t2 = __fadd_rn(t1, c3);
       const float t3 = __fmul_rn(c1, (float)ip);
       const float oq = __fadd_rn(t3, t2);
-      const float e = __fdiv_rn(oq, f.y);
+      const float e = __fmul_rn(oq, __fdiv_rn(1.0f, f.y));
       const float a = __fmul_rn(f.x, f.x);
       const float s = __fadd_rn(a, rq2);
       const float ff = __fmul_rn(__fmul_rn(2.0f, f.x), r);

@@ -15,9 +15,12 @@
 //   k_inv_*       : inverted probe index (list -> pairs), for the sample pass (j < nsamp) or
 //                   the Push pass (all j).
 //   k_rbq_mma     : CTA = (list L, tile of 128 objects); A (128 x D bytes) staged once, then
-//                   for each tile of 64 pairs: B (64 x D bytes) staged, D/32 MMAs (M=128, N=64,
-//                   K=32), epilogue in registers: estimate -> estimate (sample) or bucket id +
-//                   per-pair histogram in shared memory (Push).
+//                   for each tile of 32 pairs: B (32 x D bytes, cp.async, double-buffered),
+//                   D/32 MMAs (M=128, N=32, K=32), epilogue in registers: estimate (sample)
+//                   or bucket id (Push).
+//   k_cell_hist   : Push histogram per query from its bucket ids (query-major, shared-memory
+//                   counts, one global flush per CTA: list-major partial histograms would need
+//                   a global atomic per (pair, bucket)).
 // Operand layout: canonical K-major, no swizzle: 8-row x 16-byte core matrices, LBO = 128 B
 // (K-adjacent), SBO = (D/16) x 128 B (8-row groups).
 #pragma once
@@ -25,62 +28,81 @@
 
 namespace bbc {
 
-constexpr int kRbM = 128, kRbN = 64, kRbNT = 256;
+constexpr int kRbM = 128, kRbN = 32, kRbNT = 512;
 
 // ------------------------------------------------------------------ per-pair query codes
-// One warp per pair p = q * nprobe + j; lane handles dims lane + 32 m.
+// One warp per (query, 4 consecutive probes): the query's rotated vector u stays in registers
+// (lane holds dims 2 lane + 64 m, m < D/64) across the 4 pairs; w_L is read as float2.
+constexpr int kPairsPerWarp = 4;
 __global__ void __launch_bounds__(256) k_rbq_pairs(Batch b, Dev ix, uint8_t* __restrict__ qbar,
                                                    float4* __restrict__ pairc) {
   const int lane = threadIdx.x & 31;
-  const long long p = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (p >= (long long)b.nq * b.nprobe) return;
-  const int q = (int)(p / b.nprobe);
+  const int groups = (b.nprobe + kPairsPerWarp - 1) / kPairsPerWarp;
+  const long long gw = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (gw >= (long long)b.nq * groups) return;
+  const int q = (int)(gw / groups);
+  const int j0 = (int)(gw % groups) * kPairsPerWarp;
   const int D = ix.D;
-  const int L = b.probe[p];
-  const float rq2 = b.rq2[p];
-  const float r = __fsqrt_rn(rq2);
-  const float* u = b.table + (size_t)q * D;
-  const float* w = ix.wL + (size_t)L * D;
-  constexpr int kMaxM = 32;                           // D <= 1024
-  float qp[kMaxM];
-  float mn = INFINITY, mx = -INFINITY;
+  const int M2 = D / 64;                              // float2 slots per lane (D % 64 == 0)
+  constexpr int kMaxM2 = 16;                          // D <= 1024
+  const float2* u2 = reinterpret_cast<const float2*>(b.table + (size_t)q * D);
+  float2 uu[kMaxM2];
 #pragma unroll
-  for (int m = 0; m < kMaxM; ++m) {
-    const int i = lane + 32 * m;
-    if (i < D) {
-      const float v = r > 0.f ? __fdiv_rn(__fsub_rn(u[i], w[i]), r) : 0.f;
-      qp[m] = v;
-      mn = fminf(mn, v);
-      mx = fmaxf(mx, v);
-    }
-  }
-  mn = warp_min(mn);
-  mx = warp_max(mx);
-  const float delta = __fdiv_rn(__fsub_rn(mx, mn), 15.0f);
-  int sq = 0;
-  uint8_t* qb = qbar + (size_t)p * D;
+  for (int m = 0; m < kMaxM2; ++m)
+    if (m < M2) uu[m] = u2[lane + 32 * m];
+  const float sD = __fsqrt_rn((float)D);
+  for (int jj = 0; jj < kPairsPerWarp; ++jj) {
+    const int j = j0 + jj;
+    if (j >= b.nprobe) break;
+    const long long p = (long long)q * b.nprobe + j;
+    const int L = b.probe[p];
+    const float rq2 = b.rq2[p];
+    const float r = __fsqrt_rn(rq2);
+    const float rinv = r > 0.f ? __fdiv_rn(1.0f, r) : 0.f;
+    const float2* w2 = reinterpret_cast<const float2*>(ix.wL + (size_t)L * D);
+    float2 qp[kMaxM2];
+    float mn = INFINITY, mx = -INFINITY;
 #pragma unroll
-  for (int m = 0; m < kMaxM; ++m) {
-    const int i = lane + 32 * m;
-    if (i < D) {
-      int v = 0;
-      if (delta > 0.f) {
-        const float t = floorf(__fadd_rn(__fdiv_rn(__fsub_rn(qp[m], mn), delta), 0.5f));
-        v = t < 0.f ? 0 : (t > 15.f ? 15 : (int)t);
+    for (int m = 0; m < kMaxM2; ++m) {
+      if (m < M2) {
+        const float2 w = w2[lane + 32 * m];
+        float2 v;
+        v.x = r > 0.f ? __fmul_rn(__fsub_rn(uu[m].x, w.x), rinv) : 0.f;
+        v.y = r > 0.f ? __fmul_rn(__fsub_rn(uu[m].y, w.y), rinv) : 0.f;
+        qp[m] = v;
+        mn = fminf(mn, fminf(v.x, v.y));
+        mx = fmaxf(mx, fmaxf(v.x, v.y));
       }
-      qb[i] = (uint8_t)v;
-      sq += v;
     }
-  }
-  sq = warp_sum(sq);
-  if (lane == 0) {
-    const float sD = __fsqrt_rn((float)D);
-    float4 c;
-    c.x = __fdiv_rn(__fmul_rn(2.0f, delta), sD);                                        // c1
-    c.y = __fdiv_rn(__fmul_rn(2.0f, mn), sD);                                           // c2
-    c.z = __fsub_rn(-__fdiv_rn(__fmul_rn(delta, (float)sq), sD), __fmul_rn(sD, mn));     // c3
-    c.w = r;
-    pairc[p] = c;
+    mn = warp_min(mn);
+    mx = warp_max(mx);
+    const float delta = __fdiv_rn(__fsub_rn(mx, mn), 15.0f);
+    const float dinv = delta > 0.f ? __fdiv_rn(1.0f, delta) : 0.f;
+    int sq = 0;
+    uint16_t* qb = reinterpret_cast<uint16_t*>(qbar + (size_t)p * D);
+#pragma unroll
+    for (int m = 0; m < kMaxM2; ++m) {
+      if (m < M2) {
+        int v0 = 0, v1 = 0;
+        if (delta > 0.f) {
+          const float t0 = floorf(__fadd_rn(__fmul_rn(__fsub_rn(qp[m].x, mn), dinv), 0.5f));
+          const float t1 = floorf(__fadd_rn(__fmul_rn(__fsub_rn(qp[m].y, mn), dinv), 0.5f));
+          v0 = t0 < 0.f ? 0 : (t0 > 15.f ? 15 : (int)t0);
+          v1 = t1 < 0.f ? 0 : (t1 > 15.f ? 15 : (int)t1);
+        }
+        qb[lane + 32 * m] = (uint16_t)(v0 | (v1 << 8));
+        sq += v0 + v1;
+      }
+    }
+    sq = warp_sum(sq);
+    if (lane == 0) {
+      float4 c;
+      c.x = __fdiv_rn(__fmul_rn(2.0f, delta), sD);                                        // c1
+      c.y = __fdiv_rn(__fmul_rn(2.0f, mn), sD);                                           // c2
+      c.z = __fsub_rn(-__fdiv_rn(__fmul_rn(delta, (float)sq), sD), __fmul_rn(sD, mn));     // c3
+      c.w = r;
+      pairc[p] = c;
+    }
   }
 }
 
@@ -201,17 +223,24 @@ __device__ __forceinline__ void i8_mma(uint32_t tmem_d, uint64_t a, uint64_t bde
 
 __device__ __forceinline__ uint32_t nib_bytes(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
 
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+
+// Pipeline per CTA: A staged once; for query tile i: (B_i, pair info_i) were copied with
+// cp.async into buffer i&1 during tile i-1's epilogue -> wait -> MMA_i (one thread) -> issue the
+// copies of tile i+1 -> wait for MMA_i -> epilogue_i (16 warps: 4 row quarters x 4 column
+// groups of 8 pairs).
 template <bool SAMPLE>
 __global__ void __launch_bounds__(kRbNT, 1) k_rbq_mma(Batch b, Dev ix, RbqTc t) {
   extern __shared__ __align__(1024) uint8_t rsm2[];
   const int D = ix.D;
   const int sbo = (D / 16) * 128;
   uint8_t* sA = rsm2;                                             // [128 x D] bytes
-  uint8_t* sB = sA + kRbM * D;                                    // [64 x D] bytes
-  uint32_t* hist = reinterpret_cast<uint32_t*>(sB + kRbN * D);    // [64 x 64] packed 4 x u8
-  RbqPair* pi = reinterpret_cast<RbqPair*>(hist + kRbN * 64);     // [64]
-  float* o_r = reinterpret_cast<float*>(pi + kRbN);               // [128] r_o
-  float* o_g = o_r + kRbM;                                        // [128] g_o
+  uint8_t* sB = sA + kRbM * D;                                    // [2][kRbN x D] bytes
+  RbqPair* pi = reinterpret_cast<RbqPair*>(sB + 2 * kRbN * D);    // [2][kRbN]
+  float* o_r = reinterpret_cast<float*>(pi + 2 * kRbN);           // [128] r_o
+  float* o_g = o_r + kRbM;                                        // [128] 1 / g_o
   float* o_pc = o_g + kRbM;                                       // [128] popcount (float)
   uint64_t* bar = reinterpret_cast<uint64_t*>(o_pc + kRbM);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
@@ -224,6 +253,38 @@ __global__ void __launch_bounds__(kRbNT, 1) k_rbq_mma(Batch b, Dev ix, RbqTc t) 
   const int nobj = min(kRbM, (int)(ix.loff[L + 1] - row0));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bar_a = smem_u32(bar);
+  const int nkc = D / 16;                                         // 16-byte chunks per row
+  // copies of query tile qi (pairs [qi*kRbN, ...)) into buffer qi & 1: B rows by cp.async,
+  // pair info by plain loads/stores (small)
+  auto stage_tile = [&](int qi) {
+    const int qt = qi * kRbN;
+    const int nqt = min(kRbN, np - qt);
+    uint8_t* B = sB + (qi & 1) * kRbN * D;
+    RbqPair* P = pi + (qi & 1) * kRbN;
+    for (int idx = threadIdx.x; idx < kRbN * nkc; idx += kRbNT) {
+      const int s = idx / nkc, kc = idx % nkc;
+      uint8_t* dst = B + (s >> 3) * sbo + kc * 128 + (s & 7) * 16;
+      if (s < nqt) {
+        const int p = t.inv[p0 + qt + s];
+        cp_async16(smem_u32(dst), t.qbar + (size_t)p * D + 16 * kc);
+      } else {
+        *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    for (int s = threadIdx.x; s < nqt; s += kRbNT) {
+      const int p = t.inv[p0 + qt + s];
+      const int q = p / b.nprobe, j = p % b.nprobe;
+      const float4 c = t.pairc[p];
+      RbqPair e;
+      e.c1 = c.x; e.c2 = c.y; e.c3 = c.z; e.r = c.w;
+      e.rq2 = b.rq2[p];
+      if (!SAMPLE) e.cf.init(b.edges[2 * q], b.edges[2 * q + 1]);
+      e.obase = (long long)q * b.cap + b.poff[(size_t)q * (b.nprobe + 1) + j] + o0;
+      e.q = q;
+      P[s] = e;
+    }
+  };
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -233,6 +294,7 @@ __global__ void __launch_bounds__(kRbNT, 1) k_rbq_mma(Batch b, Dev ix, RbqTc t) 
                  ::"r"(smem_u32(tslot)), "r"(kRbN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  stage_tile(0);
   // A: code bits of the tile's objects -> bytes 0/1 in the K-major core-matrix layout
   const int W = D / 32;
   for (int idx = threadIdx.x; idx < kRbM * W; idx += kRbNT) {
@@ -252,7 +314,7 @@ __global__ void __launch_bounds__(kRbNT, 1) k_rbq_mma(Batch b, Dev ix, RbqTc t) 
     float fr = 0.f, fg = 1.f, fp = 0.f;
     if (r < nobj) {
       const float2 f = reinterpret_cast<const float2*>(ix.factors)[row0 + r];
-      fr = f.x; fg = f.y; fp = (float)t.pc[row0 + r];
+      fr = f.x; fg = __fdiv_rn(1.0f, f.y); fp = (float)t.pc[row0 + r];
     }
     o_r[r] = fr; o_g[r] = fg; o_pc[r] = fp;
   }
@@ -260,40 +322,21 @@ __global__ void __launch_bounds__(kRbNT, 1) k_rbq_mma(Batch b, Dev ix, RbqTc t) 
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
-  const uint32_t aA = smem_u32(sA), aB = smem_u32(sB);
-  uint32_t phase = 0;
-  for (int qt = 0; qt < np; qt += kRbN) {
-    const int nqt = min(kRbN, np - qt);
-    // pair info and B (4-bit query codes as bytes)
-    for (int s = threadIdx.x; s < kRbN; s += kRbNT) {
-      if (s < nqt) {
-        const int p = t.inv[p0 + qt + s];
-        const int q = p / b.nprobe, j = p % b.nprobe;
-        const float4 c = t.pairc[p];
-        RbqPair e;
-        e.c1 = c.x; e.c2 = c.y; e.c3 = c.z; e.r = c.w;
-        e.rq2 = b.rq2[p];
-        if (!SAMPLE) e.cf.init(b.edges[2 * q], b.edges[2 * q + 1]);
-        e.obase = (long long)q * b.cap + b.poff[(size_t)q * (b.nprobe + 1) + j] + o0;
-        e.q = q;
-        pi[s] = e;
-      }
-    }
-    for (int idx = threadIdx.x; idx < kRbN * (D / 16); idx += kRbNT) {
-      const int s = idx / (D / 16), kc = idx % (D / 16);
-      uint4 v = make_uint4(0u, 0u, 0u, 0u);
-      if (s < nqt) {
-        const int p = t.inv[p0 + qt + s];
-        v = reinterpret_cast<const uint4*>(t.qbar + (size_t)p * D)[kc];
-      }
-      *reinterpret_cast<uint4*>(sB + (s >> 3) * sbo + kc * 128 + (s & 7) * 16) = v;
-    }
-    if (!SAMPLE)
-      for (int i = threadIdx.x; i < kRbN * 64; i += kRbNT) hist[i] = 0u;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  const uint32_t aA = smem_u32(sA);
+  const int ntile = (np + kRbN - 1) / kRbN;
+  const int rq = warp & 3, cg = warp >> 2;            // row quarter, column group (8 pairs)
+  const int r = 32 * rq + lane;
+  float ro = 0.f, ginv = 0.f, pcf = 0.f;
+  if (r < nobj) { ro = o_r[r]; ginv = o_g[r]; pcf = o_pc[r]; }
+  const float a_ro = __fmul_rn(ro, ro), ro2 = __fmul_rn(2.0f, ro);
+  for (int qi = 0; qi < ntile; ++qi) {
+    const int nqt = min(kRbN, np - qi * kRbN);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // cp.async/STS -> MMA reads
     __syncthreads();
     if (threadIdx.x == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t aB = smem_u32(sB + (qi & 1) * kRbN * D);
       for (int s = 0; s < D / 32; ++s) {              // K = 32 bytes per MMA: 2 core matrices
         const uint32_t o = (uint32_t)s * 256u;
         i8_mma(tmem, umma_desc_k(aA + o, (uint32_t)sbo), umma_desc_k(aB + o, (uint32_t)sbo), s ? 1u : 0u);
@@ -301,72 +344,75 @@ __global__ void __launch_bounds__(kRbNT, 1) k_rbq_mma(Batch b, Dev ix, RbqTc t) 
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                    ::"r"(bar_a) : "memory");
     }
-    mbar_wait(bar_a, phase);
-    phase ^= 1u;
+    if (qi + 1 < ntile) stage_tile(qi + 1);           // overlaps the MMA and the epilogue
+    mbar_wait(bar_a, (uint32_t)(qi & 1));
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    // epilogue: warp w -> object rows 32 (w % 4) + lane, pair columns 32 (w / 4) .. + 31
     {
-      const int r = 32 * (warp & 3) + lane;
-      const int cbase = 32 * (warp >> 2);
-      uint32_t v[32];
-      const uint32_t taddr = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)cbase;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
-          "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-            "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
-            "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
-            "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-          : "r"(taddr));
+      uint32_t v[8];
+      const uint32_t taddr = tmem + ((uint32_t)(32 * rq) << 16) + (uint32_t)(8 * cg);
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                     "=r"(v[6]), "=r"(v[7])
+                   : "r"(taddr));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      const RbqPair* P = pi + (qi & 1) * kRbN;
       if (r < nobj) {
-        const float ro = o_r[r], go = o_g[r], pc = o_pc[r];
-        const float a = __fmul_rn(ro, ro);
-        const float ro2 = __fmul_rn(2.0f, ro);
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const int s = cbase + c;
+        for (int c = 0; c < 8; ++c) {
+          const int s = 8 * cg + c;
           if (s >= nqt) continue;
-          const RbqPair& e = pi[s];
+          const RbqPair& e = P[s];
           // canonical estimator, identical to k_rbq_scan
-          const float t1 = __fmul_rn(e.c2, pc);
+          const float t1 = __fmul_rn(e.c2, pcf);
           const float t2 = __fadd_rn(t1, e.c3);
           const float t3 = __fmul_rn(e.c1, (float)(int)v[c]);
           const float oq = __fadd_rn(t3, t2);
-          const float ee = __fdiv_rn(oq, go);
-          const float sum = __fadd_rn(a, e.rq2);
+          const float ee = __fmul_rn(oq, ginv);
+          const float sum = __fadd_rn(a_ro, e.rq2);
           const float ff = __fmul_rn(ro2, e.r);
           const float est = __fsub_rn(sum, __fmul_rn(ff, ee));
-          if (SAMPLE) {
-            b.val[e.obase + r] = est;
-          } else {
-            const int cell = e.cf(est);
-            b.cells[e.obase + r] = (uint8_t)cell;
-            if (cell < 255) atomicAdd(&hist[s * 64 + (cell >> 2)], 1u << (8 * (cell & 3)));
-          }
+          if (SAMPLE) b.val[e.obase + r] = est;
+          else b.cells[e.obase + r] = (uint8_t)e.cf(est);   // histogram: k_cell_hist
         }
       }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();                                  // TMEM and smem free for the next tile
-    if (!SAMPLE) {
-      for (int i = threadIdx.x; i < nqt * 64; i += kRbNT) {
-        const uint32_t h = hist[i];
-        if (!h) continue;
-        const int s = i >> 6, c4 = (i & 63) * 4;
-        int* gh = b.hist + (size_t)pi[s].q * kCells + c4;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint32_t cnt = (h >> (8 * u)) & 255u;
-          if (cnt) atomicAdd(gh + u, (int)cnt);
-        }
-      }
-      __syncthreads();
-    }
+    __syncthreads();                                  // TMEM and buffer qi & 1 free
   }
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kRbN));
+}
+
+// Histogram of the bucket ids < 255 of query q's probed objects (Push, Alg. 1 l.1-4).
+__global__ void __launch_bounds__(256) k_cell_hist(Batch b) {
+  __shared__ int h[8][kCells];
+  const int q = blockIdx.y;
+  if (b.nsamp[q] == 0) return;
+  const int n = b.poff[(size_t)q * (b.nprobe + 1) + b.nprobe];
+  const int wid = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 8 * kCells; i += 256) (&h[0][0])[i] = 0;
+  __syncthreads();
+  const uint8_t* c = b.cells + (size_t)q * b.cap;
+  const int n16 = n >> 4;
+  for (int v = blockIdx.x * 256 + threadIdx.x; v < n16; v += gridDim.x * 256) {
+    const uint4 x = reinterpret_cast<const uint4*>(c)[v];
+    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int cell = (w[e >> 2] >> (8 * (e & 3))) & 255;
+      if (cell < 255) atomicAdd(&h[wid][cell], 1);
+    }
+  }
+  if (blockIdx.x == 0)                               // ragged tail
+    for (int i = (n16 << 4) + threadIdx.x; i < n; i += 256)
+      if (c[i] < 255) atomicAdd(&h[wid][c[i]], 1);
+  __syncthreads();
+  for (int i = threadIdx.x; i < kCells; i += 256) {
+    int t = 0;
+#pragma unroll
+    for (int w8 = 0; w8 < 8; ++w8) t += h[w8][i];
+    if (t) atomicAdd(&b.hist[(size_t)q * kCells + i], t);
+  }
 }
 
 }  // namespace bbc
