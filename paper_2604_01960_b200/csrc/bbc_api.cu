@@ -141,7 +141,8 @@ struct StageScope {
 
 struct RbqBufs {
   uint8_t* qbar = nullptr;
-  float4* pairc = nullptr;
+  RbqPair* pinfo = nullptr;
+  CellQ* cq = nullptr;
   int* inv = nullptr;
   int* inv_cnt = nullptr;
   int* inv_off = nullptr;
@@ -169,7 +170,7 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1) {
   p.per_query += 8 + 8 + kCells * 4 + 4 + 4 + (size_t)4 * world;   // DistBuf
   p.fixed = 64 * 256;
   if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) {            // pair codes + inverted index
-    p.per_query += (size_t)nprobe * ((size_t)ix->D + 16 + 4) + 3 * 256;
+    p.per_query += (size_t)nprobe * ((size_t)ix->D + 32 + 4) + 16 + 4 * 256;
     p.fixed += (size_t)3 * (ix->nlist + 1) * 4 + 3 * 256;
   }
   return p;
@@ -217,7 +218,8 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, 
   if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) {
     const size_t pairs = (size_t)nqb * nprobe;
     rb->qbar = (uint8_t*)take(pairs * ix->D);
-    rb->pairc = (float4*)take(pairs * 16);
+    rb->pinfo = (RbqPair*)take(pairs * sizeof(RbqPair));
+    rb->cq = (CellQ*)take((size_t)nqb * sizeof(CellQ));
     rb->inv = (int*)take(pairs * 4);
     rb->inv_cnt = (int*)take((size_t)(ix->nlist + 1) * 4);
     rb->inv_off = (int*)take((size_t)(ix->nlist + 1) * 4);
@@ -369,7 +371,7 @@ void stage_tables(Shard& s, cudaStream_t st) {
     const long long pairs = (long long)s.b.nq * s.b.nprobe;
     if (pairs > 0) {
       const long long warps = (long long)s.b.nq * ((s.b.nprobe + kPairsPerWarp - 1) / kPairsPerWarp);
-      k_rbq_pairs<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(s.b, s.dv, s.rb.qbar, s.rb.pairc);
+      k_rbq_pairs<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(s.b, s.dv, s.rb.qbar, s.rb.pinfo);
       g_launches += 1;
     }
   }
@@ -385,8 +387,13 @@ void rbq_tc_pass(Shard& s, const Batch& b, cudaStream_t st, bool sample) {
   k_inv_count<<<gp, 256, 0, st>>>(b, s.dv, s.rb.inv_cnt, sample ? 1 : 0);
   k_inv_scan<<<1, 1024, 0, st>>>(s.rb.inv_cnt, s.rb.inv_off, s.rb.inv_cur, ix->nlist);
   k_inv_fill<<<gp, 256, 0, st>>>(b, s.dv, s.rb.inv_cur, s.rb.inv, sample ? 1 : 0);
-  RbqTc t{s.rb.qbar, s.rb.pairc, s.rb.inv_off, s.rb.inv, ix->rbq_tiles, ix->rbq_pc};
-  const size_t sm = (size_t)(kRbM + 2 * kRbN) * ix->D + 2 * kRbN * sizeof(RbqPair) + 3 * kRbM * 4 + 64;
+  if (!sample) {
+    k_rbq_cellq<<<(b.nq + 255) / 256, 256, 0, st>>>(b, s.rb.cq);
+    g_launches += 1;
+  }
+  RbqTc t{s.rb.qbar, s.rb.pinfo, s.rb.cq, s.rb.inv_off, s.rb.inv, ix->rbq_tiles, ix->rbq_pc};
+  const size_t sm = (size_t)(kRbM + 2 * kRbN) * ix->D + 2 * kRbN * sizeof(RbqPair) +
+                    (size_t)kRbMaxPairs * 4 + 3 * kRbM * 4 + 64;
   if (sample) {
     set_smem(k_rbq_mma<true>, sm);
     k_rbq_mma<true><<<ix->rbq_ntiles, kRbNT, sm, st>>>(b, s.dv, t);
@@ -689,7 +696,9 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
           CU(cudaMemcpyAsync(ns_all, all.data(), (size_t)nb * 4, cudaMemcpyHostToDevice, st));
           CU(cudaStreamSynchronize(st));
           b2.nsamp = ns_all;
-          if (ix->rbq_tc) {
+          if (ix->rbq_tc) {                           // pair records address b2's buffer
+            const long long warps = (long long)nb * ((nprobe + kPairsPerWarp - 1) / kPairsPerWarp);
+            k_rbq_pairs<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(b2, s0.dv, s0.rb.qbar, s0.rb.pinfo);
             rbq_tc_pass(s0, b2, st, true);
           } else {
             const size_t sm = (size_t)ix->D * 4 + 4 * (ix->D / 32) * 4;

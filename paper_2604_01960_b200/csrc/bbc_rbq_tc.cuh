@@ -29,13 +29,24 @@
 namespace bbc {
 
 constexpr int kRbM = 128, kRbN = 32, kRbNT = 512;
+constexpr int kRbMaxPairs = 4096;   // pair ids of one list kept in shared memory
+
+struct __align__(16) RbqPair {   // per (query, probed list), written by k_rbq_pairs
+  float c1, c2, c3, r;
+  float rq2;
+  int q;
+  long long obase;       // q * cap + poff[q][j]: probe-order position of the list's object 0
+};
+static_assert(sizeof(RbqPair) == 32, "two 16-byte copies per pair");
+
+struct __align__(16) CellQ { float dmin, dmax, inv; int degen; };   // per query (Eq. 6, R3)
 
 // ------------------------------------------------------------------ per-pair query codes
 // One warp per (query, 4 consecutive probes): the query's rotated vector u stays in registers
 // (lane holds dims 2 lane + 64 m, m < D/64) across the 4 pairs; w_L is read as float2.
 constexpr int kPairsPerWarp = 4;
 __global__ void __launch_bounds__(256) k_rbq_pairs(Batch b, Dev ix, uint8_t* __restrict__ qbar,
-                                                   float4* __restrict__ pairc) {
+                                                   RbqPair* __restrict__ pinfo) {
   const int lane = threadIdx.x & 31;
   const int groups = (b.nprobe + kPairsPerWarp - 1) / kPairsPerWarp;
   const long long gw = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -62,17 +73,23 @@ __global__ void __launch_bounds__(256) k_rbq_pairs(Batch b, Dev ix, uint8_t* __r
     const float2* w2 = reinterpret_cast<const float2*>(ix.wL + (size_t)L * D);
     float2 qp[kMaxM2];
     float mn = INFINITY, mx = -INFINITY;
+    if (r > 0.f) {
 #pragma unroll
-    for (int m = 0; m < kMaxM2; ++m) {
-      if (m < M2) {
-        const float2 w = w2[lane + 32 * m];
-        float2 v;
-        v.x = r > 0.f ? __fmul_rn(__fsub_rn(uu[m].x, w.x), rinv) : 0.f;
-        v.y = r > 0.f ? __fmul_rn(__fsub_rn(uu[m].y, w.y), rinv) : 0.f;
-        qp[m] = v;
-        mn = fminf(mn, fminf(v.x, v.y));
-        mx = fmaxf(mx, fmaxf(v.x, v.y));
+      for (int m = 0; m < kMaxM2; ++m) {
+        if (m < M2) {
+          const float2 w = w2[lane + 32 * m];
+          float2 v;
+          v.x = __fmul_rn(__fsub_rn(uu[m].x, w.x), rinv);
+          v.y = __fmul_rn(__fsub_rn(uu[m].y, w.y), rinv);
+          qp[m] = v;
+          mn = fminf(mn, fminf(v.x, v.y));
+          mx = fmaxf(mx, fmaxf(v.x, v.y));
+        }
       }
+    } else {
+#pragma unroll
+      for (int m = 0; m < kMaxM2; ++m) qp[m] = make_float2(0.f, 0.f);
+      mn = mx = 0.f;
     }
     mn = warp_min(mn);
     mx = warp_max(mx);
@@ -84,11 +101,11 @@ __global__ void __launch_bounds__(256) k_rbq_pairs(Batch b, Dev ix, uint8_t* __r
     for (int m = 0; m < kMaxM2; ++m) {
       if (m < M2) {
         int v0 = 0, v1 = 0;
-        if (delta > 0.f) {
-          const float t0 = floorf(__fadd_rn(__fmul_rn(__fsub_rn(qp[m].x, mn), dinv), 0.5f));
-          const float t1 = floorf(__fadd_rn(__fmul_rn(__fsub_rn(qp[m].y, mn), dinv), 0.5f));
-          v0 = t0 < 0.f ? 0 : (t0 > 15.f ? 15 : (int)t0);
-          v1 = t1 < 0.f ? 0 : (t1 > 15.f ? 15 : (int)t1);
+        if (delta > 0.f) {                            // floor + convert in one cvt.rmi
+          v0 = __float2int_rd(__fadd_rn(__fmul_rn(__fsub_rn(qp[m].x, mn), dinv), 0.5f));
+          v1 = __float2int_rd(__fadd_rn(__fmul_rn(__fsub_rn(qp[m].y, mn), dinv), 0.5f));
+          v0 = min(15, max(0, v0));
+          v1 = min(15, max(0, v1));
         }
         qb[lane + 32 * m] = (uint16_t)(v0 | (v1 << 8));
         sq += v0 + v1;
@@ -96,12 +113,15 @@ __global__ void __launch_bounds__(256) k_rbq_pairs(Batch b, Dev ix, uint8_t* __r
     }
     sq = warp_sum(sq);
     if (lane == 0) {
-      float4 c;
-      c.x = __fdiv_rn(__fmul_rn(2.0f, delta), sD);                                        // c1
-      c.y = __fdiv_rn(__fmul_rn(2.0f, mn), sD);                                           // c2
-      c.z = __fsub_rn(-__fdiv_rn(__fmul_rn(delta, (float)sq), sD), __fmul_rn(sD, mn));     // c3
-      c.w = r;
-      pairc[p] = c;
+      RbqPair e;
+      e.c1 = __fdiv_rn(__fmul_rn(2.0f, delta), sD);
+      e.c2 = __fdiv_rn(__fmul_rn(2.0f, mn), sD);
+      e.c3 = __fsub_rn(-__fdiv_rn(__fmul_rn(delta, (float)sq), sD), __fmul_rn(sD, mn));
+      e.r = r;
+      e.rq2 = rq2;
+      e.q = q;
+      e.obase = (long long)q * b.cap + b.poff[(size_t)q * (b.nprobe + 1) + j];
+      pinfo[p] = e;
     }
   }
 }
@@ -176,6 +196,17 @@ __global__ void k_inv_fill(Batch b, Dev ix, int* cur, int* inv, int sample) {
   if (inv_selected(b, ix, p, sample != 0, &L)) inv[atomicAdd(&cur[L], 1)] = (int)p;
 }
 
+// Per query: the bucket-id function of its edges (after the sample stage).
+__global__ void k_rbq_cellq(Batch b, CellQ* cq) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= b.nq) return;
+  CellFn f;
+  f.init(b.edges[2 * q], b.edges[2 * q + 1]);
+  CellQ c;
+  c.dmin = f.dmin; c.dmax = f.dmax; c.inv = f.inv; c.degen = f.degen ? 1 : 0;
+  cq[q] = c;
+}
+
 // Index-load-time: popcount of every code and the (list, 128-object tile) work list.
 __global__ void k_rbq_popc(const uint8_t* bits, long long n, int D, int* pc) {
   const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -189,19 +220,15 @@ __global__ void k_rbq_popc(const uint8_t* bits, long long n, int D, int* pc) {
 // ------------------------------------------------------------------ the list-major GEMM
 struct RbqTc {
   const uint8_t* qbar;   // [pairs x D]
-  const float4* pairc;   // [pairs] (c1, c2, c3, r)
+  const RbqPair* pinfo;  // [pairs]
+  const CellQ* cq;       // [nq]
   const int* inv_off;    // [nlist + 1]
   const int* inv;        // pair ids grouped by list
   const int2* tiles;     // [ntiles] (list, first object)
   const int* pc;         // [n_local] popcount of each code
 };
 
-struct RbqPair {
-  float c1, c2, c3, r, rq2;
-  CellFn cf;
-  long long obase;       // q * cap + poff[q][j] + first object of the tile
-  int q;
-};
+
 
 constexpr int kRbqIdesc = (2 << 4) | ((kRbN >> 3) << 17) | ((kRbM >> 4) << 24);   // s32 += u8 x u8
 
@@ -239,7 +266,8 @@ __global__ void __launch_bounds__(kRbNT, 1) k_rbq_mma(Batch b, Dev ix, RbqTc t) 
   uint8_t* sA = rsm2;                                             // [128 x D] bytes
   uint8_t* sB = sA + kRbM * D;                                    // [2][kRbN x D] bytes
   RbqPair* pi = reinterpret_cast<RbqPair*>(sB + 2 * kRbN * D);    // [2][kRbN]
-  float* o_r = reinterpret_cast<float*>(pi + 2 * kRbN);           // [128] r_o
+  int* s_pid = reinterpret_cast<int*>(pi + 2 * kRbN);             // [kRbMaxPairs] pair ids
+  float* o_r = reinterpret_cast<float*>(s_pid + kRbMaxPairs);     // [128] r_o
   float* o_g = o_r + kRbM;                                        // [128] 1 / g_o
   float* o_pc = o_g + kRbM;                                       // [128] popcount (float)
   uint64_t* bar = reinterpret_cast<uint64_t*>(o_pc + kRbM);
@@ -254,36 +282,30 @@ __global__ void __launch_bounds__(kRbNT, 1) k_rbq_mma(Batch b, Dev ix, RbqTc t) 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bar_a = smem_u32(bar);
   const int nkc = D / 16;                                         // 16-byte chunks per row
-  // copies of query tile qi (pairs [qi*kRbN, ...)) into buffer qi & 1: B rows by cp.async,
-  // pair info by plain loads/stores (small)
+  const bool pid_smem = np <= kRbMaxPairs;
+  for (int i = threadIdx.x; i < np && pid_smem; i += kRbNT) s_pid[i] = t.inv[p0 + i];
+  __syncthreads();
+  // asynchronous copies of query tile qi (pairs [qi*kRbN, ...)) into buffer qi & 1: the query
+  // codes (B rows) and the pair records, 16 bytes per cp.async
   auto stage_tile = [&](int qi) {
     const int qt = qi * kRbN;
     const int nqt = min(kRbN, np - qt);
     uint8_t* B = sB + (qi & 1) * kRbN * D;
     RbqPair* P = pi + (qi & 1) * kRbN;
-    for (int idx = threadIdx.x; idx < kRbN * nkc; idx += kRbNT) {
-      const int s = idx / nkc, kc = idx % nkc;
-      uint8_t* dst = B + (s >> 3) * sbo + kc * 128 + (s & 7) * 16;
-      if (s < nqt) {
-        const int p = t.inv[p0 + qt + s];
-        cp_async16(smem_u32(dst), t.qbar + (size_t)p * D + 16 * kc);
-      } else {
-        *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);
+    for (int idx = threadIdx.x; idx < kRbN * (nkc + 2); idx += kRbNT) {
+      const int s = idx / (nkc + 2), kc = idx % (nkc + 2);
+      const int p = s < nqt ? (pid_smem ? s_pid[qt + s] : t.inv[p0 + qt + s]) : 0;
+      if (kc < nkc) {
+        uint8_t* dst = B + (s >> 3) * sbo + kc * 128 + (s & 7) * 16;
+        if (s < nqt) cp_async16(smem_u32(dst), t.qbar + (size_t)p * D + 16 * kc);
+        else *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);
+      } else if (s < nqt) {
+        const int h = kc - nkc;
+        cp_async16(smem_u32(reinterpret_cast<uint8_t*>(P + s) + 16 * h),
+                   reinterpret_cast<const uint8_t*>(t.pinfo + p) + 16 * h);
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
-    for (int s = threadIdx.x; s < nqt; s += kRbNT) {
-      const int p = t.inv[p0 + qt + s];
-      const int q = p / b.nprobe, j = p % b.nprobe;
-      const float4 c = t.pairc[p];
-      RbqPair e;
-      e.c1 = c.x; e.c2 = c.y; e.c3 = c.z; e.r = c.w;
-      e.rq2 = b.rq2[p];
-      if (!SAMPLE) e.cf.init(b.edges[2 * q], b.edges[2 * q + 1]);
-      e.obase = (long long)q * b.cap + b.poff[(size_t)q * (b.nprobe + 1) + j] + o0;
-      e.q = q;
-      P[s] = e;
-    }
   };
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a));
@@ -362,6 +384,7 @@ __global__ void __launch_bounds__(kRbNT, 1) k_rbq_mma(Batch b, Dev ix, RbqTc t) 
           const int s = 8 * cg + c;
           if (s >= nqt) continue;
           const RbqPair& e = P[s];
+          const long long at = e.obase + o0 + r;
           // canonical estimator, identical to k_rbq_scan
           const float t1 = __fmul_rn(e.c2, pcf);
           const float t2 = __fadd_rn(t1, e.c3);
@@ -371,8 +394,19 @@ __global__ void __launch_bounds__(kRbNT, 1) k_rbq_mma(Batch b, Dev ix, RbqTc t) 
           const float sum = __fadd_rn(a_ro, e.rq2);
           const float ff = __fmul_rn(ro2, e.r);
           const float est = __fsub_rn(sum, __fmul_rn(ff, ee));
-          if (SAMPLE) b.val[e.obase + r] = est;
-          else b.cells[e.obase + r] = (uint8_t)e.cf(est);   // histogram: k_cell_hist
+          if (SAMPLE) {
+            b.val[at] = est;
+          } else {                                    // bucket id (Eq. 6, R3); histogram: k_cell_hist
+            const CellQ cq = t.cq[e.q];
+            int cell;
+            if (est > cq.dmax) cell = 255;
+            else if (cq.degen) cell = 0;
+            else {
+              const float f = floorf(__fmul_rn(__fsub_rn(est, cq.dmin), cq.inv));
+              cell = f < 0.f ? 0 : (f > 254.f ? 254 : (int)f);
+            }
+            b.cells[at] = (uint8_t)cell;
+          }
         }
       }
     }
