@@ -79,6 +79,17 @@ def smem_lookup_peak_gbs():
     return 148 * 128 * mhz * 1e6 / 1e9
 
 
+def tensor_peak_tops(dtype: str) -> float:
+    """Dense tensor peak in TOP/s: measured bf16 (MEASURED_PEAKS.json) x the nominal ratio of
+    the dtype to bf16 (tf32 0.5, int8 2)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            bf16 = float(json.load(f)["bf16_tflops"])
+    except Exception:
+        bf16 = 2250.0
+    return bf16 * {"bf16": 1.0, "tf32": 0.5, "i8": 2.0}[dtype]
+
+
 def measured_traffic(workload, nprobe, budget, kernel):
     """DRAM bytes per launch of `kernel` from the committed ncu capture of the same workload and
     operating point (profiles/traffic.json), or None."""
@@ -352,16 +363,29 @@ def main():
             hv = v["hbm_view"]
             hv["GBs"] = hv["code_bytes"] / (v["ms"] / 1e3) / 1e9
             hv["frac"] = hv["GBs"] / peak
-    if info.kind != 1:                                  # RaBitQ scan: popcount, report HBM view
-        per["scan"].update(bound="hbm", bytes=main_objs * code_bytes, peak_GBs=peak)
-        per["scan"]["GBs"] = per["scan"]["bytes"] / (scan_ms / 1e3) / 1e9 if scan_ms > 0 else None
-        per["scan"]["frac"] = per["scan"]["GBs"] / peak if per["scan"]["GBs"] else None
+    if info.kind != 1:
+        # RaBitQ scan = list-major integer GEMM on the tensor cores (kind::i8): 2 ops per code bit
+        # per (object, query) pair of the Push pass, against the int8 dense peak (measured bf16
+        # TFLOP/s x the nominal int8/bf16 ratio 2, B200_PROFILING.md)
+        ops = 2.0 * stats["probed"] * info.dpad
+        tpk = tensor_peak_tops("i8")
+        per["scan"] = {"ms": scan_ms, "bound": "tensor", "pipe": "tcgen05.mma kind::i8",
+                       "ops": ops, "peak_TOPs": tpk,
+                       "TOPs": ops / (scan_ms / 1e3) / 1e12 if scan_ms > 0 else None,
+                       "hbm_view": {"code_bytes": main_objs * code_bytes, "peak_GBs": peak}}
+        per["scan"]["frac"] = per["scan"]["TOPs"] / tpk if per["scan"]["TOPs"] else None
+        per["scan"]["GBs"] = None
     dom = max(per, key=lambda n: per[n]["ms"])
     traffic = measured_traffic(cfg.name, nprobe, budget, dom)
-    roof = {"bound": per[dom]["bound"], "kernel": dom, "achieved": per[dom]["GBs"],
-            "peak": per[dom]["peak_GBs"], "unit": "GB/s", "frac": per[dom]["frac"],
-            "traffic": traffic, "peak_source": peak_src if per[dom]["bound"] == "hbm" else
-            "derived: 148 SMs x 128 B/clk shared-memory wavefronts x sm_max_mhz (DESIGN.md 5)",
+    tens = per[dom]["bound"] == "tensor"
+    roof = {"bound": per[dom]["bound"], "kernel": dom,
+            "achieved": per[dom]["TOPs"] if tens else per[dom]["GBs"],
+            "peak": per[dom]["peak_TOPs"] if tens else per[dom]["peak_GBs"],
+            "unit": "TOP/s" if tens else "GB/s", "frac": per[dom]["frac"],
+            "traffic": traffic,
+            "peak_source": (peak_src if per[dom]["bound"] == "hbm" else
+                            "measured bf16 TFLOP/s x 2 (int8/bf16 nominal ratio)" if tens else
+                            "derived: 148 SMs x 128 B/clk shared-memory wavefronts x sm_max_mhz (DESIGN.md 5)"),
             "per_kernel": per,
             "stage_ms_per_step": {k_: v / args.steps for k_, v in stage_ms.items()}}
 

@@ -32,7 +32,7 @@ def main(src, dst, key=None, traffic_path=None):
         for i in order:
             n = k[i]["name"]
             b = k[i].get("dram__bytes_read.sum", 0) + k[i].get("dram__bytes_write.sum", 0)
-            if "k_pq_scan_rq" in n and ", 0>" in n or "k_rbq_scan<false>" in n:
+            if ("k_pq_scan_rq" in n and ", 0>" in n) or "k_rbq_scan<false>" in n or "k_rbq_mma<0>" in n:
                 ent["scan"] = {"dram_bytes": b, "source": dst + " (ncu, one launch)"}
             if n.startswith("void k_rerank") or n.startswith("k_rerank"):
                 ent["rerank"] = {"dram_bytes": b, "source": dst + " (ncu, one launch)"}
