@@ -21,12 +21,15 @@ Paper passages followed
 Determinism: every random choice comes from the config seed's `kmeans` / `quantizer` streams;
 ties in assignments go to the smaller index (argmin semantics).  Assignments (k-means and PQ
 encoding) use GEMM-form fp32 distances, so a near-tie may pick a codeword whose exact distance
-exceeds the minimum by a rounding error; tests/test_datagen.py bounds that slack.  Heavy linear algebra runs on
-the CPU through torch (plumbing only) in chunks.
+exceeds the minimum by a rounding error; tests/test_datagen.py bounds that slack.  Heavy linear algebra runs
+through torch (plumbing only) in chunks: on a CUDA device when one is present (cuBLAS fp32
+GEMMs; BBC_BUILD_DEVICE=cpu forces the CPU), so an index built on a GPU box can differ from one
+built on a CPU at near-ties -- the serialized file, not the build, is what both query paths share.
 """
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 import torch
@@ -37,17 +40,35 @@ from .configs import Config
 _CHUNK_ELEMS = 1 << 25   # elements of one distance tile (rows x centroids)
 
 
+def _device() -> str:
+    want = os.environ.get("BBC_BUILD_DEVICE", "auto")
+    return "cuda" if want != "cpu" and torch.cuda.is_available() else "cpu"
+
+
 def _assign(X: np.ndarray, C: np.ndarray) -> np.ndarray:
     """Nearest centroid per row (GEMM-form fp32 distances; ties -> smaller id)."""
-    Ct = torch.from_numpy(np.ascontiguousarray(C, dtype=np.float32))
+    dev = _device()
+    Ct = torch.from_numpy(np.ascontiguousarray(C, dtype=np.float32)).to(dev)
     cn = (Ct * Ct).sum(1)
     out = np.empty(len(X), dtype=np.int64)
     rows = max(1, _CHUNK_ELEMS // max(1, len(C)))
-    for lo in range(0, len(X), rows):
-        xb = torch.from_numpy(np.ascontiguousarray(X[lo:lo + rows], dtype=np.float32))
-        dist = cn[None, :] - 2.0 * (xb @ Ct.T)
-        out[lo:lo + len(xb)] = torch.argmin(dist, dim=1).numpy()
+    with _NoTF32():
+        for lo in range(0, len(X), rows):
+            xb = torch.from_numpy(np.ascontiguousarray(X[lo:lo + rows], dtype=np.float32)).to(dev)
+            dist = cn[None, :] - 2.0 * (xb @ Ct.T)
+            out[lo:lo + len(xb)] = torch.argmin(dist, dim=1).cpu().numpy()
     return out
+
+
+class _NoTF32:
+    """fp32 GEMMs (no TF32 rounding of the inputs) while building."""
+
+    def __enter__(self):
+        self.prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = False
+
+    def __exit__(self, *a):
+        torch.backends.cuda.matmul.allow_tf32 = self.prev
 
 
 def kmeans(X: np.ndarray, K: int, iters: int, g: np.random.Generator, train_n: int) -> np.ndarray:

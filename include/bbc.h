@@ -86,17 +86,20 @@ bbc_status bbc_index_info(bbc_index index, bbc_index_info_t* info);
 
 /*
  * bbc_set_probe_mode -- how step a1 (coarse probe, route P:L392; nearest-first order P:L1146)
- * computes the nprobe nearest lists.  Both modes return the same lists: the nprobe smallest
+ * computes the nprobe nearest lists.  All modes return the same lists: the nprobe smallest
  * (canonical fp32 d^2, list id) keys.
  *   BBC_PROBE_SIMT   : canonical fp32 d^2 of every (query, centroid) on the CUDA cores.
- *   BBC_PROBE_TENSOR : (default when d <= 1024) the tensor cores (tcgen05, kind::tf32, 3xTF32
- *                      split) compute d~ with a proven error bound; the shortlist that provably
- *                      holds the nprobe nearest lists is re-scored canonically.
+ *   BBC_PROBE_TENSOR : (d <= 1024) the tensor cores (tcgen05, kind::tf32, 3xTF32 split)
+ *                      compute d~ with a proven error bound; the shortlist that provably holds
+ *                      the nprobe nearest lists is re-scored canonically.
+ *   BBC_PROBE_AUTO   : (default) TENSOR when available and nprobe <= nlist / 32 (the re-score
+ *                      reads nprobe centroid rows per query), SIMT otherwise.
  * Errors: BBC_ERR_ARG for a null index, an unknown mode, or TENSOR with d > 1024.  The mode is
  * per handle; it must not change while a search on the handle is in flight.
  */
 #define BBC_PROBE_SIMT 0
 #define BBC_PROBE_TENSOR 1
+#define BBC_PROBE_AUTO 2
 bbc_status bbc_set_probe_mode(bbc_index index, int32_t mode);
 
 /*

@@ -264,11 +264,12 @@ class Index:
         _check(lib().bbc_comm_init(self._h, buf, rank, world))
 
     # ------------------------------------------------------------------ instrumentation
-    PROBE_SIMT, PROBE_TENSOR = 0, 1
+    PROBE_SIMT, PROBE_TENSOR, PROBE_AUTO = 0, 1, 2
 
     def set_probe_mode(self, mode: int) -> None:
-        """Step a1 on the CUDA cores (canonical d^2 everywhere, PROBE_SIMT) or the tensor-core
-        shortlist + canonical re-score (PROBE_TENSOR, default for d <= 1024)."""
+        """Step a1 on the CUDA cores (canonical d^2 everywhere, PROBE_SIMT), as the tensor-core
+        shortlist + canonical re-score (PROBE_TENSOR), or chosen per search (PROBE_AUTO, the
+        default: tensor cores when nprobe <= nlist / 32).  Same probe lists in every mode."""
         _check(lib().bbc_set_probe_mode(self._h, int(mode)))
 
     SCAN_SIMT, SCAN_TENSOR = 0, 1

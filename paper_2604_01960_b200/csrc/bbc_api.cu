@@ -62,7 +62,8 @@ struct bbc_index_s {
   float* cmu = nullptr;                 // [d] centroid mean (tensor-core probe)
   float* cnorm = nullptr;               // [nlist] |c - mu|^2
   float cmax = 0.f;                     // max |c - mu|, rounded up
-  int probe_tc = 0;                     // 1: tensor-core shortlist probe (bbc_probe_tc.cuh)
+  int probe_mode = BBC_PROBE_AUTO;       // BBC_PROBE_* (bbc_probe_tc.cuh)
+  bool probe_tc_ok = false;             // d <= 1024: the tensor-core probe is available
   int rbq_tc = 0;                       // 1: RaBitQ estimates on the tensor cores (bbc_rbq_tc.cuh)
   int2* rbq_tiles = nullptr;            // [rbq_ntiles] (list, first object) of 128-object tiles
   int rbq_ntiles = 0;
@@ -103,7 +104,7 @@ Dev dev_view(const bbc_index_s* ix) {
   v.centroids = ix->centroids; v.loff = ix->loff; v.gsize = ix->gsize_d; v.ids = ix->ids;
   v.books = ix->books; v.codes = ix->codes; v.P = ix->P; v.wL = ix->wL; v.bits = ix->bits;
   v.factors = ix->factors; v.raw = ix->raw;
-  v.cmu = ix->cmu; v.cnorm = ix->cnorm; v.cmax = ix->cmax; v.probe_tc = ix->probe_tc;
+  v.cmu = ix->cmu; v.cnorm = ix->cnorm; v.cmax = ix->cmax; v.probe_tc = 0;
   return v;
 }
 
@@ -346,7 +347,7 @@ struct Shard {
 void stage_probe(Shard& s, cudaStream_t st) {
   bbc_index_s* ix = s.ix;
   StageScope sc(ix, st, BBC_STAGE_PROBE);
-  if (ix->probe_tc) {
+  if (s.dv.probe_tc) {
     const dim3 gt((ix->nlist + kTcN - 1) / kTcN, (s.b.nq + kTcM - 1) / kTcM);
     set_smem(k_probe_mma, kTcSmem);
     k_probe_mma<<<gt, kTcNT, kTcSmem, st>>>(s.b.Q, ix->centroids, ix->cmu, ix->cnorm, s.b.coarse,
@@ -606,6 +607,11 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
     s.ix->microbatches = 0;
     if (s.ix->timing) s.ix->timed_calls++;
     s.dv = dev_view(s.ix);
+    // a1 on the tensor cores when it wins: the shortlist re-score reads nprobe centroid rows per
+    // query, the SIMT tiled kernel all nlist: tensor cores for nprobe <= nlist/32
+    const int pm = s.ix->probe_mode;
+    s.dv.probe_tc = s.ix->probe_tc_ok &&
+                    (pm == BBC_PROBE_TENSOR || (pm == BBC_PROBE_AUTO && 32LL * nprobe <= s.ix->nlist));
   }
   for (long long q0 = 0; q0 < nq; q0 += nqb) {
     const int nb = (int)std::min<long long>(nqb, nq - q0);
@@ -924,7 +930,7 @@ bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_
     ok = ok && dalloc((void**)&ix->cmu, (size_t)d * 4) && dalloc((void**)&ix->cnorm, (size_t)nlist * 4) &&
          cudaMemcpy(ix->cmu, mu.data(), (size_t)d * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
          cudaMemcpy(ix->cnorm, cn.data(), (size_t)nlist * 4, cudaMemcpyHostToDevice) == cudaSuccess;
-    ix->probe_tc = d <= kMaxDimTc ? 1 : 0;
+    ix->probe_tc_ok = d <= kMaxDimTc;
   }
   if (ok && kind == BBC_KIND_RABITQ && D <= 1024 && D % 64 == 0) {
     std::vector<int2> tiles;
@@ -985,9 +991,10 @@ void ivf_free(bbc_index ix) {
 
 bbc_status bbc_set_probe_mode(bbc_index ix, int32_t mode) {
   if (!ix) return fail(BBC_ERR_ARG, "null index");
-  if (mode != BBC_PROBE_SIMT && mode != BBC_PROBE_TENSOR) return fail(BBC_ERR_ARG, "unknown probe mode");
-  if (mode == BBC_PROBE_TENSOR && ix->d > kMaxDimTc) return fail(BBC_ERR_ARG, "d too large for the tensor-core probe");
-  ix->probe_tc = mode == BBC_PROBE_TENSOR ? 1 : 0;
+  if (mode != BBC_PROBE_SIMT && mode != BBC_PROBE_TENSOR && mode != BBC_PROBE_AUTO)
+    return fail(BBC_ERR_ARG, "unknown probe mode");
+  if (mode == BBC_PROBE_TENSOR && !ix->probe_tc_ok) return fail(BBC_ERR_ARG, "d too large for the tensor-core probe");
+  ix->probe_mode = mode;
   return BBC_OK;
 }
 

@@ -265,7 +265,7 @@ def test_probe_modes_identical(name):
         torch.cuda.synchronize()
         outs[mode] = (ids.cpu().numpy(), d2.cpu().numpy(), t["probe"].cpu().numpy(),
                       t["rq2"].cpu().numpy())
-    g.set_probe_mode(g.PROBE_TENSOR)
+    g.set_probe_mode(g.PROBE_AUTO)
     a, b = outs[g.PROBE_SIMT], outs[g.PROBE_TENSOR]
     for x, y in zip(a, b):
         assert np.array_equal(x.view(np.uint8), y.view(np.uint8))
@@ -285,7 +285,7 @@ def test_probe_tensor_large_nprobe_and_ties():
         _, _, t = g.search_debug(q, cfg.k, cfg.nlist, cfg.budget)
         torch.cuda.synchronize()
         res.append(t["probe"].cpu().numpy())
-    g.set_probe_mode(g.PROBE_TENSOR)
+    g.set_probe_mode(g.PROBE_AUTO)
     assert np.array_equal(res[0], res[1])
 
 
