@@ -176,12 +176,14 @@ class Index:
         return b.value, m.value
 
     def workspace(self, nq: int, k: int, nprobe: int, budget: int, max_bytes: int | None = None):
-        """A cached device workspace (uint8 tensor) big enough for nq queries in one micro-batch
-        (capped at max_bytes, never below the minimum)."""
+        """A cached device workspace (uint8 tensor) big enough for nq queries in one micro-batch,
+        capped at max_bytes (default 40% of the device memory; the library then processes the
+        queries in micro-batches), never below the minimum."""
         torch = _torch()
         want, mn = self.workspace_size(nq, k, nprobe, budget)
-        if max_bytes is not None:
-            want = max(mn, min(want, max_bytes))
+        if max_bytes is None:          # default: at most 40% of the device; queries micro-batch
+            max_bytes = int(0.4 * torch.cuda.get_device_properties(self.device).total_memory)
+        want = max(mn, min(want, max_bytes))
         if self._ws is None or self._ws.numel() < want:
             self._ws = None
             self._ws = torch.empty(want, dtype=torch.uint8, device=f"cuda:{self.device}")

@@ -61,6 +61,7 @@ struct bbc_index_s {
   long long* tbase = nullptr;           // [nlist] byte offset of each list in codes_t
   float* cmu = nullptr;                 // [d] centroid mean (tensor-core probe)
   float* cnorm = nullptr;               // [nlist] |c - mu|^2
+  int* lrank = nullptr;                 // [nlist] (region << 20 | list): query locality order
   float cmax = 0.f;                     // max |c - mu|, rounded up
   int probe_mode = BBC_PROBE_AUTO;       // BBC_PROBE_* (bbc_probe_tc.cuh)
   bool probe_tc_ok = false;             // d <= 1024: the tensor-core probe is available
@@ -165,7 +166,7 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1) {
   if (cap < 16) cap = 16;
   p.cap = cap;
   size_t table = ix->kind == BBC_KIND_PQ ? (size_t)ix->M * 256 * 4 : (size_t)ix->D * 4;
-  p.per_query = (size_t)ix->nlist * 4 + (size_t)nprobe * 20 + 4 + 4 + 8 + kCells * 4 + 4 + 4 +
+  p.per_query = (size_t)ix->nlist * 4 + (size_t)nprobe * 20 + 8 + 4 + 8 + kCells * 4 + 4 + 4 +
                 table + (size_t)cap * 13 + (size_t)ix->d * 4 + (size_t)k * 12 + 64 +
                 (size_t)((cap + kChunk - 1) / kChunk) * 8 + (size_t)(nprobe + 1) * 4;
   p.per_query += 8 + 8 + kCells * 4 + 4 + 4 + (size_t)4 * world;   // DistBuf
@@ -194,6 +195,7 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, 
   b.poff = (int*)take((size_t)nqb * (nprobe + 1) * 4);
   b.popad = (int*)take((size_t)nqb * (nprobe + 1) * 4);
   b.rbase = (long long*)take((size_t)nqb * nprobe * 8);
+  b.qperm = (int*)take((size_t)nqb * 4);
   b.nsamp = (int*)take((size_t)nqb * 4);
   b.edges = (float*)take((size_t)nqb * 8);
   b.hist = (int*)take((size_t)nqb * kCells * 4);
@@ -231,6 +233,11 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, 
 template <typename Kern>
 void set_smem(Kern kern, size_t bytes) {
   if (bytes > 0) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+__global__ void k_iota(int* p, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = i;
 }
 
 __global__ void k_debug_cands(const int* cpos, const float* val, const int* ncand, long long cap,
@@ -358,6 +365,17 @@ void stage_probe(Shard& s, cudaStream_t st) {
   }
   k_probe_select<<<s.b.nq, kSelNT, 0, st>>>(s.b, s.dv);
   g_launches += 2;
+  if (s.b.nq > 0) {
+    int P2 = 1;
+    while (P2 < s.b.nq) P2 <<= 1;
+    if (P2 <= kQpermMax) {
+      set_smem(k_qperm, (size_t)P2 * 8);
+      k_qperm<<<1, 1024, (size_t)P2 * 8, st>>>(s.b, ix->lrank, const_cast<int*>(s.b.qperm));
+    } else {
+      k_iota<<<(s.b.nq + 255) / 256, 256, 0, st>>>(const_cast<int*>(s.b.qperm), s.b.nq);
+    }
+    g_launches += 1;
+  }
 }
 
 void stage_tables(Shard& s, cudaStream_t st) {
@@ -927,6 +945,23 @@ bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_
       mx = std::max(mx, a);
     }
     ix->cmax = (float)(std::sqrt(mx) * (1.0 + 1e-6));
+    // list regions for the query locality order: nearest of 256 evenly spaced pivot centroids
+    const int npiv = std::min(256, nlist);
+    std::vector<int> lr(nlist);
+    for (int c = 0; c < nlist; ++c) {
+      int best = 0;
+      double bd = 1e300;
+      for (int pv = 0; pv < npiv; ++pv) {
+        const float* a = &C[(size_t)c * d];
+        const float* bb = &C[(size_t)((long long)pv * nlist / npiv) * d];
+        double s2 = 0.0;
+        for (int t = 0; t < d; ++t) { const double y = (double)a[t] - bb[t]; s2 += y * y; }
+        if (s2 < bd) { bd = s2; best = pv; }
+      }
+      lr[c] = (best << 20) | c;
+    }
+    ok = ok && dalloc((void**)&ix->lrank, (size_t)nlist * 4) &&
+         cudaMemcpy(ix->lrank, lr.data(), (size_t)nlist * 4, cudaMemcpyHostToDevice) == cudaSuccess;
     ok = ok && dalloc((void**)&ix->cmu, (size_t)d * 4) && dalloc((void**)&ix->cnorm, (size_t)nlist * 4) &&
          cudaMemcpy(ix->cmu, mu.data(), (size_t)d * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
          cudaMemcpy(ix->cnorm, cn.data(), (size_t)nlist * 4, cudaMemcpyHostToDevice) == cudaSuccess;
@@ -980,7 +1015,7 @@ void ivf_free(bbc_index ix) {
   cudaSetDevice(ix->device);
   void* ptrs[] = {ix->centroids, ix->loff, ix->gsize_d, ix->ids, ix->books, ix->codes, ix->P,
                   ix->wL, ix->bits, ix->factors, ix->raw, ix->stats, ix->codes_t, ix->tbase,
-                  ix->cmu, ix->cnorm, ix->rbq_tiles, ix->rbq_pc};
+                  ix->cmu, ix->cnorm, ix->rbq_tiles, ix->rbq_pc, ix->lrank};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& t : ix->timers) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }

@@ -36,6 +36,7 @@ struct Batch {
   int* cid;           // [nq x cap]  candidate original ids
   float* val;         // [nq x cap]  sample estimates, then exact d^2 of candidates
   long long* stats;   // [3] sum n_o, sum |S*|, sum sample objects
+  const int* qperm;   // [nq] locality order of the queries (k_qperm): CTA row y -> query qperm[y]
   int* chunk;         // [nq x nchunk]  per-chunk candidate counts -> offsets (compaction)
   int* chunkj;        // [nq x nchunk]  probed list holding each chunk's first element
 };
@@ -336,6 +337,32 @@ __global__ void __launch_bounds__(kSelNT) k_probe_select(Batch b, Dev ix) {
   }
 }
 
+// Locality order of the micro-batch's queries: sorted by (region of the nearest list, nearest
+// list, query), region = nearest of 256 pivot centroids (ivf_load).  Queries of one region
+// probe mostly the same lists, so scheduling their scan / re-rank CTAs together turns some
+// repeated code and row reads into L2 hits.  Only the order of CTAs changes, never a result.
+// One CTA, bitonic sort of (lrank[probe[q][0]] << 32 | q).
+constexpr int kQpermMax = 1 << 14;          // 128 KB of keys
+__global__ void __launch_bounds__(1024) k_qperm(Batch b, const int* lrank, int* perm) {
+  extern __shared__ unsigned long long qk[];
+  int P2 = 1;
+  while (P2 < b.nq) P2 <<= 1;
+  for (int i = threadIdx.x; i < P2; i += 1024)
+    qk[i] = i < b.nq ? ((unsigned long long)lrank[b.probe[(size_t)i * b.nprobe]] << 32) | (unsigned)i : ~0ull;
+  __syncthreads();
+  for (int size = 2; size <= P2; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < P2 / 2; i += 1024) {
+        const int lo = 2 * stride * (i / stride) + (i % stride), hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const unsigned long long a = qk[lo], c = qk[hi];
+        if ((a > c) == up) { qk[lo] = c; qk[hi] = a; }
+      }
+      __syncthreads();
+    }
+  for (int i = threadIdx.x; i < b.nq; i += 1024) perm[i] = (int)(qk[i] & 0xffffffffu);
+}
+
 // ------------------------------------------------------------------------------------------
 // a2  PQ lookup table: LUT[q][m][c] = sum_t (q_t - C[m][c][t])^2, t ascending (canonical)
 // ------------------------------------------------------------------------------------------
@@ -479,7 +506,7 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
   int* gcnt = reinterpret_cast<int*>(rsm + kRqOffCnt);
   int* hist = reinterpret_cast<int*>(rsm + kRqOffHist);
   int* s_popad = reinterpret_cast<int*>(rsm + kRqOffPo);
-  const int q = blockIdx.y;
+  const int q = b.qperm[blockIdx.y];        // neighbours run together: L2 reuse
   const int ns = b.nsamp[q];
   if (mode != 2 && ns == 0) return;                  // tau = infinity: nothing to bucket
   const int first = mode == 1 ? ns : 0;
@@ -1042,7 +1069,7 @@ constexpr int kRrNT = 256;
 template <bool U8, int LPC, int MAXV, int STEPS, int MINB = 1>
 __global__ void __launch_bounds__(kRrNT, MINB) k_rerank(Batch b, Dev ix) {
   constexpr int CPW = 32 / LPC;                       // candidates per warp step
-  const int q = blockIdx.y;
+  const int q = b.qperm[blockIdx.y];        // neighbours run together: L2 reuse
   const int lane = threadIdx.x & 31, sub = lane / LPC, sl = lane % LPC;
   const int d = ix.d;
   const int rowb = U8 ? d : d * 4;

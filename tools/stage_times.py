@@ -28,7 +28,7 @@ g = Index(path)
 if a.probe_simt:
     g.set_probe_mode(g.PROBE_SIMT)
 q = torch.from_numpy(synth.generate_queries(cfg)).cuda()
-ws = g.workspace(len(q), cfg.k, a.nprobe, a.budget)
+ws = g.workspace(len(q), cfg.k, a.nprobe, a.budget, max_bytes=48 << 30)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for _ in range(3):
     ids, d2 = g.search(q, cfg.k, a.nprobe, a.budget, workspace=ws)
