@@ -22,7 +22,8 @@ EXPORTS = ("ivf_load", "ivf_free", "bbc_index_info", "bbc_workspace_size", "bbc_
            "bbc_search",
            "bbc_search_host", "bbc_search_debug", "bbc_set_timing", "bbc_get_timing",
            "bbc_last_stats", "bbc_launch_count", "bbc_last_error", "bbc_nccl_unique_id",
-           "bbc_comm_init", "bbc_search_group", "bbc_last_stats2")
+           "bbc_comm_init", "bbc_search_group", "bbc_last_stats2", "bbc_set_probe_mode",
+           "bbc_set_scan_mode", "bbc_stats_vector")
 
 STAGES = ("probe", "tables", "sample", "scan", "compact", "rerank", "select", "comm")
 TAU_INF = 1 << 30
@@ -94,7 +95,8 @@ def lib() -> ctypes.CDLL:
         for fn in ("ivf_load", "bbc_index_info", "bbc_workspace_size", "bbc_search",
                    "bbc_search_host", "bbc_search_debug", "bbc_set_timing", "bbc_get_timing",
                    "bbc_last_stats", "bbc_query_capacity", "bbc_nccl_unique_id",
-                   "bbc_comm_init", "bbc_search_group", "bbc_last_stats2"):
+                   "bbc_comm_init", "bbc_search_group", "bbc_last_stats2", "bbc_set_probe_mode",
+           "bbc_set_scan_mode", "bbc_stats_vector"):
             getattr(L, fn).restype = ctypes.c_int
         _lib = L
     return _lib
