@@ -395,12 +395,13 @@ def main():
     if rq > 0 and not args.profile_steps:
         X = database_in_id_order(path)
         gi, gd = groundtruth.cached_topk(f"{cfg.name}_{os.path.basename(path)}", Qh[:rq], X, k,
-                                         datagen.cache_dir())
+                                         datagen.cache_dir(), metric=cfg.metric)
         ids = out[0][:rq].cpu().numpy()
-        ex = groundtruth.exact_of(Qh[:rq], X, ids)
+        ex = groundtruth.exact_of(Qh[:rq], X, ids, metric=cfg.metric)
         rec = {"recall": groundtruth.recall(ids, ex, gi, gd),
-               "relative_error": groundtruth.relative_error(out[1][:rq].cpu().numpy(), gd),
-               "queries": rq}
+               "relative_error": (groundtruth.relative_error(out[1][:rq].cpu().numpy(), gd)
+                                  if cfg.metric == "l2" else None),
+               "metric": cfg.metric, "queries": rq}
     cpu = None
     if world == 1 and not args.no_cpu_baseline and not args.profile_steps:
         cpu = cpu_baseline(cfg, path, nprobe, budget, args.cpu_seconds)
@@ -440,7 +441,7 @@ def sweep(cfg, path, g, rank):
     q = torch.from_numpy(Q).cuda()
     rq = 100
     gi, gd = groundtruth.cached_topk(f"{cfg.name}_{os.path.basename(path)}", Q[:rq], X, cfg.k,
-                                     datagen.cache_dir())
+                                     datagen.cache_dir(), metric=cfg.metric)
     st = torch.cuda.current_stream()
     for nprobe in sorted({cfg.nprobe, 2 * cfg.nprobe, 3 * cfg.nprobe, 4 * cfg.nprobe,
                           6 * cfg.nprobe, 8 * cfg.nprobe}):
@@ -458,7 +459,7 @@ def sweep(cfg, path, g, rank):
             torch.cuda.synchronize()
             ms = a.elapsed_time(b)
             idn = ids[:rq].cpu().numpy()
-            r = groundtruth.recall(idn, groundtruth.exact_of(Q[:rq], X, idn), gi, gd)
+            r = groundtruth.recall(idn, groundtruth.exact_of(Q[:rq], X, idn, metric=cfg.metric), gi, gd)
             s = g.last_stats()
             print(json.dumps({"sweep": cfg.name, "nprobe": nprobe, "budget": budget,
                               "recall": round(r, 4), "qps": len(Q) / (ms / 1e3), "ms": ms,

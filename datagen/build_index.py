@@ -133,7 +133,10 @@ def build(cfg: Config, X: np.ndarray | None = None, verbose: bool = False) -> di
     sizes = np.bincount(lab, minlength=cfg.nlist)
     offsets = np.zeros(cfg.nlist + 1, dtype=np.int64)
     np.cumsum(sizes, out=offsets[1:])
+    if cfg.metric == "ip" and cfg.kind != "pq":
+        raise ValueError("the inner-product metric is built for PQ indexes only")
     out = dict(kind=cfg.kind, raw_dtype=cfg.raw_dtype, N=N, d=d, nlist=cfg.nlist, seed=cfg.seed,
+               metric=cfg.metric,
                centroids=cent, list_offsets=offsets, ids=order.astype(np.int64),
                raw=np.ascontiguousarray(X[order]))
     if verbose:

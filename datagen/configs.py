@@ -38,6 +38,7 @@ class Config:
     kmeans_train_per_list: int = 64
     pq_train: int = 65536
     pq_iters: int = 12
+    metric: str = "l2"   # "l2" (squared L2) or "ip" (inner product, keys -<q,x>)
     extra: dict = field(default_factory=dict, compare=False, hash=False)
 
     @property
@@ -77,7 +78,15 @@ SMALL = {
                       kmeans_iters=6),
 }
 
-ALL = {**FULL, **SMALL}
+# Inner-product / cosine variants ("our result buffer
+# applies to ... cosine similarity and inner product"): the C4 generator's vectors are unit norm,
+# so inner product = cosine similarity.  The IVF lists are the same L2 k-means lists.
+IP = {
+    "C4ip": C4.replace(name="C4ip", metric="ip"),
+    "C4ip_s": SMALL["C4s"].replace(name="C4ip_s", metric="ip"),
+}
+
+ALL = {**FULL, **SMALL, **IP}
 
 
 def get(name: str) -> Config:

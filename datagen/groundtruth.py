@@ -14,23 +14,27 @@ import os
 import numpy as np
 
 
-def _sqdist(Q: np.ndarray, X: np.ndarray, chunk: int = 1 << 17) -> np.ndarray:
+def _sqdist(Q: np.ndarray, X: np.ndarray, chunk: int = 1 << 17, metric: str = "l2") -> np.ndarray:
+    """fp64 keys: squared L2, or -<q, x> for the inner-product metric."""
     Q64 = np.asarray(Q, dtype=np.float64)
     qn = (Q64 * Q64).sum(1)
     out = np.empty((len(Q), len(X)), dtype=np.float64)
     for lo in range(0, len(X), chunk):
         xb = np.asarray(X[lo:lo + chunk], dtype=np.float64)
-        out[:, lo:lo + len(xb)] = np.maximum(0.0, qn[:, None] + (xb * xb).sum(1)[None] - 2.0 * (Q64 @ xb.T))
+        if metric == "ip":
+            out[:, lo:lo + len(xb)] = -(Q64 @ xb.T)
+        else:
+            out[:, lo:lo + len(xb)] = np.maximum(0.0, qn[:, None] + (xb * xb).sum(1)[None] - 2.0 * (Q64 @ xb.T))
     return out
 
 
-def topk(Q: np.ndarray, X: np.ndarray, k: int, block: int = 16):
+def topk(Q: np.ndarray, X: np.ndarray, k: int, block: int = 16, metric: str = "l2"):
     """(ids int64 [nq x k], d2 fp64 [nq x k]) exact, ordered by (d2, id)."""
     nq = len(Q)
     gi = np.empty((nq, k), dtype=np.int64)
     gd = np.empty((nq, k), dtype=np.float64)
     for lo in range(0, nq, block):
-        D = _sqdist(Q[lo:lo + block], X)
+        D = _sqdist(Q[lo:lo + block], X, metric=metric)
         for r in range(len(D)):
             d = D[r]
             cand = np.argpartition(d, k - 1)[:k] if k < len(d) else np.arange(len(d))
@@ -42,23 +46,26 @@ def topk(Q: np.ndarray, X: np.ndarray, k: int, block: int = 16):
     return gi, gd
 
 
-def cached_topk(tag: str, Q: np.ndarray, X: np.ndarray, k: int, cache_dir: str):
+def cached_topk(tag: str, Q: np.ndarray, X: np.ndarray, k: int, cache_dir: str, metric: str = "l2"):
     path = os.path.join(cache_dir, f"gt_{tag}_{len(Q)}_{k}.npz")
     if os.path.exists(path):
         z = np.load(path)
         return z["ids"], z["d2"]
-    gi, gd = topk(Q, X, k)
+    gi, gd = topk(Q, X, k, metric=metric)
     np.savez(path, ids=gi, d2=gd)
     return gi, gd
 
 
-def exact_of(Q: np.ndarray, X: np.ndarray, ids: np.ndarray) -> np.ndarray:
-    """fp64 exact d^2 of the returned ids (inf for padding ids < 0)."""
+def exact_of(Q: np.ndarray, X: np.ndarray, ids: np.ndarray, metric: str = "l2") -> np.ndarray:
+    """fp64 exact keys of the returned ids (inf for padding ids < 0)."""
     out = np.full(ids.shape, np.inf)
     for i in range(len(Q)):
         ok = ids[i] >= 0
         rows = np.asarray(X[ids[i][ok]], dtype=np.float64)
-        out[i][ok] = ((rows - Q[i].astype(np.float64)) ** 2).sum(1)
+        if metric == "ip":
+            out[i][ok] = -(rows @ Q[i].astype(np.float64))
+        else:
+            out[i][ok] = ((rows - Q[i].astype(np.float64)) ** 2).sum(1)
     return out
 
 
@@ -72,6 +79,7 @@ def recall(ids: np.ndarray, d2_exact: np.ndarray, gt_ids: np.ndarray, gt_d2: np.
 
 
 def relative_error(d2: np.ndarray, gt_d2: np.ndarray) -> float:
+    """Squared-L2 keys only (Euclidean ratios); None-free: callers skip it for inner product."""
     r = np.sqrt(np.sort(np.asarray(d2, dtype=np.float64), axis=1))
     g = np.sqrt(np.sort(np.asarray(gt_d2, dtype=np.float64), axis=1))
     m = (g > 0) & np.isfinite(r)

@@ -6,6 +6,7 @@ Layout (little-endian; DESIGN.md section 4 is the normative copy, `include/bbc.h
   bytes [8, 256)    31 x int64 header fields:
                       0 version(=1)  1 kind(1=PQ, 2=RaBitQ)  2 raw_dtype(0=f32, 1=u8)
                       3 N  4 d  5 nlist  6 M  7 nbits  8 D  9 seed  10 n_sections(=10)
+                      11 metric (0 = squared L2, 1 = inner product; keys are -<q, x>)
   bytes [256, 416)  section table: 10 x (int64 offset, int64 nbytes); offset 0 = absent
   sections, each 256-byte aligned, in this order:
       0 centroids    f32 [nlist x d]
@@ -33,6 +34,7 @@ SECTIONS = ("centroids", "list_offsets", "ids", "codebooks", "codes", "P", "wL",
             "factors", "raw")
 KIND = {"pq": 1, "rabitq": 2}
 RAW = {"f32": 0, "u8": 1}
+METRIC = {"l2": 0, "ip": 1}
 
 
 def _align(x: int, a: int = 256) -> int:
@@ -53,6 +55,7 @@ def write(path: str, idx: dict) -> None:
     hdr[8] = idx.get("D", 0)
     hdr[9] = idx.get("seed", 0)
     hdr[10] = len(SECTIONS)
+    hdr[11] = METRIC[idx.get("metric", "l2")]
     want = {
         "centroids": np.float32, "list_offsets": np.int64, "ids": np.int64,
         "codebooks": np.float32, "codes": np.uint8, "P": np.float32, "wL": np.float32,
@@ -102,8 +105,9 @@ def read(path: str, mmap: bool = True) -> dict:
         "bits": ((N, D // 8), np.uint8), "factors": ((N, 2), np.float32),
         "raw": ((N, d), np.uint8 if raw_dtype == "u8" else np.float32),
     }
+    metric = {v: k for k, v in METRIC.items()}[int(hdr[11])]
     out = dict(kind=kind, raw_dtype=raw_dtype, N=N, d=d, nlist=nlist, M=M, nbits=nbits, D=D,
-               seed=seed)
+               seed=seed, metric=metric)
     for i, name in enumerate(SECTIONS):
         off, nb = (int(x) for x in table[i])
         if off == 0:

@@ -53,6 +53,13 @@ typedef enum {
 /* Index kinds (file header field `kind`). */
 #define BBC_KIND_PQ 1      /* 8-bit product quantization, M sub-quantizers of 256 codewords   */
 #define BBC_KIND_RABITQ 2  /* 1-bit RaBitQ codes over a random rotation, factors (r_o, g_o)  */
+/* Metric of an index (header field 11).  Every distance the library handles is a key where
+ * smaller is better: squared L2, or for inner product the negated similarity -<q, x> (the
+ * result buffer "applies to ... cosine similarity and inner product"; cosine =
+ * inner product of unit-norm vectors).  IP is supported for PQ indexes (BBC_ERR_FORMAT for
+ * RaBitQ); its out_d2 holds -<q, x>. */
+#define BBC_METRIC_L2 0
+#define BBC_METRIC_IP 1
 
 /*
  * ivf_load -- read a BBCIVF01 index file (layout: DESIGN.md section 4 / datagen/index_file.py):
@@ -80,6 +87,7 @@ typedef struct {
   int64_t n_local;     /* objects held by this rank                    */
   int32_t max_list;    /* largest list size                            */
   int32_t rank, world; /* shard of this handle                         */
+  int32_t metric;      /* BBC_METRIC_L2 or BBC_METRIC_IP               */
 } bbc_index_info_t;
 
 bbc_status bbc_index_info(bbc_index index, bbc_index_info_t* info);

@@ -32,6 +32,12 @@ below, with each +,-,*,/ rounded separately (no fused multiply-add): that is the
 precision, and both sides take the decision in it.  Exact re-rank distances are accumulated in
 fp64 and rounded to fp32 once.
 
+Metrics (the result buffer "applies to ... cosine
+similarity and inner product").  Squared L2 is the default.  For an inner-product index
+(ix["metric"] == "ip", PQ only) every key is the negated similarity, so "smaller is better"
+everywhere: probe key -<q, c_j>, LUT[m][c] = -<q_m, C[m][c]>, estimate = sum of LUT entries,
+exact key -<q, x>; the sample, buckets, threshold, superset and selection are unchanged.
+
 Parity pins (tests/test_oracle.py): brute force on tiny inputs, the LUT identity, the closed form
 tau = cell(budget-th smallest estimate), the superset invariants, Fig. 3 of the paper, Eq. 3, the
 RaBitQ closed forms and error bound, and full-probe/unlimited-budget == brute force.
@@ -49,20 +55,25 @@ SAMPLE_MIN_LISTS = 8       # "5-10 nearest clusters", reading R5
 # ----------------------------------------------------------------------------------------------
 # O1  coarse probe
 # ----------------------------------------------------------------------------------------------
-def coarse_d2(Q: np.ndarray, C: np.ndarray) -> np.ndarray:
-    """d^2(q, c_j) [nq x nlist]: acc = 0; for t ascending: diff = q_t - c_t; acc = acc + diff*diff."""
+def coarse_d2(Q: np.ndarray, C: np.ndarray, metric: str = "l2") -> np.ndarray:
+    """Probe keys [nq x nlist].  L2: acc = 0; for t ascending: diff = q_t - c_t;
+    acc = acc + diff*diff.  IP: acc = 0; for t ascending: acc = acc + q_t*c_t; key = -acc."""
     Q = np.asarray(Q, dtype=F32)
     C = np.asarray(C, dtype=F32)
     acc = np.zeros((len(Q), len(C)), dtype=F32)
     for t in range(Q.shape[1]):
-        diff = Q[:, t, None] - C[None, :, t]
-        acc = acc + diff * diff
-    return acc
+        if metric == "ip":
+            acc = acc + Q[:, t, None] * C[None, :, t]
+        else:
+            diff = Q[:, t, None] - C[None, :, t]
+            acc = acc + diff * diff
+    return -acc if metric == "ip" else acc
 
 
-def probe(Q: np.ndarray, C: np.ndarray, nprobe: int):
-    """The nprobe nearest lists per query, nearest first, ties by list id.  -> (probe i32, rq2 f32)."""
-    d2 = coarse_d2(Q, C)
+def probe(Q: np.ndarray, C: np.ndarray, nprobe: int, metric: str = "l2"):
+    """The nprobe nearest lists per query (smallest keys), ties by list id.
+    -> (probe i32, rq2 f32 = the probe keys)."""
+    d2 = coarse_d2(Q, C, metric)
     nq, nlist = d2.shape
     pr = np.empty((nq, nprobe), dtype=np.int32)
     rq = np.empty((nq, nprobe), dtype=F32)
@@ -77,15 +88,19 @@ def probe(Q: np.ndarray, C: np.ndarray, nprobe: int):
 # ----------------------------------------------------------------------------------------------
 # O2/O3  PQ
 # ----------------------------------------------------------------------------------------------
-def pq_lut(q: np.ndarray, books: np.ndarray) -> np.ndarray:
-    """LUT[m][c] = sum_{t < dsub} (q[m*dsub + t] - C[m][c][t])^2, t ascending, fp32 [M x 256]."""
+def pq_lut(q: np.ndarray, books: np.ndarray, metric: str = "l2") -> np.ndarray:
+    """LUT[m][c] = sum_{t < dsub} (q[m*dsub + t] - C[m][c][t])^2, t ascending, fp32 [M x 256];
+    inner product: LUT[m][c] = -(sum_t q[m*dsub + t] * C[m][c][t]), t ascending."""
     M, K, ds = books.shape
     qs = np.asarray(q, dtype=F32).reshape(M, ds)
     acc = np.zeros((M, K), dtype=F32)
     for t in range(ds):
-        diff = qs[:, t, None] - books[:, :, t]
-        acc = acc + diff * diff
-    return acc
+        if metric == "ip":
+            acc = acc + qs[:, t, None] * books[:, :, t]
+        else:
+            diff = qs[:, t, None] - books[:, :, t]
+            acc = acc + diff * diff
+    return -acc if metric == "ip" else acc
 
 
 def pq_est(lut: np.ndarray, codes: np.ndarray) -> np.ndarray:
@@ -214,8 +229,10 @@ def threshold(H: np.ndarray, budget: int) -> int:
 # ----------------------------------------------------------------------------------------------
 # O9  exact re-rank and final selection
 # ----------------------------------------------------------------------------------------------
-def exact_d2(q: np.ndarray, rows: np.ndarray) -> np.ndarray:
-    """||q - x||^2 accumulated in fp64, rounded to fp32 once."""
+def exact_d2(q: np.ndarray, rows: np.ndarray, metric: str = "l2") -> np.ndarray:
+    """||q - x||^2 (inner product: -<q, x>) accumulated in fp64, rounded to fp32 once."""
+    if metric == "ip":
+        return (-(rows.astype(np.float64) @ np.asarray(q, dtype=np.float64))).astype(F32)
     diff = rows.astype(np.float64) - np.asarray(q, dtype=np.float64)[None, :]
     return (diff * diff).sum(1).astype(F32)
 
@@ -251,7 +268,10 @@ def search(ix: dict, Q: np.ndarray, k: int, nprobe: int, budget: int, want_debug
     off = np.asarray(ix["list_offsets"])
     ids_all = ix["ids"]
     raw = ix["raw"]
-    pr, rq = probe(Q, ix["centroids"], nprobe) if probe_result is None else probe_result
+    metric = ix.get("metric", "l2")
+    if metric == "ip" and ix["kind"] != "pq":
+        raise ValueError("the inner-product metric is defined for PQ indexes only")
+    pr, rq = probe(Q, ix["centroids"], nprobe, metric) if probe_result is None else probe_result
     out_ids = np.empty((nq, k), dtype=np.int64)
     out_d2 = np.empty((nq, k), dtype=F32)
     dbg = []
@@ -260,7 +280,7 @@ def search(ix: dict, Q: np.ndarray, k: int, nprobe: int, budget: int, want_debug
         sizes = off[lists + 1] - off[lists]
         pos = np.concatenate([np.arange(off[L], off[L + 1]) for L in lists])  # probe order
         if ix["kind"] == "pq":
-            lut = pq_lut(Q[i], ix["codebooks"])
+            lut = pq_lut(Q[i], ix["codebooks"], metric)
             est = pq_est(lut, np.asarray(ix["codes"][pos]))
         else:
             u = rabitq_rotate(Q[i], ix["P"])
@@ -288,7 +308,7 @@ def search(ix: dict, Q: np.ndarray, k: int, nprobe: int, budget: int, want_debug
             sup = np.flatnonzero(cell <= tau)
         spos = pos[sup]
         sid = np.asarray(ids_all[spos])
-        d2 = exact_d2(Q[i], np.asarray(raw[spos]))
+        d2 = exact_d2(Q[i], np.asarray(raw[spos]), metric)
         out_ids[i], out_d2[i] = select_topk(d2, sid, k)
         if want_debug:
             dbg.append(dict(probe=lists, rq2=rq[i], n_o=n_o, s=s, d_min=dmin, d_max=dmax, H=H,

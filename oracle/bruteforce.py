@@ -12,25 +12,29 @@ from __future__ import annotations
 import numpy as np
 
 
-def exact_all(q: np.ndarray, X: np.ndarray, chunk: int = 1 << 18) -> np.ndarray:
-    """fp64 ||q - x||^2 for every row of X (norm expansion in fp64)."""
+def exact_all(q: np.ndarray, X: np.ndarray, chunk: int = 1 << 18, metric: str = "l2") -> np.ndarray:
+    """fp64 ||q - x||^2 for every row of X (norm expansion in fp64); inner product: -<q, x>."""
     q64 = np.asarray(q, dtype=np.float64)
     qn = q64 @ q64
     out = np.empty(len(X), dtype=np.float64)
     for lo in range(0, len(X), chunk):
         xb = np.asarray(X[lo:lo + chunk], dtype=np.float64)
-        out[lo:lo + len(xb)] = np.maximum(0.0, qn + (xb * xb).sum(1) - 2.0 * (xb @ q64))
+        if metric == "ip":
+            out[lo:lo + len(xb)] = -(xb @ q64)
+        else:
+            out[lo:lo + len(xb)] = np.maximum(0.0, qn + (xb * xb).sum(1) - 2.0 * (xb @ q64))
     return out
 
 
-def ground_truth(Q: np.ndarray, X: np.ndarray, k: int):
-    """(ids int64 [nq x k], d2 fp64 [nq x k]) of the exact k nearest rows, ordered by (d2, id)."""
+def ground_truth(Q: np.ndarray, X: np.ndarray, k: int, metric: str = "l2"):
+    """(ids int64 [nq x k], d2 fp64 [nq x k]) of the exact k nearest rows (smallest keys),
+    ordered by (key, id)."""
     nq = len(Q)
     gi = np.empty((nq, k), dtype=np.int64)
     gd = np.empty((nq, k), dtype=np.float64)
     ids = np.arange(len(X))
     for i in range(nq):
-        d2 = exact_all(Q[i], X)
+        d2 = exact_all(Q[i], X, metric=metric)
         cand = np.argpartition(d2, k - 1)[:k] if k < len(X) else ids
         kth = d2[cand].max()
         cand = np.flatnonzero(d2 <= kth)                  # keep every tie of the k-th distance

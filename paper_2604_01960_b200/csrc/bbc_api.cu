@@ -38,7 +38,7 @@ struct Timer {
 struct bbc_index_s {
   int device = 0;
   int rank = 0, world = 1;
-  int kind = 0, d = 0, nlist = 0, M = 0, D = 0, raw_u8 = 0;
+  int kind = 0, d = 0, nlist = 0, M = 0, D = 0, raw_u8 = 0, metric = BBC_METRIC_L2;
   long long N = 0, n_local = 0;
   int max_list = 0;
   std::vector<int> lsize;               // local list sizes
@@ -101,7 +101,7 @@ namespace {
 Dev dev_view(const bbc_index_s* ix) {
   Dev v;
   v.kind = ix->kind; v.d = ix->d; v.nlist = ix->nlist; v.M = ix->M; v.D = ix->D;
-  v.raw_u8 = ix->raw_u8; v.n_local = ix->n_local;
+  v.raw_u8 = ix->raw_u8; v.n_local = ix->n_local; v.metric = ix->metric;
   v.centroids = ix->centroids; v.loff = ix->loff; v.gsize = ix->gsize_d; v.ids = ix->ids;
   v.books = ix->books; v.codes = ix->codes; v.P = ix->P; v.wL = ix->wL; v.bits = ix->bits;
   v.factors = ix->factors; v.raw = ix->raw;
@@ -361,7 +361,10 @@ void stage_probe(Shard& s, cudaStream_t st) {
                                             s.b.nq, ix->nlist, ix->d);
   } else {
     dim3 g1((ix->nlist + kPT - 1) / kPT, (s.b.nq + kPT - 1) / kPT);
-    k_probe_d2<<<g1, 256, 0, st>>>(s.b.Q, ix->centroids, s.b.coarse, s.b.nq, ix->nlist, ix->d);
+    if (ix->metric == BBC_METRIC_IP)
+      k_probe_d2<true><<<g1, 256, 0, st>>>(s.b.Q, ix->centroids, s.b.coarse, s.b.nq, ix->nlist, ix->d);
+    else
+      k_probe_d2<false><<<g1, 256, 0, st>>>(s.b.Q, ix->centroids, s.b.coarse, s.b.nq, ix->nlist, ix->d);
   }
   k_probe_select<<<s.b.nq, kSelNT, 0, st>>>(s.b, s.dv);
   g_launches += 2;
@@ -476,6 +479,22 @@ void stage_compact(Shard& s, cudaStream_t st) {
   g_launches += 4;
 }
 
+template <bool IP>
+void launch_rerank(Shard& s, dim3 g, cudaStream_t st, int rowb) {
+  const bool u8 = s.ix->raw_u8 != 0;
+  if (rowb <= 128) {
+    if (u8) k_rerank<true, 8, 1, 4, 4, IP><<<g, kRrNT, 0, st>>>(s.b, s.dv);
+    else k_rerank<false, 8, 1, 4, 4, IP><<<g, kRrNT, 0, st>>>(s.b, s.dv);
+  } else if (rowb <= 512) {
+    if (u8) k_rerank<true, 8, 4, 1, 4, IP><<<g, kRrNT, 0, st>>>(s.b, s.dv);
+    else k_rerank<false, 8, 4, 1, 4, IP><<<g, kRrNT, 0, st>>>(s.b, s.dv);
+  } else if (rowb <= 1024) {
+    k_rerank<false, 8, 8, 1, 3, IP><<<g, kRrNT, 0, st>>>(s.b, s.dv);
+  } else {
+    k_rerank<false, 32, 8, 1, 2, IP><<<g, kRrNT, 0, st>>>(s.b, s.dv);
+  }
+}
+
 void stage_rerank(Shard& s, cudaStream_t st) {
   bbc_index_s* ix = s.ix;
   StageScope sc(ix, st, BBC_STAGE_RERANK);
@@ -487,17 +506,8 @@ void stage_rerank(Shard& s, cudaStream_t st) {
   // lanes per candidate and 16-byte chunks per lane by row size; one row per lane group in
   // flight and high occupancy (4 CTAs/SM) beat deeper per-warp unrolling (tuned on C2: 1.55 ms
   // with 2 rows in flight at 2 CTAs/SM -> 0.92 ms)
-  if (rowb <= 128) {
-    if (ix->raw_u8) k_rerank<true, 8, 1, 4, 4><<<g, kRrNT, 0, st>>>(s.b, s.dv);
-    else k_rerank<false, 8, 1, 4, 4><<<g, kRrNT, 0, st>>>(s.b, s.dv);
-  } else if (rowb <= 512) {
-    if (ix->raw_u8) k_rerank<true, 8, 4, 1, 4><<<g, kRrNT, 0, st>>>(s.b, s.dv);
-    else k_rerank<false, 8, 4, 1, 4><<<g, kRrNT, 0, st>>>(s.b, s.dv);
-  } else if (rowb <= 1024) {
-    k_rerank<false, 8, 8, 1, 3><<<g, kRrNT, 0, st>>>(s.b, s.dv);
-  } else {
-    k_rerank<false, 32, 8, 1, 2><<<g, kRrNT, 0, st>>>(s.b, s.dv);
-  }
+  if (ix->metric == BBC_METRIC_IP) launch_rerank<true>(s, g, st, rowb);
+  else launch_rerank<false>(s, g, st, rowb);
   g_launches += 1;
 }
 
@@ -804,6 +814,15 @@ bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_
     fclose(f);
     return fail(BBC_ERR_FORMAT, "RaBitQ needs D a multiple of 64, D >= d");
   }
+  const int metric = (int)hdr[11];
+  if (metric != BBC_METRIC_L2 && metric != BBC_METRIC_IP) {
+    fclose(f);
+    return fail(BBC_ERR_FORMAT, "unknown metric");
+  }
+  if (metric == BBC_METRIC_IP && kind != BBC_KIND_PQ) {
+    fclose(f);
+    return fail(BBC_ERR_FORMAT, "the inner-product metric is supported for PQ indexes only");
+  }
   if (raw_u8 ? (d % 16 != 0 || d > 512) : (d % 4 != 0 || d > 1024)) {
     fclose(f);
     return fail(BBC_ERR_FORMAT, "d must be a multiple of 4 and <= 1024 (f32) or of 16 and <= 512 (u8)");
@@ -833,6 +852,7 @@ bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_
   ix = new bbc_index_s();
   ix->device = cuda_device; ix->rank = rank; ix->world = world;
   ix->kind = kind; ix->d = d; ix->nlist = nlist; ix->M = M; ix->D = D; ix->raw_u8 = raw_u8;
+  ix->metric = metric;
   ix->N = N;
   ix->gsize.resize(nlist);
   for (int L = 0; L < nlist; ++L) ix->gsize[L] = (int)(goff[L + 1] - goff[L]);
@@ -965,7 +985,7 @@ bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_
     ok = ok && dalloc((void**)&ix->cmu, (size_t)d * 4) && dalloc((void**)&ix->cnorm, (size_t)nlist * 4) &&
          cudaMemcpy(ix->cmu, mu.data(), (size_t)d * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
          cudaMemcpy(ix->cnorm, cn.data(), (size_t)nlist * 4, cudaMemcpyHostToDevice) == cudaSuccess;
-    ix->probe_tc_ok = d <= kMaxDimTc;
+    ix->probe_tc_ok = d <= kMaxDimTc && metric == BBC_METRIC_L2;
   }
   if (ok && kind == BBC_KIND_RABITQ && D <= 1024 && D % 64 == 0) {
     std::vector<int2> tiles;
@@ -1047,6 +1067,7 @@ bbc_status bbc_index_info(bbc_index ix, bbc_index_info_t* info) {
   info->n = ix->N; info->d = ix->d; info->nlist = ix->nlist; info->kind = ix->kind;
   info->m = ix->M; info->dpad = ix->D; info->raw_u8 = ix->raw_u8; info->n_local = ix->n_local;
   info->max_list = ix->max_list; info->rank = ix->rank; info->world = ix->world;
+  info->metric = ix->metric;
   return BBC_OK;
 }
 

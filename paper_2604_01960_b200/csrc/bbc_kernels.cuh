@@ -44,6 +44,7 @@ struct Batch {
 // Index arrays on the device.
 struct Dev {
   int kind, d, nlist, M, D, raw_u8;
+  int metric;                    // BBC_METRIC_L2 | BBC_METRIC_IP (keys -<q, x>)
   long long n_local;
   const float* centroids;        // [nlist x d]
   const long long* loff;         // [nlist + 1] local list offsets (rows of this shard)
@@ -67,6 +68,7 @@ struct Dev {
 // a1  coarse probe: canonical d^2 of every (query, centroid), 64 x 64 tiles, 4 x 4 per thread.
 // ------------------------------------------------------------------------------------------
 constexpr int kPT = 64, kPK = 16;
+template <bool IP>
 __global__ void __launch_bounds__(256) k_probe_d2(const float* __restrict__ Q,
                                                   const float* __restrict__ C, float* __restrict__ out,
                                                   int nq, int nlist, int d) {
@@ -98,8 +100,12 @@ __global__ void __launch_bounds__(256) k_probe_d2(const float* __restrict__ Q,
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          float df = __fsub_rn(qv[i], cv[j]);
-          acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(df, df));
+          if (IP) {                                    // inner product: acc += q_t c_t
+            acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(qv[i], cv[j]));
+          } else {
+            float df = __fsub_rn(qv[i], cv[j]);
+            acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(df, df));
+          }
         }
     }
     __syncthreads();
@@ -111,7 +117,7 @@ __global__ void __launch_bounds__(256) k_probe_d2(const float* __restrict__ Q,
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       int cc = c0 + tx + 16 * j;
-      if (cc < nlist) out[(size_t)qq * nlist + cc] = acc[i][j];
+      if (cc < nlist) out[(size_t)qq * nlist + cc] = IP ? -acc[i][j] : acc[i][j];
     }
   }
 }
@@ -372,9 +378,14 @@ __global__ void __launch_bounds__(256) k_pq_lut(Batch b, Dev ix) {
   const float* qv = b.Q + (size_t)q * ix.d + m * ds;
   const float* cb = ix.books + ((size_t)m * 256 + c) * ds;
   float acc = 0.f;
-  for (int t = 0; t < ds; ++t) {
-    float df = __fsub_rn(qv[t], cb[t]);
-    acc = __fadd_rn(acc, __fmul_rn(df, df));
+  if (ix.metric == BBC_METRIC_IP) {                   // LUT[m][c] = -<q_m, C[m][c]>
+    for (int t = 0; t < ds; ++t) acc = __fadd_rn(acc, __fmul_rn(qv[t], cb[t]));
+    acc = -acc;
+  } else {
+    for (int t = 0; t < ds; ++t) {
+      float df = __fsub_rn(qv[t], cb[t]);
+      acc = __fadd_rn(acc, __fmul_rn(df, df));
+    }
   }
   b.table[((size_t)q * ix.M + m) * 256 + c] = acc;
 }
@@ -1066,7 +1077,7 @@ __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chu
 // of the lane split; tolerance 1e-5 relative to the oracle's fp64).
 // ------------------------------------------------------------------------------------------
 constexpr int kRrNT = 256;
-template <bool U8, int LPC, int MAXV, int STEPS, int MINB = 1>
+template <bool U8, int LPC, int MAXV, int STEPS, int MINB = 1, bool IP = false>
 __global__ void __launch_bounds__(kRrNT, MINB) k_rerank(Batch b, Dev ix) {
   constexpr int CPW = 32 / LPC;                       // candidates per warp step
   const int q = b.qperm[blockIdx.y];        // neighbours run together: L2 reuse
@@ -1121,9 +1132,15 @@ __global__ void __launch_bounds__(kRrNT, MINB) k_rerank(Batch b, Dev ix) {
               for (int h = 0; h < 4; ++h)
 #pragma unroll
                 for (int by = 0; by < 4; ++by) {
-                  const float df = (float)((wv[h] >> (8 * by)) & 255u) - __ldg(qv + t * 16 + h * 4 + by);
-                  acc = fmaf(df, df, acc);
+                  const float xv = (float)((wv[h] >> (8 * by)) & 255u), qq = __ldg(qv + t * 16 + h * 4 + by);
+                  if (IP) acc = fmaf(xv, qq, acc);
+                  else { const float df = xv - qq; acc = fmaf(df, df, acc); }
                 }
+            } else if (IP) {
+              acc = fmaf(__uint_as_float(x[s][v].x), qr[v][0], acc);
+              acc = fmaf(__uint_as_float(x[s][v].y), qr[v][1], acc);
+              acc = fmaf(__uint_as_float(x[s][v].z), qr[v][2], acc);
+              acc = fmaf(__uint_as_float(x[s][v].w), qr[v][3], acc);
             } else {
               const float a0 = __uint_as_float(x[s][v].x) - qr[v][0], a1 = __uint_as_float(x[s][v].y) - qr[v][1];
               const float a2 = __uint_as_float(x[s][v].z) - qr[v][2], a3 = __uint_as_float(x[s][v].w) - qr[v][3];
@@ -1136,7 +1153,7 @@ __global__ void __launch_bounds__(kRrNT, MINB) k_rerank(Batch b, Dev ix) {
         }
 #pragma unroll
         for (int o = LPC / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (sl == 0 && kk[s] < n32) vv[cb + kk[s]] = acc;
+        if (sl == 0 && kk[s] < n32) vv[cb + kk[s]] = IP ? -acc : acc;
       }
     }
   }

@@ -85,13 +85,13 @@ def check_final_ids(gi, gd, oi, od, k):
     assert len(go) == len(gi[gi >= 0])                   # no duplicates
 
 
-@pytest.mark.parametrize("name", ["C1t", "C1s", "C2s", "C3s", "C4s", "C5s"])
+@pytest.mark.parametrize("name", ["C1t", "C1s", "C2s", "C3s", "C4s", "C5s", "C4ip_s"])
 def test_parity_config_point(name):
     cfg, ix, Q, g = gpu_index(name)
     compare(cfg, ix, Q, g, cfg.k, cfg.nprobe, cfg.budget)
 
 
-@pytest.mark.parametrize("name", ["C1t", "C2s", "C3s"])
+@pytest.mark.parametrize("name", ["C1t", "C2s", "C3s", "C4ip_s"])
 def test_parity_parameter_grid(name):
     cfg, ix, Q, g = gpu_index(name)
     for nprobe, bm in ((1, 1), (3, 2), (cfg.nprobe * 2, 1), (min(cfg.nlist, 64), 3)):
@@ -314,3 +314,22 @@ def test_rabitq_scan_modes_identical(nprobe_mult):
                 assert np.array_equal(a[key][i][:n].view(np.uint8), b[key][i][:n].view(np.uint8)), key
         else:
             assert np.array_equal(a[key].view(np.uint8), b[key].view(np.uint8)), key
+
+
+def test_ip_full_probe_unlimited_budget_is_brute_force_mips():
+    """Inner-product index (f4): every list probed and budget >= N give the brute-force maximum
+    inner product top-k, keys -<q, x> within 1e-5 relative (ids up to key ties)."""
+    from oracle import bruteforce as BF
+    cfg, ix, Q, g = gpu_index("C4ip_s")
+    assert g.info.metric == 1
+    raw = np.asarray(ix["raw"])
+    X = np.empty_like(raw)
+    X[np.asarray(ix["ids"])] = raw
+    Qs = np.ascontiguousarray(Q[:3])
+    k = 50
+    ids, key = g.search(torch.from_numpy(Qs).cuda(), k, cfg.nlist, cfg.N)
+    torch.cuda.synchronize()
+    gi, gd = BF.ground_truth(Qs, X, k, metric="ip")
+    for i in range(len(Qs)):
+        check_final_ids(ids[i].cpu().numpy(), key[i].cpu().numpy(), gi[i], gd[i].astype(np.float32), k)
+        np.testing.assert_allclose(np.sort(key[i].cpu().numpy()), gd[i], rtol=1e-5, atol=1e-6)

@@ -368,3 +368,56 @@ def test_rabitq_full_probe_is_brute_force(c3s):
     ids, d2 = O.search(ix, Q[:2], 50, cfg.nlist, cfg.N)
     gi, gd = BF.ground_truth(Q[:2], X, 50)
     assert np.array_equal(ids, gi)
+
+
+# ---------------------------------------------------------------- f4 inner-product metric
+def _tiny_ip(n=900, nlist=8, M=8):
+    """Tiny unit-norm (cosine = inner product) PQ index from the C4 generator, IP metric."""
+    from datagen import build_index, configs, synth
+    cfg = configs.get("C4ip_s").replace(name="tiny_ip", N=n, nlist=nlist, nq=3, k=20, nprobe=nlist,
+                                        budget=n, M=M, kmeans_iters=3, pq_train=n, pq_iters=3)
+    X = synth.generate_data(cfg)
+    ix = build_index.build(cfg, X=X)
+    return cfg, ix, X, synth.generate_queries(cfg)
+
+
+def test_ip_lut_identity_and_probe_sort():
+    """Inner product: sum_m LUT[m][code_m] == -<q, decode(code)> (fp64 within
+    fp32 rounding) and the probe order is the textbook sort of -<q, c_j> with ties by id."""
+    cfg, ix, X, Q = _tiny_ip()
+    books = np.asarray(ix["codebooks"])
+    codes = np.asarray(ix["codes"])
+    for q in Q:
+        est = O.pq_est(O.pq_lut(q, books, "ip"), codes)
+        dec = np.concatenate([books[m][codes[:, m]] for m in range(books.shape[0])], axis=1)
+        ref = -(dec.astype(np.float64) @ q.astype(np.float64))
+        np.testing.assert_allclose(est, ref, rtol=1e-5, atol=1e-6)
+    C = np.asarray(ix["centroids"])
+    pr, rq = O.probe(Q, C, cfg.nlist, "ip")
+    sim = Q.astype(np.float64) @ C.astype(np.float64).T
+    for i in range(len(Q)):
+        np.testing.assert_allclose(rq[i], -sim[i][pr[i]], rtol=1e-5, atol=1e-6)
+        assert np.all(np.diff(rq[i]) >= 0)
+
+
+def test_ip_full_probe_is_brute_force_mips():
+    """IP index, every list probed, budget >= N: the result is the brute-force maximum inner
+    product top-k for every k (keys -<q, x>, ties by id)."""
+    cfg, ix, X, Q = _tiny_ip()
+    for k in (1, 7, 20, cfg.N):
+        ids, key = O.search(ix, Q, k, cfg.nlist, max(k, cfg.N))
+        gi, gd = BF.ground_truth(Q, X, k, metric="ip")
+        assert np.array_equal(ids, gi)
+        np.testing.assert_allclose(key, gd, rtol=1e-5, atol=1e-6)
+
+
+def test_ip_index_file_roundtrip(tmp_path):
+    from datagen import index_file
+    cfg, ix, X, Q = _tiny_ip(n=300, nlist=4)
+    p = str(tmp_path / "ip.bbcivf")
+    index_file.write(p, ix)
+    back = index_file.read(p, mmap=False)
+    assert back["metric"] == "ip"
+    a, _ = O.search(ix, Q, 5, 4, 300)
+    b, _ = O.search(back, Q, 5, 4, 300)
+    assert np.array_equal(a, b)
