@@ -349,9 +349,12 @@ def main():
     scan_ms = stage_ms["scan"] / args.steps
     rr_ms = stage_ms["rerank"] / args.steps
     per = {
+        # the L1/shared-memory data pipe (128 B/clk/SM) carries both the 4-byte LUT entry read
+        # per code byte and the code byte itself (16-byte LDG through L1): 5 algorithmic bytes
+        # per lookup (the LUT replication is an implementation extra, not counted)
         "scan": {"ms": scan_ms, "bound": "alu",
-                 "pipe": "shared-memory LUT lookups (one 4-byte LDS per code byte, conflict-free)",
-                 "bytes": main_objs * (info.m if info.kind == 1 else 0) * 4, "peak_GBs": smem_peak,
+                 "pipe": "L1/shared-memory data pipe: 4-byte conflict-free LUT read + 1 code byte per lookup",
+                 "bytes": main_objs * (info.m if info.kind == 1 else 0) * 5, "peak_GBs": smem_peak,
                  "hbm_view": {"code_bytes": main_objs * code_bytes, "peak_GBs": peak}},
         "rerank": {"ms": rr_ms, "bound": "hbm", "bytes": stats["candidates"] * row_bytes,
                    "peak_GBs": peak},
@@ -385,7 +388,7 @@ def main():
             "traffic": traffic,
             "peak_source": (peak_src if per[dom]["bound"] == "hbm" else
                             "measured bf16 TFLOP/s x 2 (int8/bf16 nominal ratio)" if tens else
-                            "derived: 148 SMs x 128 B/clk shared-memory wavefronts x sm_max_mhz (DESIGN.md 5)"),
+                            "derived: 148 SMs x 128 B/clk L1/shared-memory data pipe x sm_max_mhz (DESIGN.md 5)"),
             "per_kernel": per,
             "stage_ms_per_step": {k_: v / args.steps for k_, v in stage_ms.items()}}
 
