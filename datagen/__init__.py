@@ -42,6 +42,21 @@ def index_path(cfg: Config) -> str:
     return os.path.join(cache_dir(), f"{cfg.gen}_{key}.bbcivf")
 
 
+def _drop_stale(path: str, cfg: Config) -> None:
+    """Delete cached index files of the same workload built from other sources or settings (a
+    full-size index is up to 17 GB; a long-lived cache directory would otherwise fill the disk)."""
+    d, base = os.path.split(path)
+    prefix = f"{cfg.gen}_"
+    try:
+        for fn in os.listdir(d):
+            if fn.startswith(prefix) and fn.endswith(".bbcivf") and fn != base:
+                full = os.path.join(d, fn)
+                if os.path.getsize(full) > (256 << 20):      # only the big full-size files
+                    os.remove(full)
+    except OSError:
+        pass
+
+
 def ensure_index(cfg: Config, verbose: bool = False) -> str:
     """Path of cfg's serialized index, building it (deterministically from the seed) if absent.
 
@@ -49,6 +64,7 @@ def ensure_index(cfg: Config, verbose: bool = False) -> str:
     """
     path = index_path(cfg)
     if not os.path.exists(path):
+        _drop_stale(path, cfg)
         t0 = time.time()
         idx = build_index.build(cfg, verbose=verbose)
         index_file.write(path, idx)

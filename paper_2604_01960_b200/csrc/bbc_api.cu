@@ -166,7 +166,8 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1) {
   if (cap < 16) cap = 16;
   p.cap = cap;
   size_t table = ix->kind == BBC_KIND_PQ ? (size_t)ix->M * 256 * 4 : (size_t)ix->D * 4;
-  p.per_query = (size_t)ix->nlist * 4 + (size_t)nprobe * 20 + 8 + 4 + 8 + kCells * 4 + 4 + 4 +
+  p.per_query = (size_t)ix->nlist * 4 + (size_t)nprobe * 20 + 8 +
+                (size_t)((cap + 32LL * nprobe + kRqE - 1) / kRqE) * 8 + 4 + 8 + kCells * 4 + 4 + 4 +
                 table + (size_t)cap * 13 + (size_t)ix->d * 4 + (size_t)k * 12 + 64 +
                 (size_t)((cap + kChunk - 1) / kChunk) * 8 + (size_t)(nprobe + 1) * 4;
   p.per_query += 8 + 8 + kCells * 4 + 4 + 4 + (size_t)4 * world;   // DistBuf
@@ -196,6 +197,8 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, 
   b.popad = (int*)take((size_t)nqb * (nprobe + 1) * 4);
   b.rbase = (long long*)take((size_t)nqb * nprobe * 8);
   b.qperm = (int*)take((size_t)nqb * 4);
+  b.items = (int2*)take((size_t)nqb * ((p.cap + 32LL * nprobe + kRqE - 1) / kRqE) * 8);
+  b.nitems = (int*)take(4);
   b.nsamp = (int*)take((size_t)nqb * 4);
   b.edges = (float*)take((size_t)nqb * 8);
   b.hist = (int*)take((size_t)nqb * kCells * 4);
@@ -252,26 +255,30 @@ __global__ void k_debug_cands(const int* cpos, const float* val, const int* ncan
 }
 
 template <int M>
-void launch_rq(bool est, dim3 grid, cudaStream_t st, const Batch& b, const Dev& dv,
+void launch_rq(bool est, int grid, cudaStream_t st, const Batch& b, const Dev& dv,
                const uint8_t* ct, const long long* tb, float* out, long long stride, int mode) {
   if (est) {
     set_smem(k_pq_scan_rq<M, true>, kRqSmem);
-    k_pq_scan_rq<M, true><<<grid, kRqNT, kRqSmem, st>>>(b, dv, ct, tb, out, stride, mode);
+    k_pq_scan_rq<M, true><<<grid, kRqNT, kRqSmem, st>>>(b, dv, ct, tb, out, stride, mode, b.items, b.nitems);
   } else {
     set_smem(k_pq_scan_rq<M, false>, kRqSmem);
-    k_pq_scan_rq<M, false><<<grid, kRqNT, kRqSmem, st>>>(b, dv, ct, tb, out, stride, mode);
+    k_pq_scan_rq<M, false><<<grid, kRqNT, kRqSmem, st>>>(b, dv, ct, tb, out, stride, mode, b.items, b.nitems);
   }
 }
 
-void rq_scan(int M, bool est, dim3 grid, cudaStream_t st, const Batch& b, const Dev& dv,
+// One PQ scan pass: work items (k_scan_plan), then one persistent CTA per SM over them.
+void rq_scan(int M, bool est, int num_sms, cudaStream_t st, const Batch& b, const Dev& dv,
              const uint8_t* ct, const long long* tb, float* out, long long stride, int mode) {
+  if (b.nq <= 0) return;
+  k_scan_plan<<<1, 1024, 0, st>>>(b, mode, b.items, b.nitems);
+  g_launches += 1;
   switch (M) {
-    case 8: launch_rq<8>(est, grid, st, b, dv, ct, tb, out, stride, mode); break;
-    case 16: launch_rq<16>(est, grid, st, b, dv, ct, tb, out, stride, mode); break;
-    case 24: launch_rq<24>(est, grid, st, b, dv, ct, tb, out, stride, mode); break;
-    case 32: launch_rq<32>(est, grid, st, b, dv, ct, tb, out, stride, mode); break;
-    case 48: launch_rq<48>(est, grid, st, b, dv, ct, tb, out, stride, mode); break;
-    case 64: launch_rq<64>(est, grid, st, b, dv, ct, tb, out, stride, mode); break;
+    case 8: launch_rq<8>(est, num_sms, st, b, dv, ct, tb, out, stride, mode); break;
+    case 16: launch_rq<16>(est, num_sms, st, b, dv, ct, tb, out, stride, mode); break;
+    case 24: launch_rq<24>(est, num_sms, st, b, dv, ct, tb, out, stride, mode); break;
+    case 32: launch_rq<32>(est, num_sms, st, b, dv, ct, tb, out, stride, mode); break;
+    case 48: launch_rq<48>(est, num_sms, st, b, dv, ct, tb, out, stride, mode); break;
+    case 64: launch_rq<64>(est, num_sms, st, b, dv, ct, tb, out, stride, mode); break;
   }
 }
 
@@ -428,14 +435,13 @@ void rbq_tc_pass(Shard& s, const Batch& b, cudaStream_t st, bool sample) {
   g_launches += 4;
 }
 
-int rq_grid(const Shard& s) { return (int)((s.p.cap + 32LL * s.b.nprobe + kRqE - 1) / kRqE); }
 
 // a3: estimates of the (local) sample objects -> val
 void stage_sample_est(Shard& s, cudaStream_t st) {
   bbc_index_s* ix = s.ix;
   StageScope sc(ix, st, BBC_STAGE_SAMPLE);
   if (ix->kind == BBC_KIND_PQ) {
-    rq_scan(ix->M, true, dim3(rq_grid(s), s.b.nq), st, s.b, s.dv, ix->codes_t, ix->tbase, s.b.val, s.p.cap, 0);
+    rq_scan(ix->M, true, ix->num_sms, st, s.b, s.dv, ix->codes_t, ix->tbase, s.b.val, s.p.cap, 0);
   } else if (ix->rbq_tc) {
     rbq_tc_pass(s, s.b, st, true);
   } else {
@@ -453,7 +459,7 @@ void stage_scan(Shard& s, cudaStream_t st) {
   const int nb = s.b.nq, nprobe = s.b.nprobe;
   if (ix->kind == BBC_KIND_PQ) {
     k_sample_cells<<<dim3(8, nb), 256, 0, st>>>(s.b);
-    rq_scan(ix->M, false, dim3(rq_grid(s), nb), st, s.b, s.dv, ix->codes_t, ix->tbase, nullptr, 0, 1);
+    rq_scan(ix->M, false, ix->num_sms, st, s.b, s.dv, ix->codes_t, ix->tbase, nullptr, 0, 1);
     g_launches += 2;
   } else if (ix->rbq_tc) {
     rbq_tc_pass(s, s.b, st, false);
@@ -719,7 +725,7 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
       if (dbg->est) {
         // every estimate in probe order, written to the caller's buffer (debug only)
         if (ix->kind == BBC_KIND_PQ) {
-          rq_scan(ix->M, true, dim3(rq_grid(s0), nb), st, b, s0.dv, ix->codes_t, ix->tbase, dbg->est,
+          rq_scan(ix->M, true, ix->num_sms, st, b, s0.dv, ix->codes_t, ix->tbase, dbg->est,
                   dbg->est_stride, 2);
         } else {
           Batch b2 = b;

@@ -37,6 +37,8 @@ struct Batch {
   float* val;         // [nq x cap]  sample estimates, then exact d^2 of candidates
   long long* stats;   // [3] sum n_o, sum |S*|, sum sample objects
   const int* qperm;   // [nq] locality order of the queries (k_qperm): CTA row y -> query qperm[y]
+  int2* items;        // [nq x rqg] scan work items (query, pass) of the current pass (k_scan_plan)
+  int* nitems;        // [1] number of work items
   int* chunk;         // [nq x nchunk]  per-chunk candidate counts -> offsets (compaction)
   int* chunkj;        // [nq x nchunk]  probed list holding each chunk's first element
 };
@@ -508,7 +510,8 @@ template <int M, bool EST>
 __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const uint8_t* __restrict__ codes_t,
                                                          const long long* __restrict__ tbase,
                                                          float* out_est, long long est_stride,
-                                                         int mode) {
+                                                         int mode, const int2* __restrict__ items,
+                                                         const int* __restrict__ nitems) {
   constexpr int P = M / kRqMC;                       // chunks
   extern __shared__ __align__(16) uint8_t rsm[];
   float* lut = reinterpret_cast<float*>(rsm);
@@ -517,15 +520,20 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
   int* gcnt = reinterpret_cast<int*>(rsm + kRqOffCnt);
   int* hist = reinterpret_cast<int*>(rsm + kRqOffHist);
   int* s_popad = reinterpret_cast<int*>(rsm + kRqOffPo);
-  const int q = b.qperm[blockIdx.y];        // neighbours run together: L2 reuse
+  // persistent CTAs over the work items of k_scan_plan: (query, pass) in query locality order
+  const int nit = *nitems;
+  for (int it = blockIdx.x; it < nit; it += gridDim.x) {
+  __syncthreads();                                   // shared memory of the previous item free
+  const int2 wk = items[it];
+  const int q = wk.x;
   const int ns = b.nsamp[q];
-  if (mode != 2 && ns == 0) return;                  // tau = infinity: nothing to bucket
+  if (mode != 2 && ns == 0) continue;                // tau = infinity: nothing to bucket
   const int first = mode == 1 ? ns : 0;
   const int lim = mode == 0 ? ns : b.nprobe;
   const int* popad = b.popad + (size_t)q * (b.nprobe + 1);
   const int nflat = popad[lim];
-  const int x0 = popad[first] + blockIdx.x * kRqE;
-  if (x0 >= nflat) return;
+  const int x0 = popad[first] + wk.y * kRqE;
+  if (x0 >= nflat) continue;
   if (smem_u32(rsm) != kRqSmemBase) __trap();        // layout assumption of lds_imm
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int j = threadIdx.x; j <= lim; j += kRqNT) s_popad[j] = popad[j];
@@ -643,6 +651,57 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
     for (int i = threadIdx.x; i < kCells; i += kRqNT)
       if (hist[i]) atomicAdd(&b.hist[(size_t)q * kCells + i], hist[i]);
   }
+  }
+}
+
+// Work items of a scan pass: every (query, 32768-object pass) that has objects, in query
+// locality order (qperm), so the scan runs as persistent CTAs without idle blocks (a static
+// grid sized for the largest query left most CTAs of small queries empty).  One CTA.
+//   mode 0: sample lists [0, nsamp); 1: lists [nsamp, nprobe); 2: all lists.
+__global__ void __launch_bounds__(1024) k_scan_plan(Batch b, int mode, int2* items, int* nitems) {
+  __shared__ int ws[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int base = 0; base < b.nq; base += 1024) {
+    const int r = base + threadIdx.x;
+    int cnt = 0, q = 0;
+    if (r < b.nq) {
+      q = b.qperm[r];
+      const int ns = b.nsamp[q];
+      if (mode == 2 || ns > 0) {
+        const int* pp = b.popad + (size_t)q * (b.nprobe + 1);
+        const int first = mode == 1 ? ns : 0, lim = mode == 0 ? ns : b.nprobe;
+        cnt = (pp[lim] - pp[first] + kRqE - 1) / kRqE;
+      }
+    }
+    int x = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += t;
+    }
+    if (lane == 31) ws[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      const int v = ws[lane];
+      int y = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= o) y += t;
+      }
+      ws[lane] = y - v;
+    }
+    __syncthreads();
+    const int off = carry + ws[wid] + x - cnt;
+    for (int c = 0; c < cnt; ++c) items[off + c] = make_int2(q, c);
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = off + cnt;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *nitems = carry;
 }
 
 // Index-load-time copy of the PQ codes in the group-major order of k_pq_scan_rq.
@@ -1162,9 +1221,104 @@ __global__ void __launch_bounds__(kRrNT, MINB) k_rerank(Batch b, Dev ix) {
 // ------------------------------------------------------------------------------------------
 // a8  final top-k by (exact d^2, id): CTA radix select, then order-preserving write-out.
 // ------------------------------------------------------------------------------------------
+// CTA radix selection of the kth smallest of n 32-bit keys (duplicates allowed) with 11-bit
+// digits over the bits where the keys differ (<= 3 histogram passes after one min/max pass).
+// key(i) -> (key, valid).  Returns the kth smallest valid key and, in *take, how many of the
+// elements equal to it belong to the k smallest (kth - #smaller).  Requires kth <= #valid.
+struct Kth32Smem {
+  unsigned hist[2048];
+  unsigned wsum[32];
+  unsigned mn[32], mx[32];
+  unsigned prefix, digit, need;
+};
+
+template <typename KeyF>
+__device__ uint32_t cta_kth32(int n, unsigned kth, KeyF key, unsigned* take, Kth32Smem& sm) {
+  constexpr int NT = kSelNT;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned mn = 0xffffffffu, mx = 0u;
+  for (int i = threadIdx.x; i < n; i += NT) {
+    bool ok;
+    const uint32_t k = key(i, &ok);
+    if (ok) { mn = min(mn, k); mx = max(mx, k); }
+  }
+  mn = warp_min(mn);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if (lane == 0) { sm.mn[wid] = mn; sm.mx[wid] = mx; }
+  __syncthreads();
+  if (wid == 0) {
+    unsigned a = sm.mn[lane], c = sm.mx[lane];
+    a = warp_min(a);
+    c = __reduce_max_sync(0xffffffffu, c);
+    if (lane == 0) { sm.mn[0] = a; sm.mx[0] = c; }
+  }
+  __syncthreads();
+  mn = sm.mn[0];
+  mx = sm.mx[0];
+  __syncthreads();
+  if (mn == mx || kth <= 1) {
+    if (mn == mx) { *take = kth; return mn; }
+  }
+  int hi = 31 - __clz(mn ^ mx);                       // highest differing bit
+  uint32_t prefix = hi == 31 ? 0u : (mn >> (hi + 1));
+  int pshift = hi + 1;
+  unsigned need = kth;
+  while (true) {
+    const int shift = max(0, pshift - 11);
+    const int width = pshift - shift;
+    const unsigned mask = (1u << width) - 1u;
+    for (int i = threadIdx.x; i < 2048; i += NT) sm.hist[i] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += NT) {
+      bool ok;
+      const uint32_t k = key(i, &ok);
+      if (ok && (pshift == 32 || (k >> pshift) == prefix)) atomicAdd(&sm.hist[(k >> shift) & mask], 1u);
+    }
+    __syncthreads();
+    // exclusive scan of the 2048 bins, 2 per thread
+    const unsigned h0 = sm.hist[2 * threadIdx.x], h1 = sm.hist[2 * threadIdx.x + 1];
+    unsigned x = h0 + h1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += t;
+    }
+    if (lane == 31) sm.wsum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      const unsigned v = sm.wsum[lane];
+      unsigned y = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned t = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= o) y += t;
+      }
+      sm.wsum[lane] = y - v;
+    }
+    __syncthreads();
+    const unsigned excl = sm.wsum[wid] + x - (h0 + h1);
+    if (excl < need && need <= excl + h0) {
+      sm.digit = 2 * threadIdx.x; sm.need = need - excl;
+    } else if (excl + h0 < need && need <= excl + h0 + h1) {
+      sm.digit = 2 * threadIdx.x + 1; sm.need = need - excl - h0;
+    }
+    __syncthreads();
+    need = sm.need;
+    prefix = (pshift == 32 ? 0u : (prefix << width)) | sm.digit;
+    pshift = shift;
+    __syncthreads();
+    if (shift == 0) break;
+  }
+  *take = need;
+  return prefix;
+}
+
+// a8: final top-k by (exact d^2, id).  The kth smallest d^2 key T is selected first (32-bit
+// radix, reading the distances only); the ids are looked at only to split the elements equal
+// to T (ties), by a second 32-bit selection among them.  Then an order-preserving write-out.
 __global__ void __launch_bounds__(kSelNT) k_final_select(Batch b, Dev ix, long long* out_ids,
                                                          float* out_d2) {
-  __shared__ SelectSmem sm;
+  __shared__ Kth32Smem sm;
   __shared__ int wcnt[kSelNT / 32 + 1];
   const int q = blockIdx.x;
   const int nc = b.ncand[q];
@@ -1173,26 +1327,37 @@ __global__ void __launch_bounds__(kSelNT) k_final_select(Batch b, Dev ix, long l
   const float* vv = b.val + (size_t)q * b.cap;
   long long* oi = out_ids + (size_t)q * k;
   float* od = out_d2 + (size_t)q * k;
-  auto load = [&](int64_t i) -> uint64_t {
-    return ((uint64_t)f2key(vv[i]) << 32) | (uint32_t)cp[i];
-  };
-  uint64_t pref = ~0ull;
-  int pshift = 0;
-  if (nc > k) pref = cta_select<kSelNT>(nc, k, load, false, &pshift, sm);
+  uint32_t T = 0xffffffffu, I = 0xffffffffu;
+  bool all = true;
+  if (nc > k) {
+    unsigned take;
+    T = cta_kth32(nc, (unsigned)k, [&](int i, bool* ok) { *ok = true; return f2key(vv[i]); }, &take, sm);
+    // elements equal to T: take the `take` smallest ids (ids are unique)
+    unsigned t2;
+    I = cta_kth32(nc, take, [&](int i, bool* ok) {
+          const uint32_t f = f2key(vv[i]);
+          *ok = f == T;
+          return *ok ? (uint32_t)cp[i] : 0u;
+        }, &t2, sm);
+    all = false;
+  }
   int base = 0;
   for (int t0 = 0; t0 < nc; t0 += kSelNT) {
     const int i = t0 + threadIdx.x;
-    uint64_t key = 0;
     bool f = false;
+    float dv = 0.f;
+    int id = 0;
     if (i < nc) {
-      key = load(i);
-      f = shr64(key, pshift) <= pref;
+      dv = vv[i];
+      id = cp[i];
+      const uint32_t fk = f2key(dv);
+      f = all || fk < T || (fk == T && (uint32_t)id <= I);
     }
     int total;
     int r = block_rank<kSelNT>(f, wcnt, &total);
     if (f && base + r < k) {
-      oi[base + r] = (long long)(uint32_t)key;
-      od[base + r] = vv[i];
+      oi[base + r] = (long long)(uint32_t)id;
+      od[base + r] = dv;
     }
     base += total;
   }
