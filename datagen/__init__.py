@@ -39,14 +39,14 @@ def index_path(cfg: Config) -> str:
     """Cache path keyed by the build-relevant fields of cfg and this package's sources."""
     desc = repr(tuple(getattr(cfg, f) for f in _BUILD_FIELDS))
     key = hashlib.sha1(desc.encode() + _source_hash().encode()).hexdigest()[:12]
-    return os.path.join(cache_dir(), f"{cfg.gen}_{key}.bbcivf")
+    return os.path.join(cache_dir(), f"{cfg.name}_{key}.bbcivf")
 
 
 def _drop_stale(path: str, cfg: Config) -> None:
     """Delete cached index files of the same workload built from other sources or settings (a
     full-size index is up to 17 GB; a long-lived cache directory would otherwise fill the disk)."""
     d, base = os.path.split(path)
-    prefix = f"{cfg.gen}_"
+    prefix = f"{cfg.name}_"
     try:
         for fn in os.listdir(d):
             if fn.startswith(prefix) and fn.endswith(".bbcivf") and fn != base:
