@@ -79,6 +79,8 @@ struct bbc_index_s {
   int num_sms = 148;
   void* nccl = nullptr;                 // ncclComm_t of this rank (bbc_comm_init)
   int force_dist = 0;                   // run the sharded code path even at world 1 (tests)
+  cudaStream_t copy_stream = nullptr;   // host path: device->host result copies
+  cudaEvent_t ev_done[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -168,7 +170,7 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1) {
   size_t table = ix->kind == BBC_KIND_PQ ? (size_t)ix->M * 256 * 4 : (size_t)ix->D * 4;
   p.per_query = (size_t)ix->nlist * 4 + (size_t)nprobe * 20 + 8 +
                 (size_t)((cap + 32LL * nprobe + kRqE - 1) / kRqE) * 8 + 4 + 8 + kCells * 4 + 4 + 4 +
-                table + (size_t)cap * 13 + (size_t)ix->d * 4 + (size_t)k * 12 + 64 +
+                table + (size_t)cap * 13 + (size_t)ix->d * 4 + (size_t)k * 24 + 64 +
                 (size_t)((cap + kChunk - 1) / kChunk) * 8 + (size_t)(nprobe + 1) * 4;
   p.per_query += 8 + 8 + kCells * 4 + 4 + 4 + (size_t)4 * world;   // DistBuf
   p.fixed = 64 * 256;
@@ -215,6 +217,8 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, 
   *qstage = (float*)take((size_t)nqb * ix->d * 4);
   *ostage_ids = (long long*)take((size_t)nqb * k * 8);
   *ostage_d2 = (float*)take((size_t)nqb * k * 4);
+  b.ostage2_ids = (long long*)take((size_t)nqb * k * 8);   // second output staging (host path)
+  b.ostage2_d2 = (float*)take((size_t)nqb * k * 4);
   db->prefix = (unsigned long long*)take((size_t)nqb * 8);
   db->need = (long long*)take((size_t)nqb * 8);
   db->dh = (int*)take((size_t)nqb * kCells * 4);
@@ -635,6 +639,21 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
     nqb = std::min<long long>(nqb, (long long)((s.ws_bytes - s.p.fixed) / s.p.per_query));
   }
   if (dbg && nqb < nq) return fail(BBC_ERR_ARG, "debug search needs all queries in one micro-batch");
+  // host path: the device->host copy of micro-batch i (copy stream) overlaps the search of
+  // micro-batch i+1; outputs alternate between two staging buffers.  At least 4 micro-batches
+  // (of >= 256 queries) so that most of the copy time is hidden.
+  const bool pipe = host && !dist && !dbg;
+  if (pipe) {
+    nqb = std::min<long long>(nqb, std::max<long long>(256, (nq + 3) / 4));
+    if (!ix->copy_stream) {
+      CU(cudaStreamCreateWithFlags(&ix->copy_stream, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; ++i) {
+        CU(cudaEventCreateWithFlags(&ix->ev_done[i], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&ix->ev_copied[i], cudaEventDisableTiming));
+      }
+    }
+  }
+  int mb_index = 0;
   const long long budget_c = std::min<long long>(budget, (long long)1 << 40);
   for (auto& s : sh) {
     CU(cudaMemsetAsync(s.ix->stats, 0, 4 * sizeof(long long), st));
@@ -680,10 +699,23 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
       stage_scan(s, st);
       stage_compact(s, st);
       stage_rerank(s, st);
+      const int bi = mb_index & 1;
+      if (pipe) {
+        if (bi == 1) { s.oids = s.b.ostage2_ids; s.od2 = s.b.ostage2_d2; }
+        if (mb_index >= 2) CU(cudaStreamWaitEvent(st, ix->ev_copied[bi], 0));   // buffer free
+      }
       {
         StageScope sc(s.ix, st, BBC_STAGE_SELECT);
         k_final_select<<<nb, kSelNT, 0, st>>>(s.b, s.dv, s.oids, s.od2);
         g_launches += 1;
+      }
+      if (pipe) {
+        cudaStream_t cs = ix->copy_stream;
+        CU(cudaEventRecord(ix->ev_done[bi], st));
+        CU(cudaStreamWaitEvent(cs, ix->ev_done[bi], 0));
+        CU(cudaMemcpyAsync(out_ids + q0 * k, s.oids, (size_t)nb * k * 8, cudaMemcpyDeviceToHost, cs));
+        CU(cudaMemcpyAsync(out_d2 + q0 * k, s.od2, (size_t)nb * k * 4, cudaMemcpyDeviceToHost, cs));
+        CU(cudaEventRecord(ix->ev_copied[bi], cs));
       }
     } else {
       bbc_status e = dist_edges(sh, comm, st);
@@ -749,12 +781,15 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
         CU(cudaGetLastError());
       }
     }
-    if (host) {
+    if (host && !pipe) {
       CU(cudaMemcpyAsync(out_ids + q0 * k, s0.oids, (size_t)nb * k * 8, cudaMemcpyDeviceToHost, st));
       CU(cudaMemcpyAsync(out_d2 + q0 * k, s0.od2, (size_t)nb * k * 4, cudaMemcpyDeviceToHost, st));
     }
     for (auto& s : sh) s.ix->microbatches++;
+    ++mb_index;
   }
+  if (pipe)                                           // the caller's stream covers every copy
+    for (int i = 0; i < std::min(mb_index, 2); ++i) CU(cudaStreamWaitEvent(st, ix->ev_copied[i], 0));
   if (host || dbg) CU(cudaStreamSynchronize(st));
   return BBC_OK;
 }
@@ -1047,6 +1082,11 @@ void ivf_free(bbc_index ix) {
   for (auto& t : ix->timers) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
   if (ix->nccl) ncclCommDestroy((ncclComm_t)ix->nccl);
   for (auto e : ix->pool) cudaEventDestroy(e);
+  if (ix->copy_stream) cudaStreamDestroy(ix->copy_stream);
+  for (int i = 0; i < 2; ++i) {
+    if (ix->ev_done[i]) cudaEventDestroy(ix->ev_done[i]);
+    if (ix->ev_copied[i]) cudaEventDestroy(ix->ev_copied[i]);
+  }
   delete ix;
 }
 

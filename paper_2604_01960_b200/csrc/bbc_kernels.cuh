@@ -38,6 +38,8 @@ struct Batch {
   long long* stats;   // [3] sum n_o, sum |S*|, sum sample objects
   const int* qperm;   // [nq] locality order of the queries (k_qperm): CTA row y -> query qperm[y]
   int2* items;        // [nq x rqg] scan work items (query, pass) of the current pass (k_scan_plan)
+  long long* ostage2_ids;  // second output staging buffer (host path, double-buffered copies)
+  float* ostage2_d2;
   int* nitems;        // [1] number of work items
   int* chunk;         // [nq x nchunk]  per-chunk candidate counts -> offsets (compaction)
   int* chunkj;        // [nq x nchunk]  probed list holding each chunk's first element
@@ -1158,6 +1160,22 @@ __global__ void __launch_bounds__(kRrNT, MINB) k_rerank(Batch b, Dev ix) {
       qr[v][0] = x.x; qr[v][1] = x.y; qr[v][2] = x.z; qr[v][3] = x.w;
     }
   }
+  // uint8 rows: the lane's 16 query values per 16-byte chunk stay in registers (MAXV <= 2)
+  constexpr bool QREG = U8 && MAXV <= 2;
+  float qu[QREG ? MAXV : 1][16];
+  if (QREG) {
+#pragma unroll
+    for (int v = 0; v < (QREG ? MAXV : 1); ++v) {
+      const int t = sl + LPC * v;
+      if (v < per && t < nv) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float4 x = reinterpret_cast<const float4*>(qv)[4 * t + e];
+          qu[v][4 * e] = x.x; qu[v][4 * e + 1] = x.y; qu[v][4 * e + 2] = x.z; qu[v][4 * e + 3] = x.w;
+        }
+      }
+    }
+  }
   const uint8_t* raw = static_cast<const uint8_t*>(ix.raw);
   const int gw = blockIdx.x * (kRrNT / 32) + (threadIdx.x >> 5);
   const int nw = gridDim.x * (kRrNT / 32);
@@ -1191,7 +1209,8 @@ __global__ void __launch_bounds__(kRrNT, MINB) k_rerank(Batch b, Dev ix) {
               for (int h = 0; h < 4; ++h)
 #pragma unroll
                 for (int by = 0; by < 4; ++by) {
-                  const float xv = (float)((wv[h] >> (8 * by)) & 255u), qq = __ldg(qv + t * 16 + h * 4 + by);
+                  const float xv = (float)((wv[h] >> (8 * by)) & 255u);
+                  const float qq = QREG ? qu[QREG ? v : 0][h * 4 + by] : __ldg(qv + t * 16 + h * 4 + by);
                   if (IP) acc = fmaf(xv, qq, acc);
                   else { const float df = xv - qq; acc = fmaf(df, df, acc); }
                 }

@@ -172,6 +172,20 @@ def test_host_api_matches_device_api():
     assert np.array_equal(a_d2.cpu().numpy(), h_d2)
 
 
+def test_host_api_pipelined_microbatches():
+    """Host path with >= 4 micro-batches (device->host copies on a second stream, double-buffered
+    staging) returns the device path's results bit for bit, also on a short last batch."""
+    from datagen import configs, synth
+    cfg, ix, Q, g = gpu_index("C2s")
+    Qm = np.ascontiguousarray(synth.generate_queries(cfg, 1100))
+    q = torch.from_numpy(Qm).cuda()
+    a_ids, a_d2 = g.search(q, 200, cfg.nprobe, 400)
+    h_ids, h_d2 = g.search_host(Qm, 200, cfg.nprobe, 400)
+    assert g.last_stats()["microbatches"] >= 4
+    assert np.array_equal(a_ids.cpu().numpy(), h_ids)
+    assert np.array_equal(a_d2.cpu().numpy(), h_d2)
+
+
 def test_recall_matches_oracle():
     from oracle import bbc_oracle as O
     from oracle import bruteforce as BF
