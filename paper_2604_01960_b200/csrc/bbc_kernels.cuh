@@ -170,6 +170,31 @@ __device__ __forceinline__ float canonical_d2(const float* sq, const float* __re
 }
 
 __device__ __forceinline__ void bitonic_sort_keys(uint64_t* keys, int P2) {
+  if (P2 <= kSelNT) {
+    // one key per thread: exchanges at stride < 32 by warp shuffles (no barrier), larger
+    // strides through shared memory
+    const int t = threadIdx.x;
+    uint64_t v = t < P2 ? keys[t] : ~0ull;
+    for (int size = 2; size <= P2; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        uint64_t o;
+        if (stride >= 32) {
+          __syncthreads();
+          if (t < P2) keys[t] = v;
+          __syncthreads();
+          o = t < P2 ? keys[t ^ stride] : ~0ull;
+        } else {
+          o = __shfl_xor_sync(0xffffffffu, v, stride);
+        }
+        const bool keepmin = ((t & stride) == 0) == ((t & size) == 0);
+        v = keepmin ? (o < v ? o : v) : (o > v ? o : v);
+      }
+    }
+    __syncthreads();
+    if (t < P2) keys[t] = v;
+    __syncthreads();
+    return;
+  }
   for (int size = 2; size <= P2; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       for (int i = threadIdx.x; i < P2 / 2; i += kSelNT) {
@@ -876,20 +901,114 @@ __global__ void __launch_bounds__(kScanNT) k_rbq_scan(Batch b, Dev ix, int G) {
   }
 }
 
+// CTA radix selection of the kth smallest of n 32-bit keys (duplicates allowed) with 11-bit
+// digits over the bits where the keys differ (<= 3 histogram passes after one min/max pass).
+// key(i) -> (key, valid).  Returns the kth smallest valid key and, in *take, how many of the
+// elements equal to it belong to the k smallest (kth - #smaller).  Requires kth <= #valid.
+struct Kth32Smem {
+  unsigned hist[2048];
+  unsigned wsum[32];
+  unsigned mn[32], mx[32];
+  unsigned prefix, digit, need;
+};
+
+template <typename KeyF>
+__device__ uint32_t cta_kth32(int n, unsigned kth, KeyF key, unsigned* take, Kth32Smem& sm,
+                              uint32_t* min_out = nullptr) {
+  constexpr int NT = kSelNT;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned mn = 0xffffffffu, mx = 0u;
+  for (int i = threadIdx.x; i < n; i += NT) {
+    bool ok;
+    const uint32_t k = key(i, &ok);
+    if (ok) { mn = min(mn, k); mx = max(mx, k); }
+  }
+  mn = warp_min(mn);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if (lane == 0) { sm.mn[wid] = mn; sm.mx[wid] = mx; }
+  __syncthreads();
+  if (wid == 0) {
+    unsigned a = sm.mn[lane], c = sm.mx[lane];
+    a = warp_min(a);
+    c = __reduce_max_sync(0xffffffffu, c);
+    if (lane == 0) { sm.mn[0] = a; sm.mx[0] = c; }
+  }
+  __syncthreads();
+  mn = sm.mn[0];
+  mx = sm.mx[0];
+  if (min_out) *min_out = mn;
+  __syncthreads();
+  if (mn == mx || kth <= 1) {
+    if (mn == mx) { *take = kth; return mn; }
+  }
+  int hi = 31 - __clz(mn ^ mx);                       // highest differing bit
+  uint32_t prefix = hi == 31 ? 0u : (mn >> (hi + 1));
+  int pshift = hi + 1;
+  unsigned need = kth;
+  while (true) {
+    const int shift = max(0, pshift - 11);
+    const int width = pshift - shift;
+    const unsigned mask = (1u << width) - 1u;
+    for (int i = threadIdx.x; i < 2048; i += NT) sm.hist[i] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += NT) {
+      bool ok;
+      const uint32_t k = key(i, &ok);
+      if (ok && (pshift == 32 || (k >> pshift) == prefix)) atomicAdd(&sm.hist[(k >> shift) & mask], 1u);
+    }
+    __syncthreads();
+    // exclusive scan of the 2048 bins, 2 per thread
+    const unsigned h0 = sm.hist[2 * threadIdx.x], h1 = sm.hist[2 * threadIdx.x + 1];
+    unsigned x = h0 + h1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += t;
+    }
+    if (lane == 31) sm.wsum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      const unsigned v = sm.wsum[lane];
+      unsigned y = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned t = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= o) y += t;
+      }
+      sm.wsum[lane] = y - v;
+    }
+    __syncthreads();
+    const unsigned excl = sm.wsum[wid] + x - (h0 + h1);
+    if (excl < need && need <= excl + h0) {
+      sm.digit = 2 * threadIdx.x; sm.need = need - excl;
+    } else if (excl + h0 < need && need <= excl + h0 + h1) {
+      sm.digit = 2 * threadIdx.x + 1; sm.need = need - excl - h0;
+    }
+    __syncthreads();
+    need = sm.need;
+    prefix = (pshift == 32 ? 0u : (prefix << width)) | sm.digit;
+    pshift = shift;
+    __syncthreads();
+    if (shift == 0) break;
+  }
+  *take = need;
+  return prefix;
+}
+
 // ------------------------------------------------------------------------------------------
 // a3  edges: d_min = min of the sample estimates, d_max = budget-th smallest
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kSelNT) k_select_edges(Batch b, Dev ix) {
-  __shared__ SelectSmem sm;
+  __shared__ Kth32Smem sm;
   const int q = blockIdx.x;
   const int ns = b.nsamp[q];
   if (ns == 0) return;
   const int n = b.poff[(size_t)q * (b.nprobe + 1) + ns];
   const float* v = b.val + (size_t)q * b.cap;
-  auto load = [&](int64_t i) -> uint64_t { return (uint64_t)f2key(v[i]); };
-  int ps;
-  uint64_t kmin = cta_select<kSelNT>(n, 1, load, true, &ps, sm);
-  uint64_t kmax = cta_select<kSelNT>(n, b.budget, load, true, &ps, sm);
+  unsigned take;
+  uint32_t kmin;
+  const uint32_t kmax = cta_kth32(n, (unsigned)b.budget, [&](int i, bool* ok) { *ok = true; return f2key(v[i]); },
+                                  &take, sm, &kmin);
   if (threadIdx.x == 0) {
     b.edges[2 * q] = key2f((uint32_t)kmin);
     b.edges[2 * q + 1] = key2f((uint32_t)kmax);
@@ -1047,8 +1166,8 @@ __global__ void __launch_bounds__(256) k_chunk_offsets(Batch b, int* chunk_cnt, 
 // One chunk per CTA.  The lists covering the chunk (from chunkj) have their offsets and row
 // bases staged in shared memory with one parallel load; a candidate's list is then a
 // shared-memory binary search and its row rbase[j] + i.  The chunk's candidate rows are placed
-// in shared memory at their block-scan rank, then written out (rows and original ids) with
-// coalesced stores.  Few dependent global accesses per CTA: the kernel is latency-bound.
+// in shared memory at their block-scan rank, then written out with coalesced stores (the
+// original ids are gathered by the re-rank, which reads each candidate's row anyway).  Few dependent global accesses per CTA: the kernel is latency-bound.
 constexpr int kEmitWin = 1024;                       // lists staged per chunk (else global search)
 __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chunk_off, int nchunk) {
   __shared__ int wcnt[kCmpNT / 32];
@@ -1121,12 +1240,7 @@ __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chu
   __syncthreads();
   const int base = chunk_off[(size_t)q * nchunk + c];
   int* out = b.cpos + (size_t)q * b.cap + base;
-  int* oid = b.cid + (size_t)q * b.cap + base;
-  for (int t = threadIdx.x; t < tot; t += kCmpNT) {
-    const int row = s_row[t];
-    out[t] = row;
-    oid[t] = (int)ix.ids[row];
-  }
+  for (int t = threadIdx.x; t < tot; t += kCmpNT) out[t] = s_row[t];   // ids: gathered by k_rerank
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1185,10 +1299,12 @@ __global__ void __launch_bounds__(kRrNT, MINB) k_rerank(Batch b, Dev ix) {
     for (int k0 = 0; k0 < n32; k0 += CPW * STEPS) {
       uint4 x[STEPS][MAXV];
       int kk[STEPS];
+      int idr[STEPS];
 #pragma unroll
       for (int s = 0; s < STEPS; ++s) {
         kk[s] = k0 + s * CPW + sub;
         const int r = __shfl_sync(0xffffffffu, myrow, kk[s] & 31);
+        idr[s] = (sl == 0 && kk[s] < n32) ? (int)__ldg(ix.ids + r) : 0;   // original id (final select)
         const uint4* rp = reinterpret_cast<const uint4*>(raw + (size_t)r * rowb);
 #pragma unroll
         for (int v = 0; v < MAXV; ++v) {
@@ -1231,7 +1347,10 @@ __global__ void __launch_bounds__(kRrNT, MINB) k_rerank(Batch b, Dev ix) {
         }
 #pragma unroll
         for (int o = LPC / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (sl == 0 && kk[s] < n32) vv[cb + kk[s]] = IP ? -acc : acc;
+        if (sl == 0 && kk[s] < n32) {
+          vv[cb + kk[s]] = IP ? -acc : acc;
+          b.cid[(size_t)q * b.cap + cb + kk[s]] = idr[s];
+        }
       }
     }
   }
@@ -1240,98 +1359,6 @@ __global__ void __launch_bounds__(kRrNT, MINB) k_rerank(Batch b, Dev ix) {
 // ------------------------------------------------------------------------------------------
 // a8  final top-k by (exact d^2, id): CTA radix select, then order-preserving write-out.
 // ------------------------------------------------------------------------------------------
-// CTA radix selection of the kth smallest of n 32-bit keys (duplicates allowed) with 11-bit
-// digits over the bits where the keys differ (<= 3 histogram passes after one min/max pass).
-// key(i) -> (key, valid).  Returns the kth smallest valid key and, in *take, how many of the
-// elements equal to it belong to the k smallest (kth - #smaller).  Requires kth <= #valid.
-struct Kth32Smem {
-  unsigned hist[2048];
-  unsigned wsum[32];
-  unsigned mn[32], mx[32];
-  unsigned prefix, digit, need;
-};
-
-template <typename KeyF>
-__device__ uint32_t cta_kth32(int n, unsigned kth, KeyF key, unsigned* take, Kth32Smem& sm) {
-  constexpr int NT = kSelNT;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  unsigned mn = 0xffffffffu, mx = 0u;
-  for (int i = threadIdx.x; i < n; i += NT) {
-    bool ok;
-    const uint32_t k = key(i, &ok);
-    if (ok) { mn = min(mn, k); mx = max(mx, k); }
-  }
-  mn = warp_min(mn);
-  mx = __reduce_max_sync(0xffffffffu, mx);
-  if (lane == 0) { sm.mn[wid] = mn; sm.mx[wid] = mx; }
-  __syncthreads();
-  if (wid == 0) {
-    unsigned a = sm.mn[lane], c = sm.mx[lane];
-    a = warp_min(a);
-    c = __reduce_max_sync(0xffffffffu, c);
-    if (lane == 0) { sm.mn[0] = a; sm.mx[0] = c; }
-  }
-  __syncthreads();
-  mn = sm.mn[0];
-  mx = sm.mx[0];
-  __syncthreads();
-  if (mn == mx || kth <= 1) {
-    if (mn == mx) { *take = kth; return mn; }
-  }
-  int hi = 31 - __clz(mn ^ mx);                       // highest differing bit
-  uint32_t prefix = hi == 31 ? 0u : (mn >> (hi + 1));
-  int pshift = hi + 1;
-  unsigned need = kth;
-  while (true) {
-    const int shift = max(0, pshift - 11);
-    const int width = pshift - shift;
-    const unsigned mask = (1u << width) - 1u;
-    for (int i = threadIdx.x; i < 2048; i += NT) sm.hist[i] = 0;
-    __syncthreads();
-    for (int i = threadIdx.x; i < n; i += NT) {
-      bool ok;
-      const uint32_t k = key(i, &ok);
-      if (ok && (pshift == 32 || (k >> pshift) == prefix)) atomicAdd(&sm.hist[(k >> shift) & mask], 1u);
-    }
-    __syncthreads();
-    // exclusive scan of the 2048 bins, 2 per thread
-    const unsigned h0 = sm.hist[2 * threadIdx.x], h1 = sm.hist[2 * threadIdx.x + 1];
-    unsigned x = h0 + h1;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned t = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += t;
-    }
-    if (lane == 31) sm.wsum[wid] = x;
-    __syncthreads();
-    if (wid == 0) {
-      const unsigned v = sm.wsum[lane];
-      unsigned y = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned t = __shfl_up_sync(0xffffffffu, y, o);
-        if (lane >= o) y += t;
-      }
-      sm.wsum[lane] = y - v;
-    }
-    __syncthreads();
-    const unsigned excl = sm.wsum[wid] + x - (h0 + h1);
-    if (excl < need && need <= excl + h0) {
-      sm.digit = 2 * threadIdx.x; sm.need = need - excl;
-    } else if (excl + h0 < need && need <= excl + h0 + h1) {
-      sm.digit = 2 * threadIdx.x + 1; sm.need = need - excl - h0;
-    }
-    __syncthreads();
-    need = sm.need;
-    prefix = (pshift == 32 ? 0u : (prefix << width)) | sm.digit;
-    pshift = shift;
-    __syncthreads();
-    if (shift == 0) break;
-  }
-  *take = need;
-  return prefix;
-}
-
 // a8: final top-k by (exact d^2, id).  The kth smallest d^2 key T is selected first (32-bit
 // radix, reading the distances only); the ids are looked at only to split the elements equal
 // to T (ties), by a second 32-bit selection among them.  Then an order-preserving write-out.
