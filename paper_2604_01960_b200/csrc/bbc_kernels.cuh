@@ -1181,6 +1181,10 @@ __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chu
   const int tau = b.tau[q];
   const int c = blockIdx.x;
   if (c * kChunk >= n) return;
+  const int need = (n + kChunk - 1) / kChunk;        // chunks without candidates exit at once
+  const int cbeg = chunk_off[(size_t)q * nchunk + c];
+  const int cend = c + 1 < need ? chunk_off[(size_t)q * nchunk + c + 1] : b.ncand[q];
+  if (cend == cbeg) return;
   const long long* rb = b.rbase + (size_t)q * nprobe;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int i0 = c * kChunk + threadIdx.x * kPerThr;
