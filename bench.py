@@ -56,6 +56,9 @@ def parse():
     p.add_argument("--sweep", action="store_true", help="recall/QPS over an (nprobe, budget) grid")
     p.add_argument("--profile-steps", action="store_true", help="no warm-up/recall/cpu (ncu runs)")
     p.add_argument("--shard", default="queries", choices=["queries", "lists"])
+    p.add_argument("--buckets", type=int, default=255, help="B regular buckets (Eq. 6)")
+    p.add_argument("--bucket-sweep", action="store_true",
+                   help="QPS, |S*|/budget and recall over B (Table 4 analog) at the operating point")
     return p.parse_args()
 
 
@@ -262,8 +265,11 @@ def main():
         g.comm_init(obj[0], rank, world)
     else:
         g = Index(path, device=local)
+    g.set_buckets(args.buckets)
     if args.sweep:
         return sweep(cfg, path, g, rank)
+    if args.bucket_sweep:
+        return bucket_sweep(cfg, path, g, *operating_point(cfg, args))
     if lists:                                            # same queries on every rank
         Qh = np.ascontiguousarray(synth.generate_queries(cfg))
     else:
@@ -435,6 +441,40 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def bucket_sweep(cfg, path, g, nprobe, budget):
+    """Exp-6 / Table 4 analog: the number of buckets B against the candidate
+    superset size, recall and device time, at the workload's operating point."""
+    import torch
+    X = database_in_id_order(path)
+    Q = synth.generate_queries(cfg)
+    q = torch.from_numpy(Q).cuda()
+    rq = 100
+    gi, gd = groundtruth.cached_topk(f"{cfg.name}_{os.path.basename(path)}", Q[:rq], X, cfg.k,
+                                     datagen.cache_dir(), metric=cfg.metric)
+    st = torch.cuda.current_stream()
+    ws = g.workspace(len(Q), cfg.k, nprobe, budget)
+    for B in (1, 3, 7, 15, 31, 63, 127, 255):
+        g.set_buckets(B)
+        g.search(q, cfg.k, nprobe, budget, workspace=ws)
+        torch.cuda.synchronize()
+        ms = []
+        for _ in range(3):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            ids, _ = g.search(q, cfg.k, nprobe, budget, workspace=ws)
+            b.record(st)
+            torch.cuda.synchronize()
+            ms.append(a.elapsed_time(b))
+        idn = ids[:rq].cpu().numpy()
+        r = groundtruth.recall(idn, groundtruth.exact_of(Q[:rq], X, idn, metric=cfg.metric), gi, gd)
+        s = g.last_stats()
+        print(json.dumps({"bucket_sweep": cfg.name, "B": B, "nprobe": nprobe, "budget": budget,
+                          "ms": float(np.median(ms)), "qps": len(Q) / (float(np.median(ms)) / 1e3),
+                          "superset_over_budget": s["candidates"] / len(Q) / budget,
+                          "recall": round(r, 4)}), flush=True)
+    g.set_buckets(255)
 
 
 def sweep(cfg, path, g, rank):

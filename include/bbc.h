@@ -121,6 +121,14 @@ bbc_status bbc_set_probe_mode(bbc_index index, int32_t mode);
  * Errors: BBC_ERR_ARG for a null index, an unknown mode, or TENSOR on a RaBitQ index with
  * D > 1024.  Must not change while a search on the handle is in flight.
  */
+/*
+ * bbc_set_buckets -- B, the number of regular equal-width buckets of the result buffer over
+ * [d_min, d_max] (Eq. 6; the paper's m, Eq. 3 and Table 4).  Default
+ * 255 (8-bit bucket ids; id 255 = beyond d_max, never a candidate).  Fewer buckets give a
+ * coarser threshold and a larger candidate superset S*.  BBC_ERR_ARG unless 1 <= B <= 255.
+ */
+bbc_status bbc_set_buckets(bbc_index index, int32_t nbuckets);
+
 #define BBC_SCAN_SIMT 0
 #define BBC_SCAN_TENSOR 1
 bbc_status bbc_set_scan_mode(bbc_index index, int32_t mode);

@@ -202,20 +202,23 @@ def edges(sample_est: np.ndarray, budget: int):
     return F32(v.min()), F32(np.partition(v, budget - 1)[budget - 1])
 
 
-def cells(x: np.ndarray, d_min: F32, d_max: F32) -> np.ndarray:
-    """Bucket id (Eq. 6, reading R3): 255 for x > d_max; otherwise
-    clamp(floor((x - d_min) * inv), 0, 254) with inv = 255/(d_max - d_min) in fp32;
+def cells(x: np.ndarray, d_min: F32, d_max: F32, nbuckets: int = 255) -> np.ndarray:
+    """Bucket id (Eq. 6, reading R3) with B = nbuckets regular equal-width buckets
+    over [d_min, d_max] (1 <= B <= 255; the paper's m, Eq. 3 / Table 4): 255 for x > d_max;
+    otherwise clamp(floor((x - d_min) * inv), 0, B - 1) with inv = B/(d_max - d_min) in fp32;
     0 when d_max == d_min (or inv is not finite)."""
+    if not 1 <= nbuckets <= 255:
+        raise ValueError("nbuckets must be in [1, 255]")
     x = np.asarray(x, dtype=F32)
     out = np.full(len(x), 255, dtype=np.int64)
     inb = ~(x > d_max)
     width = F32(d_max - d_min)
-    inv = F32(255.0) / width if width > 0 else F32(np.inf)
+    inv = F32(nbuckets) / width if width > 0 else F32(np.inf)
     if not np.isfinite(inv):
         out[inb] = 0
         return out
     t = (x[inb] - d_min) * inv
-    out[inb] = np.clip(np.floor(t), 0, 254).astype(np.int64)
+    out[inb] = np.clip(np.floor(t), 0, nbuckets - 1).astype(np.int64)
     return out
 
 
@@ -251,7 +254,7 @@ def select_topk(d2: np.ndarray, ids: np.ndarray, k: int):
 # the whole path
 # ----------------------------------------------------------------------------------------------
 def search(ix: dict, Q: np.ndarray, k: int, nprobe: int, budget: int, want_debug: bool = False,
-           probe_result=None):
+           probe_result=None, nbuckets: int = 255):
     """BBC search of every query in Q over the index dict `ix` (datagen.index_file.read).
 
     Returns (ids int64 [nq x k], d2 fp32 [nq x k]) -- rows sorted by (d^2, id) -- and, when
@@ -302,7 +305,7 @@ def search(ix: dict, Q: np.ndarray, k: int, nprobe: int, budget: int, want_debug
         else:
             ns = int(sizes[:s].sum())
             dmin, dmax = edges(est[:ns], budget)
-            cell = cells(est, dmin, dmax)
+            cell = cells(est, dmin, dmax, nbuckets)
             H = np.bincount(cell, minlength=NCELL)
             tau = threshold(H, budget)
             sup = np.flatnonzero(cell <= tau)

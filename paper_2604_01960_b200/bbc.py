@@ -23,7 +23,7 @@ EXPORTS = ("ivf_load", "ivf_free", "bbc_index_info", "bbc_workspace_size", "bbc_
            "bbc_search_host", "bbc_search_debug", "bbc_set_timing", "bbc_get_timing",
            "bbc_last_stats", "bbc_launch_count", "bbc_last_error", "bbc_nccl_unique_id",
            "bbc_comm_init", "bbc_search_group", "bbc_last_stats2", "bbc_set_probe_mode",
-           "bbc_set_scan_mode", "bbc_stats_vector")
+           "bbc_set_scan_mode", "bbc_stats_vector", "bbc_set_buckets")
 
 STAGES = ("probe", "tables", "sample", "scan", "compact", "rerank", "select", "comm")
 TAU_INF = 1 << 30
@@ -82,6 +82,7 @@ def lib() -> ctypes.CDLL:
         L.bbc_set_timing.argtypes = [vp, ctypes.c_int]
         L.bbc_set_probe_mode.argtypes = [vp, i32]
         L.bbc_set_scan_mode.argtypes = [vp, i32]
+        L.bbc_set_buckets.argtypes = [vp, i32]
         L.bbc_stats_vector.argtypes = [vp, ctypes.POINTER(i64), i32]
         L.bbc_get_timing.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int,
                                      ctypes.POINTER(ctypes.c_int64)]
@@ -97,7 +98,7 @@ def lib() -> ctypes.CDLL:
                    "bbc_search_host", "bbc_search_debug", "bbc_set_timing", "bbc_get_timing",
                    "bbc_last_stats", "bbc_query_capacity", "bbc_nccl_unique_id",
                    "bbc_comm_init", "bbc_search_group", "bbc_last_stats2", "bbc_set_probe_mode",
-           "bbc_set_scan_mode", "bbc_stats_vector"):
+                   "bbc_set_scan_mode", "bbc_stats_vector", "bbc_set_buckets"):
             getattr(L, fn).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -276,6 +277,10 @@ class Index:
         shortlist + canonical re-score (PROBE_TENSOR), or chosen per search (PROBE_AUTO, the
         default: tensor cores when nprobe <= nlist / 32).  Same probe lists in every mode."""
         _check(lib().bbc_set_probe_mode(self._h, int(mode)))
+
+    def set_buckets(self, nbuckets: int) -> None:
+        """B regular buckets of the result buffer (1..255, default 255; Eq. 6, Table 4)."""
+        _check(lib().bbc_set_buckets(self._h, int(nbuckets)))
 
     SCAN_SIMT, SCAN_TENSOR = 0, 1
 

@@ -64,6 +64,7 @@ struct bbc_index_s {
   int* lrank = nullptr;                 // [nlist] (region << 20 | list): query locality order
   float cmax = 0.f;                     // max |c - mu|, rounded up
   int probe_mode = BBC_PROBE_AUTO;       // BBC_PROBE_* (bbc_probe_tc.cuh)
+  int nbuckets = 255;                   // B regular buckets of the result buffer (Eq. 6)
   bool probe_tc_ok = false;             // d <= 1024: the tensor-core probe is available
   int rbq_tc = 0;                       // 1: RaBitQ estimates on the tensor cores (bbc_rbq_tc.cuh)
   int2* rbq_tiles = nullptr;            // [rbq_ntiles] (list, first object) of 128-object tiles
@@ -672,6 +673,7 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
       carve(s.ix, s.p, nb, nprobe, s.ws, s.b, &s.qstage, &s.oids, &s.od2, k, &s.db, W, &s.rb);
       Batch& b = s.b;
       b.nq = nb; b.nprobe = nprobe; b.k = k; b.budget = budget_c; b.cap = s.p.cap;
+      b.nbuckets = s.ix->nbuckets;
       b.stats = s.ix->stats;
       if (host) {
         CU(cudaMemcpyAsync(s.qstage, queries + q0 * ix->d, (size_t)nb * ix->d * 4,
@@ -1096,6 +1098,13 @@ bbc_status bbc_set_probe_mode(bbc_index ix, int32_t mode) {
     return fail(BBC_ERR_ARG, "unknown probe mode");
   if (mode == BBC_PROBE_TENSOR && !ix->probe_tc_ok) return fail(BBC_ERR_ARG, "d too large for the tensor-core probe");
   ix->probe_mode = mode;
+  return BBC_OK;
+}
+
+bbc_status bbc_set_buckets(bbc_index ix, int32_t nbuckets) {
+  if (!ix) return fail(BBC_ERR_ARG, "null index");
+  if (nbuckets < 1 || nbuckets > 255) return fail(BBC_ERR_ARG, "nbuckets must be in [1, 255]");
+  ix->nbuckets = nbuckets;
   return BBC_OK;
 }
 

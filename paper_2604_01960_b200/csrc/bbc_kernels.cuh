@@ -14,6 +14,7 @@ namespace bbc {
 // micro-batch.
 struct Batch {
   int nq;             // queries in this micro-batch
+  int nbuckets;       // B regular equal-width buckets over [d_min, d_max] (1..255; 255 = overflow)
   int nprobe;
   int k;
   long long budget;
@@ -435,14 +436,15 @@ __global__ void __launch_bounds__(256) k_rbq_rotate(Batch b, Dev ix) {
 // bucket id (Eq. 6 with DESIGN R3): precomputed per query
 // ------------------------------------------------------------------------------------------
 struct CellFn {
-  float dmin, dmax, inv;
+  float dmin, dmax, inv, bmax;  // bmax = B - 1
   bool degen;
-  __device__ __forceinline__ void init(float lo, float hi) {
+  __device__ __forceinline__ void init(float lo, float hi, int nb) {
     dmin = lo;
     dmax = hi;
+    bmax = (float)(nb - 1);
     float w = __fsub_rn(hi, lo);
     degen = !(w > 0.f);
-    inv = degen ? 0.f : __fdiv_rn(255.0f, w);
+    inv = degen ? 0.f : __fdiv_rn((float)nb, w);
     if (!degen && isinf(inv)) degen = true;
   }
   __device__ __forceinline__ int operator()(float x) const {
@@ -450,7 +452,7 @@ struct CellFn {
     if (degen) return 0;
     float t = __fmul_rn(__fsub_rn(x, dmin), inv);
     float f = floorf(t);
-    return f < 0.f ? 0 : (f > 254.f ? 254 : (int)f);
+    return f < 0.f ? 0 : (f > bmax ? (int)bmax : (int)f);
   }
 };
 
@@ -654,7 +656,7 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
   }
   // epilogue: lane l holds objects 4(l&7)+j of its groups
   CellFn cf;
-  if (!EST) cf.init(b.edges[2 * q], b.edges[2 * q + 1]);
+  if (!EST) cf.init(b.edges[2 * q], b.edges[2 * q + 1], b.nbuckets);
 #pragma unroll
   for (int i = 0; i < kRqGPL; ++i) {
     const int G = gl0 + 4 * i;
@@ -760,7 +762,7 @@ __global__ void __launch_bounds__(256) k_sample_cells(Batch b) {
   if (blockIdx.x * 256 >= n) return;
   for (int i = threadIdx.x; i < kCells; i += 256) hist[i] = 0;
   CellFn cf;
-  cf.init(b.edges[2 * q], b.edges[2 * q + 1]);
+  cf.init(b.edges[2 * q], b.edges[2 * q + 1], b.nbuckets);
   __syncthreads();
   const float* v = b.val + (size_t)q * b.cap;
   uint8_t* cl = b.cells + (size_t)q * b.cap;
@@ -796,7 +798,7 @@ __global__ void __launch_bounds__(kScanNT) k_rbq_scan(Batch b, Dev ix, int G) {
   CellFn cf;
   if (!SAMPLE) {
     for (int i = threadIdx.x; i < kCells; i += kScanNT) hist[i] = 0;
-    cf.init(b.edges[2 * q], b.edges[2 * q + 1]);
+    cf.init(b.edges[2 * q], b.edges[2 * q + 1], b.nbuckets);
   }
   const float* u = b.table + (size_t)q * D;
   const int* po = b.poff + (size_t)q * (b.nprobe + 1);

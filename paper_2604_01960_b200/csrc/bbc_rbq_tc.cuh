@@ -39,7 +39,7 @@ struct __align__(16) RbqPair {   // per (query, probed list), written by k_rbq_p
 };
 static_assert(sizeof(RbqPair) == 32, "two 16-byte copies per pair");
 
-struct __align__(16) CellQ { float dmin, dmax, inv; int degen; };   // per query (Eq. 6, R3)
+struct __align__(16) CellQ { float dmin, dmax, inv, bmax; int degen; int pad[3]; };   // per query (Eq. 6, R3)
 
 // ------------------------------------------------------------------ per-pair query codes
 // One warp per (query, 4 consecutive probes): the query's rotated vector u stays in registers
@@ -201,9 +201,9 @@ __global__ void k_rbq_cellq(Batch b, CellQ* cq) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= b.nq) return;
   CellFn f;
-  f.init(b.edges[2 * q], b.edges[2 * q + 1]);
+  f.init(b.edges[2 * q], b.edges[2 * q + 1], b.nbuckets);
   CellQ c;
-  c.dmin = f.dmin; c.dmax = f.dmax; c.inv = f.inv; c.degen = f.degen ? 1 : 0;
+  c.dmin = f.dmin; c.dmax = f.dmax; c.inv = f.inv; c.bmax = f.bmax; c.degen = f.degen ? 1 : 0;
   cq[q] = c;
 }
 
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(kRbNT, 1) k_rbq_mma(Batch b, Dev ix, RbqTc t) 
             else if (cq.degen) cell = 0;
             else {
               const float f = floorf(__fmul_rn(__fsub_rn(est, cq.dmin), cq.inv));
-              cell = f < 0.f ? 0 : (f > 254.f ? 254 : (int)f);
+              cell = f < 0.f ? 0 : (f > cq.bmax ? (int)cq.bmax : (int)f);
             }
             b.cells[at] = (uint8_t)cell;
           }

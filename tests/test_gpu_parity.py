@@ -34,14 +34,16 @@ def gpu_index(name):
     return cfg, ix, Q, _IDX[name]
 
 
-def compare(cfg, ix, Q, gidx, k, nprobe, budget, want_est=True, check_final=True):
+def compare(cfg, ix, Q, gidx, k, nprobe, budget, want_est=True, check_final=True, nbuckets=255):
     from oracle import bbc_oracle as O
     q = torch.from_numpy(Q).cuda()
+    gidx.set_buckets(nbuckets)
     ids, d2, t = gidx.search_debug(q, k, nprobe, budget, want_est=want_est)
     torch.cuda.synchronize()
+    gidx.set_buckets(255)
     t = {a: b.cpu().numpy() for a, b in t.items()}
     ids, d2 = ids.cpu().numpy(), d2.cpu().numpy()
-    oi, od, dbg = O.search(ix, Q, k, nprobe, budget, want_debug=True)
+    oi, od, dbg = O.search(ix, Q, k, nprobe, budget, want_debug=True, nbuckets=nbuckets)
     for i, g in enumerate(dbg):
         assert np.array_equal(t["probe"][i], g["probe"]), f"q{i} probe"
         assert np.array_equal(t["rq2"][i].view(np.uint32), g["rq2"].view(np.uint32)), f"q{i} rq2"
@@ -347,3 +349,12 @@ def test_ip_full_probe_unlimited_budget_is_brute_force_mips():
     for i in range(len(Qs)):
         check_final_ids(ids[i].cpu().numpy(), key[i].cpu().numpy(), gi[i], gd[i].astype(np.float32), k)
         np.testing.assert_allclose(np.sort(key[i].cpu().numpy()), gd[i], rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("name", ["C2s", "C3s"])
+@pytest.mark.parametrize("nbuckets", [1, 15, 100])
+def test_parity_bucket_counts(name, nbuckets):
+    """B regular buckets (Eq. 6; Table 4 sweep): histograms, tau, supersets and results equal the
+    oracle's for coarse bucket grids too (PQ and the tensor-core RaBitQ path)."""
+    cfg, ix, Q, g = gpu_index(name)
+    compare(cfg, ix, Q[:8], g, cfg.k, cfg.nprobe, cfg.budget, want_est=False, nbuckets=nbuckets)

@@ -421,3 +421,29 @@ def test_ip_index_file_roundtrip(tmp_path):
     a, _ = O.search(ix, Q, 5, 4, 300)
     b, _ = O.search(back, Q, 5, 4, 300)
     assert np.array_equal(a, b)
+
+
+def test_bucket_count_closed_forms(c1t):
+    """B regular buckets (Eq. 6): B = 1 puts every object <= d_max in bucket 0, so tau = 0 and
+    S* = {est <= d_max}; for every B, tau is the bucket of the budget-th smallest estimate and the
+    superset shrinks (weakly) as the grid refines by doubling within rounding."""
+    cfg, ix, Q, _ = c1t
+    q = Q[0]
+    est, sizes, pos = _probed_est(ix, q, cfg.nprobe)
+    s = O.sample_lists(sizes, cfg.budget)
+    dmin, dmax = O.edges(est[: int(sizes[:s].sum())], cfg.budget)
+    c1 = O.cells(est, dmin, dmax, 1)
+    assert set(np.unique(c1)) <= {0, 255}
+    assert np.array_equal(c1 == 0, ~(est > dmax))
+    assert O.threshold(np.bincount(c1, minlength=256), cfg.budget) == 0
+    kth = np.sort(est)[cfg.budget - 1]
+    sizes_S = []
+    for B in (1, 2, 4, 8, 16, 32, 64, 128, 255):
+        c = O.cells(est, dmin, dmax, B)
+        tau = O.threshold(np.bincount(c, minlength=256), cfg.budget)
+        assert tau == O.cells(np.array([kth], dtype=np.float32), dmin, dmax, B)[0]
+        sizes_S.append(int(np.count_nonzero(c <= tau)))
+        assert sizes_S[-1] >= cfg.budget
+    assert all(a >= b - 2 for a, b in zip(sizes_S[:-2], sizes_S[1:-1]))   # doubling B: nested up to rounding
+    with pytest.raises(ValueError):
+        O.cells(est, dmin, dmax, 0)
