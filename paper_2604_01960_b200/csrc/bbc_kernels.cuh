@@ -484,7 +484,10 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
 }
 
-constexpr int kRqWarps = 32, kRqNT = kRqWarps * 32, kRqEW = 32;
+#ifndef BBC_RQ_WARPS
+#define BBC_RQ_WARPS 32
+#endif
+constexpr int kRqWarps = BBC_RQ_WARPS, kRqNT = kRqWarps * 32, kRqEW = 32;
 constexpr int kRqE = kRqNT * kRqEW;                      // objects per CTA (32768)
 constexpr int kRqMC = 4;                                 // sub-quantizers per chunk
 constexpr int kRqGPL = kRqEW / 4;                        // groups per lane (8)
@@ -569,11 +572,11 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
   if (!EST)
     for (int i = threadIdx.x; i < kCells; i += kRqNT) hist[i] = 0;
   const float* glut = b.table + (size_t)q * M * 256;
-  constexpr int kStage = kRqMC * 256 / kRqNT;        // LUT entries staged per thread
-  static_assert(kStage * kRqNT == kRqMC * 256, "chunk entries must divide evenly");
+  constexpr int kStage = (kRqMC * 256 + kRqNT - 1) / kRqNT;   // LUT entries staged per thread
   float nv[kStage];
 #pragma unroll
-  for (int h = 0; h < kStage; ++h) nv[h] = __ldg(glut + threadIdx.x + h * kRqNT);   // chunk 0
+  for (int h = 0; h < kStage; ++h)
+    nv[h] = threadIdx.x + h * kRqNT < kRqMC * 256 ? __ldg(glut + threadIdx.x + h * kRqNT) : 0.f;   // chunk 0
   __syncthreads();
   // group table: group G = 32 objects starting at flat x0 + 32 G (never straddles a list)
   const int* po = b.poff + (size_t)q * (b.nprobe + 1);
@@ -631,13 +634,17 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
     for (int h = 0; h < kStage; ++h) {
       const float4 a4 = make_float4(nv[h], nv[h], nv[h], nv[h]);
       const int ea = threadIdx.x + h * kRqNT;
-      float4* ra = reinterpret_cast<float4*>(lut + (size_t)((ea >> 9) * 256 + (ea & 255)) * 64 + ((ea >> 8) & 1) * 32);
+      if ((kRqMC * 256) % kRqNT == 0 || ea < kRqMC * 256) {
+        float4* ra = reinterpret_cast<float4*>(lut + (size_t)((ea >> 9) * 256 + (ea & 255)) * 64 + ((ea >> 8) & 1) * 32);
 #pragma unroll
-      for (int r = 0; r < 8; ++r) ra[(r + lane) & 7] = a4;
+        for (int r = 0; r < 8; ++r) ra[(r + lane) & 7] = a4;
+      }
     }
     if (p + 1 < P) {                                  // prefetch chunk p+1's entries
 #pragma unroll
-      for (int h = 0; h < kStage; ++h) nv[h] = __ldg(glut + (p + 1) * kRqMC * 256 + threadIdx.x + h * kRqNT);
+      for (int h = 0; h < kStage; ++h)
+        if ((kRqMC * 256) % kRqNT == 0 || threadIdx.x + h * kRqNT < kRqMC * 256)
+          nv[h] = __ldg(glut + (p + 1) * kRqMC * 256 + threadIdx.x + h * kRqNT);
     }
     __syncthreads();
     const int pn = p + 1 < P ? p + 1 : p;            // code loads run one chunk ahead at the tail
