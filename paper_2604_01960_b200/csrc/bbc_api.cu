@@ -147,7 +147,6 @@ struct StageScope {
 struct RbqBufs {
   uint8_t* qbar = nullptr;
   RbqPair* pinfo = nullptr;
-  CellQ* cq = nullptr;
   int* inv = nullptr;
   int* inv_cnt = nullptr;
   int* inv_off = nullptr;
@@ -176,7 +175,7 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1) {
   p.per_query += 8 + 8 + kCells * 4 + 4 + 4 + (size_t)4 * world;   // DistBuf
   p.fixed = 64 * 256;
   if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) {            // pair codes + inverted index
-    p.per_query += (size_t)nprobe * ((size_t)ix->D + 32 + 4) + 16 + 4 * 256;
+    p.per_query += (size_t)nprobe * ((size_t)ix->D + sizeof(RbqPair) + 4);   // codes, records, inverted index
     p.fixed += (size_t)3 * (ix->nlist + 1) * 4 + 3 * 256;
   }
   return p;
@@ -230,7 +229,6 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, 
     const size_t pairs = (size_t)nqb * nprobe;
     rb->qbar = (uint8_t*)take(pairs * ix->D);
     rb->pinfo = (RbqPair*)take(pairs * sizeof(RbqPair));
-    rb->cq = (CellQ*)take((size_t)nqb * sizeof(CellQ));
     rb->inv = (int*)take(pairs * 4);
     rb->inv_cnt = (int*)take((size_t)(ix->nlist + 1) * 4);
     rb->inv_off = (int*)take((size_t)(ix->nlist + 1) * 4);
@@ -422,10 +420,10 @@ void rbq_tc_pass(Shard& s, const Batch& b, cudaStream_t st, bool sample) {
   k_inv_scan<<<1, 1024, 0, st>>>(s.rb.inv_cnt, s.rb.inv_off, s.rb.inv_cur, ix->nlist);
   k_inv_fill<<<gp, 256, 0, st>>>(b, s.dv, s.rb.inv_cur, s.rb.inv, sample ? 1 : 0);
   if (!sample) {
-    k_rbq_cellq<<<(b.nq + 255) / 256, 256, 0, st>>>(b, s.rb.cq);
+    k_rbq_paircell<<<(unsigned)((pairs + 255) / 256), 256, 0, st>>>(b, s.rb.pinfo);
     g_launches += 1;
   }
-  RbqTc t{s.rb.qbar, s.rb.pinfo, s.rb.cq, s.rb.inv_off, s.rb.inv, ix->rbq_tiles, ix->rbq_pc};
+  RbqTc t{s.rb.qbar, s.rb.pinfo, s.rb.inv_off, s.rb.inv, ix->rbq_tiles, ix->rbq_pc};
   const size_t sm = (size_t)(kRbM + 2 * kRbN) * ix->D + 2 * kRbN * sizeof(RbqPair) +
                     (size_t)kRbMaxPairs * 4 + 3 * kRbM * 4 + 64;
   if (sample) {

@@ -36,10 +36,12 @@ struct __align__(16) RbqPair {   // per (query, probed list), written by k_rbq_p
   float rq2;
   int q;
   long long obase;       // q * cap + poff[q][j]: probe-order position of the list's object 0
+  // the query's bucket function (Eq. 6, R3), filled by k_rbq_paircell once the edges are known
+  float dmin, dmax, inv, bmax;
+  int degen, pad0, pad1, pad2;
 };
-static_assert(sizeof(RbqPair) == 32, "two 16-byte copies per pair");
+static_assert(sizeof(RbqPair) == 64, "four 16-byte copies per pair");
 
-struct __align__(16) CellQ { float dmin, dmax, inv, bmax; int degen; int pad[3]; };   // per query (Eq. 6, R3)
 
 // ------------------------------------------------------------------ per-pair query codes
 // One warp per (query, 4 consecutive probes): the query's rotated vector u stays in registers
@@ -196,15 +198,16 @@ __global__ void k_inv_fill(Batch b, Dev ix, int* cur, int* inv, int sample) {
   if (inv_selected(b, ix, p, sample != 0, &L)) inv[atomicAdd(&cur[L], 1)] = (int)p;
 }
 
-// Per query: the bucket-id function of its edges (after the sample stage).
-__global__ void k_rbq_cellq(Batch b, CellQ* cq) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= b.nq) return;
+// Per pair: the bucket-id function of its query's edges (after the sample stage), copied into
+// the pair record so the GEMM epilogue reads it from shared memory with the other constants.
+__global__ void k_rbq_paircell(Batch b, RbqPair* pinfo) {
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= (long long)b.nq * b.nprobe) return;
+  const int q = (int)(p / b.nprobe);
   CellFn f;
   f.init(b.edges[2 * q], b.edges[2 * q + 1], b.nbuckets);
-  CellQ c;
-  c.dmin = f.dmin; c.dmax = f.dmax; c.inv = f.inv; c.bmax = f.bmax; c.degen = f.degen ? 1 : 0;
-  cq[q] = c;
+  RbqPair& e = pinfo[p];
+  e.dmin = f.dmin; e.dmax = f.dmax; e.inv = f.inv; e.bmax = f.bmax; e.degen = f.degen ? 1 : 0;
 }
 
 // Index-load-time: popcount of every code and the (list, 128-object tile) work list.
@@ -221,7 +224,6 @@ __global__ void k_rbq_popc(const uint8_t* bits, long long n, int D, int* pc) {
 struct RbqTc {
   const uint8_t* qbar;   // [pairs x D]
   const RbqPair* pinfo;  // [pairs]
-  const CellQ* cq;       // [nq]
   const int* inv_off;    // [nlist + 1]
   const int* inv;        // pair ids grouped by list
   const int2* tiles;     // [ntiles] (list, first object)
@@ -292,8 +294,9 @@ __global__ void __launch_bounds__(kRbNT, 1) k_rbq_mma(Batch b, Dev ix, RbqTc t) 
     const int nqt = min(kRbN, np - qt);
     uint8_t* B = sB + (qi & 1) * kRbN * D;
     RbqPair* P = pi + (qi & 1) * kRbN;
-    for (int idx = threadIdx.x; idx < kRbN * (nkc + 2); idx += kRbNT) {
-      const int s = idx / (nkc + 2), kc = idx % (nkc + 2);
+    constexpr int kRec = (int)sizeof(RbqPair) / 16;   // 16-byte copies per pair record
+    for (int idx = threadIdx.x; idx < kRbN * (nkc + kRec); idx += kRbNT) {
+      const int s = idx / (nkc + kRec), kc = idx % (nkc + kRec);
       const int p = s < nqt ? (pid_smem ? s_pid[qt + s] : t.inv[p0 + qt + s]) : 0;
       if (kc < nkc) {
         uint8_t* dst = B + (s >> 3) * sbo + kc * 128 + (s & 7) * 16;
@@ -397,13 +400,12 @@ __global__ void __launch_bounds__(kRbNT, 1) k_rbq_mma(Batch b, Dev ix, RbqTc t) 
           if (SAMPLE) {
             b.val[at] = est;
           } else {                                    // bucket id (Eq. 6, R3); histogram: k_cell_hist
-            const CellQ cq = t.cq[e.q];
             int cell;
-            if (est > cq.dmax) cell = 255;
-            else if (cq.degen) cell = 0;
+            if (est > e.dmax) cell = 255;
+            else if (e.degen) cell = 0;
             else {
-              const float f = floorf(__fmul_rn(__fsub_rn(est, cq.dmin), cq.inv));
-              cell = f < 0.f ? 0 : (f > cq.bmax ? (int)cq.bmax : (int)f);
+              const float f = floorf(__fmul_rn(__fsub_rn(est, e.dmin), e.inv));
+              cell = f < 0.f ? 0 : (f > e.bmax ? (int)e.bmax : (int)f);
             }
             b.cells[at] = (uint8_t)cell;
           }

@@ -358,3 +358,21 @@ def test_parity_bucket_counts(name, nbuckets):
     oracle's for coarse bucket grids too (PQ and the tensor-core RaBitQ path)."""
     cfg, ix, Q, g = gpu_index(name)
     compare(cfg, ix, Q[:8], g, cfg.k, cfg.nprobe, cfg.budget, want_est=False, nbuckets=nbuckets)
+
+
+@pytest.mark.parametrize("name,mult", [("C2s", 4), ("C3s", 8), ("C5s", 4), ("C4ip_s", 2)])
+def test_workspace_bounds_respected(name, mult):
+    """The search stays inside the workspace bbc_workspace_size asks for: a guard region placed
+    right after exactly that many bytes is left untouched (one micro-batch and the minimum)."""
+    cfg, ix, Q, g = gpu_index(name)
+    q = torch.from_numpy(Q).cuda()
+    nprobe = min(cfg.nlist, cfg.nprobe * mult)
+    want, mn = g.workspace_size(len(Q), cfg.k, nprobe, cfg.budget)
+    ref_ids, ref_d2 = g.search(q, cfg.k, nprobe, cfg.budget)
+    for size in (want, mn):
+        guard = 1 << 20
+        buf = torch.full((size + guard,), 0xA5, dtype=torch.uint8, device="cuda")
+        ids, d2 = g.search(q, cfg.k, nprobe, cfg.budget, workspace=buf[:size])
+        torch.cuda.synchronize()
+        assert bool((buf[size:] == 0xA5).all()), f"workspace overflow ({size} bytes)"
+        assert torch.equal(ids, ref_ids) and torch.equal(d2, ref_d2)
