@@ -134,6 +134,25 @@ bbc_status bbc_set_buckets(bbc_index index, int32_t nbuckets);
 bbc_status bbc_set_scan_mode(bbc_index index, int32_t mode);
 
 /*
+ * bbc_set_rerank_order -- the work order of step a7, the exact re-rank of S* (P:L413).
+ * Results are identical in both orders (each candidate's distance is computed by the same lanes
+ * in the same arithmetic order); only which rows are read together differs.
+ *   BBC_RERANK_QUERY : CTAs walk one query's candidates (rows of one query in flight).
+ *   BBC_RERANK_LIST  : the run of candidates a query has in one inverted list is a segment;
+ *                      segments are ordered by list, so the rows in flight belong to a few
+ *                      lists shared by every query probing them and are served from L2.
+ *   BBC_RERANK_AUTO  : (default) LIST when the raw rows exceed 8x the L2 size and the
+ *                      micro-batch re-ranks each row >= 8 times on average (nq * budget / N),
+ *                      else QUERY.
+ * BBC_ERR_ARG for a null index or an unknown order.  Must not change while a search on the
+ * handle is in flight.
+ */
+#define BBC_RERANK_QUERY 0
+#define BBC_RERANK_LIST 1
+#define BBC_RERANK_AUTO 2
+bbc_status bbc_set_rerank_order(bbc_index index, int32_t order);
+
+/*
  * bbc_workspace_size -- bytes of device workspace bbc_search needs for (nq, k, nprobe, budget).
  * The workspace holds per-query scratch sized for the nprobe largest lists (cell ids, candidate
  * rows and distances) plus query/output staging used by bbc_search_host.  Queries are processed

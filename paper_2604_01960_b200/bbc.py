@@ -23,7 +23,7 @@ EXPORTS = ("ivf_load", "ivf_free", "bbc_index_info", "bbc_workspace_size", "bbc_
            "bbc_search_host", "bbc_search_debug", "bbc_set_timing", "bbc_get_timing",
            "bbc_last_stats", "bbc_launch_count", "bbc_last_error", "bbc_nccl_unique_id",
            "bbc_comm_init", "bbc_search_group", "bbc_last_stats2", "bbc_set_probe_mode",
-           "bbc_set_scan_mode", "bbc_stats_vector", "bbc_set_buckets")
+           "bbc_set_scan_mode", "bbc_stats_vector", "bbc_set_buckets", "bbc_set_rerank_order")
 
 STAGES = ("probe", "tables", "sample", "scan", "compact", "rerank", "select", "comm")
 TAU_INF = 1 << 30
@@ -83,6 +83,7 @@ def lib() -> ctypes.CDLL:
         L.bbc_set_probe_mode.argtypes = [vp, i32]
         L.bbc_set_scan_mode.argtypes = [vp, i32]
         L.bbc_set_buckets.argtypes = [vp, i32]
+        L.bbc_set_rerank_order.argtypes = [vp, i32]
         L.bbc_stats_vector.argtypes = [vp, ctypes.POINTER(i64), i32]
         L.bbc_get_timing.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int,
                                      ctypes.POINTER(ctypes.c_int64)]
@@ -98,7 +99,7 @@ def lib() -> ctypes.CDLL:
                    "bbc_search_host", "bbc_search_debug", "bbc_set_timing", "bbc_get_timing",
                    "bbc_last_stats", "bbc_query_capacity", "bbc_nccl_unique_id",
                    "bbc_comm_init", "bbc_search_group", "bbc_last_stats2", "bbc_set_probe_mode",
-                   "bbc_set_scan_mode", "bbc_stats_vector", "bbc_set_buckets"):
+                   "bbc_set_scan_mode", "bbc_stats_vector", "bbc_set_buckets", "bbc_set_rerank_order"):
             getattr(L, fn).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -288,6 +289,14 @@ class Index:
         """RaBitQ estimates with popcounts per (query, list) (SCAN_SIMT) or as list-major integer
         GEMMs on the tensor cores (SCAN_TENSOR, default); PQ indexes ignore it."""
         _check(lib().bbc_set_scan_mode(self._h, int(mode)))
+
+    RERANK_QUERY, RERANK_LIST, RERANK_AUTO = 0, 1, 2
+
+    def set_rerank_order(self, order: int) -> None:
+        """Exact re-rank work order: per query (RERANK_QUERY), per (list, query) segment in list
+        order (RERANK_LIST: rows shared by the queries of a list come from L2), or chosen from
+        the data size and reuse (RERANK_AUTO, default)."""
+        _check(lib().bbc_set_rerank_order(self._h, int(order)))
 
     def set_timing(self, on: bool) -> None:
         _check(lib().bbc_set_timing(self._h, int(on)))

@@ -67,6 +67,7 @@ struct bbc_index_s {
   int nbuckets = 255;                   // B regular buckets of the result buffer (Eq. 6)
   bool probe_tc_ok = false;             // d <= 1024: the tensor-core probe is available
   int rbq_tc = 0;                       // 1: RaBitQ estimates on the tensor cores (bbc_rbq_tc.cuh)
+  int rerank_order = BBC_RERANK_AUTO;    // BBC_RERANK_*: work order of the exact re-rank (a7)
   int2* rbq_tiles = nullptr;            // [rbq_ntiles] (list, first object) of 128-object tiles
   int rbq_ntiles = 0;
   int* rbq_pc = nullptr;                // [n_local] popcount of each code
@@ -78,6 +79,7 @@ struct bbc_index_s {
   long long timed_calls = 0;
   long long microbatches = 0;
   int num_sms = 148;
+  int l2_bytes = 126 << 20;
   void* nccl = nullptr;                 // ncclComm_t of this rank (bbc_comm_init)
   int force_dist = 0;                   // run the sharded code path even at world 1 (tests)
   cudaStream_t copy_stream = nullptr;   // host path: device->host result copies
@@ -173,7 +175,8 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1) {
                 table + (size_t)cap * 13 + (size_t)ix->d * 4 + (size_t)k * 24 + 64 +
                 (size_t)((cap + kChunk - 1) / kChunk) * 8 + (size_t)(nprobe + 1) * 4;
   p.per_query += 8 + 8 + kCells * 4 + 4 + 4 + (size_t)4 * world;   // DistBuf
-  p.fixed = 64 * 256;
+  p.per_query += (size_t)nprobe * 20;                                  // re-rank segments
+  p.fixed = 64 * 256 + (size_t)3 * (ix->nlist + 1) * 4 + 3 * 256;
   if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) {            // pair codes + inverted index
     p.per_query += (size_t)nprobe * ((size_t)ix->D + sizeof(RbqPair) + 4);   // codes, records, inverted index
     p.fixed += (size_t)3 * (ix->nlist + 1) * 4 + 3 * 256;
@@ -213,6 +216,11 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, 
   b.val = (float*)take((size_t)nqb * p.cap * 4);
   b.chunk = (int*)take((size_t)nqb * ((p.cap + kChunk - 1) / kChunk) * 4);
   b.chunkj = (int*)take((size_t)nqb * ((p.cap + kChunk - 1) / kChunk) * 4);
+  b.sstart = (int*)take((size_t)nqb * nprobe * 4);
+  b.rseg = (int4*)take((size_t)nqb * nprobe * 16);
+  b.rs_cnt = (int*)take((size_t)(ix->nlist + 1) * 4);
+  b.rs_off = (int*)take((size_t)(ix->nlist + 1) * 4);
+  b.rs_cur = (int*)take((size_t)(ix->nlist + 1) * 4);
 
   *qstage = (float*)take((size_t)nqb * ix->d * 4);
   *ostage_ids = (long long*)take((size_t)nqb * k * 8);
@@ -402,8 +410,9 @@ void stage_tables(Shard& s, cudaStream_t st) {
   if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) {
     const long long pairs = (long long)s.b.nq * s.b.nprobe;
     if (pairs > 0) {
-      const long long warps = (long long)s.b.nq * ((s.b.nprobe + kPairsPerWarp - 1) / kPairsPerWarp);
-      k_rbq_pairs<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(s.b, s.dv, s.rb.qbar, s.rb.pinfo);
+      set_smem(k_rbq_pairs, (size_t)ix->D * 4);
+      k_rbq_pairs<<<dim3((s.b.nprobe + kPairsPerCta - 1) / kPairsPerCta, s.b.nq), 256, (size_t)ix->D * 4, st>>>(
+          s.b, s.dv, s.rb.qbar, s.rb.pinfo);
       g_launches += 1;
     }
   }
@@ -476,6 +485,17 @@ void stage_scan(Shard& s, cudaStream_t st) {
   }
 }
 
+// AUTO: list order when the raw rows overflow L2 several times over (query order then streams
+// each row from HBM once per query) and each row is, on average, a candidate of several queries
+// of the micro-batch (C3, C4); query order otherwise (C2: rows ~4x L2, already served from L2 in
+// query order; C5: ~3 queries per row).
+bool rerank_list_order(const bbc_index_s* ix, const Batch& b, int rowb) {
+  if (ix->rerank_order != BBC_RERANK_AUTO) return ix->rerank_order == BBC_RERANK_LIST;
+  const double data = (double)ix->n_local * rowb;
+  const double reuse = (double)b.nq * (double)b.budget / std::max<double>(1.0, (double)ix->n_local);
+  return data >= 8.0 * ix->l2_bytes && reuse >= 8.0;
+}
+
 void stage_compact(Shard& s, cudaStream_t st) {
   StageScope sc(s.ix, st, BBC_STAGE_COMPACT);
   const int nb = s.b.nq;
@@ -484,38 +504,78 @@ void stage_compact(Shard& s, cudaStream_t st) {
   k_count<<<dim3((nchunk + kCntPer - 1) / kCntPer, nb), kCmpNT, 0, st>>>(s.b, s.b.chunk, nchunk);
   k_chunk_offsets<<<nb, 256, 0, st>>>(s.b, s.b.chunk, nchunk);
   set_smem(k_emit, (size_t)kChunk * 4);
-  k_emit<<<dim3(nchunk, nb), kCmpNT, (size_t)kChunk * 4, st>>>(s.b, s.dv, s.b.chunk, nchunk);
+  Batch be = s.b;                                   // segment starts only for the list-order re-rank
+  if (!rerank_list_order(s.ix, s.b, s.ix->raw_u8 ? s.ix->d : s.ix->d * 4)) be.sstart = nullptr;
+  k_emit<<<dim3(nchunk, nb), kCmpNT, (size_t)kChunk * 4, st>>>(be, s.dv, s.b.chunk, nchunk);
   g_launches += 4;
 }
+
+// rows per lane group and 16-byte chunks per lane by row size; one row per lane group in flight
+// and high occupancy (4 CTAs/SM) beat deeper per-warp unrolling (tuned on C2: 1.55 ms with 2
+// rows in flight at 2 CTAs/SM -> 0.92 ms)
+#define BBC_RR_VARIANTS(X)                                      \
+  if (rowb <= 128) {                                            \
+    if (u8) X(true, 8, 1, 4, 4);                                \
+    else X(false, 8, 1, 4, 4);                                  \
+  } else if (rowb <= 512) {                                     \
+    if (u8) X(true, 8, 4, 1, 4);                                \
+    else X(false, 8, 4, 1, 4);                                  \
+  } else if (rowb <= 1024) {                                    \
+    X(false, 8, 8, 1, 3);                                       \
+  } else {                                                      \
+    X(false, 32, 8, 1, 2);                                      \
+  }
 
 template <bool IP>
 void launch_rerank(Shard& s, dim3 g, cudaStream_t st, int rowb) {
   const bool u8 = s.ix->raw_u8 != 0;
-  if (rowb <= 128) {
-    if (u8) k_rerank<true, 8, 1, 4, 4, IP><<<g, kRrNT, 0, st>>>(s.b, s.dv);
-    else k_rerank<false, 8, 1, 4, 4, IP><<<g, kRrNT, 0, st>>>(s.b, s.dv);
-  } else if (rowb <= 512) {
-    if (u8) k_rerank<true, 8, 4, 1, 4, IP><<<g, kRrNT, 0, st>>>(s.b, s.dv);
-    else k_rerank<false, 8, 4, 1, 4, IP><<<g, kRrNT, 0, st>>>(s.b, s.dv);
-  } else if (rowb <= 1024) {
-    k_rerank<false, 8, 8, 1, 3, IP><<<g, kRrNT, 0, st>>>(s.b, s.dv);
-  } else {
-    k_rerank<false, 32, 8, 1, 2, IP><<<g, kRrNT, 0, st>>>(s.b, s.dv);
-  }
+#define BBC_RR_Q(U8, LPC, MAXV, STEPS, MINB) k_rerank<U8, LPC, MAXV, STEPS, MINB, IP><<<g, kRrNT, 0, st>>>(s.b, s.dv)
+  BBC_RR_VARIANTS(BBC_RR_Q)
+#undef BBC_RR_Q
 }
+
+template <bool IP, int SPW>
+void launch_rerank_seg(Shard& s, cudaStream_t st, int rowb) {
+  const bool u8 = s.ix->raw_u8 != 0;
+  const long long pairs = (long long)s.b.nq * s.b.nprobe;      // upper bound on the segments
+  const unsigned grid = (unsigned)((pairs + (kRrNT / 32) * SPW - 1) / ((kRrNT / 32) * SPW));
+#define BBC_RR_S(U8, LPC, MAXV, STEPS, MINB) \
+  k_rerank_seg<U8, LPC, MAXV, STEPS, MINB, IP, SPW><<<grid, kRrNT, 0, st>>>(s.b, s.dv, s.b.rseg, s.b.rs_off + s.ix->nlist)
+  BBC_RR_VARIANTS(BBC_RR_S)
+#undef BBC_RR_S
+}
+
+// segments per warp: 8 for rows >= 1 KB, else 4 (tuned: C3 3840 B rows 8 ~ 16 > 4 > 2 > 1; C4 384 B
+// rows 4 > 8 > 2)
+template <bool IP>
+void launch_rerank_list(Shard& s, cudaStream_t st, int rowb) {
+  if (rowb >= 1024) launch_rerank_seg<IP, 8>(s, st, rowb);
+  else launch_rerank_seg<IP, 4>(s, st, rowb);
+}
+
 
 void stage_rerank(Shard& s, cudaStream_t st) {
   bbc_index_s* ix = s.ix;
   StageScope sc(ix, st, BBC_STAGE_RERANK);
   const int nb = s.b.nq;
+  const int rowb = ix->raw_u8 ? ix->d : ix->d * 4;
+  const bool ip = ix->metric == BBC_METRIC_IP;
+  if (rerank_list_order(ix, s.b, rowb)) {
+    // segments (query, first candidate, length) counted, offset and placed by list
+    const unsigned gp = (unsigned)(((long long)nb * s.b.nprobe + 255) / 256);
+    cudaMemsetAsync(s.b.rs_cnt, 0, (size_t)(ix->nlist + 1) * 4, st);
+    k_rr_segments<false><<<gp, 256, 0, st>>>(s.b, s.b.rs_cnt, s.b.rseg);
+    k_inv_scan<<<1, 1024, 0, st>>>(s.b.rs_cnt, s.b.rs_off, s.b.rs_cur, ix->nlist);
+    k_rr_segments<true><<<gp, 256, 0, st>>>(s.b, s.b.rs_cur, s.b.rseg);
+    if (ip) launch_rerank_list<true>(s, st, rowb);
+    else launch_rerank_list<false>(s, st, rowb);
+    g_launches += 4;
+    return;
+  }
   // ~32 CTAs per SM in total: short CTAs keep every SM busy to the end (tuned on C2)
   const int gy = std::max(1, (32 * ix->num_sms + nb - 1) / nb);
-  const int rowb = ix->raw_u8 ? ix->d : ix->d * 4;
   const dim3 g(gy, nb);
-  // lanes per candidate and 16-byte chunks per lane by row size; one row per lane group in
-  // flight and high occupancy (4 CTAs/SM) beat deeper per-warp unrolling (tuned on C2: 1.55 ms
-  // with 2 rows in flight at 2 CTAs/SM -> 0.92 ms)
-  if (ix->metric == BBC_METRIC_IP) launch_rerank<true>(s, g, st, rowb);
+  if (ip) launch_rerank<true>(s, g, st, rowb);
   else launch_rerank<false>(s, g, st, rowb);
   g_launches += 1;
 }
@@ -769,8 +829,9 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
           CU(cudaStreamSynchronize(st));
           b2.nsamp = ns_all;
           if (ix->rbq_tc) {                           // pair records address b2's buffer
-            const long long warps = (long long)nb * ((nprobe + kPairsPerWarp - 1) / kPairsPerWarp);
-            k_rbq_pairs<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(b2, s0.dv, s0.rb.qbar, s0.rb.pinfo);
+            set_smem(k_rbq_pairs, (size_t)ix->D * 4);
+            k_rbq_pairs<<<dim3((nprobe + kPairsPerCta - 1) / kPairsPerCta, nb), 256, (size_t)ix->D * 4, st>>>(
+                b2, s0.dv, s0.rb.qbar, s0.rb.pinfo);
             rbq_tc_pass(s0, b2, st, true);
           } else {
             const size_t sm = (size_t)ix->D * 4 + 4 * (ix->D / 32) * 4;
@@ -1043,6 +1104,7 @@ bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_
     ix->rbq_tc = ok ? 1 : 0;
   }
   cudaDeviceGetAttribute(&ix->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
+  cudaDeviceGetAttribute(&ix->l2_bytes, cudaDevAttrL2CacheSize, cuda_device);
   if (ok && kind == BBC_KIND_PQ) {
     // chunk-major copy of the codes for the replicated-LUT scan (layout: k_transpose_codes)
     std::vector<long long> tb(nlist, 0);
@@ -1112,6 +1174,14 @@ bbc_status bbc_set_scan_mode(bbc_index ix, int32_t mode) {
   if (mode == BBC_SCAN_TENSOR && ix->kind == BBC_KIND_RABITQ && !ix->rbq_pc)
     return fail(BBC_ERR_ARG, "tensor-core RaBitQ scan unavailable for this index (D > 1024)");
   ix->rbq_tc = (mode == BBC_SCAN_TENSOR && ix->kind == BBC_KIND_RABITQ) ? 1 : 0;
+  return BBC_OK;
+}
+
+bbc_status bbc_set_rerank_order(bbc_index ix, int32_t order) {
+  if (!ix) return fail(BBC_ERR_ARG, "null index");
+  if (order != BBC_RERANK_QUERY && order != BBC_RERANK_LIST && order != BBC_RERANK_AUTO)
+    return fail(BBC_ERR_ARG, "unknown re-rank order");
+  ix->rerank_order = order;
   return BBC_OK;
 }
 

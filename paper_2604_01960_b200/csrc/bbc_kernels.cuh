@@ -44,6 +44,11 @@ struct Batch {
   int* nitems;        // [1] number of work items
   int* chunk;         // [nq x nchunk]  per-chunk candidate counts -> offsets (compaction)
   int* chunkj;        // [nq x nchunk]  probed list holding each chunk's first element
+  int* sstart;        // [nq x nprobe]  first candidate of each (query, probe) pair (pairs with poff < n)
+  int4* rseg;         // [nq x nprobe]  re-rank segments (query, first, length) in list order
+  int* rs_cnt;        // [nlist + 1]    segment counts -> offsets (rs_off[nlist] = #segments)
+  int* rs_off;        // [nlist + 1]
+  int* rs_cur;        // [nlist + 1]
 };
 
 // Index arrays on the device.
@@ -1180,6 +1185,8 @@ __global__ void __launch_bounds__(256) k_chunk_offsets(Batch b, int* chunk_cnt, 
 constexpr int kEmitWin = 1024;                       // lists staged per chunk (else global search)
 __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chunk_off, int nchunk) {
   __shared__ int wcnt[kCmpNT / 32];
+  __shared__ int s_pre[kCmpNT];
+  __shared__ unsigned s_flg[kCmpNT];
   __shared__ int s_po[kEmitWin + 1];
   __shared__ long long s_rb[kEmitWin];
   extern __shared__ int s_row[];                     // [kChunk]
@@ -1193,7 +1200,7 @@ __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chu
   const int need = (n + kChunk - 1) / kChunk;        // chunks without candidates exit at once
   const int cbeg = chunk_off[(size_t)q * nchunk + c];
   const int cend = c + 1 < need ? chunk_off[(size_t)q * nchunk + c + 1] : b.ncand[q];
-  if (cend == cbeg) return;
+  if (cend == cbeg) return;                           // segment starts here: rr_segment
   const long long* rb = b.rbase + (size_t)q * nprobe;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int i0 = c * kChunk + threadIdx.x * kPerThr;
@@ -1201,6 +1208,23 @@ __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chu
   const int jc = b.chunkj[(size_t)q * nchunk + c];
   const int jn = (c + 1) * kChunk < n ? b.chunkj[(size_t)q * nchunk + c + 1] : nprobe - 1;
   const int W = jn - jc + 1;                          // lists touching this chunk
+  // pairs whose object range starts in this chunk: j in [jlo, jhi) (first j with po[j] >= x0, x1);
+  // only for the list-order re-rank (sstart != null)
+  const int x0 = c * kChunk, x1 = min(n, x0 + kChunk);
+  int jlo = jc, jhi = jc;
+  if (!b.sstart) {
+  } else if (po[jlo] < x0) ++jlo;
+  else while (jlo > 0 && po[jlo - 1] >= x0) --jlo;
+  if (!b.sstart) {
+    jhi = jlo;
+  } else if (x1 < n) {
+    jhi = jn;
+    if (po[jhi] < x1) ++jhi;
+    else while (jhi > 0 && po[jhi - 1] >= x1) --jhi;
+  } else {
+    jhi = nprobe;
+    while (jhi > 0 && po[jhi - 1] >= n) --jhi;
+  }
   const bool win = W <= kEmitWin;
   if (win)
     for (int t = threadIdx.x; t < W; t += kCmpNT) {
@@ -1227,6 +1251,8 @@ __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chu
     tot += v;
   }
   int pos = pre + incl - mine;
+  s_pre[threadIdx.x] = pos;
+  s_flg[threadIdx.x] = f;
   if (f) {
     // list of the first candidate: last j with po[j] <= i, then walk forward
     const int ifirst = i0 + __ffs(f) - 1;
@@ -1252,6 +1278,11 @@ __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chu
   }
   __syncthreads();
   const int base = chunk_off[(size_t)q * nchunk + c];
+  int* ss = b.sstart + (size_t)q * nprobe;
+  for (int j = jlo + threadIdx.x; j < jhi; j += kCmpNT) {   // candidates before po[j]
+    const int o = po[j] - x0, th = o / kPerThr, bit = o % kPerThr;
+    ss[j] = base + s_pre[th] + __popc(s_flg[th] & ((1u << bit) - 1u));
+  }
   int* out = b.cpos + (size_t)q * b.cap + base;
   for (int t = threadIdx.x; t < tot; t += kCmpNT) out[t] = s_row[t];   // ids: gathered by k_rerank
 }
@@ -1265,11 +1296,123 @@ __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chu
 // of the lane split; tolerance 1e-5 relative to the oracle's fp64).
 // ------------------------------------------------------------------------------------------
 constexpr int kRrNT = 256;
+
+// The lane's share of query q: fp32 rows keep 4 values per 16-byte chunk (qr), uint8 rows 16
+// (qu, MAXV <= 2; else read from L1 per use).
+template <bool U8, int LPC, int MAXV>
+struct RrQuery {
+  static constexpr bool QREG = U8 && MAXV <= 2;
+  float qr[MAXV][4];
+  float qu[QREG ? MAXV : 1][16];
+  const float* qv;
+  __device__ __forceinline__ void load(const float* q, int sl, int per, int nv) {
+    qv = q;
+#pragma unroll
+    for (int v = 0; v < MAXV; ++v) {
+      const int t = sl + LPC * v;
+      if (v < per && t < nv && !U8) {
+        const float4 x = reinterpret_cast<const float4*>(qv)[t];
+        qr[v][0] = x.x; qr[v][1] = x.y; qr[v][2] = x.z; qr[v][3] = x.w;
+      }
+    }
+    if (QREG) {
+#pragma unroll
+      for (int v = 0; v < (QREG ? MAXV : 1); ++v) {
+        const int t = sl + LPC * v;
+        if (v < per && t < nv) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float4 x = reinterpret_cast<const float4*>(qv)[4 * t + e];
+            qu[v][4 * e] = x.x; qu[v][4 * e + 1] = x.y; qu[v][4 * e + 2] = x.z; qu[v][4 * e + 3] = x.w;
+          }
+        }
+      }
+    }
+  }
+};
+
+// One warp: exact d^2 (IP: -<q, x>) of up to 32 candidates whose rows are cp[0 .. n32); writes
+// vv[k] and the original id cid[k].  Rows are fetched with one coalesced load and broadcast by
+// shuffle; LPC lanes per row, STEPS rows per lane group in flight.
+template <bool U8, int LPC, int MAXV, int STEPS, bool IP>
+__device__ __forceinline__ void rr_rows32(const Dev& ix, const RrQuery<U8, LPC, MAXV>& Q,
+                                          const int* __restrict__ cp, int n32, float* __restrict__ vv,
+                                          int* __restrict__ cid, int lane, int per, int nv, int rowb) {
+  constexpr int CPW = 32 / LPC;
+  const int sub = lane / LPC, sl = lane % LPC;
+  const uint8_t* raw = static_cast<const uint8_t*>(ix.raw);
+  const int myrow = lane < n32 ? cp[lane] : 0;
+  for (int k0 = 0; k0 < n32; k0 += CPW * STEPS) {
+    uint4 x[STEPS][MAXV];
+    int kk[STEPS];
+    int idr[STEPS];
+#pragma unroll
+    for (int s = 0; s < STEPS; ++s) {
+      kk[s] = k0 + s * CPW + sub;
+      const int r = __shfl_sync(0xffffffffu, myrow, kk[s] & 31);
+      idr[s] = (sl == 0 && kk[s] < n32) ? (int)__ldg(ix.ids + r) : 0;   // original id (final select)
+      const uint4* rp = reinterpret_cast<const uint4*>(raw + (size_t)r * rowb);
+#pragma unroll
+      for (int v = 0; v < MAXV; ++v) {
+        const int t = sl + LPC * v;
+        if (v < per && t < nv) x[s][v] = __ldg(rp + t);
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < STEPS; ++s) {
+      float acc = 0.f;
+#pragma unroll
+      for (int v = 0; v < MAXV; ++v) {
+        const int t = sl + LPC * v;
+        if (v < per && t < nv) {
+          if (U8) {
+            const uint32_t wv[4] = {x[s][v].x, x[s][v].y, x[s][v].z, x[s][v].w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h)
+#pragma unroll
+              for (int by = 0; by < 4; ++by) {
+                const float xv = (float)((wv[h] >> (8 * by)) & 255u);
+                const float qq = Q.QREG ? Q.qu[Q.QREG ? v : 0][h * 4 + by] : __ldg(Q.qv + t * 16 + h * 4 + by);
+                if (IP) acc = fmaf(xv, qq, acc);
+                else { const float df = xv - qq; acc = fmaf(df, df, acc); }
+              }
+          } else if (IP) {
+            acc = fmaf(__uint_as_float(x[s][v].x), Q.qr[v][0], acc);
+            acc = fmaf(__uint_as_float(x[s][v].y), Q.qr[v][1], acc);
+            acc = fmaf(__uint_as_float(x[s][v].z), Q.qr[v][2], acc);
+            acc = fmaf(__uint_as_float(x[s][v].w), Q.qr[v][3], acc);
+          } else {
+            const float a0 = __uint_as_float(x[s][v].x) - Q.qr[v][0], a1 = __uint_as_float(x[s][v].y) - Q.qr[v][1];
+            const float a2 = __uint_as_float(x[s][v].z) - Q.qr[v][2], a3 = __uint_as_float(x[s][v].w) - Q.qr[v][3];
+            acc = fmaf(a0, a0, acc);
+            acc = fmaf(a1, a1, acc);
+            acc = fmaf(a2, a2, acc);
+            acc = fmaf(a3, a3, acc);
+          }
+        }
+      }
+#pragma unroll
+      for (int o = LPC / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (sl == 0 && kk[s] < n32) {
+        vv[kk[s]] = IP ? -acc : acc;
+        cid[kk[s]] = idr[s];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// a7  exact re-rank.  CTA = (query q, slice of its candidates).  LPC lanes cooperate on one
+// candidate row (LPC = 8 for rows <= 1 KB, else 32): each lane holds its share of the query in
+// registers and loads its share of the row with 16-byte loads; several warp-steps are unrolled
+// so that 8 x 16-byte loads per lane are in flight.  Candidate rows are fetched 32 at a time
+// with one coalesced load and broadcast by shuffle.  Writes exact d^2 to val (fp32, FMA order
+// of the lane split; tolerance 1e-5 relative to the oracle's fp64).
+// ------------------------------------------------------------------------------------------
 template <bool U8, int LPC, int MAXV, int STEPS, int MINB = 1, bool IP = false>
 __global__ void __launch_bounds__(kRrNT, MINB) k_rerank(Batch b, Dev ix) {
-  constexpr int CPW = 32 / LPC;                       // candidates per warp step
   const int q = b.qperm[blockIdx.y];        // neighbours run together: L2 reuse
-  const int lane = threadIdx.x & 31, sub = lane / LPC, sl = lane % LPC;
+  const int lane = threadIdx.x & 31, sl = lane % LPC;
   const int d = ix.d;
   const int rowb = U8 ? d : d * 4;
   const int nv = rowb / 16;
@@ -1277,95 +1420,88 @@ __global__ void __launch_bounds__(kRrNT, MINB) k_rerank(Batch b, Dev ix) {
   const int nc = b.ncand[q];
   const int* cp = b.cpos + (size_t)q * b.cap;
   float* vv = b.val + (size_t)q * b.cap;
-  float qr[MAXV][4];
-  const float* qv = b.Q + (size_t)q * d;
-#pragma unroll
-  for (int v = 0; v < MAXV; ++v) {
-    const int t = sl + LPC * v;
-    if (v < per && t < nv && !U8) {
-      const float4 x = reinterpret_cast<const float4*>(qv)[t];
-      qr[v][0] = x.x; qr[v][1] = x.y; qr[v][2] = x.z; qr[v][3] = x.w;
-    }
-  }
-  // uint8 rows: the lane's 16 query values per 16-byte chunk stay in registers (MAXV <= 2)
-  constexpr bool QREG = U8 && MAXV <= 2;
-  float qu[QREG ? MAXV : 1][16];
-  if (QREG) {
-#pragma unroll
-    for (int v = 0; v < (QREG ? MAXV : 1); ++v) {
-      const int t = sl + LPC * v;
-      if (v < per && t < nv) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float4 x = reinterpret_cast<const float4*>(qv)[4 * t + e];
-          qu[v][4 * e] = x.x; qu[v][4 * e + 1] = x.y; qu[v][4 * e + 2] = x.z; qu[v][4 * e + 3] = x.w;
-        }
-      }
-    }
-  }
-  const uint8_t* raw = static_cast<const uint8_t*>(ix.raw);
+  int* ci = b.cid + (size_t)q * b.cap;
+  RrQuery<U8, LPC, MAXV> Q;
+  Q.load(b.Q + (size_t)q * d, sl, per, nv);
   const int gw = blockIdx.x * (kRrNT / 32) + (threadIdx.x >> 5);
   const int nw = gridDim.x * (kRrNT / 32);
-  for (int cb = gw * 32; cb < nc; cb += nw * 32) {    // 32 candidates per warp round
-    const int myrow = cb + lane < nc ? cp[cb + lane] : 0;
-    const int n32 = min(32, nc - cb);
-    for (int k0 = 0; k0 < n32; k0 += CPW * STEPS) {
-      uint4 x[STEPS][MAXV];
-      int kk[STEPS];
-      int idr[STEPS];
-#pragma unroll
-      for (int s = 0; s < STEPS; ++s) {
-        kk[s] = k0 + s * CPW + sub;
-        const int r = __shfl_sync(0xffffffffu, myrow, kk[s] & 31);
-        idr[s] = (sl == 0 && kk[s] < n32) ? (int)__ldg(ix.ids + r) : 0;   // original id (final select)
-        const uint4* rp = reinterpret_cast<const uint4*>(raw + (size_t)r * rowb);
-#pragma unroll
-        for (int v = 0; v < MAXV; ++v) {
-          const int t = sl + LPC * v;
-          if (v < per && t < nv) x[s][v] = __ldg(rp + t);
-        }
-      }
-#pragma unroll
-      for (int s = 0; s < STEPS; ++s) {
-        float acc = 0.f;
-#pragma unroll
-        for (int v = 0; v < MAXV; ++v) {
-          const int t = sl + LPC * v;
-          if (v < per && t < nv) {
-            if (U8) {
-              const uint32_t wv[4] = {x[s][v].x, x[s][v].y, x[s][v].z, x[s][v].w};
-#pragma unroll
-              for (int h = 0; h < 4; ++h)
-#pragma unroll
-                for (int by = 0; by < 4; ++by) {
-                  const float xv = (float)((wv[h] >> (8 * by)) & 255u);
-                  const float qq = QREG ? qu[QREG ? v : 0][h * 4 + by] : __ldg(qv + t * 16 + h * 4 + by);
-                  if (IP) acc = fmaf(xv, qq, acc);
-                  else { const float df = xv - qq; acc = fmaf(df, df, acc); }
-                }
-            } else if (IP) {
-              acc = fmaf(__uint_as_float(x[s][v].x), qr[v][0], acc);
-              acc = fmaf(__uint_as_float(x[s][v].y), qr[v][1], acc);
-              acc = fmaf(__uint_as_float(x[s][v].z), qr[v][2], acc);
-              acc = fmaf(__uint_as_float(x[s][v].w), qr[v][3], acc);
-            } else {
-              const float a0 = __uint_as_float(x[s][v].x) - qr[v][0], a1 = __uint_as_float(x[s][v].y) - qr[v][1];
-              const float a2 = __uint_as_float(x[s][v].z) - qr[v][2], a3 = __uint_as_float(x[s][v].w) - qr[v][3];
-              acc = fmaf(a0, a0, acc);
-              acc = fmaf(a1, a1, acc);
-              acc = fmaf(a2, a2, acc);
-              acc = fmaf(a3, a3, acc);
-            }
-          }
-        }
-#pragma unroll
-        for (int o = LPC / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (sl == 0 && kk[s] < n32) {
-          vv[cb + kk[s]] = IP ? -acc : acc;
-          b.cid[(size_t)q * b.cap + cb + kk[s]] = idr[s];
-        }
-      }
+  for (int cb = gw * 32; cb < nc; cb += nw * 32)      // 32 candidates per warp round
+    rr_rows32<U8, LPC, MAXV, STEPS, IP>(ix, Q, cp + cb, min(32, nc - cb), vv + cb, ci + cb, lane, per,
+                                        nv, rowb);
+}
+
+// ------------------------------------------------------------------------------------------
+// a7, list-major order.  The same per-candidate arithmetic as k_rerank, but the work is the
+// run of candidates a query has in one inverted list (a "segment"), ordered by list: the warps
+// in flight read the rows of a few lists, which every query probing them shares, so the rows
+// come from L2 instead of HBM (C3: each row is a candidate of ~20 queries of a batch).
+// ------------------------------------------------------------------------------------------
+// Candidates of query q before object position P < n: k_emit's count for a chunk with candidates,
+// the chunk's offset for an empty one (k_emit exits before writing).
+__device__ __forceinline__ int rr_start(const Batch& b, int q, int P, int n, int written) {
+  const int nchunk = (int)((b.cap + kChunk - 1) / kChunk);
+  const int c = P / kChunk;
+  const int need = (n + kChunk - 1) / kChunk;
+  const int cb = b.chunk[(size_t)q * nchunk + c];
+  const int ce = c + 1 < need ? b.chunk[(size_t)q * nchunk + c + 1] : b.ncand[q];
+  return cb == ce ? cb : written;
+}
+
+// The segment of pair p = (q, j): candidates [sstart[p], end) where end is the next pair's start
+// (ncand after the last pair with objects).  Empty segments are not scheduled.
+__device__ __forceinline__ int2 rr_segment(const Batch& b, long long p) {
+  const int q = (int)(p / b.nprobe), j = (int)(p % b.nprobe);
+  const int* po = b.poff + (size_t)q * (b.nprobe + 1);
+  const int n = po[b.nprobe];
+  const int P = po[j];
+  if (P >= n) return make_int2(0, 0);
+  const int s0 = rr_start(b, q, P, n, b.sstart[p]);
+  const int s1 = (j + 1 < b.nprobe && po[j + 1] < n) ? rr_start(b, q, po[j + 1], n, b.sstart[p + 1]) : b.ncand[q];
+  return make_int2(s0, s1 - s0);
+}
+
+// FILL = 0: count the non-empty segments of every list; FILL = 1: write (q, first, length, 0)
+// at the list's cursor.  One thread per pair.
+template <bool FILL>
+__global__ void __launch_bounds__(256) k_rr_segments(Batch b, int* __restrict__ cnt, int4* __restrict__ seg) {
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= (long long)b.nq * b.nprobe) return;
+  const int2 g = rr_segment(b, p);
+  if (g.y <= 0) return;
+  const int L = b.probe[p];
+  if (!FILL) atomicAdd(cnt + L, 1);
+  else seg[atomicAdd(cnt + L, 1)] = make_int4((int)(p / b.nprobe), g.x, g.y, 0);
+}
+
+// Warp w of CTA c takes segments (c * 8 + w) * kRrSPW ..: CTAs are dispatched in index order, so
+// the segments in flight stay a narrow window of the list order (nseg = off[nlist], device-side).
+template <bool U8, int LPC, int MAXV, int STEPS, int MINB, bool IP, int kRrSPW>
+__global__ void __launch_bounds__(kRrNT, MINB) k_rerank_seg(Batch b, Dev ix, const int4* __restrict__ seg,
+                                                            const int* __restrict__ nseg_p) {
+  const int lane = threadIdx.x & 31, sl = lane % LPC;
+  const int d = ix.d;
+  const int rowb = U8 ? d : d * 4;
+  const int nv = rowb / 16;
+  const int per = (nv + LPC - 1) / LPC;
+  const int nseg = *nseg_p;
+  const int s0 = (blockIdx.x * (kRrNT / 32) + (threadIdx.x >> 5)) * kRrSPW;
+  if (s0 >= nseg) return;
+  const int4 mine = lane < kRrSPW && s0 + lane < nseg ? seg[s0 + lane] : make_int4(-1, 0, 0, 0);
+  RrQuery<U8, LPC, MAXV> Q;
+  int qcur = -1;
+#pragma unroll 1
+  for (int i = 0; i < kRrSPW; ++i) {
+    const int q = __shfl_sync(0xffffffffu, mine.x, i);
+    if (q < 0) break;
+    const int t0 = __shfl_sync(0xffffffffu, mine.y, i), len = __shfl_sync(0xffffffffu, mine.z, i);
+    if (q != qcur) {
+      Q.load(b.Q + (size_t)q * d, sl, per, nv);
+      qcur = q;
     }
+    const size_t base = (size_t)q * b.cap + t0;
+    for (int cb = 0; cb < len; cb += 32)
+      rr_rows32<U8, LPC, MAXV, STEPS, IP>(ix, Q, b.cpos + base + cb, min(32, len - cb), b.val + base + cb,
+                                          b.cid + base + cb, lane, per, nv, rowb);
   }
 }
 

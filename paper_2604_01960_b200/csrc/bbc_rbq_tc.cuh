@@ -44,75 +44,74 @@ static_assert(sizeof(RbqPair) == 64, "four 16-byte copies per pair");
 
 
 // ------------------------------------------------------------------ per-pair query codes
-// One warp per (query, 4 consecutive probes): the query's rotated vector u stays in registers
-// (lane holds dims 2 lane + 64 m, m < D/64) across the 4 pairs; w_L is read as float2.
-constexpr int kPairsPerWarp = 4;
+// CTA = (query, 32 consecutive probes): the query's rotated vector u is staged once in shared
+// memory; each warp computes 4 pairs (lane holds dims 4 (lane + 32 m) .. +3 of q').
+constexpr int kPairsPerWarp = 4, kPairsPerCta = 8 * kPairsPerWarp;
 __global__ void __launch_bounds__(256) k_rbq_pairs(Batch b, Dev ix, uint8_t* __restrict__ qbar,
                                                    RbqPair* __restrict__ pinfo) {
-  const int lane = threadIdx.x & 31;
-  const int groups = (b.nprobe + kPairsPerWarp - 1) / kPairsPerWarp;
-  const long long gw = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (gw >= (long long)b.nq * groups) return;
-  const int q = (int)(gw / groups);
-  const int j0 = (int)(gw % groups) * kPairsPerWarp;
+  extern __shared__ __align__(16) float su[];          // [D]
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int q = blockIdx.y;
   const int D = ix.D;
-  const int M2 = D / 64;                              // float2 slots per lane (D % 64 == 0)
-  constexpr int kMaxM2 = 16;                          // D <= 1024
-  const float2* u2 = reinterpret_cast<const float2*>(b.table + (size_t)q * D);
-  float2 uu[kMaxM2];
-#pragma unroll
-  for (int m = 0; m < kMaxM2; ++m)
-    if (m < M2) uu[m] = u2[lane + 32 * m];
+  const int D4 = D / 4;                               // float4 slots; lane holds slots lane + 32 m
+  constexpr int kMaxM4 = 8;                           // D <= 1024
+  for (int i = threadIdx.x; i < D4; i += 256)
+    reinterpret_cast<float4*>(su)[i] = reinterpret_cast<const float4*>(b.table + (size_t)q * D)[i];
+  __syncthreads();
+  const float4* u4 = reinterpret_cast<const float4*>(su);
   const float sD = __fsqrt_rn((float)D);
   for (int jj = 0; jj < kPairsPerWarp; ++jj) {
-    const int j = j0 + jj;
+    const int j = blockIdx.x * kPairsPerCta + wid * kPairsPerWarp + jj;
     if (j >= b.nprobe) break;
     const long long p = (long long)q * b.nprobe + j;
     const int L = b.probe[p];
     const float rq2 = b.rq2[p];
     const float r = __fsqrt_rn(rq2);
     const float rinv = r > 0.f ? __fdiv_rn(1.0f, r) : 0.f;
-    const float2* w2 = reinterpret_cast<const float2*>(ix.wL + (size_t)L * D);
-    float2 qp[kMaxM2];
+    const float4* w4 = reinterpret_cast<const float4*>(ix.wL + (size_t)L * D);
+    float4 qp[kMaxM4];
     float mn = INFINITY, mx = -INFINITY;
-    if (r > 0.f) {
 #pragma unroll
-      for (int m = 0; m < kMaxM2; ++m) {
-        if (m < M2) {
-          const float2 w = w2[lane + 32 * m];
-          float2 v;
-          v.x = __fmul_rn(__fsub_rn(uu[m].x, w.x), rinv);
-          v.y = __fmul_rn(__fsub_rn(uu[m].y, w.y), rinv);
-          qp[m] = v;
-          mn = fminf(mn, fminf(v.x, v.y));
-          mx = fmaxf(mx, fmaxf(v.x, v.y));
-        }
+    for (int m = 0; m < kMaxM4; ++m) {
+      const int i = lane + 32 * m;
+      if (i < D4) {
+        const float4 w = __ldg(w4 + i);
+        const float4 uu = u4[i];
+        float4 v;                                     // q' = (u - w) / r   (r = 0: q' = 0)
+        v.x = __fmul_rn(__fsub_rn(uu.x, w.x), rinv);
+        v.y = __fmul_rn(__fsub_rn(uu.y, w.y), rinv);
+        v.z = __fmul_rn(__fsub_rn(uu.z, w.z), rinv);
+        v.w = __fmul_rn(__fsub_rn(uu.w, w.w), rinv);
+        qp[m] = v;
+        mn = fminf(mn, fminf(fminf(v.x, v.y), fminf(v.z, v.w)));
+        mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
       }
-    } else {
-#pragma unroll
-      for (int m = 0; m < kMaxM2; ++m) qp[m] = make_float2(0.f, 0.f);
-      mn = mx = 0.f;
     }
     mn = warp_min(mn);
     mx = warp_max(mx);
+    if (!(r > 0.f)) mn = mx = 0.f;                    // q' = 0 exactly (no signed zeros)
     const float delta = __fdiv_rn(__fsub_rn(mx, mn), 15.0f);
     const float dinv = delta > 0.f ? __fdiv_rn(1.0f, delta) : 0.f;
-    int sq = 0;
-    uint16_t* qb = reinterpret_cast<uint16_t*>(qbar + (size_t)p * D);
+    unsigned acc = 0;
+    uint32_t* qb = reinterpret_cast<uint32_t*>(qbar + (size_t)p * D);
 #pragma unroll
-    for (int m = 0; m < kMaxM2; ++m) {
-      if (m < M2) {
-        int v0 = 0, v1 = 0;
-        if (delta > 0.f) {                            // floor + convert in one cvt.rmi
-          v0 = __float2int_rd(__fadd_rn(__fmul_rn(__fsub_rn(qp[m].x, mn), dinv), 0.5f));
-          v1 = __float2int_rd(__fadd_rn(__fmul_rn(__fsub_rn(qp[m].y, mn), dinv), 0.5f));
-          v0 = min(15, max(0, v0));
-          v1 = min(15, max(0, v1));
-        }
-        qb[lane + 32 * m] = (uint16_t)(v0 | (v1 << 8));
-        sq += v0 + v1;
+    for (int m = 0; m < kMaxM4; ++m) {
+      const int i = lane + 32 * m;
+      if (i < D4) {
+        // t = fl(fl(q' - mn) * dinv) + 0.5 >= 0; floor(t) = low bits of fl_down(t + 2^23)
+        // (spacing 1 in [2^23, 2^24)), clamped to 15 bytewise. dinv = 0 gives t = 0.5 -> 0.
+        const float f0 = __fadd_rd(__fadd_rn(__fmul_rn(__fsub_rn(qp[m].x, mn), dinv), 0.5f), 8388608.0f);
+        const float f1 = __fadd_rd(__fadd_rn(__fmul_rn(__fsub_rn(qp[m].y, mn), dinv), 0.5f), 8388608.0f);
+        const float f2 = __fadd_rd(__fadd_rn(__fmul_rn(__fsub_rn(qp[m].z, mn), dinv), 0.5f), 8388608.0f);
+        const float f3 = __fadd_rd(__fadd_rn(__fmul_rn(__fsub_rn(qp[m].w, mn), dinv), 0.5f), 8388608.0f);
+        const unsigned lo = __byte_perm(__float_as_uint(f0), __float_as_uint(f1), 0x0040);
+        const unsigned hi = __byte_perm(__float_as_uint(f2), __float_as_uint(f3), 0x0040);
+        const unsigned v4 = __vminu4(__byte_perm(lo, hi, 0x5410), 0x0F0F0F0Fu);
+        qb[i] = v4;
+        acc = __dp4a(v4, 0x01010101u, acc);
       }
     }
+    int sq = (int)acc;
     sq = warp_sum(sq);
     if (lane == 0) {
       RbqPair e;
