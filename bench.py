@@ -242,6 +242,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2604_01960_b200 import Index, launch_count
+    from paper_2604_01960_b200.bbc import measure_l2_read_gbs
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -365,6 +366,14 @@ def main():
         "rerank": {"ms": rr_ms, "bound": "hbm", "bytes": stats["candidates"] * row_bytes,
                    "peak_GBs": peak},
     }
+    if stats.get("rerank_list_batches", 0) > 0:
+        # list-order re-rank: the rows a list's queries share are read from L2, so the bound is
+        # the L2 -> SM read bandwidth, measured on this GPU by bbc_measure_l2_read
+        l2 = measure_l2_read_gbs(0)
+        per["rerank"].update({"bound": "l2", "peak_GBs": l2,
+                              "pipe": "L2 -> SM reads (rows shared by the queries of a list)",
+                              "hbm_view": {"code_bytes": stats["candidates"] * row_bytes,
+                                           "peak_GBs": peak}})
     for v in per.values():
         v["GBs"] = v["bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] > 0 else None
         v["frac"] = v["GBs"] / v["peak_GBs"] if v["GBs"] else None
@@ -393,6 +402,8 @@ def main():
             "unit": "TOP/s" if tens else "GB/s", "frac": per[dom]["frac"],
             "traffic": traffic,
             "peak_source": (peak_src if per[dom]["bound"] == "hbm" else
+                            "measured: bbc_measure_l2_read (L2-resident 48 MiB, 16-byte loads)"
+                            if per[dom]["bound"] == "l2" else
                             "measured bf16 TFLOP/s x 2 (int8/bf16 nominal ratio)" if tens else
                             "derived: 148 SMs x 128 B/clk L1/shared-memory data pipe x sm_max_mhz (DESIGN.md 5)"),
             "per_kernel": per,

@@ -141,9 +141,8 @@ bbc_status bbc_set_scan_mode(bbc_index index, int32_t mode);
  *   BBC_RERANK_LIST  : the run of candidates a query has in one inverted list is a segment;
  *                      segments are ordered by list, so the rows in flight belong to a few
  *                      lists shared by every query probing them and are served from L2.
- *   BBC_RERANK_AUTO  : (default) LIST when the raw rows exceed 8x the L2 size and the
- *                      micro-batch re-ranks each row >= 8 times on average (nq * budget / N),
- *                      else QUERY.
+ *   BBC_RERANK_AUTO  : (default) LIST when the micro-batch re-ranks each row >= 4 times on
+ *                      average (nq * budget / N), else QUERY.
  * BBC_ERR_ARG for a null index or an unknown order.  Must not change while a search on the
  * handle is in flight.
  */
@@ -285,12 +284,22 @@ bbc_status bbc_last_stats(bbc_index index, int64_t* probed, int64_t* candidates,
 bbc_status bbc_last_stats2(bbc_index index, int64_t* probed, int64_t* candidates,
                            int64_t* microbatches, int64_t* sampled);
 /* Counters of the last search, in order: probed objects, candidates |S*|, sample objects,
- * lists shortlisted by the tensor-core probe (0 in SIMT mode), micro-batches.  Copies the first
- * n (<= 5) into out (host memory).  BBC_ERR_ARG for a null index or out with n > 0. */
+ * lists shortlisted by the tensor-core probe (0 in SIMT mode), micro-batches, micro-batches
+ * re-ranked in list order.  Copies the first n (<= 6) into out (host memory).  BBC_ERR_ARG for
+ * a null index or out with n > 0. */
 bbc_status bbc_stats_vector(bbc_index index, int64_t* out, int32_t n);
 
 /* Number of CUDA kernels this library has launched in this process. */
 int64_t bbc_launch_count(void);
+
+/*
+ * bbc_measure_l2_read -- measurement utility (not part of the search path): the device's L2 ->
+ * SM read bandwidth in GB/s, from CTAs that each stream an L2-resident buffer of `bytes`
+ * (>= 1 MiB; choose well below the L2 size) `reps` times with 16-byte loads.  The roofline of
+ * the list-order re-rank, whose rows are served from L2.  Allocates and frees its own buffer
+ * on `cuda_device`.  BBC_ERR_ARG for bad sizes, BBC_ERR_CUDA on a CUDA failure.
+ */
+bbc_status bbc_measure_l2_read(int32_t cuda_device, size_t bytes, int32_t reps, double* gbs);
 
 /* Message for the last non-OK status returned on the calling thread. */
 const char* bbc_last_error(void);

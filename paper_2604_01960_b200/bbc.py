@@ -23,7 +23,8 @@ EXPORTS = ("ivf_load", "ivf_free", "bbc_index_info", "bbc_workspace_size", "bbc_
            "bbc_search_host", "bbc_search_debug", "bbc_set_timing", "bbc_get_timing",
            "bbc_last_stats", "bbc_launch_count", "bbc_last_error", "bbc_nccl_unique_id",
            "bbc_comm_init", "bbc_search_group", "bbc_last_stats2", "bbc_set_probe_mode",
-           "bbc_set_scan_mode", "bbc_stats_vector", "bbc_set_buckets", "bbc_set_rerank_order")
+           "bbc_set_scan_mode", "bbc_stats_vector", "bbc_set_buckets", "bbc_set_rerank_order",
+           "bbc_measure_l2_read")
 
 STAGES = ("probe", "tables", "sample", "scan", "compact", "rerank", "select", "comm")
 TAU_INF = 1 << 30
@@ -84,6 +85,7 @@ def lib() -> ctypes.CDLL:
         L.bbc_set_scan_mode.argtypes = [vp, i32]
         L.bbc_set_buckets.argtypes = [vp, i32]
         L.bbc_set_rerank_order.argtypes = [vp, i32]
+        L.bbc_measure_l2_read.argtypes = [i32, ctypes.c_size_t, i32, ctypes.POINTER(ctypes.c_double)]
         L.bbc_stats_vector.argtypes = [vp, ctypes.POINTER(i64), i32]
         L.bbc_get_timing.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int,
                                      ctypes.POINTER(ctypes.c_int64)]
@@ -99,7 +101,8 @@ def lib() -> ctypes.CDLL:
                    "bbc_search_host", "bbc_search_debug", "bbc_set_timing", "bbc_get_timing",
                    "bbc_last_stats", "bbc_query_capacity", "bbc_nccl_unique_id",
                    "bbc_comm_init", "bbc_search_group", "bbc_last_stats2", "bbc_set_probe_mode",
-                   "bbc_set_scan_mode", "bbc_stats_vector", "bbc_set_buckets", "bbc_set_rerank_order"):
+                   "bbc_set_scan_mode", "bbc_stats_vector", "bbc_set_buckets",
+                   "bbc_set_rerank_order", "bbc_measure_l2_read"):
             getattr(L, fn).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -112,6 +115,14 @@ def _check(status: int) -> None:
 
 def launch_count() -> int:
     return int(lib().bbc_launch_count())
+
+
+def measure_l2_read_gbs(device: int = 0, nbytes: int = 48 << 20, reps: int = 20) -> float:
+    """L2 -> SM read bandwidth (GB/s) of `device` (bbc_measure_l2_read; the roofline of the
+    list-order re-rank)."""
+    v = ctypes.c_double()
+    _check(lib().bbc_measure_l2_read(int(device), int(nbytes), int(reps), ctypes.byref(v)))
+    return v.value
 
 
 def _torch():
@@ -311,7 +322,7 @@ class Index:
         a, b, c, d = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         _check(lib().bbc_last_stats2(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
                                      ctypes.byref(d)))
-        v = (ctypes.c_int64 * 5)()
-        _check(lib().bbc_stats_vector(self._h, v, 5))
+        v = (ctypes.c_int64 * 6)()
+        _check(lib().bbc_stats_vector(self._h, v, 6))
         return dict(probed=a.value, candidates=b.value, microbatches=c.value, sampled=d.value,
-                    shortlisted=v[3])
+                    shortlisted=v[3], rerank_list_batches=v[5])

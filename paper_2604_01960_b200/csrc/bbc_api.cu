@@ -78,6 +78,7 @@ struct bbc_index_s {
   double stage_ms[BBC_NUM_STAGES] = {0};
   long long timed_calls = 0;
   long long microbatches = 0;
+  long long rr_list_batches = 0;        // micro-batches of the last search re-ranked in list order
   int num_sms = 148;
   int l2_bytes = 126 << 20;
   void* nccl = nullptr;                 // ncclComm_t of this rank (bbc_comm_init)
@@ -175,7 +176,7 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1) {
                 table + (size_t)cap * 13 + (size_t)ix->d * 4 + (size_t)k * 24 + 64 +
                 (size_t)((cap + kChunk - 1) / kChunk) * 8 + (size_t)(nprobe + 1) * 4;
   p.per_query += 8 + 8 + kCells * 4 + 4 + 4 + (size_t)4 * world;   // DistBuf
-  p.per_query += (size_t)nprobe * 20;                                  // re-rank segments
+  p.per_query += (size_t)nprobe * 20 + (size_t)(cap / kRrPiece) * 16;   // re-rank pieces
   p.fixed = 64 * 256 + (size_t)3 * (ix->nlist + 1) * 4 + 3 * 256;
   if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) {            // pair codes + inverted index
     p.per_query += (size_t)nprobe * ((size_t)ix->D + sizeof(RbqPair) + 4);   // codes, records, inverted index
@@ -217,7 +218,7 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, 
   b.chunk = (int*)take((size_t)nqb * ((p.cap + kChunk - 1) / kChunk) * 4);
   b.chunkj = (int*)take((size_t)nqb * ((p.cap + kChunk - 1) / kChunk) * 4);
   b.sstart = (int*)take((size_t)nqb * nprobe * 4);
-  b.rseg = (int4*)take((size_t)nqb * nprobe * 16);
+  b.rseg = (int4*)take((size_t)nqb * (nprobe + p.cap / kRrPiece) * 16);
   b.rs_cnt = (int*)take((size_t)(ix->nlist + 1) * 4);
   b.rs_off = (int*)take((size_t)(ix->nlist + 1) * 4);
   b.rs_cur = (int*)take((size_t)(ix->nlist + 1) * 4);
@@ -485,15 +486,15 @@ void stage_scan(Shard& s, cudaStream_t st) {
   }
 }
 
-// AUTO: list order when the raw rows overflow L2 several times over (query order then streams
-// each row from HBM once per query) and each row is, on average, a candidate of several queries
-// of the micro-batch (C3, C4); query order otherwise (C2: rows ~4x L2, already served from L2 in
-// query order; C5: ~3 queries per row).
+// AUTO: list order when each row is, on average, a candidate of >= 4 queries of the micro-batch
+// (nq * budget / N): the queries of a list then share its rows through L2 (C2 0.93 -> 0.90 ms,
+// C3 11.2 -> 6.6, C4 49.8 -> 25.3); query order otherwise (C5: ~3 queries per row, list order
+// 11 % slower -- its segment and query-vector overheads are not repaid).
 bool rerank_list_order(const bbc_index_s* ix, const Batch& b, int rowb) {
+  (void)rowb;
   if (ix->rerank_order != BBC_RERANK_AUTO) return ix->rerank_order == BBC_RERANK_LIST;
-  const double data = (double)ix->n_local * rowb;
   const double reuse = (double)b.nq * (double)b.budget / std::max<double>(1.0, (double)ix->n_local);
-  return data >= 8.0 * ix->l2_bytes && reuse >= 8.0;
+  return reuse >= 4.0;
 }
 
 void stage_compact(Shard& s, cudaStream_t st) {
@@ -534,13 +535,26 @@ void launch_rerank(Shard& s, dim3 g, cudaStream_t st, int rowb) {
 #undef BBC_RR_Q
 }
 
+// Grid: about one warp per kRrSPW pieces.  Pieces <= segments + candidates / kRrPiece, segments
+// <= nq * nprobe; candidates are taken as 1.5x the budget (|S*| is the budget plus part of the
+// threshold bucket); the kernel strides by the grid, so an underestimate costs time, not results.
 template <bool IP, int SPW>
 void launch_rerank_seg(Shard& s, cudaStream_t st, int rowb) {
   const bool u8 = s.ix->raw_u8 != 0;
-  const long long pairs = (long long)s.b.nq * s.b.nprobe;      // upper bound on the segments
-  const unsigned grid = (unsigned)((pairs + (kRrNT / 32) * SPW - 1) / ((kRrNT / 32) * SPW));
-#define BBC_RR_S(U8, LPC, MAXV, STEPS, MINB) \
-  k_rerank_seg<U8, LPC, MAXV, STEPS, MINB, IP, SPW><<<grid, kRrNT, 0, st>>>(s.b, s.dv, s.b.rseg, s.b.rs_off + s.ix->nlist)
+  const long long nq = s.b.nq;
+  const long long cand = std::min<long long>(s.p.cap, s.b.budget + s.b.budget / 2);
+  const long long pieces = nq * s.b.nprobe + nq * cand / kRrPiece;
+  const long long per_cta = (kRrNT / 32) * SPW;
+  const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((pieces + per_cta - 1) / per_cta,
+                                                                           (1LL << 30) / per_cta));
+  const int covered = (int)(grid * per_cta);
+  const int* nseg = s.b.rs_off + s.ix->nlist;
+#define BBC_RR_S(U8, LPC, MAXV, STEPS, MINB)                                                           \
+  do {                                                                                                \
+    k_rerank_seg<U8, LPC, MAXV, STEPS, MINB, IP, SPW, false><<<grid, kRrNT, 0, st>>>(s.b, s.dv, s.b.rseg, nseg, 0); \
+    k_rerank_seg<U8, LPC, MAXV, STEPS, MINB, IP, SPW, true><<<2 * s.ix->num_sms, kRrNT, 0, st>>>(      \
+        s.b, s.dv, s.b.rseg, nseg, covered);                                                          \
+  } while (0)
   BBC_RR_VARIANTS(BBC_RR_S)
 #undef BBC_RR_S
 }
@@ -561,6 +575,7 @@ void stage_rerank(Shard& s, cudaStream_t st) {
   const int rowb = ix->raw_u8 ? ix->d : ix->d * 4;
   const bool ip = ix->metric == BBC_METRIC_IP;
   if (rerank_list_order(ix, s.b, rowb)) {
+    ix->rr_list_batches++;
     // segments (query, first candidate, length) counted, offset and placed by list
     const unsigned gp = (unsigned)(((long long)nb * s.b.nprobe + 255) / 256);
     cudaMemsetAsync(s.b.rs_cnt, 0, (size_t)(ix->nlist + 1) * 4, st);
@@ -569,7 +584,7 @@ void stage_rerank(Shard& s, cudaStream_t st) {
     k_rr_segments<true><<<gp, 256, 0, st>>>(s.b, s.b.rs_cur, s.b.rseg);
     if (ip) launch_rerank_list<true>(s, st, rowb);
     else launch_rerank_list<false>(s, st, rowb);
-    g_launches += 4;
+    g_launches += 5;
     return;
   }
   // ~32 CTAs per SM in total: short CTAs keep every SM busy to the end (tuned on C2)
@@ -717,6 +732,7 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
   for (auto& s : sh) {
     CU(cudaMemsetAsync(s.ix->stats, 0, 4 * sizeof(long long), st));
     s.ix->microbatches = 0;
+    s.ix->rr_list_batches = 0;
     if (s.ix->timing) s.ix->timed_calls++;
     s.dv = dev_view(s.ix);
     // a1 on the tensor cores when it wins: the shortlist re-score reads nprobe centroid rows per
@@ -886,6 +902,61 @@ extern "C" {
 
 const char* bbc_last_error(void) { return g_err.c_str(); }
 int64_t bbc_launch_count(void) { return g_launches.load(); }
+
+// L2 read roofline probe: every CTA streams the whole L2-resident buffer (16-byte loads, 4 in
+// flight per thread, starting at a CTA-specific offset), so after the first pass all reads hit L2.
+__global__ void __launch_bounds__(256) k_l2_read(const uint4* __restrict__ buf, long long n16, int reps,
+                                                 unsigned* __restrict__ sink) {
+  unsigned acc = 0;
+  const long long start = ((long long)blockIdx.x * 7919 * 256) % n16;
+  for (int r = 0; r < reps; ++r) {
+    for (long long i = threadIdx.x; i < n16; i += 4 * 256) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        long long k = start + i + u * 256;
+        k = k >= n16 ? k - n16 : k;
+        v[u] = i + u * 256 < n16 ? __ldcg(buf + k) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc ^= v[u].x ^ v[u].y ^ v[u].z ^ v[u].w;
+    }
+  }
+  if (acc == 0x9e3779b9u) sink[0] = acc;
+}
+
+bbc_status bbc_measure_l2_read(int32_t cuda_device, size_t bytes, int32_t reps, double* gbs) {
+  if (!gbs || bytes < (1u << 20) || reps < 1) return fail(BBC_ERR_ARG, "bad arguments");
+  if (cudaSetDevice(cuda_device) != cudaSuccess) return fail(BBC_ERR_CUDA, "cudaSetDevice failed");
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
+  void* buf = nullptr;
+  unsigned* sink = nullptr;
+  if (cudaMalloc(&buf, bytes) != cudaSuccess || cudaMalloc(&sink, 4) != cudaSuccess) {
+    cudaFree(buf);
+    return fail(BBC_ERR_CUDA, "cudaMalloc failed");
+  }
+  cudaMemset(buf, 1, bytes);
+  const long long n16 = (long long)(bytes / 16);
+  const int grid = sms * 8;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  k_l2_read<<<grid, 256>>>((const uint4*)buf, n16, 1, sink);          // warm L2
+  cudaEventRecord(e0);
+  k_l2_read<<<grid, 256>>>((const uint4*)buf, n16, reps, sink);
+  cudaEventRecord(e1);
+  cudaError_t err = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(buf);
+  cudaFree(sink);
+  if (err != cudaSuccess || ms <= 0.f) return fail(BBC_ERR_CUDA, "L2 probe failed");
+  *gbs = (double)grid * reps * (double)(n16 * 16) / (ms * 1e-3) / 1e9;
+  return BBC_OK;
+}
 
 bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_index* out) {
   bbc_index_s* ix = nullptr;
@@ -1325,8 +1396,8 @@ bbc_status bbc_stats_vector(bbc_index ix, int64_t* out, int32_t n) {
   if (!ix || (!out && n > 0) || n < 0) return fail(BBC_ERR_ARG, "bad argument");
   long long h[4];
   CU(cudaMemcpy(h, ix->stats, sizeof(h), cudaMemcpyDeviceToHost));
-  const long long v[5] = {h[0], h[1], h[2], h[3], ix->microbatches};
-  for (int i = 0; i < n && i < 5; ++i) out[i] = v[i];
+  const long long v[6] = {h[0], h[1], h[2], h[3], ix->microbatches, ix->rr_list_batches};
+  for (int i = 0; i < n && i < 6; ++i) out[i] = v[i];
   return BBC_OK;
 }
 

@@ -45,8 +45,8 @@ struct Batch {
   int* chunk;         // [nq x nchunk]  per-chunk candidate counts -> offsets (compaction)
   int* chunkj;        // [nq x nchunk]  probed list holding each chunk's first element
   int* sstart;        // [nq x nprobe]  first candidate of each (query, probe) pair (pairs with poff < n)
-  int4* rseg;         // [nq x nprobe]  re-rank segments (query, first, length) in list order
-  int* rs_cnt;        // [nlist + 1]    segment counts -> offsets (rs_off[nlist] = #segments)
+  int4* rseg;         // [nq x (nprobe + cap/64)] re-rank pieces (query, first, length) in list order
+  int* rs_cnt;        // [nlist + 1]    piece counts (rs_off[nlist] = #pieces)
   int* rs_off;        // [nlist + 1]
   int* rs_cur;        // [nlist + 1]
 };
@@ -1460,8 +1460,11 @@ __device__ __forceinline__ int2 rr_segment(const Batch& b, long long p) {
   return make_int2(s0, s1 - s0);
 }
 
-// FILL = 0: count the non-empty segments of every list; FILL = 1: write (q, first, length, 0)
-// at the list's cursor.  One thread per pair.
+// FILL = 0: count the work pieces of every list; FILL = 1: write (q, first, length, 0) of each
+// piece at the list's cursor.  One thread per pair; a segment is cut into pieces of at most
+// kRrPiece candidates so that a warp's work is bounded (segment lengths are heavy-tailed: the
+// nearest lists keep most of their objects).
+constexpr int kRrPiece = 64;
 template <bool FILL>
 __global__ void __launch_bounds__(256) k_rr_segments(Batch b, int* __restrict__ cnt, int4* __restrict__ seg) {
   const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1469,39 +1472,53 @@ __global__ void __launch_bounds__(256) k_rr_segments(Batch b, int* __restrict__ 
   const int2 g = rr_segment(b, p);
   if (g.y <= 0) return;
   const int L = b.probe[p];
-  if (!FILL) atomicAdd(cnt + L, 1);
-  else seg[atomicAdd(cnt + L, 1)] = make_int4((int)(p / b.nprobe), g.x, g.y, 0);
+  const int np = (g.y + kRrPiece - 1) / kRrPiece;
+  if (!FILL) {
+    atomicAdd(cnt + L, np);
+  } else {
+    const int at = atomicAdd(cnt + L, np);
+    const int q = (int)(p / b.nprobe);
+    for (int i = 0; i < np; ++i)
+      seg[at + i] = make_int4(q, g.x + i * kRrPiece, min(kRrPiece, g.y - i * kRrPiece), 0);
+  }
 }
 
-// Warp w of CTA c takes segments (c * 8 + w) * kRrSPW ..: CTAs are dispatched in index order, so
-// the segments in flight stay a narrow window of the list order (nseg = off[nlist], device-side).
-template <bool U8, int LPC, int MAXV, int STEPS, int MINB, bool IP, int kRrSPW>
+// Warp w of CTA c takes pieces first + (c * 8 + w) * kRrSPW .. + kRrSPW - 1.  CTAs are
+// dispatched in index order and the grid is sized to about the number of pieces, so the pieces
+// in flight stay a narrow window of the list order (a persistent grid drifts apart over many
+// iterations; a global work counter serialises on one address).  The main launch is single-pass
+// (no loop state: no spills at 64 registers); a TAIL launch strides over any pieces beyond its
+// coverage (normally none).  nseg = off[nlist], device-side.
+template <bool U8, int LPC, int MAXV, int STEPS, int MINB, bool IP, int kRrSPW, bool TAIL>
 __global__ void __launch_bounds__(kRrNT, MINB) k_rerank_seg(Batch b, Dev ix, const int4* __restrict__ seg,
-                                                            const int* __restrict__ nseg_p) {
+                                                            const int* __restrict__ nseg_p, int first) {
   const int lane = threadIdx.x & 31, sl = lane % LPC;
   const int d = ix.d;
   const int rowb = U8 ? d : d * 4;
   const int nv = rowb / 16;
   const int per = (nv + LPC - 1) / LPC;
   const int nseg = *nseg_p;
-  const int s0 = (blockIdx.x * (kRrNT / 32) + (threadIdx.x >> 5)) * kRrSPW;
-  if (s0 >= nseg) return;
-  const int4 mine = lane < kRrSPW && s0 + lane < nseg ? seg[s0 + lane] : make_int4(-1, 0, 0, 0);
   RrQuery<U8, LPC, MAXV> Q;
   int qcur = -1;
+  const int stride = gridDim.x * (kRrNT / 32) * kRrSPW;
 #pragma unroll 1
-  for (int i = 0; i < kRrSPW; ++i) {
-    const int q = __shfl_sync(0xffffffffu, mine.x, i);
-    if (q < 0) break;
-    const int t0 = __shfl_sync(0xffffffffu, mine.y, i), len = __shfl_sync(0xffffffffu, mine.z, i);
-    if (q != qcur) {
-      Q.load(b.Q + (size_t)q * d, sl, per, nv);
-      qcur = q;
+  for (int s0 = first + (blockIdx.x * (kRrNT / 32) + (threadIdx.x >> 5)) * kRrSPW; s0 < nseg;
+       s0 = TAIL ? s0 + stride : nseg) {
+    const int4 mine = lane < kRrSPW && s0 + lane < nseg ? seg[s0 + lane] : make_int4(-1, 0, 0, 0);
+#pragma unroll 1
+    for (int i = 0; i < kRrSPW; ++i) {
+      const int q = __shfl_sync(0xffffffffu, mine.x, i);
+      if (q < 0) break;
+      const int t0 = __shfl_sync(0xffffffffu, mine.y, i), len = __shfl_sync(0xffffffffu, mine.z, i);
+      if (q != qcur) {
+        Q.load(b.Q + (size_t)q * d, sl, per, nv);
+        qcur = q;
+      }
+      const size_t base = (size_t)q * b.cap + t0;
+      for (int cb = 0; cb < len; cb += 32)
+        rr_rows32<U8, LPC, MAXV, STEPS, IP>(ix, Q, b.cpos + base + cb, min(32, len - cb), b.val + base + cb,
+                                            b.cid + base + cb, lane, per, nv, rowb);
     }
-    const size_t base = (size_t)q * b.cap + t0;
-    for (int cb = 0; cb < len; cb += 32)
-      rr_rows32<U8, LPC, MAXV, STEPS, IP>(ix, Q, b.cpos + base + cb, min(32, len - cb), b.val + base + cb,
-                                          b.cid + base + cb, lane, per, nv, rowb);
   }
 }
 

@@ -22,6 +22,7 @@ p.add_argument("--steps", type=int, default=5)
 p.add_argument("--tag", default="")
 p.add_argument("--probe-simt", action="store_true")
 p.add_argument("--scan-simt", action="store_true")
+p.add_argument("--nq", type=int, default=0, help="first nq queries only (0: all)")
 p.add_argument("--rerank", choices=("auto", "query", "list"), default="auto", help="re-rank order")
 a = p.parse_args()
 cfg = configs.get(a.workload)
@@ -33,6 +34,8 @@ if a.scan_simt:
     g.set_scan_mode(g.SCAN_SIMT)
 g.set_rerank_order({"auto": g.RERANK_AUTO, "query": g.RERANK_QUERY, "list": g.RERANK_LIST}[a.rerank])
 q = torch.from_numpy(synth.generate_queries(cfg)).cuda()
+if a.nq:
+    q = q[:a.nq].contiguous()
 ws = g.workspace(len(q), cfg.k, a.nprobe, a.budget, max_bytes=48 << 30)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for _ in range(3):
