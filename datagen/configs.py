@@ -76,6 +76,10 @@ SMALL = {
                       kmeans_iters=6),
     "C5s": C5.replace(name="C5s", N=200_000, nlist=512, nq=24, k=1_500, nprobe=32, budget=3_000,
                       kmeans_iters=6),
+    # fine lists (~20 objects): a compaction chunk of 8,192 objects spans > 256 lists, the
+    # global-search path of k_emit; probe sets of 600 lists
+    "C2f": C2.replace(name="C2f", N=40_000, nlist=2_048, nq=8, k=500, nprobe=600, budget=1_000,
+                      kmeans_iters=4),
 }
 
 # Inner-product / cosine variants ("our result buffer

@@ -1182,7 +1182,7 @@ __global__ void __launch_bounds__(256) k_chunk_offsets(Batch b, int* chunk_cnt, 
 // shared-memory binary search and its row rbase[j] + i.  The chunk's candidate rows are placed
 // in shared memory at their block-scan rank, then written out with coalesced stores (the
 // original ids are gathered by the re-rank, which reads each candidate's row anyway).  Few dependent global accesses per CTA: the kernel is latency-bound.
-constexpr int kEmitWin = 1024;                       // lists staged per chunk (else global search)
+constexpr int kEmitWin = 256;                        // lists staged per chunk (else global search); 6 CTAs/SM
 __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chunk_off, int nchunk) {
   __shared__ int wcnt[kCmpNT / 32];
   __shared__ int s_pre[kCmpNT];
@@ -1191,42 +1191,36 @@ __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chu
   __shared__ long long s_rb[kEmitWin];
   extern __shared__ int s_row[];                     // [kChunk]
   const int q = blockIdx.y;
+  const int c = blockIdx.x;
   const int nprobe = b.nprobe;
   const int* po = b.poff + (size_t)q * (nprobe + 1);
-  const int n = po[nprobe];
-  const int tau = b.tau[q];
-  const int c = blockIdx.x;
-  if (c * kChunk >= n) return;
-  const int need = (n + kChunk - 1) / kChunk;        // chunks without candidates exit at once
-  const int cbeg = chunk_off[(size_t)q * nchunk + c];
-  const int cend = c + 1 < need ? chunk_off[(size_t)q * nchunk + c + 1] : b.ncand[q];
-  if (cend == cbeg) return;                           // segment starts here: rr_segment
-  const long long* rb = b.rbase + (size_t)q * nprobe;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int i0 = c * kChunk + threadIdx.x * kPerThr;
-  const Cells32 cx = chunk_load(b, q, i0, tau == kTauInf ? 0 : n);
-  const int jc = b.chunkj[(size_t)q * nchunk + c];
-  const int jn = (c + 1) * kChunk < n ? b.chunkj[(size_t)q * nchunk + c + 1] : nprobe - 1;
-  const int W = jn - jc + 1;                          // lists touching this chunk
-  // pairs whose object range starts in this chunk: j in [jlo, jhi) (first j with po[j] >= x0, x1);
-  // only for the list-order re-rank (sstart != null)
-  const int x0 = c * kChunk, x1 = min(n, x0 + kChunk);
-  int jlo = jc, jhi = jc;
-  if (!b.sstart) {
-  } else if (po[jlo] < x0) ++jlo;
-  else while (jlo > 0 && po[jlo - 1] >= x0) --jlo;
-  if (!b.sstart) {
-    jhi = jlo;
-  } else if (x1 < n) {
-    jhi = jn;
-    if (po[jhi] < x1) ++jhi;
-    else while (jhi > 0 && po[jhi - 1] >= x1) --jhi;
-  } else {
-    jhi = nprobe;
-    while (jhi > 0 && po[jhi - 1] >= n) --jhi;
+  // Round 1: every load that depends on (q, c) only, issued together (the kernel is bound by
+  // dependent-load latency, not bandwidth).  Cell bytes past n are masked by chunk_flags.
+  const size_t cq = (size_t)q * nchunk + c;
+  const int n = po[nprobe];
+  const int tau = b.tau[q];
+  const int ncq = b.ncand[q];
+  const int cbeg = chunk_off[cq];
+  const int cnext = c + 1 < nchunk ? chunk_off[cq + 1] : 0;
+  const int jc = b.chunkj[cq];
+  const int jnext = c + 1 < nchunk ? b.chunkj[cq + 1] : 0;
+  Cells32 cx{make_uint4(~0u, ~0u, ~0u, ~0u), make_uint4(~0u, ~0u, ~0u, ~0u)};
+  {
+    const uint4* cl = reinterpret_cast<const uint4*>(b.cells + (size_t)q * b.cap + i0);
+    if (i0 + 16 <= b.cap) cx.a = cl[0];              // cap is a multiple of 16, i0 of 32
+    if (i0 + 32 <= b.cap) cx.b = cl[1];
   }
+  if (c * kChunk >= n) return;
+  const int need = (n + kChunk - 1) / kChunk;        // chunks without candidates exit at once
+  const int cend = c + 1 < need ? cnext : ncq;
+  if (cend == cbeg) return;                           // segment starts here: rr_segment
+  const long long* rb = b.rbase + (size_t)q * nprobe;
+  const int jn = (c + 1) * kChunk < n ? jnext : nprobe - 1;
+  const int W = jn - jc + 1;                          // lists touching this chunk
   const bool win = W <= kEmitWin;
-  if (win)
+  if (win)                                            // round 2: the chunk's list window
     for (int t = threadIdx.x; t < W; t += kCmpNT) {
       s_po[t] = po[jc + t];
       s_rb[t] = rb[jc + t];
@@ -1277,13 +1271,29 @@ __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chu
     }
   }
   __syncthreads();
-  const int base = chunk_off[(size_t)q * nchunk + c];
-  int* ss = b.sstart + (size_t)q * nprobe;
-  for (int j = jlo + threadIdx.x; j < jhi; j += kCmpNT) {   // candidates before po[j]
-    const int o = po[j] - x0, th = o / kPerThr, bit = o % kPerThr;
-    ss[j] = base + s_pre[th] + __popc(s_flg[th] & ((1u << bit) - 1u));
+  if (b.sstart) {
+    // list-order re-rank: candidates before the start of every pair whose object range starts
+    // in this chunk, j in [jlo, jhi) (first j with po[j] >= x0, resp. x1)
+    auto P = [&](int j) { return win && j >= jc && j <= jc + W ? s_po[j - jc] : po[j]; };
+    const int x0 = c * kChunk, x1 = min(n, x0 + kChunk);
+    int jlo = jc, jhi;
+    if (P(jlo) < x0) ++jlo;
+    else while (jlo > 0 && P(jlo - 1) >= x0) --jlo;  // empty pairs at x0 (rare)
+    if (x1 < n) {
+      jhi = jn;
+      if (P(jhi) < x1) ++jhi;
+      else while (jhi > 0 && P(jhi - 1) >= x1) --jhi;
+    } else {
+      jhi = nprobe;
+      while (jhi > 0 && P(jhi - 1) >= n) --jhi;
+    }
+    int* ss = b.sstart + (size_t)q * nprobe;
+    for (int j = jlo + threadIdx.x; j < jhi; j += kCmpNT) {
+      const int o = P(j) - x0, th = o / kPerThr, bit = o % kPerThr;
+      ss[j] = cbeg + s_pre[th] + __popc(s_flg[th] & ((1u << bit) - 1u));
+    }
   }
-  int* out = b.cpos + (size_t)q * b.cap + base;
+  int* out = b.cpos + (size_t)q * b.cap + cbeg;
   for (int t = threadIdx.x; t < tot; t += kCmpNT) out[t] = s_row[t];   // ids: gathered by k_rerank
 }
 
