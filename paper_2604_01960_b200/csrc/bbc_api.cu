@@ -434,14 +434,32 @@ void rbq_tc_pass(Shard& s, const Batch& b, cudaStream_t st, bool sample) {
     g_launches += 1;
   }
   RbqTc t{s.rb.qbar, s.rb.pinfo, s.rb.inv_off, s.rb.inv, ix->rbq_tiles, ix->rbq_pc};
+  // warp-specialised pipeline (k_rbq_mma_ws) with 3 query-tile stages when they fit, else 2
+  auto ws_smem = [&](int nst) {
+    return (size_t)(kRbM + nst * kRbN) * ix->D + (size_t)nst * kRbN * sizeof(RbqPair) + 3 * kRbM * 4 +
+           (size_t)(2 * nst + 4) * 8 + 16;
+  };
+  const int nst = ws_smem(3) <= 227 * 1024 ? 3 : 2;
+  const size_t smw = ws_smem(nst);
+  static const bool legacy = getenv("BBC_RBQ_LEGACY") != nullptr;
   const size_t sm = (size_t)(kRbM + 2 * kRbN) * ix->D + 2 * kRbN * sizeof(RbqPair) +
                     (size_t)kRbMaxPairs * 4 + 3 * kRbM * 4 + 64;
   if (sample) {
-    set_smem(k_rbq_mma<true>, sm);
-    k_rbq_mma<true><<<ix->rbq_ntiles, kRbNT, sm, st>>>(b, s.dv, t);
+    if (legacy) {
+      set_smem(k_rbq_mma<true>, sm);
+      k_rbq_mma<true><<<ix->rbq_ntiles, kRbNT, sm, st>>>(b, s.dv, t);
+    } else {
+      set_smem(k_rbq_mma_ws<true>, smw);
+      k_rbq_mma_ws<true><<<ix->rbq_ntiles, kRbWsNT, smw, st>>>(b, s.dv, t, nst);
+    }
   } else {
-    set_smem(k_rbq_mma<false>, sm);
-    k_rbq_mma<false><<<ix->rbq_ntiles, kRbNT, sm, st>>>(b, s.dv, t);
+    if (legacy) {
+      set_smem(k_rbq_mma<false>, sm);
+      k_rbq_mma<false><<<ix->rbq_ntiles, kRbNT, sm, st>>>(b, s.dv, t);
+    } else {
+      set_smem(k_rbq_mma_ws<false>, smw);
+      k_rbq_mma_ws<false><<<ix->rbq_ntiles, kRbWsNT, smw, st>>>(b, s.dv, t, nst);
+    }
     k_cell_hist<<<dim3(std::max(1, (8 * ix->num_sms + b.nq - 1) / b.nq), b.nq), 256, 0, st>>>(b);
     g_launches += 1;
   }

@@ -418,6 +418,210 @@ __global__ void __launch_bounds__(kRbNT, 1) k_rbq_mma(Batch b, Dev ix, RbqTc t) 
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kRbN));
 }
 
+// ------------------------------------------------------------------ warp-specialised variant
+// The same tile work and the same estimates as k_rbq_mma, pipelined: warps 16-23 copy the query
+// tiles (B codes + pair records, cp.async; 8 threads per pair row) into a ring of nst stages,
+// warp 24 (one lane) issues
+// the MMAs of tile qi into one of two TMEM accumulators (64 columns), and warps 0-15 run the
+// epilogue of tile qi - 1 meanwhile.  Hand-offs are mbarriers:
+//   full[s]  (256 producer arrivals) tile's copies landed (after the producer's proxy fence)
+//   empty[s] (1 commit + 16 warps)   MMA read B and the epilogue read the records: stage free
+//   accf[a]  (1 commit)              accumulator a holds tile qi's products
+//   acce[a]  (16 warps)              accumulator a read out: free for tile qi + 2
+constexpr int kRbWsEpi = 16, kRbWsProd = 8, kRbWsNT = (kRbWsEpi + kRbWsProd + 1) * 32;   // 800 threads
+__device__ __forceinline__ void mbar_init(uint32_t a, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(a) : "memory");
+}
+
+template <bool SAMPLE>
+__global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqTc t, int nst) {
+  extern __shared__ __align__(1024) uint8_t rsm3[];
+  const int D = ix.D;
+  const int sbo = (D / 16) * 128;
+  uint8_t* sA = rsm3;                                             // [128 x D] bytes
+  uint8_t* sB = sA + kRbM * D;                                    // [nst][kRbN x D] bytes
+  RbqPair* pi = reinterpret_cast<RbqPair*>(sB + (size_t)nst * kRbN * D);   // [nst][kRbN]
+  float* o_r = reinterpret_cast<float*>(pi + nst * kRbN);         // [128] r_o
+  float* o_g = o_r + kRbM;                                        // [128] 1 / g_o
+  float* o_pc = o_g + kRbM;                                       // [128] popcount (float)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(o_pc + kRbM);      // full[nst] empty[nst] accf[2] acce[2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * nst + 4);
+  const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8u * nst;
+  const uint32_t accf0 = empty0 + 8u * nst, acce0 = accf0 + 16u;
+
+  const int2 tile = t.tiles[blockIdx.x];
+  const int L = tile.x, o0 = tile.y;
+  const int p0 = t.inv_off[L], np = t.inv_off[L + 1] - p0;
+  if (np == 0) return;
+  const long long row0 = ix.loff[L] + o0;
+  const int nobj = min(kRbM, (int)(ix.loff[L + 1] - row0));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nkc = D / 16;
+  const int ntile = (np + kRbN - 1) / kRbN;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nst; ++i) {
+      mbar_init(full0 + 8u * i, kRbWsProd * 32);
+      mbar_init(empty0 + 8u * i, 1 + kRbWsEpi);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(accf0 + 8u * a, 1);
+      mbar_init(acce0 + 8u * a, kRbWsEpi);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(smem_u32(tslot)), "r"(2 * kRbN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // A: code bits of the tile's objects -> bytes 0/1 in the K-major core-matrix layout
+  const int W = D / 32;
+  for (int idx = threadIdx.x; idx < kRbM * W; idx += kRbWsNT) {
+    const int r = idx / W, wv = idx % W;
+    uint32_t x = 0;
+    if (r < nobj) x = reinterpret_cast<const uint32_t*>(ix.bits + (size_t)(row0 + r) * (D / 8))[wv];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t s16 = (x >> (16 * h)) & 0xFFFFu;
+      const uint4 v = make_uint4(nib_bytes(s16 & 15u), nib_bytes((s16 >> 4) & 15u),
+                                 nib_bytes((s16 >> 8) & 15u), nib_bytes(s16 >> 12));
+      const int kc = 2 * wv + h;
+      *reinterpret_cast<uint4*>(sA + (r >> 3) * sbo + kc * 128 + (r & 7) * 16) = v;
+    }
+  }
+  for (int r = threadIdx.x; r < kRbM; r += kRbWsNT) {
+    float fr = 0.f, fg = 1.f, fp = 0.f;
+    if (r < nobj) {
+      const float2 f = reinterpret_cast<const float2*>(ix.factors)[row0 + r];
+      fr = f.x; fg = __fdiv_rn(1.0f, f.y); fp = (float)t.pc[row0 + r];
+    }
+    o_r[r] = fr; o_g[r] = fg; o_pc[r] = fp;
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");     // A (STS) -> MMA reads
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+
+  if (warp >= kRbWsEpi && warp < kRbWsEpi + kRbWsProd) {
+    // ---- producer: 256 threads copy query tile qi into stage qi % nst; thread = (pair row sr,
+    // 16-byte column kc0 + 8 m) of the tile
+    const int pt = threadIdx.x - kRbWsEpi * 32;
+    const int sr = pt >> 3, kc0 = pt & 7;
+    constexpr int kRec = (int)sizeof(RbqPair) / 16;
+    for (int qi = 0; qi < ntile; ++qi) {
+      const int st = qi % nst;
+      if (qi >= nst) mbar_wait(empty0 + 8u * st, (unsigned)((qi / nst - 1) & 1));
+      const int qt = qi * kRbN;
+      if (sr < np - qt) {
+        const int p = t.inv[p0 + qt + sr];
+        uint8_t* Brow = sB + (size_t)st * kRbN * D + (sr >> 3) * sbo + (sr & 7) * 16;
+        const uint8_t* src = t.qbar + (size_t)p * D;
+        for (int kc = kc0; kc < nkc; kc += 8) cp_async16(smem_u32(Brow + kc * 128), src + 16 * kc);
+        if (kc0 < kRec)
+          cp_async16(smem_u32(reinterpret_cast<uint8_t*>(pi + st * kRbN + sr) + 16 * kc0),
+                     reinterpret_cast<const uint8_t*>(t.pinfo + p) + 16 * kc0);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      if (qi > 0) {                                   // tile qi - 1 complete
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(full0 + 8u * ((qi - 1) % nst));
+      }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive(full0 + 8u * ((ntile - 1) % nst));
+  } else if (warp == kRbWsEpi + kRbWsProd) {
+    // ---- MMA issuer
+    if (lane == 0) {
+      for (int qi = 0; qi < ntile; ++qi) {
+        const int st = qi % nst, a = qi & 1;
+        mbar_wait(full0 + 8u * st, (unsigned)((qi / nst) & 1));
+        if (qi >= 2) mbar_wait(acce0 + 8u * a, (unsigned)((qi / 2 - 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t aA = smem_u32(sA), aB = smem_u32(sB + (size_t)st * kRbN * D);
+        const uint32_t acc = tmem + (uint32_t)(a * kRbN);
+        for (int k = 0; k < D / 32; ++k) {
+          const uint32_t o = (uint32_t)k * 256u;
+          i8_mma(acc, umma_desc_k(aA + o, (uint32_t)sbo), umma_desc_k(aB + o, (uint32_t)sbo), k ? 1u : 0u);
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                     ::"r"(accf0 + 8u * a) : "memory");
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                     ::"r"(empty0 + 8u * st) : "memory");
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---- epilogue: warps 0-15, thread = object row r, 8 pairs per warp
+    const int rq = warp & 3, cg = warp >> 2;
+    const int r = 32 * rq + lane;
+    float ro = 0.f, ginv = 0.f, pcf = 0.f;
+    if (r < nobj) { ro = o_r[r]; ginv = o_g[r]; pcf = o_pc[r]; }
+    const float a_ro = __fmul_rn(ro, ro), ro2 = __fmul_rn(2.0f, ro);
+    for (int qi = 0; qi < ntile; ++qi) {
+      const int st = qi % nst, a = qi & 1;
+      const int nqt = min(kRbN, np - qi * kRbN);
+      mbar_wait(accf0 + 8u * a, (unsigned)((qi / 2) & 1));
+      mbar_wait(full0 + 8u * st, (unsigned)((qi / nst) & 1));   // records visible (landed long ago)
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t v[8];
+      const uint32_t taddr = tmem + ((uint32_t)(32 * rq) << 16) + (uint32_t)(a * kRbN + 8 * cg);
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                     "=r"(v[6]), "=r"(v[7])
+                   : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acce0 + 8u * a);
+      const RbqPair* P = pi + st * kRbN;
+      if (r < nobj) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int sp = 8 * cg + c;
+          if (sp >= nqt) continue;
+          const RbqPair& e = P[sp];
+          const long long at = e.obase + o0 + r;
+          // canonical estimator, identical to k_rbq_scan
+          const float t1 = __fmul_rn(e.c2, pcf);
+          const float t2 = __fadd_rn(t1, e.c3);
+          const float t3 = __fmul_rn(e.c1, (float)(int)v[c]);
+          const float oq = __fadd_rn(t3, t2);
+          const float ee = __fmul_rn(oq, ginv);
+          const float sum = __fadd_rn(a_ro, e.rq2);
+          const float ff = __fmul_rn(ro2, e.r);
+          const float est = __fsub_rn(sum, __fmul_rn(ff, ee));
+          if (SAMPLE) {
+            b.val[at] = est;
+          } else {
+            int cell;
+            if (est > e.dmax) cell = 255;
+            else if (e.degen) cell = 0;
+            else {
+              const float f = floorf(__fmul_rn(__fsub_rn(est, e.dmin), e.inv));
+              cell = f < 0.f ? 0 : (f > e.bmax ? (int)e.bmax : (int)f);
+            }
+            b.cells[at] = (uint8_t)cell;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8u * st);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kRbN));
+  }
+}
+
 // Histogram of the bucket ids < 255 of query q's probed objects (Push, Alg. 1 l.1-4).
 __global__ void __launch_bounds__(256) k_cell_hist(Batch b) {
   __shared__ int h[8][kCells];
