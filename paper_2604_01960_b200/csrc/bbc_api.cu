@@ -148,12 +148,14 @@ struct StageScope {
 };
 
 struct RbqBufs {
-  uint8_t* qbar = nullptr;
-  RbqPair* pinfo = nullptr;
-  int* inv = nullptr;
-  int* inv_cnt = nullptr;
-  int* inv_off = nullptr;
-  int* inv_cur = nullptr;
+  uint8_t* qbar = nullptr;     // [slots x D] 32-slot tiles in the MMA operand layout
+  RbqPair* pinfo = nullptr;    // [slots]
+  int* islot = nullptr;        // [nq x nprobe] slot of each pair (-1: not estimated)
+  int* cnt_m = nullptr;        // [nlist + 1] pairs per list
+  int* cnt_s = nullptr;        // [nlist + 1] sample pairs per list
+  int* off = nullptr;          // [nlist + 1] first slot per list (multiple of 32)
+  int* cur_s = nullptr;        // [nlist + 1] fill cursors
+  int* cur_m = nullptr;
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -179,8 +181,9 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1) {
   p.per_query += (size_t)nprobe * 20 + (size_t)(cap / kRrPiece) * 16;   // re-rank pieces
   p.fixed = 64 * 256 + (size_t)3 * (ix->nlist + 1) * 4 + 3 * 256;
   if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) {            // pair codes + inverted index
-    p.per_query += (size_t)nprobe * ((size_t)ix->D + sizeof(RbqPair) + 4);   // codes, records, inverted index
-    p.fixed += (size_t)3 * (ix->nlist + 1) * 4 + 3 * 256;
+    p.per_query += (size_t)nprobe * ((size_t)ix->D + sizeof(RbqPair) + 4);   // codes, records, slots
+    p.fixed += (size_t)32 * ix->nlist * ((size_t)ix->D + sizeof(RbqPair)) +   // per-list padding
+               (size_t)5 * (ix->nlist + 1) * 4 + 8 * 256;
   }
   return p;
 }
@@ -236,12 +239,15 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, 
   db->cnt = (int*)take((size_t)nqb * world * 4);
   if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) {
     const size_t pairs = (size_t)nqb * nprobe;
-    rb->qbar = (uint8_t*)take(pairs * ix->D);
-    rb->pinfo = (RbqPair*)take(pairs * sizeof(RbqPair));
-    rb->inv = (int*)take(pairs * 4);
-    rb->inv_cnt = (int*)take((size_t)(ix->nlist + 1) * 4);
-    rb->inv_off = (int*)take((size_t)(ix->nlist + 1) * 4);
-    rb->inv_cur = (int*)take((size_t)(ix->nlist + 1) * 4);
+    const size_t slots = pairs + (size_t)32 * ix->nlist;   // each list padded to 32 slots
+    rb->qbar = (uint8_t*)take(slots * ix->D);
+    rb->pinfo = (RbqPair*)take(slots * sizeof(RbqPair));
+    rb->islot = (int*)take(pairs * 4);
+    rb->cnt_m = (int*)take((size_t)(ix->nlist + 1) * 4);
+    rb->cnt_s = (int*)take((size_t)(ix->nlist + 1) * 4);
+    rb->off = (int*)take((size_t)(ix->nlist + 1) * 4);
+    rb->cur_s = (int*)take((size_t)(ix->nlist + 1) * 4);
+    rb->cur_m = (int*)take((size_t)(ix->nlist + 1) * 4);
   }
 }
 
@@ -400,6 +406,49 @@ void stage_probe(Shard& s, cudaStream_t st) {
   }
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda): a 2-D uint8 map
+// [rows x cols] (row stride = cols bytes) with boxes of box_rows x box_cols and 128-byte swizzle.
+bool encode_tmap_u8(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint32_t box_cols,
+                    uint32_t box_rows) {
+  using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                          const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                          CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Fn fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !f)
+      return false;
+    fn = reinterpret_cast<Fn>(f);
+  }
+  const cuuint64_t gdim[2] = {cols, rows};
+  const cuuint64_t gstride[1] = {cols};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), gdim, gstride, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// RaBitQ tensor-core path, after the probe: the pair layout (slots grouped by list, sample pairs
+// first, lists padded to 32) and every estimated pair's query code + record at its slot.
+void rbq_pairs(Shard& s, const Batch& b, cudaStream_t st) {
+  bbc_index_s* ix = s.ix;
+  const long long pairs = (long long)b.nq * b.nprobe;
+  if (pairs == 0) return;
+  const unsigned gp = (unsigned)((pairs + 255) / 256);
+  cudaMemsetAsync(s.rb.cnt_m, 0, (size_t)(ix->nlist + 1) * 4, st);
+  cudaMemsetAsync(s.rb.cnt_s, 0, (size_t)(ix->nlist + 1) * 4, st);
+  k_rbq_lcount<<<gp, 256, 0, st>>>(b, s.dv, s.rb.cnt_m, s.rb.cnt_s);
+  k_rbq_lscan<<<1, 1024, 0, st>>>(s.rb.cnt_m, s.rb.cnt_s, s.rb.off, s.rb.cur_s, s.rb.cur_m, ix->nlist);
+  k_rbq_lfill<<<gp, 256, 0, st>>>(b, s.dv, s.rb.cur_s, s.rb.cur_m, s.rb.islot);
+  set_smem(k_rbq_pairs, (size_t)ix->D * 4);
+  k_rbq_pairs<<<dim3((b.nprobe + kPairsPerCta - 1) / kPairsPerCta, b.nq), 256, (size_t)ix->D * 4, st>>>(
+      b, s.dv, s.rb.islot, s.rb.qbar, s.rb.pinfo);
+  g_launches += 4;
+}
+
 void stage_tables(Shard& s, cudaStream_t st) {
   bbc_index_s* ix = s.ix;
   StageScope sc(ix, st, BBC_STAGE_TABLES);
@@ -408,15 +457,7 @@ void stage_tables(Shard& s, cudaStream_t st) {
   else
     k_rbq_rotate<<<dim3((ix->D + 255) / 256, s.b.nq), 256, (size_t)ix->d * 4, st>>>(s.b, s.dv);
   g_launches += 1;
-  if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) {
-    const long long pairs = (long long)s.b.nq * s.b.nprobe;
-    if (pairs > 0) {
-      set_smem(k_rbq_pairs, (size_t)ix->D * 4);
-      k_rbq_pairs<<<dim3((s.b.nprobe + kPairsPerCta - 1) / kPairsPerCta, s.b.nq), 256, (size_t)ix->D * 4, st>>>(
-          s.b, s.dv, s.rb.qbar, s.rb.pinfo);
-      g_launches += 1;
-    }
-  }
+  if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) rbq_pairs(s, s.b, st);
 }
 
 // RaBitQ tensor-core pass over the selected (query, list) pairs: inverted index + list-major GEMM
@@ -424,46 +465,36 @@ void rbq_tc_pass(Shard& s, const Batch& b, cudaStream_t st, bool sample) {
   bbc_index_s* ix = s.ix;
   const long long pairs = (long long)b.nq * b.nprobe;
   if (pairs == 0 || ix->rbq_ntiles == 0) return;
-  const unsigned gp = (unsigned)((pairs + 255) / 256);
-  cudaMemsetAsync(s.rb.inv_cnt, 0, (size_t)(ix->nlist + 1) * 4, st);
-  k_inv_count<<<gp, 256, 0, st>>>(b, s.dv, s.rb.inv_cnt, sample ? 1 : 0);
-  k_inv_scan<<<1, 1024, 0, st>>>(s.rb.inv_cnt, s.rb.inv_off, s.rb.inv_cur, ix->nlist);
-  k_inv_fill<<<gp, 256, 0, st>>>(b, s.dv, s.rb.inv_cur, s.rb.inv, sample ? 1 : 0);
   if (!sample) {
-    k_rbq_paircell<<<(unsigned)((pairs + 255) / 256), 256, 0, st>>>(b, s.rb.pinfo);
+    k_rbq_paircell<<<(unsigned)((pairs + 255) / 256), 256, 0, st>>>(b, s.rb.islot, s.rb.pinfo);
     g_launches += 1;
   }
-  RbqTc t{s.rb.qbar, s.rb.pinfo, s.rb.inv_off, s.rb.inv, ix->rbq_tiles, ix->rbq_pc};
-  // warp-specialised pipeline (k_rbq_mma_ws) with 3 query-tile stages when they fit, else 2
+  RbqTc t{s.rb.qbar, s.rb.pinfo, s.rb.off, s.rb.cnt_s, s.rb.cnt_m, ix->rbq_tiles, ix->rbq_pc};
+  // TMA map of the query codes: [slots x D] bytes, boxes of 32 rows x 128 B, 128-byte swizzle
+  const long long slots = pairs + 32LL * ix->nlist;
+  CUtensorMap tm;
+  if (!encode_tmap_u8(&tm, s.rb.qbar, (uint64_t)ix->D, (uint64_t)slots, 128, kRbN)) {
+    ix->broken = true;                               // reported by the CU check after the stage
+    return;
+  }
+  // 3 query-tile stages when they fit in shared memory, else 2
+  const int nkb = (ix->D + 127) / 128;
   auto ws_smem = [&](int nst) {
-    return (size_t)(kRbM + nst * kRbN) * ix->D + (size_t)nst * kRbN * sizeof(RbqPair) + 3 * kRbM * 4 +
-           (size_t)(2 * nst + 4) * 8 + 16;
+    return (size_t)kRbM * ix->D + (size_t)nst * nkb * kRbN * 128 + (size_t)nst * kRbN * sizeof(RbqPair) +
+           3 * kRbM * 4 + (size_t)(2 * nst + 4) * 8 + 16;
   };
   const int nst = ws_smem(3) <= 227 * 1024 ? 3 : 2;
   const size_t smw = ws_smem(nst);
-  static const bool legacy = getenv("BBC_RBQ_LEGACY") != nullptr;
-  const size_t sm = (size_t)(kRbM + 2 * kRbN) * ix->D + 2 * kRbN * sizeof(RbqPair) +
-                    (size_t)kRbMaxPairs * 4 + 3 * kRbM * 4 + 64;
   if (sample) {
-    if (legacy) {
-      set_smem(k_rbq_mma<true>, sm);
-      k_rbq_mma<true><<<ix->rbq_ntiles, kRbNT, sm, st>>>(b, s.dv, t);
-    } else {
-      set_smem(k_rbq_mma_ws<true>, smw);
-      k_rbq_mma_ws<true><<<ix->rbq_ntiles, kRbWsNT, smw, st>>>(b, s.dv, t, nst);
-    }
+    set_smem(k_rbq_mma_ws<true>, smw);
+    k_rbq_mma_ws<true><<<ix->rbq_ntiles, kRbWsNT, smw, st>>>(b, s.dv, t, nst, tm);
   } else {
-    if (legacy) {
-      set_smem(k_rbq_mma<false>, sm);
-      k_rbq_mma<false><<<ix->rbq_ntiles, kRbNT, sm, st>>>(b, s.dv, t);
-    } else {
-      set_smem(k_rbq_mma_ws<false>, smw);
-      k_rbq_mma_ws<false><<<ix->rbq_ntiles, kRbWsNT, smw, st>>>(b, s.dv, t, nst);
-    }
+    set_smem(k_rbq_mma_ws<false>, smw);
+    k_rbq_mma_ws<false><<<ix->rbq_ntiles, kRbWsNT, smw, st>>>(b, s.dv, t, nst, tm);
     k_cell_hist<<<dim3(std::max(1, (8 * ix->num_sms + b.nq - 1) / b.nq), b.nq), 256, 0, st>>>(b);
     g_launches += 1;
   }
-  g_launches += 4;
+  g_launches += 1;
 }
 
 
@@ -782,6 +813,7 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
       stage_probe(s, st);
       stage_tables(s, st);
       stage_sample_est(s, st);
+      if (s.ix->broken) return fail(BBC_ERR_CUDA, "cuTensorMapEncodeTiled failed (RaBitQ query codes)");
     }
     if (!dist) {
       Shard& s = sh[0];
@@ -863,9 +895,7 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
           CU(cudaStreamSynchronize(st));
           b2.nsamp = ns_all;
           if (ix->rbq_tc) {                           // pair records address b2's buffer
-            set_smem(k_rbq_pairs, (size_t)ix->D * 4);
-            k_rbq_pairs<<<dim3((nprobe + kPairsPerCta - 1) / kPairsPerCta, nb), 256, (size_t)ix->D * 4, st>>>(
-                b2, s0.dv, s0.rb.qbar, s0.rb.pinfo);
+            rbq_pairs(s0, b2, st);
             rbq_tc_pass(s0, b2, st, true);
           } else {
             const size_t sm = (size_t)ix->D * 4 + 4 * (ix->D / 32) * 4;

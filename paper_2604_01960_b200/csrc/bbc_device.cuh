@@ -3,6 +3,7 @@
 // (d_max) and the final top-k by (exact d^2, id) (Collect l.22-23).
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace bbc {

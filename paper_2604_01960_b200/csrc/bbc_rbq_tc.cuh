@@ -10,26 +10,29 @@
 // codes as bytes 0..15, exact int32 accumulation in TMEM).  ip is exact, so every estimate is
 // bit-identical to the SIMT kernel's (same fp32 expression tree afterwards).
 //
+//   k_rbq_l*      : the pair layout: pairs grouped by list (sample pairs j < nsamp first),
+//                   each list's slot range padded to a multiple of 32 (one MMA query tile).
 //   k_rbq_pairs   : per (query, probed list): q' = (u - w_L)/r, v_l, Delta, qbar (bytes), s_q,
-//                   and (c1, c2, c3, r) -- the canonical per-pair part of the estimator.
-//   k_inv_*       : inverted probe index (list -> pairs), for the sample pass (j < nsamp) or
-//                   the Push pass (all j).
-//   k_rbq_mma     : CTA = (list L, tile of 128 objects); A (128 x D bytes) staged once, then
-//                   for each tile of 32 pairs: B (32 x D bytes, cp.async, double-buffered),
-//                   D/32 MMAs (M=128, N=32, K=32), epilogue in registers: estimate (sample)
-//                   or bucket id (Push).
+//                   and (c1, c2, c3, r) -- the canonical per-pair part of the estimator, at the
+//                   pair's slot (codes row-major, coalesced).
+//   k_rbq_mma_ws  : CTA = (list L, tile of 128 objects); A (128 x D bytes) staged once, then
+//                   for each tile of 32 pairs: B (32 x D bytes, TMA tensor copies with 128-byte
+//                   swizzle, one per 128-byte K block) + records (bulk copy) into a ring of
+//                   stages (mbarrier complete_tx), D/32 MMAs
+//                   (M=128, N=32, K=32) into one of two TMEM accumulators, epilogue by 16
+//                   warps: estimate (sample pass) or bucket id (Push).
 //   k_cell_hist   : Push histogram per query from its bucket ids (query-major, shared-memory
 //                   counts, one global flush per CTA: list-major partial histograms would need
 //                   a global atomic per (pair, bucket)).
-// Operand layout: canonical K-major, no swizzle: 8-row x 16-byte core matrices, LBO = 128 B
-// (K-adjacent), SBO = (D/16) x 128 B (8-row groups).
+// Operand layouts, K-major: A (object bits as bytes, written by the CTA) without swizzle: 8-row x
+// 16-byte core matrices, LBO = 128 B (K-adjacent), SBO = (D/16) x 128 B (8-row groups).  B (query
+// codes, TMA) in 128-byte-swizzled K blocks of 32 rows x 128 B (4 KB), SBO = 1 KB.
 #pragma once
 #include "bbc_probe_tc.cuh"
 
 namespace bbc {
 
-constexpr int kRbM = 128, kRbN = 32, kRbNT = 512;
-constexpr int kRbMaxPairs = 4096;   // pair ids of one list kept in shared memory
+constexpr int kRbM = 128, kRbN = 32;
 
 struct __align__(16) RbqPair {   // per (query, probed list), written by k_rbq_pairs
   float c1, c2, c3, r;
@@ -47,8 +50,8 @@ static_assert(sizeof(RbqPair) == 64, "four 16-byte copies per pair");
 // CTA = (query, 32 consecutive probes): the query's rotated vector u is staged once in shared
 // memory; each warp computes 4 pairs (lane holds dims 4 (lane + 32 m) .. +3 of q').
 constexpr int kPairsPerWarp = 4, kPairsPerCta = 8 * kPairsPerWarp;
-__global__ void __launch_bounds__(256) k_rbq_pairs(Batch b, Dev ix, uint8_t* __restrict__ qbar,
-                                                   RbqPair* __restrict__ pinfo) {
+__global__ void __launch_bounds__(256) k_rbq_pairs(Batch b, Dev ix, const int* __restrict__ islot,
+                                                   uint8_t* __restrict__ qbar, RbqPair* __restrict__ pinfo) {
   extern __shared__ __align__(16) float su[];          // [D]
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int q = blockIdx.y;
@@ -64,6 +67,8 @@ __global__ void __launch_bounds__(256) k_rbq_pairs(Batch b, Dev ix, uint8_t* __r
     const int j = blockIdx.x * kPairsPerCta + wid * kPairsPerWarp + jj;
     if (j >= b.nprobe) break;
     const long long p = (long long)q * b.nprobe + j;
+    const int slot = islot[p];
+    if (slot < 0) continue;                           // not estimated on this shard / pass
     const int L = b.probe[p];
     const float rq2 = b.rq2[p];
     const float r = __fsqrt_rn(rq2);
@@ -93,7 +98,7 @@ __global__ void __launch_bounds__(256) k_rbq_pairs(Batch b, Dev ix, uint8_t* __r
     const float delta = __fdiv_rn(__fsub_rn(mx, mn), 15.0f);
     const float dinv = delta > 0.f ? __fdiv_rn(1.0f, delta) : 0.f;
     unsigned acc = 0;
-    uint32_t* qb = reinterpret_cast<uint32_t*>(qbar + (size_t)p * D);
+    uint32_t* qrow = reinterpret_cast<uint32_t*>(qbar + (size_t)slot * D);   // row-major at the slot
 #pragma unroll
     for (int m = 0; m < kMaxM4; ++m) {
       const int i = lane + 32 * m;
@@ -107,7 +112,7 @@ __global__ void __launch_bounds__(256) k_rbq_pairs(Batch b, Dev ix, uint8_t* __r
         const unsigned lo = __byte_perm(__float_as_uint(f0), __float_as_uint(f1), 0x0040);
         const unsigned hi = __byte_perm(__float_as_uint(f2), __float_as_uint(f3), 0x0040);
         const unsigned v4 = __vminu4(__byte_perm(lo, hi, 0x5410), 0x0F0F0F0Fu);
-        qb[i] = v4;
+        qrow[i] = v4;
         acc = __dp4a(v4, 0x01010101u, acc);
       }
     }
@@ -122,31 +127,89 @@ __global__ void __launch_bounds__(256) k_rbq_pairs(Batch b, Dev ix, uint8_t* __r
       e.rq2 = rq2;
       e.q = q;
       e.obase = (long long)q * b.cap + b.poff[(size_t)q * (b.nprobe + 1) + j];
-      pinfo[p] = e;
+      pinfo[slot] = e;
     }
   }
 }
 
-// ------------------------------------------------------------------ inverted probe index
-// Pairs selected for a pass: queries with a sample (nsamp > 0; otherwise tau = infinity and no
-// estimate is needed) and j < nsamp (SAMPLE) or j < nprobe (Push); lists empty on this shard
-// are skipped.
-__device__ __forceinline__ bool inv_selected(const Batch& b, const Dev& ix, long long p, bool sample,
-                                             int* L_out) {
+// ------------------------------------------------------------------ pair layout
+// Pairs estimated on the tensor cores: queries with a sample (nsamp > 0; otherwise tau = infinity
+// and no estimate is needed) and lists non-empty on this shard.  The sample pass uses the pairs
+// with j < nsamp, the Push pass all of them.  Slots: per list L, [off[L], off[L] + cnt_s[L]) the
+// sample pairs, then the others up to off[L] + cnt_m[L]; off[L] is a multiple of 32.
+__device__ __forceinline__ bool rbq_pair_sel(const Batch& b, const Dev& ix, long long p, int* L_out,
+                                             bool* sample) {
   const int q = (int)(p / b.nprobe), j = (int)(p % b.nprobe);
   const int ns = b.nsamp[q];
-  if (ns == 0 || (sample && j >= ns)) return false;
+  if (ns == 0) return false;
   const int L = b.probe[p];
   if (ix.loff[L + 1] == ix.loff[L]) return false;
   *L_out = L;
+  *sample = j < ns;
   return true;
 }
 
-__global__ void k_inv_count(Batch b, Dev ix, int* cnt, int sample) {
+__global__ void k_rbq_lcount(Batch b, Dev ix, int* cnt_m, int* cnt_s) {
   const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= (long long)b.nq * b.nprobe) return;
   int L;
-  if (inv_selected(b, ix, p, sample != 0, &L)) atomicAdd(&cnt[L], 1);
+  bool smp;
+  if (rbq_pair_sel(b, ix, p, &L, &smp)) {
+    atomicAdd(&cnt_m[L], 1);
+    if (smp) atomicAdd(&cnt_s[L], 1);
+  }
+}
+
+__global__ void k_rbq_lfill(Batch b, Dev ix, int* cur_s, int* cur_m, int* islot) {
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= (long long)b.nq * b.nprobe) return;
+  int L;
+  bool smp;
+  islot[p] = rbq_pair_sel(b, ix, p, &L, &smp) ? atomicAdd(smp ? &cur_s[L] : &cur_m[L], 1) : -1;
+}
+
+// off[L] = exclusive scan of cnt_m rounded up to 32; cur_s = off, cur_m = off + cnt_s (one CTA)
+__global__ void __launch_bounds__(1024) k_rbq_lscan(const int* cnt_m, const int* cnt_s, int* off,
+                                                    int* cur_s, int* cur_m, int nlist) {
+  __shared__ int ws[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int base = 0; base < nlist; base += 1024) {
+    const int i = base + threadIdx.x;
+    const int v = i < nlist ? (cnt_m[i] + 31) & ~31 : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += t;
+    }
+    if (lane == 31) ws[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      const int s = ws[lane];
+      int y = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= o) y += t;
+      }
+      ws[lane] = y - s;
+    }
+    __syncthreads();
+    const int c0 = carry;
+    if (i < nlist) {
+      const int o = c0 + ws[wid] + x - v;
+      off[i] = o;
+      cur_s[i] = o;
+      cur_m[i] = o + cnt_s[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = c0 + ws[wid] + x;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) off[nlist] = carry;
 }
 
 // exclusive scan of cnt[nlist] -> off[nlist + 1]; cur = off (one CTA of 1024 threads)
@@ -190,22 +253,17 @@ __global__ void __launch_bounds__(1024) k_inv_scan(const int* cnt, int* off, int
   if (threadIdx.x == 0) off[nlist] = carry;
 }
 
-__global__ void k_inv_fill(Batch b, Dev ix, int* cur, int* inv, int sample) {
-  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= (long long)b.nq * b.nprobe) return;
-  int L;
-  if (inv_selected(b, ix, p, sample != 0, &L)) inv[atomicAdd(&cur[L], 1)] = (int)p;
-}
-
 // Per pair: the bucket-id function of its query's edges (after the sample stage), copied into
 // the pair record so the GEMM epilogue reads it from shared memory with the other constants.
-__global__ void k_rbq_paircell(Batch b, RbqPair* pinfo) {
+__global__ void k_rbq_paircell(Batch b, const int* __restrict__ islot, RbqPair* pinfo) {
   const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= (long long)b.nq * b.nprobe) return;
+  const int slot = islot[p];
+  if (slot < 0) return;
   const int q = (int)(p / b.nprobe);
   CellFn f;
   f.init(b.edges[2 * q], b.edges[2 * q + 1], b.nbuckets);
-  RbqPair& e = pinfo[p];
+  RbqPair& e = pinfo[slot];
   e.dmin = f.dmin; e.dmax = f.dmax; e.inv = f.inv; e.bmax = f.bmax; e.degen = f.degen ? 1 : 0;
 }
 
@@ -221,10 +279,11 @@ __global__ void k_rbq_popc(const uint8_t* bits, long long n, int D, int* pc) {
 
 // ------------------------------------------------------------------ the list-major GEMM
 struct RbqTc {
-  const uint8_t* qbar;   // [pairs x D]
-  const RbqPair* pinfo;  // [pairs]
-  const int* inv_off;    // [nlist + 1]
-  const int* inv;        // pair ids grouped by list
+  const uint8_t* qbar;   // [slots x D] in 32-slot tiles, operand layout (k_rbq_pairs)
+  const RbqPair* pinfo;  // [slots]
+  const int* off;        // [nlist + 1] first slot of each list (multiple of 32)
+  const int* cnt_s;      // [nlist] sample pairs of each list
+  const int* cnt_m;      // [nlist] all pairs of each list
   const int2* tiles;     // [ntiles] (list, first object)
   const int* pc;         // [n_local] popcount of each code
 };
@@ -242,6 +301,23 @@ __device__ __forceinline__ uint64_t umma_desc_k(uint32_t saddr, uint32_t sbo) {
   return d;
 }
 
+// K-major, 128-byte swizzle: rows of 128 B, 8-row atoms of 1 KB (SBO), K advanced inside an atom
+// by moving the start address (32 B per MMA step)
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1 << 16;                            // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024u >> 4) << 32;                 // SBO: 8-row atoms
+  d |= (uint64_t)1 << 46;                            // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                            // SWIZZLE_128B
+  return d;
+}
+
+__device__ __forceinline__ void tma_2d_g2s(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+               ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar) : "memory");
+}
+
 __device__ __forceinline__ void i8_mma(uint32_t tmem_d, uint64_t a, uint64_t bdesc, uint32_t acc) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
@@ -251,199 +327,44 @@ __device__ __forceinline__ void i8_mma(uint32_t tmem_d, uint64_t a, uint64_t bde
 
 __device__ __forceinline__ uint32_t nib_bytes(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
 
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+// bulk global -> shared copy (async proxy) completing on an mbarrier's transaction count
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
 
-// Pipeline per CTA: A staged once; for query tile i: (B_i, pair info_i) were copied with
-// cp.async into buffer i&1 during tile i-1's epilogue -> wait -> MMA_i (one thread) -> issue the
-// copies of tile i+1 -> wait for MMA_i -> epilogue_i (16 warps: 4 row quarters x 4 column
-// groups of 8 pairs).
-template <bool SAMPLE>
-__global__ void __launch_bounds__(kRbNT, 1) k_rbq_mma(Batch b, Dev ix, RbqTc t) {
-  extern __shared__ __align__(1024) uint8_t rsm2[];
-  const int D = ix.D;
-  const int sbo = (D / 16) * 128;
-  uint8_t* sA = rsm2;                                             // [128 x D] bytes
-  uint8_t* sB = sA + kRbM * D;                                    // [2][kRbN x D] bytes
-  RbqPair* pi = reinterpret_cast<RbqPair*>(sB + 2 * kRbN * D);    // [2][kRbN]
-  int* s_pid = reinterpret_cast<int*>(pi + 2 * kRbN);             // [kRbMaxPairs] pair ids
-  float* o_r = reinterpret_cast<float*>(s_pid + kRbMaxPairs);     // [128] r_o
-  float* o_g = o_r + kRbM;                                        // [128] 1 / g_o
-  float* o_pc = o_g + kRbM;                                       // [128] popcount (float)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(o_pc + kRbM);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
-
-  const int2 tile = t.tiles[blockIdx.x];
-  const int L = tile.x, o0 = tile.y;
-  const int p0 = t.inv_off[L], np = t.inv_off[L + 1] - p0;
-  if (np == 0) return;
-  const long long row0 = ix.loff[L] + o0;
-  const int nobj = min(kRbM, (int)(ix.loff[L + 1] - row0));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t bar_a = smem_u32(bar);
-  const int nkc = D / 16;                                         // 16-byte chunks per row
-  const bool pid_smem = np <= kRbMaxPairs;
-  for (int i = threadIdx.x; i < np && pid_smem; i += kRbNT) s_pid[i] = t.inv[p0 + i];
-  __syncthreads();
-  // asynchronous copies of query tile qi (pairs [qi*kRbN, ...)) into buffer qi & 1: the query
-  // codes (B rows) and the pair records, 16 bytes per cp.async
-  auto stage_tile = [&](int qi) {
-    const int qt = qi * kRbN;
-    const int nqt = min(kRbN, np - qt);
-    uint8_t* B = sB + (qi & 1) * kRbN * D;
-    RbqPair* P = pi + (qi & 1) * kRbN;
-    constexpr int kRec = (int)sizeof(RbqPair) / 16;   // 16-byte copies per pair record
-    for (int idx = threadIdx.x; idx < kRbN * (nkc + kRec); idx += kRbNT) {
-      const int s = idx / (nkc + kRec), kc = idx % (nkc + kRec);
-      const int p = s < nqt ? (pid_smem ? s_pid[qt + s] : t.inv[p0 + qt + s]) : 0;
-      if (kc < nkc) {
-        uint8_t* dst = B + (s >> 3) * sbo + kc * 128 + (s & 7) * 16;
-        if (s < nqt) cp_async16(smem_u32(dst), t.qbar + (size_t)p * D + 16 * kc);
-        else *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);
-      } else if (s < nqt) {
-        const int h = kc - nkc;
-        cp_async16(smem_u32(reinterpret_cast<uint8_t*>(P + s) + 16 * h),
-                   reinterpret_cast<const uint8_t*>(t.pinfo + p) + 16 * h);
-      }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                 ::"r"(smem_u32(tslot)), "r"(kRbN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  stage_tile(0);
-  // A: code bits of the tile's objects -> bytes 0/1 in the K-major core-matrix layout
-  const int W = D / 32;
-  for (int idx = threadIdx.x; idx < kRbM * W; idx += kRbNT) {
-    const int r = idx / W, wv = idx % W;
-    uint32_t x = 0;
-    if (r < nobj) x = reinterpret_cast<const uint32_t*>(ix.bits + (size_t)(row0 + r) * (D / 8))[wv];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {                     // 16 bits -> one 16-byte core-matrix row
-      const uint32_t s16 = (x >> (16 * h)) & 0xFFFFu;
-      const uint4 v = make_uint4(nib_bytes(s16 & 15u), nib_bytes((s16 >> 4) & 15u),
-                                 nib_bytes((s16 >> 8) & 15u), nib_bytes(s16 >> 12));
-      const int kc = 2 * wv + h;                      // 16-dim chunk index
-      *reinterpret_cast<uint4*>(sA + (r >> 3) * sbo + kc * 128 + (r & 7) * 16) = v;
-    }
-  }
-  for (int r = threadIdx.x; r < kRbM; r += kRbNT) {
-    float fr = 0.f, fg = 1.f, fp = 0.f;
-    if (r < nobj) {
-      const float2 f = reinterpret_cast<const float2*>(ix.factors)[row0 + r];
-      fr = f.x; fg = __fdiv_rn(1.0f, f.y); fp = (float)t.pc[row0 + r];
-    }
-    o_r[r] = fr; o_g[r] = fg; o_pc[r] = fp;
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = *tslot;
-  const uint32_t aA = smem_u32(sA);
-  const int ntile = (np + kRbN - 1) / kRbN;
-  const int rq = warp & 3, cg = warp >> 2;            // row quarter, column group (8 pairs)
-  const int r = 32 * rq + lane;
-  float ro = 0.f, ginv = 0.f, pcf = 0.f;
-  if (r < nobj) { ro = o_r[r]; ginv = o_g[r]; pcf = o_pc[r]; }
-  const float a_ro = __fmul_rn(ro, ro), ro2 = __fmul_rn(2.0f, ro);
-  for (int qi = 0; qi < ntile; ++qi) {
-    const int nqt = min(kRbN, np - qi * kRbN);
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // cp.async/STS -> MMA reads
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t aB = smem_u32(sB + (qi & 1) * kRbN * D);
-      for (int s = 0; s < D / 32; ++s) {              // K = 32 bytes per MMA: 2 core matrices
-        const uint32_t o = (uint32_t)s * 256u;
-        i8_mma(tmem, umma_desc_k(aA + o, (uint32_t)sbo), umma_desc_k(aB + o, (uint32_t)sbo), s ? 1u : 0u);
-      }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-                   ::"r"(bar_a) : "memory");
-    }
-    if (qi + 1 < ntile) stage_tile(qi + 1);           // overlaps the MMA and the epilogue
-    mbar_wait(bar_a, (uint32_t)(qi & 1));
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    {
-      uint32_t v[8];
-      const uint32_t taddr = tmem + ((uint32_t)(32 * rq) << 16) + (uint32_t)(8 * cg);
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                   : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
-                     "=r"(v[6]), "=r"(v[7])
-                   : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      const RbqPair* P = pi + (qi & 1) * kRbN;
-      if (r < nobj) {
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const int s = 8 * cg + c;
-          if (s >= nqt) continue;
-          const RbqPair& e = P[s];
-          const long long at = e.obase + o0 + r;
-          // canonical estimator, identical to k_rbq_scan
-          const float t1 = __fmul_rn(e.c2, pcf);
-          const float t2 = __fadd_rn(t1, e.c3);
-          const float t3 = __fmul_rn(e.c1, (float)(int)v[c]);
-          const float oq = __fadd_rn(t3, t2);
-          const float ee = __fmul_rn(oq, ginv);
-          const float sum = __fadd_rn(a_ro, e.rq2);
-          const float ff = __fmul_rn(ro2, e.r);
-          const float est = __fsub_rn(sum, __fmul_rn(ff, ee));
-          if (SAMPLE) {
-            b.val[at] = est;
-          } else {                                    // bucket id (Eq. 6, R3); histogram: k_cell_hist
-            int cell;
-            if (est > e.dmax) cell = 255;
-            else if (e.degen) cell = 0;
-            else {
-              const float f = floorf(__fmul_rn(__fsub_rn(est, e.dmin), e.inv));
-              cell = f < 0.f ? 0 : (f > e.bmax ? (int)e.bmax : (int)f);
-            }
-            b.cells[at] = (uint8_t)cell;
-          }
-        }
-      }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();                                  // TMEM and buffer qi & 1 free
-  }
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kRbN));
-}
-
-// ------------------------------------------------------------------ warp-specialised variant
-// The same tile work and the same estimates as k_rbq_mma, pipelined: warps 16-23 copy the query
-// tiles (B codes + pair records, cp.async; 8 threads per pair row) into a ring of nst stages,
-// warp 24 (one lane) issues
-// the MMAs of tile qi into one of two TMEM accumulators (64 columns), and warps 0-15 run the
-// epilogue of tile qi - 1 meanwhile.  Hand-offs are mbarriers:
-//   full[s]  (256 producer arrivals) tile's copies landed (after the producer's proxy fence)
+// ------------------------------------------------------------------ the list-major GEMM
+// Warp-specialised pipeline.  Warp 16 (one lane) copies query tile qi -- 32 slots of codes, one
+// contiguous block already in the operand layout, plus their records -- with two bulk copies into
+// stage qi % nst; warp 17 (one lane) issues the MMAs of tile qi into one of two TMEM accumulators
+// (64 columns); warps 0-15 run the epilogue of tile qi - 1 meanwhile.  Hand-offs are mbarriers:
+//   full[s]  (1 arrival + tx bytes)  tile landed in stage s
 //   empty[s] (1 commit + 16 warps)   MMA read B and the epilogue read the records: stage free
 //   accf[a]  (1 commit)              accumulator a holds tile qi's products
 //   acce[a]  (16 warps)              accumulator a read out: free for tile qi + 2
-constexpr int kRbWsEpi = 16, kRbWsProd = 8, kRbWsNT = (kRbWsEpi + kRbWsProd + 1) * 32;   // 800 threads
+constexpr int kRbWsEpi = 16, kRbWsNT = (kRbWsEpi + 2) * 32;   // 576 threads
 __device__ __forceinline__ void mbar_init(uint32_t a, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count));
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t a) {
   asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(a) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_tx(uint32_t a, uint32_t bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}"
+               ::"r"(a), "r"(bytes) : "memory");
+}
 
 template <bool SAMPLE>
-__global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqTc t, int nst) {
+__global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqTc t, int nst,
+                                                            const __grid_constant__ CUtensorMap tmB) {
   extern __shared__ __align__(1024) uint8_t rsm3[];
   const int D = ix.D;
   const int sbo = (D / 16) * 128;
+  const int nkb = (D + 127) / 128;                                // 128-byte K blocks
+  const int bst = nkb * kRbN * 128;                               // bytes per B stage
   uint8_t* sA = rsm3;                                             // [128 x D] bytes
-  uint8_t* sB = sA + kRbM * D;                                    // [nst][kRbN x D] bytes
-  RbqPair* pi = reinterpret_cast<RbqPair*>(sB + (size_t)nst * kRbN * D);   // [nst][kRbN]
+  uint8_t* sB = sA + kRbM * D;                                    // [nst][nkb][32 x 128 B] swizzled
+  RbqPair* pi = reinterpret_cast<RbqPair*>(sB + (size_t)nst * bst);   // [nst][kRbN]
   float* o_r = reinterpret_cast<float*>(pi + nst * kRbN);         // [128] r_o
   float* o_g = o_r + kRbM;                                        // [128] 1 / g_o
   float* o_pc = o_g + kRbM;                                       // [128] popcount (float)
@@ -454,16 +375,15 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
 
   const int2 tile = t.tiles[blockIdx.x];
   const int L = tile.x, o0 = tile.y;
-  const int p0 = t.inv_off[L], np = t.inv_off[L + 1] - p0;
+  const int p0 = t.off[L], np = SAMPLE ? t.cnt_s[L] : t.cnt_m[L];
   if (np == 0) return;
   const long long row0 = ix.loff[L] + o0;
   const int nobj = min(kRbM, (int)(ix.loff[L + 1] - row0));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nkc = D / 16;
   const int ntile = (np + kRbN - 1) / kRbN;
   if (threadIdx.x == 0) {
     for (int i = 0; i < nst; ++i) {
-      mbar_init(full0 + 8u * i, kRbWsProd * 32);
+      mbar_init(full0 + 8u * i, 1);
       mbar_init(empty0 + 8u * i, 1 + kRbWsEpi);
     }
     for (int a = 0; a < 2; ++a) {
@@ -506,36 +426,24 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
 
-  if (warp >= kRbWsEpi && warp < kRbWsEpi + kRbWsProd) {
-    // ---- producer: 256 threads copy query tile qi into stage qi % nst; thread = (pair row sr,
-    // 16-byte column kc0 + 8 m) of the tile
-    const int pt = threadIdx.x - kRbWsEpi * 32;
-    const int sr = pt >> 3, kc0 = pt & 7;
-    constexpr int kRec = (int)sizeof(RbqPair) / 16;
-    for (int qi = 0; qi < ntile; ++qi) {
-      const int st = qi % nst;
-      if (qi >= nst) mbar_wait(empty0 + 8u * st, (unsigned)((qi / nst - 1) & 1));
-      const int qt = qi * kRbN;
-      if (sr < np - qt) {
-        const int p = t.inv[p0 + qt + sr];
-        uint8_t* Brow = sB + (size_t)st * kRbN * D + (sr >> 3) * sbo + (sr & 7) * 16;
-        const uint8_t* src = t.qbar + (size_t)p * D;
-        for (int kc = kc0; kc < nkc; kc += 8) cp_async16(smem_u32(Brow + kc * 128), src + 16 * kc);
-        if (kc0 < kRec)
-          cp_async16(smem_u32(reinterpret_cast<uint8_t*>(pi + st * kRbN + sr) + 16 * kc0),
-                     reinterpret_cast<const uint8_t*>(t.pinfo + p) + 16 * kc0);
-      }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      if (qi > 0) {                                   // tile qi - 1 complete
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(full0 + 8u * ((qi - 1) % nst));
+  if (warp == kRbWsEpi) {
+    // ---- producer: one lane; per query tile nkb TMA copies (32 rows x 128 B each) + one bulk
+    // copy of the 32 records
+    if (lane == 0) {
+      const uint32_t rb = (uint32_t)(kRbN * sizeof(RbqPair));
+      for (int qi = 0; qi < ntile; ++qi) {
+        const int st = qi % nst;
+        if (qi >= nst) mbar_wait(empty0 + 8u * st, (unsigned)((qi / nst - 1) & 1));
+        const uint32_t fb = full0 + 8u * st;
+        mbar_arrive_tx(fb, (uint32_t)bst + rb);
+        const int slot = p0 + qi * kRbN;
+        const uint32_t dB = smem_u32(sB + (size_t)st * bst);
+        for (int kb = 0; kb < nkb; ++kb) tma_2d_g2s(dB + kb * kRbN * 128, &tmB, 128 * kb, slot, fb);
+        bulk_g2s(smem_u32(pi + st * kRbN), t.pinfo + slot, rb, fb);
       }
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_arrive(full0 + 8u * ((ntile - 1) % nst));
-  } else if (warp == kRbWsEpi + kRbWsProd) {
+    __syncwarp();
+  } else if (warp == kRbWsEpi + 1) {
     // ---- MMA issuer
     if (lane == 0) {
       for (int qi = 0; qi < ntile; ++qi) {
@@ -543,11 +451,11 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
         mbar_wait(full0 + 8u * st, (unsigned)((qi / nst) & 1));
         if (qi >= 2) mbar_wait(acce0 + 8u * a, (unsigned)((qi / 2 - 1) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t aA = smem_u32(sA), aB = smem_u32(sB + (size_t)st * kRbN * D);
+        const uint32_t aA = smem_u32(sA), aB = smem_u32(sB + (size_t)st * bst);
         const uint32_t acc = tmem + (uint32_t)(a * kRbN);
         for (int k = 0; k < D / 32; ++k) {
-          const uint32_t o = (uint32_t)k * 256u;
-          i8_mma(acc, umma_desc_k(aA + o, (uint32_t)sbo), umma_desc_k(aB + o, (uint32_t)sbo), k ? 1u : 0u);
+          const uint32_t oB = (uint32_t)(k >> 2) * (kRbN * 128u) + (uint32_t)(k & 3) * 32u;
+          i8_mma(acc, umma_desc_k(aA + (uint32_t)k * 256u, (uint32_t)sbo), umma_desc_sw128(aB + oB), k ? 1u : 0u);
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                      ::"r"(accf0 + 8u * a) : "memory");
