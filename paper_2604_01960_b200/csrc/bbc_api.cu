@@ -182,7 +182,7 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1) {
   p.fixed = 64 * 256 + (size_t)3 * (ix->nlist + 1) * 4 + 3 * 256;
   if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) {            // pair codes + inverted index
     p.per_query += (size_t)nprobe * ((size_t)ix->D + sizeof(RbqPair) + 4);   // codes, records, slots
-    p.fixed += (size_t)32 * ix->nlist * ((size_t)ix->D + sizeof(RbqPair)) +   // per-list padding
+    p.fixed += (size_t)kRbN * ix->nlist * ((size_t)ix->D + sizeof(RbqPair)) +   // per-list padding
                (size_t)5 * (ix->nlist + 1) * 4 + 8 * 256;
   }
   return p;
@@ -239,7 +239,7 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, 
   db->cnt = (int*)take((size_t)nqb * world * 4);
   if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) {
     const size_t pairs = (size_t)nqb * nprobe;
-    const size_t slots = pairs + (size_t)32 * ix->nlist;   // each list padded to 32 slots
+    const size_t slots = pairs + (size_t)kRbN * ix->nlist;   // each list padded to kRbN slots
     rb->qbar = (uint8_t*)take(slots * ix->D);
     rb->pinfo = (RbqPair*)take(slots * sizeof(RbqPair));
     rb->islot = (int*)take(pairs * 4);
@@ -471,19 +471,19 @@ void rbq_tc_pass(Shard& s, const Batch& b, cudaStream_t st, bool sample) {
   }
   RbqTc t{s.rb.qbar, s.rb.pinfo, s.rb.off, s.rb.cnt_s, s.rb.cnt_m, ix->rbq_tiles, ix->rbq_pc};
   // TMA map of the query codes: [slots x D] bytes, boxes of 32 rows x 128 B, 128-byte swizzle
-  const long long slots = pairs + 32LL * ix->nlist;
+  const long long slots = pairs + (long long)kRbN * ix->nlist;
   CUtensorMap tm;
   if (!encode_tmap_u8(&tm, s.rb.qbar, (uint64_t)ix->D, (uint64_t)slots, 128, kRbN)) {
     ix->broken = true;                               // reported by the CU check after the stage
     return;
   }
-  // 3 query-tile stages when they fit in shared memory, else 2
+  // 3 query-tile stages of 64 pairs (A lives in tensor memory; shared memory holds B and records)
   const int nkb = (ix->D + 127) / 128;
   auto ws_smem = [&](int nst) {
-    return (size_t)kRbM * ix->D + (size_t)nst * nkb * kRbN * 128 + (size_t)nst * kRbN * sizeof(RbqPair) +
-           3 * kRbM * 4 + (size_t)(2 * nst + 4) * 8 + 16;
+    return (size_t)nst * nkb * kRbN * 128 + (size_t)nst * kRbN * sizeof(RbqPair) + 3 * kRbM * 4 +
+           (size_t)(2 * nst + 4) * 8 + 16;
   };
-  const int nst = ws_smem(3) <= 227 * 1024 ? 3 : 2;
+  const int nst = 3;
   const size_t smw = ws_smem(nst);
   if (sample) {
     set_smem(k_rbq_mma_ws<true>, smw);

@@ -32,7 +32,7 @@
 
 namespace bbc {
 
-constexpr int kRbM = 128, kRbN = 32;
+constexpr int kRbM = 128, kRbN = 64;   // object tile x query tile of one MMA
 
 struct __align__(16) RbqPair {   // per (query, probed list), written by k_rbq_pairs
   float c1, c2, c3, r;
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(256) k_rbq_pairs(Batch b, Dev ix, const int* _
 // Pairs estimated on the tensor cores: queries with a sample (nsamp > 0; otherwise tau = infinity
 // and no estimate is needed) and lists non-empty on this shard.  The sample pass uses the pairs
 // with j < nsamp, the Push pass all of them.  Slots: per list L, [off[L], off[L] + cnt_s[L]) the
-// sample pairs, then the others up to off[L] + cnt_m[L]; off[L] is a multiple of 32.
+// sample pairs, then the others up to off[L] + cnt_m[L]; off[L] is a multiple of kRbN.
 __device__ __forceinline__ bool rbq_pair_sel(const Batch& b, const Dev& ix, long long p, int* L_out,
                                              bool* sample) {
   const int q = (int)(p / b.nprobe), j = (int)(p % b.nprobe);
@@ -168,7 +168,7 @@ __global__ void k_rbq_lfill(Batch b, Dev ix, int* cur_s, int* cur_m, int* islot)
   islot[p] = rbq_pair_sel(b, ix, p, &L, &smp) ? atomicAdd(smp ? &cur_s[L] : &cur_m[L], 1) : -1;
 }
 
-// off[L] = exclusive scan of cnt_m rounded up to 32; cur_s = off, cur_m = off + cnt_s (one CTA)
+// off[L] = exclusive scan of cnt_m rounded up to kRbN; cur_s = off, cur_m = off + cnt_s (one CTA)
 __global__ void __launch_bounds__(1024) k_rbq_lscan(const int* cnt_m, const int* cnt_s, int* off,
                                                     int* cur_s, int* cur_m, int nlist) {
   __shared__ int ws[32];
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(1024) k_rbq_lscan(const int* cnt_m, const int*
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int base = 0; base < nlist; base += 1024) {
     const int i = base + threadIdx.x;
-    const int v = i < nlist ? (cnt_m[i] + 31) & ~31 : 0;
+    const int v = i < nlist ? (cnt_m[i] + kRbN - 1) / kRbN * kRbN : 0;
     int x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -318,6 +318,14 @@ __device__ __forceinline__ void tma_2d_g2s(uint32_t dst, const CUtensorMap* map,
                ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar) : "memory");
 }
 
+// A from tensor memory (lane = object row, 4 K bytes per 32-bit column), B from shared memory
+__device__ __forceinline__ void i8_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n"
+      ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"((uint32_t)kRbqIdesc), "r"(acc));
+}
+
 __device__ __forceinline__ void i8_mma(uint32_t tmem_d, uint64_t a, uint64_t bdesc, uint32_t acc) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
@@ -359,11 +367,9 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
                                                             const __grid_constant__ CUtensorMap tmB) {
   extern __shared__ __align__(1024) uint8_t rsm3[];
   const int D = ix.D;
-  const int sbo = (D / 16) * 128;
   const int nkb = (D + 127) / 128;                                // 128-byte K blocks
   const int bst = nkb * kRbN * 128;                               // bytes per B stage
-  uint8_t* sA = rsm3;                                             // [128 x D] bytes
-  uint8_t* sB = sA + kRbM * D;                                    // [nst][nkb][32 x 128 B] swizzled
+  uint8_t* sB = rsm3;                                             // [nst][nkb][32 x 128 B] swizzled
   RbqPair* pi = reinterpret_cast<RbqPair*>(sB + (size_t)nst * bst);   // [nst][kRbN]
   float* o_r = reinterpret_cast<float*>(pi + nst * kRbN);         // [128] r_o
   float* o_g = o_r + kRbM;                                        // [128] 1 / g_o
@@ -392,25 +398,45 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 0) {
+  const uint32_t rbytes = (uint32_t)(kRbN * sizeof(RbqPair));
+  // copies of query tile qi into stage qi % nst (the first nst are issued before A is staged)
+  auto load_tile = [&](int qi) {
+    const int st = qi % nst;
+    const uint32_t fb = full0 + 8u * st;
+    mbar_arrive_tx(fb, (uint32_t)bst + rbytes);
+    const int slot = p0 + qi * kRbN;
+    const uint32_t dB = smem_u32(sB + (size_t)st * bst);
+    for (int kb = 0; kb < nkb; ++kb) tma_2d_g2s(dB + kb * kRbN * 128, &tmB, 128 * kb, slot, fb);
+    bulk_g2s(smem_u32(pi + st * kRbN), t.pinfo + slot, rbytes, fb);
+  };
+  if (threadIdx.x == 0)
+    for (int qi = 0; qi < min(nst, ntile); ++qi) load_tile(qi);
+  __syncwarp();
+  if (warp == 0) {                                    // all 512 columns: 2 accumulators + A
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                 ::"r"(smem_u32(tslot)), "r"(2 * kRbN));
+                 ::"r"(smem_u32(tslot)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  // A: code bits of the tile's objects -> bytes 0/1 in the K-major core-matrix layout
-  const int W = D / 32;
-  for (int idx = threadIdx.x; idx < kRbM * W; idx += kRbWsNT) {
-    const int r = idx / W, wv = idx % W;
-    uint32_t x = 0;
-    if (r < nobj) x = reinterpret_cast<const uint32_t*>(ix.bits + (size_t)(row0 + r) * (D / 8))[wv];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const uint32_t s16 = (x >> (16 * h)) & 0xFFFFu;
-      const uint4 v = make_uint4(nib_bytes(s16 & 15u), nib_bytes((s16 >> 4) & 15u),
-                                 nib_bytes((s16 >> 8) & 15u), nib_bytes(s16 >> 12));
-      const int kc = 2 * wv + h;
-      *reinterpret_cast<uint4*>(sA + (r >> 3) * sbo + kc * 128 + (r & 7) * 16) = v;
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+  const uint32_t tA = tmem + 2 * kRbN;                // A: columns [2 kRbN, 2 kRbN + D/4)
+  // A: code bits of the tile's objects -> bytes 0/1 in tensor memory (lane = row); warp w of
+  // 0-15 writes lanes 32 (w & 3) .. +31, 32-bit code words g = (w >> 2) + 4 i, 8 columns each
+  if (warp < kRbWsEpi) {
+    const int rq = warp & 3, r = 32 * rq + lane;
+    const uint32_t* brow = reinterpret_cast<const uint32_t*>(ix.bits + (size_t)(row0 + min(r, nobj - 1)) * (D / 8));
+    for (int g = warp >> 2; g < D / 32; g += 4) {
+      const uint32_t x = r < nobj ? brow[g] : 0u;
+      const uint32_t taddr = tA + ((uint32_t)(32 * rq) << 16) + (uint32_t)(8 * g);
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                   ::"r"(taddr), "r"(nib_bytes(x & 15u)), "r"(nib_bytes((x >> 4) & 15u)),
+                     "r"(nib_bytes((x >> 8) & 15u)), "r"(nib_bytes((x >> 12) & 15u)),
+                     "r"(nib_bytes((x >> 16) & 15u)), "r"(nib_bytes((x >> 20) & 15u)),
+                     "r"(nib_bytes((x >> 24) & 15u)), "r"(nib_bytes(x >> 28)) : "memory");
     }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   }
   for (int r = threadIdx.x; r < kRbM; r += kRbWsNT) {
     float fr = 0.f, fg = 1.f, fp = 0.f;
@@ -420,26 +446,17 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
     }
     o_r[r] = fr; o_g[r] = fg; o_pc[r] = fp;
   }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");     // A (STS) -> MMA reads
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = *tslot;
 
   if (warp == kRbWsEpi) {
     // ---- producer: one lane; per query tile nkb TMA copies (32 rows x 128 B each) + one bulk
     // copy of the 32 records
     if (lane == 0) {
-      const uint32_t rb = (uint32_t)(kRbN * sizeof(RbqPair));
-      for (int qi = 0; qi < ntile; ++qi) {
-        const int st = qi % nst;
-        if (qi >= nst) mbar_wait(empty0 + 8u * st, (unsigned)((qi / nst - 1) & 1));
-        const uint32_t fb = full0 + 8u * st;
-        mbar_arrive_tx(fb, (uint32_t)bst + rb);
-        const int slot = p0 + qi * kRbN;
-        const uint32_t dB = smem_u32(sB + (size_t)st * bst);
-        for (int kb = 0; kb < nkb; ++kb) tma_2d_g2s(dB + kb * kRbN * 128, &tmB, 128 * kb, slot, fb);
-        bulk_g2s(smem_u32(pi + st * kRbN), t.pinfo + slot, rb, fb);
+      for (int qi = nst; qi < ntile; ++qi) {
+        mbar_wait(empty0 + 8u * (qi % nst), (unsigned)((qi / nst - 1) & 1));
+        load_tile(qi);
       }
     }
     __syncwarp();
@@ -451,11 +468,11 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
         mbar_wait(full0 + 8u * st, (unsigned)((qi / nst) & 1));
         if (qi >= 2) mbar_wait(acce0 + 8u * a, (unsigned)((qi / 2 - 1) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t aA = smem_u32(sA), aB = smem_u32(sB + (size_t)st * bst);
+        const uint64_t d0 = umma_desc_sw128(smem_u32(sB + (size_t)st * bst));
         const uint32_t acc = tmem + (uint32_t)(a * kRbN);
-        for (int k = 0; k < D / 32; ++k) {
-          const uint32_t oB = (uint32_t)(k >> 2) * (kRbN * 128u) + (uint32_t)(k & 3) * 32u;
-          i8_mma(acc, umma_desc_k(aA + (uint32_t)k * 256u, (uint32_t)sbo), umma_desc_sw128(aB + oB), k ? 1u : 0u);
+        for (int k = 0; k < D / 32; ++k) {             // B start address advanced in 16-byte units
+          const uint32_t oB = (uint32_t)(k >> 2) * (kRbN * 128u / 16u) + (uint32_t)(k & 3) * 2u;
+          i8_mma_ts(acc, tA + (uint32_t)(8 * k), d0 + oB, k ? 1u : 0u);
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                      ::"r"(accf0 + 8u * a) : "memory");
@@ -465,7 +482,8 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
     }
     __syncwarp();
   } else {
-    // ---- epilogue: warps 0-15, thread = object row r, 8 pairs per warp
+    // ---- epilogue: warps 0-15, thread = object row r, kPW pairs per warp
+    constexpr int kPW = kRbN / 4;
     const int rq = warp & 3, cg = warp >> 2;
     const int r = 32 * rq + lane;
     float ro = 0.f, ginv = 0.f, pcf = 0.f;
@@ -477,12 +495,15 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
       mbar_wait(accf0 + 8u * a, (unsigned)((qi / 2) & 1));
       mbar_wait(full0 + 8u * st, (unsigned)((qi / nst) & 1));   // records visible (landed long ago)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      uint32_t v[8];
-      const uint32_t taddr = tmem + ((uint32_t)(32 * rq) << 16) + (uint32_t)(a * kRbN + 8 * cg);
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                   : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
-                     "=r"(v[6]), "=r"(v[7])
-                   : "r"(taddr));
+      uint32_t v[kPW];
+#pragma unroll
+      for (int h = 0; h < kPW / 8; ++h) {
+        const uint32_t taddr = tmem + ((uint32_t)(32 * rq) << 16) + (uint32_t)(a * kRbN + kPW * cg + 8 * h);
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(v[8 * h + 0]), "=r"(v[8 * h + 1]), "=r"(v[8 * h + 2]), "=r"(v[8 * h + 3]),
+                       "=r"(v[8 * h + 4]), "=r"(v[8 * h + 5]), "=r"(v[8 * h + 6]), "=r"(v[8 * h + 7])
+                     : "r"(taddr));
+      }
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -490,8 +511,8 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
       const RbqPair* P = pi + st * kRbN;
       if (r < nobj) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const int sp = 8 * cg + c;
+        for (int c = 0; c < kPW; ++c) {
+          const int sp = kPW * cg + c;
           if (sp >= nqt) continue;
           const RbqPair& e = P[sp];
           const long long at = e.obase + o0 + r;
@@ -526,7 +547,7 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
   __syncthreads();
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kRbN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
 }
 
