@@ -483,7 +483,7 @@ void rbq_tc_pass(Shard& s, const Batch& b, cudaStream_t st, bool sample) {
     return (size_t)nst * nkb * kRbN * 128 + (size_t)nst * kRbN * sizeof(RbqPair) + 3 * kRbM * 4 +
            (size_t)(2 * nst + 4) * 8 + 16;
   };
-  const int nst = 3;
+  const int nst = 2;
   const size_t smw = ws_smem(nst);
   if (sample) {
     set_smem(k_rbq_mma_ws<true>, smw);

@@ -19,8 +19,8 @@
 //                   for each tile of 32 pairs: B (32 x D bytes, TMA tensor copies with 128-byte
 //                   swizzle, one per 128-byte K block) + records (bulk copy) into a ring of
 //                   stages (mbarrier complete_tx), D/32 MMAs
-//                   (M=128, N=32, K=32) into one of two TMEM accumulators, epilogue by 16
-//                   warps: estimate (sample pass) or bucket id (Push).
+//                   (M=128, N=96, K=32, A in tensor memory) into one of two TMEM accumulators,
+//                   epilogue by 24 warps: estimate (sample pass) or bucket id (Push).
 //   k_cell_hist   : Push histogram per query from its bucket ids (query-major, shared-memory
 //                   counts, one global flush per CTA: list-major partial histograms would need
 //                   a global atomic per (pair, bucket)).
@@ -32,7 +32,7 @@
 
 namespace bbc {
 
-constexpr int kRbM = 128, kRbN = 64;   // object tile x query tile of one MMA
+constexpr int kRbM = 128, kRbN = 96;   // object tile x query tile of one MMA
 
 struct __align__(16) RbqPair {   // per (query, probed list), written by k_rbq_pairs
   float c1, c2, c3, r;
@@ -342,15 +342,19 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 }
 
 // ------------------------------------------------------------------ the list-major GEMM
-// Warp-specialised pipeline.  Warp 16 (one lane) copies query tile qi -- 32 slots of codes, one
-// contiguous block already in the operand layout, plus their records -- with two bulk copies into
-// stage qi % nst; warp 17 (one lane) issues the MMAs of tile qi into one of two TMEM accumulators
-// (64 columns); warps 0-15 run the epilogue of tile qi - 1 meanwhile.  Hand-offs are mbarriers:
-//   full[s]  (1 arrival + tx bytes)  tile landed in stage s
-//   empty[s] (1 commit + 16 warps)   MMA read B and the epilogue read the records: stage free
-//   accf[a]  (1 commit)              accumulator a holds tile qi's products
-//   acce[a]  (16 warps)              accumulator a read out: free for tile qi + 2
-constexpr int kRbWsEpi = 16, kRbWsNT = (kRbWsEpi + 2) * 32;   // 576 threads
+// Warp-specialised pipeline.  Warp 24 (one lane) copies query tile qi -- kRbN slots of codes,
+// row-major in global memory, by TMA into 128-byte-swizzled K blocks, plus their records by a bulk
+// copy -- into stage qi % nst; warp 25 (one lane) issues the MMAs of tile qi (A in tensor memory)
+// into one of two TMEM accumulators; warps 0-23 run the epilogue of tile qi - 1 meanwhile (warp w
+// reads TMEM lanes 32 (w & 3) .. +31 and pairs kPW (w >> 2) .. +kPW-1).  Measured: an MMA with
+// N <= 64 costs ~51-57 cycles whatever N (tools/mma_microbench.cu), and the epilogue -- not the
+// MMAs -- set the pace at N = 64 with 16 warps; N = 96 with 24 epilogue warps is faster.
+// Hand-offs are mbarriers:
+//   full[s]  (1 arrival + tx bytes)     tile landed in stage s
+//   empty[s] (1 commit + 24 warps)      MMA read B and the epilogue read the records: stage free
+//   accf[a]  (1 commit)                 accumulator a holds tile qi's products
+//   acce[a]  (24 warps)                 accumulator a read out: free for tile qi + 2
+constexpr int kRbWsEpi = 24, kRbWsNT = (kRbWsEpi + 2) * 32;   // 832 threads
 __device__ __forceinline__ void mbar_init(uint32_t a, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count));
 }
@@ -427,7 +431,7 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
   if (warp < kRbWsEpi) {
     const int rq = warp & 3, r = 32 * rq + lane;
     const uint32_t* brow = reinterpret_cast<const uint32_t*>(ix.bits + (size_t)(row0 + min(r, nobj - 1)) * (D / 8));
-    for (int g = warp >> 2; g < D / 32; g += 4) {
+    for (int g = warp >> 2; g < D / 32; g += kRbWsEpi / 4) {
       const uint32_t x = r < nobj ? brow[g] : 0u;
       const uint32_t taddr = tA + ((uint32_t)(32 * rq) << 16) + (uint32_t)(8 * g);
       asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
@@ -482,8 +486,8 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
     }
     __syncwarp();
   } else {
-    // ---- epilogue: warps 0-15, thread = object row r, kPW pairs per warp
-    constexpr int kPW = kRbN / 4;
+    // ---- epilogue: warps 0-23, thread = object row r, kPW pairs per warp
+    constexpr int kPW = kRbN * 4 / kRbWsEpi;          // pairs per warp
     const int rq = warp & 3, cg = warp >> 2;
     const int r = 32 * rq + lane;
     float ro = 0.f, ginv = 0.f, pcf = 0.f;
