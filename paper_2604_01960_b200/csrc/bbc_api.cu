@@ -573,7 +573,7 @@ void stage_compact(Shard& s, cudaStream_t st) {
   } else if (rowb <= 1024) {                                    \
     X(false, 8, 8, 1, 3);                                       \
   } else {                                                      \
-    X(false, 32, 8, 1, 2);                                      \
+    X(false, 32, 8, 1, 3);                                      \
   }
 
 template <bool IP>
@@ -767,7 +767,7 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
   // (of >= 256 queries) so that most of the copy time is hidden.
   const bool pipe = host && !dist && !dbg;
   if (pipe) {
-    nqb = std::min<long long>(nqb, std::max<long long>(256, (nq + 3) / 4));
+    nqb = std::min<long long>(nqb, std::max<long long>(256, (nq + 1) / 2));
     if (!ix->copy_stream) {
       CU(cudaStreamCreateWithFlags(&ix->copy_stream, cudaStreamNonBlocking));
       for (int i = 0; i < 2; ++i) {
@@ -790,8 +790,14 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
     s.dv.probe_tc = s.ix->probe_tc_ok &&
                     (pm == BBC_PROBE_TENSOR || (pm == BBC_PROBE_AUTO && 32LL * nprobe <= s.ix->nlist));
   }
-  for (long long q0 = 0; q0 < nq; q0 += nqb) {
-    const int nb = (int)std::min<long long>(nqb, nq - q0);
+  // host path: the tail of the batch is cut into halving micro-batches (down to nqb / 8) so that
+  // the one device->host copy left exposed, the last micro-batch's, is small
+  const long long min_nb = std::max<long long>(32, nqb / 8);
+  int nb = 0;
+  for (long long q0 = 0; q0 < nq; q0 += nb) {
+    const long long rem = nq - q0;
+    nb = (int)(pipe ? std::min<long long>(nqb, std::max<long long>(std::min(rem, min_nb), (rem + 1) / 2))
+                    : std::min<long long>(nqb, rem));
     for (auto& s : sh) {
       carve(s.ix, s.p, nb, nprobe, s.ws, s.b, &s.qstage, &s.oids, &s.od2, k, &s.db, W, &s.rb);
       Batch& b = s.b;
