@@ -32,7 +32,7 @@ def cache_dir() -> str:
 
 
 _BUILD_FIELDS = ("gen", "N", "d", "raw_dtype", "kind", "nlist", "M", "seed", "kmeans_iters",
-                 "kmeans_train_per_list", "pq_train", "pq_iters", "metric")
+                 "kmeans_train_per_list", "pq_train", "pq_iters", "metric", "pq_bits")
 
 
 def index_path(cfg: Config) -> str:

@@ -145,16 +145,17 @@ def build(cfg: Config, X: np.ndarray | None = None, verbose: bool = False) -> di
         M, ds = cfg.M, cfg.dsub
         trq = np.sort(gq.choice(N, size=min(N, cfg.pq_train), replace=False))
         Tq = X[trq].astype(np.float32)
-        books = np.empty((M, 256, ds), dtype=np.float32)
+        ksub = 1 << cfg.pq_bits
+        books = np.empty((M, ksub, ds), dtype=np.float32)
         for m in range(M):
-            books[m] = kmeans(Tq[:, m * ds:(m + 1) * ds], 256, cfg.pq_iters, gq, len(Tq))
+            books[m] = kmeans(Tq[:, m * ds:(m + 1) * ds], ksub, cfg.pq_iters, gq, len(Tq))
         codes = np.empty((N, M), dtype=np.uint8)
         raw = out["raw"]
         for lo in range(0, N, 1 << 18):
             blk = raw[lo:lo + (1 << 18)].astype(np.float32)
             for m in range(M):
                 codes[lo:lo + len(blk), m] = _assign(blk[:, m * ds:(m + 1) * ds], books[m])
-        out.update(M=M, nbits=8, codebooks=books, codes=codes)
+        out.update(M=M, nbits=cfg.pq_bits, codebooks=books, codes=codes)
     else:
         D = ((d + 63) // 64) * 64
         G = gq.standard_normal((D, D))

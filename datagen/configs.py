@@ -39,6 +39,7 @@ class Config:
     pq_train: int = 65536
     pq_iters: int = 12
     metric: str = "l2"   # "l2" (squared L2) or "ip" (inner product, keys -<q,x>)
+    pq_bits: int = 8     # bits per PQ sub-quantizer code: 8 (256 centroids) or 4 (16)
     extra: dict = field(default_factory=dict, compare=False, hash=False)
 
     @property
@@ -90,7 +91,15 @@ IP = {
     "C4ip_s": SMALL["C4s"].replace(name="C4ip_s", metric="ip"),
 }
 
-ALL = {**FULL, **SMALL, **IP}
+# 4-bit PQ, the paper's PQ setting ("M = d/4 ... 4 bits per
+# sub-vector, B = d"): C2's data with M = 32 sub-quantizers of 16 centroids (dsub 4), estimated
+# with the FastScan-style 8-bit quantised lookup table (reading R20).
+PQ4 = {
+    "C2q4": C2.replace(name="C2q4", pq_bits=4),
+    "C2q4s": SMALL["C2s"].replace(name="C2q4s", pq_bits=4),
+}
+
+ALL = {**FULL, **SMALL, **IP, **PQ4}
 
 
 def get(name: str) -> Config:

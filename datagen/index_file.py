@@ -12,8 +12,8 @@ Layout (little-endian; DESIGN.md section 4 is the normative copy, `include/bbc.h
       0 centroids    f32 [nlist x d]
       1 list_offsets i64 [nlist + 1]          (list L = rows [off[L], off[L+1]) of the list-ordered arrays)
       2 ids          i64 [N]                  (original id of each list-ordered row)
-      3 codebooks    f32 [M x 256 x d/M]      (PQ only)
-      4 codes        u8  [N x M]              (PQ only, list order)
+      3 codebooks    f32 [M x 2^nbits x d/M]  (PQ only; nbits 8 or 4)
+      4 codes        u8  [N x M]              (PQ only, list order; one code per byte)
       5 P            f32 [D x D]              (RaBitQ only; y = P^T o)
       6 wL           f32 [nlist x D]          (RaBitQ only; w_L = P^T c_L, c_L zero-padded to D)
       7 bits         u8  [N x D/8]            (RaBitQ only; bit i of row in byte i/8, LSB first)
@@ -100,7 +100,7 @@ def read(path: str, mmap: bool = True) -> dict:
     N, d, nlist, M, nbits, D, seed = (int(x) for x in hdr[3:10])
     shapes = {
         "centroids": ((nlist, d), np.float32), "list_offsets": ((nlist + 1,), np.int64),
-        "ids": ((N,), np.int64), "codebooks": ((M, 256, d // M if M else 0), np.float32),
+        "ids": ((N,), np.int64), "codebooks": ((M, 1 << nbits if kind == "pq" else 256, d // M if M else 0), np.float32),
         "codes": ((N, M), np.uint8), "P": ((D, D), np.float32), "wL": ((nlist, D), np.float32),
         "bits": ((N, D // 8), np.uint8), "factors": ((N, 2), np.float32),
         "raw": ((N, d), np.uint8 if raw_dtype == "u8" else np.float32),

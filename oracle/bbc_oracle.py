@@ -14,7 +14,9 @@ What it computes (steps O1-O9; "P:Lnnn" = line of PAPER.md)
                        between the query and the codebook vectors")
                        RaBitQ: u = P^T q, per probed list the 4-bit query code (B_q = 4)
   O3 estimate          PQ: est = sum_m LUT[m][code_m] ("use these pre-computed distances to
-                       efficiently estimate"); RaBitQ: unbiased inner-product estimator
+                       efficiently estimate"); 4-bit PQ: the FastScan estimate from the
+                       8-bit quantised LUT (P:L1440, P:L1798; reading R20);
+                       RaBitQ: unbiased inner-product estimator
   O4 sample            codebook generation from the nearest clusters
   O5 edges             d_min = smallest, d_max = budget-th smallest estimate of the sample
                        ("partial sort ... derive d_min and d_max from the local top-k", P:L898)
@@ -109,6 +111,43 @@ def pq_est(lut: np.ndarray, codes: np.ndarray) -> np.ndarray:
     for m in range(1, lut.shape[0]):
         acc = acc + lut[m][codes[:, m]]
     return acc
+
+
+def pq4_fastscan_lut(lut: np.ndarray):
+    """The 8-bit quantised lookup table of 4-bit PQ (FastScan, P:L1798 with the paper's 4-bit PQ
+    setting P:L1440; reading R20), from the fp32 LUT [M x 16] of pq_lut:
+        lo_m  = min_c LUT[m][c]
+        span  = max_m (max_c LUT[m][c] - lo_m)            (fp32 subtraction)
+        delta = span / 255                                  (fp32 division)
+        Q[m][c] = min(255, floor((LUT[m][c] - lo_m) / delta + 0.5))   (0 when delta = 0)
+        bias  = lo_0 + lo_1 + ... + lo_{M-1}                (fp32, left to right)
+    Returns (Q uint8 [M x 16], delta fp32, bias fp32)."""
+    lut = np.asarray(lut, dtype=F32)
+    lo = lut.min(axis=1)
+    span = F32(0.0)
+    for m in range(lut.shape[0]):
+        span = max(span, F32(lut[m].max() - lo[m]))
+    delta = F32(span / F32(255.0))
+    if delta > 0:
+        t = ((lut - lo[:, None]) / delta).astype(F32)
+        qt = np.minimum(F32(255.0), np.floor((t + F32(0.5)).astype(F32))).astype(np.uint8)
+    else:
+        qt = np.zeros(lut.shape, dtype=np.uint8)
+    bias = F32(0.0)
+    for m in range(lut.shape[0]):
+        bias = F32(bias + lo[m])
+    return qt, delta, bias
+
+
+def pq4_est(qlut: np.ndarray, delta: F32, bias: F32, codes: np.ndarray) -> np.ndarray:
+    """est = delta * S + bias (fp32, multiply then add) with S = sum_m Q[m][code_m], an exact
+    integer (<= 255 M): the FastScan estimate of the PQ distance, within M * delta / 2 of the
+    fp32 LUT sum up to rounding."""
+    codes = np.asarray(codes)
+    S = np.zeros(len(codes), dtype=np.int64)
+    for m in range(qlut.shape[0]):
+        S += qlut[m][codes[:, m]]
+    return (F32(delta) * S.astype(F32)).astype(F32) + F32(bias)
 
 
 # ----------------------------------------------------------------------------------------------
@@ -282,7 +321,10 @@ def search(ix: dict, Q: np.ndarray, k: int, nprobe: int, budget: int, want_debug
         lists = pr[i]
         sizes = off[lists + 1] - off[lists]
         pos = np.concatenate([np.arange(off[L], off[L + 1]) for L in lists])  # probe order
-        if ix["kind"] == "pq":
+        if ix["kind"] == "pq" and ix.get("nbits", 8) == 4:
+            qlut, delta, bias = pq4_fastscan_lut(pq_lut(Q[i], ix["codebooks"], metric))
+            est = pq4_est(qlut, delta, bias, np.asarray(ix["codes"][pos]))
+        elif ix["kind"] == "pq":
             lut = pq_lut(Q[i], ix["codebooks"], metric)
             est = pq_est(lut, np.asarray(ix["codes"][pos]))
         else:

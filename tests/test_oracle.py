@@ -447,3 +447,67 @@ def test_bucket_count_closed_forms(c1t):
     assert all(a >= b - 2 for a, b in zip(sizes_S[:-2], sizes_S[1:-1]))   # doubling B: nested up to rounding
     with pytest.raises(ValueError):
         O.cells(est, dmin, dmax, 0)
+
+
+# ---------------------------------------------------------------------------------------------
+# 4-bit PQ ("M = d/4 ... 4 bits per sub-vector"; FastScan P:L1798):
+# the 8-bit quantised lookup table and its estimate (reading R20)
+# ---------------------------------------------------------------------------------------------
+def test_pq4_lut_hand_example():
+    """A 2 x 16 LUT worked by hand: row 0 spans [1, 3.55] (span 2.55, the largest), row 1 is
+    [10, 10.51].  delta = 2.55 / 255 = 0.01; row 0 maps 1 + 0.01 c' to c', row 1's 10.51 to 51."""
+    lut = np.full((2, 16), 0.0, dtype=np.float32)
+    lut[0] = np.float32(1.0) + np.float32(0.17) * np.arange(16, dtype=np.float32)   # 1 .. 3.55
+    lut[1] = np.float32(10.0)
+    lut[1][7] = np.float32(10.51)
+    Q, delta, bias = O.pq4_fastscan_lut(lut)
+    assert abs(float(delta) - 0.01) < 1e-8
+    assert abs(float(bias) - 11.0) < 1e-6
+    assert list(Q[0]) == [17 * c for c in range(16)]      # 0.17 c / 0.01 = 17 c
+    assert Q[1][7] == 51 and Q[1].sum() == 51
+    est = O.pq4_est(Q, delta, bias, np.array([[15, 7], [0, 0]]))
+    assert abs(float(est[0]) - (3.55 + 10.51)) < 1e-5 and abs(float(est[1]) - 11.0) < 1e-6
+
+
+def test_pq4_lut_invariants_and_error_bound(rng):
+    """Row minima map to 0, the widest row's maximum to 255, every entry dequantises to within
+    delta/2 of the fp32 LUT, and the estimate is within M*delta/2 (+ rounding) of pq_est."""
+    for trial in range(20):
+        M = int(rng.integers(1, 40))
+        lut = (rng.random((M, 16)) * rng.random() * 50 + rng.normal() * 10).astype(np.float32)
+        Q, delta, bias = O.pq4_fastscan_lut(lut)
+        lo = lut.min(axis=1)
+        assert np.all(Q.min(axis=1) == 0)
+        assert Q.max() == 255
+        deq = lo[:, None].astype(np.float64) + float(delta) * Q.astype(np.float64)
+        assert np.all(np.abs(deq - lut) <= float(delta) * 0.5 * (1 + 1e-5) + 1e-6)
+        codes = rng.integers(0, 16, (500, M))
+        e4 = O.pq4_est(Q, delta, bias, codes).astype(np.float64)
+        e = O.pq_est(lut, codes).astype(np.float64)
+        tol = M * float(delta) * 0.5 * (1 + 1e-5) + 1e-5 * (np.abs(e) + M * np.abs(lut).max())
+        assert np.all(np.abs(e4 - e) <= tol)
+
+
+def test_pq4_degenerate_lut():
+    """All entries of every row equal: delta = 0, codes 0, the estimate is the bias exactly."""
+    lut = np.tile(np.arange(5, dtype=np.float32)[:, None], (1, 16))
+    Q, delta, bias = O.pq4_fastscan_lut(lut)
+    assert delta == 0 and not Q.any() and bias == np.float32(10.0)
+    assert np.all(O.pq4_est(Q, delta, bias, np.zeros((3, 5), dtype=int)) == np.float32(10.0))
+
+
+def test_pq4_full_probe_is_brute_force(rng):
+    """A tiny 4-bit PQ index from the builder: every list probed and budget >= N give the
+    brute-force top-k (the estimate only decides buckets; re-rank distances are exact)."""
+    from datagen import build_index, configs, synth
+    cfg = configs.get("C2q4s").replace(name="tiny_q4", N=800, nlist=8, nq=3, k=25, nprobe=8,
+                                      budget=800, kmeans_iters=3, pq_train=800, pq_iters=3)
+    X = synth.generate_data(cfg)
+    ix = build_index.build(cfg, X=X)
+    assert ix["nbits"] == 4 and ix["codebooks"].shape == (cfg.M, 16, cfg.d // cfg.M)
+    assert int(np.asarray(ix["codes"]).max()) <= 15
+    Q = synth.generate_queries(cfg)
+    for k in (1, 25):
+        ids, d2 = O.search(ix, Q, k, cfg.nlist, cfg.N)
+        gi, gd = BF.ground_truth(Q, X, k)
+        assert np.array_equal(ids, gi)
