@@ -37,7 +37,8 @@ from datagen import configs, groundtruth, index_file, synth  # noqa: E402
 
 # Operating points (nprobe, budget) per workload where GPU recall@k >= 0.95 on the first 100
 # queries (sweep: `python bench.py --sweep`).  None = use the config point.
-RECALL95 = {"C2": (768, 20000), "C3": (2048, 20000), "C4": (1024, 75000), "C5": (1024, 30000), "C4ip": (1024, 75000)}
+RECALL95 = {"C2": (768, 20000), "C3": (2048, 20000), "C4": (1024, 75000), "C5": (1024, 30000), "C4ip": (1024, 75000),
+            "C2q4": (1024, 60000)}
 METRIC = "queries/sec at recall@k=0.95 (k=5k\u201350k); scan+rerank HBM GB/s vs peak"
 
 
@@ -381,6 +382,24 @@ def main():
             hv = v["hbm_view"]
             hv["GBs"] = hv["code_bytes"] / (v["ms"] / 1e3) / 1e9
             hv["frac"] = hv["GBs"] / peak
+    if info.kind == 1 and getattr(info, "nbits", 8) == 4:
+        # 4-bit PQ scan: lookups by byte permutes on the integer ALU pipe (64 lanes/clk/SM);
+        # the kernel spends 16 ALU operations per 8 lookups (bbc_pq4.cuh), so the pipe's lookup
+        # peak is 148 x 64 / 2 per clock at the measured max SM clock
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                mhz = float(json.load(f)["sm_max_mhz"])
+        except Exception:
+            mhz = 1965.0
+        lk = main_objs * info.m
+        pk = 148 * 32 * mhz * 1e6 / 1e9                      # G lookups / s
+        per["scan"] = {"ms": scan_ms, "bound": "alu", "unit": "Glookup/s",
+                       "pipe": "integer ALU: PRMT/LOP3/SHF, 16 ops per 8 lookups",
+                       "lookups": lk, "peak_Glookups": pk,
+                       "Glookups": lk / (scan_ms / 1e3) / 1e9 if scan_ms > 0 else None,
+                       "hbm_view": {"code_bytes": main_objs * info.m / 2, "peak_GBs": peak}}
+        per["scan"]["frac"] = per["scan"]["Glookups"] / pk if per["scan"]["Glookups"] else None
+        per["scan"]["GBs"] = None
     if info.kind != 1:
         # RaBitQ scan = list-major integer GEMM on the tensor cores (kind::i8): 2 ops per code bit
         # per (object, query) pair of the Push pass, against the int8 dense peak (measured bf16
@@ -396,15 +415,17 @@ def main():
     dom = max(per, key=lambda n: per[n]["ms"])
     traffic = measured_traffic(cfg.name, nprobe, budget, dom)
     tens = per[dom]["bound"] == "tensor"
+    lkp = "Glookups" in per[dom]
     roof = {"bound": per[dom]["bound"], "kernel": dom,
-            "achieved": per[dom]["TOPs"] if tens else per[dom]["GBs"],
-            "peak": per[dom]["peak_TOPs"] if tens else per[dom]["peak_GBs"],
-            "unit": "TOP/s" if tens else "GB/s", "frac": per[dom]["frac"],
+            "achieved": per[dom]["TOPs"] if tens else per[dom]["Glookups"] if lkp else per[dom]["GBs"],
+            "peak": per[dom]["peak_TOPs"] if tens else per[dom]["peak_Glookups"] if lkp else per[dom]["peak_GBs"],
+            "unit": "TOP/s" if tens else "Glookup/s" if lkp else "GB/s", "frac": per[dom]["frac"],
             "traffic": traffic,
             "peak_source": (peak_src if per[dom]["bound"] == "hbm" else
                             "measured: bbc_measure_l2_read (L2-resident 48 MiB, 16-byte loads)"
                             if per[dom]["bound"] == "l2" else
                             "measured bf16 TFLOP/s x 2 (int8/bf16 nominal ratio)" if tens else
+                            "derived: 148 SMs x 64 ALU lanes/clk / 2 ops per lookup x sm_max_mhz (DESIGN.md 5)" if lkp else
                             "derived: 148 SMs x 128 B/clk L1/shared-memory data pipe x sm_max_mhz (DESIGN.md 5)"),
             "per_kernel": per,
             "stage_ms_per_step": {k_: v / args.steps for k_, v in stage_ms.items()}}
@@ -501,7 +522,7 @@ def sweep(cfg, path, g, rank):
                           6 * cfg.nprobe, 8 * cfg.nprobe}):
         if nprobe > cfg.nlist or nprobe > 2048:
             continue
-        for bm in (1.0, 1.5, 2.0, 3.0, 4.0):
+        for bm in (1.0, 1.5, 2.0, 3.0, 4.0) + ((6.0, 8.0) if cfg.pq_bits == 4 else ()):
             budget = int(bm * cfg.k)
             ws = g.workspace(len(Q), cfg.k, nprobe, budget, max_bytes=60 << 30)
             g.search(q, cfg.k, nprobe, budget, workspace=ws)

@@ -88,6 +88,7 @@ typedef struct {
   int32_t max_list;    /* largest list size                            */
   int32_t rank, world; /* shard of this handle                         */
   int32_t metric;      /* BBC_METRIC_L2 or BBC_METRIC_IP               */
+  int32_t nbits;       /* PQ code bits (8 or 4); 1 for RaBitQ          */
 } bbc_index_info_t;
 
 bbc_status bbc_index_info(bbc_index index, bbc_index_info_t* info);

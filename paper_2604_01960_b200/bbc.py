@@ -40,7 +40,7 @@ class IndexInfo(ctypes.Structure):
                 ("kind", ctypes.c_int32), ("m", ctypes.c_int32), ("dpad", ctypes.c_int32),
                 ("raw_u8", ctypes.c_int32), ("n_local", ctypes.c_int64),
                 ("max_list", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
-                ("metric", ctypes.c_int32)]
+                ("metric", ctypes.c_int32), ("nbits", ctypes.c_int32)]
 
 
 class DebugBufs(ctypes.Structure):

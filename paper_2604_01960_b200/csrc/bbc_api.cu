@@ -15,6 +15,7 @@
 #include "bbc_dist.cuh"
 #include "bbc_probe_tc.cuh"
 #include "bbc_rbq_tc.cuh"
+#include "bbc_pq4.cuh"
 
 using namespace bbc;
 
@@ -39,6 +40,7 @@ struct bbc_index_s {
   int device = 0;
   int rank = 0, world = 1;
   int kind = 0, d = 0, nlist = 0, M = 0, D = 0, raw_u8 = 0, metric = BBC_METRIC_L2;
+  int nbits = 8;                        // PQ code bits: 8 (replicated-LUT scan) or 4 (bbc_pq4.cuh)
   long long N = 0, n_local = 0;
   int max_list = 0;
   std::vector<int> lsize;               // local list sizes
@@ -57,7 +59,8 @@ struct bbc_index_s {
   float* factors = nullptr;
   void* raw = nullptr;
   long long* stats = nullptr;           // [4]
-  uint8_t* codes_t = nullptr;           // PQ codes, per-list chunk-major (replicated-LUT scan)
+  uint8_t* codes_t = nullptr;           // PQ codes, per-list chunk-major (8-bit: replicated-LUT scan;
+                                        // 4-bit: k_pack_codes4 layout)
   long long* tbase = nullptr;           // [nlist] byte offset of each list in codes_t
   float* cmu = nullptr;                 // [d] centroid mean (tensor-core probe)
   float* cnorm = nullptr;               // [nlist] |c - mu|^2
@@ -107,6 +110,7 @@ namespace {
 Dev dev_view(const bbc_index_s* ix) {
   Dev v;
   v.kind = ix->kind; v.d = ix->d; v.nlist = ix->nlist; v.M = ix->M; v.D = ix->D;
+  v.ksub = 1 << ix->nbits;
   v.raw_u8 = ix->raw_u8; v.n_local = ix->n_local; v.metric = ix->metric;
   v.centroids = ix->centroids; v.loff = ix->loff; v.gsize = ix->gsize_d; v.ids = ix->ids;
   v.books = ix->books; v.codes = ix->codes; v.P = ix->P; v.wL = ix->wL; v.bits = ix->bits;
@@ -300,6 +304,37 @@ void rq_scan(int M, bool est, int num_sms, cudaStream_t st, const Batch& b, cons
   }
 }
 
+template <int M>
+void launch_q4(bool est, int grid, cudaStream_t st, const Batch& b, const Dev& dv, const uint8_t* ct,
+               const long long* tb, float* out, long long stride, int mode) {
+  if (est) k_pq4_scan<M, true><<<grid, kQ4NT, 0, st>>>(b, dv, ct, tb, out, stride, mode, b.items, b.nitems);
+  else k_pq4_scan<M, false><<<grid, kQ4NT, 0, st>>>(b, dv, ct, tb, out, stride, mode, b.items, b.nitems);
+}
+
+// One 4-bit PQ scan pass: the same work items, two CTAs of 512 threads per SM.
+void q4_scan(int M, bool est, int num_sms, cudaStream_t st, const Batch& b, const Dev& dv,
+             const uint8_t* ct, const long long* tb, float* out, long long stride, int mode) {
+  if (b.nq <= 0) return;
+  k_scan_plan<<<1, 1024, 0, st>>>(b, mode, b.items, b.nitems);
+  g_launches += 1;
+  const int grid = 2 * num_sms;
+  switch (M) {
+    case 8: launch_q4<8>(est, grid, st, b, dv, ct, tb, out, stride, mode); break;
+    case 16: launch_q4<16>(est, grid, st, b, dv, ct, tb, out, stride, mode); break;
+    case 24: launch_q4<24>(est, grid, st, b, dv, ct, tb, out, stride, mode); break;
+    case 32: launch_q4<32>(est, grid, st, b, dv, ct, tb, out, stride, mode); break;
+    case 48: launch_q4<48>(est, grid, st, b, dv, ct, tb, out, stride, mode); break;
+    case 64: launch_q4<64>(est, grid, st, b, dv, ct, tb, out, stride, mode); break;
+  }
+}
+
+// PQ scan pass of either code width
+void pq_scan(const bbc_index_s* ix, bool est, cudaStream_t st, const Batch& b, const Dev& dv, float* out,
+             long long stride, int mode) {
+  if (ix->nbits == 4) q4_scan(ix->M, est, ix->num_sms, st, b, dv, ix->codes_t, ix->tbase, out, stride, mode);
+  else rq_scan(ix->M, est, ix->num_sms, st, b, dv, ix->codes_t, ix->tbase, out, stride, mode);
+}
+
 bbc_status check_args(bbc_index ix, const void* q, int64_t nq, int32_t k, int32_t nprobe,
                       int64_t budget, const void* oi, const void* od, const void* ws) {
   if (!ix) return fail(BBC_ERR_ARG, "null index");
@@ -452,9 +487,13 @@ void rbq_pairs(Shard& s, const Batch& b, cudaStream_t st) {
 void stage_tables(Shard& s, cudaStream_t st) {
   bbc_index_s* ix = s.ix;
   StageScope sc(ix, st, BBC_STAGE_TABLES);
-  if (ix->kind == BBC_KIND_PQ)
-    k_pq_lut<<<dim3(ix->M, s.b.nq), 256, 0, st>>>(s.b, s.dv);
-  else
+  if (ix->kind == BBC_KIND_PQ) {
+    k_pq_lut<<<dim3(ix->M, s.b.nq), 1 << ix->nbits, 0, st>>>(s.b, s.dv);
+    if (ix->nbits == 4) {
+      k_pq4_qlut<<<s.b.nq, ix->M * 16, 0, st>>>(s.b, s.dv);
+      g_launches += 1;
+    }
+  } else
     k_rbq_rotate<<<dim3((ix->D + 255) / 256, s.b.nq), 256, (size_t)ix->d * 4, st>>>(s.b, s.dv);
   g_launches += 1;
   if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) rbq_pairs(s, s.b, st);
@@ -503,7 +542,7 @@ void stage_sample_est(Shard& s, cudaStream_t st) {
   bbc_index_s* ix = s.ix;
   StageScope sc(ix, st, BBC_STAGE_SAMPLE);
   if (ix->kind == BBC_KIND_PQ) {
-    rq_scan(ix->M, true, ix->num_sms, st, s.b, s.dv, ix->codes_t, ix->tbase, s.b.val, s.p.cap, 0);
+    pq_scan(ix, true, st, s.b, s.dv, s.b.val, s.p.cap, 0);
   } else if (ix->rbq_tc) {
     rbq_tc_pass(s, s.b, st, true);
   } else {
@@ -521,7 +560,7 @@ void stage_scan(Shard& s, cudaStream_t st) {
   const int nb = s.b.nq, nprobe = s.b.nprobe;
   if (ix->kind == BBC_KIND_PQ) {
     k_sample_cells<<<dim3(8, nb), 256, 0, st>>>(s.b);
-    rq_scan(ix->M, false, ix->num_sms, st, s.b, s.dv, ix->codes_t, ix->tbase, nullptr, 0, 1);
+    pq_scan(ix, false, st, s.b, s.dv, nullptr, 0, 1);
     g_launches += 2;
   } else if (ix->rbq_tc) {
     rbq_tc_pass(s, s.b, st, false);
@@ -889,8 +928,7 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
       if (dbg->est) {
         // every estimate in probe order, written to the caller's buffer (debug only)
         if (ix->kind == BBC_KIND_PQ) {
-          rq_scan(ix->M, true, ix->num_sms, st, b, s0.dv, ix->codes_t, ix->tbase, dbg->est,
-                  dbg->est_stride, 2);
+          pq_scan(ix, true, st, b, s0.dv, dbg->est, dbg->est_stride, 2);
         } else {
           Batch b2 = b;
           b2.val = dbg->est;
@@ -1033,9 +1071,9 @@ bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_
     fclose(f);
     return fail(BBC_ERR_FORMAT, "bad header fields");
   }
-  if (kind == BBC_KIND_PQ && (M <= 0 || d % M != 0 || M % 8 != 0 || M > 64 || hdr[7] != 8)) {
+  if (kind == BBC_KIND_PQ && (M <= 0 || d % M != 0 || M % 8 != 0 || M > 64 || (hdr[7] != 8 && hdr[7] != 4))) {
     fclose(f);
-    return fail(BBC_ERR_FORMAT, "PQ needs 8-bit codes, M in {8,16,24,32,48,64}, M | d");
+    return fail(BBC_ERR_FORMAT, "PQ needs 8- or 4-bit codes, M in {8,16,24,32,48,64}, M | d");
   }
   if (kind == BBC_KIND_RABITQ && (D % 64 != 0 || D < d)) {
     fclose(f);
@@ -1057,7 +1095,7 @@ bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_
   const size_t rowraw = (size_t)d * (raw_u8 ? 1 : 4);
   const size_t dsub = kind == BBC_KIND_PQ ? d / M : 0;
   const size_t expect[10] = {(size_t)nlist * d * 4, (size_t)(nlist + 1) * 8, (size_t)N * 8,
-                             kind == BBC_KIND_PQ ? (size_t)M * 256 * dsub * 4 : 0,
+                             kind == BBC_KIND_PQ ? (size_t)M * ((size_t)1 << hdr[7]) * dsub * 4 : 0,
                              kind == BBC_KIND_PQ ? (size_t)N * M : 0,
                              kind == BBC_KIND_RABITQ ? (size_t)D * D * 4 : 0,
                              kind == BBC_KIND_RABITQ ? (size_t)nlist * D * 4 : 0,
@@ -1079,6 +1117,7 @@ bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_
   ix = new bbc_index_s();
   ix->device = cuda_device; ix->rank = rank; ix->world = world;
   ix->kind = kind; ix->d = d; ix->nlist = nlist; ix->M = M; ix->D = D; ix->raw_u8 = raw_u8;
+  ix->nbits = kind == BBC_KIND_PQ ? (int)hdr[7] : 8;
   ix->metric = metric;
   ix->N = N;
   ix->gsize.resize(nlist);
@@ -1234,17 +1273,21 @@ bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_
     // chunk-major copy of the codes for the replicated-LUT scan (layout: k_transpose_codes)
     std::vector<long long> tb(nlist, 0);
     long long tot = 0;
+    const long long gbytes = ix->nbits == 4 ? 16LL * M : 32LL * M;   // bytes per 32-object group
     for (int L = 0; L < nlist; ++L) {
       tb[L] = tot;
-      tot += (long long)((ix->lsize[L] + 31) / 32) * M * 32;
+      tot += (long long)((ix->lsize[L] + 31) / 32) * gbytes;
     }
     ok = dalloc((void**)&ix->codes_t, (size_t)tot + kCodesTailPad) &&
          dalloc((void**)&ix->tbase, (size_t)nlist * 8) &&
          cudaMemcpy(ix->tbase, tb.data(), (size_t)nlist * 8, cudaMemcpyHostToDevice) == cudaSuccess &&
          cudaMemset(ix->codes_t, 0, (size_t)tot + kCodesTailPad) == cudaSuccess;
     if (ok && ix->n_local > 0) {
-      k_transpose_codes<<<(unsigned)((ix->n_local + 255) / 256), 256>>>(
-          ix->codes, ix->loff, ix->tbase, nlist, ix->n_local, M, ix->codes_t);
+      if (ix->nbits == 4)
+        k_pack_codes4<<<nlist, 256>>>(ix->codes, ix->loff, ix->tbase, M, ix->codes_t);
+      else
+        k_transpose_codes<<<(unsigned)((ix->n_local + 255) / 256), 256>>>(
+            ix->codes, ix->loff, ix->tbase, nlist, ix->n_local, M, ix->codes_t);
       ok = cudaDeviceSynchronize() == cudaSuccess;
     }
   }
@@ -1316,6 +1359,7 @@ bbc_status bbc_index_info(bbc_index ix, bbc_index_info_t* info) {
   info->m = ix->M; info->dpad = ix->D; info->raw_u8 = ix->raw_u8; info->n_local = ix->n_local;
   info->max_list = ix->max_list; info->rank = ix->rank; info->world = ix->world;
   info->metric = ix->metric;
+  info->nbits = ix->kind == BBC_KIND_PQ ? ix->nbits : 1;
   return BBC_OK;
 }
 

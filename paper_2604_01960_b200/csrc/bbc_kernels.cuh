@@ -54,6 +54,7 @@ struct Batch {
 // Index arrays on the device.
 struct Dev {
   int kind, d, nlist, M, D, raw_u8;
+  int ksub;                      // PQ centroids per sub-quantizer: 256 (8-bit) or 16 (4-bit)
   int metric;                    // BBC_METRIC_L2 | BBC_METRIC_IP (keys -<q, x>)
   long long n_local;
   const float* centroids;        // [nlist x d]
@@ -407,11 +408,12 @@ __global__ void __launch_bounds__(1024) k_qperm(Batch b, const int* lrank, int* 
 // ------------------------------------------------------------------------------------------
 // a2  PQ lookup table: LUT[q][m][c] = sum_t (q_t - C[m][c][t])^2, t ascending (canonical)
 // ------------------------------------------------------------------------------------------
+// One CTA of ksub threads per (m, q); entry (m, c) at b.table[q * M * 256 + m * ksub + c].
 __global__ void __launch_bounds__(256) k_pq_lut(Batch b, Dev ix) {
   const int m = blockIdx.x, q = blockIdx.y, c = threadIdx.x;
   const int ds = ix.d / ix.M;
   const float* qv = b.Q + (size_t)q * ix.d + m * ds;
-  const float* cb = ix.books + ((size_t)m * 256 + c) * ds;
+  const float* cb = ix.books + ((size_t)m * ix.ksub + c) * ds;
   float acc = 0.f;
   if (ix.metric == BBC_METRIC_IP) {                   // LUT[m][c] = -<q_m, C[m][c]>
     for (int t = 0; t < ds; ++t) acc = __fadd_rn(acc, __fmul_rn(qv[t], cb[t]));
@@ -422,7 +424,7 @@ __global__ void __launch_bounds__(256) k_pq_lut(Batch b, Dev ix) {
       acc = __fadd_rn(acc, __fmul_rn(df, df));
     }
   }
-  b.table[((size_t)q * ix.M + m) * 256 + c] = acc;
+  b.table[(size_t)q * ix.M * 256 + (size_t)m * ix.ksub + c] = acc;
 }
 
 // RaBitQ rotated query u = P^T q: u_i = sum_{t<d} P[t][i] q_t, t ascending (canonical).

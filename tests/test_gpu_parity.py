@@ -87,13 +87,13 @@ def check_final_ids(gi, gd, oi, od, k):
     assert len(go) == len(gi[gi >= 0])                   # no duplicates
 
 
-@pytest.mark.parametrize("name", ["C1t", "C1s", "C2s", "C2f", "C3s", "C4s", "C5s", "C4ip_s"])
+@pytest.mark.parametrize("name", ["C1t", "C1s", "C2s", "C2f", "C3s", "C4s", "C5s", "C4ip_s", "C2q4s"])
 def test_parity_config_point(name):
     cfg, ix, Q, g = gpu_index(name)
     compare(cfg, ix, Q, g, cfg.k, cfg.nprobe, cfg.budget)
 
 
-@pytest.mark.parametrize("name", ["C1t", "C2s", "C3s", "C4ip_s"])
+@pytest.mark.parametrize("name", ["C1t", "C2s", "C3s", "C4ip_s", "C2q4s"])
 def test_parity_parameter_grid(name):
     cfg, ix, Q, g = gpu_index(name)
     for nprobe, bm in ((1, 1), (3, 2), (cfg.nprobe * 2, 1), (min(cfg.nlist, 64), 3)):
@@ -333,7 +333,7 @@ def test_rabitq_scan_modes_identical(nprobe_mult):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["C2s", "C2f", "C3s", "C4s", "C5s", "C4ip_s"])
+@pytest.mark.parametrize("name", ["C2s", "C2f", "C3s", "C4s", "C5s", "C4ip_s", "C2q4s"])
 def test_rerank_orders_identical(name):
     """The list-major re-rank (segments ordered by inverted list) and the query-major
     one compute every candidate's exact distance identically: candidate distances, ids and
