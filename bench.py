@@ -476,8 +476,9 @@ def main():
 
 
 def bucket_sweep(cfg, path, g, nprobe, budget):
-    """Exp-6 / Table 4 analog: the number of buckets B against the candidate
-    superset size, recall and device time, at the workload's operating point."""
+    """Exp-6 / Table 4 analog: the number of buckets (equal-width B, or m
+    equal-depth buckets remapped from the 255 cells) against the candidate superset size, recall
+    and device time, at the workload's operating point."""
     import torch
     X = database_in_id_order(path)
     Q = synth.generate_queries(cfg)
@@ -487,8 +488,12 @@ def bucket_sweep(cfg, path, g, nprobe, budget):
                                      datagen.cache_dir(), metric=cfg.metric)
     st = torch.cuda.current_stream()
     ws = g.workspace(len(Q), cfg.k, nprobe, budget)
-    for B in (1, 3, 7, 15, 31, 63, 127, 255):
+    # equal-width B, then the paper's n_ew = 256 -> m equal-depth remap at its m values (56, 80,
+    # 92, 120 for its datasets) and a few more
+    runs = [(B, 0) for B in (1, 3, 7, 15, 31, 63, 127, 255)] + [(255, m) for m in (8, 16, 56, 80, 92, 120, 255)]
+    for B, m in runs:
         g.set_buckets(B)
+        g.set_remap(m)
         g.search(q, cfg.k, nprobe, budget, workspace=ws)
         torch.cuda.synchronize()
         ms = []
@@ -502,11 +507,12 @@ def bucket_sweep(cfg, path, g, nprobe, budget):
         idn = ids[:rq].cpu().numpy()
         r = groundtruth.recall(idn, groundtruth.exact_of(Q[:rq], X, idn, metric=cfg.metric), gi, gd)
         s = g.last_stats()
-        print(json.dumps({"bucket_sweep": cfg.name, "B": B, "nprobe": nprobe, "budget": budget,
+        print(json.dumps({"bucket_sweep": cfg.name, "B": B, "equal_depth_m": m, "nprobe": nprobe, "budget": budget,
                           "ms": float(np.median(ms)), "qps": len(Q) / (float(np.median(ms)) / 1e3),
                           "superset_over_budget": s["candidates"] / len(Q) / budget,
                           "recall": round(r, 4)}), flush=True)
     g.set_buckets(255)
+    g.set_remap(0)
 
 
 def sweep(cfg, path, g, rank):

@@ -130,6 +130,18 @@ bbc_status bbc_set_probe_mode(bbc_index index, int32_t mode);
  */
 bbc_status bbc_set_buckets(bbc_index index, int32_t nbuckets);
 
+/*
+ * bbc_set_remap -- the n_ew -> m equal-depth remap of the result buffer ("first computes
+ * n_ew equal-width buckets and then reassigns these buckets into m equal-depth buckets, where a
+ * lookup table map is used"; Eq. 6 with map; reading R6).  m = 0 (default):
+ * the equal-width cells are the buckets.  m in [1, 255]: per query, the sample's histogram over
+ * the cells defines m equal-depth buckets (greedy: a bucket closes at the first cell where the
+ * running sample count reaches its share); the threshold is the first bucket whose count reaches
+ * the budget, and S* is every object whose bucket is at or below it -- a superset of the
+ * equal-width S*.  BBC_ERR_ARG for m outside [0, 255] or m > 0 on a sharded handle.
+ */
+bbc_status bbc_set_remap(bbc_index index, int32_t m);
+
 #define BBC_SCAN_SIMT 0
 #define BBC_SCAN_TENSOR 1
 bbc_status bbc_set_scan_mode(bbc_index index, int32_t mode);

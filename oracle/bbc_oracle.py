@@ -268,6 +268,41 @@ def threshold(H: np.ndarray, budget: int) -> int:
     return int(hit[0]) if len(hit) else TAU_INF
 
 
+def equal_depth_map(H0: np.ndarray, m: int, nbuckets: int = 255) -> np.ndarray:
+    """The n_ew -> m remap ("first computes n_ew equal-width buckets and then reassigns
+    these buckets into m equal-depth buckets, where a lookup table map is used", Eq. 6 with map,
+    P:L922-932; reading R6): walk the equal-width cells c = 0 .. nbuckets-1 accumulating the
+    sample histogram H0; cell c goes to the current bucket b, and b advances after c once the
+    running count reaches (b+1)/m of the sample total (exact integer test run*m >= (b+1)*T),
+    b <= m-1.  Cells >= nbuckets (incl. the overflow cell 255) map to 255 (never a candidate)."""
+    if not 1 <= m <= 255:
+        raise ValueError("m must be in [1, 255]")
+    H0 = np.asarray(H0, dtype=np.int64)
+    T = int(H0[:nbuckets].sum())
+    mp = np.full(256, 255, dtype=np.int64)
+    b, run = 0, 0
+    for c in range(nbuckets):
+        mp[c] = b
+        run += int(H0[c])
+        if b < m - 1 and run * m >= (b + 1) * T:
+            b += 1
+    return mp
+
+
+def remap_threshold(H: np.ndarray, mp: np.ndarray, budget: int, m: int) -> int:
+    """Update over the m equal-depth buckets: the first bucket tau_b whose cumulative count
+    (cells mapped to it) reaches the budget; returned as the last cell mapped to a bucket
+    <= tau_b, so that {map[cell] <= tau_b} = {cell <= returned} (map is nondecreasing)."""
+    Hb = np.zeros(m, dtype=np.int64)
+    for c in range(255):
+        if mp[c] < m:
+            Hb[mp[c]] += int(H[c])
+    tb = threshold(Hb, budget)
+    if tb == TAU_INF:
+        return TAU_INF
+    return int(np.flatnonzero(mp[:255] <= tb).max())
+
+
 # ----------------------------------------------------------------------------------------------
 # O9  exact re-rank and final selection
 # ----------------------------------------------------------------------------------------------
@@ -293,7 +328,7 @@ def select_topk(d2: np.ndarray, ids: np.ndarray, k: int):
 # the whole path
 # ----------------------------------------------------------------------------------------------
 def search(ix: dict, Q: np.ndarray, k: int, nprobe: int, budget: int, want_debug: bool = False,
-           probe_result=None, nbuckets: int = 255):
+           probe_result=None, nbuckets: int = 255, remap_m: int = 0):
     """BBC search of every query in Q over the index dict `ix` (datagen.index_file.read).
 
     Returns (ids int64 [nq x k], d2 fp32 [nq x k]) -- rows sorted by (d^2, id) -- and, when
@@ -349,7 +384,11 @@ def search(ix: dict, Q: np.ndarray, k: int, nprobe: int, budget: int, want_debug
             dmin, dmax = edges(est[:ns], budget)
             cell = cells(est, dmin, dmax, nbuckets)
             H = np.bincount(cell, minlength=NCELL)
-            tau = threshold(H, budget)
+            if remap_m:                                # equal-depth buckets (reading R6)
+                H0 = np.bincount(cell[:ns], minlength=NCELL)
+                tau = remap_threshold(H, equal_depth_map(H0, remap_m, nbuckets), budget, remap_m)
+            else:
+                tau = threshold(H, budget)
             sup = np.flatnonzero(cell <= tau)
         spos = pos[sup]
         sid = np.asarray(ids_all[spos])

@@ -24,7 +24,7 @@ EXPORTS = ("ivf_load", "ivf_free", "bbc_index_info", "bbc_workspace_size", "bbc_
            "bbc_last_stats", "bbc_launch_count", "bbc_last_error", "bbc_nccl_unique_id",
            "bbc_comm_init", "bbc_search_group", "bbc_last_stats2", "bbc_set_probe_mode",
            "bbc_set_scan_mode", "bbc_stats_vector", "bbc_set_buckets", "bbc_set_rerank_order",
-           "bbc_measure_l2_read")
+           "bbc_measure_l2_read", "bbc_set_remap")
 
 STAGES = ("probe", "tables", "sample", "scan", "compact", "rerank", "select", "comm")
 TAU_INF = 1 << 30
@@ -85,6 +85,7 @@ def lib() -> ctypes.CDLL:
         L.bbc_set_scan_mode.argtypes = [vp, i32]
         L.bbc_set_buckets.argtypes = [vp, i32]
         L.bbc_set_rerank_order.argtypes = [vp, i32]
+        L.bbc_set_remap.argtypes = [vp, i32]
         L.bbc_measure_l2_read.argtypes = [i32, ctypes.c_size_t, i32, ctypes.POINTER(ctypes.c_double)]
         L.bbc_stats_vector.argtypes = [vp, ctypes.POINTER(i64), i32]
         L.bbc_get_timing.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int,
@@ -102,7 +103,7 @@ def lib() -> ctypes.CDLL:
                    "bbc_last_stats", "bbc_query_capacity", "bbc_nccl_unique_id",
                    "bbc_comm_init", "bbc_search_group", "bbc_last_stats2", "bbc_set_probe_mode",
                    "bbc_set_scan_mode", "bbc_stats_vector", "bbc_set_buckets",
-                   "bbc_set_rerank_order", "bbc_measure_l2_read"):
+                   "bbc_set_rerank_order", "bbc_measure_l2_read", "bbc_set_remap"):
             getattr(L, fn).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -300,6 +301,11 @@ class Index:
         """RaBitQ estimates with popcounts per (query, list) (SCAN_SIMT) or as list-major integer
         GEMMs on the tensor cores (SCAN_TENSOR, default); PQ indexes ignore it."""
         _check(lib().bbc_set_scan_mode(self._h, int(mode)))
+
+    def set_remap(self, m: int) -> None:
+        """m equal-depth buckets from the sample (the paper's n_ew -> m remap, reading R6); 0
+        (default) keeps the equal-width cells as the buckets."""
+        _check(lib().bbc_set_remap(self._h, int(m)))
 
     RERANK_QUERY, RERANK_LIST, RERANK_AUTO = 0, 1, 2
 

@@ -71,6 +71,7 @@ struct bbc_index_s {
   bool probe_tc_ok = false;             // d <= 1024: the tensor-core probe is available
   int rbq_tc = 0;                       // 1: RaBitQ estimates on the tensor cores (bbc_rbq_tc.cuh)
   int rerank_order = BBC_RERANK_AUTO;    // BBC_RERANK_*: work order of the exact re-rank (a7)
+  int remap_m = 0;                       // 0 or m equal-depth buckets (bbc_set_remap)
   int2* rbq_tiles = nullptr;            // [rbq_ntiles] (list, first object) of 128-object tiles
   int rbq_ntiles = 0;
   int* rbq_pc = nullptr;                // [n_local] popcount of each code
@@ -183,6 +184,7 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1) {
                 (size_t)((cap + kChunk - 1) / kChunk) * 8 + (size_t)(nprobe + 1) * 4;
   p.per_query += 8 + 8 + kCells * 4 + 4 + 4 + (size_t)4 * world;   // DistBuf
   p.per_query += (size_t)nprobe * 20 + (size_t)(cap / kRrPiece) * 16;   // re-rank pieces
+  p.per_query += kCells;                                                 // remap
   p.fixed = 64 * 256 + (size_t)3 * (ix->nlist + 1) * 4 + 3 * 256;
   if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) {            // pair codes + inverted index
     p.per_query += (size_t)nprobe * ((size_t)ix->D + sizeof(RbqPair) + 4);   // codes, records, slots
@@ -225,6 +227,7 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, 
   b.chunk = (int*)take((size_t)nqb * ((p.cap + kChunk - 1) / kChunk) * 4);
   b.chunkj = (int*)take((size_t)nqb * ((p.cap + kChunk - 1) / kChunk) * 4);
   b.sstart = (int*)take((size_t)nqb * nprobe * 4);
+  b.rmap = (uint8_t*)take((size_t)nqb * kCells);
   b.rseg = (int4*)take((size_t)nqb * (nprobe + p.cap / kRrPiece) * 16);
   b.rs_cnt = (int*)take((size_t)(ix->nlist + 1) * 4);
   b.rs_off = (int*)take((size_t)(ix->nlist + 1) * 4);
@@ -589,6 +592,10 @@ void stage_compact(Shard& s, cudaStream_t st) {
   StageScope sc(s.ix, st, BBC_STAGE_COMPACT);
   const int nb = s.b.nq;
   const int nchunk = (int)((s.p.cap + kChunk - 1) / kChunk);
+  if (s.b.remap_m > 0) {
+    k_remap<<<nb, 256, 0, st>>>(s.b);
+    g_launches += 1;
+  }
   k_tau<<<nb, 32, 0, st>>>(s.b);
   k_count<<<dim3((nchunk + kCntPer - 1) / kCntPer, nb), kCmpNT, 0, st>>>(s.b, s.b.chunk, nchunk);
   k_chunk_offsets<<<nb, 256, 0, st>>>(s.b, s.b.chunk, nchunk);
@@ -842,6 +849,7 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
       Batch& b = s.b;
       b.nq = nb; b.nprobe = nprobe; b.k = k; b.budget = budget_c; b.cap = s.p.cap;
       b.nbuckets = s.ix->nbuckets;
+      b.remap_m = s.ix->remap_m;
       b.stats = s.ix->stats;
       if (host) {
         CU(cudaMemcpyAsync(s.qstage, queries + q0 * ix->d, (size_t)nb * ix->d * 4,
@@ -1342,6 +1350,14 @@ bbc_status bbc_set_scan_mode(bbc_index ix, int32_t mode) {
   if (mode == BBC_SCAN_TENSOR && ix->kind == BBC_KIND_RABITQ && !ix->rbq_pc)
     return fail(BBC_ERR_ARG, "tensor-core RaBitQ scan unavailable for this index (D > 1024)");
   ix->rbq_tc = (mode == BBC_SCAN_TENSOR && ix->kind == BBC_KIND_RABITQ) ? 1 : 0;
+  return BBC_OK;
+}
+
+bbc_status bbc_set_remap(bbc_index ix, int32_t m) {
+  if (!ix) return fail(BBC_ERR_ARG, "null index");
+  if (m < 0 || m > 255) return fail(BBC_ERR_ARG, "m must be 0 (off) or in [1, 255]");
+  if (m > 0 && ix->world > 1) return fail(BBC_ERR_ARG, "the equal-depth remap is single-shard only");
+  ix->remap_m = m;
   return BBC_OK;
 }
 

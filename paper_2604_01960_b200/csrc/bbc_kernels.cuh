@@ -45,6 +45,8 @@ struct Batch {
   int* chunk;         // [nq x nchunk]  per-chunk candidate counts -> offsets (compaction)
   int* chunkj;        // [nq x nchunk]  probed list holding each chunk's first element
   int* sstart;        // [nq x nprobe]  first candidate of each (query, probe) pair (pairs with poff < n)
+  uint8_t* rmap;      // [nq x 256]     equal-depth remap of the cells (remap_m > 0)
+  int remap_m;        // 0: buckets are the equal-width cells; else m equal-depth buckets (R6)
   int4* rseg;         // [nq x (nprobe + cap/64)] re-rank pieces (query, first, length) in list order
   int* rs_cnt;        // [nlist + 1]    piece counts (rs_off[nlist] = #pieces)
   int* rs_off;        // [nlist + 1]
@@ -1036,9 +1038,74 @@ __global__ void __launch_bounds__(kSelNT) k_select_edges(Batch b, Dev ix) {
 // a5  Update: tau = first cell whose cumulative count reaches the budget (Alg. 1 l.5-11).
 //     One warp per query, 8 cells per lane, inclusive scan.  tau = infinity when no sample.
 // ------------------------------------------------------------------------------------------
+// The n_ew -> m equal-depth remap (Eq. 6 with map; reading R6): the sample's histogram
+// over the equal-width cells (its estimates are the first poff[nsamp] entries of val), then the
+// greedy equal-depth walk by one thread (256 steps).  One CTA per query.
+__global__ void __launch_bounds__(256) k_remap(Batch b) {
+  __shared__ int h0[kCells];
+  const int q = blockIdx.x;
+  const int ns = b.nsamp[q];
+  uint8_t* mp = b.rmap + (size_t)q * kCells;
+  h0[threadIdx.x] = 0;
+  __syncthreads();
+  if (ns > 0) {
+    CellFn cf;
+    cf.init(b.edges[2 * q], b.edges[2 * q + 1], b.nbuckets);
+    const int n = b.poff[(size_t)q * (b.nprobe + 1) + ns];
+    const float* v = b.val + (size_t)q * b.cap;
+    for (int i = threadIdx.x; i < n; i += 256) {
+      const int c = cf(v[i]);
+      if (c < 255) atomicAdd(&h0[c], 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int m = b.remap_m, nb = b.nbuckets;
+    long long T = 0;
+    for (int c = 0; c < nb; ++c) T += h0[c];
+    long long run = 0;
+    int bk = 0;
+    for (int c = 0; c < kCells; ++c) {
+      if (c >= nb) { mp[c] = 255; continue; }
+      mp[c] = (uint8_t)bk;
+      run += h0[c];
+      if (bk < m - 1 && run * m >= (long long)(bk + 1) * T) ++bk;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(32) k_tau(Batch b) {
   const int q = blockIdx.x, lane = threadIdx.x;
   int tau = kTauInf;
+  if (b.nsamp[q] > 0 && b.remap_m > 0) {
+    // equal-depth buckets: histogram of the buckets, first bucket reaching the budget, then
+    // the last cell mapped at or below it ({map[cell] <= tau_b} = {cell <= tau})
+    __shared__ long long hb[kCells];
+    const int* H = b.hist + (size_t)q * kCells;
+    const uint8_t* mp = b.rmap + (size_t)q * kCells;
+    for (int i = lane; i < kCells; i += 32) hb[i] = 0;
+    __syncwarp();
+    if (lane == 0)
+      for (int c = 0; c < 255; ++c)
+        if (mp[c] < b.remap_m) hb[mp[c]] += H[c];
+    __syncwarp();
+    if (lane == 0) {
+      long long cum = 0;
+      int tb = -1;
+      for (int i = 0; i < b.remap_m && tb < 0; ++i) {
+        cum += hb[i];
+        if (cum >= b.budget) tb = i;
+      }
+      if (tb >= 0) {
+        int last = 0;
+        for (int c = 0; c < 255; ++c)
+          if (mp[c] <= tb) last = c;
+        tau = last;
+      }
+    }
+    if (lane == 0) b.tau[q] = tau;
+    return;
+  }
   if (b.nsamp[q] > 0) {
     const int* H = b.hist + (size_t)q * kCells;
     long long v[8], s = 0;

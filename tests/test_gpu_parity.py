@@ -34,16 +34,20 @@ def gpu_index(name):
     return cfg, ix, Q, _IDX[name]
 
 
-def compare(cfg, ix, Q, gidx, k, nprobe, budget, want_est=True, check_final=True, nbuckets=255):
+def compare(cfg, ix, Q, gidx, k, nprobe, budget, want_est=True, check_final=True, nbuckets=255,
+            remap_m=0):
     from oracle import bbc_oracle as O
     q = torch.from_numpy(Q).cuda()
     gidx.set_buckets(nbuckets)
+    gidx.set_remap(remap_m)
     ids, d2, t = gidx.search_debug(q, k, nprobe, budget, want_est=want_est)
     torch.cuda.synchronize()
     gidx.set_buckets(255)
+    gidx.set_remap(0)
     t = {a: b.cpu().numpy() for a, b in t.items()}
     ids, d2 = ids.cpu().numpy(), d2.cpu().numpy()
-    oi, od, dbg = O.search(ix, Q, k, nprobe, budget, want_debug=True, nbuckets=nbuckets)
+    oi, od, dbg = O.search(ix, Q, k, nprobe, budget, want_debug=True, nbuckets=nbuckets,
+                           remap_m=remap_m)
     for i, g in enumerate(dbg):
         assert np.array_equal(t["probe"][i], g["probe"]), f"q{i} probe"
         assert np.array_equal(t["rq2"][i].view(np.uint32), g["rq2"].view(np.uint32)), f"q{i} rq2"
@@ -386,6 +390,19 @@ def test_parity_bucket_counts(name, nbuckets):
     oracle's for coarse bucket grids too (PQ and the tensor-core RaBitQ path)."""
     cfg, ix, Q, g = gpu_index(name)
     compare(cfg, ix, Q[:8], g, cfg.k, cfg.nprobe, cfg.budget, want_est=False, nbuckets=nbuckets)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["C2s", "C3s", "C2q4s"])
+@pytest.mark.parametrize("m", [1, 8, 56, 255])
+def test_parity_equal_depth_remap(name, m):
+    """The n_ew -> m equal-depth remap (reading R6): thresholds, supersets and results equal the
+    oracle's for m buckets (56 = the paper's Wiki setting), also with B = 100 cells."""
+    cfg, ix, Q, g = gpu_index(name)
+    compare(cfg, ix, Q[:8], g, cfg.k, cfg.nprobe, cfg.budget, want_est=False, remap_m=m)
+    if m == 56:
+        compare(cfg, ix, Q[:8], g, cfg.k, cfg.nprobe, cfg.budget, want_est=False, remap_m=m,
+                nbuckets=100)
 
 
 @pytest.mark.parametrize("name,mult", [("C2s", 4), ("C3s", 8), ("C5s", 4), ("C4ip_s", 2)])

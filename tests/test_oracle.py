@@ -511,3 +511,68 @@ def test_pq4_full_probe_is_brute_force(rng):
         ids, d2 = O.search(ix, Q, k, cfg.nlist, cfg.N)
         gi, gd = BF.ground_truth(Q, X, k)
         assert np.array_equal(ids, gi)
+
+
+# ---------------------------------------------------------------------------------------------
+# n_ew -> m equal-depth remap (Eq. 6 with map P:L922-932; reading R6)
+# ---------------------------------------------------------------------------------------------
+def test_equal_depth_map_hand_example():
+    """Sample histogram 4, 0, 2, 2 (T = 8) into m = 2 buckets: the first bucket closes after
+    cell 0 (4 of 8 = half); cells 1..254 form the second; the overflow cell stays 255."""
+    H0 = np.zeros(256, dtype=np.int64)
+    H0[:4] = [4, 0, 2, 2]
+    mp = O.equal_depth_map(H0, 2)
+    assert mp[0] == 0 and np.all(mp[1:255] == 1) and mp[255] == 255
+    # m = 4: bucket b closes at the first cell where the running count reaches 2 (b + 1),
+    # at most one bucket per cell: after cells 0 (4), 1 (4), 2 (6)
+    mp4 = O.equal_depth_map(H0, 4)
+    assert list(mp4[:5]) == [0, 1, 2, 3, 3]
+
+
+def test_equal_depth_map_invariants(rng):
+    """Nondecreasing, starts at 0, at most m buckets, and every bucket but the last closes as
+    soon as the running sample count reaches its share (the greedy equal-depth rule)."""
+    for trial in range(30):
+        H0 = np.zeros(256, dtype=np.int64)
+        nz = rng.integers(1, 255)
+        H0[:255] = rng.integers(0, 50, 255) * (rng.random(255) < nz / 255)
+        H0[0] += 1
+        m = int(rng.integers(1, 60))
+        mp = O.equal_depth_map(H0, m)
+        assert mp[0] == 0 and np.all(np.diff(mp[:255]) >= 0) and mp[:255].max() <= m - 1
+        assert np.all(np.diff(mp[:255]) <= 1)
+        T = H0[:255].sum()
+        run = np.cumsum(H0[:255])
+        for c in range(1, 255):
+            if mp[c] > mp[c - 1]:                      # bucket mp[c-1] closed after cell c-1
+                assert run[c - 1] * m >= (mp[c - 1] + 1) * T
+                assert c - 1 == 0 or mp[c - 2] < mp[c - 1] or run[c - 2] * m < (mp[c - 1] + 1) * T
+
+
+def test_remap_identity_reduces_to_threshold(rng):
+    """One sample object per cell and m = 255: the map is the identity, so the remapped
+    threshold is the equal-width one."""
+    H0 = np.zeros(256, dtype=np.int64)
+    H0[:255] = 1
+    mp = O.equal_depth_map(H0, 255)
+    assert np.array_equal(mp[:255], np.arange(255))
+    for trial in range(20):
+        H = rng.integers(0, 100, 256)
+        budget = int(rng.integers(1, H[:255].sum() + 50))
+        assert O.remap_threshold(H, mp, budget, 255) == O.threshold(H[:255], budget)
+
+
+def test_remap_superset_contains_equal_width(c1t):
+    """Equal-depth buckets are unions of equal-width cells: the remapped superset contains the
+    equal-width one for every m, and m = 1 takes every object within d_max."""
+    cfg, ix, Q, _ = c1t
+    for m in (1, 4, 16, 64):
+        _, _, d0 = O.search(ix, Q[:3], cfg.k, cfg.nprobe, cfg.budget, want_debug=True)
+        _, _, d1 = O.search(ix, Q[:3], cfg.k, cfg.nprobe, cfg.budget, want_debug=True, remap_m=m)
+        for a, b in zip(d0, d1):
+            if a["tau"] == O.TAU_INF:
+                continue
+            assert b["tau"] >= a["tau"]
+            assert set(a["sup_pos"].tolist()) <= set(b["sup_pos"].tolist())
+            if m == 1:
+                assert b["tau"] == 254 and len(b["sup_pos"]) == int((b["cell"] < 255).sum())
