@@ -11,22 +11,22 @@
 // bit-identical to the SIMT kernel's (same fp32 expression tree afterwards).
 //
 //   k_rbq_l*      : the pair layout: pairs grouped by list (sample pairs j < nsamp first),
-//                   each list's slot range padded to a multiple of 32 (one MMA query tile).
+//                   each list's slot range padded to a multiple of kRbN (one MMA query tile).
 //   k_rbq_pairs   : per (query, probed list): q' = (u - w_L)/r, v_l, Delta, qbar (bytes), s_q,
 //                   and (c1, c2, c3, r) -- the canonical per-pair part of the estimator, at the
 //                   pair's slot (codes row-major, coalesced).
-//   k_rbq_mma_ws  : CTA = (list L, tile of 128 objects); A (128 x D bytes) staged once, then
-//                   for each tile of 32 pairs: B (32 x D bytes, TMA tensor copies with 128-byte
-//                   swizzle, one per 128-byte K block) + records (bulk copy) into a ring of
-//                   stages (mbarrier complete_tx), D/32 MMAs
-//                   (M=128, N=96, K=32, A in tensor memory) into one of two TMEM accumulators,
+//   k_rbq_mma_ws  : CTA = (list L, tile of 128 objects); A (the objects' bits as bytes 0/1)
+//                   written once into tensor memory, then for each tile of kRbN = 96 pairs: B
+//                   (96 x D bytes, TMA tensor copies with 128-byte swizzle, one per 128-byte K
+//                   block) + records (bulk copy) into a ring of stages (mbarrier complete_tx),
+//                   D/32 MMAs (M=128, N=96, K=32, A from TMEM) into one of two TMEM accumulators,
 //                   epilogue by 24 warps: estimate (sample pass) or bucket id (Push).
 //   k_cell_hist   : Push histogram per query from its bucket ids (query-major, shared-memory
 //                   counts, one global flush per CTA: list-major partial histograms would need
 //                   a global atomic per (pair, bucket)).
-// Operand layouts, K-major: A (object bits as bytes, written by the CTA) without swizzle: 8-row x
-// 16-byte core matrices, LBO = 128 B (K-adjacent), SBO = (D/16) x 128 B (8-row groups).  B (query
-// codes, TMA) in 128-byte-swizzled K blocks of 32 rows x 128 B (4 KB), SBO = 1 KB.
+// Operands, K-major: A (object bits as bytes 0/1) in tensor memory, lane = object, 4 K bytes per
+// 32-bit column; B (query codes, TMA) in shared memory as 128-byte-swizzled K blocks of kRbN rows
+// x 128 B, SBO = 1 KB (8-row atoms).
 #pragma once
 #include "bbc_probe_tc.cuh"
 
@@ -292,14 +292,6 @@ struct RbqTc {
 
 constexpr int kRbqIdesc = (2 << 4) | ((kRbN >> 3) << 17) | ((kRbM >> 4) << 24);   // s32 += u8 x u8
 
-__device__ __forceinline__ uint64_t umma_desc_k(uint32_t saddr, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)(128u >> 4) << 16;                  // LBO: K-adjacent core matrices
-  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;       // SBO: 8-row groups
-  d |= (uint64_t)1 << 46;                            // descriptor version (sm_100)
-  return d;
-}
 
 // K-major, 128-byte swizzle: rows of 128 B, 8-row atoms of 1 KB (SBO), K advanced inside an atom
 // by moving the start address (32 B per MMA step)
@@ -326,12 +318,6 @@ __device__ __forceinline__ void i8_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint
       ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"((uint32_t)kRbqIdesc), "r"(acc));
 }
 
-__device__ __forceinline__ void i8_mma(uint32_t tmem_d, uint64_t a, uint64_t bdesc, uint32_t acc) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
-      ::"r"(tmem_d), "l"(a), "l"(bdesc), "r"((uint32_t)kRbqIdesc), "r"(acc));
-}
 
 __device__ __forceinline__ uint32_t nib_bytes(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
 
