@@ -77,6 +77,12 @@ SMALL = {
                       kmeans_iters=6),
     "C5s": C5.replace(name="C5s", N=200_000, nlist=512, nq=24, k=1_500, nprobe=32, budget=3_000,
                       kmeans_iters=6),
+    # RaBitQ at the dimension limits of the tensor-core path: D = 1024 (two B stages, all 512 TMEM
+    # columns in use) and D = 64 (one K block, two MMAs per tile)
+    "C3d1024s": C3.replace(name="C3d1024s", d=1024, N=20_000, nlist=64, nq=8, k=300, nprobe=10,
+                           budget=900, kmeans_iters=6),
+    "C3d64s": C3.replace(name="C3d64s", d=64, N=30_000, nlist=96, nq=8, k=300, nprobe=12,
+                         budget=900, kmeans_iters=6),
     # fine lists (~20 objects): a compaction chunk of 8,192 objects spans > 256 lists, the
     # global-search path of k_emit; probe sets of 600 lists
     "C2f": C2.replace(name="C2f", N=40_000, nlist=2_048, nq=8, k=500, nprobe=600, budget=1_000,

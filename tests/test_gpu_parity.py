@@ -91,7 +91,8 @@ def check_final_ids(gi, gd, oi, od, k):
     assert len(go) == len(gi[gi >= 0])                   # no duplicates
 
 
-@pytest.mark.parametrize("name", ["C1t", "C1s", "C2s", "C2f", "C3s", "C4s", "C5s", "C4ip_s", "C2q4s"])
+@pytest.mark.parametrize("name", ["C1t", "C1s", "C2s", "C2f", "C3s", "C4s", "C5s", "C4ip_s", "C2q4s",
+                                  "C3d1024s", "C3d64s"])
 def test_parity_config_point(name):
     cfg, ix, Q, g = gpu_index(name)
     compare(cfg, ix, Q, g, cfg.k, cfg.nprobe, cfg.budget)
