@@ -836,9 +836,18 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
     s.dv.probe_tc = s.ix->probe_tc_ok &&
                     (pm == BBC_PROBE_TENSOR || (pm == BBC_PROBE_AUTO && 32LL * nprobe <= s.ix->nlist));
   }
-  // host path: the tail of the batch is cut into halving micro-batches (down to nqb / 8) so that
-  // the one device->host copy left exposed, the last micro-batch's, is small
-  const long long min_nb = std::max<long long>(32, nqb / 8);
+  // host path: the tail of the batch is cut into halving micro-batches so that the one
+  // device->host copy left exposed, the last micro-batch's, is small.
+  // How far: the output copy against the work per query (code bytes of the nprobe largest lists
+  // plus the budget's raw rows).  Where the copy is < 1/1000 of the work (C3: 60 KB vs ~230 MB)
+  // two equal micro-batches hide it and small ones only cost efficiency (C3 e2e 49k -> 65k);
+  // otherwise down to nqb / 4 (C2: 150k -> 158k; measured divisors 1, 2, 4, 8).
+  const double code_b = ix->kind == BBC_KIND_PQ ? (ix->nbits == 4 ? ix->M / 2.0 : (double)ix->M)
+                                                : ix->D / 8.0 + 8.0;
+  const double work_b = (double)sh[0].p.cap * code_b + (double)std::min<long long>(budget, ix->N) *
+                                                           (ix->raw_u8 ? ix->d : 4.0 * ix->d);
+  const int tail_div = (double)k * 12.0 * 1000.0 < work_b ? 1 : 4;
+  const long long min_nb = std::max<long long>(32, nqb / tail_div);
   int nb = 0;
   for (long long q0 = 0; q0 < nq; q0 += nb) {
     const long long rem = nq - q0;
