@@ -63,6 +63,10 @@ struct bbc_index_s {
                                         // 4-bit: k_pack_codes4 layout)
   long long* tbase = nullptr;           // [nlist] byte offset of each list in codes_t
   float* cmu = nullptr;                 // [d] centroid mean (tensor-core probe)
+  float* pb_hi = nullptr;               // [nlist_pad x d] centred centroids, tf32 hi part (d <= 128)
+  float* pb_lo = nullptr;               //                 and the remainder
+  CUtensorMap ptm_hi, ptm_lo;           // their TMA maps (k_probe_mma_ws)
+  bool probe_ws_ok = false;
   float* cnorm = nullptr;               // [nlist] |c - mu|^2
   int* lrank = nullptr;                 // [nlist] (region << 20 | list): query locality order
   float cmax = 0.f;                     // max |c - mu|, rounded up
@@ -417,7 +421,14 @@ struct Shard {
 void stage_probe(Shard& s, cudaStream_t st) {
   bbc_index_s* ix = s.ix;
   StageScope sc(ix, st, BBC_STAGE_PROBE);
-  if (s.dv.probe_tc) {
+  if (s.dv.probe_tc && ix->probe_ws_ok) {
+    const int qt = (s.b.nq + kTcM - 1) / kTcM;
+    const int stripes = std::max(1, std::min((ix->nlist + kTcN - 1) / kTcN, ix->num_sms / std::max(1, qt)));
+    set_smem(k_probe_mma_ws, kPwSmem);
+    if (qt > 0)
+      k_probe_mma_ws<<<qt * stripes, kPwNT, kPwSmem, st>>>(s.b.Q, ix->cmu, ix->cnorm, s.b.coarse, s.b.nq,
+                                                         ix->nlist, ix->d, stripes, ix->ptm_hi, ix->ptm_lo);
+  } else if (s.dv.probe_tc) {
     const dim3 gt((ix->nlist + kTcN - 1) / kTcN, (s.b.nq + kTcM - 1) / kTcM);
     set_smem(k_probe_mma, kTcSmem);
     k_probe_mma<<<gt, kTcNT, kTcSmem, st>>>(s.b.Q, ix->centroids, ix->cmu, ix->cnorm, s.b.coarse,
@@ -444,10 +455,11 @@ void stage_probe(Shard& s, cudaStream_t st) {
   }
 }
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda): a 2-D uint8 map
-// [rows x cols] (row stride = cols bytes) with boxes of box_rows x box_cols and 128-byte swizzle.
-bool encode_tmap_u8(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint32_t box_cols,
-                    uint32_t box_rows) {
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda): a 2-D map
+// [rows x cols] of esize-byte elements (row stride = cols elements) with boxes of box_rows x
+// box_cols and 128-byte swizzle.
+bool encode_tmap(CUtensorMap* m, const void* base, CUtensorMapDataType dt, uint32_t esize, uint64_t cols,
+                 uint64_t rows, uint32_t box_cols, uint32_t box_rows) {
   using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                           const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                           CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -461,10 +473,10 @@ bool encode_tmap_u8(CUtensorMap* m, const void* base, uint64_t cols, uint64_t ro
     fn = reinterpret_cast<Fn>(f);
   }
   const cuuint64_t gdim[2] = {cols, rows};
-  const cuuint64_t gstride[1] = {cols};
+  const cuuint64_t gstride[1] = {cols * esize};
   const cuuint32_t box[2] = {box_cols, box_rows};
   const cuuint32_t estr[2] = {1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), gdim, gstride, box, estr,
+  return fn(m, dt, 2, const_cast<void*>(base), gdim, gstride, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -515,7 +527,7 @@ void rbq_tc_pass(Shard& s, const Batch& b, cudaStream_t st, bool sample) {
   // TMA map of the query codes: [slots x D] bytes, boxes of 32 rows x 128 B, 128-byte swizzle
   const long long slots = pairs + (long long)kRbN * ix->nlist;
   CUtensorMap tm;
-  if (!encode_tmap_u8(&tm, s.rb.qbar, (uint64_t)ix->D, (uint64_t)slots, 128, kRbN)) {
+  if (!encode_tmap(&tm, s.rb.qbar, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, (uint64_t)ix->D, (uint64_t)slots, 128, kRbN)) {
     ix->broken = true;                               // reported by the CU check after the stage
     return;
   }
@@ -1269,6 +1281,21 @@ bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_
          cudaMemcpy(ix->cmu, mu.data(), (size_t)d * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
          cudaMemcpy(ix->cnorm, cn.data(), (size_t)nlist * 4, cudaMemcpyHostToDevice) == cudaSuccess;
     ix->probe_tc_ok = d <= kMaxDimTc && metric == BBC_METRIC_L2;
+    if (ok && ix->probe_tc_ok && d <= 128 && d % 8 == 0) {
+      // the TMA-fed probe (k_probe_mma_ws): centred centroids split hi/lo once, rows padded to 128
+      const int npad = (nlist + kTcN - 1) / kTcN * kTcN;
+      const size_t nb = (size_t)npad * d * 4;
+      ok = dalloc((void**)&ix->pb_hi, nb) && dalloc((void**)&ix->pb_lo, nb);
+      if (ok) {
+        k_probe_split<<<(unsigned)(((long long)npad * d + 255) / 256), 256>>>(ix->centroids, ix->cmu, nlist,
+                                                                              npad, d, ix->pb_hi, ix->pb_lo);
+        ok = cudaDeviceSynchronize() == cudaSuccess;
+      }
+      ix->probe_ws_ok = ok && encode_tmap(&ix->ptm_hi, ix->pb_hi, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (uint64_t)d,
+                                          (uint64_t)npad, 32, kTcN) &&
+                        encode_tmap(&ix->ptm_lo, ix->pb_lo, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (uint64_t)d,
+                                    (uint64_t)npad, 32, kTcN);
+    }
   }
   if (ok && kind == BBC_KIND_RABITQ && D <= 1024 && D % 64 == 0) {
     std::vector<int2> tiles;
@@ -1323,7 +1350,7 @@ void ivf_free(bbc_index ix) {
   cudaSetDevice(ix->device);
   void* ptrs[] = {ix->centroids, ix->loff, ix->gsize_d, ix->ids, ix->books, ix->codes, ix->P,
                   ix->wL, ix->bits, ix->factors, ix->raw, ix->stats, ix->codes_t, ix->tbase,
-                  ix->cmu, ix->cnorm, ix->rbq_tiles, ix->rbq_pc, ix->lrank};
+                  ix->cmu, ix->cnorm, ix->rbq_tiles, ix->rbq_pc, ix->lrank, ix->pb_hi, ix->pb_lo};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& t : ix->timers) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }

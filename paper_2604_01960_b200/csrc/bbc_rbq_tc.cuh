@@ -293,22 +293,7 @@ struct RbqTc {
 constexpr int kRbqIdesc = (2 << 4) | ((kRbN >> 3) << 17) | ((kRbM >> 4) << 24);   // s32 += u8 x u8
 
 
-// K-major, 128-byte swizzle: rows of 128 B, 8-row atoms of 1 KB (SBO), K advanced inside an atom
-// by moving the start address (32 B per MMA step)
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)1 << 16;                            // LBO (unused for swizzled K-major)
-  d |= (uint64_t)(1024u >> 4) << 32;                 // SBO: 8-row atoms
-  d |= (uint64_t)1 << 46;                            // descriptor version (sm_100)
-  d |= (uint64_t)2 << 61;                            // SWIZZLE_128B
-  return d;
-}
 
-__device__ __forceinline__ void tma_2d_g2s(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
-  asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-               ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar) : "memory");
-}
 
 // A from tensor memory (lane = object row, 4 K bytes per 32-bit column), B from shared memory
 __device__ __forceinline__ void i8_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t acc) {
@@ -321,11 +306,6 @@ __device__ __forceinline__ void i8_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint
 
 __device__ __forceinline__ uint32_t nib_bytes(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
 
-// bulk global -> shared copy (async proxy) completing on an mbarrier's transaction count
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
-}
 
 // ------------------------------------------------------------------ the list-major GEMM
 // Warp-specialised pipeline.  Warp 24 (one lane) copies query tile qi -- kRbN slots of codes,
@@ -341,16 +321,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 //   accf[a]  (1 commit)                 accumulator a holds tile qi's products
 //   acce[a]  (24 warps)                 accumulator a read out: free for tile qi + 2
 constexpr int kRbWsEpi = 24, kRbWsNT = (kRbWsEpi + 2) * 32;   // 832 threads
-__device__ __forceinline__ void mbar_init(uint32_t a, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t a) {
-  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(a) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint32_t a, uint32_t bytes) {
-  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}"
-               ::"r"(a), "r"(bytes) : "memory");
-}
 
 template <bool SAMPLE>
 __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqTc t, int nst,
