@@ -22,6 +22,7 @@ p.add_argument("--steps", type=int, default=5)
 p.add_argument("--tag", default="")
 p.add_argument("--probe-simt", action="store_true")
 p.add_argument("--scan-simt", action="store_true")
+p.add_argument("--probe-tc", action="store_true", help="force the tensor-core probe")
 p.add_argument("--nq", type=int, default=0, help="first nq queries only (0: all)")
 p.add_argument("--rerank", choices=("auto", "query", "list"), default="auto", help="re-rank order")
 a = p.parse_args()
@@ -30,6 +31,8 @@ path = datagen.ensure_index(cfg)
 g = Index(path)
 if a.probe_simt:
     g.set_probe_mode(g.PROBE_SIMT)
+if a.probe_tc:
+    g.set_probe_mode(g.PROBE_TENSOR)
 if a.scan_simt:
     g.set_scan_mode(g.SCAN_SIMT)
 g.set_rerank_order({"auto": g.RERANK_AUTO, "query": g.RERANK_QUERY, "list": g.RERANK_LIST}[a.rerank])
