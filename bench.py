@@ -370,7 +370,7 @@ def main():
     if stats.get("rerank_list_batches", 0) > 0:
         # list-order re-rank: the rows a list's queries share are read from L2, so the bound is
         # the L2 -> SM read bandwidth, measured on this GPU by bbc_measure_l2_read
-        l2 = measure_l2_read_gbs(0)
+        l2 = max(measure_l2_read_gbs(0) for _ in range(5))        # a peak: best of 5
         per["rerank"].update({"bound": "l2", "peak_GBs": l2,
                               "pipe": "L2 -> SM reads (rows shared by the queries of a list)",
                               "hbm_view": {"code_bytes": stats["candidates"] * row_bytes,
@@ -422,7 +422,7 @@ def main():
             "unit": "TOP/s" if tens else "Glookup/s" if lkp else "GB/s", "frac": per[dom]["frac"],
             "traffic": traffic,
             "peak_source": (peak_src if per[dom]["bound"] == "hbm" else
-                            "measured: bbc_measure_l2_read (L2-resident 48 MiB, 16-byte loads)"
+                            "measured: bbc_measure_l2_read (L2-resident 48 MiB, 16-byte loads, best of 5)"
                             if per[dom]["bound"] == "l2" else
                             "measured bf16 TFLOP/s x 2 (int8/bf16 nominal ratio)" if tens else
                             "derived: 148 SMs x 64 ALU lanes/clk / 2 ops per lookup x sm_max_mhz (DESIGN.md 5)" if lkp else
