@@ -611,10 +611,10 @@ void stage_compact(Shard& s, cudaStream_t st) {
   k_tau<<<nb, 32, 0, st>>>(s.b);
   k_count<<<dim3((nchunk + kCntPer - 1) / kCntPer, nb), kCmpNT, 0, st>>>(s.b, s.b.chunk, nchunk);
   k_chunk_offsets<<<nb, 256, 0, st>>>(s.b, s.b.chunk, nchunk);
-  set_smem(k_emit, (size_t)kChunk * 4);
+
   Batch be = s.b;                                   // segment starts only for the list-order re-rank
   if (!rerank_list_order(s.ix, s.b, s.ix->raw_u8 ? s.ix->d : s.ix->d * 4)) be.sstart = nullptr;
-  k_emit<<<dim3(nchunk, nb), kCmpNT, (size_t)kChunk * 4, st>>>(be, s.dv, s.b.chunk, nchunk);
+  k_emit<<<dim3(nchunk, nb), kCmpNT, 0, st>>>(be, s.dv, s.b.chunk, nchunk);
   g_launches += 4;
 }
 

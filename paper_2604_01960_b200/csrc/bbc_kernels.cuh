@@ -1258,7 +1258,6 @@ __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chu
   __shared__ unsigned s_flg[kCmpNT];
   __shared__ int s_po[kEmitWin + 1];
   __shared__ long long s_rb[kEmitWin];
-  extern __shared__ int s_row[];                     // [kChunk]
   const int q = blockIdx.y;
   const int c = blockIdx.x;
   const int nprobe = b.nprobe;
@@ -1306,14 +1305,11 @@ __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chu
   }
   if (lane == 31) wcnt[wid] = incl;
   __syncthreads();
-  int pre = 0, tot = 0;
+  int pre = 0;
 #pragma unroll
-  for (int w = 0; w < kCmpNT / 32; ++w) {
-    const int v = wcnt[w];
-    pre += w < wid ? v : 0;
-    tot += v;
-  }
+  for (int w = 0; w < kCmpNT / 32; ++w) pre += w < wid ? wcnt[w] : 0;
   int pos = pre + incl - mine;
+  int* outp = b.cpos + (size_t)q * b.cap + cbeg;     // candidate rows, written in place
   s_pre[threadIdx.x] = pos;
   s_flg[threadIdx.x] = f;
   if (f) {
@@ -1336,7 +1332,7 @@ __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chu
         jend = sp[j + 1];
         rbase = win ? s_rb[j] : rb[jc + j];
       }
-      s_row[pos++] = (int)(rbase + i);
+      outp[pos++] = (int)(rbase + i);
     }
   }
   __syncthreads();
@@ -1362,8 +1358,7 @@ __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chu
       ss[j] = cbeg + s_pre[th] + __popc(s_flg[th] & ((1u << bit) - 1u));
     }
   }
-  int* out = b.cpos + (size_t)q * b.cap + cbeg;
-  for (int t = threadIdx.x; t < tot; t += kCmpNT) out[t] = s_row[t];   // ids: gathered by k_rerank
+
 }
 
 // ------------------------------------------------------------------------------------------
