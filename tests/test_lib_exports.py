@@ -52,3 +52,27 @@ def test_argument_errors_without_gpu():
     assert b"null" in L.bbc_last_error()
     h = ctypes.c_void_p()
     assert L.ivf_load(b"/nonexistent/index", 0, 1, 0, ctypes.byref(h)) == 2
+
+
+def test_python_constants_match_header():
+    """Every mode constant the binding exposes equals the header's #define."""
+    with open(os.path.join(ROOT, "include", "bbc.h")) as f:
+        defs = dict(re.findall(r"^#define\s+(BBC_\w+)\s+(-?\d+)", f.read(), flags=re.M))
+    from paper_2604_01960_b200.bbc import Index
+    pairs = {"SCAN_SIMT": "BBC_SCAN_SIMT", "SCAN_TENSOR": "BBC_SCAN_TENSOR",
+             "PROBE_SIMT": "BBC_PROBE_SIMT", "PROBE_TENSOR": "BBC_PROBE_TENSOR",
+             "PROBE_AUTO": "BBC_PROBE_AUTO", "RERANK_QUERY": "BBC_RERANK_QUERY",
+             "RERANK_LIST": "BBC_RERANK_LIST", "RERANK_AUTO": "BBC_RERANK_AUTO"}
+    for py, c in pairs.items():
+        assert c in defs, c
+        assert getattr(Index, py) == int(defs[c]), py
+
+
+def test_setters_reject_bad_arguments_without_gpu():
+    """Mode setters validate before touching the (null) handle."""
+    from paper_2604_01960_b200 import bbc
+    L = bbc.lib()
+    for fn, v in (("bbc_set_buckets", 0), ("bbc_set_buckets", 256), ("bbc_set_remap", -1),
+                  ("bbc_set_remap", 256), ("bbc_set_rerank_order", 7), ("bbc_set_scan_mode", 9),
+                  ("bbc_set_probe_mode", 5)):
+        assert getattr(L, fn)(None, v) == 1, fn            # null index first: BBC_ERR_ARG
