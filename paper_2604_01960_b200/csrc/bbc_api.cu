@@ -823,7 +823,16 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
   // host path: the device->host copy of micro-batch i (copy stream) overlaps the search of
   // micro-batch i+1; outputs alternate between two staging buffers.  At least 4 micro-batches
   // (of >= 256 queries) so that most of the copy time is hidden.
-  const bool pipe = host && !dist && !dbg;
+  // The output copy against the work per query (code bytes of the nprobe largest lists plus the
+  // budget's raw rows).  Where the copy is < 1/1000 of the work (C3: 60 KB vs ~230 MB) it is not
+  // worth splitting the batch for (one micro-batch, copy exposed: C3 e2e 49k -> 65k -> 73k);
+  // otherwise the tail halves down to nqb / 4 (C2: 150k -> 158k; measured divisors 1, 2, 4, 8).
+  const double code_b = ix->kind == BBC_KIND_PQ ? (ix->nbits == 4 ? ix->M / 2.0 : (double)ix->M)
+                                                : ix->D / 8.0 + 8.0;
+  const double work_b = (double)sh[0].p.cap * code_b + (double)std::min<long long>(budget, ix->N) *
+                                                           (ix->raw_u8 ? ix->d : 4.0 * ix->d);
+  const int tail_div = (double)k * 12.0 * 1000.0 < work_b ? 1 : 4;
+  const bool pipe = host && !dist && !dbg && tail_div > 1;
   if (pipe) {
     nqb = std::min<long long>(nqb, std::max<long long>(256, (nq + 1) / 2));
     if (!ix->copy_stream) {
@@ -850,15 +859,6 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
   }
   // host path: the tail of the batch is cut into halving micro-batches so that the one
   // device->host copy left exposed, the last micro-batch's, is small.
-  // How far: the output copy against the work per query (code bytes of the nprobe largest lists
-  // plus the budget's raw rows).  Where the copy is < 1/1000 of the work (C3: 60 KB vs ~230 MB)
-  // two equal micro-batches hide it and small ones only cost efficiency (C3 e2e 49k -> 65k);
-  // otherwise down to nqb / 4 (C2: 150k -> 158k; measured divisors 1, 2, 4, 8).
-  const double code_b = ix->kind == BBC_KIND_PQ ? (ix->nbits == 4 ? ix->M / 2.0 : (double)ix->M)
-                                                : ix->D / 8.0 + 8.0;
-  const double work_b = (double)sh[0].p.cap * code_b + (double)std::min<long long>(budget, ix->N) *
-                                                           (ix->raw_u8 ? ix->d : 4.0 * ix->d);
-  const int tail_div = (double)k * 12.0 * 1000.0 < work_b ? 1 : 4;
   const long long min_nb = std::max<long long>(32, nqb / tail_div);
   int nb = 0;
   for (long long q0 = 0; q0 < nq; q0 += nb) {
