@@ -456,12 +456,12 @@ struct CellFn {
     inv = degen ? 0.f : __fdiv_rn((float)nb, w);
     if (!degen && isinf(inv)) degen = true;
   }
+  // branch-free: clamp(floor((x - dmin) * inv), 0, bmax); 0 if degenerate; 255 beyond dmax
   __device__ __forceinline__ int operator()(float x) const {
-    if (x > dmax) return 255;
-    if (degen) return 0;
-    float t = __fmul_rn(__fsub_rn(x, dmin), inv);
-    float f = floorf(t);
-    return f < 0.f ? 0 : (f > bmax ? (int)bmax : (int)f);
+    const float f = floorf(__fmul_rn(__fsub_rn(x, dmin), inv));
+    int c = (int)fminf(fmaxf(f, 0.f), bmax);
+    c = degen ? 0 : c;
+    return x > dmax ? 255 : c;
   }
 };
 

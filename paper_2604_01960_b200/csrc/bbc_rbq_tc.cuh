@@ -488,13 +488,11 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
           if (SAMPLE) {
             b.val[at] = est;
           } else {
-            int cell;
-            if (est > e.dmax) cell = 255;
-            else if (e.degen) cell = 0;
-            else {
-              const float f = floorf(__fmul_rn(__fsub_rn(est, e.dmin), e.inv));
-              cell = f < 0.f ? 0 : (f > e.bmax ? (int)e.bmax : (int)f);
-            }
+            // bucket id (Eq. 6, R3), branch-free as CellFn
+            const float f = floorf(__fmul_rn(__fsub_rn(est, e.dmin), e.inv));
+            int cell = (int)fminf(fmaxf(f, 0.f), e.bmax);
+            cell = e.degen ? 0 : cell;
+            cell = est > e.dmax ? 255 : cell;
             b.cells[at] = (uint8_t)cell;
           }
         }
