@@ -286,13 +286,16 @@ __global__ void k_debug_cands(const int* cpos, const float* val, const int* ncan
 template <int M>
 void launch_rq(bool est, int grid, cudaStream_t st, const Batch& b, const Dev& dv,
                const uint8_t* ct, const long long* tb, float* out, long long stride, int mode) {
-  if (est) {
-    set_smem(k_pq_scan_rq<M, true>, kRqSmem);
-    k_pq_scan_rq<M, true><<<grid, kRqNT, kRqSmem, st>>>(b, dv, ct, tb, out, stride, mode, b.items, b.nitems);
-  } else {
-    set_smem(k_pq_scan_rq<M, false>, kRqSmem);
-    k_pq_scan_rq<M, false><<<grid, kRqNT, kRqSmem, st>>>(b, dv, ct, tb, out, stride, mode, b.items, b.nitems);
-  }
+  // codes that do not fit in L2 are streamed past L1 (see k_pq_scan_rq)
+  const bool na = (double)dv.n_local * M > 0.5 * (126 << 20);
+#define BBC_RQ_L(E, NA)                                                                                  \
+  do {                                                                                                  \
+    set_smem(k_pq_scan_rq<M, E, NA>, kRqSmem);                                                          \
+    k_pq_scan_rq<M, E, NA><<<grid, kRqNT, kRqSmem, st>>>(b, dv, ct, tb, out, stride, mode, b.items, b.nitems); \
+  } while (0)
+  if (est) { if (na) BBC_RQ_L(true, true); else BBC_RQ_L(true, false); }
+  else { if (na) BBC_RQ_L(false, true); else BBC_RQ_L(false, false); }
+#undef BBC_RQ_L
 }
 
 // One PQ scan pass: work items (k_scan_plan), then one persistent CTA per SM over them.
