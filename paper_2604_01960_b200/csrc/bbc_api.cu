@@ -187,7 +187,8 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1) {
                 table + (size_t)cap * 13 + (size_t)ix->d * 4 + (size_t)k * 24 + 64 +
                 (size_t)((cap + kChunk - 1) / kChunk) * 8 + (size_t)(nprobe + 1) * 4;
   p.per_query += 8 + 8 + kCells * 4 + 4 + 4 + (size_t)4 * world;   // DistBuf
-  p.per_query += (size_t)nprobe * 20 + (size_t)(cap / kRrPiece) * 16;   // re-rank pieces
+  const int piece = rr_piece(ix->raw_u8 ? ix->d : 4 * ix->d);
+  p.per_query += (size_t)nprobe * 20 + (size_t)(cap / piece) * 16;      // re-rank pieces
   p.per_query += kCells;                                                 // remap
   p.fixed = 64 * 256 + (size_t)3 * (ix->nlist + 1) * 4 + 3 * 256;
   if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) {            // pair codes + inverted index
@@ -232,7 +233,7 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, 
   b.chunkj = (int*)take((size_t)nqb * ((p.cap + kChunk - 1) / kChunk) * 4);
   b.sstart = (int*)take((size_t)nqb * nprobe * 4);
   b.rmap = (uint8_t*)take((size_t)nqb * kCells);
-  b.rseg = (int4*)take((size_t)nqb * (nprobe + p.cap / kRrPiece) * 16);
+  b.rseg = (int4*)take((size_t)nqb * (nprobe + p.cap / rr_piece(ix->raw_u8 ? ix->d : 4 * ix->d)) * 16);
   b.rs_cnt = (int*)take((size_t)(ix->nlist + 1) * 4);
   b.rs_off = (int*)take((size_t)(ix->nlist + 1) * 4);
   b.rs_cur = (int*)take((size_t)(ix->nlist + 1) * 4);
@@ -645,7 +646,7 @@ void launch_rerank(Shard& s, dim3 g, cudaStream_t st, int rowb) {
 #undef BBC_RR_Q
 }
 
-// Grid: about one warp per kRrSPW pieces.  Pieces <= segments + candidates / kRrPiece, segments
+// Grid: about one warp per kRrSPW pieces.  Pieces <= segments + candidates / piece, segments
 // <= nq * nprobe; candidates are taken as 1.5x the budget (|S*| is the budget plus part of the
 // threshold bucket); the kernel strides by the grid, so an underestimate costs time, not results.
 template <bool IP, int SPW>
@@ -653,7 +654,7 @@ void launch_rerank_seg(Shard& s, cudaStream_t st, int rowb) {
   const bool u8 = s.ix->raw_u8 != 0;
   const long long nq = s.b.nq;
   const long long cand = std::min<long long>(s.p.cap, s.b.budget + s.b.budget / 2);
-  const long long pieces = nq * s.b.nprobe + nq * cand / kRrPiece;
+  const long long pieces = nq * s.b.nprobe + nq * cand / rr_piece(rowb);
   const long long per_cta = (kRrNT / 32) * SPW;
   const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((pieces + per_cta - 1) / per_cta,
                                                                            (1LL << 30) / per_cta));
@@ -689,9 +690,9 @@ void stage_rerank(Shard& s, cudaStream_t st) {
     // segments (query, first candidate, length) counted, offset and placed by list
     const unsigned gp = (unsigned)(((long long)nb * s.b.nprobe + 255) / 256);
     cudaMemsetAsync(s.b.rs_cnt, 0, (size_t)(ix->nlist + 1) * 4, st);
-    k_rr_segments<false><<<gp, 256, 0, st>>>(s.b, s.b.rs_cnt, s.b.rseg);
+    k_rr_segments<false><<<gp, 256, 0, st>>>(s.b, s.b.rs_cnt, s.b.rseg, rr_piece(rowb));
     k_inv_scan<<<1, 1024, 0, st>>>(s.b.rs_cnt, s.b.rs_off, s.b.rs_cur, ix->nlist);
-    k_rr_segments<true><<<gp, 256, 0, st>>>(s.b, s.b.rs_cur, s.b.rseg);
+    k_rr_segments<true><<<gp, 256, 0, st>>>(s.b, s.b.rs_cur, s.b.rseg, rr_piece(rowb));
     if (ip) launch_rerank_list<true>(s, st, rowb);
     else launch_rerank_list<false>(s, st, rowb);
     g_launches += 5;
