@@ -538,8 +538,8 @@ void rbq_tc_pass(Shard& s, const Batch& b, cudaStream_t st, bool sample) {
   // 3 query-tile stages of 64 pairs (A lives in tensor memory; shared memory holds B and records)
   const int nkb = (ix->D + 127) / 128;
   auto ws_smem = [&](int nst) {
-    return (size_t)nst * nkb * kRbN * 128 + (size_t)nst * kRbN * sizeof(RbqPair) + 3 * kRbM * 4 +
-           (size_t)(2 * nst + 4) * 8 + 16;
+    return (size_t)nst * nkb * kRbN * 128 + (size_t)kRbRec * kRbN * sizeof(RbqPair) + 3 * kRbM * 4 +
+           (size_t)(2 * nst + 2 * kRbRec + 4) * 8 + 16;
   };
   const int nst = 2;
   const size_t smw = ws_smem(nst);

@@ -321,6 +321,7 @@ __device__ __forceinline__ uint32_t nib_bytes(uint32_t nib) { return (nib * 0x00
 //   accf[a]  (1 commit)                 accumulator a holds tile qi's products
 //   acce[a]  (24 warps)                 accumulator a read out: free for tile qi + 2
 constexpr int kRbWsEpi = 24, kRbWsNT = (kRbWsEpi + 2) * 32;   // 832 threads
+constexpr int kRbRec = 4;                                      // records ring depth
 
 template <bool SAMPLE>
 __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqTc t, int nst,
@@ -330,14 +331,17 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
   const int nkb = (D + 127) / 128;                                // 128-byte K blocks
   const int bst = nkb * kRbN * 128;                               // bytes per B stage
   uint8_t* sB = rsm3;                                             // [nst][nkb][32 x 128 B] swizzled
-  RbqPair* pi = reinterpret_cast<RbqPair*>(sB + (size_t)nst * bst);   // [nst][kRbN]
-  float* o_r = reinterpret_cast<float*>(pi + nst * kRbN);         // [128] r_o
+  RbqPair* pi = reinterpret_cast<RbqPair*>(sB + (size_t)nst * bst);   // [kRbRec][kRbN] records ring
+  float* o_r = reinterpret_cast<float*>(pi + kRbRec * kRbN);      // [128] r_o
   float* o_g = o_r + kRbM;                                        // [128] 1 / g_o
   float* o_pc = o_g + kRbM;                                       // [128] popcount (float)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(o_pc + kRbM);      // full[nst] empty[nst] accf[2] acce[2]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * nst + 4);
+  // full[nst] empty[nst] (B stages: freed by the MMA commit alone) rfull[kRbRec] rempty[kRbRec]
+  // (records: freed by the epilogue) accf[2] acce[2]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(o_pc + kRbM);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * nst + 2 * kRbRec + 4);
   const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8u * nst;
-  const uint32_t accf0 = empty0 + 8u * nst, acce0 = accf0 + 16u;
+  const uint32_t rfull0 = empty0 + 8u * nst, rempty0 = rfull0 + 8u * kRbRec;
+  const uint32_t accf0 = rempty0 + 8u * kRbRec, acce0 = accf0 + 16u;
 
   const int2 tile = t.tiles[blockIdx.x];
   const int L = tile.x, o0 = tile.y;
@@ -350,7 +354,11 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
   if (threadIdx.x == 0) {
     for (int i = 0; i < nst; ++i) {
       mbar_init(full0 + 8u * i, 1);
-      mbar_init(empty0 + 8u * i, 1 + kRbWsEpi);
+      mbar_init(empty0 + 8u * i, 1);
+    }
+    for (int i = 0; i < kRbRec; ++i) {
+      mbar_init(rfull0 + 8u * i, 1);
+      mbar_init(rempty0 + 8u * i, kRbWsEpi);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(accf0 + 8u * a, 1);
@@ -361,13 +369,14 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
   const uint32_t rbytes = (uint32_t)(kRbN * sizeof(RbqPair));
   // copies of query tile qi into stage qi % nst (the first nst are issued before A is staged)
   auto load_tile = [&](int qi) {
-    const int st = qi % nst;
-    const uint32_t fb = full0 + 8u * st;
-    mbar_arrive_tx(fb, (uint32_t)bst + rbytes);
+    const int st = qi % nst, rs = qi % kRbRec;
+    const uint32_t fb = full0 + 8u * st, rb = rfull0 + 8u * rs;
+    mbar_arrive_tx(fb, (uint32_t)bst);
+    mbar_arrive_tx(rb, rbytes);
     const int slot = p0 + qi * kRbN;
     const uint32_t dB = smem_u32(sB + (size_t)st * bst);
     for (int kb = 0; kb < nkb; ++kb) tma_2d_g2s(dB + kb * kRbN * 128, &tmB, 128 * kb, slot, fb);
-    bulk_g2s(smem_u32(pi + st * kRbN), t.pinfo + slot, rbytes, fb);
+    bulk_g2s(smem_u32(pi + rs * kRbN), t.pinfo + slot, rbytes, rb);
   };
   if (threadIdx.x == 0)
     for (int qi = 0; qi < min(nst, ntile); ++qi) load_tile(qi);
@@ -416,6 +425,7 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
     if (lane == 0) {
       for (int qi = nst; qi < ntile; ++qi) {
         mbar_wait(empty0 + 8u * (qi % nst), (unsigned)((qi / nst - 1) & 1));
+        if (qi >= kRbRec) mbar_wait(rempty0 + 8u * (qi % kRbRec), (unsigned)((qi / kRbRec - 1) & 1));
         load_tile(qi);
       }
     }
@@ -450,10 +460,11 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
     if (r < nobj) { ro = o_r[r]; ginv = o_g[r]; pcf = o_pc[r]; }
     const float a_ro = __fmul_rn(ro, ro), ro2 = __fmul_rn(2.0f, ro);
     for (int qi = 0; qi < ntile; ++qi) {
-      const int st = qi % nst, a = qi & 1;
+      const int a = qi & 1;
       const int nqt = min(kRbN, np - qi * kRbN);
       mbar_wait(accf0 + 8u * a, (unsigned)((qi / 2) & 1));
-      mbar_wait(full0 + 8u * st, (unsigned)((qi / nst) & 1));   // records visible (landed long ago)
+      const int rs = qi % kRbRec;
+      mbar_wait(rfull0 + 8u * rs, (unsigned)((qi / kRbRec) & 1));   // records landed
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       uint32_t v[kPW];
 #pragma unroll
@@ -468,7 +479,7 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(acce0 + 8u * a);
-      const RbqPair* P = pi + st * kRbN;
+      const RbqPair* P = pi + rs * kRbN;
       if (r < nobj) {
 #pragma unroll
         for (int c = 0; c < kPW; ++c) {
@@ -498,7 +509,7 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(empty0 + 8u * st);
+      if (lane == 0) mbar_arrive(rempty0 + 8u * rs);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
