@@ -77,20 +77,19 @@ __global__ void __launch_bounds__(256, 4) k_rbq_pairs(Batch b, Dev ix, const int
     float4 qp[kMaxM4];
     float mn = INFINITY, mx = -INFINITY;
 #pragma unroll
-    for (int m = 0; m < kMaxM4; ++m) {
-      const int i = lane + 32 * m;
-      if (i < D4) {
-        const float4 w = __ldg(w4 + i);
-        const float4 uu = u4[i];
-        float4 v;                                     // q' = (u - w) / r   (r = 0: q' = 0)
-        v.x = __fmul_rn(__fsub_rn(uu.x, w.x), rinv);
-        v.y = __fmul_rn(__fsub_rn(uu.y, w.y), rinv);
-        v.z = __fmul_rn(__fsub_rn(uu.z, w.z), rinv);
-        v.w = __fmul_rn(__fsub_rn(uu.w, w.w), rinv);
-        qp[m] = v;
-        mn = fminf(mn, fminf(fminf(v.x, v.y), fminf(v.z, v.w)));
-        mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
-      }
+    for (int m = 0; m < kMaxM4; ++m) {               // slots past D4 repeat slot D4 - 1 (min/max
+      const int i = min(lane + 32 * m, D4 - 1);       // unchanged; their codes are not stored)
+      const float4 w = __ldg(w4 + i), uu = u4[i];
+      float4 v;                                       // q' = (u - w) / r   (r = 0: q' = 0)
+      v.x = __fmul_rn(__fsub_rn(uu.x, w.x), rinv);
+      v.y = __fmul_rn(__fsub_rn(uu.y, w.y), rinv);
+      v.z = __fmul_rn(__fsub_rn(uu.z, w.z), rinv);
+      v.w = __fmul_rn(__fsub_rn(uu.w, w.w), rinv);
+      qp[m] = v;
+      mn = fminf(fminf(mn, v.x), v.y);
+      mn = fminf(fminf(mn, v.z), v.w);
+      mx = fmaxf(fmaxf(mx, v.x), v.y);
+      mx = fmaxf(fmaxf(mx, v.z), v.w);
     }
     mn = warp_min(mn);
     mx = warp_max(mx);
@@ -102,19 +101,16 @@ __global__ void __launch_bounds__(256, 4) k_rbq_pairs(Batch b, Dev ix, const int
 #pragma unroll
     for (int m = 0; m < kMaxM4; ++m) {
       const int i = lane + 32 * m;
-      if (i < D4) {
-        // t = fl(fl(q' - mn) * dinv) + 0.5 >= 0; floor(t) = low bits of fl_down(t + 2^23)
-        // (spacing 1 in [2^23, 2^24)), clamped to 15 bytewise. dinv = 0 gives t = 0.5 -> 0.
-        const float f0 = __fadd_rd(__fadd_rn(__fmul_rn(__fsub_rn(qp[m].x, mn), dinv), 0.5f), 8388608.0f);
-        const float f1 = __fadd_rd(__fadd_rn(__fmul_rn(__fsub_rn(qp[m].y, mn), dinv), 0.5f), 8388608.0f);
-        const float f2 = __fadd_rd(__fadd_rn(__fmul_rn(__fsub_rn(qp[m].z, mn), dinv), 0.5f), 8388608.0f);
-        const float f3 = __fadd_rd(__fadd_rn(__fmul_rn(__fsub_rn(qp[m].w, mn), dinv), 0.5f), 8388608.0f);
-        const unsigned lo = __byte_perm(__float_as_uint(f0), __float_as_uint(f1), 0x0040);
-        const unsigned hi = __byte_perm(__float_as_uint(f2), __float_as_uint(f3), 0x0040);
-        const unsigned v4 = __vminu4(__byte_perm(lo, hi, 0x5410), 0x0F0F0F0Fu);
-        qrow[i] = v4;
-        acc = __dp4a(v4, 0x01010101u, acc);
-      }
+      // t = fl(fl(q' - mn) * dinv) + 0.5 >= 0; clamp(floor(t), 0, 15) = floor(min(t, 15)), and
+      // floor(t) = low bits of fl_down(t + 2^23) (spacing 1 in [2^23, 2^24)). dinv = 0: t = 0.5 -> 0.
+#define BBC_QB(c) __fadd_rd(fminf(__fadd_rn(__fmul_rn(__fsub_rn(qp[m].c, mn), dinv), 0.5f), 15.0f), 8388608.0f)
+      const float f0 = BBC_QB(x), f1 = BBC_QB(y), f2 = BBC_QB(z), f3 = BBC_QB(w);
+#undef BBC_QB
+      const unsigned lo = __byte_perm(__float_as_uint(f0), __float_as_uint(f1), 0x0040);
+      const unsigned hi = __byte_perm(__float_as_uint(f2), __float_as_uint(f3), 0x0040);
+      const unsigned v4 = __byte_perm(lo, hi, 0x5410);
+      if (i < D4) qrow[i] = v4;
+      acc = __dp4a(i < D4 ? v4 : 0u, 0x01010101u, acc);
     }
     int sq = (int)acc;
     sq = warp_sum(sq);
