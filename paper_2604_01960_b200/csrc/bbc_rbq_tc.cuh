@@ -63,14 +63,23 @@ __global__ void __launch_bounds__(256, 4) k_rbq_pairs(Batch b, Dev ix, const int
   __syncthreads();
   const float4* u4 = reinterpret_cast<const float4*>(su);
   const float sD = __fsqrt_rn((float)D);
+  // the warp's pairs' metadata, loaded up front by lanes 0..kPairsPerWarp-1
+  const int j0 = blockIdx.x * kPairsPerCta + wid * kPairsPerWarp;
+  int m_slot = -1, m_L = 0, m_poff = 0;
+  float m_rq2 = 0.f;
+  if (lane < kPairsPerWarp && j0 + lane < b.nprobe) {
+    const long long p = (long long)q * b.nprobe + j0 + lane;
+    m_slot = islot[p];
+    m_L = b.probe[p];
+    m_rq2 = b.rq2[p];
+    m_poff = b.poff[(size_t)q * (b.nprobe + 1) + j0 + lane];
+  }
   for (int jj = 0; jj < kPairsPerWarp; ++jj) {
-    const int j = blockIdx.x * kPairsPerCta + wid * kPairsPerWarp + jj;
-    if (j >= b.nprobe) break;
-    const long long p = (long long)q * b.nprobe + j;
-    const int slot = islot[p];
-    if (slot < 0) continue;                           // not estimated on this shard / pass
-    const int L = b.probe[p];
-    const float rq2 = b.rq2[p];
+    const int slot = __shfl_sync(0xffffffffu, m_slot, jj);
+    if (slot < 0) continue;                           // not estimated on this shard / pass (or j >= nprobe)
+    const int L = __shfl_sync(0xffffffffu, m_L, jj);
+    const float rq2 = __shfl_sync(0xffffffffu, m_rq2, jj);
+    const int poff = __shfl_sync(0xffffffffu, m_poff, jj);
     const float r = __fsqrt_rn(rq2);
     const float rinv = r > 0.f ? __fdiv_rn(1.0f, r) : 0.f;
     const float4* w4 = reinterpret_cast<const float4*>(ix.wL + (size_t)L * D);
@@ -122,7 +131,7 @@ __global__ void __launch_bounds__(256, 4) k_rbq_pairs(Batch b, Dev ix, const int
       e.r = r;
       e.rq2 = rq2;
       e.q = q;
-      e.obase = (long long)q * b.cap + b.poff[(size_t)q * (b.nprobe + 1) + j];
+      e.obase = (long long)q * b.cap + poff;
       pinfo[slot] = e;
     }
   }
