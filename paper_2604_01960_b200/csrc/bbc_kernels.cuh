@@ -430,15 +430,30 @@ __global__ void __launch_bounds__(256) k_pq_lut(Batch b, Dev ix) {
 }
 
 // RaBitQ rotated query u = P^T q: u_i = sum_{t<d} P[t][i] q_t, t ascending (canonical).
+// CTA = (256 output dims, QB queries): each P element is read once for kRotQ queries (P is
+// re-read nq / QB times from L2 instead of nq times), QB independent sums per thread.
+template <int QB>
 __global__ void __launch_bounds__(256) k_rbq_rotate(Batch b, Dev ix) {
-  extern __shared__ float sq[];
-  const int q = blockIdx.y, i = blockIdx.x * 256 + threadIdx.x;
-  for (int t = threadIdx.x; t < ix.d; t += 256) sq[t] = b.Q[(size_t)q * ix.d + t];
+  extern __shared__ __align__(16) float sq[];   // [d][QB]
+  const int q0 = blockIdx.y * QB, i = blockIdx.x * 256 + threadIdx.x;
+  for (int e = threadIdx.x; e < ix.d * QB; e += 256) {
+    const int t = e / QB, k = e % QB;
+    sq[e] = q0 + k < b.nq ? b.Q[(size_t)(q0 + k) * ix.d + t] : 0.f;
+  }
   __syncthreads();
   if (i >= ix.D) return;
-  float acc = 0.f;
-  for (int t = 0; t < ix.d; ++t) acc = __fadd_rn(acc, __fmul_rn(ix.P[(size_t)t * ix.D + i], sq[t]));
-  b.table[(size_t)q * ix.D + i] = acc;
+  float acc[QB];
+#pragma unroll
+  for (int k = 0; k < QB; ++k) acc[k] = 0.f;
+#pragma unroll 4
+  for (int t = 0; t < ix.d; ++t) {
+    const float p = ix.P[(size_t)t * ix.D + i];
+#pragma unroll
+    for (int k = 0; k < QB; ++k) acc[k] = __fadd_rn(acc[k], __fmul_rn(p, sq[t * QB + k]));
+  }
+#pragma unroll
+  for (int k = 0; k < QB; ++k)
+    if (q0 + k < b.nq) b.table[(size_t)(q0 + k) * ix.D + i] = acc[k];
 }
 
 // ------------------------------------------------------------------------------------------
