@@ -495,7 +495,8 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
           // canonical estimator, identical to k_rbq_scan
           const float t1 = __fmul_rn(e.c2, pcf);
           const float t2 = __fadd_rn(t1, e.c3);
-          const float t3 = __fmul_rn(e.c1, (float)(int)v[c]);
+          // (float)v exactly, off the conversion pipe: 0 <= v < 2^23, so 2^23 + v is exact
+          const float t3 = __fmul_rn(e.c1, __fsub_rn(__int_as_float((int)v[c] + 0x4B000000), 8388608.0f));
           const float oq = __fadd_rn(t3, t2);
           const float ee = __fmul_rn(oq, ginv);
           const float sum = __fadd_rn(a_ro, e.rq2);
@@ -504,9 +505,11 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
           if (SAMPLE) {
             b.val[at] = est;
           } else {
-            // bucket id (Eq. 6, R3), branch-free as CellFn
-            const float f = floorf(__fmul_rn(__fsub_rn(est, e.dmin), e.inv));
-            int cell = (int)fminf(fmaxf(f, 0.f), e.bmax);
+            // bucket id (Eq. 6, R3), branch-free as CellFn: clamp(floor(x), 0, bmax) =
+            // floor(clamp(x, 0, bmax)) (integer bounds; NaN -> 0), floor of y in [0, 255] = low
+            // byte of fl_down(y + 2^23) -- no conversion-pipe instructions
+            const float y = fminf(fmaxf(__fmul_rn(__fsub_rn(est, e.dmin), e.inv), 0.f), e.bmax);
+            int cell = __float_as_int(__fadd_rd(y, 8388608.0f)) & 0xFF;
             cell = e.degen ? 0 : cell;
             cell = est > e.dmax ? 255 : cell;
             b.cells[at] = (uint8_t)cell;
