@@ -471,10 +471,12 @@ struct CellFn {
     inv = degen ? 0.f : __fdiv_rn((float)nb, w);
     if (!degen && isinf(inv)) degen = true;
   }
-  // branch-free: clamp(floor((x - dmin) * inv), 0, bmax); 0 if degenerate; 255 beyond dmax
+  // branch-free: clamp(floor((x - dmin) * inv), 0, bmax); 0 if degenerate; 255 beyond dmax.
+  // clamp(floor(f), 0, bmax) = floor(clamp(f, 0, bmax)) (integer bounds; NaN -> 0), and floor of
+  // y in [0, 255] is the low byte of fl_down(y + 2^23): no conversion-pipe instructions.
   __device__ __forceinline__ int operator()(float x) const {
-    const float f = floorf(__fmul_rn(__fsub_rn(x, dmin), inv));
-    int c = (int)fminf(fmaxf(f, 0.f), bmax);
+    const float y = fminf(fmaxf(__fmul_rn(__fsub_rn(x, dmin), inv), 0.f), bmax);
+    int c = __float_as_int(__fadd_rd(y, 8388608.0f)) & 0xFF;
     c = degen ? 0 : c;
     return x > dmax ? 255 : c;
   }
