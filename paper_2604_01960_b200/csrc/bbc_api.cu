@@ -513,10 +513,10 @@ void stage_tables(Shard& s, cudaStream_t st) {
       g_launches += 1;
     }
   } else if ((size_t)ix->d * 4 * 8 <= 48 * 1024) {
-    k_rbq_rotate<8><<<dim3((ix->D + 255) / 256, (s.b.nq + 7) / 8), 256, (size_t)ix->d * 4 * 8, st>>>(s.b, s.dv);
+    k_rbq_rotate<8><<<dim3((ix->D + kRotNT - 1) / kRotNT, (s.b.nq + 7) / 8), kRotNT, (size_t)ix->d * 4 * 8, st>>>(s.b, s.dv);
   } else {
     set_smem(k_rbq_rotate<1>, (size_t)ix->d * 4);
-    k_rbq_rotate<1><<<dim3((ix->D + 255) / 256, s.b.nq), 256, (size_t)ix->d * 4, st>>>(s.b, s.dv);
+    k_rbq_rotate<1><<<dim3((ix->D + kRotNT - 1) / kRotNT, s.b.nq), kRotNT, (size_t)ix->d * 4, st>>>(s.b, s.dv);
   }
   g_launches += 1;
   if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) rbq_pairs(s, s.b, st);

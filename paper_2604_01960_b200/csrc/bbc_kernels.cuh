@@ -430,13 +430,14 @@ __global__ void __launch_bounds__(256) k_pq_lut(Batch b, Dev ix) {
 }
 
 // RaBitQ rotated query u = P^T q: u_i = sum_{t<d} P[t][i] q_t, t ascending (canonical).
-// CTA = (256 output dims, QB queries): each P element is read once for kRotQ queries (P is
+// CTA = (kRotNT output dims, QB queries): each P element is read once for QB queries (P is
 // re-read nq / QB times from L2 instead of nq times), QB independent sums per thread.
+constexpr int kRotNT = 128;   // output dims per CTA (1000 queries, D = 960: 1000 CTAs)
 template <int QB>
-__global__ void __launch_bounds__(256) k_rbq_rotate(Batch b, Dev ix) {
+__global__ void __launch_bounds__(kRotNT) k_rbq_rotate(Batch b, Dev ix) {
   extern __shared__ __align__(16) float sq[];   // [d][QB]
-  const int q0 = blockIdx.y * QB, i = blockIdx.x * 256 + threadIdx.x;
-  for (int e = threadIdx.x; e < ix.d * QB; e += 256) {
+  const int q0 = blockIdx.y * QB, i = blockIdx.x * kRotNT + threadIdx.x;
+  for (int e = threadIdx.x; e < ix.d * QB; e += kRotNT) {
     const int t = e / QB, k = e % QB;
     sq[e] = q0 + k < b.nq ? b.Q[(size_t)(q0 + k) * ix.d + t] : 0.f;
   }
@@ -445,9 +446,27 @@ __global__ void __launch_bounds__(256) k_rbq_rotate(Batch b, Dev ix) {
   float acc[QB];
 #pragma unroll
   for (int k = 0; k < QB; ++k) acc[k] = 0.f;
-#pragma unroll 4
-  for (int t = 0; t < ix.d; ++t) {
-    const float p = ix.P[(size_t)t * ix.D + i];
+  // P column i in blocks of 16 rows, the next block's loads issued before this block's sums
+  constexpr int kB = 16;
+  const float* Pi = ix.P + i;
+  const int nfull = ix.d / kB;
+  float pc[kB], pn[kB];
+#pragma unroll
+  for (int u = 0; u < kB; ++u) pc[u] = nfull > 0 ? __ldg(Pi + (size_t)u * ix.D) : 0.f;
+  for (int blk = 0; blk < nfull; ++blk) {
+    const int t0 = blk * kB;
+#pragma unroll
+    for (int u = 0; u < kB; ++u)
+      pn[u] = blk + 1 < nfull ? __ldg(Pi + (size_t)(t0 + kB + u) * ix.D) : 0.f;
+#pragma unroll
+    for (int u = 0; u < kB; ++u)
+#pragma unroll
+      for (int k = 0; k < QB; ++k) acc[k] = __fadd_rn(acc[k], __fmul_rn(pc[u], sq[(t0 + u) * QB + k]));
+#pragma unroll
+    for (int u = 0; u < kB; ++u) pc[u] = pn[u];
+  }
+  for (int t = nfull * kB; t < ix.d; ++t) {
+    const float p = __ldg(Pi + (size_t)t * ix.D);
 #pragma unroll
     for (int k = 0; k < QB; ++k) acc[k] = __fadd_rn(acc[k], __fmul_rn(p, sq[t * QB + k]));
   }
