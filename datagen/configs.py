@@ -83,6 +83,10 @@ SMALL = {
                            budget=900, kmeans_iters=6),
     "C3d64s": C3.replace(name="C3d64s", d=64, N=30_000, nlist=96, nq=8, k=300, nprobe=12,
                          budget=900, kmeans_iters=6),
+    # d = 200: D = 256 with 56 zero-padded dimensions, d not a multiple of the rotation's 16-row
+    # P blocks, 11 queries (the rotation's last CTA holds 3 of its 8)
+    "C3d200s": C3.replace(name="C3d200s", d=200, N=20_000, nlist=64, nq=11, k=300, nprobe=10,
+                          budget=900, kmeans_iters=6),
     # fine lists (~20 objects): a compaction chunk of 8,192 objects spans > 256 lists, the
     # global-search path of k_emit; probe sets of 600 lists
     "C2f": C2.replace(name="C2f", N=40_000, nlist=2_048, nq=8, k=500, nprobe=600, budget=1_000,
