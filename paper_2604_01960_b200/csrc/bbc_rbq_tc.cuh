@@ -49,7 +49,7 @@ static_assert(sizeof(RbqPair) == 64, "four 16-byte copies per pair");
 // ------------------------------------------------------------------ per-pair query codes
 // CTA = (query, 32 consecutive probes): the query's rotated vector u is staged once in shared
 // memory; each warp computes 4 pairs (lane holds dims 4 (lane + 32 m) .. +3 of q').
-constexpr int kPairsPerWarp = 4, kPairsPerCta = 8 * kPairsPerWarp;
+constexpr int kPairsPerWarp = 8, kPairsPerCta = 8 * kPairsPerWarp;
 __global__ void __launch_bounds__(256, 4) k_rbq_pairs(Batch b, Dev ix, const int* __restrict__ islot,
                                                    uint8_t* __restrict__ qbar, RbqPair* __restrict__ pinfo) {
   extern __shared__ __align__(16) float su[];          // [D]
