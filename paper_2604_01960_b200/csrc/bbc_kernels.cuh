@@ -204,6 +204,45 @@ __device__ __forceinline__ void bitonic_sort_keys(uint64_t* keys, int P2) {
     __syncthreads();
     return;
   }
+  if (P2 == 2 * kSelNT) {
+    // two adjacent keys per thread (elements 2t, 2t + 1): stride 1 inside the thread, strides
+    // 2..32 by shuffles with thread t ^ (stride / 2), larger strides through shared memory
+    const int t = threadIdx.x;
+    __syncthreads();
+    uint64_t v0 = keys[2 * t], v1 = keys[2 * t + 1];
+    for (int size = 2; size <= P2; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        const bool up = ((2 * t) & size) == 0;
+        if (stride == 1) {
+          const uint64_t lo = v0 < v1 ? v0 : v1, hi = v0 < v1 ? v1 : v0;
+          v0 = up ? lo : hi;
+          v1 = up ? hi : lo;
+          continue;
+        }
+        const int h = stride >> 1;                    // partner thread distance
+        uint64_t o0, o1;
+        if (h >= 32) {
+          __syncthreads();
+          keys[2 * t] = v0;
+          keys[2 * t + 1] = v1;
+          __syncthreads();
+          o0 = keys[2 * (t ^ h)];
+          o1 = keys[2 * (t ^ h) + 1];
+        } else {
+          o0 = __shfl_xor_sync(0xffffffffu, v0, h);
+          o1 = __shfl_xor_sync(0xffffffffu, v1, h);
+        }
+        const bool keepmin = (((2 * t) & stride) == 0) == up;
+        v0 = keepmin ? (o0 < v0 ? o0 : v0) : (o0 > v0 ? o0 : v0);
+        v1 = keepmin ? (o1 < v1 ? o1 : v1) : (o1 > v1 ? o1 : v1);
+      }
+    }
+    __syncthreads();
+    keys[2 * t] = v0;
+    keys[2 * t + 1] = v1;
+    __syncthreads();
+    return;
+  }
   for (int size = 2; size <= P2; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       for (int i = threadIdx.x; i < P2 / 2; i += kSelNT) {

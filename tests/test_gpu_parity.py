@@ -98,6 +98,14 @@ def test_parity_config_point(name):
     compare(cfg, ix, Q, g, cfg.k, cfg.nprobe, cfg.budget)
 
 
+@pytest.mark.parametrize("nprobe", [1025, 1500, 2048])
+def test_parity_probe_sets_past_1024(nprobe):
+    """Probe sets of 1,025-2,048 lists (C3's operating point has 2,048): the probe selection's
+    two-keys-per-thread sort, and every list probed at 2,048."""
+    cfg, ix, Q, g = gpu_index("C2f")
+    compare(cfg, ix, Q[:4], g, cfg.k, nprobe, cfg.budget)
+
+
 @pytest.mark.parametrize("name", ["C1t", "C2s", "C3s", "C4ip_s", "C2q4s"])
 def test_parity_parameter_grid(name):
     cfg, ix, Q, g = gpu_index(name)
