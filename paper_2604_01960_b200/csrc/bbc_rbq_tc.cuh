@@ -47,8 +47,9 @@ static_assert(sizeof(RbqPair) == 64, "four 16-byte copies per pair");
 
 
 // ------------------------------------------------------------------ per-pair query codes
-// CTA = (query, 32 consecutive probes): the query's rotated vector u is staged once in shared
-// memory; each warp computes 4 pairs (lane holds dims 4 (lane + 32 m) .. +3 of q').
+// CTA = (query, kPairsPerCta consecutive probes): the query's rotated vector u is staged once in
+// shared memory; each warp computes kPairsPerWarp pairs (lane holds dims 4 (lane + 32 m) .. +3 of
+// q'), their metadata loaded up front by lanes 0..kPairsPerWarp-1.
 constexpr int kPairsPerWarp = 8, kPairsPerCta = 8 * kPairsPerWarp;
 __global__ void __launch_bounds__(256, 4) k_rbq_pairs(Batch b, Dev ix, const int* __restrict__ islot,
                                                    uint8_t* __restrict__ qbar, RbqPair* __restrict__ pinfo) {
