@@ -87,6 +87,15 @@ SMALL = {
     # P blocks, 11 queries (the rotation's last CTA holds 3 of its 8)
     "C3d200s": C3.replace(name="C3d200s", d=200, N=20_000, nlist=64, nq=11, k=300, nprobe=10,
                           budget=900, kmeans_iters=6),
+    # RaBitQ tensor-core GEMM beyond one query tile per list: every query probes (nearly) every
+    # list, so each list's Push pass runs >= 5 query tiles of kRbN = 96 pairs (both TMEM
+    # accumulators, the B-stage ring and the 4-deep records ring wrap; the producer loop runs),
+    # the sample pass >= 2.  D = 128 keeps the oracle fast; C3mt960 repeats it at C3's D = 960
+    # (8 K blocks per B stage).
+    "C3mt": C3.replace(name="C3mt", d=128, N=24_000, nlist=16, nq=480, k=300, nprobe=14,
+                       budget=900, kmeans_iters=6),
+    "C3mt960": C3.replace(name="C3mt960", N=8_000, nlist=8, nq=400, k=200, nprobe=8, budget=600,
+                          kmeans_iters=6),
     # fine lists (~20 objects): a compaction chunk of 8,192 objects spans > 256 lists, the
     # global-search path of k_emit; probe sets of 600 lists
     "C2f": C2.replace(name="C2f", N=40_000, nlist=2_048, nq=8, k=500, nprobe=600, budget=1_000,

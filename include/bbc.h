@@ -165,6 +165,20 @@ bbc_status bbc_set_scan_mode(bbc_index index, int32_t mode);
 bbc_status bbc_set_rerank_order(bbc_index index, int32_t order);
 
 /*
+ * bbc_set_code_loads -- the L1 policy of the 8-bit PQ scan's 16-byte code loads (step a4).  Same
+ * results in every mode; only the cache behaviour differs.
+ *   BBC_CODES_CACHED : ld.global.nc through L1 (best when the codes are L2-resident).
+ *   BBC_CODES_STREAM : ld.global.nc.L1::no_allocate (codes streamed once from HBM only evict L1).
+ *   BBC_CODES_AUTO   : (default) STREAM when this shard's codes exceed half of the L2 size the
+ *                      device reports (cudaDevAttrL2CacheSize), CACHED otherwise.
+ * BBC_ERR_ARG for a null index or an unknown mode.  Must not change while a search is in flight.
+ */
+#define BBC_CODES_AUTO 0
+#define BBC_CODES_CACHED 1
+#define BBC_CODES_STREAM 2
+bbc_status bbc_set_code_loads(bbc_index index, int32_t mode);
+
+/*
  * bbc_workspace_size -- bytes of device workspace bbc_search needs for (nq, k, nprobe, budget).
  * The workspace holds per-query scratch sized for the nprobe largest lists (cell ids, candidate
  * rows and distances) plus query/output staging used by bbc_search_host.  Queries are processed

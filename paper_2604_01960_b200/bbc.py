@@ -24,7 +24,7 @@ EXPORTS = ("ivf_load", "ivf_free", "bbc_index_info", "bbc_workspace_size", "bbc_
            "bbc_last_stats", "bbc_launch_count", "bbc_last_error", "bbc_nccl_unique_id",
            "bbc_comm_init", "bbc_search_group", "bbc_last_stats2", "bbc_set_probe_mode",
            "bbc_set_scan_mode", "bbc_stats_vector", "bbc_set_buckets", "bbc_set_rerank_order",
-           "bbc_measure_l2_read", "bbc_set_remap")
+           "bbc_measure_l2_read", "bbc_set_remap", "bbc_set_code_loads")
 
 STAGES = ("probe", "tables", "sample", "scan", "compact", "rerank", "select", "comm")
 TAU_INF = 1 << 30
@@ -86,6 +86,7 @@ def lib() -> ctypes.CDLL:
         L.bbc_set_buckets.argtypes = [vp, i32]
         L.bbc_set_rerank_order.argtypes = [vp, i32]
         L.bbc_set_remap.argtypes = [vp, i32]
+        L.bbc_set_code_loads.argtypes = [vp, i32]
         L.bbc_measure_l2_read.argtypes = [i32, ctypes.c_size_t, i32, ctypes.POINTER(ctypes.c_double)]
         L.bbc_stats_vector.argtypes = [vp, ctypes.POINTER(i64), i32]
         L.bbc_get_timing.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int,
@@ -103,7 +104,8 @@ def lib() -> ctypes.CDLL:
                    "bbc_last_stats", "bbc_query_capacity", "bbc_nccl_unique_id",
                    "bbc_comm_init", "bbc_search_group", "bbc_last_stats2", "bbc_set_probe_mode",
                    "bbc_set_scan_mode", "bbc_stats_vector", "bbc_set_buckets",
-                   "bbc_set_rerank_order", "bbc_measure_l2_read", "bbc_set_remap"):
+                   "bbc_set_rerank_order", "bbc_measure_l2_read", "bbc_set_remap",
+                   "bbc_set_code_loads"):
             getattr(L, fn).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -139,15 +141,46 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def _check_queries(q, d: int, device: int) -> None:
+    """The C ABI takes no d: a query matrix of the wrong shape or device would be read past its
+    end, so the binding checks it (2-D, d columns, fp32, contiguous, on the index's device)."""
+    torch = _torch()
+    if not (isinstance(q, torch.Tensor) and q.is_cuda and q.dtype == torch.float32
+            and q.is_contiguous() and q.ndim == 2 and q.shape[1] == d and q.device.index == device):
+        raise BBCError(f"queries must be a contiguous cuda:{device} float32 tensor [nq, {d}]")
+
+
+def _check_out(out, nq: int, k: int, device=None) -> None:
+    """Caller-supplied outputs: (ids int64 [nq, k], d2 float32 [nq, k]), contiguous, on the device
+    (device None: host numpy arrays)."""
+    ids, d2 = out
+    if device is None:
+        ok = (isinstance(ids, np.ndarray) and isinstance(d2, np.ndarray) and ids.dtype == np.int64
+              and d2.dtype == np.float32 and ids.shape == (nq, k) and d2.shape == (nq, k)
+              and ids.flags.c_contiguous and d2.flags.c_contiguous)
+    else:
+        torch = _torch()
+        ok = (ids.dtype == torch.int64 and d2.dtype == torch.float32
+              and tuple(ids.shape) == (nq, k) and tuple(d2.shape) == (nq, k)
+              and ids.is_contiguous() and d2.is_contiguous() and ids.is_cuda and d2.is_cuda
+              and ids.device.index == device and d2.device.index == device)
+    if not ok:
+        raise BBCError(f"out must be (int64 [{nq}, {k}], float32 [{nq}, {k}]) contiguous "
+                       + ("host arrays" if device is None else f"cuda:{device} tensors"))
+
+
 def search_group(shards, q, k: int, nprobe: int, budget: int, out=None, stream=None):
     """Sharded search over shards (Index objects loaded with rank i, world len(shards)) held by
     this process on one device: exchange steps are device reductions (bbc_search_group)."""
     torch = _torch()
     nq = q.shape[0]
     G = len(shards)
+    for s in shards:
+        _check_queries(q, s.info.d, s.device)
     if out is None:
         out = (torch.empty((nq, k), dtype=torch.int64, device=q.device),
                torch.empty((nq, k), dtype=torch.float32, device=q.device))
+    _check_out(out, nq, k, shards[0].device)
     wss = [s.workspace(nq, k, nprobe, budget) for s in shards]
     hs = (ctypes.c_void_p * G)(*[s._h.value for s in shards])
     wp = (ctypes.c_void_p * G)(*[w.data_ptr() for w in wss])
@@ -210,11 +243,12 @@ class Index:
     def search(self, q, k: int, nprobe: int, budget: int, out=None, workspace=None, stream=None):
         """q: cuda fp32 [nq, d] -> (ids int64 [nq, k], d2 fp32 [nq, k]) on the same device."""
         torch = _torch()
-        assert q.is_cuda and q.dtype == torch.float32 and q.is_contiguous()
+        _check_queries(q, self.info.d, self.device)
         nq = q.shape[0]
         if out is None:
             out = (torch.empty((nq, k), dtype=torch.int64, device=q.device),
                    torch.empty((nq, k), dtype=torch.float32, device=q.device))
+        _check_out(out, nq, k, self.device)
         ws = self.workspace(nq, k, nprobe, budget) if workspace is None else workspace
         st = torch.cuda.current_stream(q.device).cuda_stream if stream is None else stream
         _check(lib().bbc_search(self._h, q.data_ptr(), nq, k, nprobe, budget, out[0].data_ptr(),
@@ -226,9 +260,12 @@ class Index:
         """Host arrays in and out (bbc_search_host); pinned numpy views are fastest."""
         torch = _torch()
         q = np.ascontiguousarray(q, dtype=np.float32)
+        if q.ndim != 2 or q.shape[1] != self.info.d:
+            raise BBCError(f"queries must be [nq, {self.info.d}]")
         nq = q.shape[0]
         if out is None:
             out = (np.empty((nq, k), dtype=np.int64), np.empty((nq, k), dtype=np.float32))
+        _check_out(out, nq, k)
         ws = self.workspace(nq, k, nprobe, budget) if workspace is None else workspace
         st = torch.cuda.current_stream(self.device).cuda_stream if stream is None else stream
         _check(lib().bbc_search_host(self._h, q.ctypes.data, nq, k, nprobe, budget,
@@ -236,13 +273,18 @@ class Index:
                                      ws.numel(), st))
         return out
 
-    def search_debug(self, q, k: int, nprobe: int, budget: int, want_est: bool = False):
-        """Search plus every intermediate (parity tests).  Returns (ids, d2, dict of tensors)."""
+    def search_debug(self, q, k: int, nprobe: int, budget: int, want_est: bool = False,
+                     cand_stride: int | None = None):
+        """Search plus every intermediate (parity tests).  Returns (ids, d2, dict of tensors).
+        cand_stride: per-query capacity of the candidate buffers (default: the probed-object
+        capacity; candidates past it are not copied, n_cand still counts them)."""
         torch = _torch()
+        _check_queries(q, self.info.d, self.device)
         nq = q.shape[0]
         dev = q.device
-        ws = self.workspace(nq, k, nprobe, budget)
+        ws = self.workspace(nq, k, nprobe, budget, max_bytes=1 << 62)
         cap = int(self.cap(nprobe))
+        cs = cap if cand_stride is None else int(cand_stride)
         t = dict(
             probe=torch.empty((nq, nprobe), dtype=torch.int32, device=dev),
             rq2=torch.empty((nq, nprobe), dtype=torch.float32, device=dev),
@@ -252,8 +294,8 @@ class Index:
             tau=torch.empty(nq, dtype=torch.int32, device=dev),
             n_probed=torch.empty(nq, dtype=torch.int32, device=dev),
             n_cand=torch.empty(nq, dtype=torch.int32, device=dev),
-            cand_ids=torch.full((nq, cap), -1, dtype=torch.int64, device=dev),
-            cand_d2=torch.empty((nq, cap), dtype=torch.float32, device=dev),
+            cand_ids=torch.full((nq, cs), -1, dtype=torch.int64, device=dev),
+            cand_d2=torch.empty((nq, cs), dtype=torch.float32, device=dev),
         )
         if want_est:
             t["est"] = torch.empty((nq, cap), dtype=torch.float32, device=dev)
@@ -261,7 +303,7 @@ class Index:
                        t["edges"].data_ptr(), t["hist"].data_ptr(), t["tau"].data_ptr(),
                        t["n_probed"].data_ptr(), t["est"].data_ptr() if want_est else None, cap,
                        t["n_cand"].data_ptr(), t["cand_ids"].data_ptr(), t["cand_d2"].data_ptr(),
-                       cap)
+                       cs)
         ids = torch.empty((nq, k), dtype=torch.int64, device=dev)
         d2 = torch.empty((nq, k), dtype=torch.float32, device=dev)
         st = torch.cuda.current_stream(dev).cuda_stream
@@ -306,6 +348,14 @@ class Index:
         """m equal-depth buckets from the sample (the paper's n_ew -> m remap, reading R6); 0
         (default) keeps the equal-width cells as the buckets."""
         _check(lib().bbc_set_remap(self._h, int(m)))
+
+    CODES_AUTO, CODES_CACHED, CODES_STREAM = 0, 1, 2
+
+    def set_code_loads(self, mode: int) -> None:
+        """L1 policy of the 8-bit PQ scan's code loads: cached (CODES_CACHED), streamed past L1
+        (CODES_STREAM) or chosen from the codes' size against the L2 size (CODES_AUTO, default).
+        Same results in every mode."""
+        _check(lib().bbc_set_code_loads(self._h, int(mode)))
 
     RERANK_QUERY, RERANK_LIST, RERANK_AUTO = 0, 1, 2
 

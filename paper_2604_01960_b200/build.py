@@ -1,6 +1,7 @@
 """Build libbbc.so in-tree with nvcc for sm_100a (the C-ABI library of include/bbc.h)."""
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
@@ -9,8 +10,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libbbc.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in ("bbc_api.cu",)]
-DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("bbc_kernels.cuh", "bbc_device.cuh",
-                                                          "bbc_dist.cuh")] + [
+# every header the library includes: an edit to any of them rebuilds it (stale())
+DEPS = SOURCES + sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [
     os.path.join(ROOT, "include", "bbc.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

@@ -76,6 +76,7 @@ struct bbc_index_s {
   int rbq_tc = 0;                       // 1: RaBitQ estimates on the tensor cores (bbc_rbq_tc.cuh)
   int rerank_order = BBC_RERANK_AUTO;    // BBC_RERANK_*: work order of the exact re-rank (a7)
   int remap_m = 0;                       // 0 or m equal-depth buckets (bbc_set_remap)
+  int code_loads = BBC_CODES_AUTO;       // BBC_CODES_*: L1 policy of the PQ scan's code loads
   int2* rbq_tiles = nullptr;            // [rbq_ntiles] (list, first object) of 128-object tiles
   int rbq_ntiles = 0;
   int* rbq_pc = nullptr;                // [n_local] popcount of each code
@@ -90,6 +91,7 @@ struct bbc_index_s {
   int num_sms = 148;
   int l2_bytes = 126 << 20;
   void* nccl = nullptr;                 // ncclComm_t of this rank (bbc_comm_init)
+  long long* nccl_scratch = nullptr;    // [1] device scalar of the host-value agreement
   int force_dist = 0;                   // run the sharded code path even at world 1 (tests)
   cudaStream_t copy_stream = nullptr;   // host path: device->host result copies
   cudaEvent_t ev_done[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
@@ -157,12 +159,12 @@ struct StageScope {
 };
 
 struct RbqBufs {
-  uint8_t* qbar = nullptr;     // [slots x D] 32-slot tiles in the MMA operand layout
+  uint8_t* qbar = nullptr;     // [slots x D] query codes, row-major (TMA loads kRbN-slot tiles)
   RbqPair* pinfo = nullptr;    // [slots]
   int* islot = nullptr;        // [nq x nprobe] slot of each pair (-1: not estimated)
   int* cnt_m = nullptr;        // [nlist + 1] pairs per list
   int* cnt_s = nullptr;        // [nlist + 1] sample pairs per list
-  int* off = nullptr;          // [nlist + 1] first slot per list (multiple of 32)
+  int* off = nullptr;          // [nlist + 1] first slot per list (multiple of kRbN)
   int* cur_s = nullptr;        // [nlist + 1] fill cursors
   int* cur_m = nullptr;
 };
@@ -199,8 +201,11 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1) {
   return p;
 }
 
-// Carve the micro-batch arrays out of the workspace.
-void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, Batch& b,
+// Carve the micro-batch arrays out of the workspace.  The query and output staging buffers come
+// first, sized for the largest micro-batch (nqmax), so they sit at the same offsets in every
+// micro-batch of a search: the host path's device->host copy of micro-batch i (copy stream) may
+// still read its output buffer while micro-batch i+1 (possibly smaller: the tail halves) runs.
+void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nqmax, int nprobe, char* ws, Batch& b,
            float** qstage, long long** ostage_ids, float** ostage_d2, int k, DistBuf* db, int world,
            RbqBufs* rb) {
   size_t off = 0;
@@ -209,6 +214,11 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, 
     off = align256(off + bytes);
     return r;
   };
+  *qstage = (float*)take((size_t)nqmax * ix->d * 4);
+  *ostage_ids = (long long*)take((size_t)nqmax * k * 8);
+  *ostage_d2 = (float*)take((size_t)nqmax * k * 4);
+  b.ostage2_ids = (long long*)take((size_t)nqmax * k * 8);   // second output staging (host path)
+  b.ostage2_d2 = (float*)take((size_t)nqmax * k * 4);
   size_t table = ix->kind == BBC_KIND_PQ ? (size_t)ix->M * 256 : (size_t)ix->D;
   b.coarse = (float*)take((size_t)nqb * ix->nlist * 4);
   b.probe = (int*)take((size_t)nqb * nprobe * 4);
@@ -238,11 +248,6 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nprobe, char* ws, 
   b.rs_off = (int*)take((size_t)(ix->nlist + 1) * 4);
   b.rs_cur = (int*)take((size_t)(ix->nlist + 1) * 4);
 
-  *qstage = (float*)take((size_t)nqb * ix->d * 4);
-  *ostage_ids = (long long*)take((size_t)nqb * k * 8);
-  *ostage_d2 = (float*)take((size_t)nqb * k * 4);
-  b.ostage2_ids = (long long*)take((size_t)nqb * k * 8);   // second output staging (host path)
-  b.ostage2_d2 = (float*)take((size_t)nqb * k * 4);
   db->prefix = (unsigned long long*)take((size_t)nqb * 8);
   db->need = (long long*)take((size_t)nqb * 8);
   db->dh = (int*)take((size_t)nqb * kCells * 4);
@@ -286,9 +291,7 @@ __global__ void k_debug_cands(const int* cpos, const float* val, const int* ncan
 
 template <int M>
 void launch_rq(bool est, int grid, cudaStream_t st, const Batch& b, const Dev& dv,
-               const uint8_t* ct, const long long* tb, float* out, long long stride, int mode) {
-  // codes that do not fit in L2 are streamed past L1 (see k_pq_scan_rq)
-  const bool na = (double)dv.n_local * M > 0.5 * (126 << 20);
+               const uint8_t* ct, const long long* tb, float* out, long long stride, int mode, bool na) {
 #define BBC_RQ_L(E, NA)                                                                                  \
   do {                                                                                                  \
     set_smem(k_pq_scan_rq<M, E, NA>, kRqSmem);                                                          \
@@ -300,18 +303,20 @@ void launch_rq(bool est, int grid, cudaStream_t st, const Batch& b, const Dev& d
 }
 
 // One PQ scan pass: work items (k_scan_plan), then one persistent CTA per SM over them.
+// na: code loads bypass L1 allocation (codes larger than half of L2, or forced by
+// bbc_set_code_loads).
 void rq_scan(int M, bool est, int num_sms, cudaStream_t st, const Batch& b, const Dev& dv,
-             const uint8_t* ct, const long long* tb, float* out, long long stride, int mode) {
+             const uint8_t* ct, const long long* tb, float* out, long long stride, int mode, bool na) {
   if (b.nq <= 0) return;
   k_scan_plan<<<1, 1024, 0, st>>>(b, mode, b.items, b.nitems);
   g_launches += 1;
   switch (M) {
-    case 8: launch_rq<8>(est, num_sms, st, b, dv, ct, tb, out, stride, mode); break;
-    case 16: launch_rq<16>(est, num_sms, st, b, dv, ct, tb, out, stride, mode); break;
-    case 24: launch_rq<24>(est, num_sms, st, b, dv, ct, tb, out, stride, mode); break;
-    case 32: launch_rq<32>(est, num_sms, st, b, dv, ct, tb, out, stride, mode); break;
-    case 48: launch_rq<48>(est, num_sms, st, b, dv, ct, tb, out, stride, mode); break;
-    case 64: launch_rq<64>(est, num_sms, st, b, dv, ct, tb, out, stride, mode); break;
+    case 8: launch_rq<8>(est, num_sms, st, b, dv, ct, tb, out, stride, mode, na); break;
+    case 16: launch_rq<16>(est, num_sms, st, b, dv, ct, tb, out, stride, mode, na); break;
+    case 24: launch_rq<24>(est, num_sms, st, b, dv, ct, tb, out, stride, mode, na); break;
+    case 32: launch_rq<32>(est, num_sms, st, b, dv, ct, tb, out, stride, mode, na); break;
+    case 48: launch_rq<48>(est, num_sms, st, b, dv, ct, tb, out, stride, mode, na); break;
+    case 64: launch_rq<64>(est, num_sms, st, b, dv, ct, tb, out, stride, mode, na); break;
   }
 }
 
@@ -342,8 +347,14 @@ void q4_scan(int M, bool est, int num_sms, cudaStream_t st, const Batch& b, cons
 // PQ scan pass of either code width
 void pq_scan(const bbc_index_s* ix, bool est, cudaStream_t st, const Batch& b, const Dev& dv, float* out,
              long long stride, int mode) {
-  if (ix->nbits == 4) q4_scan(ix->M, est, ix->num_sms, st, b, dv, ix->codes_t, ix->tbase, out, stride, mode);
-  else rq_scan(ix->M, est, ix->num_sms, st, b, dv, ix->codes_t, ix->tbase, out, stride, mode);
+  if (ix->nbits == 4) {
+    q4_scan(ix->M, est, ix->num_sms, st, b, dv, ix->codes_t, ix->tbase, out, stride, mode);
+    return;
+  }
+  // codes that do not fit in L2 are streamed past L1 (see k_pq_scan_rq); L2 size queried at load
+  const bool na = ix->code_loads == BBC_CODES_STREAM ||
+                  (ix->code_loads == BBC_CODES_AUTO && (double)ix->n_local * ix->M > 0.5 * (double)ix->l2_bytes);
+  rq_scan(ix->M, est, ix->num_sms, st, b, dv, ix->codes_t, ix->tbase, out, stride, mode, na);
 }
 
 bbc_status check_args(bbc_index ix, const void* q, int64_t nq, int32_t k, int32_t nprobe,
@@ -371,6 +382,9 @@ struct Comm {
   virtual ~Comm() {}
   virtual int world() const = 0;
   virtual bool allreduce(const std::vector<void*>& bufs, size_t n, Dt dt, Op op, cudaStream_t st) = 0;
+  // host value -> its minimum over the processes of the communicator (synchronises `st`); the
+  // shards of one process already agree
+  virtual bool agree_min(long long* v, cudaStream_t st) { (void)v; (void)st; return true; }
 };
 
 struct GroupComm : Comm {
@@ -397,12 +411,20 @@ struct GroupComm : Comm {
 struct NcclComm : Comm {
   ncclComm_t c;
   int W;
-  NcclComm(ncclComm_t comm, int w) : c(comm), W(w) {}
+  long long* scratch;                 // one device int64 (bbc_comm_init)
+  NcclComm(ncclComm_t comm, int w, long long* sc) : c(comm), W(w), scratch(sc) {}
   int world() const override { return W; }
   bool allreduce(const std::vector<void*>& bufs, size_t n, Dt dt, Op op, cudaStream_t st) override {
     if (n == 0) return true;
     ncclDataType_t t = dt == Dt::I32 ? ncclInt32 : dt == Dt::U32 ? ncclUint32 : dt == Dt::I64 ? ncclInt64 : ncclFloat32;
     return ncclAllReduce(bufs[0], bufs[0], n, t, op == Op::Sum ? ncclSum : ncclMin, c, st) == ncclSuccess;
+  }
+  bool agree_min(long long* v, cudaStream_t st) override {
+    if (W == 1) return true;
+    return cudaMemcpyAsync(scratch, v, 8, cudaMemcpyHostToDevice, st) == cudaSuccess &&
+           ncclAllReduce(scratch, scratch, 1, ncclInt64, ncclMin, c, st) == ncclSuccess &&
+           cudaMemcpyAsync(v, scratch, 8, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+           cudaStreamSynchronize(st) == cudaSuccess;
   }
 };
 
@@ -486,7 +508,8 @@ bool encode_tmap(CUtensorMap* m, const void* base, CUtensorMapDataType dt, uint3
 }
 
 // RaBitQ tensor-core path, after the probe: the pair layout (slots grouped by list, sample pairs
-// first, lists padded to 32) and every estimated pair's query code + record at its slot.
+// first, each list's slot range padded to a multiple of kRbN) and every estimated pair's query
+// code + record at its slot.
 void rbq_pairs(Shard& s, const Batch& b, cudaStream_t st) {
   bbc_index_s* ix = s.ix;
   const long long pairs = (long long)b.nq * b.nprobe;
@@ -539,7 +562,8 @@ void rbq_tc_pass(Shard& s, const Batch& b, cudaStream_t st, bool sample) {
     ix->broken = true;                               // reported by the CU check after the stage
     return;
   }
-  // 3 query-tile stages of 64 pairs (A lives in tensor memory; shared memory holds B and records)
+  // nst = 2 query-tile stages of kRbN pairs (A lives in tensor memory; shared memory holds the B
+  // stages and the kRbRec-deep records ring)
   const int nkb = (ix->D + 127) / 128;
   auto ws_smem = [&](int nst) {
     return (size_t)nst * nkb * kRbN * 128 + (size_t)kRbRec * kRbN * sizeof(RbqPair) + 3 * kRbM * 4 +
@@ -827,6 +851,9 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
       return fail(BBC_ERR_ARG, "workspace smaller than bbc_workspace_size min_bytes");
     nqb = std::min<long long>(nqb, (long long)((s.ws_bytes - s.p.fixed) / s.p.per_query));
   }
+  // every rank must cut the batch into the same micro-batches (the collectives of each must
+  // match): the per-query scratch depends on the local list sizes, so agree on the minimum
+  if (dist && !comm->agree_min(&nqb, st)) return fail(BBC_ERR_NCCL, "all-reduce (micro-batch size) failed");
   if (dbg && nqb < nq) return fail(BBC_ERR_ARG, "debug search needs all queries in one micro-batch");
   // host path: the device->host copy of micro-batch i (copy stream) overlaps the search of
   // micro-batch i+1; outputs alternate between two staging buffers.  At least 4 micro-batches
@@ -874,7 +901,7 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
     nb = (int)(pipe ? std::min<long long>(nqb, std::max<long long>(std::min(rem, min_nb), (rem + 1) / 2))
                     : std::min<long long>(nqb, rem));
     for (auto& s : sh) {
-      carve(s.ix, s.p, nb, nprobe, s.ws, s.b, &s.qstage, &s.oids, &s.od2, k, &s.db, W, &s.rb);
+      carve(s.ix, s.p, nb, (int)nqb, nprobe, s.ws, s.b, &s.qstage, &s.oids, &s.od2, k, &s.db, W, &s.rb);
       Batch& b = s.b;
       b.nq = nb; b.nprobe = nprobe; b.k = k; b.budget = budget_c; b.cap = s.p.cap;
       b.nbuckets = s.ix->nbuckets;
@@ -1011,12 +1038,12 @@ bbc_status run_one(bbc_index ix, const float* queries, int64_t nq, int32_t k, in
   sh[0].rank = ix->rank;
   if (ix->world > 1) {
     if (!ix->nccl) return fail(BBC_ERR_STATE, "sharded index: call bbc_comm_init first");
-    NcclComm c((ncclComm_t)ix->nccl, ix->world);
+    NcclComm c((ncclComm_t)ix->nccl, ix->world, ix->nccl_scratch);
     return run(sh, &c, queries, nq, k, nprobe, budget, out_ids, out_d2, stream, host, dbg);
   }
   if (ix->force_dist) {                            // world-1 NCCL communicator (tests)
     if (!ix->nccl) return fail(BBC_ERR_STATE, "call bbc_comm_init first");
-    NcclComm c((ncclComm_t)ix->nccl, 1);
+    NcclComm c((ncclComm_t)ix->nccl, 1, ix->nccl_scratch);
     return run(sh, &c, queries, nq, k, nprobe, budget, out_ids, out_d2, stream, host, dbg);
   }
   return run(sh, nullptr, queries, nq, k, nprobe, budget, out_ids, out_d2, stream, host, dbg);
@@ -1358,7 +1385,8 @@ void ivf_free(bbc_index ix) {
   cudaSetDevice(ix->device);
   void* ptrs[] = {ix->centroids, ix->loff, ix->gsize_d, ix->ids, ix->books, ix->codes, ix->P,
                   ix->wL, ix->bits, ix->factors, ix->raw, ix->stats, ix->codes_t, ix->tbase,
-                  ix->cmu, ix->cnorm, ix->rbq_tiles, ix->rbq_pc, ix->lrank, ix->pb_hi, ix->pb_lo};
+                  ix->cmu, ix->cnorm, ix->rbq_tiles, ix->rbq_pc, ix->lrank, ix->pb_hi, ix->pb_lo,
+                  ix->nccl_scratch};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& t : ix->timers) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
@@ -1402,6 +1430,14 @@ bbc_status bbc_set_remap(bbc_index ix, int32_t m) {
   if (m < 0 || m > 255) return fail(BBC_ERR_ARG, "m must be 0 (off) or in [1, 255]");
   if (m > 0 && ix->world > 1) return fail(BBC_ERR_ARG, "the equal-depth remap is single-shard only");
   ix->remap_m = m;
+  return BBC_OK;
+}
+
+bbc_status bbc_set_code_loads(bbc_index ix, int32_t mode) {
+  if (!ix) return fail(BBC_ERR_ARG, "null index");
+  if (mode != BBC_CODES_AUTO && mode != BBC_CODES_CACHED && mode != BBC_CODES_STREAM)
+    return fail(BBC_ERR_ARG, "unknown code-load mode");
+  ix->code_loads = mode;
   return BBC_OK;
 }
 
@@ -1506,6 +1542,8 @@ bbc_status bbc_comm_init(bbc_index ix, const void* id128, int rank, int world) {
   if (r != ncclSuccess) return fail(BBC_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
   if (ix->nccl) ncclCommDestroy((ncclComm_t)ix->nccl);
   ix->nccl = (void*)c;
+  if (!ix->nccl_scratch && cudaMalloc((void**)&ix->nccl_scratch, 8) != cudaSuccess)
+    return fail(BBC_ERR_CUDA, "cudaMalloc (communicator scratch)");
   ix->force_dist = world == 1;
   return BBC_OK;
 }

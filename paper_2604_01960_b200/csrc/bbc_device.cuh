@@ -48,6 +48,18 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
+// Warp-aggregated shared-memory histogram update (north_star: "the bucket histogram uses
+// warp-aggregated shared-memory atomics"): all 32 lanes call it with their bucket id (255 = beyond
+// d_max, not counted); the lanes holding the same id are found with one match, and one of them
+// adds their number -- one atomic per distinct id per warp instead of one per object.
+__device__ __forceinline__ void warp_hist_add(int* hist, int cell) {
+  const unsigned act = __ballot_sync(0xffffffffu, cell < 255);
+  if (cell < 255) {
+    const unsigned peers = __match_any_sync(act, cell);
+    if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[cell], __popc(peers));
+  }
+}
+
 // Block-wide min and max of a 64-bit key; result broadcast to all threads.  `red` needs
 // 2 * (NT/32) slots.
 template <int NT>

@@ -763,14 +763,13 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
     const long long oo = gout[G] + 4 * (lane & 7);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      if (4 * (lane & 7) + j < cnt) {
-        if (EST) {
-          out_est[oo + j] = acc[4 * i + j];
-        } else {
-          const int cell = cf(acc[4 * i + j]);
-          b.cells[oo + j] = (uint8_t)cell;
-          if (cell < 255) atomicAdd(&hist[cell], 1);
-        }
+      const bool valid = 4 * (lane & 7) + j < cnt;
+      if (EST) {
+        if (valid) out_est[oo + j] = acc[4 * i + j];
+      } else {
+        const int cell = valid ? cf(acc[4 * i + j]) : 255;
+        if (valid) b.cells[oo + j] = (uint8_t)cell;
+        warp_hist_add(hist, cell);                     // warp-uniform: every lane calls
       }
     }
   }
@@ -865,10 +864,15 @@ __global__ void __launch_bounds__(256) k_sample_cells(Batch b) {
   __syncthreads();
   const float* v = b.val + (size_t)q * b.cap;
   uint8_t* cl = b.cells + (size_t)q * b.cap;
-  for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
-    const int c = cf(v[i]);
-    cl[i] = (uint8_t)c;
-    if (c < 255) atomicAdd(&hist[c], 1);
+  // warp-uniform trip count (warp_hist_add needs every lane)
+  for (int i0 = blockIdx.x * 256 + (threadIdx.x & ~31); i0 < n; i0 += gridDim.x * 256) {
+    const int i = i0 + (threadIdx.x & 31);
+    int c = 255;
+    if (i < n) {
+      c = cf(v[i]);
+      cl[i] = (uint8_t)c;
+    }
+    warp_hist_add(hist, c);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kCells; i += 256)
@@ -964,7 +968,12 @@ __global__ void __launch_bounds__(kScanNT) k_rbq_scan(Batch b, Dev ix, int G) {
     const long long row0 = ix.loff[L];
     const int n = (int)(ix.loff[L + 1] - row0);
     const long long e0 = (long long)q * b.cap + po[j];
-    for (int i = threadIdx.x; i < n; i += kScanNT) {
+    for (int i0 = 0; i0 < n; i0 += kScanNT) {           // warp-uniform trip count (warp_hist_add)
+      const int i = i0 + threadIdx.x;
+      if (i >= n) {
+        if (!SAMPLE) warp_hist_add(hist, 255);
+        continue;
+      }
       const uint2* bp = reinterpret_cast<const uint2*>(ix.bits + (size_t)(row0 + i) * (D / 8));
       int ip = 0, pc = 0;
       for (int v = 0; v < W / 2; ++v) {
@@ -990,7 +999,7 @@ __global__ void __launch_bounds__(kScanNT) k_rbq_scan(Batch b, Dev ix, int G) {
       } else {
         const int cell = cf(est);
         b.cells[e0 + i] = (uint8_t)cell;
-        if (cell < 255) atomicAdd(&hist[cell], 1);
+        warp_hist_add(hist, cell);
       }
     }
     __syncthreads();
@@ -1136,9 +1145,9 @@ __global__ void __launch_bounds__(256) k_remap(Batch b) {
     cf.init(b.edges[2 * q], b.edges[2 * q + 1], b.nbuckets);
     const int n = b.poff[(size_t)q * (b.nprobe + 1) + ns];
     const float* v = b.val + (size_t)q * b.cap;
-    for (int i = threadIdx.x; i < n; i += 256) {
-      const int c = cf(v[i]);
-      if (c < 255) atomicAdd(&h0[c], 1);
+    for (int i0 = 0; i0 < n; i0 += 256) {
+      const int i = i0 + threadIdx.x;
+      warp_hist_add(h0, i < n ? cf(v[i]) : 255);
     }
   }
   __syncthreads();

@@ -285,21 +285,16 @@ __global__ void k_rbq_popc(const uint8_t* bits, long long n, int D, int* pc) {
 
 // ------------------------------------------------------------------ the list-major GEMM
 struct RbqTc {
-  const uint8_t* qbar;   // [slots x D] in 32-slot tiles, operand layout (k_rbq_pairs)
+  const uint8_t* qbar;   // [slots x D] query codes, row-major (k_rbq_pairs; TMA tiles of kRbN rows)
   const RbqPair* pinfo;  // [slots]
-  const int* off;        // [nlist + 1] first slot of each list (multiple of 32)
+  const int* off;        // [nlist + 1] first slot of each list (multiple of kRbN)
   const int* cnt_s;      // [nlist] sample pairs of each list
   const int* cnt_m;      // [nlist] all pairs of each list
   const int2* tiles;     // [ntiles] (list, first object)
   const int* pc;         // [n_local] popcount of each code
 };
 
-
-
 constexpr int kRbqIdesc = (2 << 4) | ((kRbN >> 3) << 17) | ((kRbM >> 4) << 24);   // s32 += u8 x u8
-
-
-
 
 // A from tensor memory (lane = object row, 4 K bytes per 32-bit column), B from shared memory
 __device__ __forceinline__ void i8_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t acc) {
@@ -309,14 +304,12 @@ __device__ __forceinline__ void i8_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint
       ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"((uint32_t)kRbqIdesc), "r"(acc));
 }
 
-
 __device__ __forceinline__ uint32_t nib_bytes(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
-
 
 // ------------------------------------------------------------------ the list-major GEMM
 // Warp-specialised pipeline.  Warp 24 (one lane) copies query tile qi -- kRbN slots of codes,
 // row-major in global memory, by TMA into 128-byte-swizzled K blocks, plus their records by a bulk
-// copy -- into stage qi % nst; warp 25 (one lane) issues the MMAs of tile qi (A in tensor memory)
+// copy into ring entry qi % kRbRec -- into stage qi % nst; warp 25 (one lane) issues the MMAs of tile qi (A in tensor memory)
 // into one of two TMEM accumulators; warps 0-23 run the epilogue of tile qi - 1 meanwhile (warp w
 // reads TMEM lanes 32 (w & 3) .. +31 and pairs kPW (w >> 2) .. +kPW-1).  Measured: an MMA with
 // N <= 64 costs ~51-57 cycles whatever N (tools/mma_microbench.cu), and the epilogue -- not the
@@ -426,8 +419,8 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
   if (warp == kRbWsEpi) {
-    // ---- producer: one lane; per query tile nkb TMA copies (32 rows x 128 B each) + one bulk
-    // copy of the 32 records
+    // ---- producer: one lane; per query tile nkb TMA copies (kRbN rows x 128 B each) + one bulk
+    // copy of the tile's kRbN records
     if (lane == 0) {
       for (int qi = nst; qi < ntile; ++qi) {
         mbar_wait(empty0 + 8u * (qi % nst), (unsigned)((qi / nst - 1) & 1));
@@ -540,18 +533,18 @@ __global__ void __launch_bounds__(256) k_cell_hist(Batch b) {
   __syncthreads();
   const uint8_t* c = b.cells + (size_t)q * b.cap;
   const int n16 = n >> 4;
-  for (int v = blockIdx.x * 256 + threadIdx.x; v < n16; v += gridDim.x * 256) {
-    const uint4 x = reinterpret_cast<const uint4*>(c)[v];
+  for (int v0 = blockIdx.x * 256 + (threadIdx.x & ~31); v0 < n16; v0 += gridDim.x * 256) {
+    const int v = v0 + (threadIdx.x & 31);              // warp-uniform trip count (warp_hist_add)
+    const uint4 x = v < n16 ? reinterpret_cast<const uint4*>(c)[v] : make_uint4(~0u, ~0u, ~0u, ~0u);
     const uint32_t w[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const int cell = (w[e >> 2] >> (8 * (e & 3))) & 255;
-      if (cell < 255) atomicAdd(&h[wid][cell], 1);
-    }
+    for (int e = 0; e < 16; ++e) warp_hist_add(h[wid], (w[e >> 2] >> (8 * (e & 3))) & 255);
   }
-  if (blockIdx.x == 0)                               // ragged tail
-    for (int i = (n16 << 4) + threadIdx.x; i < n; i += 256)
-      if (c[i] < 255) atomicAdd(&h[wid][c[i]], 1);
+  if (blockIdx.x == 0)                               // ragged tail (< 16 objects)
+    for (int i0 = n16 << 4; i0 < n; i0 += 256) {
+      const int i = i0 + threadIdx.x;
+      warp_hist_add(h[wid], i < n ? c[i] : 255);
+    }
   __syncthreads();
   for (int i = threadIdx.x; i < kCells; i += 256) {
     int t = 0;

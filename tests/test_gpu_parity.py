@@ -34,42 +34,83 @@ def gpu_index(name):
     return cfg, ix, Q, _IDX[name]
 
 
+def integer_exact(cfg):
+    """Integer-valued data and queries (C2: integers 0-255 stored as fp32; C5: uint8) under L2:
+    every partial sum of an exact d^2 is an integer < 2^24, so fp32 and fp64 exact distances are
+    identical and the final (d^2, id) selection is compared exactly."""
+    return cfg.gen in ("C2", "C5") and cfg.metric == "l2"
+
+
 def compare(cfg, ix, Q, gidx, k, nprobe, budget, want_est=True, check_final=True, nbuckets=255,
-            remap_m=0):
+            remap_m=0, sel=None, cand_stride=None):
+    """GPU search of all of Q in one call; the oracle's intermediates of the queries `sel`
+    (default: all) compared element by element.  Rows are selected on the device before any copy
+    (full-size debug buffers are gigabytes)."""
     from oracle import bbc_oracle as O
-    q = torch.from_numpy(Q).cuda()
+    q = torch.from_numpy(np.ascontiguousarray(Q)).cuda()
     gidx.set_buckets(nbuckets)
     gidx.set_remap(remap_m)
-    ids, d2, t = gidx.search_debug(q, k, nprobe, budget, want_est=want_est)
-    torch.cuda.synchronize()
-    gidx.set_buckets(255)
-    gidx.set_remap(0)
-    t = {a: b.cpu().numpy() for a, b in t.items()}
-    ids, d2 = ids.cpu().numpy(), d2.cpu().numpy()
-    oi, od, dbg = O.search(ix, Q, k, nprobe, budget, want_debug=True, nbuckets=nbuckets,
-                           remap_m=remap_m)
+    try:
+        ids, d2, t = gidx.search_debug(q, k, nprobe, budget, want_est=want_est, cand_stride=cand_stride)
+        torch.cuda.synchronize()
+    finally:
+        gidx.set_buckets(255)
+        gidx.set_remap(0)
+    sel = np.arange(len(Q)) if sel is None else np.asarray(sel)
+    si = torch.from_numpy(sel).cuda()
+    t = {a: b[si].cpu().numpy() for a, b in t.items()}
+    ids, d2 = ids[si].cpu().numpy(), d2[si].cpu().numpy()
+    del si
+    oi, od, dbg = O.search(ix, np.ascontiguousarray(Q[sel]), k, nprobe, budget, want_debug=True,
+                           nbuckets=nbuckets, remap_m=remap_m)
+    exact = integer_exact(cfg)
+    cs = t["cand_ids"].shape[1]
     for i, g in enumerate(dbg):
-        assert np.array_equal(t["probe"][i], g["probe"]), f"q{i} probe"
-        assert np.array_equal(t["rq2"][i].view(np.uint32), g["rq2"].view(np.uint32)), f"q{i} rq2"
-        assert t["n_probed"][i] == g["n_o"], f"q{i} n_o"
-        assert t["nsample"][i] == g["s"], f"q{i} sample lists"
+        qi = int(sel[i])
+        assert np.array_equal(t["probe"][i], g["probe"]), f"q{qi} probe"
+        assert np.array_equal(t["rq2"][i].view(np.uint32), g["rq2"].view(np.uint32)), f"q{qi} rq2"
+        assert t["n_probed"][i] == g["n_o"], f"q{qi} n_o"
+        assert t["nsample"][i] == g["s"], f"q{qi} sample lists"
         if want_est:
             ge = t["est"][i][: g["n_o"]]
             assert np.array_equal(ge.view(np.uint32), g["est"].view(np.uint32)), \
-                f"q{i} est: {np.count_nonzero(ge != g['est'])} differ"
+                f"q{qi} est: {np.count_nonzero(ge != g['est'])} differ"
         if g["s"] > 0:
-            assert t["edges"][i][0] == g["d_min"] and t["edges"][i][1] == g["d_max"], f"q{i} edges"
-            assert np.array_equal(t["hist"][i][:255], g["H"][:255]), f"q{i} hist"
-            assert t["tau"][i] == g["tau"], f"q{i} tau"
+            assert t["edges"][i][0] == g["d_min"] and t["edges"][i][1] == g["d_max"], f"q{qi} edges"
+            assert np.array_equal(t["hist"][i][:255], g["H"][:255]), f"q{qi} hist"
+            assert t["tau"][i] == g["tau"], f"q{qi} tau"
         else:
             assert t["tau"][i] == O.TAU_INF
         nc = t["n_cand"][i]
-        assert nc == len(g["sup_ids"]), f"q{i} |S*|"
-        assert np.array_equal(t["cand_ids"][i][:nc], g["sup_ids"]), f"q{i} superset ids"
-        np.testing.assert_allclose(t["cand_d2"][i][:nc], g["sup_d2"], rtol=1e-5, atol=1e-6)
+        assert nc == len(g["sup_ids"]), f"q{qi} |S*|"
+        assert nc <= cs, f"q{qi}: |S*| {nc} exceeds the debug stride {cs}"
+        assert np.array_equal(t["cand_ids"][i][:nc], g["sup_ids"]), f"q{qi} superset ids"
+        if exact:
+            assert np.array_equal(t["cand_d2"][i][:nc], g["sup_d2"]), f"q{qi} exact d2 (integer data)"
+        else:
+            np.testing.assert_allclose(t["cand_d2"][i][:nc], g["sup_d2"], rtol=1e-5, atol=1e-6)
         if check_final:
-            check_final_ids(ids[i], d2[i], oi[i], od[i], k)
+            # the GPU row is exactly the k smallest (GPU d^2, id) of its own candidates ...
+            check_final_self(ids[i], d2[i], t["cand_ids"][i][:nc], t["cand_d2"][i][:nc], k)
+            # ... and the oracle's: identical (integer data), else up to ties within 1e-5
+            if exact:
+                assert np.array_equal(np.sort(ids[i]), np.sort(oi[i])), f"q{qi} final ids"
+            else:
+                check_final_ids(ids[i], d2[i], oi[i], od[i], k)
     return ids, d2, t
+
+
+def check_final_self(gi, gd, cand_ids, cand_d2, k):
+    """The (d^2, id) tie-break of k_final_select, exactly: the row is the k smallest (d^2, id) of
+    the candidate set (ids and d^2 as the GPU computed them), padded with (-1, inf)."""
+    order = np.lexsort((cand_ids, cand_d2))[:k]
+    want = np.sort(cand_ids[order])
+    got = gi[gi >= 0]
+    assert np.array_equal(np.sort(got), want), "final selection is not the (d2, id) top-k"
+    assert len(got) == min(k, len(cand_ids))
+    assert (gi[len(got):] == -1).all() and np.isinf(gd[len(got):]).all()
+    pos = {int(x): j for j, x in enumerate(cand_ids)}
+    assert all(gd[j] == cand_d2[pos[int(x)]] for j, x in enumerate(got[:64])), "d2 of the selected ids"
 
 
 def check_final_ids(gi, gd, oi, od, k):
@@ -96,6 +137,38 @@ def check_final_ids(gi, gd, oi, od, k):
 def test_parity_config_point(name):
     cfg, ix, Q, g = gpu_index(name)
     compare(cfg, ix, Q, g, cfg.k, cfg.nprobe, cfg.budget)
+
+
+def _pairs_per_list(ix, Q, nprobe, nsamp_lists=None):
+    from oracle import bbc_oracle as O
+    pr, _ = O.probe(Q, np.asarray(ix["centroids"]), nprobe)
+    return np.bincount(pr.ravel(), minlength=int(ix["nlist"]))
+
+
+@pytest.mark.parametrize("name,stride", [("C3mt", 1), ("C3mt960", 4)])
+def test_parity_rabitq_multitile(name, stride):
+    """The tensor-core RaBitQ GEMM with >= 5 query tiles of kRbN = 96 pairs per list (Push pass):
+    both TMEM accumulators, the wrap of the two B stages and of the 4-deep records ring, and the
+    producer's loop past the first stages.  The whole batch runs in one call; every `stride`-th
+    query is compared with the oracle (estimates, edges, histogram, tau, superset, results)."""
+    cfg, ix, Q, g = gpu_index(name)
+    per_list = _pairs_per_list(ix, Q, cfg.nprobe)
+    assert per_list.max() >= 5 * 96, per_list            # the configuration reaches the paths
+    g.set_scan_mode(g.SCAN_TENSOR)
+    compare(cfg, ix, Q, g, cfg.k, cfg.nprobe, cfg.budget, sel=np.arange(0, len(Q), stride))
+
+
+@pytest.mark.parametrize("name", ["C2s", "C4s", "C5s"])
+def test_parity_code_load_modes(name):
+    """The PQ scan with its code loads streamed past L1 (BBC_CODES_STREAM, the instantiation the
+    full-size C4/C5 codes take) and cached (BBC_CODES_CACHED): both equal the oracle bit for bit."""
+    cfg, ix, Q, g = gpu_index(name)
+    try:
+        for mode in (g.CODES_STREAM, g.CODES_CACHED):
+            g.set_code_loads(mode)
+            compare(cfg, ix, Q, g, cfg.k, cfg.nprobe, cfg.budget)
+    finally:
+        g.set_code_loads(g.CODES_AUTO)
 
 
 @pytest.mark.parametrize("nprobe", [1025, 1500, 2048])
@@ -220,21 +293,26 @@ def test_recall_matches_oracle():
 
 
 @pytest.mark.slow
-def test_full_size_c2_sampled_queries():
-    """BASELINE.json configs[1] at full size, in the launch configuration bench.py times (all 1,000
-    queries in one call); 24 sampled queries compared with the oracle one by one."""
-    from oracle import bbc_oracle as O
-    cfg, ix, Q, g = gpu_index("C2")
-    q = torch.from_numpy(Q).cuda()
-    ids, d2 = g.search(q, cfg.k, cfg.nprobe, cfg.budget)
-    ids, d2 = ids.cpu().numpy(), d2.cpu().numpy()
-    sample = np.random.default_rng(7).choice(len(Q), 24, replace=False)
-    oi, od = O.search(ix, Q[sample], cfg.k, cfg.nprobe, cfg.budget)
-    for j, i in enumerate(sample):
-        check_final_ids(ids[i], d2[i], oi[j], od[j], cfg.k)
-    # invariants over every query: k distinct ids, distances ascending in no particular order
-    for i in range(len(Q)):
-        assert len(set(ids[i].tolist())) == cfg.k
+@pytest.mark.parametrize("name,nprobe,budget,nq,nsel", [
+    ("C2", 768, 20000, 1000, 16),        # bench.py's C2 operating point, the whole batch in one call
+    ("C2", 128, 20000, 1000, 8),         # BASELINE.json's C2 point
+    ("C3", 2048, 20000, 500, 10),        # C3's operating point, 500 queries (~250 pairs per list:
+                                         #   several query tiles of the RaBitQ GEMM per list)
+    ("C4", 1024, 75000, 2500, 12),       # C4's operating point, one micro-batch of bench.py's run
+])
+def test_full_size_sampled_parity(name, nprobe, budget, nq, nsel):
+    """BASELINE.json configs at full size, at the operating points bench.py times, with the batch
+    size of one bench micro-batch: `nsel` sampled queries compared with the oracle element by
+    element (probe, estimates, edges, histogram, tau, superset ids and exact d^2, final ids), and
+    every query's row checked for k distinct valid ids."""
+    cfg, ix, Q, g = gpu_index(name)
+    Q = np.ascontiguousarray(Q[:nq])
+    sel = np.sort(np.random.default_rng(7).choice(nq, nsel, replace=False))
+    ids, _, _ = compare(cfg, ix, Q, g, cfg.k, nprobe, budget, sel=sel, cand_stride=3 * budget)
+    a, _ = g.search(torch.from_numpy(Q).cuda(), cfg.k, nprobe, budget)
+    a = a.sort(dim=1).values
+    assert bool((a >= 0).all())
+    assert bool((a[:, 1:] != a[:, :-1]).all()), "duplicate ids in a row"
 
 
 # ------------------------------------------------------------------ list-sharded path (8(e))
@@ -246,8 +324,11 @@ def _sorted_by_id(ids, d2):
 @pytest.mark.parametrize("name,G", [("C1t", 2), ("C2s", 3), ("C3s", 2), ("C5s", 4)])
 def test_sharded_group_equals_single(name, G):
     """Lists sharded over G shards (greedy by size, as ivf_load does on G GPUs), the exchange
-    steps (MIN/histogram all-reduces, radix passes, result sum) done by the single-process group:
-    ids and exact d^2 identical to the unsharded search."""
+    steps (MIN/histogram all-reduces, radix passes, result gather) done by the single-process
+    group: results equal the ORACLE's (oracle/bbc_oracle.py: the sharded algebra reproduces the
+    unsharded search, tests/test_sharded_gloo.py) -- identical ids for integer data, up to ties
+    within 1e-5 otherwise -- and are bit-identical to the unsharded CUDA search."""
+    from oracle import bbc_oracle as O
     from paper_2604_01960_b200 import Index
     from paper_2604_01960_b200.bbc import search_group
     cfg, ix, Q, g = gpu_index(name)
@@ -258,8 +339,15 @@ def test_sharded_group_equals_single(name, G):
     for k, nprobe, budget in ((cfg.k, cfg.nprobe, cfg.budget), (17, 3, 40), (cfg.k, 1, cfg.k)):
         a_ids, a_d2 = g.search(q, k, nprobe, budget)
         b_ids, b_d2 = search_group(shards, q, k, nprobe, budget)
+        oi, od = O.search(ix, Q, k, nprobe, budget)
+        bi, bd = b_ids.cpu().numpy(), b_d2.cpu().numpy()
+        for i in range(len(Q)):
+            if integer_exact(cfg):
+                assert np.array_equal(np.sort(bi[i]), np.sort(oi[i])), f"q{i} sharded ids vs oracle"
+            else:
+                check_final_ids(bi[i], bd[i], oi[i], od[i], k)
         a = _sorted_by_id(a_ids.cpu().numpy(), a_d2.cpu().numpy())
-        b = _sorted_by_id(b_ids.cpu().numpy(), b_d2.cpu().numpy())
+        b = _sorted_by_id(bi, bd)
         assert np.array_equal(a[0], b[0])
         assert np.array_equal(a[1].view(np.uint32), b[1].view(np.uint32))
 

@@ -62,7 +62,9 @@ def test_python_constants_match_header():
     pairs = {"SCAN_SIMT": "BBC_SCAN_SIMT", "SCAN_TENSOR": "BBC_SCAN_TENSOR",
              "PROBE_SIMT": "BBC_PROBE_SIMT", "PROBE_TENSOR": "BBC_PROBE_TENSOR",
              "PROBE_AUTO": "BBC_PROBE_AUTO", "RERANK_QUERY": "BBC_RERANK_QUERY",
-             "RERANK_LIST": "BBC_RERANK_LIST", "RERANK_AUTO": "BBC_RERANK_AUTO"}
+             "RERANK_LIST": "BBC_RERANK_LIST", "RERANK_AUTO": "BBC_RERANK_AUTO",
+             "CODES_AUTO": "BBC_CODES_AUTO", "CODES_CACHED": "BBC_CODES_CACHED",
+             "CODES_STREAM": "BBC_CODES_STREAM"}
     for py, c in pairs.items():
         assert c in defs, c
         assert getattr(Index, py) == int(defs[c]), py
@@ -74,5 +76,5 @@ def test_setters_reject_bad_arguments_without_gpu():
     L = bbc.lib()
     for fn, v in (("bbc_set_buckets", 0), ("bbc_set_buckets", 256), ("bbc_set_remap", -1),
                   ("bbc_set_remap", 256), ("bbc_set_rerank_order", 7), ("bbc_set_scan_mode", 9),
-                  ("bbc_set_probe_mode", 5)):
+                  ("bbc_set_probe_mode", 5), ("bbc_set_code_loads", 3)):
         assert getattr(L, fn)(None, v) == 1, fn            # null index first: BBC_ERR_ARG

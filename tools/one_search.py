@@ -17,11 +17,13 @@ p.add_argument("--workload", default="C2")
 p.add_argument("--nprobe", type=int, default=768)
 p.add_argument("--budget", type=int, default=20000)
 p.add_argument("--reps", type=int, default=2)
+p.add_argument("--nq", type=int, default=0, help="first nq queries (0: the config's batch)")
 a = p.parse_args()
 cfg = configs.get(a.workload)
 path = datagen.ensure_index(cfg)
 g = Index(path)
-q = torch.from_numpy(synth.generate_queries(cfg)).cuda()
+Q = synth.generate_queries(cfg)
+q = torch.from_numpy(Q[:a.nq] if a.nq else Q).contiguous().cuda()
 for _ in range(a.reps):
     ids, d2 = g.search(q, cfg.k, a.nprobe, a.budget)
 torch.cuda.synchronize()
