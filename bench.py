@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Benchmark of the B200 BBC query path (one JSON line on rank 0).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2] [--impl bbc|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C4] [--impl bbc|reference]
 
 A step = one bbc_search over the workload's whole query batch (all steps a1-a8 of DESIGN.md
 section 1) with queries already resident in HBM; L2 is flushed (256 MB write) between timed steps,
@@ -9,13 +9,14 @@ outside the timed events.  `value` = queries/s of the whole job (all ranks), tim
 events on the search stream, max over ranks.  `e2e` = the same through bbc_search_host with the
 host->device query copy and the device->host result copy inside the timed region.
 
-Multi-GPU (torchrun), --shard queries (default): each rank runs its own batch of `nq` queries
-on a replicated index (independent problems, no data-path collective, "scaling": "weak").
---shard lists: the index is sharded by IVF list, every rank runs the same `nq` queries and the
-exchange steps are NCCL all-reduces inside libbbc.so ("scaling": "strong").
+Multi-GPU (torchrun), --shard lists (default for N > 1): the index is sharded by IVF list, every
+rank runs the same `nq` queries and the exchange steps (histogram all-reduces, result
+all-gather) are NCCL collectives inside libbbc.so ("scaling": "strong": the job's work is fixed).
+--shard queries: each rank runs its own batch of `nq` queries on a replicated index (independent
+problems, no data-path collective, "scaling": "weak").
 
---impl reference times the CPU oracle (oracle/, test infrastructure) on a bounded sample of the
-same workload, on rank 0 only.
+--impl reference times the CPU oracle (oracle/, test infrastructure) on every host core (one
+single-threaded process per core) on a bounded sample of the same workload, on rank 0 only.
 """
 from __future__ import annotations
 
@@ -48,7 +49,9 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="bbc", choices=["bbc", "reference"])
-    p.add_argument("--workload", default="C2")
+    p.add_argument("--workload", default="C4",
+                   help="C4 (default): BASELINE.json configs[3], the largest configuration quoted "
+                        "at 1 GPU that the metric's k range covers; C2, C3, C5, C4ip, C2q4 also")
     p.add_argument("--nprobe", type=int, default=None)
     p.add_argument("--budget", type=int, default=None)
     p.add_argument("--recall-queries", type=int, default=100)
@@ -56,7 +59,11 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=15.0)
     p.add_argument("--sweep", action="store_true", help="recall/QPS over an (nprobe, budget) grid")
     p.add_argument("--profile-steps", action="store_true", help="no warm-up/recall/cpu (ncu runs)")
-    p.add_argument("--shard", default="queries", choices=["queries", "lists"])
+    p.add_argument("--shard", default=None, choices=["queries", "lists"],
+                   help="multi-GPU partitioning: lists (default for --gpus > 1: the north_star's "
+                        "IVF-list sharding with NCCL exchanges) or queries (replicas)")
+    p.add_argument("--cpu-workers", type=int, default=0,
+                   help="processes of the oracle baseline (0: every host core)")
     p.add_argument("--buckets", type=int, default=255, help="B regular buckets (Eq. 6)")
     p.add_argument("--bucket-sweep", action="store_true",
                    help="QPS, |S*|/budget and recall over B (Table 4 analog) at the operating point")
@@ -72,17 +79,6 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def smem_lookup_peak_gbs():
-    """Shared-memory read peak: one 128-byte wavefront per clock per SM (32 conflict-free 4-byte
-    LUT lookups), 148 SMs, at the measured max SM clock."""
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            mhz = float(json.load(f)["sm_max_mhz"])
-    except Exception:
-        mhz = 1965.0
-    return 148 * 128 * mhz * 1e6 / 1e9
-
-
 def tensor_peak_tops(dtype: str) -> float:
     """Dense tensor peak in TOP/s: measured bf16 (MEASURED_PEAKS.json) x the nominal ratio of
     the dtype to bf16 (tf32 0.5, int8 2)."""
@@ -95,13 +91,16 @@ def tensor_peak_tops(dtype: str) -> float:
 
 
 def measured_traffic(workload, nprobe, budget, kernel):
-    """DRAM bytes per launch of `kernel` from the committed ncu capture of the same workload and
-    operating point (profiles/traffic.json), or None."""
+    """DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of `kernel`'s launches in one
+    step of the same workload and operating point, summed over every launch of the step, from the
+    committed ncu capture (profiles/traffic.json, tools/traffic_from_ncu.py), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             t = json.load(f)
         e = t[f"{workload}/{nprobe}/{budget}"][kernel]
-        return {"dram_bytes_per_launch": e["dram_bytes"], "source": e["source"]}
+        return {"dram_bytes_per_step": e["dram_bytes_per_step"], "launches_per_step": e["launches"],
+                "dram_bytes_per_launch": e["dram_bytes_per_step"] / max(1, e["launches"]),
+                "source": e["source"]}
     except Exception:
         return None
 
@@ -180,30 +179,95 @@ def database_in_id_order(path):
     return X
 
 
-# ------------------------------------------------------------------------------------ reference
+# ------------------------------------------------------------------------------------ CPU oracle
+# The oracle (oracle/bbc_oracle.py, test infrastructure) as it stands, timed on every host core:
+# queries are independent, so a pool of single-threaded worker processes (fork; the index file is
+# memory-mapped and shared through the page cache) each answers a slice of the sample.
+
+_ORC = {}
+
+
+def _orc_init(path):
+    for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[v] = "1"
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:
+        pass
+    from oracle import bbc_oracle as O
+    _ORC["O"] = O
+    _ORC["ix"] = index_file.read(path)
+
+
+def _orc_run(job):
+    Q, k, nprobe, budget = job
+    _ORC["O"].search(_ORC["ix"], Q, k, nprobe, budget)
+    return len(Q)
+
+
+def host_cpu():
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    model = ""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return cores, model
+
+
+class OraclePool:
+    """`workers` single-threaded oracle processes (default: every host core)."""
+
+    def __init__(self, path, workers=0):
+        import multiprocessing as mp
+        self.cores, self.model = host_cpu()
+        self.workers = workers or self.cores
+        self.pool = mp.get_context("fork").Pool(self.workers, initializer=_orc_init, initargs=(path,))
+
+    def run(self, Q, k, nprobe, budget):
+        """Answers the queries of Q (one per task, round-robin over the workers); wall seconds."""
+        jobs = [(Q[i:i + 1], k, nprobe, budget) for i in range(len(Q))]
+        t0 = time.perf_counter()
+        n = sum(self.pool.map(_orc_run, jobs, chunksize=1))
+        assert n == len(Q)
+        return time.perf_counter() - t0
+
+    def per_query_s(self, Q, k, nprobe, budget):
+        """Single-core seconds per query (one query on each worker, warm)."""
+        w = min(self.workers, len(Q))
+        el = self.run(Q[:w], k, nprobe, budget)
+        return el                                       # w queries in parallel ~ one query's time
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    from oracle import bbc_oracle as O
     cfg, path = load_workload(args.workload)
     nprobe, budget = operating_point(cfg, args)
-    ix = index_file.read(path)
     Q = synth.generate_queries(cfg)
-    t0 = time.perf_counter()
-    O.search(ix, Q[:2], cfg.k, nprobe, budget)
-    per_q = max(1e-3, (time.perf_counter() - t0) / 2)
+    pool = OraclePool(path, args.cpu_workers)
+    per_q = max(1e-3, pool.per_query_s(Q, cfg.k, nprobe, budget))
     # each step a bounded sample: the whole run stays within a few minutes
-    budget_s = 120.0 / max(1, args.steps + args.warmup)
-    ns = int(max(1, min(cfg.nq, budget_s / per_q)))
+    budget_s = 150.0 / max(1, args.steps + args.warmup)
+    ns = int(max(pool.workers, min(cfg.nq, pool.workers * budget_s / per_q)))
+    ns = min(ns, cfg.nq)
     for w in range(args.warmup):
-        O.search(ix, Q[:ns], cfg.k, nprobe, budget)
+        pool.run(Q[:ns], cfg.k, nprobe, budget)
     tot = 0.0
     for s in range(args.steps):
-        sl = Q[(s * ns) % cfg.nq:][:ns]
-        t0 = time.perf_counter()
-        O.search(ix, sl, cfg.k, nprobe, budget)
-        tot += time.perf_counter() - t0
+        lo = (s * ns) % cfg.nq
+        sl = np.concatenate([Q[lo:], Q[:lo]])[:ns]
+        tot += pool.run(sl, cfg.k, nprobe, budget)
+    pool.close()
     qps = ns * args.steps / tot
     line = {"impl": "reference", "metric": json.loads('"' + METRIC + '"'),
             "value": qps, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
@@ -212,27 +276,31 @@ def run_reference(args):
             "data": "synthetic",
             "config": {"workload": cfg.name, "nq": cfg.nq, "k": cfg.k, "nprobe": nprobe,
                        "budget": budget},
-            "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{ns} of {cfg.nq} {cfg.name} queries per step"},
+            "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": pool.workers,
+                             "host_cores": pool.cores, "cpu_model": pool.model, "kind": "oracle",
+                             "sample": f"{ns} of {cfg.nq} {cfg.name} queries per step, one "
+                                       f"single-threaded numpy oracle process per core"},
             "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(cfg, path, nprobe, budget, seconds):
-    from oracle import bbc_oracle as O
-    ix = index_file.read(path)
+def cpu_baseline(cfg, path, nprobe, budget, seconds, workers=0):
+    """The oracle on every host core over a bounded sample (~`seconds` of wall time)."""
     Q = synth.generate_queries(cfg)
-    t0 = time.perf_counter()
-    O.search(ix, Q[:2], cfg.k, nprobe, budget)
-    per_q = max(1e-3, (time.perf_counter() - t0) / 2)
-    ns = int(max(2, min(cfg.nq, seconds / per_q)))
-    t0 = time.perf_counter()
-    O.search(ix, Q[:ns], cfg.k, nprobe, budget)
-    el = time.perf_counter() - t0
-    return {"value": ns / el, "unit": "queries/s", "cores": 1, "kind": "oracle",
+    pool = OraclePool(path, workers)
+    try:
+        per_q = max(1e-3, pool.per_query_s(Q, cfg.k, nprobe, budget))
+        ns = int(max(pool.workers, min(cfg.nq, pool.workers * seconds / per_q)))
+        ns = min(ns, cfg.nq)
+        el = pool.run(Q[:ns], cfg.k, nprobe, budget)
+    finally:
+        pool.close()
+    return {"value": ns / el, "unit": "queries/s", "cores": pool.workers, "host_cores": pool.cores,
+            "cpu_model": pool.model, "kind": "oracle",
             "sample": f"first {ns} of {cfg.nq} {cfg.name} queries (nprobe={nprobe}, "
-                      f"budget={budget}), single-threaded numpy oracle, {el:.1f} s"}
+                      f"budget={budget}), one single-threaded numpy oracle process per core, "
+                      f"{el:.1f} s wall"}
 
 
 # ------------------------------------------------------------------------------------ GPU arm
@@ -243,7 +311,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2604_01960_b200 import Index, launch_count
-    from paper_2604_01960_b200.bbc import measure_l2_read_gbs
+    from paper_2604_01960_b200.bbc import measure_l2_read_gbs, measure_smem_lookups
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -258,7 +326,8 @@ def main():
     nprobe, budget = operating_point(cfg, args)
     k = cfg.k
 
-    lists = args.shard == "lists" and world > 1
+    shard = args.shard or ("lists" if world > 1 else "queries")
+    lists = shard == "lists" and world > 1
     if lists:
         from paper_2604_01960_b200.bbc import nccl_unique_id
         g = Index(path, rank=rank, world=world, device=local)
@@ -319,7 +388,17 @@ def main():
     jobq = nq if lists else world * nq                   # queries answered by the whole job
     value = jobq * args.steps / (ms_max / 1e3)
 
-    # ---------------- e2e through the host API (pinned host buffers)
+    # ---------------- e2e through the host API (pinned host buffers); skipped under
+    # --profile-steps so that an ncu capture holds exactly the K timed searches
+    if args.profile_steps:
+        if rank == 0:
+            print(json.dumps({"profile_steps": args.steps, "ms_per_step": ms_max / args.steps,
+                              "stage_ms_per_step": {k_: v / args.steps for k_, v in stage_ms.items()},
+                              "stats": stats}), flush=True)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     qh = torch.from_numpy(Qh).pin_memory()
     oh = (torch.empty((nq, k), dtype=torch.int64).pin_memory(),
           torch.empty((nq, k), dtype=torch.float32).pin_memory())
@@ -353,20 +432,25 @@ def main():
     row_bytes = info.d * (1 if info.raw_u8 else 4)
     main_objs = stats["probed"] - stats["sampled"]
     peak, peak_src = peaks()
-    smem_peak = smem_lookup_peak_gbs()
     scan_ms = stage_ms["scan"] / args.steps
     rr_ms = stage_ms["rerank"] / args.steps
+    # the scan's second roofline: its M LUT reads per object are conflict-free shared-memory
+    # loads, bounded by the measured lookup rate (bbc_measure_smem_lookups, best of 3)
+    lds_peak = max(measure_smem_lookups(0) for _ in range(3))
+    lookups = main_objs * (info.m if info.kind == 1 else 0)
     per = {
-        # the L1/shared-memory data pipe (128 B/clk/SM) carries both the 4-byte LUT entry read
-        # per code byte and the code byte itself (16-byte LDG through L1): 5 algorithmic bytes
-        # per lookup (the LUT replication is an implementation extra, not counted)
-        "scan": {"ms": scan_ms, "bound": "alu",
-                 "pipe": "L1/shared-memory data pipe: 4-byte conflict-free LUT read + 1 code byte per lookup",
-                 "bytes": main_objs * (info.m if info.kind == 1 else 0) * 5, "peak_GBs": smem_peak,
-                 "hbm_view": {"code_bytes": main_objs * code_bytes, "peak_GBs": peak}},
+        # SURVEY 8(d) / north_star: algorithmic code bytes (M per object of the main pass) over
+        # the scan's event-timed duration, against the measured HBM copy peak
+        "scan": {"ms": scan_ms, "bound": "hbm", "bytes": main_objs * code_bytes, "peak_GBs": peak,
+                 "lds_view": {"lookups": lookups, "peak_Glookups": lds_peak,
+                              "Glookups": lookups / (scan_ms / 1e3) / 1e9 if scan_ms > 0 else None,
+                              "peak_source": "measured: bbc_measure_smem_lookups (conflict-free "
+                                             "LDS.32 + FADD, 32 warps/SM, best of 3)"}},
         "rerank": {"ms": rr_ms, "bound": "hbm", "bytes": stats["candidates"] * row_bytes,
                    "peak_GBs": peak},
     }
+    if per["scan"]["lds_view"]["Glookups"]:
+        per["scan"]["lds_view"]["frac"] = per["scan"]["lds_view"]["Glookups"] / lds_peak
     if stats.get("rerank_list_batches", 0) > 0:
         # list-order re-rank: the rows a list's queries share are read from L2, so the bound is
         # the L2 -> SM read bandwidth, measured on this GPU by bbc_measure_l2_read
@@ -421,12 +505,11 @@ def main():
             "peak": per[dom]["peak_TOPs"] if tens else per[dom]["peak_Glookups"] if lkp else per[dom]["peak_GBs"],
             "unit": "TOP/s" if tens else "Glookup/s" if lkp else "GB/s", "frac": per[dom]["frac"],
             "traffic": traffic,
-            "peak_source": (peak_src if per[dom]["bound"] == "hbm" else
+            "peak_source": (f"{peak_src}: MEASURED_PEAKS.json hbm_gbs (copy)" if per[dom]["bound"] == "hbm" else
                             "measured: bbc_measure_l2_read (L2-resident 48 MiB, 16-byte loads, best of 5)"
                             if per[dom]["bound"] == "l2" else
                             "measured bf16 TFLOP/s x 2 (int8/bf16 nominal ratio)" if tens else
-                            "derived: 148 SMs x 64 ALU lanes/clk / 2 ops per lookup x sm_max_mhz (DESIGN.md 5)" if lkp else
-                            "derived: 148 SMs x 128 B/clk L1/shared-memory data pipe x sm_max_mhz (DESIGN.md 5)"),
+                            "derived: 148 SMs x 64 ALU lanes/clk / 2 ops per lookup x sm_max_mhz (DESIGN.md 5)"),
             "per_kernel": per,
             "stage_ms_per_step": {k_: v / args.steps for k_, v in stage_ms.items()}}
 
@@ -445,7 +528,7 @@ def main():
                "metric": cfg.metric, "queries": rq}
     cpu = None
     if world == 1 and not args.no_cpu_baseline and not args.profile_steps:
-        cpu = cpu_baseline(cfg, path, nprobe, budget, args.cpu_seconds)
+        cpu = cpu_baseline(cfg, path, nprobe, budget, args.cpu_seconds, args.cpu_workers)
 
     line = {
         "metric": json.loads('"' + METRIC + '"'),

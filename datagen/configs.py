@@ -92,7 +92,7 @@ SMALL = {
     # accumulators, the B-stage ring and the 4-deep records ring wrap; the producer loop runs),
     # the sample pass >= 2.  D = 128 keeps the oracle fast; C3mt960 repeats it at C3's D = 960
     # (8 K blocks per B stage).
-    "C3mt": C3.replace(name="C3mt", d=128, N=24_000, nlist=16, nq=480, k=300, nprobe=14,
+    "C3mt": C3.replace(name="C3mt", d=128, N=24_000, nlist=16, nq=540, k=300, nprobe=15,
                        budget=900, kmeans_iters=6),
     "C3mt960": C3.replace(name="C3mt960", N=8_000, nlist=8, nq=400, k=200, nprobe=8, budget=600,
                           kmeans_iters=6),

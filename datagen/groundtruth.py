@@ -46,12 +46,52 @@ def topk(Q: np.ndarray, X: np.ndarray, k: int, block: int = 16, metric: str = "l
     return gi, gd
 
 
+def topk_cuda(Q: np.ndarray, X: np.ndarray, k: int, metric: str = "l2", block: int = 8):
+    """Same as topk (fp64 keys by the same norm expansion, ties of the k-th key kept and ordered
+    by (key, id)) with the fp64 arithmetic on a CUDA device through torch: measurement plumbing,
+    not the query path.  X is streamed to the device once in row chunks per query block."""
+    import torch
+    dev = torch.device("cuda")
+    nq, N = len(Q), len(X)
+    gi = np.empty((nq, k), dtype=np.int64)
+    gd = np.empty((nq, k), dtype=np.float64)
+    chunk = 1 << 21
+    Xd = [torch.from_numpy(np.ascontiguousarray(X[lo:lo + chunk])).to(dev) for lo in range(0, N, chunk)]
+    xn = [(x.double() * x.double()).sum(1) for x in Xd] if metric != "ip" else None
+    for lo in range(0, nq, block):
+        qb = torch.from_numpy(np.asarray(Q[lo:lo + block], dtype=np.float64)).to(dev)
+        qn = (qb * qb).sum(1)
+        D = torch.empty((len(qb), N), dtype=torch.float64, device=dev)
+        c0 = 0
+        for j, x in enumerate(Xd):
+            xb = x.double()
+            if metric == "ip":
+                D[:, c0:c0 + len(xb)] = -(qb @ xb.T)
+            else:
+                D[:, c0:c0 + len(xb)] = torch.clamp(qn[:, None] + xn[j][None, :] - 2.0 * (qb @ xb.T), min=0.0)
+            c0 += len(xb)
+        kth = torch.topk(D, k, dim=1, largest=False).values.max(dim=1).values
+        for r in range(len(qb)):
+            cand = torch.nonzero(D[r] <= kth[r]).squeeze(1).cpu().numpy()
+            d = D[r, torch.from_numpy(cand).to(dev)].cpu().numpy()
+            order = np.lexsort((cand, d))[:k]
+            gi[lo + r] = cand[order]
+            gd[lo + r] = d[order]
+        del D
+    return gi, gd
+
+
 def cached_topk(tag: str, Q: np.ndarray, X: np.ndarray, k: int, cache_dir: str, metric: str = "l2"):
     path = os.path.join(cache_dir, f"gt_{tag}_{len(Q)}_{k}.npz")
     if os.path.exists(path):
         z = np.load(path)
         return z["ids"], z["d2"]
-    gi, gd = topk(Q, X, k, metric=metric)
+    try:
+        import torch
+        cuda = torch.cuda.is_available()
+    except Exception:
+        cuda = False
+    gi, gd = topk_cuda(Q, X, k, metric=metric) if cuda else topk(Q, X, k, metric=metric)
     np.savez(path, ids=gi, d2=gd)
     return gi, gd
 

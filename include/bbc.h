@@ -292,8 +292,8 @@ bbc_status bbc_search_group(const bbc_index* shards, int nshards, const float* q
 enum {
   BBC_STAGE_PROBE = 0,   /* a1: coarse distances + nprobe selection */
   BBC_STAGE_TABLES = 1,  /* a2: LUT / rotation                      */
-  BBC_STAGE_SAMPLE = 2,  /* a3: sample estimates + edge selection   */
-  BBC_STAGE_SCAN = 3,    /* a4: Push (code scan + histogram)        */
+  BBC_STAGE_SAMPLE = 2,  /* a3: sample estimates + edge selection (+ the sample objects' bucket ids) */
+  BBC_STAGE_SCAN = 3,    /* a4: Push of the other probed objects (code scan + histogram)           */
   BBC_STAGE_COMPACT = 4, /* a5+a6: threshold + superset compaction  */
   BBC_STAGE_RERANK = 5,  /* a7: exact re-rank gather                */
   BBC_STAGE_SELECT = 6,  /* a8: final top-k                         */
@@ -327,6 +327,15 @@ int64_t bbc_launch_count(void);
  * on `cuda_device`.  BBC_ERR_ARG for bad sizes, BBC_ERR_CUDA on a CUDA failure.
  */
 bbc_status bbc_measure_l2_read(int32_t cuda_device, size_t bytes, int32_t reps, double* gbs);
+
+/*
+ * bbc_measure_smem_lookups -- measurement utility (not part of the search path): the device's
+ * shared-memory lookup rate in G lookups/s -- one CTA of 32 warps per SM, every lane reading
+ * 4-byte words at conflict-free addresses (one wavefront per warp instruction, as the 8-bit PQ
+ * scan's replicated LUT) and adding them into fp32 sums, `rounds` x 32 reads per thread.  The
+ * roofline of the LUT lookups of the PQ scan.  BBC_ERR_ARG for rounds < 1.
+ */
+bbc_status bbc_measure_smem_lookups(int32_t cuda_device, int32_t rounds, double* glookups);
 
 /* Message for the last non-OK status returned on the calling thread. */
 const char* bbc_last_error(void);

@@ -24,7 +24,8 @@ EXPORTS = ("ivf_load", "ivf_free", "bbc_index_info", "bbc_workspace_size", "bbc_
            "bbc_last_stats", "bbc_launch_count", "bbc_last_error", "bbc_nccl_unique_id",
            "bbc_comm_init", "bbc_search_group", "bbc_last_stats2", "bbc_set_probe_mode",
            "bbc_set_scan_mode", "bbc_stats_vector", "bbc_set_buckets", "bbc_set_rerank_order",
-           "bbc_measure_l2_read", "bbc_set_remap", "bbc_set_code_loads")
+           "bbc_measure_l2_read", "bbc_set_remap", "bbc_set_code_loads",
+           "bbc_measure_smem_lookups")
 
 STAGES = ("probe", "tables", "sample", "scan", "compact", "rerank", "select", "comm")
 TAU_INF = 1 << 30
@@ -87,6 +88,7 @@ def lib() -> ctypes.CDLL:
         L.bbc_set_rerank_order.argtypes = [vp, i32]
         L.bbc_set_remap.argtypes = [vp, i32]
         L.bbc_set_code_loads.argtypes = [vp, i32]
+        L.bbc_measure_smem_lookups.argtypes = [i32, i32, ctypes.POINTER(ctypes.c_double)]
         L.bbc_measure_l2_read.argtypes = [i32, ctypes.c_size_t, i32, ctypes.POINTER(ctypes.c_double)]
         L.bbc_stats_vector.argtypes = [vp, ctypes.POINTER(i64), i32]
         L.bbc_get_timing.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int,
@@ -105,7 +107,7 @@ def lib() -> ctypes.CDLL:
                    "bbc_comm_init", "bbc_search_group", "bbc_last_stats2", "bbc_set_probe_mode",
                    "bbc_set_scan_mode", "bbc_stats_vector", "bbc_set_buckets",
                    "bbc_set_rerank_order", "bbc_measure_l2_read", "bbc_set_remap",
-                   "bbc_set_code_loads"):
+                   "bbc_set_code_loads", "bbc_measure_smem_lookups"):
             getattr(L, fn).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -125,6 +127,15 @@ def measure_l2_read_gbs(device: int = 0, nbytes: int = 48 << 20, reps: int = 20)
     list-order re-rank)."""
     v = ctypes.c_double()
     _check(lib().bbc_measure_l2_read(int(device), int(nbytes), int(reps), ctypes.byref(v)))
+    return v.value
+
+
+def measure_smem_lookups(device: int = 0, rounds: int = 4096) -> float:
+    """Shared-memory lookup rate (G lookups/s) of `device`: conflict-free 4-byte reads, one
+    wavefront per warp instruction (bbc_measure_smem_lookups; the roofline of the PQ scan's LUT
+    lookups)."""
+    v = ctypes.c_double()
+    _check(lib().bbc_measure_smem_lookups(int(device), int(rounds), ctypes.byref(v)))
     return v.value
 
 

@@ -603,12 +603,16 @@ void stage_sample_est(Shard& s, cudaStream_t st) {
 // a4: bucket ids + local histogram of every probed object (sample ids from stored estimates)
 void stage_scan(Shard& s, cudaStream_t st) {
   bbc_index_s* ix = s.ix;
-  StageScope sc(ix, st, BBC_STAGE_SCAN);
   const int nb = s.b.nq, nprobe = s.b.nprobe;
-  if (ix->kind == BBC_KIND_PQ) {
+  if (ix->kind == BBC_KIND_PQ) {                  // the sample objects' ids: timed with the sample stage
+    StageScope sc2(ix, st, BBC_STAGE_SAMPLE);
     k_sample_cells<<<dim3(8, nb), 256, 0, st>>>(s.b);
+    g_launches += 1;
+  }
+  StageScope sc(ix, st, BBC_STAGE_SCAN);
+  if (ix->kind == BBC_KIND_PQ) {
     pq_scan(ix, false, st, s.b, s.dv, nullptr, 0, 1);
-    g_launches += 2;
+    g_launches += 1;
   } else if (ix->rbq_tc) {
     rbq_tc_pass(s, s.b, st, false);
   } else {
@@ -1111,6 +1115,61 @@ bbc_status bbc_measure_l2_read(int32_t cuda_device, size_t bytes, int32_t reps, 
   cudaFree(sink);
   if (err != cudaSuccess || ms <= 0.f) return fail(BBC_ERR_CUDA, "L2 probe failed");
   *gbs = (double)grid * reps * (double)(n16 * 16) / (ms * 1e-3) / 1e9;
+  return BBC_OK;
+}
+
+// Shared-memory lookup roofline probe: 32 warps per SM, each lane reading 4-byte words at
+// conflict-free addresses (lane l -> bank l, as the replicated-LUT scan's lookups) with 32
+// immediates off one base register per round, each read added into one of 8 fp32 sums: per
+// lookup one LDS.32 (one wavefront per warp instruction) and one FADD, the scan's minimum.
+__global__ void __launch_bounds__(1024, 1) k_lds_peak(int rounds, float* __restrict__ sink) {
+  extern __shared__ __align__(16) float lsm[];                  // 128 KB
+  for (int i = threadIdx.x; i < 32768; i += 1024) lsm[i] = (float)(i & 7);
+  __syncthreads();
+  const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(lsm) + 4u * (threadIdx.x & 31);
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  uint32_t off = 128u * (threadIdx.x >> 5);
+#pragma unroll 1
+  for (int r = 0; r < rounds; ++r) {
+    const uint32_t a = s0 + off;
+    static_for<32>([&](auto ic) {
+      constexpr int u = decltype(ic)::value;
+      float v;
+      asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(a), "n"(u * 2048));
+      acc[u & 7] += v;
+    });
+    off = (off + 128u * 33u) & 0xFFFFu;                         // a + 31 x 2048 + 124 < 128 KB
+  }
+  float t = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) t += acc[i];
+  if (t == -1.f) sink[0] = t;
+}
+
+bbc_status bbc_measure_smem_lookups(int32_t cuda_device, int32_t rounds, double* glookups) {
+  if (!glookups || rounds < 1) return fail(BBC_ERR_ARG, "bad arguments");
+  if (cudaSetDevice(cuda_device) != cudaSuccess) return fail(BBC_ERR_CUDA, "cudaSetDevice failed");
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
+  float* sink = nullptr;
+  if (cudaMalloc(&sink, 4) != cudaSuccess) return fail(BBC_ERR_CUDA, "cudaMalloc failed");
+  const size_t smem = 128 << 10;
+  cudaFuncSetAttribute(k_lds_peak, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  k_lds_peak<<<sms, 1024, smem>>>(rounds / 10 + 1, sink);            // warm-up
+  cudaEventRecord(e0);
+  k_lds_peak<<<sms, 1024, smem>>>(rounds, sink);
+  cudaEventRecord(e1);
+  cudaError_t err = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  if (err != cudaSuccess || ms <= 0.f) return fail(BBC_ERR_CUDA, "shared-memory probe failed");
+  *glookups = (double)sms * 1024.0 * 32.0 * (double)rounds / (ms * 1e-3) / 1e9;
   return BBC_OK;
 }
 
