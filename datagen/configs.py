@@ -94,7 +94,7 @@ SMALL = {
     # (8 K blocks per B stage).
     "C3mt": C3.replace(name="C3mt", d=128, N=24_000, nlist=16, nq=540, k=300, nprobe=15,
                        budget=900, kmeans_iters=6),
-    "C3mt960": C3.replace(name="C3mt960", N=8_000, nlist=8, nq=400, k=200, nprobe=8, budget=600,
+    "C3mt960": C3.replace(name="C3mt960", N=8_000, nlist=8, nq=500, k=200, nprobe=8, budget=600,
                           kmeans_iters=6),
     # fine lists (~20 objects): a compaction chunk of 8,192 objects spans > 256 lists, the
     # global-search path of k_emit; probe sets of 600 lists

@@ -11,8 +11,10 @@ steps are the ones DESIGN.md section 6 specifies for the GPU path:
     all-reduced 256-bin histograms;
   * the bucket histogram is all-reduced (sum), so every rank applies one threshold bucket;
   * the k smallest (exact d^2, id) keys over all ranks: 8 x 8-bit digits of the 64-bit key from
-    all-reduced histograms; every rank writes its selected pairs at its offset into a zeroed
-    output and the outputs are summed.
+    all-reduced 256-bin histograms; the per-(rank, query) counts of selected pairs are all-reduced,
+    and every rank's selected (d^2, id) pairs, packed query after query, are all-gathered
+    (north_star: "an all-gather of (distance, id) pairs feeds the final top-k"); each rank places
+    rank r's pairs of query q after those of ranks < r, so every rank holds the whole result.
 
 It reuses the per-rank arithmetic of bbc_oracle (probe, LUT, estimates, buckets, exact d^2) and
 must reproduce bbc_oracle.search exactly (tests/test_sharded_gloo.py).
@@ -67,15 +69,15 @@ def radix_select(local_keys: np.ndarray, need: int, nbits: int, allreduce) -> in
 
 
 def search(ix: dict, Q: np.ndarray, k: int, nprobe: int, budget: int, rank: int, world: int,
-           allreduce):
+           allreduce, allgather):
+    """allreduce(array, "sum" | "min") -> array; allgather(array) -> list of every rank's array
+    (rank order, sizes may differ)."""
     off = np.asarray(ix["list_offsets"])
     gsize = np.diff(off)
     owner = assign_lists(gsize, world)
     pr, rq = O.probe(np.asarray(Q, dtype=np.float32), ix["centroids"], nprobe)
     nq = len(Q)
-    out_ids = np.zeros((nq, k), dtype=np.int64)
-    out_d2 = np.zeros((nq, k), dtype=np.float32)
-    counts = []
+    mine_sel = []                                         # per query: this rank's selected pairs
     for i in range(nq):
         lists = pr[i]
         s = O.sample_lists(gsize[lists], budget)          # global sizes: same on every rank
@@ -121,18 +123,29 @@ def search(ix: dict, Q: np.ndarray, k: int, nprobe: int, budget: int, rank: int,
             chosen = keys <= np.uint64(thr)
         else:
             chosen = np.ones(len(keys), bool)
-        cnt = np.zeros(world, np.int64)
-        cnt[rank] = int(chosen.sum())
-        cnt = allreduce(cnt, "sum")
-        o = int(cnt[:rank].sum())
-        n_mine = int(cnt[rank])
-        order = np.flatnonzero(chosen)
-        out_ids[i, o:o + n_mine] = sid[order]
-        out_d2[i, o:o + n_mine] = d2[order]
-        counts.append(int(cnt.sum()))
-    out_ids = allreduce(out_ids, "sum")
-    out_d2 = allreduce(out_d2, "sum")
-    for i, n in enumerate(counts):
-        out_ids[i, n:] = -1
-        out_d2[i, n:] = np.inf
+        order = np.flatnonzero(chosen)                    # candidate (probe) order
+        mine_sel.append((sid[order], d2[order]))
+    # counts of selected pairs per (rank, query), all-reduced: every rank knows every offset
+    cnt = np.zeros((world, nq), np.int64)
+    cnt[rank] = [len(x[0]) for x in mine_sel]
+    cnt = allreduce(cnt, "sum")
+    # this rank's pairs packed query after query, as (fp32 bits of d^2) << 32 | id
+    packed = np.concatenate(
+        [(np.asarray(d, np.float32).view(np.uint32).astype(np.uint64) << np.uint64(32))
+         | np.asarray(i_, np.uint64) for i_, d in mine_sel]) if nq else np.zeros(0, np.uint64)
+    parts = allgather(packed)
+    out_ids = np.full((nq, k), -1, dtype=np.int64)
+    out_d2 = np.full((nq, k), np.inf, dtype=np.float32)
+    fill = np.zeros(nq, np.int64)
+    for r in range(world):                                # rank r's pairs after those of ranks < r
+        pr_ = np.asarray(parts[r], np.uint64)
+        assert len(pr_) == int(cnt[r].sum())
+        o = 0
+        for i in range(nq):
+            c = int(cnt[r, i])
+            blk = pr_[o:o + c]
+            out_ids[i, fill[i]:fill[i] + c] = (blk & np.uint64(0xFFFFFFFF)).astype(np.int64)
+            out_d2[i, fill[i]:fill[i] + c] = (blk >> np.uint64(32)).astype(np.uint32).view(np.float32)
+            fill[i] += c
+            o += c
     return out_ids, out_d2

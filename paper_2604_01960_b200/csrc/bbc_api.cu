@@ -92,6 +92,9 @@ struct bbc_index_s {
   int l2_bytes = 126 << 20;
   void* nccl = nullptr;                 // ncclComm_t of this rank (bbc_comm_init)
   long long* nccl_scratch = nullptr;    // [1] device scalar of the host-value agreement
+  void* nccl_x = nullptr;               // ncclComm_t split from nccl: the result all-gather on the
+                                        // copy stream, concurrent with the next micro-batch's collectives
+  long long* h_tot = nullptr;           // [8] pinned host: pairs each rank packs (exchange sizes)
   int force_dist = 0;                   // run the sharded code path even at world 1 (tests)
   cudaStream_t copy_stream = nullptr;   // host path: device->host result copies
   cudaEvent_t ev_done[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
@@ -192,6 +195,7 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1) {
   const int piece = rr_piece(ix->raw_u8 ? ix->d : 4 * ix->d);
   p.per_query += (size_t)nprobe * 20 + (size_t)(cap / piece) * 16;      // re-rank pieces
   p.per_query += kCells;                                                 // remap
+  if (world > 1) p.per_query += (size_t)k * 16 + (size_t)world * 8;      // result exchange (XBuf)
   p.fixed = 64 * 256 + (size_t)3 * (ix->nlist + 1) * 4 + 3 * 256;
   if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) {            // pair codes + inverted index
     p.per_query += (size_t)nprobe * ((size_t)ix->D + sizeof(RbqPair) + 4);   // codes, records, slots
@@ -207,7 +211,7 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1) {
 // still read its output buffer while micro-batch i+1 (possibly smaller: the tail halves) runs.
 void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nqmax, int nprobe, char* ws, Batch& b,
            float** qstage, long long** ostage_ids, float** ostage_d2, int k, DistBuf* db, int world,
-           RbqBufs* rb) {
+           RbqBufs* rb, XBuf* xb) {
   size_t off = 0;
   auto take = [&](size_t bytes) {
     char* r = ws + off;
@@ -219,6 +223,13 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nqmax, int nprobe,
   *ostage_d2 = (float*)take((size_t)nqmax * k * 4);
   b.ostage2_ids = (long long*)take((size_t)nqmax * k * 8);   // second output staging (host path)
   b.ostage2_d2 = (float*)take((size_t)nqmax * k * 4);
+  if (world > 1) {                  // result exchange: read by the copy stream past this micro-batch
+    xb->send = (unsigned long long*)take((size_t)nqmax * k * 8);
+    xb->recv = (unsigned long long*)take((size_t)nqmax * k * 8);
+    xb->cnt = (int*)take((size_t)world * nqmax * 4);
+    xb->coff = (int*)take((size_t)world * nqmax * 4);
+    xb->tot = (long long*)take((size_t)world * 8);
+  }
   size_t table = ix->kind == BBC_KIND_PQ ? (size_t)ix->M * 256 : (size_t)ix->D;
   b.coarse = (float*)take((size_t)nqb * ix->nlist * 4);
   b.probe = (int*)take((size_t)nqb * nprobe * 4);
@@ -385,6 +396,10 @@ struct Comm {
   // host value -> its minimum over the processes of the communicator (synchronises `st`); the
   // shards of one process already agree
   virtual bool agree_min(long long* v, cudaStream_t st) { (void)v; (void)st; return true; }
+  // all-gather with per-rank sizes of 8-byte elements: rank r's send[r] (count[r] elements) lands
+  // at recv + displ[r] of the receiving rank(s) (for a single-process group: shard 0)
+  virtual bool allgatherv(const std::vector<const void*>& send, const std::vector<void*>& recv,
+                          const long long* count, const long long* displ, cudaStream_t st) = 0;
 };
 
 struct GroupComm : Comm {
@@ -406,13 +421,23 @@ struct GroupComm : Comm {
     g_launches += 1;
     return cudaGetLastError() == cudaSuccess;
   }
+  bool allgatherv(const std::vector<const void*>& send, const std::vector<void*>& recv,
+                  const long long* count, const long long* displ, cudaStream_t st) override {
+    for (int r = 0; r < G; ++r)
+      if (count[r] > 0 && cudaMemcpyAsync((unsigned long long*)recv[0] + displ[r], send[r], (size_t)count[r] * 8,
+                                          cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return false;
+    return true;
+  }
 };
 
 struct NcclComm : Comm {
   ncclComm_t c;
-  int W;
+  ncclComm_t cx;                      // second communicator: the result all-gather (copy stream)
+  int W, me;
   long long* scratch;                 // one device int64 (bbc_comm_init)
-  NcclComm(ncclComm_t comm, int w, long long* sc) : c(comm), W(w), scratch(sc) {}
+  NcclComm(ncclComm_t comm, ncclComm_t commx, int w, int rank, long long* sc)
+      : c(comm), cx(commx), W(w), me(rank), scratch(sc) {}
   int world() const override { return W; }
   bool allreduce(const std::vector<void*>& bufs, size_t n, Dt dt, Op op, cudaStream_t st) override {
     if (n == 0) return true;
@@ -426,10 +451,24 @@ struct NcclComm : Comm {
            cudaMemcpyAsync(v, scratch, 8, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
            cudaStreamSynchronize(st) == cudaSuccess;
   }
+  // grouped broadcasts, one per root rank: an all-gather with per-rank sizes
+  bool allgatherv(const std::vector<const void*>& send, const std::vector<void*>& recv,
+                  const long long* count, const long long* displ, cudaStream_t st) override {
+    if (ncclGroupStart() != ncclSuccess) return false;
+    bool ok = true;
+    for (int r = 0; r < W && ok; ++r) {
+      if (count[r] == 0) continue;
+      unsigned long long* dst = (unsigned long long*)recv[0] + displ[r];
+      ok = ncclBroadcast(r == me ? send[0] : (const void*)dst, dst, (size_t)count[r], ncclUint64, r, cx, st) ==
+           ncclSuccess;
+    }
+    return ncclGroupEnd() == ncclSuccess && ok;
+  }
 };
 
 struct Shard {
   RbqBufs rb;
+  XBuf xb;
   bbc_index_s* ix;
   char* ws;
   size_t ws_bytes;
@@ -784,9 +823,12 @@ bbc_status dist_hist(std::vector<Shard>& sh, Comm* comm, cudaStream_t st) {
   return BBC_OK;
 }
 
+// select, part 1 (search stream): global |S*| per query, the (d^2, id) threshold of the k
+// smallest by 8 radix passes, the per-(rank, query) counts of selected pairs and their packed
+// offsets (every rank computes every rank's offsets from the all-reduced counts).
 bbc_status dist_select(std::vector<Shard>& sh, Comm* comm, cudaStream_t st) {
   bbc_index_s* ix = sh[0].ix;
-  const int nb = sh[0].b.nq, k = sh[0].b.k, W = comm->world();
+  const int nb = sh[0].b.nq, W = comm->world();
   StageScope sc(ix, st, BBC_STAGE_SELECT);
   for (auto& s : sh) {
     k_ds_ncand<<<(nb + 255) / 256, 256, 0, st>>>(s.b, s.db);
@@ -813,24 +855,77 @@ bbc_status dist_select(std::vector<Shard>& sh, Comm* comm, cudaStream_t st) {
   }
   for (auto& s : sh) {
     CU_NOIX(cudaMemsetAsync(s.db.cnt, 0, (size_t)W * nb * 4, st));
-    k_ds_select<false><<<nb, kSelNT, 0, st>>>(s.b, s.db, s.rank, W, nullptr, nullptr);
+    k_ds_select<false><<<nb, kSelNT, 0, st>>>(s.b, s.db, s.rank, s.xb);
     g_launches += 1;
   }
   if (!all_reduce(comm, sh, nullptr, (size_t)W * nb, Dt::I32, Op::Sum, st, [](Shard& s) { return (void*)s.db.cnt; }))
     return fail(BBC_ERR_NCCL, "all-reduce (selected counts) failed");
+  return BBC_OK;
+}
+
+// select, part 2 (search stream, after the previous micro-batch's exchange released the
+// buffers): counts and packed offsets into the exchange buffer, this rank's pairs packed, the
+// per-rank totals copied to pinned host memory (the exchange sizes); ev_x[0] marks them ready.
+bbc_status dist_pack(std::vector<Shard>& sh, Comm* comm, cudaStream_t st) {
+  bbc_index_s* ix = sh[0].ix;
+  const int nb = sh[0].b.nq, W = comm->world();
+  StageScope sc(ix, st, BBC_STAGE_SELECT);
   for (auto& s : sh) {
-    CU_NOIX(cudaMemsetAsync(s.oids, 0, (size_t)nb * k * 8, st));
-    CU_NOIX(cudaMemsetAsync(s.od2, 0, (size_t)nb * k * 4, st));
-    k_ds_select<true><<<nb, kSelNT, 0, st>>>(s.b, s.db, s.rank, W, s.oids, s.od2);
-    g_launches += 1;
+    k_ds_counts_scan<<<W, 1024, 0, st>>>(s.b, s.db, s.xb);
+    k_ds_select<true><<<nb, kSelNT, 0, st>>>(s.b, s.db, s.rank, s.xb);
+    g_launches += 2;
   }
-  if (!all_reduce(comm, sh, nullptr, (size_t)nb * k, Dt::I64, Op::Sum, st, [](Shard& s) { return (void*)s.oids; }) ||
-      !all_reduce(comm, sh, nullptr, (size_t)nb * k, Dt::F32, Op::Sum, st, [](Shard& s) { return (void*)s.od2; }))
-    return fail(BBC_ERR_NCCL, "all-reduce (results) failed");
+  CU(cudaMemcpyAsync(ix->h_tot, sh[0].xb.tot, (size_t)W * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaEventRecord(ix->ev_done[0], st));
+  return BBC_OK;
+}
+
+// A micro-batch whose pairs are packed, waiting for its all-gather (enqueued once the search
+// stream has the next micro-batch's work queued, so the host wait does not idle the GPU).
+struct PendingX {
+  bool on = false;
+  long long q0 = 0;
+  int nb = 0, bi = 0;
+};
+
+// The all-gather of a packed micro-batch and the unpack into the output, on the copy stream
+// (the second communicator); ev_copied[0] marks the exchange buffers free again.
+bbc_status dist_exchange(std::vector<Shard>& sh, Comm* comm, const PendingX& px, int k, bool host,
+                         int64_t* out_ids, float* out_d2) {
+  bbc_index_s* ix = sh[0].ix;
+  const int W = comm->world();
+  cudaStream_t cs = ix->copy_stream;
+  CU(cudaEventSynchronize(ix->ev_done[0]));            // the sizes (h_tot) are on the host
+  Displs dp{};
+  long long cnt[8], dsp[8], acc = 0;
+  for (int r = 0; r < W; ++r) {
+    cnt[r] = ix->h_tot[r];
+    dsp[r] = acc;
+    dp.d[r] = acc;
+    acc += cnt[r];
+  }
+  if (acc > (long long)px.nb * k) return fail(BBC_ERR_STATE, "exchange larger than its buffer");
+  CU(cudaStreamWaitEvent(cs, ix->ev_done[0], 0));
+  std::vector<const void*> sends;
+  std::vector<void*> recvs;
   for (auto& s : sh) {
-    k_ds_pad<<<dim3(4, nb), 256, 0, st>>>(s.b, s.db, W, s.oids, s.od2);
-    g_launches += 1;
+    sends.push_back(s.xb.send);
+    recvs.push_back(s.xb.recv);
   }
+  {
+    StageScope sc(ix, cs, BBC_STAGE_COMM);
+    if (!comm->allgatherv(sends, recvs, cnt, dsp, cs)) return fail(BBC_ERR_NCCL, "all-gather (results) failed");
+  }
+  Shard& s0 = sh[0];
+  long long* oi = host ? (px.bi ? s0.b.ostage2_ids : s0.oids) : (long long*)out_ids + px.q0 * k;
+  float* od = host ? (px.bi ? s0.b.ostage2_d2 : s0.od2) : out_d2 + px.q0 * k;
+  k_ds_unpack<<<px.nb, 256, 0, cs>>>(px.nb, k, W, s0.xb, dp, oi, od);
+  g_launches += 1;
+  if (host) {
+    CU(cudaMemcpyAsync(out_ids + px.q0 * k, oi, (size_t)px.nb * k * 8, cudaMemcpyDeviceToHost, cs));
+    CU(cudaMemcpyAsync(out_d2 + px.q0 * k, od, (size_t)px.nb * k * 4, cudaMemcpyDeviceToHost, cs));
+  }
+  CU(cudaEventRecord(ix->ev_copied[0], cs));
   return BBC_OK;
 }
 
@@ -872,16 +967,17 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
                                                            (ix->raw_u8 ? ix->d : 4.0 * ix->d);
   const int tail_div = (double)k * 12.0 * 1000.0 < work_b ? 1 : 4;
   const bool pipe = host && !dist && !dbg && tail_div > 1;
-  if (pipe) {
-    nqb = std::min<long long>(nqb, std::max<long long>(256, (nq + 1) / 2));
-    if (!ix->copy_stream) {
-      CU(cudaStreamCreateWithFlags(&ix->copy_stream, cudaStreamNonBlocking));
-      for (int i = 0; i < 2; ++i) {
-        CU(cudaEventCreateWithFlags(&ix->ev_done[i], cudaEventDisableTiming));
-        CU(cudaEventCreateWithFlags(&ix->ev_copied[i], cudaEventDisableTiming));
-      }
+  if (pipe) nqb = std::min<long long>(nqb, std::max<long long>(256, (nq + 1) / 2));
+  if ((pipe || dist) && !ix->copy_stream) {
+    CU(cudaStreamCreateWithFlags(&ix->copy_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CU(cudaEventCreateWithFlags(&ix->ev_done[i], cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&ix->ev_copied[i], cudaEventDisableTiming));
     }
   }
+  if (dist && !ix->h_tot) CU(cudaHostAlloc((void**)&ix->h_tot, 8 * sizeof(long long), cudaHostAllocDefault));
+  PendingX px;                                        // sharded: micro-batch awaiting its all-gather
+  bool xbusy = false;                                 // an all-gather is enqueued on the copy stream
   int mb_index = 0;
   const long long budget_c = std::min<long long>(budget, (long long)1 << 40);
   for (auto& s : sh) {
@@ -905,7 +1001,7 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
     nb = (int)(pipe ? std::min<long long>(nqb, std::max<long long>(std::min(rem, min_nb), (rem + 1) / 2))
                     : std::min<long long>(nqb, rem));
     for (auto& s : sh) {
-      carve(s.ix, s.p, nb, (int)nqb, nprobe, s.ws, s.b, &s.qstage, &s.oids, &s.od2, k, &s.db, W, &s.rb);
+      carve(s.ix, s.p, nb, (int)nqb, nprobe, s.ws, s.b, &s.qstage, &s.oids, &s.od2, k, &s.db, W, &s.rb, &s.xb);
       Batch& b = s.b;
       b.nq = nb; b.nprobe = nprobe; b.k = k; b.budget = budget_c; b.cap = s.p.cap;
       b.nbuckets = s.ix->nbuckets;
@@ -966,10 +1062,19 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
         stage_rerank(s, st);
       }
       if ((e = dist_select(sh, comm, st)) != BBC_OK) return e;
-      if (!host) {                                     // results are replicated: shard 0's copy
-        CU(cudaMemcpyAsync(out_ids + q0 * k, sh[0].oids, (size_t)nb * k * 8, cudaMemcpyDeviceToDevice, st));
-        CU(cudaMemcpyAsync(out_d2 + q0 * k, sh[0].od2, (size_t)nb * k * 4, cudaMemcpyDeviceToDevice, st));
+      // the previous micro-batch's all-gather, now that this one's work is queued ahead of the
+      // host wait; this micro-batch's packing waits until that exchange released the buffers
+      if (px.on) {
+        if ((e = dist_exchange(sh, comm, px, k, host, out_ids, out_d2)) != BBC_OK) return e;
+        xbusy = true;
+        px.on = false;
       }
+      if (xbusy) CU(cudaStreamWaitEvent(st, ix->ev_copied[0], 0));
+      if ((e = dist_pack(sh, comm, st)) != BBC_OK) return e;
+      px.on = true;
+      px.q0 = q0;
+      px.nb = nb;
+      px.bi = mb_index & 1;
     }
     CU(cudaGetLastError());
     Shard& s0 = sh[0];
@@ -1018,13 +1123,19 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
         CU(cudaGetLastError());
       }
     }
-    if (host && !pipe) {
+    if (host && !pipe && !dist) {
       CU(cudaMemcpyAsync(out_ids + q0 * k, s0.oids, (size_t)nb * k * 8, cudaMemcpyDeviceToHost, st));
       CU(cudaMemcpyAsync(out_d2 + q0 * k, s0.od2, (size_t)nb * k * 4, cudaMemcpyDeviceToHost, st));
     }
     for (auto& s : sh) s.ix->microbatches++;
     ++mb_index;
   }
+  if (px.on) {                                        // the last micro-batch's all-gather
+    bbc_status e = dist_exchange(sh, comm, px, k, host, out_ids, out_d2);
+    if (e != BBC_OK) return e;
+    xbusy = true;
+  }
+  if (xbusy) CU(cudaStreamWaitEvent(st, ix->ev_copied[0], 0));   // results complete on `st`
   if (pipe)                                           // the caller's stream covers every copy
     for (int i = 0; i < std::min(mb_index, 2); ++i) CU(cudaStreamWaitEvent(st, ix->ev_copied[i], 0));
   if (host || dbg) CU(cudaStreamSynchronize(st));
@@ -1042,12 +1153,12 @@ bbc_status run_one(bbc_index ix, const float* queries, int64_t nq, int32_t k, in
   sh[0].rank = ix->rank;
   if (ix->world > 1) {
     if (!ix->nccl) return fail(BBC_ERR_STATE, "sharded index: call bbc_comm_init first");
-    NcclComm c((ncclComm_t)ix->nccl, ix->world, ix->nccl_scratch);
+    NcclComm c((ncclComm_t)ix->nccl, (ncclComm_t)ix->nccl_x, ix->world, ix->rank, ix->nccl_scratch);
     return run(sh, &c, queries, nq, k, nprobe, budget, out_ids, out_d2, stream, host, dbg);
   }
   if (ix->force_dist) {                            // world-1 NCCL communicator (tests)
     if (!ix->nccl) return fail(BBC_ERR_STATE, "call bbc_comm_init first");
-    NcclComm c((ncclComm_t)ix->nccl, 1, ix->nccl_scratch);
+    NcclComm c((ncclComm_t)ix->nccl, (ncclComm_t)ix->nccl_x, 1, 0, ix->nccl_scratch);
     return run(sh, &c, queries, nq, k, nprobe, budget, out_ids, out_d2, stream, host, dbg);
   }
   return run(sh, nullptr, queries, nq, k, nprobe, budget, out_ids, out_d2, stream, host, dbg);
@@ -1449,7 +1560,9 @@ void ivf_free(bbc_index ix) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& t : ix->timers) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
+  if (ix->nccl_x) ncclCommDestroy((ncclComm_t)ix->nccl_x);
   if (ix->nccl) ncclCommDestroy((ncclComm_t)ix->nccl);
+  if (ix->h_tot) cudaFreeHost(ix->h_tot);
   for (auto e : ix->pool) cudaEventDestroy(e);
   if (ix->copy_stream) cudaStreamDestroy(ix->copy_stream);
   for (int i = 0; i < 2; ++i) {
@@ -1599,8 +1712,16 @@ bbc_status bbc_comm_init(bbc_index ix, const void* id128, int rank, int world) {
   ncclComm_t c;
   const ncclResult_t r = ncclCommInitRank(&c, world, id, rank);
   if (r != ncclSuccess) return fail(BBC_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  ncclComm_t cx;                      // the result all-gather's own communicator (copy stream)
+  const ncclResult_t r2 = ncclCommSplit(c, 0, rank, &cx, nullptr);
+  if (r2 != ncclSuccess) {
+    ncclCommDestroy(c);
+    return fail(BBC_ERR_NCCL, std::string("ncclCommSplit: ") + ncclGetErrorString(r2));
+  }
+  if (ix->nccl_x) ncclCommDestroy((ncclComm_t)ix->nccl_x);
   if (ix->nccl) ncclCommDestroy((ncclComm_t)ix->nccl);
   ix->nccl = (void*)c;
+  ix->nccl_x = (void*)cx;
   if (!ix->nccl_scratch && cudaMalloc((void**)&ix->nccl_scratch, 8) != cudaSuccess)
     return fail(BBC_ERR_CUDA, "cudaMalloc (communicator scratch)");
   ix->force_dist = world == 1;

@@ -7,8 +7,11 @@
 //                    bits over the ordered 32-bit keys, each a 256-bin histogram (all-reduce SUM)
 //   Push    the bucket histogram H (all-reduce SUM) -> one global threshold bucket tau
 //   select  the k smallest (exact d^2, id) keys over all ranks' candidates: 8 radix passes
-//           over 64-bit keys (all-reduce SUM of histograms), then every rank writes its
-//           selected pairs at its offset of a zeroed output that is summed across ranks
+//           over 64-bit keys (all-reduce SUM of histograms); the per-(rank, query) counts of
+//           selected pairs (all-reduce SUM); every rank packs its selected pairs query after
+//           query and the packed runs are all-gathered (grouped broadcasts: an all-gather with
+//           per-rank sizes) on a second stream and communicator, overlapping the next
+//           micro-batch; each rank unpacks rank r's pairs of query q after those of ranks < r
 // Integer sums and MIN are order independent, so the result is the same for every world size.
 #pragma once
 #include "bbc_kernels.cuh"
@@ -132,45 +135,114 @@ __global__ void __launch_bounds__(256) k_ds_ncand(Batch b, DistBuf db) {
   if (q < b.nq) db.tot[q] = b.ncand[q];
 }
 
-// count (FILL=false) or write (FILL=true, in candidate order, at this rank's offset) the local
+// The result exchange buffers of one micro-batch (fixed offsets in the workspace, sized for the
+// largest micro-batch): this rank's packed selected pairs, every rank's packed pairs after the
+// all-gather, and the per-(rank, query) counts and packed offsets the unpack needs.
+struct XBuf {
+  unsigned long long* send;    // [nqmax x k]  (fp32 bits of d^2) << 32 | id, query after query
+  unsigned long long* recv;    // [nqmax x k]  rank r's run at displs[r]
+  int* cnt;                    // [world x nqmax] selected pairs of (rank, query)
+  int* coff;                   // [world x nqmax] offset of (rank, query) in rank's packed run
+  long long* tot;              // [world] pairs packed by each rank
+};
+struct Displs {
+  long long d[8];              // first element of rank r's run in recv (world <= 8)
+};
+
+// count (FILL=false) or pack (FILL=true: in candidate order at send[coff[rank][q]]) the local
 // candidates whose key is <= the selected threshold
 template <bool FILL>
-__global__ void __launch_bounds__(kSelNT) k_ds_select(Batch b, DistBuf db, int rank, int world,
-                                                      long long* out_ids, float* out_d2) {
+__global__ void __launch_bounds__(kSelNT) k_ds_select(Batch b, DistBuf db, int rank, XBuf xb) {
   __shared__ int wcnt[kSelNT / 32 + 1];
   const int q = blockIdx.x;
   const int nc = b.ncand[q];
   const unsigned long long thr = db.prefix[q];
   const float* v = b.val + (size_t)q * b.cap;
   const int* id = b.cid + (size_t)q * b.cap;
-  int off = 0;
-  if (FILL)
-    for (int r = 0; r < rank; ++r) off += db.cnt[(size_t)r * b.nq + q];
+  unsigned long long* out = FILL ? xb.send + xb.coff[(size_t)rank * b.nq + q] : nullptr;
+  const int mine = FILL ? xb.cnt[(size_t)rank * b.nq + q] : 0;
   int base = 0;
   for (int t0 = 0; t0 < nc; t0 += kSelNT) {
     const int i = t0 + threadIdx.x;
     bool f = false;
-    if (i < nc) f = ((((unsigned long long)f2key(v[i]) << 32) | (unsigned)id[i]) <= thr);
+    unsigned long long key = 0;
+    if (i < nc) {
+      key = ((unsigned long long)f2key(v[i]) << 32) | (unsigned)id[i];
+      f = key <= thr;
+    }
     int total;
     const int r = block_rank<kSelNT>(f, wcnt, &total);
-    if (FILL && f && off + base + r < b.k) {
-      out_ids[(size_t)q * b.k + off + base + r] = id[i];
-      out_d2[(size_t)q * b.k + off + base + r] = v[i];
-    }
+    if (FILL && f && base + r < mine)
+      out[base + r] = ((unsigned long long)__float_as_uint(v[i]) << 32) | (unsigned)id[i];
     base += total;
   }
   if (!FILL && threadIdx.x == 0) db.cnt[(size_t)rank * b.nq + q] = base;
 }
 
-// after the output sum: positions past the global count are padding
-__global__ void __launch_bounds__(256) k_ds_pad(Batch b, DistBuf db, int world, long long* out_ids,
-                                                float* out_d2) {
-  const int q = blockIdx.y;
-  int n = 0;
-  for (int r = 0; r < world; ++r) n += db.cnt[(size_t)r * b.nq + q];
-  for (int i = n + blockIdx.x * 256 + threadIdx.x; i < b.k; i += gridDim.x * 256) {
-    out_ids[(size_t)q * b.k + i] = -1;
-    out_d2[(size_t)q * b.k + i] = INFINITY;
+// Per rank r (one CTA each): the counts of the micro-batch's queries copied into the exchange
+// buffer, their exclusive scan over queries (packed offsets) and the total.
+__global__ void __launch_bounds__(1024) k_ds_counts_scan(Batch b, DistBuf db, XBuf xb) {
+  __shared__ int ws[32];
+  __shared__ long long carry;
+  const int r = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < b.nq; base += 1024) {
+    const int q = base + threadIdx.x;
+    const int v = q < b.nq ? db.cnt[(size_t)r * b.nq + q] : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += t;
+    }
+    if (lane == 31) ws[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      const int s = ws[lane];
+      int y = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= o) y += t;
+      }
+      ws[lane] = y - s;
+    }
+    __syncthreads();
+    const long long c0 = carry;
+    if (q < b.nq) {
+      xb.cnt[(size_t)r * b.nq + q] = v;
+      xb.coff[(size_t)r * b.nq + q] = (int)(c0 + ws[wid] + x - v);
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = c0 + ws[wid] + x;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) xb.tot[r] = carry;
+}
+
+// After the all-gather: row q = rank 0's pairs of q, then rank 1's, ...; padding (-1, +inf) past
+// the global count.  One CTA per query.
+__global__ void __launch_bounds__(256) k_ds_unpack(int nq, int k, int world, XBuf xb, Displs dp,
+                                                   long long* out_ids, float* out_d2) {
+  const int q = blockIdx.x;
+  long long* oi = out_ids + (size_t)q * k;
+  float* od = out_d2 + (size_t)q * k;
+  int base = 0;
+  for (int r = 0; r < world; ++r) {
+    const int c = min(xb.cnt[(size_t)r * nq + q], k - base);
+    const unsigned long long* src = xb.recv + dp.d[r] + xb.coff[(size_t)r * nq + q];
+    for (int i = threadIdx.x; i < c; i += 256) {
+      const unsigned long long x = src[i];
+      oi[base + i] = (long long)(unsigned)(x & 0xffffffffull);
+      od[base + i] = __uint_as_float((unsigned)(x >> 32));
+    }
+    base += c;
+  }
+  for (int i = base + threadIdx.x; i < k; i += 256) {
+    oi[i] = -1;
+    od[i] = INFINITY;
   }
 }
 

@@ -218,16 +218,17 @@ __global__ void __launch_bounds__(kQ4NT, 2) k_pq4_scan(Batch b, Dev ix, const ui
         const long long oo = gout[G] + 8 * (lane & 3);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const bool valid = 8 * (lane & 3) + j < cnt;
-          const uint32_t a2 = acc[i][2 * (j >> 2) + (j & 1)];
-          const uint32_t S = (j & 2) ? (a2 >> 16) : (a2 & 0xFFFFu);
-          const float est = __fadd_rn(__fmul_rn(delta, (float)S), bias);
-          if (EST) {
-            if (valid) out_est[oo + j] = est;
-          } else {
-            const int cell = valid ? cf(est) : 255;
-            if (valid) b.cells[oo + j] = (uint8_t)cell;
-            warp_hist_add(hist, cell);                 // warp-uniform: every lane calls
+          if (8 * (lane & 3) + j < cnt) {
+            const uint32_t a2 = acc[i][2 * (j >> 2) + (j & 1)];
+            const uint32_t S = (j & 2) ? (a2 >> 16) : (a2 & 0xFFFFu);
+            const float est = __fadd_rn(__fmul_rn(delta, (float)S), bias);
+            if (EST) {
+              out_est[oo + j] = est;
+            } else {
+              const int cell = cf(est);
+              b.cells[oo + j] = (uint8_t)cell;
+              if (cell < 255) atomicAdd(&hist[cell], 1);   // plain atomics (see k_pq_scan_rq)
+            }
           }
         }
       }

@@ -1,6 +1,6 @@
 """The list-sharded exchange algebra on CPU with torch.distributed (gloo, world size 2 and 3):
 each rank runs oracle/sharded.py on its own lists and talks to the others only through
-all-reduces; the result equals the unsharded oracle exactly (ids and d^2).  The GPU path
+all-reduces and one all-gather of the selected (d^2, id) pairs; the result equals the unsharded oracle exactly (ids and d^2).  The GPU path
 implements the same exchange steps (tests/test_gpu_parity.py::test_sharded_group_equals_single
 checks it against the unsharded CUDA search)."""
 import os
@@ -39,11 +39,16 @@ def _worker(rank, world, port, name, params, outdir):
         dist.all_reduce(t, op=dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MIN)
         return t.numpy().astype(a.dtype)
 
+    def allgather(a):
+        out = [None] * world
+        dist.all_gather_object(out, np.ascontiguousarray(a))
+        return out
+
     cfg = configs.get(name)
     ix = index_file.read(datagen.ensure_index(cfg))
     Q = synth.generate_queries(cfg)[:5]
     for j, (k, nprobe, budget) in enumerate(params):
-        ids, d2 = sharded.search(ix, Q, k, nprobe, budget, rank, world, allreduce)
+        ids, d2 = sharded.search(ix, Q, k, nprobe, budget, rank, world, allreduce, allgather)
         np.savez(os.path.join(outdir, f"r{rank}_{j}.npz"), ids=ids, d2=d2)
     dist.destroy_process_group()
 

@@ -22,8 +22,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def group(name: str):
-    if re.match(r"void bbc::k_pq_scan_rq<\d+, false", name) or re.match(r"void bbc::k_pq4_scan<\d+, false", name) \
-            or name.startswith("void bbc::k_rbq_mma_ws<false>"):
+    if re.match(r"void bbc::k_pq_scan_rq<\d+, (0|false)", name) or re.match(r"void bbc::k_pq4_scan<\d+, (0|false)", name) \
+            or re.match(r"void bbc::k_rbq_mma_ws<(0|false)>", name):
         return "scan"
     if name.startswith("void bbc::k_rerank"):
         return "rerank"
