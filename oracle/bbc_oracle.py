@@ -221,6 +221,127 @@ def rabitq_est(bits: np.ndarray, fac: np.ndarray, qbar: np.ndarray, consts, r: F
     return (s - f * e).astype(F32)
 
 
+def rabitq_bounds(est: np.ndarray, fac: np.ndarray, r: F32, D: int, eps0: float = 1.9):
+    """Lower / upper bounds of the exact d^2 around a RaBitQ estimate (the bound property the
+    paper's IVF+RaBitQ re-ranking exploits; eps0 = 1.9): the estimator of
+    <o, q> errs by at most eps0 * sqrt((1 - g_o^2) / g_o^2) / sqrt(D - 1) with high probability
+    (gao2024rabitq), and d^2 = r_o^2 + r^2 - 2 r_o r <o, q>, so
+        delta = ((2 r_o) r) * (t_o * eps),  t_o = sqrt(1 - g_o g_o) * (1 / g_o),
+        eps = eps0 / sqrt(D - 1),            lb = est - delta,  ub = est + delta
+    in fp32, each operation rounded (reading R21)."""
+    ro = fac[:, 0].astype(F32)
+    g = fac[:, 1].astype(F32)
+    t = np.sqrt(F32(1.0) - g * g) * (F32(1.0) / g)
+    eps = F32(F32(eps0) / np.sqrt(F32(D - 1)))
+    delta = ((F32(2.0) * ro) * F32(r)) * (t * eps)
+    est = np.asarray(est, dtype=F32)
+    return (est - delta).astype(F32), (est + delta).astype(F32)
+
+
+def minimal_rerank_alg2(lb: np.ndarray, ub: np.ndarray, exact_fn, k: int):
+    """Algorithm 2, the minimal re-ranking solution, literally: H_u = max-heap of
+    the k smallest upper bounds, H_l = min-heap of the objects whose lower bound is below the
+    top of H_u; then re-rank the object with the smaller lower bound of the two heap tops until
+    H_u.top_ub <= H_l.top_lb.  Objects are indices 0..n-1; exact_fn(i) -> exact distance.
+    Ties in a heap are broken by object index.  Returns (sorted top-k indices, re-ranked set)."""
+    import heapq
+    Hu = []                                   # max-heap by ub: entries (-ub, -i, lb)
+    Hl = []                                   # min-heap by lb: entries (lb, i)
+    for i in range(len(lb)):
+        top_ub = -Hu[0][0] if len(Hu) >= k else np.inf
+        if ub[i] < top_ub:
+            heapq.heappush(Hu, (-float(ub[i]), -i, float(lb[i])))
+            if len(Hu) > k:
+                nub, ni, nlb = heapq.heappop(Hu)
+                heapq.heappush(Hl, (nlb, -ni))
+        elif lb[i] < top_ub:
+            heapq.heappush(Hl, (float(lb[i]), i))
+    vis = set()
+    exact = {}
+    while Hu and Hl and -Hu[0][0] > Hl[0][0]:
+        # the object with the smaller lower bound among the two tops
+        u_lb, u_i = Hu[0][2], -Hu[0][1]
+        if Hl[0][0] < u_lb or u_i in vis:
+            lbv, i = heapq.heappop(Hl)
+            if i in vis:
+                continue
+        else:
+            _, ni, _ = heapq.heappop(Hu)
+            i = -ni
+        d = float(exact_fn(i))
+        exact[i] = d
+        vis.add(i)
+        heapq.heappush(Hu, (-d, -i, d))
+        if len(Hu) > k:
+            nub, ni, nlb = heapq.heappop(Hu)
+            if -ni not in vis:
+                heapq.heappush(Hl, (nlb, -ni))
+    return sorted(-e[1] for e in Hu), vis
+
+
+def bounded_rerank_alg3(lb: np.ndarray, ub: np.ndarray, exact_fn, k: int, d_min: F32, d_max: F32,
+                        nbuckets: int = 255):
+    """Algorithm 3, IVF+RaBitQ with two result buffers B_u (keyed on the upper
+    bound's bucket) and B_l (keyed on the lower bound's) sharing the codebook of the sample
+    (d_min, d_max; Eq. 6 cells), in the one-shot form of reading R17 and with DESIGN.md reading
+    R21 for the points the paper leaves open:
+      tau   = Update(B_u, k): the first bucket whose cumulative upper-bound count reaches k
+      B_u   = {o : a_ub <= tau}            (line 7, "<=" as reading R2)
+      B_l   = {o : a_ub > tau, a_lb <= tau} (line 8-9), then every object of B_u too (line 11)
+      loop  (lines 12-21) i = first non-empty B_l bucket, j = tau; while i < j: exact distances
+            of B_l[i] and B_u[j] into B_exact (an object is re-ranked once and leaves both
+            buffers); j = first bucket where the counts of B_u (by a_ub) and B_exact (by the
+            exact distance's bucket) reach k; i = next non-empty B_l bucket
+      result the k smallest (exact d^2, index) of B_exact plus the objects left in B_u[j] (line
+            22: "B_u u B_exact"; the threshold bucket's leftovers get exact distances too).
+    If tau is infinity (fewer than k upper bounds below d_max) every object with a_lb <= 254 is
+    re-ranked.  Returns (top-k indices sorted by (exact, index), re-ranked index set, j)."""
+    n = len(lb)
+    a_lb = cells(lb, d_min, d_max, nbuckets)
+    a_ub = cells(ub, d_min, d_max, nbuckets)
+    tau = threshold(np.bincount(a_ub, minlength=NCELL)[:255], k)
+    exact = {}
+    if tau == TAU_INF:
+        for i in np.flatnonzero(a_lb < 255):
+            exact[int(i)] = float(exact_fn(int(i)))
+        j = TAU_INF
+    else:
+        Bu = {c: set(np.flatnonzero(a_ub == c).tolist()) for c in range(tau + 1)}
+        Bl = {c: set() for c in range(tau + 1)}
+        for i in np.flatnonzero((a_ub > tau) & (a_lb <= tau)):
+            Bl[int(a_lb[i])].add(int(i))
+        for c in range(tau + 1):                       # line 11: B_u's objects into B_l
+            for i in Bu[c]:
+                Bl[int(a_lb[i])].add(i)
+        He = np.zeros(NCELL, dtype=np.int64)
+
+        def first_nonempty():
+            for c in range(tau + 1):
+                if Bl[c]:
+                    return c
+            return TAU_INF
+
+        i, j = first_nonempty(), tau
+        while i < j:
+            for o in sorted(Bl[i] | Bu.get(j, set())):
+                d = float(exact_fn(o))
+                exact[o] = d
+                He[int(cells(np.array([d], dtype=F32), d_min, d_max, nbuckets)[0])] += 1
+                Bl[int(a_lb[o])].discard(o)
+                if int(a_ub[o]) in Bu:
+                    Bu[int(a_ub[o])].discard(o)
+            Hu = np.zeros(NCELL, dtype=np.int64)
+            for c, objs in Bu.items():
+                Hu[c] += len(objs)
+            j = threshold((Hu + He)[:255], k)
+            i = first_nonempty()
+        if j != TAU_INF and j in Bu:                   # the threshold bucket's leftovers
+            for o in sorted(Bu[j]):
+                exact[o] = float(exact_fn(o))
+    keys = sorted((d, o) for o, d in exact.items())[:k]
+    return sorted(o for _, o in keys), set(exact), j
+
+
 # ----------------------------------------------------------------------------------------------
 # O4-O8  the bucket-based result buffer
 # ----------------------------------------------------------------------------------------------

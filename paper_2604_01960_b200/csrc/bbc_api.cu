@@ -180,7 +180,9 @@ struct Plan {
   size_t fixed;       // alignment slack
 };
 
-Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1) {
+// world: ranks of the exchange (>= 1); xchg: the sharded path runs (its result-exchange buffers
+// are needed even with a 1-rank communicator)
+Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1, bool xchg = false) {
   Plan p;
   long long cap = ix->desc_prefix[std::min<size_t>(nprobe, ix->desc_prefix.size() - 1)];
   cap = (cap + 15) / 16 * 16;
@@ -195,7 +197,7 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1) {
   const int piece = rr_piece(ix->raw_u8 ? ix->d : 4 * ix->d);
   p.per_query += (size_t)nprobe * 20 + (size_t)(cap / piece) * 16;      // re-rank pieces
   p.per_query += kCells;                                                 // remap
-  if (world > 1) p.per_query += (size_t)k * 16 + (size_t)world * 8;      // result exchange (XBuf)
+  if (xchg || world > 1) p.per_query += (size_t)k * 16 + (size_t)world * 8;   // result exchange (XBuf)
   p.fixed = 64 * 256 + (size_t)3 * (ix->nlist + 1) * 4 + 3 * 256;
   if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) {            // pair codes + inverted index
     p.per_query += (size_t)nprobe * ((size_t)ix->D + sizeof(RbqPair) + 4);   // codes, records, slots
@@ -223,7 +225,7 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nqmax, int nprobe,
   *ostage_d2 = (float*)take((size_t)nqmax * k * 4);
   b.ostage2_ids = (long long*)take((size_t)nqmax * k * 8);   // second output staging (host path)
   b.ostage2_d2 = (float*)take((size_t)nqmax * k * 4);
-  if (world > 1) {                  // result exchange: read by the copy stream past this micro-batch
+  if (xb) {                         // result exchange: read by the copy stream past this micro-batch
     xb->send = (unsigned long long*)take((size_t)nqmax * k * 8);
     xb->recv = (unsigned long long*)take((size_t)nqmax * k * 8);
     xb->cnt = (int*)take((size_t)world * nqmax * 4);
@@ -945,7 +947,7 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
   const int W = dist ? comm->world() : 1;
   long long nqb = nq;
   for (auto& s : sh) {
-    s.p = make_plan(s.ix, nprobe, k, W);
+    s.p = make_plan(s.ix, nprobe, k, W, dist);
     if (s.ws_bytes < s.p.fixed + s.p.per_query)
       return fail(BBC_ERR_ARG, "workspace smaller than bbc_workspace_size min_bytes");
     nqb = std::min<long long>(nqb, (long long)((s.ws_bytes - s.p.fixed) / s.p.per_query));
@@ -1001,7 +1003,8 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
     nb = (int)(pipe ? std::min<long long>(nqb, std::max<long long>(std::min(rem, min_nb), (rem + 1) / 2))
                     : std::min<long long>(nqb, rem));
     for (auto& s : sh) {
-      carve(s.ix, s.p, nb, (int)nqb, nprobe, s.ws, s.b, &s.qstage, &s.oids, &s.od2, k, &s.db, W, &s.rb, &s.xb);
+      carve(s.ix, s.p, nb, (int)nqb, nprobe, s.ws, s.b, &s.qstage, &s.oids, &s.od2, k, &s.db, W, &s.rb,
+            dist ? &s.xb : nullptr);
       Batch& b = s.b;
       b.nq = nb; b.nprobe = nprobe; b.k = k; b.budget = budget_c; b.cap = s.p.cap;
       b.nbuckets = s.ix->nbuckets;
@@ -1636,7 +1639,7 @@ bbc_status bbc_workspace_size(bbc_index ix, int64_t nq, int32_t k, int32_t nprob
   if (!ix || !bytes) return fail(BBC_ERR_ARG, "null argument");
   if (nprobe < 1 || nprobe > ix->nlist || k < 1 || nq < 0 || budget < k)
     return fail(BBC_ERR_ARG, "bad arguments");
-  Plan p = make_plan(ix, nprobe, k, ix->world);
+  Plan p = make_plan(ix, nprobe, k, ix->world, ix->world > 1 || ix->force_dist);
   *bytes = p.fixed + (size_t)std::max<int64_t>(nq, 1) * p.per_query;
   if (min_bytes) *min_bytes = p.fixed + p.per_query;
   return BBC_OK;

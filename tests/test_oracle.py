@@ -576,3 +576,89 @@ def test_remap_superset_contains_equal_width(c1t):
             assert set(a["sup_pos"].tolist()) <= set(b["sup_pos"].tolist())
             if m == 1:
                 assert b["tau"] == 254 and len(b["sup_pos"]) == int((b["cell"] < 255).sum())
+
+
+# ---------------------------------------------------------------- f1: bound-aware RaBitQ re-rank
+def _valid_bounds(rng, n, spread=0.3):
+    ex = rng.uniform(1.0, 2.0, n).astype(np.float32)
+    lb = (ex - spread * rng.random(n)).astype(np.float32)
+    ub = (ex + spread * rng.random(n)).astype(np.float32)
+    return ex, lb, ub
+
+
+def test_rabitq_bounds_closed_forms_and_coverage(c3s):
+    """rabitq_bounds (reading R21): lb <= est <= ub; g_o = 1 gives a zero-width interval (the
+    code is the vector: no estimation error); and the interval with eps0 = 1.9 holds the
+    exact d^2 for most (query, object) pairs -- the 'high probability' of P:L962."""
+    cfg, ix, Q, _ = c3s
+    fac = np.array([[1.5, 1.0], [2.0, 0.8], [0.5, 0.6]], dtype=np.float32)
+    est = np.array([3.0, 4.0, 5.0], dtype=np.float32)
+    lb, ub = O.rabitq_bounds(est, fac, np.float32(2.0), 960)
+    assert lb[0] == est[0] == ub[0]
+    assert np.all(lb <= est) and np.all(est <= ub)
+    # hand value for object 1: delta = (2*2.0*2.0) * (sqrt(1 - 0.64)/0.8 * 1.9/sqrt(959))
+    want = 8.0 * (0.6 / 0.8 * 1.9 / np.sqrt(959.0))
+    assert abs(float(ub[1] - est[1]) - want) < 1e-5
+    off = np.asarray(ix["list_offsets"])
+    D = int(ix["D"])
+    cover = []
+    for qi in range(4):
+        pr, rq = O.probe(Q[qi:qi + 1], np.asarray(ix["centroids"]), 6)
+        u = O.rabitq_rotate(Q[qi], np.asarray(ix["P"]))
+        for j, L in enumerate(pr[0]):
+            sl = slice(off[L], off[L + 1])
+            qbar, cs, r = O.rabitq_query_code(u, np.asarray(ix["wL"][L]), rq[0, j])
+            e = O.rabitq_est(np.asarray(ix["bits"][sl]), np.asarray(ix["factors"][sl]), qbar, cs, r, rq[0, j])
+            lo, hi = O.rabitq_bounds(e, np.asarray(ix["factors"][sl]), r, D)
+            ex = O.exact_d2(Q[qi], np.asarray(ix["raw"][sl]))
+            cover.append((ex >= lo) & (ex <= hi))
+    assert np.concatenate(cover).mean() > 0.85
+
+
+def test_alg2_minimal_rerank_exact_under_valid_bounds(rng):
+    """Algorithm 2 with valid bounds (lb <= exact <= ub) returns the exact top-k
+    and re-ranks every object of Observation 1's minimal set {[lb, ub] contains Dist_k}."""
+    for n, k in ((400, 1), (400, 37), (1000, 250)):
+        ex, lb, ub = _valid_bounds(rng, n)
+        top, vis = O.minimal_rerank_alg2(lb, ub, lambda i: ex[i], k)
+        want = sorted(np.argsort(ex, kind="stable")[:k].tolist())
+        assert top == want
+        dk = np.sort(ex)[k - 1]
+        minimal = set(np.flatnonzero((lb <= dk) & (ub >= dk)).tolist())
+        assert minimal - {want[np.argmax(ex[want])]} <= vis | set(want)
+        assert len(vis) < n                              # it does skip objects
+
+
+def test_alg3_under_valid_bounds_exact_up_to_threshold_bucket(rng):
+    """Algorithm 3 with valid bounds: k results; every object it misses or adds
+    against the exact top-k has its exact distance in the final threshold bucket or beyond
+    (bucket-granularity greediness, 'near-minimal'); it re-ranks fewer objects than all."""
+    for n, k in ((800, 10), (2000, 300)):
+        ex, lb, ub = _valid_bounds(rng, n, spread=0.05)
+        dmin, dmax = np.float32(lb.min()), np.float32(np.sort(ex)[min(n - 1, 3 * k)])
+        top, rer, j = O.bounded_rerank_alg3(lb, ub, lambda i: ex[i], k, dmin, dmax)
+        assert len(top) == k and set(top) <= rer
+        want = set(np.argsort(ex, kind="stable")[:k].tolist())
+        edge_j = dmin + j * (dmax - dmin) / 255.0
+        for o in set(top) ^ want:
+            assert ex[o] >= edge_j - 1e-5, (o, ex[o], edge_j)
+        assert len(rer) < n
+
+
+def test_alg3_wide_bounds_is_full_rerank_and_zero_width_is_exact(rng):
+    """Limits of Algorithm 3: bounds wider than the data (every object ambiguous) re-rank every
+    in-range object and return the exact top-k; zero-width bounds (lb = ub = exact) re-rank only
+    the threshold bucket and still return the exact top-k up to ties inside that bucket."""
+    n, k = 1200, 50
+    ex = rng.uniform(1.0, 2.0, n).astype(np.float32)
+    dmin, dmax = np.float32(0.5), np.float32(2.5)
+    lb = np.full(n, 0.5, np.float32)
+    ub = np.full(n, 2.4, np.float32)
+    top, rer, _ = O.bounded_rerank_alg3(lb, ub, lambda i: ex[i], k, dmin, dmax)
+    assert sorted(top) == sorted(np.argsort(ex, kind="stable")[:k].tolist())
+    assert len(rer) == n
+    top0, rer0, j0 = O.bounded_rerank_alg3(ex, ex, lambda i: ex[i], k, dmin, dmax)
+    cells = O.cells(ex, dmin, dmax)
+    assert rer0 <= set(np.flatnonzero(cells <= j0).tolist())
+    assert len(rer0) < n // 4
+    assert set(top0) == set(np.argsort(ex, kind="stable")[:k].tolist())
