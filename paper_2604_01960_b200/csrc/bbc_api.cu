@@ -641,11 +641,12 @@ void stage_sample_est(Shard& s, cudaStream_t st) {
   g_launches += 1;
 }
 
-// a4: bucket ids + local histogram of every probed object (sample ids from stored estimates)
-void stage_scan(Shard& s, cudaStream_t st) {
+// a4: bucket ids + local histogram of every probed object (sample ids from stored estimates:
+// here when the edges were all-reduced, else already by k_select_edges<true>)
+void stage_scan(Shard& s, cudaStream_t st, bool sample_cells) {
   bbc_index_s* ix = s.ix;
   const int nb = s.b.nq, nprobe = s.b.nprobe;
-  if (ix->kind == BBC_KIND_PQ) {                  // the sample objects' ids: timed with the sample stage
+  if (ix->kind == BBC_KIND_PQ && sample_cells) {  // the sample objects' ids: timed with the sample stage
     StageScope sc2(ix, st, BBC_STAGE_SAMPLE);
     k_sample_cells<<<dim3(8, nb), 256, 0, st>>>(s.b);
     g_launches += 1;
@@ -1031,10 +1032,11 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
       Shard& s = sh[0];
       {
         StageScope sc(s.ix, st, BBC_STAGE_SAMPLE);
-        k_select_edges<<<nb, kSelNT, 0, st>>>(s.b, s.dv);
+        if (ix->kind == BBC_KIND_PQ) k_select_edges<true><<<nb, kSelNT, 0, st>>>(s.b, s.dv);
+        else k_select_edges<false><<<nb, kSelNT, 0, st>>>(s.b, s.dv);
         g_launches += 1;
       }
-      stage_scan(s, st);
+      stage_scan(s, st, false);
       stage_compact(s, st);
       stage_rerank(s, st);
       const int bi = mb_index & 1;
@@ -1058,7 +1060,7 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
     } else {
       bbc_status e = dist_edges(sh, comm, st);
       if (e != BBC_OK) return e;
-      for (auto& s : sh) stage_scan(s, st);
+      for (auto& s : sh) stage_scan(s, st, true);
       if ((e = dist_hist(sh, comm, st)) != BBC_OK) return e;
       for (auto& s : sh) {
         stage_compact(s, st);

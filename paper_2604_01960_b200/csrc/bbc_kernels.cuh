@@ -1107,8 +1107,13 @@ __device__ uint32_t cta_kth32(int n, unsigned kth, KeyF key, unsigned* take, Kth
 // ------------------------------------------------------------------------------------------
 // a3  edges: d_min = min of the sample estimates, d_max = budget-th smallest
 // ------------------------------------------------------------------------------------------
+// CELLS: also the sample objects' bucket ids and their histogram from the estimates just
+// selected over (one pass more over data the CTA has in L1/L2; replaces k_sample_cells when the
+// edges are local, i.e. not all-reduced across ranks)
+template <bool CELLS>
 __global__ void __launch_bounds__(kSelNT) k_select_edges(Batch b, Dev ix) {
   __shared__ Kth32Smem sm;
+  __shared__ int hist[CELLS ? kCells : 1];
   const int q = blockIdx.x;
   const int ns = b.nsamp[q];
   if (ns == 0) return;
@@ -1118,10 +1123,26 @@ __global__ void __launch_bounds__(kSelNT) k_select_edges(Batch b, Dev ix) {
   uint32_t kmin;
   const uint32_t kmax = cta_kth32(n, (unsigned)b.budget, [&](int i, bool* ok) { *ok = true; return f2key(v[i]); },
                                   &take, sm, &kmin);
+  const float lo = key2f((uint32_t)kmin), hi = key2f((uint32_t)kmax);
   if (threadIdx.x == 0) {
-    b.edges[2 * q] = key2f((uint32_t)kmin);
-    b.edges[2 * q + 1] = key2f((uint32_t)kmax);
+    b.edges[2 * q] = lo;
+    b.edges[2 * q + 1] = hi;
     atomicAdd((unsigned long long*)&b.stats[2], (unsigned long long)n);   // sample objects
+  }
+  if (CELLS) {
+    for (int i = threadIdx.x; i < kCells; i += kSelNT) hist[i] = 0;
+    CellFn cf;
+    cf.init(lo, hi, b.nbuckets);
+    __syncthreads();
+    uint8_t* cl = b.cells + (size_t)q * b.cap;
+    for (int i = threadIdx.x; i < n; i += kSelNT) {
+      const int c = cf(v[i]);
+      cl[i] = (uint8_t)c;
+      if (c < 255) atomicAdd(&hist[c], 1);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kCells; i += kSelNT)
+      if (hist[i]) atomicAdd(&b.hist[(size_t)q * kCells + i], hist[i]);
   }
 }
 
