@@ -16,6 +16,7 @@
 #include "bbc_probe_tc.cuh"
 #include "bbc_rbq_tc.cuh"
 #include "bbc_pq4.cuh"
+#include "bbc_rerank_tile.cuh"
 
 using namespace bbc;
 
@@ -77,6 +78,8 @@ struct bbc_index_s {
   int rerank_order = BBC_RERANK_AUTO;    // BBC_RERANK_*: work order of the exact re-rank (a7)
   int remap_m = 0;                       // 0 or m equal-depth buckets (bbc_set_remap)
   int code_loads = BBC_CODES_AUTO;       // BBC_CODES_*: L1 policy of the PQ scan's code loads
+  int2* rt_units = nullptr;             // [rt_nunits] (list, tile) of the shared-memory re-rank
+  int rt_nunits = 0;                    //   (BBC_RERANK_TILE; fp32 rows of <= 512 bytes)
   int2* rbq_tiles = nullptr;            // [rbq_ntiles] (list, first object) of 128-object tiles
   int rbq_ntiles = 0;
   int* rbq_pc = nullptr;                // [n_local] popcount of each code
@@ -673,9 +676,17 @@ void stage_scan(Shard& s, cudaStream_t st, bool sample_cells) {
 // 11 % slower -- its segment and query-vector overheads are not repaid).
 bool rerank_list_order(const bbc_index_s* ix, const Batch& b, int rowb) {
   (void)rowb;
-  if (ix->rerank_order != BBC_RERANK_AUTO) return ix->rerank_order == BBC_RERANK_LIST;
+  if (ix->rerank_order != BBC_RERANK_AUTO)
+    return ix->rerank_order == BBC_RERANK_LIST || ix->rerank_order == BBC_RERANK_TILE;
   const double reuse = (double)b.nq * (double)b.budget / std::max<double>(1.0, (double)ix->n_local);
   return reuse >= 4.0;
+}
+
+// list order with the list's rows staged in shared memory tile by tile (bbc_rerank_tile.cuh):
+// available for fp32 rows of <= 512 bytes; AUTO takes it whenever list order is chosen
+bool rerank_tile(const bbc_index_s* ix, const Batch& b, int rowb) {
+  if (!ix->rt_units || !rerank_list_order(ix, b, rowb)) return false;
+  return ix->rerank_order == BBC_RERANK_TILE || ix->rerank_order == BBC_RERANK_AUTO;
 }
 
 void stage_compact(Shard& s, cudaStream_t st) {
@@ -767,6 +778,18 @@ void stage_rerank(Shard& s, cudaStream_t st) {
     k_rr_segments<false><<<gp, 256, 0, st>>>(s.b, s.b.rs_cnt, s.b.rseg, rr_piece(rowb));
     k_inv_scan<<<1, 1024, 0, st>>>(s.b.rs_cnt, s.b.rs_off, s.b.rs_cur, ix->nlist);
     k_rr_segments<true><<<gp, 256, 0, st>>>(s.b, s.b.rs_cur, s.b.rseg, rr_piece(rowb));
+    if (rerank_tile(ix, s.b, rowb)) {
+      const size_t smem = (size_t)rt_rows(rowb) * rowb;
+      if (ip) {
+        set_smem(k_rerank_tile<4, true>, smem);
+        k_rerank_tile<4, true><<<ix->rt_nunits, kRtNT, smem, st>>>(s.b, s.dv, s.b.rseg, ix->rt_units);
+      } else {
+        set_smem(k_rerank_tile<4, false>, smem);
+        k_rerank_tile<4, false><<<ix->rt_nunits, kRtNT, smem, st>>>(s.b, s.dv, s.b.rseg, ix->rt_units);
+      }
+      g_launches += 4;
+      return;
+    }
     if (ip) launch_rerank_list<true>(s, st, rowb);
     else launch_rerank_list<false>(s, st, rowb);
     g_launches += 5;
@@ -1521,6 +1544,16 @@ bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_
     }
     ix->rbq_tc = ok ? 1 : 0;
   }
+  if (ok && !raw_u8 && (size_t)d * 4 <= 512 && ix->n_local > 0) {
+    // (list, tile) units of the shared-memory re-rank, in list order
+    const int R = rt_rows(d * 4);
+    std::vector<int2> units;
+    for (int L = 0; L < nlist; ++L)
+      for (int t = 0; t * R < ix->lsize[L]; ++t) units.push_back(make_int2(L, t));
+    ix->rt_nunits = (int)units.size();
+    ok = dalloc((void**)&ix->rt_units, units.size() * 8) &&
+         cudaMemcpy(ix->rt_units, units.data(), units.size() * 8, cudaMemcpyHostToDevice) == cudaSuccess;
+  }
   cudaDeviceGetAttribute(&ix->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
   cudaDeviceGetAttribute(&ix->l2_bytes, cudaDevAttrL2CacheSize, cuda_device);
   if (ok && kind == BBC_KIND_PQ) {
@@ -1561,7 +1594,7 @@ void ivf_free(bbc_index ix) {
   void* ptrs[] = {ix->centroids, ix->loff, ix->gsize_d, ix->ids, ix->books, ix->codes, ix->P,
                   ix->wL, ix->bits, ix->factors, ix->raw, ix->stats, ix->codes_t, ix->tbase,
                   ix->cmu, ix->cnorm, ix->rbq_tiles, ix->rbq_pc, ix->lrank, ix->pb_hi, ix->pb_lo,
-                  ix->nccl_scratch};
+                  ix->nccl_scratch, ix->rt_units};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& t : ix->timers) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
@@ -1620,8 +1653,11 @@ bbc_status bbc_set_code_loads(bbc_index ix, int32_t mode) {
 
 bbc_status bbc_set_rerank_order(bbc_index ix, int32_t order) {
   if (!ix) return fail(BBC_ERR_ARG, "null index");
-  if (order != BBC_RERANK_QUERY && order != BBC_RERANK_LIST && order != BBC_RERANK_AUTO)
+  if (order != BBC_RERANK_QUERY && order != BBC_RERANK_LIST && order != BBC_RERANK_AUTO &&
+      order != BBC_RERANK_TILE)
     return fail(BBC_ERR_ARG, "unknown re-rank order");
+  if (order == BBC_RERANK_TILE && !ix->rt_units)
+    return fail(BBC_ERR_ARG, "the shared-memory re-rank needs fp32 rows of <= 512 bytes");
   ix->rerank_order = order;
   return BBC_OK;
 }

@@ -1,0 +1,114 @@
+// a7, list-major exact re-rank with the rows staged in shared memory (BBC_RERANK_TILE).
+//
+// In list order (k_rerank_seg) every candidate row still travels L2 -> SM once per query that
+// re-ranks it: each row of C4 is a candidate of ~19 queries of a micro-batch, and the kernel runs
+// at ~0.8 of the L2 read bandwidth.  Here a CTA owns a tile of R consecutive rows of one inverted
+// list: one bulk copy (cp.async.bulk, no per-row instructions) brings them from HBM into shared
+// memory once, and the warps then compute every piece of that list -- (query, run of <= 64
+// candidates) from k_rr_segments -- against the staged rows, reading them through the
+// shared-memory pipe (128 B/clk/SM, ~2.4x the L2 -> SM rate).  Candidates of a piece outside the
+// tile are left to the list's other tiles.  Per candidate the arithmetic is rr_rows32's (8 lanes
+// per row, each lane's 16-byte chunks t = sl + 8v in order, fp32 FMAs, shuffle tree), so every
+// distance is bit-identical to the query- and list-order kernels.  fp32 rows of <= 512 bytes.
+#pragma once
+#include "bbc_probe_tc.cuh"
+
+namespace bbc {
+
+constexpr int kRtNT = 512;                    // 16 warps
+constexpr int kRtBytes = 96 * 1024;           // rows per tile = kRtBytes / row bytes (2 CTAs/SM)
+
+__host__ __device__ constexpr int rt_rows(int rowb) { return kRtBytes / rowb; }
+
+template <int MAXV, bool IP>
+__global__ void __launch_bounds__(kRtNT, 2) k_rerank_tile(Batch b, Dev ix, const int4* __restrict__ seg,
+                                                          const int2* __restrict__ units) {
+  constexpr int LPC = 8, CPW = 32 / LPC;
+  extern __shared__ __align__(128) uint8_t rtsm[];
+  __shared__ uint64_t bar;
+  const int rowb = ix.d * 4;
+  const int nv = rowb / 16, per = (nv + LPC - 1) / LPC;
+  const int R = rt_rows(rowb);
+  const int2 u = units[blockIdx.x];                   // (list, tile)
+  const int L = u.x;
+  const int p0 = b.rs_off[L], p1 = b.rs_off[L + 1];
+  if (p0 == p1) return;                               // no candidate of this micro-batch in L
+  const long long lo = ix.loff[L] + (long long)u.y * R;
+  const long long hi = min(ix.loff[L + 1], lo + R);
+  const uint32_t bsm = smem_u32(&bar);
+  if (threadIdx.x == 0) {
+    mbar_init(bsm, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t bytes = (uint32_t)((hi - lo) * rowb);
+    mbar_arrive_tx(bsm, bytes);
+    const uint8_t* src = static_cast<const uint8_t*>(ix.raw) + lo * rowb;
+    for (uint32_t o = 0; o < bytes; o += 32768u)
+      bulk_g2s(smem_u32(rtsm) + o, src + o, min(32768u, bytes - o), bsm);
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int sub = lane / LPC, sl = lane % LPC;
+  RrQuery<false, LPC, MAXV> Q;
+  int qcur = -1;
+  mbar_wait(bsm, 0);
+#pragma unroll 1
+  for (int p = p0 + wid; p < p1; p += kRtNT / 32) {
+    const int4 pc = seg[p];                           // (query, first candidate, length)
+    const int q = pc.x;
+    const size_t base = (size_t)q * b.cap + pc.y;
+#pragma unroll 1
+    for (int c0 = 0; c0 < pc.z; c0 += 32) {
+      const int n32 = min(32, pc.z - c0);
+      const int r = lane < n32 ? b.cpos[base + c0 + lane] : -1;
+      const bool in = lane < n32 && r >= lo && r < hi;
+      const unsigned m = __ballot_sync(0xffffffffu, in);
+      const int cnt = __popc(m);
+      if (cnt == 0) continue;
+      if (q != qcur) {
+        Q.load(b.Q + (size_t)q * ix.d, sl, per, nv);
+        qcur = q;
+      }
+#pragma unroll 1
+      for (int s = 0; s < cnt; s += CPW) {
+        const int j = s + sub;                         // the j-th in-tile candidate of the chunk
+        const int bit = j < cnt ? (int)__fns(m, 0, j + 1) : 0;
+        const int rr = __shfl_sync(0xffffffffu, r, bit);
+        const uint32_t row = smem_u32(rtsm) + (uint32_t)((rr - lo) * rowb);
+        float acc = 0.f;
+#pragma unroll
+        for (int v = 0; v < MAXV; ++v) {
+          const int t = sl + LPC * v;
+          if (v < per && t < nv && j < cnt) {
+            float4 x;
+            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                         : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w) : "r"(row + 16u * (uint32_t)t));
+            if (IP) {
+              acc = fmaf(x.x, Q.qr[v][0], acc);
+              acc = fmaf(x.y, Q.qr[v][1], acc);
+              acc = fmaf(x.z, Q.qr[v][2], acc);
+              acc = fmaf(x.w, Q.qr[v][3], acc);
+            } else {
+              const float a0 = x.x - Q.qr[v][0], a1 = x.y - Q.qr[v][1];
+              const float a2 = x.z - Q.qr[v][2], a3 = x.w - Q.qr[v][3];
+              acc = fmaf(a0, a0, acc);
+              acc = fmaf(a1, a1, acc);
+              acc = fmaf(a2, a2, acc);
+              acc = fmaf(a3, a3, acc);
+            }
+          }
+        }
+#pragma unroll
+        for (int o = LPC / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (sl == 0 && j < cnt) {
+          const size_t k = base + c0 + bit;
+          b.val[k] = IP ? -acc : acc;
+          b.cid[k] = (int)__ldg(ix.ids + rr);
+        }
+      }
+    }
+  }
+}
+
+}  // namespace bbc

@@ -436,29 +436,32 @@ def test_rabitq_scan_modes_identical(nprobe_mult):
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", ["C2s", "C2f", "C3s", "C4s", "C5s", "C4ip_s", "C2q4s"])
 def test_rerank_orders_identical(name):
-    """The list-major re-rank (segments ordered by inverted list) and the query-major
-    one compute every candidate's exact distance identically: candidate distances, ids and
-    results are bit-identical, at the config's nprobe and with every list probed."""
+    """The list-major re-rank (segments ordered by inverted list), its shared-memory tiled form
+    (rows of a list tile staged once per CTA) and the query-major one compute every candidate's
+    exact distance identically: candidate distances, ids and results are bit-identical, at the
+    config's nprobe and with every list probed."""
     cfg, ix, Q, g = gpu_index(name)
     q = torch.from_numpy(Q).cuda()
     for nprobe in (cfg.nprobe, cfg.nlist):
         outs = []
-        for order in (g.RERANK_QUERY, g.RERANK_LIST):
+        orders = (g.RERANK_QUERY, g.RERANK_LIST) + ((g.RERANK_TILE,) if cfg.raw_dtype == "f32" and cfg.d * 4 <= 512 else ())
+        for order in orders:
             g.set_rerank_order(order)
             ids, d2, t = g.search_debug(q, cfg.k, nprobe, cfg.budget)
             torch.cuda.synchronize()
             outs.append({"ids": ids.cpu().numpy(), "d2": d2.cpu().numpy(),
                          **{k_: v.cpu().numpy() for k_, v in t.items()}})
         g.set_rerank_order(g.RERANK_AUTO)
-        a, b = outs
+        a = outs[0]
         assert int(a["n_cand"].sum()) > 0
-        for key in ("ids", "d2"):
-            assert np.array_equal(a[key].view(np.uint8), b[key].view(np.uint8)), key
-        for i in range(len(Q)):
-            n = int(a["n_cand"][i])
-            assert n == int(b["n_cand"][i])
-            for key in ("cand_ids", "cand_d2"):
-                assert np.array_equal(a[key][i][:n].view(np.uint8), b[key][i][:n].view(np.uint8)), key
+        for b in outs[1:]:
+            for key in ("ids", "d2"):
+                assert np.array_equal(a[key].view(np.uint8), b[key].view(np.uint8)), key
+            for i in range(len(Q)):
+                n = int(a["n_cand"][i])
+                assert n == int(b["n_cand"][i])
+                for key in ("cand_ids", "cand_d2"):
+                    assert np.array_equal(a[key][i][:n].view(np.uint8), b[key][i][:n].view(np.uint8)), key
 
 
 def test_ip_full_probe_unlimited_budget_is_brute_force_mips():
