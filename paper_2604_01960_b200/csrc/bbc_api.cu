@@ -80,6 +80,8 @@ struct bbc_index_s {
   int code_loads = BBC_CODES_AUTO;       // BBC_CODES_*: L1 policy of the PQ scan's code loads
   int2* rt_units = nullptr;             // [rt_nunits] (list, tile) of the shared-memory re-rank
   int rt_nunits = 0;                    //   (BBC_RERANK_TILE; fp32 rows of <= 512 bytes)
+  int* rt_ubase = nullptr;              // [nlist] first unit of each list
+  int rt_maxtiles = 0;                  // most tiles of one list
   int2* rbq_tiles = nullptr;            // [rbq_ntiles] (list, first object) of 128-object tiles
   int rbq_ntiles = 0;
   int* rbq_pc = nullptr;                // [n_local] popcount of each code
@@ -199,9 +201,10 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1, bool xch
   p.per_query += 8 + 8 + kCells * 4 + 4 + 4 + (size_t)4 * world;   // DistBuf
   const int piece = rr_piece(ix->raw_u8 ? ix->d : 4 * ix->d);
   p.per_query += (size_t)nprobe * 20 + (size_t)(cap / piece) * 16;      // re-rank pieces
+  p.per_query += (size_t)nprobe * ix->rt_maxtiles * 16;                   //   + cuts at tile bounds
   p.per_query += kCells;                                                 // remap
   if (xchg || world > 1) p.per_query += (size_t)k * 16 + (size_t)world * 8;   // result exchange (XBuf)
-  p.fixed = 64 * 256 + (size_t)3 * (ix->nlist + 1) * 4 + 3 * 256;
+  p.fixed = 64 * 256 + (size_t)3 * (std::max(ix->nlist, ix->rt_nunits) + 1) * 4 + 3 * 256;
   if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) {            // pair codes + inverted index
     p.per_query += (size_t)nprobe * ((size_t)ix->D + sizeof(RbqPair) + 4);   // codes, records, slots
     p.fixed += (size_t)kRbN * ix->nlist * ((size_t)ix->D + sizeof(RbqPair)) +   // per-list padding
@@ -259,10 +262,12 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nqmax, int nprobe,
   b.chunkj = (int*)take((size_t)nqb * ((p.cap + kChunk - 1) / kChunk) * 4);
   b.sstart = (int*)take((size_t)nqb * nprobe * 4);
   b.rmap = (uint8_t*)take((size_t)nqb * kCells);
-  b.rseg = (int4*)take((size_t)nqb * (nprobe + p.cap / rr_piece(ix->raw_u8 ? ix->d : 4 * ix->d)) * 16);
-  b.rs_cnt = (int*)take((size_t)(ix->nlist + 1) * 4);
-  b.rs_off = (int*)take((size_t)(ix->nlist + 1) * 4);
-  b.rs_cur = (int*)take((size_t)(ix->nlist + 1) * 4);
+  b.rseg = (int4*)take((size_t)nqb * ((size_t)nprobe * (1 + ix->rt_maxtiles) +
+                                       p.cap / rr_piece(ix->raw_u8 ? ix->d : 4 * ix->d)) * 16);
+  const size_t nrs = (size_t)std::max(ix->nlist, ix->rt_nunits) + 1;   // lists, or tile units
+  b.rs_cnt = (int*)take(nrs * 4);
+  b.rs_off = (int*)take(nrs * 4);
+  b.rs_cur = (int*)take(nrs * 4);
 
   db->prefix = (unsigned long long*)take((size_t)nqb * 8);
   db->need = (long long*)take((size_t)nqb * 8);
@@ -774,22 +779,28 @@ void stage_rerank(Shard& s, cudaStream_t st) {
     ix->rr_list_batches++;
     // segments (query, first candidate, length) counted, offset and placed by list
     const unsigned gp = (unsigned)(((long long)nb * s.b.nprobe + 255) / 256);
-    cudaMemsetAsync(s.b.rs_cnt, 0, (size_t)(ix->nlist + 1) * 4, st);
-    k_rr_segments<false><<<gp, 256, 0, st>>>(s.b, s.b.rs_cnt, s.b.rseg, rr_piece(rowb));
-    k_inv_scan<<<1, 1024, 0, st>>>(s.b.rs_cnt, s.b.rs_off, s.b.rs_cur, ix->nlist);
-    k_rr_segments<true><<<gp, 256, 0, st>>>(s.b, s.b.rs_cur, s.b.rseg, rr_piece(rowb));
     if (rerank_tile(ix, s.b, rowb)) {
+      // pieces per (list, tile) unit, then one CTA per unit over its staged rows
+      const int nu = ix->rt_nunits;
+      cudaMemsetAsync(s.b.rs_cnt, 0, (size_t)(nu + 1) * 4, st);
+      k_rr_tile_pieces<false><<<gp, 256, 0, st>>>(s.b, s.dv, ix->rt_ubase, s.b.rs_cnt, s.b.rseg);
+      k_inv_scan<<<1, 1024, 0, st>>>(s.b.rs_cnt, s.b.rs_off, s.b.rs_cur, nu);
+      k_rr_tile_pieces<true><<<gp, 256, 0, st>>>(s.b, s.dv, ix->rt_ubase, s.b.rs_cur, s.b.rseg);
       const size_t smem = (size_t)rt_rows(rowb) * rowb;
       if (ip) {
         set_smem(k_rerank_tile<4, true>, smem);
-        k_rerank_tile<4, true><<<ix->rt_nunits, kRtNT, smem, st>>>(s.b, s.dv, s.b.rseg, ix->rt_units);
+        k_rerank_tile<4, true><<<nu, kRtNT, smem, st>>>(s.b, s.dv, s.b.rseg, ix->rt_units, s.b.rs_off);
       } else {
         set_smem(k_rerank_tile<4, false>, smem);
-        k_rerank_tile<4, false><<<ix->rt_nunits, kRtNT, smem, st>>>(s.b, s.dv, s.b.rseg, ix->rt_units);
+        k_rerank_tile<4, false><<<nu, kRtNT, smem, st>>>(s.b, s.dv, s.b.rseg, ix->rt_units, s.b.rs_off);
       }
       g_launches += 4;
       return;
     }
+    cudaMemsetAsync(s.b.rs_cnt, 0, (size_t)(ix->nlist + 1) * 4, st);
+    k_rr_segments<false><<<gp, 256, 0, st>>>(s.b, s.b.rs_cnt, s.b.rseg, rr_piece(rowb));
+    k_inv_scan<<<1, 1024, 0, st>>>(s.b.rs_cnt, s.b.rs_off, s.b.rs_cur, ix->nlist);
+    k_rr_segments<true><<<gp, 256, 0, st>>>(s.b, s.b.rs_cur, s.b.rseg, rr_piece(rowb));
     if (ip) launch_rerank_list<true>(s, st, rowb);
     else launch_rerank_list<false>(s, st, rowb);
     g_launches += 5;
@@ -1548,11 +1559,17 @@ bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_
     // (list, tile) units of the shared-memory re-rank, in list order
     const int R = rt_rows(d * 4);
     std::vector<int2> units;
-    for (int L = 0; L < nlist; ++L)
+    std::vector<int> ubase(nlist);
+    for (int L = 0; L < nlist; ++L) {
+      ubase[L] = (int)units.size();
       for (int t = 0; t * R < ix->lsize[L]; ++t) units.push_back(make_int2(L, t));
+      ix->rt_maxtiles = std::max(ix->rt_maxtiles, (ix->lsize[L] + R - 1) / R);
+    }
     ix->rt_nunits = (int)units.size();
     ok = dalloc((void**)&ix->rt_units, units.size() * 8) &&
-         cudaMemcpy(ix->rt_units, units.data(), units.size() * 8, cudaMemcpyHostToDevice) == cudaSuccess;
+         cudaMemcpy(ix->rt_units, units.data(), units.size() * 8, cudaMemcpyHostToDevice) == cudaSuccess &&
+         dalloc((void**)&ix->rt_ubase, (size_t)nlist * 4) &&
+         cudaMemcpy(ix->rt_ubase, ubase.data(), (size_t)nlist * 4, cudaMemcpyHostToDevice) == cudaSuccess;
   }
   cudaDeviceGetAttribute(&ix->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
   cudaDeviceGetAttribute(&ix->l2_bytes, cudaDevAttrL2CacheSize, cuda_device);
@@ -1594,7 +1611,7 @@ void ivf_free(bbc_index ix) {
   void* ptrs[] = {ix->centroids, ix->loff, ix->gsize_d, ix->ids, ix->books, ix->codes, ix->P,
                   ix->wL, ix->bits, ix->factors, ix->raw, ix->stats, ix->codes_t, ix->tbase,
                   ix->cmu, ix->cnorm, ix->rbq_tiles, ix->rbq_pc, ix->lrank, ix->pb_hi, ix->pb_lo,
-                  ix->nccl_scratch, ix->rt_units};
+                  ix->nccl_scratch, ix->rt_units, ix->rt_ubase};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& t : ix->timers) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }

@@ -20,9 +20,50 @@ constexpr int kRtBytes = 96 * 1024;           // rows per tile = kRtBytes / row 
 
 __host__ __device__ constexpr int rt_rows(int rowb) { return kRtBytes / rowb; }
 
+// Pieces per (list, tile) unit.  A segment -- the sorted run of candidate rows a query has in one
+// list -- is cut at the list's tile boundaries (binary search of its rows) and each part into
+// pieces of <= 64 candidates, counted (FILL = 0) or written (FILL = 1) at the unit's cursor, so
+// every tile CTA sees exactly the candidates in its rows.  One thread per (query, probe) pair.
+template <bool FILL>
+__global__ void __launch_bounds__(256) k_rr_tile_pieces(Batch b, Dev ix, const int* __restrict__ ubase,
+                                                        int* __restrict__ cnt, int4* __restrict__ seg) {
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= (long long)b.nq * b.nprobe) return;
+  const int2 g = rr_segment(b, p);
+  if (g.y <= 0) return;
+  const int q = (int)(p / b.nprobe);
+  const int L = b.probe[p];
+  const int R = rt_rows(ix.d * 4);
+  const long long l0 = ix.loff[L];
+  const int* cp = b.cpos + (size_t)q * b.cap + g.x;
+  const int t0 = (int)((cp[0] - l0) / R), t1 = (int)((cp[g.y - 1] - l0) / R);
+  int a = 0;
+  for (int t = t0; t <= t1; ++t) {
+    int e = g.y;                                     // first candidate of the segment past tile t
+    if (t < t1) {
+      const long long lim = l0 + (long long)(t + 1) * R;
+      int lo = a, hi = g.y;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (cp[mid] < lim) lo = mid + 1; else hi = mid;
+      }
+      e = lo;
+    }
+    const int n = e - a;
+    if (n > 0) {
+      const int np = (n + 63) / 64;
+      const int at = atomicAdd(cnt + ubase[L] + t, np);
+      if (FILL)
+        for (int i = 0; i < np; ++i) seg[at + i] = make_int4(q, g.x + a + 64 * i, min(64, n - 64 * i), 0);
+    }
+    a = e;
+  }
+}
+
 template <int MAXV, bool IP>
 __global__ void __launch_bounds__(kRtNT, 2) k_rerank_tile(Batch b, Dev ix, const int4* __restrict__ seg,
-                                                          const int2* __restrict__ units) {
+                                                          const int2* __restrict__ units,
+                                                          const int* __restrict__ uoff) {
   constexpr int LPC = 8, CPW = 32 / LPC;
   extern __shared__ __align__(128) uint8_t rtsm[];
   __shared__ uint64_t bar;
@@ -31,8 +72,8 @@ __global__ void __launch_bounds__(kRtNT, 2) k_rerank_tile(Batch b, Dev ix, const
   const int R = rt_rows(rowb);
   const int2 u = units[blockIdx.x];                   // (list, tile)
   const int L = u.x;
-  const int p0 = b.rs_off[L], p1 = b.rs_off[L + 1];
-  if (p0 == p1) return;                               // no candidate of this micro-batch in L
+  const int p0 = uoff[blockIdx.x], p1 = uoff[blockIdx.x + 1];
+  if (p0 == p1) return;                               // no candidate of this micro-batch in the tile
   const long long lo = ix.loff[L] + (long long)u.y * R;
   const long long hi = min(ix.loff[L + 1], lo + R);
   const uint32_t bsm = smem_u32(&bar);
