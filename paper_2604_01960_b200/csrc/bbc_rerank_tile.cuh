@@ -93,59 +93,71 @@ __global__ void __launch_bounds__(kRtNT, 2) k_rerank_tile(Batch b, Dev ix, const
   const int sub = lane / LPC, sl = lane % LPC;
   RrQuery<false, LPC, MAXV> Q;
   int qcur = -1;
+  const uint32_t tbase = smem_u32(rtsm) - (uint32_t)(lo * rowb);   // + row * rowb = staged row
+  // one candidate (8 lanes): d^2 of staged row rr in rr_rows32's arithmetic order
+  auto dist = [&](int rr, bool on) -> float {
+    const uint32_t row = tbase + (uint32_t)rr * (uint32_t)rowb;
+    float acc = 0.f;
+#pragma unroll
+    for (int v = 0; v < MAXV; ++v) {
+      const int t = sl + LPC * v;
+      if (v < per && t < nv && on) {
+        float4 x;
+        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w) : "r"(row + 16u * (uint32_t)t));
+        if (IP) {
+          acc = fmaf(x.x, Q.qr[v][0], acc);
+          acc = fmaf(x.y, Q.qr[v][1], acc);
+          acc = fmaf(x.z, Q.qr[v][2], acc);
+          acc = fmaf(x.w, Q.qr[v][3], acc);
+        } else {
+          const float a0 = x.x - Q.qr[v][0], a1 = x.y - Q.qr[v][1];
+          const float a2 = x.z - Q.qr[v][2], a3 = x.w - Q.qr[v][3];
+          acc = fmaf(a0, a0, acc);
+          acc = fmaf(a1, a1, acc);
+          acc = fmaf(a2, a2, acc);
+          acc = fmaf(a3, a3, acc);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = LPC / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    return acc;
+  };
   mbar_wait(bsm, 0);
 #pragma unroll 1
   for (int p = p0 + wid; p < p1; p += kRtNT / 32) {
-    const int4 pc = seg[p];                           // (query, first candidate, length)
-    const int q = pc.x;
+    // every load of the piece issued up front: its candidate rows, the query slice, the rows'
+    // original ids (the pieces lie inside this tile by construction, k_rr_tile_pieces)
+    const int4 pc = seg[p];                           // (query, first candidate, length <= 64)
+    const int q = pc.x, n = pc.z;
     const size_t base = (size_t)q * b.cap + pc.y;
+    const int r0 = lane < n ? b.cpos[base + lane] : (int)lo;
+    const int r1 = lane + 32 < n ? b.cpos[base + 32 + lane] : (int)lo;
+    if (q != qcur) {
+      Q.load(b.Q + (size_t)q * ix.d, sl, per, nv);
+      qcur = q;
+    }
+    const int id0 = lane < n ? (int)__ldg(ix.ids + r0) : 0;
+    const int id1 = lane + 32 < n ? (int)__ldg(ix.ids + r1) : 0;
 #pragma unroll 1
-    for (int c0 = 0; c0 < pc.z; c0 += 32) {
-      const int n32 = min(32, pc.z - c0);
-      const int r = lane < n32 ? b.cpos[base + c0 + lane] : -1;
-      const bool in = lane < n32 && r >= lo && r < hi;
-      const unsigned m = __ballot_sync(0xffffffffu, in);
-      const int cnt = __popc(m);
-      if (cnt == 0) continue;
-      if (q != qcur) {
-        Q.load(b.Q + (size_t)q * ix.d, sl, per, nv);
-        qcur = q;
-      }
+    for (int c0 = 0; c0 < n; c0 += 32) {
+      const int n32 = min(32, n - c0);
+      const int r = c0 ? r1 : r0, idv = c0 ? id1 : id0;
 #pragma unroll 1
-      for (int s = 0; s < cnt; s += CPW) {
-        const int j = s + sub;                         // the j-th in-tile candidate of the chunk
-        const int bit = j < cnt ? (int)__fns(m, 0, j + 1) : 0;
-        const int rr = __shfl_sync(0xffffffffu, r, bit);
-        const uint32_t row = smem_u32(rtsm) + (uint32_t)((rr - lo) * rowb);
-        float acc = 0.f;
-#pragma unroll
-        for (int v = 0; v < MAXV; ++v) {
-          const int t = sl + LPC * v;
-          if (v < per && t < nv && j < cnt) {
-            float4 x;
-            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                         : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w) : "r"(row + 16u * (uint32_t)t));
-            if (IP) {
-              acc = fmaf(x.x, Q.qr[v][0], acc);
-              acc = fmaf(x.y, Q.qr[v][1], acc);
-              acc = fmaf(x.z, Q.qr[v][2], acc);
-              acc = fmaf(x.w, Q.qr[v][3], acc);
-            } else {
-              const float a0 = x.x - Q.qr[v][0], a1 = x.y - Q.qr[v][1];
-              const float a2 = x.z - Q.qr[v][2], a3 = x.w - Q.qr[v][3];
-              acc = fmaf(a0, a0, acc);
-              acc = fmaf(a1, a1, acc);
-              acc = fmaf(a2, a2, acc);
-              acc = fmaf(a3, a3, acc);
-            }
-          }
+      for (int s = 0; s < n32; s += 2 * CPW) {         // two candidates per lane group in flight
+        const int ja = s + sub, jb = s + CPW + sub;
+        const int ra = __shfl_sync(0xffffffffu, r, ja & 31), rb = __shfl_sync(0xffffffffu, r, jb & 31);
+        const int ia = __shfl_sync(0xffffffffu, idv, ja & 31), ib = __shfl_sync(0xffffffffu, idv, jb & 31);
+        const float da = dist(ra, ja < n32);
+        const float db = dist(rb, jb < n32);
+        if (sl == 0 && ja < n32) {
+          b.val[base + c0 + ja] = IP ? -da : da;
+          b.cid[base + c0 + ja] = ia;
         }
-#pragma unroll
-        for (int o = LPC / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (sl == 0 && j < cnt) {
-          const size_t k = base + c0 + bit;
-          b.val[k] = IP ? -acc : acc;
-          b.cid[k] = (int)__ldg(ix.ids + rr);
+        if (sl == 0 && jb < n32) {
+          b.val[base + c0 + jb] = IP ? -db : db;
+          b.cid[base + c0 + jb] = ib;
         }
       }
     }
