@@ -787,13 +787,16 @@ void stage_rerank(Shard& s, cudaStream_t st) {
       k_inv_scan<<<1, 1024, 0, st>>>(s.b.rs_cnt, s.b.rs_off, s.b.rs_cur, nu);
       k_rr_tile_pieces<true><<<gp, 256, 0, st>>>(s.b, s.dv, ix->rt_ubase, s.b.rs_cur, s.b.rseg);
       const size_t smem = (size_t)rt_rows(rowb) * rowb;
-      if (ip) {
-        set_smem(k_rerank_tile<4, true>, smem);
-        k_rerank_tile<4, true><<<nu, kRtNT, smem, st>>>(s.b, s.dv, s.b.rseg, ix->rt_units, s.b.rs_off);
-      } else {
-        set_smem(k_rerank_tile<4, false>, smem);
-        k_rerank_tile<4, false><<<nu, kRtNT, smem, st>>>(s.b, s.dv, s.b.rseg, ix->rt_units, s.b.rs_off);
-      }
+#define BBC_RT(RB, IPV)                                                                          \
+  do {                                                                                          \
+    set_smem(k_rerank_tile<RB, IPV>, smem);                                                     \
+    k_rerank_tile<RB, IPV><<<nu, kRtNT, smem, st>>>(s.b, s.dv, s.b.rseg, ix->rt_units, s.b.rs_off); \
+  } while (0)
+      if (rowb == 128) { if (ip) BBC_RT(128, true); else BBC_RT(128, false); }
+      else if (rowb == 256) { if (ip) BBC_RT(256, true); else BBC_RT(256, false); }
+      else if (rowb == 384) { if (ip) BBC_RT(384, true); else BBC_RT(384, false); }
+      else { if (ip) BBC_RT(512, true); else BBC_RT(512, false); }
+#undef BBC_RT
       g_launches += 4;
       return;
     }
@@ -1555,7 +1558,7 @@ bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_
     }
     ix->rbq_tc = ok ? 1 : 0;
   }
-  if (ok && !raw_u8 && (size_t)d * 4 <= 512 && ix->n_local > 0) {
+  if (ok && !raw_u8 && (d * 4 == 128 || d * 4 == 256 || d * 4 == 384 || d * 4 == 512) && ix->n_local > 0) {
     // (list, tile) units of the shared-memory re-rank, in list order
     const int R = rt_rows(d * 4);
     std::vector<int2> units;

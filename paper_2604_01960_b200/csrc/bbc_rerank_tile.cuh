@@ -60,16 +60,19 @@ __global__ void __launch_bounds__(256) k_rr_tile_pieces(Batch b, Dev ix, const i
   }
 }
 
-template <int MAXV, bool IP>
+// ROWB = row bytes (384: C4, 512: C2).  A warp's 4 lane groups of 8 lanes work on 4 different
+// pieces at once (each group holds its own query's slice in registers), so the dependent loads of
+// a piece -- its record, candidate rows, ids, query -- of 4 pieces are in flight together; a group
+// walks its piece's candidates in rounds of 8 (lane sl holds candidate 8i + sl's row and id).
+template <int ROWB, bool IP>
 __global__ void __launch_bounds__(kRtNT, 2) k_rerank_tile(Batch b, Dev ix, const int4* __restrict__ seg,
                                                           const int2* __restrict__ units,
                                                           const int* __restrict__ uoff) {
-  constexpr int LPC = 8, CPW = 32 / LPC;
+  constexpr int LPC = 8, NV = ROWB / 16, PER = (NV + LPC - 1) / LPC;
+  constexpr int R = kRtBytes / ROWB;
+  static_assert(NV % LPC == 0, "rows of whole 128-byte lane-group strides");
   extern __shared__ __align__(128) uint8_t rtsm[];
   __shared__ uint64_t bar;
-  const int rowb = ix.d * 4;
-  const int nv = rowb / 16, per = (nv + LPC - 1) / LPC;
-  const int R = rt_rows(rowb);
   const int2 u = units[blockIdx.x];                   // (list, tile)
   const int L = u.x;
   const int p0 = uoff[blockIdx.x], p1 = uoff[blockIdx.x + 1];
@@ -83,81 +86,65 @@ __global__ void __launch_bounds__(kRtNT, 2) k_rerank_tile(Batch b, Dev ix, const
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    const uint32_t bytes = (uint32_t)((hi - lo) * rowb);
+    const uint32_t bytes = (uint32_t)((hi - lo) * ROWB);
     mbar_arrive_tx(bsm, bytes);
-    const uint8_t* src = static_cast<const uint8_t*>(ix.raw) + lo * rowb;
+    const uint8_t* src = static_cast<const uint8_t*>(ix.raw) + lo * ROWB;
     for (uint32_t o = 0; o < bytes; o += 32768u)
       bulk_g2s(smem_u32(rtsm) + o, src + o, min(32768u, bytes - o), bsm);
   }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int sub = lane / LPC, sl = lane % LPC;
-  RrQuery<false, LPC, MAXV> Q;
-  int qcur = -1;
-  const uint32_t tbase = smem_u32(rtsm) - (uint32_t)(lo * rowb);   // + row * rowb = staged row
-  // one candidate (8 lanes): d^2 of staged row rr in rr_rows32's arithmetic order
-  auto dist = [&](int rr, bool on) -> float {
-    const uint32_t row = tbase + (uint32_t)rr * (uint32_t)rowb;
-    float acc = 0.f;
-#pragma unroll
-    for (int v = 0; v < MAXV; ++v) {
-      const int t = sl + LPC * v;
-      if (v < per && t < nv && on) {
-        float4 x;
-        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                     : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w) : "r"(row + 16u * (uint32_t)t));
-        if (IP) {
-          acc = fmaf(x.x, Q.qr[v][0], acc);
-          acc = fmaf(x.y, Q.qr[v][1], acc);
-          acc = fmaf(x.z, Q.qr[v][2], acc);
-          acc = fmaf(x.w, Q.qr[v][3], acc);
-        } else {
-          const float a0 = x.x - Q.qr[v][0], a1 = x.y - Q.qr[v][1];
-          const float a2 = x.z - Q.qr[v][2], a3 = x.w - Q.qr[v][3];
-          acc = fmaf(a0, a0, acc);
-          acc = fmaf(a1, a1, acc);
-          acc = fmaf(a2, a2, acc);
-          acc = fmaf(a3, a3, acc);
-        }
-      }
-    }
-#pragma unroll
-    for (int o = LPC / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    return acc;
-  };
+  const int grp = lane / LPC, sl = lane % LPC;
+  const unsigned gmask = 0xFFu << (LPC * grp);
+  const uint32_t tbase = smem_u32(rtsm) - (uint32_t)(lo * ROWB) + 16u * (uint32_t)sl;
   mbar_wait(bsm, 0);
 #pragma unroll 1
-  for (int p = p0 + wid; p < p1; p += kRtNT / 32) {
-    // every load of the piece issued up front: its candidate rows, the query slice, the rows'
-    // original ids (the pieces lie inside this tile by construction, k_rr_tile_pieces)
+  for (int pp = p0 + 4 * wid; pp < p1; pp += 4 * (kRtNT / 32)) {
+    const int p = pp + grp;
+    if (p >= p1) continue;                            // whole lane group idle
     const int4 pc = seg[p];                           // (query, first candidate, length <= 64)
     const int q = pc.x, n = pc.z;
     const size_t base = (size_t)q * b.cap + pc.y;
-    const int r0 = lane < n ? b.cpos[base + lane] : (int)lo;
-    const int r1 = lane + 32 < n ? b.cpos[base + 32 + lane] : (int)lo;
-    if (q != qcur) {
-      Q.load(b.Q + (size_t)q * ix.d, sl, per, nv);
-      qcur = q;
+    float qr[PER][4];                                 // the lane's chunks t = sl + 8v of the query
+    const float4* q4 = reinterpret_cast<const float4*>(b.Q + (size_t)q * ix.d);
+#pragma unroll
+    for (int v = 0; v < PER; ++v) {
+      const float4 x = q4[sl + LPC * v];
+      qr[v][0] = x.x; qr[v][1] = x.y; qr[v][2] = x.z; qr[v][3] = x.w;
     }
-    const int id0 = lane < n ? (int)__ldg(ix.ids + r0) : 0;
-    const int id1 = lane + 32 < n ? (int)__ldg(ix.ids + r1) : 0;
 #pragma unroll 1
-    for (int c0 = 0; c0 < n; c0 += 32) {
-      const int n32 = min(32, n - c0);
-      const int r = c0 ? r1 : r0, idv = c0 ? id1 : id0;
+    for (int c0 = 0; c0 < n; c0 += LPC) {
+      const int m = min(LPC, n - c0);
+      const int rme = sl < m ? b.cpos[base + c0 + sl] : (int)lo;
+      const int ime = sl < m ? (int)__ldg(ix.ids + rme) : 0;
 #pragma unroll 1
-      for (int s = 0; s < n32; s += 2 * CPW) {         // two candidates per lane group in flight
-        const int ja = s + sub, jb = s + CPW + sub;
-        const int ra = __shfl_sync(0xffffffffu, r, ja & 31), rb = __shfl_sync(0xffffffffu, r, jb & 31);
-        const int ia = __shfl_sync(0xffffffffu, idv, ja & 31), ib = __shfl_sync(0xffffffffu, idv, jb & 31);
-        const float da = dist(ra, ja < n32);
-        const float db = dist(rb, jb < n32);
-        if (sl == 0 && ja < n32) {
-          b.val[base + c0 + ja] = IP ? -da : da;
-          b.cid[base + c0 + ja] = ia;
+      for (int c = 0; c < m; ++c) {
+        const int rr = __shfl_sync(gmask, rme, c, LPC);
+        const uint32_t row = tbase + (uint32_t)rr * (uint32_t)ROWB;
+        float acc = 0.f;
+#pragma unroll
+        for (int v = 0; v < PER; ++v) {               // rr_rows32's order: chunk by chunk, x y z w
+          float4 x;
+          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                       : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w) : "r"(row + 16u * LPC * v));
+          if (IP) {
+            acc = fmaf(x.x, qr[v][0], acc);
+            acc = fmaf(x.y, qr[v][1], acc);
+            acc = fmaf(x.z, qr[v][2], acc);
+            acc = fmaf(x.w, qr[v][3], acc);
+          } else {
+            const float a0 = x.x - qr[v][0], a1 = x.y - qr[v][1];
+            const float a2 = x.z - qr[v][2], a3 = x.w - qr[v][3];
+            acc = fmaf(a0, a0, acc);
+            acc = fmaf(a1, a1, acc);
+            acc = fmaf(a2, a2, acc);
+            acc = fmaf(a3, a3, acc);
+          }
         }
-        if (sl == 0 && jb < n32) {
-          b.val[base + c0 + jb] = IP ? -db : db;
-          b.cid[base + c0 + jb] = ib;
+#pragma unroll
+        for (int o = LPC / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(gmask, acc, o, LPC);
+        if (sl == c) {                                // the lane holding this candidate's id writes
+          b.val[base + c0 + c] = IP ? -acc : acc;
+          b.cid[base + c0 + c] = ime;
         }
       }
     }
