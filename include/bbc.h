@@ -156,11 +156,10 @@ bbc_status bbc_set_scan_mode(bbc_index index, int32_t mode);
  *                      lists shared by every query probing them and are served from L2.
  *   BBC_RERANK_TILE  : list order with each list's rows staged in shared memory, one tile of
  *                      consecutive rows per CTA by a bulk copy, every candidate of every query in
- *                      that tile computed from shared memory (fp32 rows of <= 512 bytes;
- *                      BBC_ERR_ARG otherwise).
- *   BBC_RERANK_AUTO  : (default) list order when the micro-batch re-ranks each row >= 4 times
- *                      on average (nq * budget / N) -- TILE where available, else LIST -- and
- *                      QUERY otherwise.
+ *                      that tile computed from shared memory (fp32 rows of 128, 256, 384 or 512
+ *                      bytes; BBC_ERR_ARG otherwise).  Measured slower than LIST.
+ *   BBC_RERANK_AUTO  : (default) LIST when the micro-batch re-ranks each row >= 4 times on
+ *                      average (nq * budget / N), else QUERY.
  * BBC_ERR_ARG for a null index or an unknown order.  Must not change while a search on the
  * handle is in flight.
  */

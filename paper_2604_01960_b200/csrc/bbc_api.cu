@@ -688,10 +688,11 @@ bool rerank_list_order(const bbc_index_s* ix, const Batch& b, int rowb) {
 }
 
 // list order with the list's rows staged in shared memory tile by tile (bbc_rerank_tile.cuh):
-// available for fp32 rows of <= 512 bytes; AUTO takes it whenever list order is chosen
+// available for fp32 rows of 128-512 bytes, on request only -- measured slower than the L2-fed
+// list order (C4 25.4 -> 37.0 ms, C2 0.90 -> 1.51 ms), so AUTO does not take it
 bool rerank_tile(const bbc_index_s* ix, const Batch& b, int rowb) {
   if (!ix->rt_units || !rerank_list_order(ix, b, rowb)) return false;
-  return ix->rerank_order == BBC_RERANK_TILE || ix->rerank_order == BBC_RERANK_AUTO;
+  return ix->rerank_order == BBC_RERANK_TILE;
 }
 
 void stage_compact(Shard& s, cudaStream_t st) {
@@ -1677,7 +1678,7 @@ bbc_status bbc_set_rerank_order(bbc_index ix, int32_t order) {
       order != BBC_RERANK_TILE)
     return fail(BBC_ERR_ARG, "unknown re-rank order");
   if (order == BBC_RERANK_TILE && !ix->rt_units)
-    return fail(BBC_ERR_ARG, "the shared-memory re-rank needs fp32 rows of <= 512 bytes");
+    return fail(BBC_ERR_ARG, "the shared-memory re-rank needs fp32 rows of 128, 256, 384 or 512 bytes");
   ix->rerank_order = order;
   return BBC_OK;
 }
