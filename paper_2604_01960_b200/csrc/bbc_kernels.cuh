@@ -611,35 +611,6 @@ __device__ __forceinline__ void static_for(F&& f) {
   }
 }
 
-// Two fp32 sums advanced by one packed add (FADD2, sm_100): each half is an IEEE
-// round-to-nearest add of its own operands, i.e. exactly __fadd_rn per object.
-__device__ __forceinline__ unsigned long long fadd2(unsigned long long a, float x, float y) {
-  unsigned long long b, r;
-  asm("mov.b64 %0, {%1,%2};" : "=l"(b) : "f"(x), "f"(y));
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ float2 unpack2(unsigned long long a) {
-  float2 r;
-  asm("mov.b64 {%0,%1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(a));
-  return r;
-}
-
-// the sums of two objects (code words w0, w1) += their 4 LUT entries of this chunk, sub-quantizer
-// by sub-quantizer (canonical order within each object)
-__device__ __forceinline__ unsigned long long rq_lookup4x2(unsigned long long a, uint32_t w0, uint32_t w1,
-                                                           uint32_t lane4) {
-  a = fadd2(a, lds_imm<kRqSmemBase + 0>(__byte_perm(w0, lane4, 0x7604)),
-            lds_imm<kRqSmemBase + 0>(__byte_perm(w1, lane4, 0x7604)));
-  a = fadd2(a, lds_imm<kRqSmemBase + 128>(__byte_perm(w0, lane4, 0x7614)),
-            lds_imm<kRqSmemBase + 128>(__byte_perm(w1, lane4, 0x7614)));
-  a = fadd2(a, lds_imm<kRqSmemBase + 65536>(__byte_perm(w0, lane4, 0x7624)),
-            lds_imm<kRqSmemBase + 65536>(__byte_perm(w1, lane4, 0x7624)));
-  a = fadd2(a, lds_imm<kRqSmemBase + 65536 + 128>(__byte_perm(w0, lane4, 0x7634)),
-            lds_imm<kRqSmemBase + 65536 + 128>(__byte_perm(w1, lane4, 0x7634)));
-  return a;
-}
-
 // acc += the 4 LUT entries selected by code word w (sub-quantizers 4p..4p+3, canonical order)
 __device__ __forceinline__ float rq_lookup4(float a, uint32_t w, uint32_t lane4) {
   a = __fadd_rn(a, lds_imm<kRqSmemBase + 0>(__byte_perm(w, lane4, 0x7604)));
@@ -739,9 +710,9 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
     }
     return __ldg(c16 + (g + 8u * (uint32_t)p));
   };
-  unsigned long long acc2[kRqEW / 2];                 // objects (2e, 2e+1) as packed fp32 pairs
+  float acc[kRqEW];
 #pragma unroll
-  for (int e = 0; e < kRqEW / 2; ++e) acc2[e] = 0ull;
+  for (int e = 0; e < kRqEW; ++e) acc[e] = 0.f;
   const uint32_t lane4 = (uint32_t)lane * 4u;
   uint4 cw[kRqDepth];
   static_for<kRqDepth>([&](auto ic) { cw[decltype(ic)::value] = ldc(ic, 0); });
@@ -776,16 +747,11 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
         cw[i % kRqDepth] = ldc(std::integral_constant<int, i + kRqDepth>{}, p);
       else
         cw[i % kRqDepth] = ldc(std::integral_constant<int, i + kRqDepth - kRqGPL>{}, pn);
-      acc2[2 * i + 0] = rq_lookup4x2(acc2[2 * i + 0], c.x, c.y, lane4);
-      acc2[2 * i + 1] = rq_lookup4x2(acc2[2 * i + 1], c.z, c.w, lane4);
+      acc[4 * i + 0] = rq_lookup4(acc[4 * i + 0], c.x, lane4);
+      acc[4 * i + 1] = rq_lookup4(acc[4 * i + 1], c.y, lane4);
+      acc[4 * i + 2] = rq_lookup4(acc[4 * i + 2], c.z, lane4);
+      acc[4 * i + 3] = rq_lookup4(acc[4 * i + 3], c.w, lane4);
     });
-  }
-  float acc[kRqEW];
-#pragma unroll
-  for (int e = 0; e < kRqEW / 2; ++e) {
-    const float2 v = unpack2(acc2[e]);
-    acc[2 * e] = v.x;
-    acc[2 * e + 1] = v.y;
   }
   // epilogue: lane l holds objects 4(l&7)+j of its groups
   CellFn cf;
