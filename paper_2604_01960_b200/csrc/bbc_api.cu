@@ -3,7 +3,6 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
-#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <numeric>
@@ -1048,9 +1047,6 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
       Batch& b = s.b;
       b.nq = nb; b.nprobe = nprobe; b.k = k; b.budget = budget_c; b.cap = s.p.cap;
       b.nbuckets = s.ix->nbuckets;
-      // PROTOTYPE switch for the Algorithm 4 measurement: BBC_PROTO_EARLY=1
-      static const bool proto_early = getenv("BBC_PROTO_EARLY") && getenv("BBC_PROTO_EARLY")[0] == '1';
-      b.tpred = (proto_early && !dist && ix->kind == BBC_KIND_PQ && ix->nbits == 8) ? b.tau : nullptr;
       b.remap_m = s.ix->remap_m;
       b.stats = s.ix->stats;
       if (host) {

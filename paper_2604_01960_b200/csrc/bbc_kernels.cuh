@@ -51,8 +51,6 @@ struct Batch {
   int* rs_cnt;        // [nlist + 1]    piece counts (rs_off[nlist] = #pieces)
   int* rs_off;        // [nlist + 1]
   int* rs_cur;        // [nlist + 1]
-  int* tpred;         // PROTOTYPE (Alg. 4 measurement): predicted threshold bucket per
-                      // query, or nullptr (off)
 };
 
 // Index arrays on the device.
@@ -587,8 +585,7 @@ constexpr int kRqOffOut = kRqOffGo + kRqGroups * 4;
 constexpr int kRqOffCnt = kRqOffOut + kRqGroups * 8;
 constexpr int kRqOffHist = kRqOffCnt + kRqGroups * 4;
 constexpr int kRqOffPo = kRqOffHist + kCells * 4;
-constexpr int kRqOffRow = kRqOffPo + (kMaxProbe + 1) * 4 + 4;      // 8-aligned: kMaxProbe + 2 ints
-constexpr size_t kRqSmem = kRqOffRow + kRqGroups * 8;
+constexpr size_t kRqSmem = kRqOffPo + (kMaxProbe + 1) * 4;
 // The kernel has no static shared memory, so its dynamic buffer starts right after the 1 KB
 // the driver reserves per CTA; the LUT lookups use that offset as an immediate (checked).
 constexpr unsigned kRqSmemBase = 1024;
@@ -641,7 +638,6 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
   int* gcnt = reinterpret_cast<int*>(rsm + kRqOffCnt);
   int* hist = reinterpret_cast<int*>(rsm + kRqOffHist);
   int* s_popad = reinterpret_cast<int*>(rsm + kRqOffPo);
-  long long* grow = reinterpret_cast<long long*>(rsm + kRqOffRow);   // PROTOTYPE: group's first row
   // persistent CTAs over the work items of k_scan_plan: (query, pass) in query locality order
   const int nit = *nitems;
   for (int it = blockIdx.x; it < nit; it += gridDim.x) {
@@ -689,7 +685,6 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
       cnt = min(32, nL - i0);
       go = (uint32_t)((tbase[L] + (long long)(i0 >> 5) * M * 32) >> 7);
       oo = obase + po[lo] + i0;
-      grow[G] = ix.loff[L] + i0;
     }
     gofs[G] = go;
     gout[G] = oo;
@@ -781,35 +776,6 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
         }
       }
     }
-  }
-  if (!EST && b.tpred) {
-    // PROTOTYPE of Algorithm 4's early re-ranking, for its measurement only:
-    // objects whose bucket is below the predicted threshold get their exact d^2 here, by the lane
-    // that holds them (written to val at the probe position, overwritten later by the re-rank)
-    const int tp = b.tpred[q];
-    const float4* q4 = reinterpret_cast<const float4*>(b.Q + (size_t)q * ix.d);
-    const int nv4 = ix.d / 4;
-    int early = 0;
-    for (int i = 0; i < kRqGPL; ++i) {
-      const int G = gl0 + 4 * i;
-      const int cnt = gcnt[G];
-      const long long oo = gout[G] + 4 * (lane & 7);
-      for (int j = 0; j < 4; ++j) {
-        if (4 * (lane & 7) + j < cnt && b.cells[oo + j] < tp) {
-          const float4* xr = reinterpret_cast<const float4*>(ix.raw) + (grow[G] + 4 * (lane & 7) + j) * nv4;
-          float a = 0.f;
-          for (int t = 0; t < nv4; ++t) {
-            const float4 x = __ldg(xr + t), y = __ldg(q4 + t);
-            a = fmaf(x.x - y.x, x.x - y.x, a); a = fmaf(x.y - y.y, x.y - y.y, a);
-            a = fmaf(x.z - y.z, x.z - y.z, a); a = fmaf(x.w - y.w, x.w - y.w, a);
-          }
-          b.val[oo + j] = a;
-          ++early;
-        }
-      }
-    }
-    early = warp_sum(early);
-    if (lane == 0 && early) atomicAdd((unsigned long long*)&b.stats[3], (unsigned long long)early);
   }
   if (!EST) {
     __syncthreads();
@@ -1162,19 +1128,6 @@ __global__ void __launch_bounds__(kSelNT) k_select_edges(Batch b, Dev ix) {
     b.edges[2 * q] = lo;
     b.edges[2 * q + 1] = hi;
     atomicAdd((unsigned long long*)&b.stats[2], (unsigned long long)n);   // sample objects
-  }
-  if (CELLS && b.tpred) {
-    // PROTOTYPE (Algorithm 4): the predicted threshold bucket holds the
-    // (|O_sample| / |O| x n_cand)-th estimate of the sample
-    const int ntot = b.poff[(size_t)q * (b.nprobe + 1) + b.nprobe];
-    const unsigned kp = (unsigned)max(1LL, (long long)((double)b.budget * n / max(1, ntot)));
-    unsigned t2;
-    const uint32_t kk = cta_kth32(n, min(kp, (unsigned)n), [&](int i, bool* ok) { *ok = true; return f2key(v[i]); },
-                                  &t2, sm);
-    CellFn cp;
-    cp.init(lo, hi, b.nbuckets);
-    if (threadIdx.x == 0) b.tpred[q] = cp(key2f(kk));
-    __syncthreads();
   }
   if (CELLS) {
     for (int i = threadIdx.x; i < kCells; i += kSelNT) hist[i] = 0;
