@@ -58,6 +58,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0)
     p.add_argument("--sweep", action="store_true", help="recall/QPS over an (nprobe, budget) grid")
+    p.add_argument("--sweep-nprobe", default="", help="comma-separated nprobe multipliers of the sweep")
+    p.add_argument("--sweep-budget", default="", help="comma-separated budget multipliers (x k)")
     p.add_argument("--profile-steps", action="store_true", help="no warm-up/recall/cpu (ncu runs)")
     p.add_argument("--shard", default=None, choices=["queries", "lists"],
                    help="multi-GPU partitioning: lists (default for --gpus > 1: the north_star's "
@@ -338,6 +340,11 @@ def main():
         g = Index(path, device=local)
     g.set_buckets(args.buckets)
     if args.sweep:
+        global args_sweep_nprobe, args_sweep_budget
+        if args.sweep_nprobe:
+            args_sweep_nprobe = tuple(float(x) for x in args.sweep_nprobe.split(","))
+        if args.sweep_budget:
+            args_sweep_budget = tuple(float(x) for x in args.sweep_budget.split(","))
         return sweep(cfg, path, g, rank)
     if args.bucket_sweep:
         return bucket_sweep(cfg, path, g, *operating_point(cfg, args))
@@ -598,6 +605,10 @@ def bucket_sweep(cfg, path, g, nprobe, budget):
     g.set_remap(0)
 
 
+args_sweep_nprobe = None
+args_sweep_budget = None
+
+
 def sweep(cfg, path, g, rank):
     import torch
     X = database_in_id_order(path)
@@ -607,11 +618,13 @@ def sweep(cfg, path, g, rank):
     gi, gd = groundtruth.cached_topk(f"{cfg.name}_{os.path.basename(path)}", Q[:rq], X, cfg.k,
                                      datagen.cache_dir(), metric=cfg.metric)
     st = torch.cuda.current_stream()
-    for nprobe in sorted({cfg.nprobe, 2 * cfg.nprobe, 3 * cfg.nprobe, 4 * cfg.nprobe,
-                          6 * cfg.nprobe, 8 * cfg.nprobe}):
+    # nprobe in {1, 1.5, 2, 3, 4} x the config's (here also 1.25 and 1.75, and
+    # 6 and 8 for the weakly clustered C2/C3), budget in {1, 1.5, 2, 3, 4} x k (and 1.25, 1.75)
+    mults = args_sweep_nprobe or (1, 1.25, 1.5, 1.75, 2, 3, 4, 6, 8)
+    for nprobe in sorted({int(round(m * cfg.nprobe)) for m in mults}):
         if nprobe > cfg.nlist or nprobe > 2048:
             continue
-        for bm in (1.0, 1.5, 2.0, 3.0, 4.0) + ((6.0, 8.0) if cfg.pq_bits == 4 else ()):
+        for bm in (args_sweep_budget or (1.0, 1.25, 1.5, 1.75, 2.0, 3.0, 4.0)) + ((6.0, 8.0) if cfg.pq_bits == 4 else ()):
             budget = int(bm * cfg.k)
             ws = g.workspace(len(Q), cfg.k, nprobe, budget, max_bytes=60 << 30)
             g.search(q, cfg.k, nprobe, budget, workspace=ws)
