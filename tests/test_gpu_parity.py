@@ -298,7 +298,8 @@ def test_recall_matches_oracle():
     ("C2", 128, 20000, 1000, 8),         # BASELINE.json's C2 point
     ("C3", 2048, 20000, 500, 10),        # C3's operating point, 500 queries (~250 pairs per list:
                                          #   several query tiles of the RaBitQ GEMM per list)
-    ("C4", 1024, 75000, 2500, 12),       # C4's operating point, one micro-batch of bench.py's run
+    ("C4", 768, 87500, 2500, 12),        # C4's operating point, one micro-batch of bench.py's run
+    ("C4", 512, 75000, 1000, 6),         # BASELINE.json's C4 point
 ])
 def test_full_size_sampled_parity(name, nprobe, budget, nq, nsel):
     """BASELINE.json configs at full size, at the operating points bench.py times, with the batch
