@@ -625,9 +625,7 @@ void rbq_tc_pass(Shard& s, const Batch& b, cudaStream_t st, bool sample) {
     k_rbq_mma_ws<true><<<ix->rbq_ntiles, kRbWsNT, smw, st>>>(b, s.dv, t, nst, tm);
   } else {
     set_smem(k_rbq_mma_ws<false>, smw);
-    k_rbq_mma_ws<false><<<ix->rbq_ntiles, kRbWsNT, smw, st>>>(b, s.dv, t, nst, tm);
-    k_cell_hist<<<dim3(std::max(1, (8 * ix->num_sms + b.nq - 1) / b.nq), b.nq), 256, 0, st>>>(b);
-    g_launches += 1;
+    k_rbq_mma_ws<false><<<ix->rbq_ntiles, kRbWsNT, smw, st>>>(b, s.dv, t, nst, tm);   // + histogram
   }
   g_launches += 1;
 }
@@ -1070,11 +1068,12 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
       Shard& s = sh[0];
       {
         StageScope sc(s.ix, st, BBC_STAGE_SAMPLE);
-        if (ix->kind == BBC_KIND_PQ) k_select_edges<true><<<nb, kSelNT, 0, st>>>(s.b, s.dv);
-        else k_select_edges<false><<<nb, kSelNT, 0, st>>>(s.b, s.dv);
+        // the sample objects' bucket ids stay a separate wide kernel (k_sample_cells): fused
+        // into this one-CTA-per-query select they cost more (C4: 2.5 + 1.5 -> 4.4 ms)
+        k_select_edges<false><<<nb, kSelNT, 0, st>>>(s.b, s.dv);
         g_launches += 1;
       }
-      stage_scan(s, st, false);
+      stage_scan(s, st, true);
       stage_compact(s, st);
       stage_rerank(s, st);
       const int bi = mb_index & 1;

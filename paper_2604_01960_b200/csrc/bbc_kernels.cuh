@@ -697,6 +697,15 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
   // wavefront per 16 lookups) rather than held in 8 registers, which would spill.
   for (int G = threadIdx.x; G < kRqGroups; G += kRqNT) gofs[G] = gofs[G] * 8u;
   __syncthreads();
+  // L2 prefetch one chunk ahead: thread G pulls group G's 128-byte block of the next chunk into
+  // L2 (no register or shared-memory cost), so that the lane loads of streamed (HBM-resident)
+  // codes wait for L2, not DRAM -- with two 16-byte loads in flight per lane (the register budget)
+  // the scan of C4's codes was bound by DRAM latency (long-scoreboard stalls)
+  const uint8_t* pf = codes_t + 16ull * (kRqGroups == kRqNT ? gofs[threadIdx.x] : 0u);
+  if (kRqGroups == kRqNT && gcnt[threadIdx.x] > 0) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(pf));
+    if (P > 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(pf + 128));
+  }
   const uint32_t gaddr = smem_u32(gofs + gl0);
   const uint4* __restrict__ c16 = reinterpret_cast<const uint4*>(codes_t) + (lane & 7);
   auto ldc = [&](auto ic, int p) -> uint4 {
@@ -719,6 +728,8 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
 #pragma unroll 1
   for (int p = 0; p < P; ++p) {
     __syncthreads();                                  // previous chunk fully consumed
+    if (kRqGroups == kRqNT && p + 2 < P && gcnt[threadIdx.x] > 0)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(pf + 128 * (p + 2)));
     // stage chunk p: entry (mm, c) replicated 32x at words ((mm>>1)*256 + c)*64 + (mm&1)*32 +
     // [0, 32): lane l reads bank l.  Each thread writes its entries as 8 rotated 16-byte
     // stores each (a quarter-warp covers all 32 banks).
