@@ -625,7 +625,12 @@ void rbq_tc_pass(Shard& s, const Batch& b, cudaStream_t st, bool sample) {
     k_rbq_mma_ws<true><<<ix->rbq_ntiles, kRbWsNT, smw, st>>>(b, s.dv, t, nst, tm);
   } else {
     set_smem(k_rbq_mma_ws<false>, smw);
-    k_rbq_mma_ws<false><<<ix->rbq_ntiles, kRbWsNT, smw, st>>>(b, s.dv, t, nst, tm);   // + histogram
+    k_rbq_mma_ws<false><<<ix->rbq_ntiles, kRbWsNT, smw, st>>>(b, s.dv, t, nst, tm);
+    // the histogram from the ids afterwards: formed in the GEMM epilogue with one global
+    // reduction per counted object it was slower (C3 Push 2.10 -> 2.99 ms: the counted ids of a
+    // query crowd a few cells)
+    k_cell_hist<<<dim3(std::max(1, (8 * ix->num_sms + b.nq - 1) / b.nq), b.nq), 256, 0, st>>>(b);
+    g_launches += 1;
   }
   g_launches += 1;
 }

@@ -697,12 +697,14 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
   // wavefront per 16 lookups) rather than held in 8 registers, which would spill.
   for (int G = threadIdx.x; G < kRqGroups; G += kRqNT) gofs[G] = gofs[G] * 8u;
   __syncthreads();
-  // L2 prefetch one chunk ahead: thread G pulls group G's 128-byte block of the next chunk into
-  // L2 (no register or shared-memory cost), so that the lane loads of streamed (HBM-resident)
-  // codes wait for L2, not DRAM -- with two 16-byte loads in flight per lane (the register budget)
-  // the scan of C4's codes was bound by DRAM latency (long-scoreboard stalls)
-  const uint8_t* pf = codes_t + 16ull * (kRqGroups == kRqNT ? gofs[threadIdx.x] : 0u);
-  if (kRqGroups == kRqNT && gcnt[threadIdx.x] > 0) {
+  // Streamed codes (NOALLOC: larger than half of L2): L2 prefetch two chunks ahead -- thread G
+  // pulls group G's 128-byte block into L2 (no register or shared-memory cost), so that the lane
+  // loads wait for L2, not DRAM.  With two 16-byte loads in flight per lane (the register budget)
+  // the scan of C4's codes was bound by DRAM latency (long-scoreboard stalls): C4 scan 52.1 ->
+  // 47.8 ms; on L2-resident codes (C2) the prefetches only cost issue slots (2.92 -> 3.13 ms).
+  constexpr bool kPf = NOALLOC && kRqGroups == kRqNT;
+  const uint8_t* pf = codes_t + 16ull * (kPf ? gofs[threadIdx.x] : 0u);
+  if (kPf && gcnt[threadIdx.x] > 0) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(pf));
     if (P > 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(pf + 128));
   }
@@ -728,7 +730,7 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
 #pragma unroll 1
   for (int p = 0; p < P; ++p) {
     __syncthreads();                                  // previous chunk fully consumed
-    if (kRqGroups == kRqNT && p + 2 < P && gcnt[threadIdx.x] > 0)
+    if (kPf && p + 2 < P && gcnt[threadIdx.x] > 0)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(pf + 128 * (p + 2)));
     // stage chunk p: entry (mm, c) replicated 32x at words ((mm>>1)*256 + c)*64 + (mm&1)*32 +
     // [0, 32): lane l reads bank l.  Each thread writes its entries as 8 rotated 16-byte

@@ -507,9 +507,6 @@ __global__ void __launch_bounds__(kRbWsNT, 1) k_rbq_mma_ws(Batch b, Dev ix, RbqT
             cell = e.degen ? 0 : cell;
             cell = est > e.dmax ? 255 : cell;
             b.cells[at] = (uint8_t)cell;
-            // the Push histogram (Alg. 1 l.1-4) directly: ids < 255 are few (~the budget per
-            // query), so one global reduction per counted object beats re-reading every id
-            if (cell < 255) atomicAdd(&b.hist[(size_t)e.q * kCells + cell], 1);
           }
         }
       }
