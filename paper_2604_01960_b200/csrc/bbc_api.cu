@@ -1051,8 +1051,6 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
       Batch& b = s.b;
       b.nq = nb; b.nprobe = nprobe; b.k = k; b.budget = budget_c; b.cap = s.p.cap;
       b.nbuckets = s.ix->nbuckets;
-      static const int pf_env = getenv("BBC_PF_AHEAD") ? atoi(getenv("BBC_PF_AHEAD")) : -1;   // tuning
-      b.pf_ahead = pf_env >= 0 ? pf_env : 2;
       b.remap_m = s.ix->remap_m;
       b.stats = s.ix->stats;
       if (host) {

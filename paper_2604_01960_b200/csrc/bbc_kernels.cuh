@@ -51,7 +51,6 @@ struct Batch {
   int* rs_cnt;        // [nlist + 1]    piece counts (rs_off[nlist] = #pieces)
   int* rs_off;        // [nlist + 1]
   int* rs_cur;        // [nlist + 1]
-  int pf_ahead;       // chunks of streamed PQ codes prefetched into L2 ahead of the lane loads
 };
 
 // Index arrays on the device.
@@ -698,16 +697,6 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
   // wavefront per 16 lookups) rather than held in 8 registers, which would spill.
   for (int G = threadIdx.x; G < kRqGroups; G += kRqNT) gofs[G] = gofs[G] * 8u;
   __syncthreads();
-  // Streamed codes (NOALLOC: larger than half of L2): L2 prefetch two chunks ahead -- thread G
-  // pulls group G's 128-byte block into L2 (no register or shared-memory cost), so that the lane
-  // loads wait for L2, not DRAM.  With two 16-byte loads in flight per lane (the register budget)
-  // the scan of C4's codes was bound by DRAM latency (long-scoreboard stalls): C4 scan 52.1 ->
-  // 47.8 ms; on L2-resident codes (C2) the prefetches only cost issue slots (2.92 -> 3.13 ms).
-  constexpr bool kPf = NOALLOC && kRqGroups == kRqNT;
-  const uint8_t* pf = codes_t + 16ull * (kPf ? gofs[threadIdx.x] : 0u);
-  const int ahead = b.pf_ahead;
-  if (kPf && gcnt[threadIdx.x] > 0)
-    for (int pp = 0; pp < ahead && pp < P; ++pp) asm volatile("prefetch.global.L2 [%0];" ::"l"(pf + 128 * pp));
   const uint32_t gaddr = smem_u32(gofs + gl0);
   const uint4* __restrict__ c16 = reinterpret_cast<const uint4*>(codes_t) + (lane & 7);
   auto ldc = [&](auto ic, int p) -> uint4 {
@@ -730,8 +719,6 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
 #pragma unroll 1
   for (int p = 0; p < P; ++p) {
     __syncthreads();                                  // previous chunk fully consumed
-    if (kPf && p + ahead < P && gcnt[threadIdx.x] > 0)
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(pf + 128 * (p + ahead)));
     // stage chunk p: entry (mm, c) replicated 32x at words ((mm>>1)*256 + c)*64 + (mm&1)*32 +
     // [0, 32): lane l reads bank l.  Each thread writes its entries as 8 rotated 16-byte
     // stores each (a quarter-warp covers all 32 banks).
