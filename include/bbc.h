@@ -327,7 +327,8 @@ int64_t bbc_launch_count(void);
 /*
  * bbc_measure_l2_read -- measurement utility (not part of the search path): the device's L2 ->
  * SM read bandwidth in GB/s, from CTAs that each stream an L2-resident buffer of `bytes`
- * (>= 1 MiB; choose well below the L2 size) `reps` times with 16-byte loads.  The roofline of
+ * (>= 1 MiB; choose well below the L2 size) `reps` times with 16-byte loads (the best of 4, 8
+ * and 16 loads in flight per thread at 4 and 8 CTAs of 256 threads per SM).  The roofline of
  * the list-order re-rank, whose rows are served from L2.  Allocates and frees its own buffer
  * on `cuda_device`.  BBC_ERR_ARG for bad sizes, BBC_ERR_CUDA on a CUDA failure.
  */

@@ -1214,6 +1214,27 @@ bbc_status run_one(bbc_index ix, const float* queries, int64_t nq, int32_t k, in
 
 }  // namespace
 
+template <int U>
+__global__ void __launch_bounds__(256) k_l2_read(const uint4* __restrict__ buf, long long n16, int reps,
+                                                 unsigned* __restrict__ sink) {
+  unsigned acc = 0;
+  const long long start = ((long long)blockIdx.x * 7919 * 256) % n16;
+  for (int r = 0; r < reps; ++r) {
+    for (long long i = threadIdx.x; i < n16; i += U * 256) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        long long k = start + i + u * 256;
+        k = k >= n16 ? k - n16 : k;
+        v[u] = i + u * 256 < n16 ? __ldcg(buf + k) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc ^= v[u].x ^ v[u].y ^ v[u].z ^ v[u].w;
+    }
+  }
+  if (acc == 0x9e3779b9u) sink[0] = acc;
+}
+
 // ============================================================================================
 // C ABI
 // ============================================================================================
@@ -1222,28 +1243,8 @@ extern "C" {
 const char* bbc_last_error(void) { return g_err.c_str(); }
 int64_t bbc_launch_count(void) { return g_launches.load(); }
 
-// L2 read roofline probe: every CTA streams the whole L2-resident buffer (16-byte loads, 4 in
-// flight per thread, starting at a CTA-specific offset), so after the first pass all reads hit L2.
-__global__ void __launch_bounds__(256) k_l2_read(const uint4* __restrict__ buf, long long n16, int reps,
-                                                 unsigned* __restrict__ sink) {
-  unsigned acc = 0;
-  const long long start = ((long long)blockIdx.x * 7919 * 256) % n16;
-  for (int r = 0; r < reps; ++r) {
-    for (long long i = threadIdx.x; i < n16; i += 4 * 256) {
-      uint4 v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        long long k = start + i + u * 256;
-        k = k >= n16 ? k - n16 : k;
-        v[u] = i + u * 256 < n16 ? __ldcg(buf + k) : make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) acc ^= v[u].x ^ v[u].y ^ v[u].z ^ v[u].w;
-    }
-  }
-  if (acc == 0x9e3779b9u) sink[0] = acc;
-}
-
+// L2 read roofline probe (k_l2_read: every CTA streams the whole L2-resident buffer with 16-byte
+// loads, U in flight per thread, from a CTA-specific offset; after the first pass all reads hit L2).
 bbc_status bbc_measure_l2_read(int32_t cuda_device, size_t bytes, int32_t reps, double* gbs) {
   if (!gbs || bytes < (1u << 20) || reps < 1) return fail(BBC_ERR_ARG, "bad arguments");
   if (cudaSetDevice(cuda_device) != cudaSuccess) return fail(BBC_ERR_CUDA, "cudaSetDevice failed");
@@ -1257,23 +1258,35 @@ bbc_status bbc_measure_l2_read(int32_t cuda_device, size_t bytes, int32_t reps, 
   }
   cudaMemset(buf, 1, bytes);
   const long long n16 = (long long)(bytes / 16);
-  const int grid = sms * 8;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  k_l2_read<<<grid, 256>>>((const uint4*)buf, n16, 1, sink);          // warm L2
-  cudaEventRecord(e0);
-  k_l2_read<<<grid, 256>>>((const uint4*)buf, n16, reps, sink);
-  cudaEventRecord(e1);
-  cudaError_t err = cudaEventSynchronize(e1);
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, e0, e1);
+  // 4, 8 or 16 loads of 16 bytes in flight per thread and 4 or 8 CTAs of 256 threads per SM: the
+  // best rate of the six (latency x bandwidth needs many bytes in flight per SM)
+  double best = 0.0;
+  cudaError_t err = cudaSuccess;
+  for (int cfg = 0; cfg < 6 && err == cudaSuccess; ++cfg) {
+    const int grid = sms * (cfg & 1 ? 8 : 4);
+    auto launch = [&](int r) {
+      if (cfg < 2) k_l2_read<4><<<grid, 256>>>((const uint4*)buf, n16, r, sink);
+      else if (cfg < 4) k_l2_read<8><<<grid, 256>>>((const uint4*)buf, n16, r, sink);
+      else k_l2_read<16><<<grid, 256>>>((const uint4*)buf, n16, r, sink);
+    };
+    launch(1);                                                          // warm L2
+    cudaEventRecord(e0);
+    launch(reps);
+    cudaEventRecord(e1);
+    err = cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms > 0.f) best = std::max(best, (double)grid * reps * (double)(n16 * 16) / (ms * 1e-3) / 1e9);
+  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaFree(buf);
   cudaFree(sink);
-  if (err != cudaSuccess || ms <= 0.f) return fail(BBC_ERR_CUDA, "L2 probe failed");
-  *gbs = (double)grid * reps * (double)(n16 * 16) / (ms * 1e-3) / 1e9;
+  if (err != cudaSuccess || best <= 0.0) return fail(BBC_ERR_CUDA, "L2 probe failed");
+  *gbs = best;
   return BBC_OK;
 }
 
