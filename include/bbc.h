@@ -68,7 +68,9 @@ typedef enum {
  *   (int64 offset, int64 nbytes); sections centroids f32[nlist*d], list_offsets i64[nlist+1],
  *   ids i64[N], codebooks f32[M*256*(d/M)], codes u8[N*M], P f32[D*D], wL f32[nlist*D],
  *   bits u8[N*D/8], factors f32[N*2], raw f32|u8[N*d]; per-object arrays in list order.
- * and upload it to `cuda_device`.  With world > 1 only the lists assigned to `rank` are kept
+ * and upload it to `cuda_device`.  N must be < 2^31 (BBC_ERR_FORMAT otherwise): the kernels
+ * carry rows and original ids as 32-bit integers (the ids file section and out_ids stay int64;
+ * ids are widened on output).  With world > 1 only the lists assigned to `rank` are kept
  * (lists sorted by (size desc, id asc) and given greedily to the least-loaded rank); centroids,
  * codebooks, rotation and every list's size are replicated.  On success *out owns the device
  * arrays until ivf_free.
