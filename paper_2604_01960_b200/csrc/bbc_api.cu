@@ -1076,7 +1076,8 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
         StageScope sc(s.ix, st, BBC_STAGE_SAMPLE);
         // the sample objects' bucket ids stay a separate wide kernel (k_sample_cells): fused
         // into this one-CTA-per-query select they cost more (C4: 2.5 + 1.5 -> 4.4 ms)
-        k_select_edges<false><<<nb, kSelNT, 0, st>>>(s.b, s.dv);
+        set_smem(k_select_edges, kFsSmem);
+        k_select_edges<<<nb, kSelNT, kFsSmem, st>>>(s.b, s.dv);
         g_launches += 1;
       }
       stage_scan(s, st, true);
@@ -1089,7 +1090,8 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
       }
       {
         StageScope sc(s.ix, st, BBC_STAGE_SELECT);
-        k_final_select<<<nb, kSelNT, 0, st>>>(s.b, s.dv, s.oids, s.od2);
+        set_smem(k_final_select, kFsSmem);
+        k_final_select<<<nb, kSelNT, kFsSmem, st>>>(s.b, s.dv, s.oids, s.od2);
         g_launches += 1;
       }
       if (pipe) {

@@ -1105,15 +1105,87 @@ __device__ uint32_t cta_kth32(int n, unsigned kth, KeyF key, unsigned* take, Kth
 }
 
 // ------------------------------------------------------------------------------------------
+// Sampled-bracket selection of the kth smallest key (used by the edge and final selections).
+// The radix selection reads all n keys once per 11-bit digit plus once for min/max (4-5 passes
+// over data that, per micro-batch, no longer fits L2).  Here: kFsS keys at evenly spaced
+// positions are drawn into shared memory, their ranks kth*S/n -/+ kFsMargin give a bracket
+// [L, H] (selected among the sample by cta_kth32 on shared memory), one pass counts the keys
+// below L and gathers the keys in [L, H] (and their ids) into shared memory, and the kth is
+// selected among the gathered keys.  The result is the kth smallest key, the same whatever the
+// method: when the bracket misses it or overflows the buffer, the full radix selection runs.
+// ------------------------------------------------------------------------------------------
+constexpr int kFsS = 4096;                 // sample size
+constexpr int kFsMargin = 160;             // bracket half-width in sample ranks (> 5 sigma)
+constexpr int kFsCap = 8192;               // gathered keys (and ids) held in shared memory
+struct FastSelSmem {
+  uint32_t samp[kFsS];
+  uint32_t key[kFsCap];
+  int id[kFsCap];
+  unsigned cnt, below, mn;
+};
+constexpr size_t kFsSmem = sizeof(FastSelSmem);
+
+// kth smallest of key(i) over i < n (all valid); *take = kth - #(keys < result).  If IDS, the
+// gathered ids (idf(i)) of the keys equal to the result are left in fs.key/fs.id[0, fs.cnt) for
+// the caller's tie split (fs.cnt = UINT_MAX when the fallback ran).  *min_out = smallest key.
+template <bool IDS, typename KeyF, typename IdF>
+__device__ uint32_t cta_kth32_bracket(int n, unsigned kth, KeyF key, IdF idf, unsigned* take, FastSelSmem& fs,
+                                      Kth32Smem& sm, uint32_t* min_out) {
+  constexpr int NT = kSelNT;
+  if (n <= 2 * kFsS) {                                // small: the radix selection directly
+    if (IDS && threadIdx.x == 0) fs.cnt = 0xFFFFFFFFu;
+    __syncthreads();
+    return cta_kth32(n, kth, [&](int i, bool* ok) { *ok = true; return key(i); }, take, sm, min_out);
+  }
+  for (int j = threadIdx.x; j < kFsS; j += NT) fs.samp[j] = key((int)(((long long)j * n) / kFsS));
+  if (threadIdx.x == 0) { fs.cnt = 0; fs.below = 0; fs.mn = 0xFFFFFFFFu; }
+  __syncthreads();
+  const long long r = ((long long)kth * kFsS + n - 1) / n;          // expected sample rank (1-based)
+  const long long rl = r - kFsMargin, rh = r + kFsMargin;
+  unsigned t0;
+  const uint32_t L = rl >= 1 ? cta_kth32(kFsS, (unsigned)rl, [&](int i, bool* ok) { *ok = true; return fs.samp[i]; },
+                                         &t0, sm) : 0u;
+  const uint32_t H = rh <= kFsS ? cta_kth32(kFsS, (unsigned)rh, [&](int i, bool* ok) { *ok = true; return fs.samp[i]; },
+                                            &t0, sm) : 0xFFFFFFFFu;
+  // one pass: count below L, gather [L, H], minimum
+  unsigned below = 0, mn = 0xFFFFFFFFu;
+  for (int i = threadIdx.x; i < n; i += NT) {
+    const uint32_t k = key(i);
+    mn = min(mn, k);
+    below += k < L;
+    if (k >= L && k <= H) {
+      const unsigned at = atomicAdd(&fs.cnt, 1u);
+      if (at < kFsCap) {
+        fs.key[at] = k;
+        if (IDS) fs.id[at] = idf(i);
+      }
+    }
+  }
+  below = warp_sum(below);
+  mn = warp_min(mn);
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&fs.below, below);
+    atomicMin(&fs.mn, mn);
+  }
+  __syncthreads();
+  const unsigned cnt = fs.cnt, nb = fs.below;
+  if (min_out) *min_out = fs.mn;
+  if (cnt > (unsigned)kFsCap || kth <= nb || kth > nb + cnt) {       // bracket missed: full radix
+    __syncthreads();
+    if (IDS && threadIdx.x == 0) fs.cnt = 0xFFFFFFFFu;
+    __syncthreads();
+    return cta_kth32(n, kth, [&](int i, bool* ok) { *ok = true; return key(i); }, take, sm, nullptr);
+  }
+  return cta_kth32((int)cnt, kth - nb, [&](int i, bool* ok) { *ok = true; return fs.key[i]; }, take, sm);
+}
+
+// ------------------------------------------------------------------------------------------
 // a3  edges: d_min = min of the sample estimates, d_max = budget-th smallest
 // ------------------------------------------------------------------------------------------
-// CELLS: also the sample objects' bucket ids and their histogram from the estimates just
-// selected over (one pass more over data the CTA has in L1/L2; replaces k_sample_cells when the
-// edges are local, i.e. not all-reduced across ranks)
-template <bool CELLS>
 __global__ void __launch_bounds__(kSelNT) k_select_edges(Batch b, Dev ix) {
   __shared__ Kth32Smem sm;
-  __shared__ int hist[CELLS ? kCells : 1];
+  extern __shared__ __align__(16) uint8_t fsm[];
+  FastSelSmem& fs = *reinterpret_cast<FastSelSmem*>(fsm);
   const int q = blockIdx.x;
   const int ns = b.nsamp[q];
   if (ns == 0) return;
@@ -1121,28 +1193,12 @@ __global__ void __launch_bounds__(kSelNT) k_select_edges(Batch b, Dev ix) {
   const float* v = b.val + (size_t)q * b.cap;
   unsigned take;
   uint32_t kmin;
-  const uint32_t kmax = cta_kth32(n, (unsigned)b.budget, [&](int i, bool* ok) { *ok = true; return f2key(v[i]); },
-                                  &take, sm, &kmin);
-  const float lo = key2f((uint32_t)kmin), hi = key2f((uint32_t)kmax);
+  const uint32_t kmax = cta_kth32_bracket<false>(n, (unsigned)b.budget, [&](int i) { return f2key(v[i]); },
+                                                 [&](int i) { return 0; }, &take, fs, sm, &kmin);
   if (threadIdx.x == 0) {
-    b.edges[2 * q] = lo;
-    b.edges[2 * q + 1] = hi;
+    b.edges[2 * q] = key2f((uint32_t)kmin);
+    b.edges[2 * q + 1] = key2f((uint32_t)kmax);
     atomicAdd((unsigned long long*)&b.stats[2], (unsigned long long)n);   // sample objects
-  }
-  if (CELLS) {
-    for (int i = threadIdx.x; i < kCells; i += kSelNT) hist[i] = 0;
-    CellFn cf;
-    cf.init(lo, hi, b.nbuckets);
-    __syncthreads();
-    uint8_t* cl = b.cells + (size_t)q * b.cap;
-    for (int i = threadIdx.x; i < n; i += kSelNT) {
-      const int c = cf(v[i]);
-      cl[i] = (uint8_t)c;
-      if (c < 255) atomicAdd(&hist[c], 1);
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < kCells; i += kSelNT)
-      if (hist[i]) atomicAdd(&b.hist[(size_t)q * kCells + i], hist[i]);
   }
 }
 
@@ -1720,6 +1776,8 @@ __global__ void __launch_bounds__(kSelNT) k_final_select(Batch b, Dev ix, long l
                                                          float* out_d2) {
   __shared__ Kth32Smem sm;
   __shared__ int wcnt[kSelNT / 32 + 1];
+  extern __shared__ __align__(16) uint8_t fsm[];
+  FastSelSmem& fs = *reinterpret_cast<FastSelSmem*>(fsm);
   const int q = blockIdx.x;
   const int nc = b.ncand[q];
   const int k = b.k;
@@ -1731,14 +1789,22 @@ __global__ void __launch_bounds__(kSelNT) k_final_select(Batch b, Dev ix, long l
   bool all = true;
   if (nc > k) {
     unsigned take;
-    T = cta_kth32(nc, (unsigned)k, [&](int i, bool* ok) { *ok = true; return f2key(vv[i]); }, &take, sm);
-    // elements equal to T: take the `take` smallest ids (ids are unique)
+    T = cta_kth32_bracket<true>(nc, (unsigned)k, [&](int i) { return f2key(vv[i]); },
+                                [&](int i) { return cp[i]; }, &take, fs, sm, nullptr);
+    // elements equal to T: take the `take` smallest ids (ids are unique) -- from the gathered
+    // bracket when it was used (it holds every key equal to T), else over all candidates
     unsigned t2;
-    I = cta_kth32(nc, take, [&](int i, bool* ok) {
-          const uint32_t f = f2key(vv[i]);
-          *ok = f == T;
-          return *ok ? (uint32_t)cp[i] : 0u;
-        }, &t2, sm);
+    if (fs.cnt != 0xFFFFFFFFu)
+      I = cta_kth32((int)fs.cnt, take, [&](int i, bool* ok) {
+            *ok = fs.key[i] == T;
+            return *ok ? (uint32_t)fs.id[i] : 0u;
+          }, &t2, sm);
+    else
+      I = cta_kth32(nc, take, [&](int i, bool* ok) {
+            const uint32_t f = f2key(vv[i]);
+            *ok = f == T;
+            return *ok ? (uint32_t)cp[i] : 0u;
+          }, &t2, sm);
     all = false;
   }
   int base = 0;
