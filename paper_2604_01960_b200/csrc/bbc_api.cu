@@ -1090,8 +1090,7 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
       }
       {
         StageScope sc(s.ix, st, BBC_STAGE_SELECT);
-        set_smem(k_final_select, kFsSmem);
-        k_final_select<<<nb, kSelNT, kFsSmem, st>>>(s.b, s.dv, s.oids, s.od2);
+        k_final_select<<<nb, kSelNT, 0, st>>>(s.b, s.dv, s.oids, s.od2);
         g_launches += 1;
       }
       if (pipe) {

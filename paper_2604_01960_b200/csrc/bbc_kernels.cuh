@@ -1776,8 +1776,6 @@ __global__ void __launch_bounds__(kSelNT) k_final_select(Batch b, Dev ix, long l
                                                          float* out_d2) {
   __shared__ Kth32Smem sm;
   __shared__ int wcnt[kSelNT / 32 + 1];
-  extern __shared__ __align__(16) uint8_t fsm[];
-  FastSelSmem& fs = *reinterpret_cast<FastSelSmem*>(fsm);
   const int q = blockIdx.x;
   const int nc = b.ncand[q];
   const int k = b.k;
@@ -1788,23 +1786,18 @@ __global__ void __launch_bounds__(kSelNT) k_final_select(Batch b, Dev ix, long l
   uint32_t T = 0xffffffffu, I = 0xffffffffu;
   bool all = true;
   if (nc > k) {
+    // (the sampled bracket, cta_kth32_bracket, measured slower here than the radix passes:
+    // C4 select 6.7 -> 7.2 ms -- k is ~60 % of the candidates, and the sample's own selections
+    // cost as much as the passes they save)
     unsigned take;
-    T = cta_kth32_bracket<true>(nc, (unsigned)k, [&](int i) { return f2key(vv[i]); },
-                                [&](int i) { return cp[i]; }, &take, fs, sm, nullptr);
-    // elements equal to T: take the `take` smallest ids (ids are unique) -- from the gathered
-    // bracket when it was used (it holds every key equal to T), else over all candidates
+    T = cta_kth32(nc, (unsigned)k, [&](int i, bool* ok) { *ok = true; return f2key(vv[i]); }, &take, sm);
+    // elements equal to T: take the `take` smallest ids (ids are unique)
     unsigned t2;
-    if (fs.cnt != 0xFFFFFFFFu)
-      I = cta_kth32((int)fs.cnt, take, [&](int i, bool* ok) {
-            *ok = fs.key[i] == T;
-            return *ok ? (uint32_t)fs.id[i] : 0u;
-          }, &t2, sm);
-    else
-      I = cta_kth32(nc, take, [&](int i, bool* ok) {
-            const uint32_t f = f2key(vv[i]);
-            *ok = f == T;
-            return *ok ? (uint32_t)cp[i] : 0u;
-          }, &t2, sm);
+    I = cta_kth32(nc, take, [&](int i, bool* ok) {
+          const uint32_t f = f2key(vv[i]);
+          *ok = f == T;
+          return *ok ? (uint32_t)cp[i] : 0u;
+        }, &t2, sm);
     all = false;
   }
   int base = 0;
