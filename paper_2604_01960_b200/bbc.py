@@ -15,7 +15,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbbc.so")
+# BBC_LIB: load a variant build instead (kernel tuning experiments)
+LIB_PATH = os.environ.get("BBC_LIB") or os.path.join(_HERE, "libbbc.so")
 
 # names exported by include/bbc.h (checked by tests/test_lib_exports.py)
 EXPORTS = ("ivf_load", "ivf_free", "bbc_index_info", "bbc_workspace_size", "bbc_query_capacity",

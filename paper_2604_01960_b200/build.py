@@ -8,7 +8,9 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-LIB = os.path.join(HERE, "libbbc.so")
+# BBC_LIB_OUT / BBC_NVCC_DEFS: build a variant library elsewhere with extra -D flags (kernel
+# tuning experiments; the default build and the product path ignore them)
+LIB = os.environ.get("BBC_LIB_OUT") or os.path.join(HERE, "libbbc.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in ("bbc_api.cu",)]
 # every header the library includes: an edit to any of them rebuilds it (stale())
 DEPS = SOURCES + sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [
@@ -37,7 +39,8 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or stale():
         nccl = _nccl_dir()
-        cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nccl, "include"),
+        defs = os.environ.get("BBC_NVCC_DEFS", "").split()
+        cmd = [NVCC, *FLAGS, *defs, "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nccl, "include"),
                *SOURCES, "-o", LIB + ".tmp", "-lcudart", "-L", os.path.join(nccl, "lib"),
                "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(nccl, "lib")]
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -179,6 +179,7 @@ struct RbqBufs {
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+constexpr int kItemMin = kRqE < kQ4Item ? kRqE : kQ4Item;   // smallest scan work item (sizes the item list)
 
 struct Plan {
   long long cap;      // per-query element capacity
@@ -196,7 +197,7 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1, bool xch
   p.cap = cap;
   size_t table = ix->kind == BBC_KIND_PQ ? (size_t)ix->M * 256 * 4 : (size_t)ix->D * 4;
   p.per_query = (size_t)ix->nlist * 4 + (size_t)nprobe * 20 + 8 +
-                (size_t)((cap + 32LL * nprobe + kRqE - 1) / kRqE) * 8 + 4 + 8 + kCells * 4 + 4 + 4 +
+                (size_t)((cap + 32LL * nprobe + kItemMin - 1) / kItemMin) * 8 + 4 + 8 + kCells * 4 + 4 + 4 +
                 table + (size_t)cap * 13 + (size_t)ix->d * 4 + (size_t)k * 24 + 64 +
                 (size_t)((cap + kChunk - 1) / kChunk) * 8 + (size_t)(nprobe + 1) * 4;
   p.per_query += 8 + 8 + kCells * 4 + 4 + 4 + (size_t)4 * world;   // DistBuf
@@ -247,7 +248,7 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nqmax, int nprobe,
   b.popad = (int*)take((size_t)nqb * (nprobe + 1) * 4);
   b.rbase = (long long*)take((size_t)nqb * nprobe * 8);
   b.qperm = (int*)take((size_t)nqb * 4);
-  b.items = (int2*)take((size_t)nqb * ((p.cap + 32LL * nprobe + kRqE - 1) / kRqE) * 8);
+  b.items = (int2*)take((size_t)nqb * ((p.cap + 32LL * nprobe + kItemMin - 1) / kItemMin) * 8);
   b.nitems = (int*)take(4);
   b.nsamp = (int*)take((size_t)nqb * 4);
   b.edges = (float*)take((size_t)nqb * 8);
@@ -330,7 +331,7 @@ void launch_rq(bool est, int grid, cudaStream_t st, const Batch& b, const Dev& d
 void rq_scan(int M, bool est, int num_sms, cudaStream_t st, const Batch& b, const Dev& dv,
              const uint8_t* ct, const long long* tb, float* out, long long stride, int mode, bool na) {
   if (b.nq <= 0) return;
-  k_scan_plan<<<1, 1024, 0, st>>>(b, mode, b.items, b.nitems);
+  k_scan_plan<<<1, 1024, 0, st>>>(b, mode, b.items, b.nitems, kRqE);
   g_launches += 1;
   switch (M) {
     case 8: launch_rq<8>(est, num_sms, st, b, dv, ct, tb, out, stride, mode, na); break;
@@ -353,7 +354,7 @@ void launch_q4(bool est, int grid, cudaStream_t st, const Batch& b, const Dev& d
 void q4_scan(int M, bool est, int num_sms, cudaStream_t st, const Batch& b, const Dev& dv,
              const uint8_t* ct, const long long* tb, float* out, long long stride, int mode) {
   if (b.nq <= 0) return;
-  k_scan_plan<<<1, 1024, 0, st>>>(b, mode, b.items, b.nitems);
+  k_scan_plan<<<1, 1024, 0, st>>>(b, mode, b.items, b.nitems, kQ4Item);
   g_launches += 1;
   const int grid = 2 * num_sms;
   switch (M) {

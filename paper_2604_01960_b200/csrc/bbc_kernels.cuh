@@ -571,12 +571,19 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 #ifndef BBC_RQ_WARPS
 #define BBC_RQ_WARPS 32
 #endif
-constexpr int kRqWarps = BBC_RQ_WARPS, kRqNT = kRqWarps * 32, kRqEW = 32;
-constexpr int kRqE = kRqNT * kRqEW;                      // objects per CTA (32768)
+#ifndef BBC_RQ_GPL
+#define BBC_RQ_GPL 8
+#endif
+#ifndef BBC_RQ_DEPTH
+#define BBC_RQ_DEPTH 2
+#endif
+constexpr int kRqWarps = BBC_RQ_WARPS, kRqNT = kRqWarps * 32;
+constexpr int kRqGPL = BBC_RQ_GPL;                       // groups per lane (8)
+constexpr int kRqEW = 4 * kRqGPL;                        // objects (running sums) per lane (32)
+constexpr int kRqE = kRqNT * kRqEW;                      // objects per CTA work item (32768)
 constexpr int kRqMC = 4;                                 // sub-quantizers per chunk
-constexpr int kRqGPL = kRqEW / 4;                        // groups per lane (8)
-constexpr int kRqDepth = 2;                              // 16-byte code loads in flight per lane
-constexpr int kRqGroups = kRqWarps * 32;                 // 32-object groups per CTA
+constexpr int kRqDepth = BBC_RQ_DEPTH;                   // 16-byte code loads in flight per lane
+constexpr int kRqGroups = kRqWarps * 4 * kRqGPL;         // 32-object groups per CTA
 constexpr int kRqLutBytes = kRqMC * 256 * 32 * 4;        // 131072
 // dynamic shared memory: [LUT chunk][group code offsets][group output offsets][group counts]
 //                        [histogram][padded probe offsets]
@@ -691,7 +698,7 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
     gcnt[G] = cnt;
   }
   __syncthreads();
-  const int gl0 = wid * 32 + (lane >> 3);            // the lane's groups: gl0 + 4 i
+  const int gl0 = wid * 4 * kRqGPL + (lane >> 3);    // the lane's groups: gl0 + 4 i
   // 16-byte index of the lane's slice of group gl0 + 4i, chunk p: gofs*8 + (lane&7) + 8p.  The
   // group offsets are re-read from shared memory per load (4 distinct words per warp: one
   // wavefront per 16 lookups) rather than held in 8 registers, which would spill.
@@ -785,11 +792,11 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
   }
 }
 
-// Work items of a scan pass: every (query, 32768-object pass) that has objects, in query
+// Work items of a scan pass: every (query, item_objs-object pass) that has objects, in query
 // locality order (qperm), so the scan runs as persistent CTAs without idle blocks (a static
 // grid sized for the largest query left most CTAs of small queries empty).  One CTA.
 //   mode 0: sample lists [0, nsamp); 1: lists [nsamp, nprobe); 2: all lists.
-__global__ void __launch_bounds__(1024) k_scan_plan(Batch b, int mode, int2* items, int* nitems) {
+__global__ void __launch_bounds__(1024) k_scan_plan(Batch b, int mode, int2* items, int* nitems, int item_objs) {
   __shared__ int ws[32];
   __shared__ int carry;
   if (threadIdx.x == 0) carry = 0;
@@ -804,7 +811,7 @@ __global__ void __launch_bounds__(1024) k_scan_plan(Batch b, int mode, int2* ite
       if (mode == 2 || ns > 0) {
         const int* pp = b.popad + (size_t)q * (b.nprobe + 1);
         const int first = mode == 1 ? ns : 0, lim = mode == 0 ? ns : b.nprobe;
-        cnt = (pp[lim] - pp[first] + kRqE - 1) / kRqE;
+        cnt = (pp[lim] - pp[first] + item_objs - 1) / item_objs;
       }
     }
     int x = cnt;

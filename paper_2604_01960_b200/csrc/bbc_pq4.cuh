@@ -25,7 +25,8 @@
 namespace bbc {
 
 constexpr int kQ4NT = 512;                            // 16 warps
-constexpr int kQ4Groups = kRqE / 32;                  // 1024 groups per work item
+constexpr int kQ4Item = 32768;                        // objects per work item
+constexpr int kQ4Groups = kQ4Item / 32;               // 1024 groups per work item
 constexpr int kQ4GPL = 4;                             // groups per lane per half
 
 // Per query q (one CTA of 32 x M threads... M * 16 <= 1024): Q, delta, bias from the fp32 LUT at
@@ -136,7 +137,7 @@ __global__ void __launch_bounds__(kQ4NT, 2) k_pq4_scan(Batch b, Dev ix, const ui
     const int lim = mode == 0 ? ns : b.nprobe;
     const int* popad = b.popad + (size_t)q * (b.nprobe + 1);
     const int nflat = popad[lim];
-    const int x0 = popad[first] + wk.y * kRqE;
+    const int x0 = popad[first] + wk.y * kQ4Item;
     if (x0 >= nflat) continue;
     for (int j = threadIdx.x; j <= lim; j += kQ4NT) s_popad[j] = popad[j];
     if (!EST)
