@@ -721,13 +721,16 @@ void stage_compact(Shard& s, cudaStream_t st) {
 // rows per lane group and 16-byte chunks per lane by row size; one row per lane group in flight
 // and high occupancy (4 CTAs/SM) beat deeper per-warp unrolling (tuned on C2: 1.55 ms with 2
 // rows in flight at 2 CTAs/SM -> 0.92 ms)
+#ifndef BBC_RR_MINB512
+#define BBC_RR_MINB512 4                                  // CTAs/SM of the <= 512-byte-row re-rank
+#endif
 #define BBC_RR_VARIANTS(X)                                      \
   if (rowb <= 128) {                                            \
     if (u8) X(true, 8, 1, 4, 4);                                \
     else X(false, 8, 1, 4, 4);                                  \
   } else if (rowb <= 512) {                                     \
-    if (u8) X(true, 8, 4, 1, 4);                                \
-    else X(false, 8, 4, 1, 4);                                  \
+    if (u8) X(true, 8, 4, 1, BBC_RR_MINB512);                   \
+    else X(false, 8, 4, 1, BBC_RR_MINB512);                     \
   } else if (rowb <= 1024) {                                    \
     X(false, 8, 8, 1, 3);                                       \
   } else {                                                      \

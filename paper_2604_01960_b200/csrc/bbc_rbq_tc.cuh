@@ -46,6 +46,40 @@ struct __align__(16) RbqPair {   // per (query, probed list), written by k_rbq_p
 static_assert(sizeof(RbqPair) == 64, "four 16-byte copies per pair");
 
 
+// Packed fp32 pairs (sm_100 FADD2/FMUL2): each half is the IEEE round-to-nearest (or, for
+// add_rm2, round-down) result of its own operands -- element by element the same arithmetic as
+// the scalar intrinsics, half the instructions.
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 up2(unsigned long long a) {
+  float2 r;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(a));
+  return r;
+}
+__device__ __forceinline__ unsigned long long sub_rn2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long mul_rn2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long add_rn2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long add_rm2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
 // ------------------------------------------------------------------ per-pair query codes
 // CTA = (query, kPairsPerCta consecutive probes): the query's rotated vector u is staged once in
 // shared memory; each warp computes kPairsPerWarp pairs (lane holds dims 4 (lane + 32 m) .. +3 of
@@ -84,22 +118,21 @@ __global__ void __launch_bounds__(256, 4) k_rbq_pairs(Batch b, Dev ix, const int
     const float r = __fsqrt_rn(rq2);
     const float rinv = r > 0.f ? __fdiv_rn(1.0f, r) : 0.f;
     const float4* w4 = reinterpret_cast<const float4*>(ix.wL + (size_t)L * D);
-    float4 qp[kMaxM4];
+    unsigned long long qp[kMaxM4][2];                 // q' as packed pairs (x, y), (z, w)
     float mn = INFINITY, mx = -INFINITY;
+    const unsigned long long rinv2 = pk2(rinv, rinv);
 #pragma unroll
     for (int m = 0; m < kMaxM4; ++m) {               // slots past D4 repeat slot D4 - 1 (min/max
       const int i = min(lane + 32 * m, D4 - 1);       // unchanged; their codes are not stored)
       const float4 w = __ldg(w4 + i), uu = u4[i];
-      float4 v;                                       // q' = (u - w) / r   (r = 0: q' = 0)
-      v.x = __fmul_rn(__fsub_rn(uu.x, w.x), rinv);
-      v.y = __fmul_rn(__fsub_rn(uu.y, w.y), rinv);
-      v.z = __fmul_rn(__fsub_rn(uu.z, w.z), rinv);
-      v.w = __fmul_rn(__fsub_rn(uu.w, w.w), rinv);
-      qp[m] = v;
-      mn = fminf(fminf(mn, v.x), v.y);
-      mn = fminf(fminf(mn, v.z), v.w);
-      mx = fmaxf(fmaxf(mx, v.x), v.y);
-      mx = fmaxf(fmaxf(mx, v.z), v.w);
+      // q' = (u - w) / r   (r = 0: q' = 0), two elements per packed subtract and multiply
+      qp[m][0] = mul_rn2(sub_rn2(pk2(uu.x, uu.y), pk2(w.x, w.y)), rinv2);
+      qp[m][1] = mul_rn2(sub_rn2(pk2(uu.z, uu.w), pk2(w.z, w.w)), rinv2);
+      const float2 a = up2(qp[m][0]), c = up2(qp[m][1]);
+      mn = fminf(fminf(mn, a.x), a.y);
+      mn = fminf(fminf(mn, c.x), c.y);
+      mx = fmaxf(fmaxf(mx, a.x), a.y);
+      mx = fmaxf(fmaxf(mx, c.x), c.y);
     }
     mn = warp_min(mn);
     mx = warp_max(mx);
@@ -108,14 +141,21 @@ __global__ void __launch_bounds__(256, 4) k_rbq_pairs(Batch b, Dev ix, const int
     const float dinv = delta > 0.f ? __fdiv_rn(1.0f, delta) : 0.f;
     unsigned acc = 0;
     uint32_t* qrow = reinterpret_cast<uint32_t*>(qbar + (size_t)slot * D);   // row-major at the slot
+    const unsigned long long mn2 = pk2(mn, mn), big2 = pk2(8388608.0f, 8388608.0f);
 #pragma unroll
     for (int m = 0; m < kMaxM4; ++m) {
       const int i = lane + 32 * m;
       // t = fl(fl(q' - mn) * dinv) + 0.5 >= 0; clamp(floor(t), 0, 15) = floor(min(t, 15)), and
       // floor(t) = low bits of fl_down(t + 2^23) (spacing 1 in [2^23, 2^24)). dinv = 0: t = 0.5 -> 0.
-#define BBC_QB(c) __fadd_rd(fminf(__fadd_rn(__fmul_rn(__fsub_rn(qp[m].c, mn), dinv), 0.5f), 15.0f), 8388608.0f)
-      const float f0 = BBC_QB(x), f1 = BBC_QB(y), f2 = BBC_QB(z), f3 = BBC_QB(w);
-#undef BBC_QB
+      // The subtraction and the final round-down add two elements per packed instruction; the
+      // multiply and + 0.5 stay scalar (ptxas contracts a packed mul.rn + add.rn pair into one
+      // FFMA2, which would round once instead of twice).
+      const float2 s01 = up2(sub_rn2(qp[m][0], mn2)), s23 = up2(sub_rn2(qp[m][1], mn2));
+#define BBC_QT(x) fminf(__fadd_rn(__fmul_rn(x, dinv), 0.5f), 15.0f)
+      const float2 g01 = up2(add_rm2(pk2(BBC_QT(s01.x), BBC_QT(s01.y)), big2));
+      const float2 g23 = up2(add_rm2(pk2(BBC_QT(s23.x), BBC_QT(s23.y)), big2));
+#undef BBC_QT
+      const float f0 = g01.x, f1 = g01.y, f2 = g23.x, f3 = g23.y;
       const unsigned lo = __byte_perm(__float_as_uint(f0), __float_as_uint(f1), 0x0040);
       const unsigned hi = __byte_perm(__float_as_uint(f2), __float_as_uint(f3), 0x0040);
       const unsigned v4 = __byte_perm(lo, hi, 0x5410);
