@@ -5,6 +5,8 @@ estimates, histograms, thresholds and superset ids bit-exact (canonical fp32 ord
 sides); exact d^2 within 1e-5 relative; final id sets identical except ids whose oracle d^2 is
 within 1e-5 relative of the oracle's k-th d^2; recall equal within 0.001.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -300,6 +302,10 @@ def test_recall_matches_oracle():
                                          #   several query tiles of the RaBitQ GEMM per list)
     ("C4", 768, 87500, 2500, 12),        # C4's operating point, one micro-batch of bench.py's run
     ("C4", 512, 75000, 1000, 6),         # BASELINE.json's C4 point
+    pytest.param("C5", 1024, 30000, 1000, 6, marks=pytest.mark.skipif(
+        os.environ.get("BBC_FULL_C5") != "1",
+        reason="C5's 100M-row index takes ~9 min to build: opt-in with BBC_FULL_C5=1 "
+               "(run and logged in profiles/r02_parity_c5_full.log)")),
 ])
 def test_full_size_sampled_parity(name, nprobe, budget, nq, nsel):
     """BASELINE.json configs at full size, at the operating points bench.py times, with the batch
