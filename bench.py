@@ -466,8 +466,8 @@ def main():
         l2 = max(measure_l2_read_gbs(0) for _ in range(5))        # a peak: best of 5
         per["rerank"].update({"bound": "l2", "peak_GBs": l2,
                               "pipe": "L2 -> SM reads (rows shared by the queries of a list)",
-                              "hbm_view": {"code_bytes": stats["candidates"] * row_bytes,
-                                           "peak_GBs": peak}})
+                              "peak_source": "measured: bbc_measure_l2_read (48 MiB L2-resident, "
+                                             "best of 4/8/16 loads in flight x 4/8 CTAs/SM, best of 5)"})
     for v in per.values():
         v["GBs"] = v["bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] > 0 else None
         v["frac"] = v["GBs"] / v["peak_GBs"] if v["GBs"] else None
@@ -515,7 +515,7 @@ def main():
             "unit": "TOP/s" if tens else "Glookup/s" if lkp else "GB/s", "frac": per[dom]["frac"],
             "traffic": traffic,
             "peak_source": (f"{peak_src}: MEASURED_PEAKS.json hbm_gbs (copy)" if per[dom]["bound"] == "hbm" else
-                            "measured: bbc_measure_l2_read (L2-resident 48 MiB, 16-byte loads, best of 5)"
+                            "measured: bbc_measure_l2_read (48 MiB L2-resident, best of 4/8/16 loads in flight x 4/8 CTAs/SM, best of 5)"
                             if per[dom]["bound"] == "l2" else
                             "measured bf16 TFLOP/s x 2 (int8/bf16 nominal ratio)" if tens else
                             "derived: 148 SMs x 64 ALU lanes/clk / 2 ops per lookup x sm_max_mhz (DESIGN.md 5)"),
