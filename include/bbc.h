@@ -103,7 +103,7 @@ bbc_status bbc_index_info(bbc_index index, bbc_index_info_t* info);
  *   BBC_PROBE_TENSOR : (d <= 1024) the tensor cores (tcgen05, kind::tf32, 3xTF32 split)
  *                      compute d~ with a proven error bound; the shortlist that provably holds
  *                      the nprobe nearest lists is re-scored canonically.
- *   BBC_PROBE_AUTO   : (default) TENSOR when available and nprobe <= nlist / 32 (the re-score
+ *   BBC_PROBE_AUTO   : (default) TENSOR when available and nprobe <= nlist / 16 (the re-score
  *                      reads nprobe centroid rows per query), SIMT otherwise.
  * Errors: BBC_ERR_ARG for a null index, an unknown mode, or TENSOR with d > 1024.  The mode is
  * per handle; it must not change while a search on the handle is in flight.

@@ -342,7 +342,7 @@ class Index:
     def set_probe_mode(self, mode: int) -> None:
         """Step a1 on the CUDA cores (canonical d^2 everywhere, PROBE_SIMT), as the tensor-core
         shortlist + canonical re-score (PROBE_TENSOR), or chosen per search (PROBE_AUTO, the
-        default: tensor cores when nprobe <= nlist / 32).  Same probe lists in every mode."""
+        default: tensor cores when nprobe <= nlist / 16).  Same probe lists in every mode."""
         _check(lib().bbc_set_probe_mode(self._h, int(mode)))
 
     def set_buckets(self, nbuckets: int) -> None:

@@ -1036,10 +1036,11 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
     if (s.ix->timing) s.ix->timed_calls++;
     s.dv = dev_view(s.ix);
     // a1 on the tensor cores when it wins: the shortlist re-score reads nprobe centroid rows per
-    // query, the SIMT tiled kernel all nlist: tensor cores for nprobe <= nlist/32
+    // query, the SIMT tiled kernel all nlist: tensor cores for nprobe <= nlist/16
+    // (C4 at nlist/21: 4.15 -> 3.44 ms; at nlist/16 even; C2 at nlist/5.3 and C3 at nlist/2 SIMT)
     const int pm = s.ix->probe_mode;
     s.dv.probe_tc = s.ix->probe_tc_ok &&
-                    (pm == BBC_PROBE_TENSOR || (pm == BBC_PROBE_AUTO && 32LL * nprobe <= s.ix->nlist));
+                    (pm == BBC_PROBE_TENSOR || (pm == BBC_PROBE_AUTO && 16LL * nprobe <= s.ix->nlist));
   }
   // host path: the tail of the batch is cut into halving micro-batches so that the one
   // device->host copy left exposed, the last micro-batch's, is small.
