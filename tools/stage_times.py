@@ -24,6 +24,7 @@ p.add_argument("--probe-simt", action="store_true")
 p.add_argument("--scan-simt", action="store_true")
 p.add_argument("--probe-tc", action="store_true", help="force the tensor-core probe")
 p.add_argument("--nq", type=int, default=0, help="first nq queries only (0: all)")
+p.add_argument("--ws-gb", type=float, default=48.0, help="workspace cap (GiB)")
 p.add_argument("--rerank", choices=("auto", "query", "list", "tile"), default="auto", help="re-rank order")
 a = p.parse_args()
 cfg = configs.get(a.workload)
@@ -40,7 +41,7 @@ g.set_rerank_order({"auto": g.RERANK_AUTO, "query": g.RERANK_QUERY, "list": g.RE
 q = torch.from_numpy(synth.generate_queries(cfg)).cuda()
 if a.nq:
     q = q[:a.nq].contiguous()
-ws = g.workspace(len(q), cfg.k, a.nprobe, a.budget, max_bytes=48 << 30)
+ws = g.workspace(len(q), cfg.k, a.nprobe, a.budget, max_bytes=int(a.ws_gb * (1 << 30)))
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for _ in range(3):
     ids, d2 = g.search(q, cfg.k, a.nprobe, a.budget, workspace=ws)
