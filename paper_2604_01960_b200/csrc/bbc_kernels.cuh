@@ -875,10 +875,18 @@ __global__ void __launch_bounds__(256) k_sample_cells(Batch b) {
   __syncthreads();
   const float* v = b.val + (size_t)q * b.cap;
   uint8_t* cl = b.cells + (size_t)q * b.cap;
-  for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
-    const int c = cf(v[i]);
-    cl[i] = (uint8_t)c;
-    if (c < 255) atomicAdd(&hist[c], 1);
+  const int stride = gridDim.x * 256;
+  for (int i0 = blockIdx.x * 256 + threadIdx.x; i0 < n; i0 += 4 * stride) {
+    float x[4];                                       // four loads in flight per thread
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = i0 + u * stride < n ? v[i0 + u * stride] : 0.f;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (i0 + u * stride >= n) break;
+      const int c = cf(x[u]);
+      cl[i0 + u * stride] = (uint8_t)c;
+      if (c < 255) atomicAdd(&hist[c], 1);
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kCells; i += 256)

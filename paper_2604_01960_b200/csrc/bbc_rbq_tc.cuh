@@ -575,14 +575,23 @@ __global__ void __launch_bounds__(256) k_cell_hist(Batch b) {
   const int n16 = n >> 4;
   // plain shared atomics into per-warp copies (most ids are the uncounted 255: 16 of them are
   // skipped with one compare; warp aggregation by match measured slower on the PQ scans)
-  for (int v = blockIdx.x * 256 + threadIdx.x; v < n16; v += gridDim.x * 256) {
-    const uint4 x = reinterpret_cast<const uint4*>(c)[v];
-    if ((x.x & x.y & x.z & x.w) == 0xFFFFFFFFu) continue;
-    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+  // four 16-byte loads in flight per thread (the ids stream from DRAM once)
+  const uint4* c16 = reinterpret_cast<const uint4*>(c);
+  const int stride = gridDim.x * 256;
+  for (int v0 = blockIdx.x * 256 + threadIdx.x; v0 < n16; v0 += 4 * stride) {
+    uint4 x[4];
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const int cell = (w[e >> 2] >> (8 * (e & 3))) & 255;
-      if (cell < 255) atomicAdd(&h[wid][cell], 1);
+    for (int u = 0; u < 4; ++u)
+      x[u] = v0 + u * stride < n16 ? c16[v0 + u * stride] : make_uint4(~0u, ~0u, ~0u, ~0u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if ((x[u].x & x[u].y & x[u].z & x[u].w) == 0xFFFFFFFFu) continue;
+      const uint32_t w[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int cell = (w[e >> 2] >> (8 * (e & 3))) & 255;
+        if (cell < 255) atomicAdd(&h[wid][cell], 1);
+      }
     }
   }
   if (blockIdx.x == 0)                               // ragged tail (< 16 objects)
