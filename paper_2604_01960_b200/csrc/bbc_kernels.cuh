@@ -1147,7 +1147,7 @@ template <bool IDS, typename KeyF, typename IdF>
 __device__ uint32_t cta_kth32_bracket(int n, unsigned kth, KeyF key, IdF idf, unsigned* take, FastSelSmem& fs,
                                       Kth32Smem& sm, uint32_t* min_out) {
   constexpr int NT = kSelNT;
-  if (n <= 2 * kFsS) {                                // small: the radix selection directly
+  if (n <= 8 * kFsS) {                                // small (<= 32k keys): the radix selection directly
     if (IDS && threadIdx.x == 0) fs.cnt = 0xFFFFFFFFu;
     __syncthreads();
     return cta_kth32(n, kth, [&](int i, bool* ok) { *ok = true; return key(i); }, take, sm, min_out);
