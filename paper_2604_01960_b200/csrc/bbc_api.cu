@@ -1050,6 +1050,11 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
     const long long rem = nq - q0;
     nb = (int)(pipe ? std::min<long long>(nqb, std::max<long long>(std::min(rem, min_nb), (rem + 1) / 2))
                     : std::min<long long>(nqb, rem));
+    // host path: a ramped head too (nqb/4, then nqb/2), so that the first device->host copy starts
+    // early -- when the copies are the longer stream (C4: 6 GB of results per step) the exposed
+    // time is the first micro-batch's search plus the last one's copy
+    if (pipe && mb_index < 2)
+      nb = (int)std::min<long long>(nb, std::max<long long>(std::min(rem, min_nb), nqb >> (2 - mb_index)));
     for (auto& s : sh) {
       carve(s.ix, s.p, nb, (int)nqb, nprobe, s.ws, s.b, &s.qstage, &s.oids, &s.od2, k, &s.db, W, &s.rb,
             dist ? &s.xb : nullptr);
