@@ -103,6 +103,8 @@ struct bbc_index_s {
   long long* h_tot = nullptr;           // [8] pinned host: pairs each rank packs (exchange sizes)
   int force_dist = 0;                   // run the sharded code path even at world 1 (tests)
   cudaStream_t copy_stream = nullptr;   // host path: device->host result copies
+  cudaStream_t copy_stream2 = nullptr;  //   (the distances on a second copy stream and engine)
+  cudaEvent_t ev_copied2[2] = {nullptr, nullptr};
   cudaEvent_t ev_done[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
 };
 
@@ -1019,6 +1021,8 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
   if (pipe) nqb = std::min<long long>(nqb, std::max<long long>(256, (nq + 1) / 2));
   if ((pipe || dist) && !ix->copy_stream) {
     CU(cudaStreamCreateWithFlags(&ix->copy_stream, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&ix->copy_stream2, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) CU(cudaEventCreateWithFlags(&ix->ev_copied2[i], cudaEventDisableTiming));
     for (int i = 0; i < 2; ++i) {
       CU(cudaEventCreateWithFlags(&ix->ev_done[i], cudaEventDisableTiming));
       CU(cudaEventCreateWithFlags(&ix->ev_copied[i], cudaEventDisableTiming));
@@ -1104,11 +1108,15 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
         g_launches += 1;
       }
       if (pipe) {
-        cudaStream_t cs = ix->copy_stream;
+        // ids and distances on two copy streams (two copy engines in flight on the PCIe link)
+        cudaStream_t cs = ix->copy_stream, cs2 = ix->copy_stream2;
         CU(cudaEventRecord(ix->ev_done[bi], st));
         CU(cudaStreamWaitEvent(cs, ix->ev_done[bi], 0));
+        CU(cudaStreamWaitEvent(cs2, ix->ev_done[bi], 0));
         CU(cudaMemcpyAsync(out_ids + q0 * k, s.oids, (size_t)nb * k * 8, cudaMemcpyDeviceToHost, cs));
-        CU(cudaMemcpyAsync(out_d2 + q0 * k, s.od2, (size_t)nb * k * 4, cudaMemcpyDeviceToHost, cs));
+        CU(cudaMemcpyAsync(out_d2 + q0 * k, s.od2, (size_t)nb * k * 4, cudaMemcpyDeviceToHost, cs2));
+        CU(cudaEventRecord(ix->ev_copied2[bi], cs2));
+        CU(cudaStreamWaitEvent(cs, ix->ev_copied2[bi], 0));   // ev_copied: both copies done
         CU(cudaEventRecord(ix->ev_copied[bi], cs));
       }
     } else {
@@ -1653,6 +1661,9 @@ void ivf_free(bbc_index ix) {
   if (ix->h_tot) cudaFreeHost(ix->h_tot);
   for (auto e : ix->pool) cudaEventDestroy(e);
   if (ix->copy_stream) cudaStreamDestroy(ix->copy_stream);
+  if (ix->copy_stream2) cudaStreamDestroy(ix->copy_stream2);
+  for (int i = 0; i < 2; ++i)
+    if (ix->ev_copied2[i]) cudaEventDestroy(ix->ev_copied2[i]);
   for (int i = 0; i < 2; ++i) {
     if (ix->ev_done[i]) cudaEventDestroy(ix->ev_done[i]);
     if (ix->ev_copied[i]) cudaEventDestroy(ix->ev_copied[i]);
