@@ -1018,7 +1018,8 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
                                                            (ix->raw_u8 ? ix->d : 4.0 * ix->d);
   const int tail_div = (double)k * 12.0 * 1000.0 < work_b ? 1 : 4;
   const bool pipe = host && !dist && !dbg && tail_div > 1;
-  if (pipe) nqb = std::min<long long>(nqb, std::max<long long>(256, (nq + 1) / 2));
+  static const int host_div = getenv("BBC_HOST_DIV") ? atoi(getenv("BBC_HOST_DIV")) : 2;   // tuning
+  if (pipe) nqb = std::min<long long>(nqb, std::max<long long>(256, (nq + host_div - 1) / host_div));
   if ((pipe || dist) && !ix->copy_stream) {
     CU(cudaStreamCreateWithFlags(&ix->copy_stream, cudaStreamNonBlocking));
     CU(cudaStreamCreateWithFlags(&ix->copy_stream2, cudaStreamNonBlocking));

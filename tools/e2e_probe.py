@@ -9,7 +9,7 @@ Q = synth.generate_queries(cfg); nq = len(Q); k = cfg.k; nprobe, budget = 768, 8
 qh = torch.from_numpy(Q).pin_memory().numpy()
 oh = (torch.empty((nq, k), dtype=torch.int64).pin_memory().numpy(), torch.empty((nq, k), dtype=torch.float32).pin_memory().numpy())
 q = torch.from_numpy(Q).cuda()
-for gb in (96, 48, 24):
+for gb in (96,):
     ws = torch.empty(int(gb * (1 << 30)), dtype=torch.uint8, device="cuda")
     g.search(q, k, nprobe, budget, workspace=ws); torch.cuda.synchronize()
     t = time.time(); g.search(q, k, nprobe, budget, workspace=ws); torch.cuda.synchronize(); td = time.time() - t
