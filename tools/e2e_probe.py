@@ -4,8 +4,9 @@ import numpy as np, torch
 import datagen
 from datagen import configs, synth
 from paper_2604_01960_b200 import Index
-cfg = configs.get("C4"); path = datagen.ensure_index(cfg); g = Index(path)
-Q = synth.generate_queries(cfg); nq = len(Q); k = cfg.k; nprobe, budget = 768, 85000
+cfg = configs.get(sys.argv[1] if len(sys.argv) > 1 else "C4"); path = datagen.ensure_index(cfg); g = Index(path)
+Q = synth.generate_queries(cfg); nq = len(Q); k = cfg.k
+nprobe, budget = {"C4": (768, 85000), "C2": (768, 20000), "C3": (2048, 20000)}[cfg.name]
 qh = torch.from_numpy(Q).pin_memory().numpy()
 oh = (torch.empty((nq, k), dtype=torch.int64).pin_memory().numpy(), torch.empty((nq, k), dtype=torch.float32).pin_memory().numpy())
 q = torch.from_numpy(Q).cuda()
