@@ -276,6 +276,39 @@ def test_host_api_pipelined_microbatches():
     assert np.array_equal(a_d2.cpu().numpy(), h_d2)
 
 
+def test_host_api_large_k_relative_to_capacity():
+    """with k large against the per-query capacity (few probed lists, padded rows) the
+    host path's pipelined micro-batches must not overwrite an output staging buffer the copy
+    stream still reads (the staging buffers sit at fixed workspace offsets): host results equal
+    the device path's bit for bit over >= 4 micro-batches of shrinking size."""
+    from datagen import synth
+    cfg, ix, Q, g = gpu_index("C2s")
+    Qm = np.ascontiguousarray(synth.generate_queries(cfg, 1300))
+    q = torch.from_numpy(Qm).cuda()
+    k, nprobe, budget = 3000, 10, 3000
+    a_ids, a_d2 = g.search(q, k, nprobe, budget)
+    h_ids, h_d2 = g.search_host(Qm, k, nprobe, budget)
+    assert g.last_stats()["microbatches"] >= 3
+    assert np.array_equal(a_ids.cpu().numpy(), h_ids)
+    assert np.array_equal(a_d2.cpu().numpy().view(np.uint32), h_d2.view(np.uint32))
+
+
+def test_binding_rejects_mismatched_arrays():
+    """The binding checks what the C ABI cannot (it takes no d): queries of the wrong width, dtype
+    or device, and caller-supplied outputs of the wrong shape or dtype, raise BBCError."""
+    from paper_2604_01960_b200.bbc import BBCError
+    cfg, ix, Q, g = gpu_index("C1t")
+    q = torch.from_numpy(Q).cuda()
+    for bad in (q[:, :-4].contiguous(), q.double(), q.cpu(), q[None]):
+        with pytest.raises(BBCError):
+            g.search(bad, 10, 4, 20)
+    with pytest.raises(BBCError):
+        g.search(q, 10, 4, 20, out=(torch.empty((len(Q), 9), dtype=torch.int64, device="cuda"),
+                                    torch.empty((len(Q), 10), dtype=torch.float32, device="cuda")))
+    with pytest.raises(BBCError):
+        g.search_host(Q[:, :-4], 10, 4, 20)
+
+
 def test_recall_matches_oracle():
     from oracle import bbc_oracle as O
     from oracle import bruteforce as BF
