@@ -561,3 +561,28 @@ def test_workspace_bounds_respected(name, mult):
         torch.cuda.synchronize()
         assert bool((buf[size:] == 0xA5).all()), f"workspace overflow ({size} bytes)"
         assert torch.equal(ids, ref_ids) and torch.equal(d2, ref_d2)
+
+
+def test_search_captures_into_a_cuda_graph():
+    """bbc_search enqueues only stream-ordered work (no host synchronisation, no allocation) on
+    the single-shard device path, so a caller can capture it into a CUDA graph once and replay it
+    (launch-bound small batches); the replays return the eager results bit for bit."""
+    cfg, ix, Q, g = gpu_index("C1t")
+    q = torch.from_numpy(Q).cuda()
+    k, nprobe, budget = cfg.k, cfg.nprobe, cfg.budget
+    ws = g.workspace(len(Q), k, nprobe, budget)
+    ref_ids, ref_d2 = g.search(q, k, nprobe, budget, workspace=ws)
+    out = (torch.empty_like(ref_ids), torch.empty_like(ref_d2))
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):                          # warm the kernels' attributes outside capture
+        g.search(q, k, nprobe, budget, out=out, workspace=ws)
+    torch.cuda.current_stream().wait_stream(s)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        g.search(q, k, nprobe, budget, out=out, workspace=ws)
+    for _ in range(3):
+        out[0].fill_(-7)
+        graph.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out[0], ref_ids) and torch.equal(out[1], ref_d2)
