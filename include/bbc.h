@@ -214,6 +214,9 @@ bbc_status bbc_query_capacity(bbc_index index, int32_t nprobe, int64_t* cap);
  *            When fewer than k objects are probed the row is padded with (id -1, d^2 +inf).
  *   workspace/workspace_bytes: device scratch of at least the `min_bytes` of bbc_workspace_size.
  *   stream   cudaStream_t (void*), NULL = default stream.
+ * On an unsharded handle without stage timing the call only enqueues stream-ordered work (no
+ * host synchronisation, no allocation), so it can be captured into a CUDA graph and replayed
+ * (tests/test_gpu_parity.py::test_search_captures_into_a_cuda_graph).
  */
 bbc_status bbc_search(bbc_index index, const float* queries, int64_t nq, int32_t k,
                       int32_t nprobe, int64_t budget, int64_t* out_ids, float* out_d2,
