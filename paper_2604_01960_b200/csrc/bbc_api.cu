@@ -319,9 +319,8 @@ void launch_rq(bool est, int grid, cudaStream_t st, const Batch& b, const Dev& d
                const uint8_t* ct, const long long* tb, float* out, long long stride, int mode, bool na) {
 #define BBC_RQ_L(E, NA)                                                                                  \
   do {                                                                                                  \
-    const size_t sm_ = NA ? kRqSmemRing : kRqSmem;                                                      \
-    set_smem(k_pq_scan_rq<M, E, NA>, sm_);                                                              \
-    k_pq_scan_rq<M, E, NA><<<grid, kRqNT, sm_, st>>>(b, dv, ct, tb, out, stride, mode, b.items, b.nitems); \
+    set_smem(k_pq_scan_rq<M, E, NA>, kRqSmem);                                                          \
+    k_pq_scan_rq<M, E, NA><<<grid, kRqNT, kRqSmem, st>>>(b, dv, ct, tb, out, stride, mode, b.items, b.nitems); \
   } while (0)
   if (est) { if (na) BBC_RQ_L(true, true); else BBC_RQ_L(true, false); }
   else { if (na) BBC_RQ_L(false, true); else BBC_RQ_L(false, false); }

@@ -593,11 +593,6 @@ constexpr int kRqOffCnt = kRqOffOut + kRqGroups * 8;
 constexpr int kRqOffHist = kRqOffCnt + kRqGroups * 4;
 constexpr int kRqOffPo = kRqOffHist + kCells * 4;
 constexpr size_t kRqSmem = kRqOffPo + (kMaxProbe + 1) * 4;
-// streamed codes (NOALLOC): a ring of kRqRing 16-byte slots per thread that cp.async fills
-// kRqRing group-chunks ahead of use (no registers held by loads in flight)
-constexpr int kRqRing = 4;
-constexpr int kRqOffRing = (int)((kRqSmem + 127) / 128 * 128);
-constexpr size_t kRqSmemRing = (size_t)kRqOffRing + (size_t)kRqRing * kRqNT * 16;
 // The kernel has no static shared memory, so its dynamic buffer starts right after the 1 KB
 // the driver reserves per CTA; the LUT lookups use that offset as an immediate (checked).
 constexpr unsigned kRqSmemBase = 1024;
@@ -726,19 +721,8 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
 #pragma unroll
   for (int e = 0; e < kRqEW; ++e) acc[e] = 0.f;
   const uint32_t lane4 = (uint32_t)lane * 4u;
-  // NOALLOC: group-chunk loads go through the shared-memory ring by cp.async (slot i % kRqRing
-  // of this thread), kRqRing ahead; otherwise kRqDepth loads in flight in registers
-  const uint32_t ring = smem_u32(rsm + kRqOffRing) + 16u * threadIdx.x;
-  auto cpa = [&](auto ic, int p) {
-    uint32_t g;
-    asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(g) : "r"(gaddr), "n"(16 * decltype(ic)::value));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n cp.async.commit_group;"
-                 ::"r"(ring + 16u * kRqNT * (uint32_t)(decltype(ic)::value % kRqRing)),
-                   "l"(c16 + (g + 8u * (uint32_t)p)) : "memory");
-  };
-  uint4 cw[NOALLOC ? 1 : kRqDepth];
-  if constexpr (NOALLOC) static_for<kRqRing>([&](auto ic) { cpa(ic, 0); });
-  else static_for<kRqDepth>([&](auto ic) { cw[decltype(ic)::value] = ldc(ic, 0); });
+  uint4 cw[kRqDepth];
+  static_for<kRqDepth>([&](auto ic) { cw[decltype(ic)::value] = ldc(ic, 0); });
 #pragma unroll 1
   for (int p = 0; p < P; ++p) {
     __syncthreads();                                  // previous chunk fully consumed
@@ -765,30 +749,17 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
     const int pn = p + 1 < P ? p + 1 : p;            // code loads run one chunk ahead at the tail
     static_for<kRqGPL>([&](auto ic) {
       constexpr int i = decltype(ic)::value;
-      uint4 c;
-      if constexpr (NOALLOC) {
-        asm volatile("cp.async.wait_group %0;" ::"n"(kRqRing - 1) : "memory");
-        const uint32_t a = ring + 16u * kRqNT * (uint32_t)(i % kRqRing);
-        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w) : "r"(a));
-        if constexpr (i + kRqRing < kRqGPL)
-          cpa(std::integral_constant<int, i + kRqRing>{}, p);
-        else
-          cpa(std::integral_constant<int, i + kRqRing - kRqGPL>{}, pn);
-      } else {
-        c = cw[i % kRqDepth];
-        if constexpr (i + kRqDepth < kRqGPL)
-          cw[i % kRqDepth] = ldc(std::integral_constant<int, i + kRqDepth>{}, p);
-        else
-          cw[i % kRqDepth] = ldc(std::integral_constant<int, i + kRqDepth - kRqGPL>{}, pn);
-      }
+      const uint4 c = cw[i % kRqDepth];
+      if constexpr (i + kRqDepth < kRqGPL)
+        cw[i % kRqDepth] = ldc(std::integral_constant<int, i + kRqDepth>{}, p);
+      else
+        cw[i % kRqDepth] = ldc(std::integral_constant<int, i + kRqDepth - kRqGPL>{}, pn);
       acc[4 * i + 0] = rq_lookup4(acc[4 * i + 0], c.x, lane4);
       acc[4 * i + 1] = rq_lookup4(acc[4 * i + 1], c.y, lane4);
       acc[4 * i + 2] = rq_lookup4(acc[4 * i + 2], c.z, lane4);
       acc[4 * i + 3] = rq_lookup4(acc[4 * i + 3], c.w, lane4);
     });
   }
-  // the ring's trailing loads (the wrap of the last chunk) land before the slots are reused
-  if constexpr (NOALLOC) asm volatile("cp.async.wait_group 0;" ::: "memory");
   // epilogue: lane l holds objects 4(l&7)+j of its groups
   CellFn cf;
   if (!EST) cf.init(b.edges[2 * q], b.edges[2 * q + 1], b.nbuckets);
