@@ -716,7 +716,7 @@ void stage_compact(Shard& s, cudaStream_t st) {
 
   Batch be = s.b;                                   // segment starts only for the list-order re-rank
   if (!rerank_list_order(s.ix, s.b, s.ix->raw_u8 ? s.ix->d : s.ix->d * 4)) be.sstart = nullptr;
-  k_emit<<<dim3(nchunk, nb), kCmpNT, 0, st>>>(be, s.dv, s.b.chunk, nchunk);
+  k_emit<<<dim3(std::min(nchunk, 24), nb), kCmpNT, 0, st>>>(be, s.dv, s.b.chunk, nchunk);
   g_launches += 4;
 }
 

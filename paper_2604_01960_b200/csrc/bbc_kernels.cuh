@@ -1435,14 +1435,21 @@ __global__ void __launch_bounds__(256) k_chunk_offsets(Batch b, int* chunk_cnt, 
 // in shared memory at their block-scan rank, then written out with coalesced stores (the
 // original ids are gathered by the re-rank, which reads each candidate's row anyway).  Few dependent global accesses per CTA: the kernel is latency-bound.
 constexpr int kEmitWin = 256;                        // lists staged per chunk (else global search); 6 CTAs/SM
-__global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chunk_off, int nchunk) {
-  __shared__ int wcnt[kCmpNT / 32];
-  __shared__ int s_pre[kCmpNT];
-  __shared__ unsigned s_flg[kCmpNT];
-  __shared__ int s_po[kEmitWin + 1];
-  __shared__ long long s_rb[kEmitWin];
-  const int q = blockIdx.y;
-  const int c = blockIdx.x;
+struct EmitSmem {
+  int wcnt[kCmpNT / 32];
+  int s_pre[kCmpNT];
+  unsigned s_flg[kCmpNT];
+  int s_po[kEmitWin + 1];
+  long long s_rb[kEmitWin];
+};
+
+__device__ __forceinline__ void emit_chunk(const Batch& b, const Dev& ix, const int* chunk_off, int nchunk, int q,
+                                           int c, EmitSmem& sm) {
+  int* wcnt = sm.wcnt;
+  int* s_pre = sm.s_pre;
+  unsigned* s_flg = sm.s_flg;
+  int* s_po = sm.s_po;
+  long long* s_rb = sm.s_rb;
   const int nprobe = b.nprobe;
   const int* po = b.poff + (size_t)q * (nprobe + 1);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1542,6 +1549,20 @@ __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chu
     }
   }
 
+}
+
+// CTA (x, query) takes chunks x, x + gridDim.x, ...: the grid covers the queries' real chunks
+// without one CTA per chunk of the capacity (most of which, past the query's probed objects, had
+// only to exit: C4 ~58 % of 735k CTAs)
+__global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chunk_off, int nchunk) {
+  __shared__ EmitSmem sm;
+  const int q = blockIdx.y;
+  const int n = b.poff[(size_t)q * (b.nprobe + 1) + b.nprobe];
+  const int need = (n + kChunk - 1) / kChunk;
+  for (int c = blockIdx.x; c < need; c += gridDim.x) {
+    __syncthreads();                                 // shared memory of the previous chunk free
+    emit_chunk(b, ix, chunk_off, nchunk, q, c, sm);
+  }
 }
 
 // ------------------------------------------------------------------------------------------
