@@ -711,7 +711,7 @@ void stage_compact(Shard& s, cudaStream_t st) {
     g_launches += 1;
   }
   k_tau<<<nb, 32, 0, st>>>(s.b);
-  k_count<<<dim3((nchunk + kCntPer - 1) / kCntPer, nb), kCmpNT, 0, st>>>(s.b, s.b.chunk, nchunk);
+  k_count<<<dim3(std::min((nchunk + kCntPer - 1) / kCntPer, 8), nb), kCmpNT, 0, st>>>(s.b, s.b.chunk, nchunk);
   k_chunk_offsets<<<nb, 256, 0, st>>>(s.b, s.b.chunk, nchunk);
 
   Batch be = s.b;                                   // segment starts only for the list-order re-rank

@@ -1367,8 +1367,9 @@ __global__ void __launch_bounds__(kCmpNT) k_count(Batch b, int* chunk_cnt, int n
   const int n = b.poff[(size_t)q * (b.nprobe + 1) + b.nprobe];
   const int tau = b.tau[q];
   const int need = (n + kChunk - 1) / kChunk;
-  const int c0 = blockIdx.x * kCntPer;
-  if (c0 >= need) return;
+  // CTA (x, query) takes chunk groups x, x + gridDim.x, ... of the query's real chunks
+  for (int c0 = blockIdx.x * kCntPer; c0 < need; c0 += gridDim.x * kCntPer) {
+  __syncthreads();                                   // red[] of the previous group read
   Cells32 x[kCntPer];
 #pragma unroll
   for (int u = 0; u < kCntPer; ++u)
@@ -1384,6 +1385,7 @@ __global__ void __launch_bounds__(kCmpNT) k_count(Batch b, int* chunk_cnt, int n
     int t = 0;
     for (int w = 0; w < kCmpNT / 32; ++w) t += red[threadIdx.x][w];
     chunk_cnt[(size_t)q * nchunk + c0 + threadIdx.x] = t;
+  }
   }
 }
 
