@@ -1039,20 +1039,13 @@ struct Kth32Smem {
 template <typename KeyF>
 __device__ uint32_t cta_kth32(int n, unsigned kth, KeyF key, unsigned* take, Kth32Smem& sm,
                               uint32_t* min_out = nullptr) {
-  constexpr int NT = kSelNT, U = 4;                   // U keys in flight per thread (latency)
+  constexpr int NT = kSelNT;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   unsigned mn = 0xffffffffu, mx = 0u;
-  for (int i0 = threadIdx.x; i0 < n; i0 += U * NT) {
-    uint32_t k[U];
-    bool ok[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      ok[u] = false;
-      k[u] = i0 + u * NT < n ? key(i0 + u * NT, &ok[u]) : 0u;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (ok[u]) { mn = min(mn, k[u]); mx = max(mx, k[u]); }
+  for (int i = threadIdx.x; i < n; i += NT) {
+    bool ok;
+    const uint32_t k = key(i, &ok);
+    if (ok) { mn = min(mn, k); mx = max(mx, k); }
   }
   mn = warp_min(mn);
   mx = __reduce_max_sync(0xffffffffu, mx);
@@ -1082,17 +1075,10 @@ __device__ uint32_t cta_kth32(int n, unsigned kth, KeyF key, unsigned* take, Kth
     const unsigned mask = (1u << width) - 1u;
     for (int i = threadIdx.x; i < 2048; i += NT) sm.hist[i] = 0;
     __syncthreads();
-    for (int i0 = threadIdx.x; i0 < n; i0 += U * NT) {
-      uint32_t k[U];
-      bool ok[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        ok[u] = false;
-        k[u] = i0 + u * NT < n ? key(i0 + u * NT, &ok[u]) : 0u;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (ok[u] && (pshift == 32 || (k[u] >> pshift) == prefix)) atomicAdd(&sm.hist[(k[u] >> shift) & mask], 1u);
+    for (int i = threadIdx.x; i < n; i += NT) {
+      bool ok;
+      const uint32_t k = key(i, &ok);
+      if (ok && (pshift == 32 || (k >> pshift) == prefix)) atomicAdd(&sm.hist[(k >> shift) & mask], 1u);
     }
     __syncthreads();
     // exclusive scan of the 2048 bins, 2 per thread
@@ -1853,32 +1839,24 @@ __global__ void __launch_bounds__(kSelNT) k_final_select(Batch b, Dev ix, long l
     all = false;
   }
   int base = 0;
-  constexpr int U = 4;                                // four rows of 1,024 loaded together
-  for (int t0 = 0; t0 < nc; t0 += U * kSelNT) {
-    float dv[U];
-    int id[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = t0 + u * kSelNT + threadIdx.x;
-      dv[u] = i < nc ? vv[i] : 0.f;
-      id[u] = i < nc ? cp[i] : 0;
+  for (int t0 = 0; t0 < nc; t0 += kSelNT) {
+    const int i = t0 + threadIdx.x;
+    bool f = false;
+    float dv = 0.f;
+    int id = 0;
+    if (i < nc) {
+      dv = vv[i];
+      id = cp[i];
+      const uint32_t fk = f2key(dv);
+      f = all || fk < T || (fk == T && (uint32_t)id <= I);
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = t0 + u * kSelNT + threadIdx.x;
-      bool f = false;
-      if (i < nc) {
-        const uint32_t fk = f2key(dv[u]);
-        f = all || fk < T || (fk == T && (uint32_t)id[u] <= I);
-      }
-      int total;
-      const int r = block_rank<kSelNT>(f, wcnt, &total);
-      if (f && base + r < k) {
-        oi[base + r] = (long long)(uint32_t)id[u];
-        od[base + r] = dv[u];
-      }
-      base += total;
+    int total;
+    int r = block_rank<kSelNT>(f, wcnt, &total);
+    if (f && base + r < k) {
+      oi[base + r] = (long long)(uint32_t)id;
+      od[base + r] = dv;
     }
+    base += total;
   }
   for (int i = base + threadIdx.x; i < k; i += kSelNT) {
     oi[i] = -1;
