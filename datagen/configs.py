@@ -96,6 +96,13 @@ SMALL = {
                        budget=900, kmeans_iters=6),
     "C3mt960": C3.replace(name="C3mt960", N=8_000, nlist=8, nq=500, k=200, nprobe=8, budget=600,
                           kmeans_iters=6),
+    # the scan's other sub-quantizer counts: M = 64 (dsub 2) and M = 24 (dsub 4), M = 8 (dsub 12)
+    "C2m64s": C2.replace(name="C2m64s", M=64, N=60_000, nlist=256, nq=12, k=800, nprobe=16, budget=1_600,
+                         kmeans_iters=6),
+    "C4m24s": C4.replace(name="C4m24s", M=24, N=60_000, nlist=256, nq=12, k=800, nprobe=16, budget=1_600,
+                         kmeans_iters=6),
+    "C4m8s": C4.replace(name="C4m8s", M=8, N=60_000, nlist=256, nq=12, k=800, nprobe=16, budget=1_600,
+                        kmeans_iters=6),
     # fine lists (~20 objects): a compaction chunk of 8,192 objects spans > 256 lists, the
     # global-search path of k_emit; probe sets of 600 lists
     "C2f": C2.replace(name="C2f", N=40_000, nlist=2_048, nq=8, k=500, nprobe=600, budget=1_000,

@@ -135,7 +135,7 @@ def check_final_ids(gi, gd, oi, od, k):
 
 
 @pytest.mark.parametrize("name", ["C1t", "C1s", "C2s", "C2f", "C3s", "C4s", "C5s", "C4ip_s", "C2q4s",
-                                  "C3d1024s", "C3d64s", "C3d200s"])
+                                  "C3d1024s", "C3d64s", "C3d200s", "C2m64s", "C4m24s", "C4m8s"])
 def test_parity_config_point(name):
     cfg, ix, Q, g = gpu_index(name)
     compare(cfg, ix, Q, g, cfg.k, cfg.nprobe, cfg.budget)
