@@ -726,13 +726,16 @@ void stage_compact(Shard& s, cudaStream_t st) {
 #ifndef BBC_RR_MINB512
 #define BBC_RR_MINB512 4                                  // CTAs/SM of the <= 512-byte-row re-rank
 #endif
+#ifndef BBC_RR_STEPS512
+#define BBC_RR_STEPS512 1                                 // rows in flight per lane group (ditto)
+#endif
 #define BBC_RR_VARIANTS(X)                                      \
   if (rowb <= 128) {                                            \
     if (u8) X(true, 8, 1, 4, 4);                                \
     else X(false, 8, 1, 4, 4);                                  \
   } else if (rowb <= 512) {                                     \
-    if (u8) X(true, 8, 4, 1, BBC_RR_MINB512);                   \
-    else X(false, 8, 4, 1, BBC_RR_MINB512);                     \
+    if (u8) X(true, 8, 4, BBC_RR_STEPS512, BBC_RR_MINB512);     \
+    else X(false, 8, 4, BBC_RR_STEPS512, BBC_RR_MINB512);       \
   } else if (rowb <= 1024) {                                    \
     X(false, 8, 8, 1, 3);                                       \
   } else {                                                      \
