@@ -41,7 +41,7 @@ from datagen import configs, groundtruth, index_file, synth  # noqa: E402
 # C4: profiles/r02_sweep_c4.jsonl and r02_sweep_c4_fine.jsonl: 768 / 85,000 -> 0.9515 at 92.7k QPS
 # (768 / 82,500: 0.9505, too close to the target; 1024 / 75,000: 0.961 at 76k); C2:
 # profiles/r02_sweep_c2.jsonl confirms 768 / 20,000 (0.957).
-RECALL95 = {"C2": (768, 20000), "C3": (2048, 20000), "C4": (768, 85000), "C5": (1024, 30000), "C4ip": (1024, 75000),
+RECALL95 = {"C2": (768, 20000), "C3": (2048, 20000), "C4": (768, 85000), "C5": (1024, 25000), "C4ip": (1024, 75000),
             "C2q4": (1024, 60000)}
 METRIC = "queries/sec at recall@k=0.95 (k=5k\u201350k); scan+rerank HBM GB/s vs peak"
 
