@@ -721,8 +721,11 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
 #pragma unroll
   for (int e = 0; e < kRqEW; ++e) acc[e] = 0.f;
   const uint32_t lane4 = (uint32_t)lane * 4u;
+  // groups are valid in a prefix of the item: a warp whose first group lies beyond the item's
+  // objects (the tail of a query's last item) only stages and syncs
+  const bool wact = gcnt[wid * 4 * kRqGPL] > 0;
   uint4 cw[kRqDepth];
-  static_for<kRqDepth>([&](auto ic) { cw[decltype(ic)::value] = ldc(ic, 0); });
+  if (wact) static_for<kRqDepth>([&](auto ic) { cw[decltype(ic)::value] = ldc(ic, 0); });
 #pragma unroll 1
   for (int p = 0; p < P; ++p) {
     __syncthreads();                                  // previous chunk fully consumed
@@ -747,7 +750,7 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
     }
     __syncthreads();
     const int pn = p + 1 < P ? p + 1 : p;            // code loads run one chunk ahead at the tail
-    static_for<kRqGPL>([&](auto ic) {
+    if (wact) static_for<kRqGPL>([&](auto ic) {
       constexpr int i = decltype(ic)::value;
       const uint4 c = cw[i % kRqDepth];
       if constexpr (i + kRqDepth < kRqGPL)

@@ -181,6 +181,7 @@ __global__ void __launch_bounds__(kQ4NT, 2) k_pq4_scan(Batch b, Dev ix, const ui
 #pragma unroll 1
     for (int half = 0; half < 2; ++half) {
       const int gl0 = half * (kQ4Groups / 2) + wid * 32 + (lane >> 2);   // groups gl0 + 8 i
+      if (gcnt[half * (kQ4Groups / 2) + wid * 32] == 0) continue;     // warp past the item's objects
       uint32_t acc[kQ4GPL][4];                        // objects (0,2) (1,3) (4,6) (5,7) of the octet
 #pragma unroll
       for (int i = 0; i < kQ4GPL; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0u;
