@@ -721,11 +721,10 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
 #pragma unroll
   for (int e = 0; e < kRqEW; ++e) acc[e] = 0.f;
   const uint32_t lane4 = (uint32_t)lane * 4u;
-  // groups are valid in a prefix of the item: a warp whose first group lies beyond the item's
-  // objects (the tail of a query's last item) only stages and syncs
-  const bool wact = gcnt[wid * 4 * kRqGPL] > 0;
+  // (warps whose groups all lie past the item's objects still run the lookups: skipping them
+  // under a warp-uniform branch measured slower on C4, 50.2 -> 54.2 ms, from the loop's codegen)
   uint4 cw[kRqDepth];
-  if (wact) static_for<kRqDepth>([&](auto ic) { cw[decltype(ic)::value] = ldc(ic, 0); });
+  static_for<kRqDepth>([&](auto ic) { cw[decltype(ic)::value] = ldc(ic, 0); });
 #pragma unroll 1
   for (int p = 0; p < P; ++p) {
     __syncthreads();                                  // previous chunk fully consumed
@@ -750,7 +749,7 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
     }
     __syncthreads();
     const int pn = p + 1 < P ? p + 1 : p;            // code loads run one chunk ahead at the tail
-    if (wact) static_for<kRqGPL>([&](auto ic) {
+    static_for<kRqGPL>([&](auto ic) {
       constexpr int i = decltype(ic)::value;
       const uint4 c = cw[i % kRqDepth];
       if constexpr (i + kRqDepth < kRqGPL)
@@ -1827,9 +1826,10 @@ __global__ void __launch_bounds__(kSelNT) k_final_select(Batch b, Dev ix, long l
   uint32_t T = 0xffffffffu, I = 0xffffffffu;
   bool all = true;
   if (nc > k) {
-    // (the sampled bracket, cta_kth32_bracket, measured slower here than the radix passes:
-    // C4 select 6.7 -> 7.2 ms -- k is ~60 % of the candidates, and the sample's own selections
-    // cost as much as the passes they save)
+    // (measured slower here than these radix passes, whose re-reads hit L2 -- the CTAs in
+    // flight hold ~100 MB of distances: the sampled bracket, cta_kth32_bracket, C4 select 6.7 ->
+    // 7.2 ms; gathering the first digit's bin with its ids into 64 KB of shared memory and
+    // finishing there, 6.5 -> 7.2 ms)
     unsigned take;
     T = cta_kth32(nc, (unsigned)k, [&](int i, bool* ok) { *ok = true; return f2key(vv[i]); }, &take, sm);
     // elements equal to T: take the `take` smallest ids (ids are unique)

@@ -242,6 +242,34 @@ def test_degenerate_identical_vectors(tmp_path):
         assert sorted(ids[i].tolist()) == list(range(100))
 
 
+def test_final_select_large_tie_bins(tmp_path):
+    """Final selection where the k-th distance is shared by thousands of candidates: two distinct
+    database vectors (15,000 + 5,000 copies) give two keys; k inside either key's run is decided
+    by id alone, and the result is the (d^2, id) top-k."""
+    from datagen import build_index, configs, index_file, synth
+    cfg = configs.get("C1t").replace(name="ties2", N=20000, nlist=4, M=16, kmeans_iters=2,
+                                     pq_train=2000, pq_iters=2)
+    base = synth.generate_data(cfg)[:2]
+    X = np.concatenate([np.repeat(base[:1], 15000, axis=0), np.repeat(base[1:], 5000, axis=0)])
+    X = X[np.random.default_rng(7).permutation(len(X))]
+    idx = build_index.build(cfg, X=np.ascontiguousarray(X))
+    p = str(tmp_path / "ties2.bbcivf")
+    index_file.write(p, idx)
+    ix = index_file.read(p)
+    g = _index(p)
+    Q = synth.generate_queries(cfg)[:2]
+    d0 = ((Q[:, None, :].astype(np.float64) - base[None].astype(np.float64)) ** 2).sum(-1)
+    for k in (10000, 17000):
+        ids, d2, t = compare(cfg, ix, Q, g, k, cfg.nlist, cfg.N)
+        for i in range(len(Q)):
+            near = np.argmin(d0[i])
+            first = np.flatnonzero((X == base[near]).all(1))
+            second = np.flatnonzero((X == base[1 - near]).all(1))
+            want = np.sort(first)[:k] if k <= len(first) else \
+                np.concatenate([first, np.sort(second)[:k - len(first)]])
+            assert np.array_equal(np.sort(ids[i]), np.sort(want)), (k, i)
+
+
 def test_microbatching_matches_one_batch():
     cfg, ix, Q, g = gpu_index("C2s")
     q = torch.from_numpy(Q).cuda()
