@@ -1705,7 +1705,7 @@ void ivf_free(bbc_index ix) {
   void* ptrs[] = {ix->centroids, ix->loff, ix->gsize_d, ix->ids, ix->books, ix->codes, ix->P,
                   ix->wL, ix->bits, ix->factors, ix->raw, ix->stats, ix->codes_t, ix->tbase,
                   ix->cmu, ix->cnorm, ix->rbq_tiles, ix->rbq_pc, ix->lrank, ix->pb_hi, ix->pb_lo,
-                  ix->nccl_scratch, ix->rt_units, ix->rt_ubase, ix->rmu};
+                  ix->nccl_scratch, ix->rt_units, ix->rt_ubase};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& t : ix->timers) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
