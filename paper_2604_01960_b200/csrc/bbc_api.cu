@@ -71,9 +71,6 @@ struct bbc_index_s {
   CUtensorMap ptm_hi, ptm_lo;           // their TMA maps (k_probe_mma_ws)
   bool probe_ws_ok = false;
   float* cnorm = nullptr;               // [nlist] |c - mu|^2
-  float* rmu = nullptr;                 // [nlist x d] per-list centring of the tensor-core re-rank:
-                                        // the centroid, rounded when the rows are small integers
-  int raw_int = 0;                      // rows integer-valued with |x| < 2^11
   int* lrank = nullptr;                 // [nlist] (region << 20 | list): query locality order
   float cmax = 0.f;                     // max |c - mu|, rounded up
   int probe_mode = BBC_PROBE_AUTO;       // BBC_PROBE_* (bbc_probe_tc.cuh)
@@ -138,7 +135,6 @@ Dev dev_view(const bbc_index_s* ix) {
   v.books = ix->books; v.codes = ix->codes; v.P = ix->P; v.wL = ix->wL; v.bits = ix->bits;
   v.factors = ix->factors; v.raw = ix->raw;
   v.cmu = ix->cmu; v.cnorm = ix->cnorm; v.cmax = ix->cmax; v.probe_tc = 0;
-  v.rmu = ix->rmu;
   return v;
 }
 
@@ -1581,23 +1577,6 @@ bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_
       mx = std::max(mx, a);
     }
     ix->cmax = (float)(std::sqrt(mx) * (1.0 + 1e-6));
-    // centring of the tensor-core re-rank: integer rows keep integer residuals (exact distances)
-    if (raw_u8) {
-      ix->raw_int = 1;
-    } else if (ok && ix->n_local > 0) {
-      int* flag = nullptr;
-      ok = dalloc((void**)&flag, 4);
-      const int one = 1;
-      ok = ok && cudaMemcpy(flag, &one, 4, cudaMemcpyHostToDevice) == cudaSuccess;
-      if (ok) k_raw_is_int<<<1024, 256>>>(static_cast<const float*>(ix->raw), ix->n_local * (long long)d, flag);
-      ok = ok && cudaMemcpy(&ix->raw_int, flag, 4, cudaMemcpyDeviceToHost) == cudaSuccess;
-      if (flag) cudaFree(flag);
-    }
-    std::vector<float> rmu(C);
-    if (ix->raw_int)
-      for (auto& v : rmu) v = std::nearbyint(v);
-    ok = ok && dalloc((void**)&ix->rmu, rmu.size() * 4) &&
-         cudaMemcpy(ix->rmu, rmu.data(), rmu.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
     // list regions for the query locality order: nearest of 256 evenly spaced pivot centroids
     const int npiv = std::min(256, nlist);
     std::vector<int> lr(nlist);

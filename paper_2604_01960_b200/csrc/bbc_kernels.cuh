@@ -75,7 +75,6 @@ struct Dev {
   const float* cnorm;            // [nlist]
   float cmax;
   int probe_tc;                  // 1: coarse holds d~ (shortlist mode of k_probe_select)
-  const float* rmu;              // [nlist x d] centring of the tensor-core re-rank (bbc_rerank_tc.cuh)
 };
 
 // ------------------------------------------------------------------------------------------

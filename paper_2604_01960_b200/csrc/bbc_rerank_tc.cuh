@@ -2,31 +2,26 @@
 //
 // The list-order re-rank (k_rerank_seg) reads every candidate's row from L2 once per query that
 // has it as a candidate: at C4 a row is a candidate of ~20 queries of a micro-batch and the
-// kernel moves 337 GB of rows per step through L2.  Here a CTA takes one inverted list L and up
-// to 128 of the (query, list) segments that reference it, and computes the dense block
-//     D[r][p] = <x_r - mu_L, q_p - mu_L>     (IP: <x_r - mu_L, q_p>)
-// for 128 rows r of the list per tile and the segments' queries p as a tensor-core GEMM (M = 128
-// rows, N = 128 queries, K = d in chunks of 32).  The block is dense while only the candidates
-// are wanted (C4: ~18 % of the (row, query) pairs), but a row is read once per list and chunk
-// of 128 queries instead of once per candidate, and the products run on the tensor cores.  The
-// epilogue parks D in shared memory and one warp per segment picks its candidates (ascending
-// rows, k_emit's order) tile by tile:
-//     L2: val = |x - mu|^2 + |q - mu|^2 - 2 D          IP: val = -(D + <mu, q>)
-// Centring on mu_L (the list's centroid; rounded to integers when the rows are integer-valued)
-// keeps the norms at the scale of the distance, so the cancellation in the L2 form stays small.
-// The dot product is split v = v_hi + v_lo (v_hi = the top 19 bits, what the tf32 MMA reads):
-// hi*hi + hi*lo + lo*hi accumulate in fp32 in tensor memory (the lo*lo term, < 2^-20 |x'||q'|,
-// is dropped).  Integer-valued rows and queries below 2^11 have lo = 0, integer partial sums
-// below 2^24 and an integer mu: their distances are exact, as in the SIMT re-rank; otherwise the
-// distance agrees with the fp64 definition within the re-rank's 1e-5 relative tolerance
-// (DESIGN.md 2.2), not bit for bit with the SIMT kernel.
+// kernel moves 337 GB of rows per step through L2.  Here a CTA takes one inverted list and up to
+// 128 of the (query, list) segments that reference it, and computes the dense block
+//     D[r][p] = <x_r, q_p>,  rows r of the list (128 per tile)  x  queries p of the segments
+// as a tensor-core GEMM (M = 128 rows, N = 128 queries, K = d in chunks of 32).  The block is
+// dense while only the candidates are wanted (C4: ~18 % of the (row, query) pairs), but the
+// rows are read once per list and chunk of 128 queries instead of once per candidate, and the
+// products run on the tensor cores.  The epilogue parks D in shared memory and each segment's
+// thread walks its candidates (ascending rows, k_emit's order) tile by tile:
+//     L2: val = |x|^2 + |q|^2 - 2 <x, q>      IP: val = -<x, q>
+// with |x|^2, |q|^2 as sequential fp32 FMAs.  The dot product is split x = x_hi + x_lo (x_hi =
+// the top 19 bits, what the tf32 MMA reads): hi*hi + hi*lo + lo*hi accumulate in fp32 in
+// tensor memory (the lo*lo term, < 2^-20 |x||q|, is dropped).  Integer-valued data below 2^11
+// has lo = 0 and integer partial sums below 2^24, so its distances are exact, as in the SIMT
+// re-rank; otherwise the distance agrees with the fp64 definition within the 1e-5 relative
+// tolerance of the re-rank, not bit for bit with the SIMT kernel.
 //
 // Operands are staged by the CTA's threads in the K-major no-swizzle core-matrix layout of
-// bbc_probe_tc.cuh (one K chunk of 32 at a time: A 128 x 32 and B 128 x 32, hi and lo, 64 KB),
-// every load of a chunk issued before its stores; the squared norms are summed on the way (8
-// partial sums per row, combined by shuffles).  One elected thread issues the MMAs and commits
-// to an mbarrier.  The accumulator block (128 TMEM columns) is read back in two halves of 64
-// columns into the (then idle) staging buffer.
+// bbc_probe_tc.cuh (one K chunk of 32 at a time: A 128 x 32 and B 128 x 32, hi and lo, 64 KB);
+// one elected thread issues the MMAs and commits to an mbarrier.  The accumulator block (128
+// TMEM columns) is read back in two halves of 64 columns into the (then idle) staging buffer.
 #pragma once
 #include "bbc_probe_tc.cuh"
 
@@ -35,66 +30,33 @@ namespace bbc {
 constexpr int kRtcNT = 128;                        // threads: 4 warps = the 128 TMEM lanes
 constexpr int kRtcN = 128;                         // queries (segments) per chunk
 constexpr int kRtcDS = 65;                         // padded row stride of the parked D half
-constexpr int kRtcSlots = 128 * (kTcKC / 4) / kRtcNT;                 // float4 slots per thread (8)
 constexpr size_t kRtcOffInfo = 2 * kTcABytes + 2 * kTcBBytes;          // 64 KB of operands
-constexpr int kRtcMaxD = 1024;
-constexpr size_t kRtcOffMu = kRtcOffInfo + (size_t)kRtcN * 16 + kRtcN * 4 + 128 * 4 + 64;
-constexpr size_t kRtcSmem = kRtcOffMu + (size_t)kRtcMaxD * 4;
+constexpr size_t kRtcSmem = kRtcOffInfo + (size_t)kRtcN * 16 + kRtcN * 4 + 128 * 4 + 64;
 
-// K chunk [k0, k0 + 32) of 128 rows row(r) (nullptr: zero row) minus mu (if CENTER) into hi/lo;
-// nrm[j] += the squares of this thread's slot j (row tid / 8 + 16 j, columns 4 (tid % 8) ..).
-template <bool U8, bool CENTER, typename RowF>
-__device__ __forceinline__ void rtc_stage(RowF row, int d, int k0, const float* __restrict__ mu, uint8_t* hi,
-                                          uint8_t* lo, float (&nrm)[kRtcSlots]) {
-  const int kq = threadIdx.x & 7;
-  const int gk = k0 + 4 * kq;
-  float4 v[kRtcSlots];
-#pragma unroll
-  for (int j = 0; j < kRtcSlots; ++j) {
-    const int r = (threadIdx.x >> 3) + 16 * j;
+// Stage K chunk [k0, k0 + 32) of 128 rows given by row(r) (a pointer or nullptr) into hi/lo.
+template <bool U8, typename RowF>
+__device__ __forceinline__ void rtc_stage(RowF row, int d, int k0, uint8_t* hi, uint8_t* lo) {
+  for (int idx = threadIdx.x; idx < 128 * (kTcKC / 4); idx += kRtcNT) {
+    const int r = idx >> 3, kq = idx & 7;
+    const int gk = k0 + 4 * kq;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     const void* p = row(r);
-    v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (p != nullptr && gk < d) {                   // d % 4 == 0
+    if (p != nullptr && gk < d) {                   // d % 4 == 0 (checked by the launcher)
       if (U8) {
         const uchar4 u = *reinterpret_cast<const uchar4*>(static_cast<const uint8_t*>(p) + gk);
-        v[j] = make_float4((float)u.x, (float)u.y, (float)u.z, (float)u.w);
+        v = make_float4((float)u.x, (float)u.y, (float)u.z, (float)u.w);
       } else {
-        v[j] = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(p) + gk));
+        v = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(p) + gk));
       }
     }
-  }
-  float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (CENTER && gk < d) m = *reinterpret_cast<const float4*>(mu + gk);
-#pragma unroll
-  for (int j = 0; j < kRtcSlots; ++j) {
-    const int r = (threadIdx.x >> 3) + 16 * j;
-    const bool live = row(r) != nullptr && gk < d;
-    float4 x = v[j];
-    if (CENTER && live) { x.x -= m.x; x.y -= m.y; x.z -= m.z; x.w -= m.w; }
-    nrm[j] = fmaf(x.x, x.x, nrm[j]);
-    nrm[j] = fmaf(x.y, x.y, nrm[j]);
-    nrm[j] = fmaf(x.z, x.z, nrm[j]);
-    nrm[j] = fmaf(x.w, x.w, nrm[j]);
     float4 h, l;
-    h.x = tf32_hi(x.x); l.x = x.x - h.x;
-    h.y = tf32_hi(x.y); l.y = x.y - h.y;
-    h.z = tf32_hi(x.z); l.z = x.z - h.z;
-    h.w = tf32_hi(x.w); l.w = x.w - h.w;
+    h.x = tf32_hi(v.x); l.x = v.x - h.x;
+    h.y = tf32_hi(v.y); l.y = v.y - h.y;
+    h.z = tf32_hi(v.z); l.z = v.z - h.z;
+    h.w = tf32_hi(v.w); l.w = v.w - h.w;
     const int off = (r >> 3) * kTcSboBytes + kq * 128 + (r & 7) * 16;
     *reinterpret_cast<float4*>(hi + off) = h;
     *reinterpret_cast<float4*>(lo + off) = l;
-  }
-}
-
-// the 8 partial sums of each slot row -> out[row] (lanes 8 apart hold the same rows)
-__device__ __forceinline__ void rtc_norms(float (&nrm)[kRtcSlots], float* out) {
-#pragma unroll
-  for (int j = 0; j < kRtcSlots; ++j) {
-    float s = nrm[j];
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    s += __shfl_xor_sync(0xffffffffu, s, 4);
-    if ((threadIdx.x & 7) == 0) out[(threadIdx.x >> 3) + 16 * j] = s;
   }
 }
 
@@ -112,16 +74,13 @@ __global__ void __launch_bounds__(kRtcNT) k_rerank_tc(Batch b, Dev ix, const int
   uint8_t* b_lo = b_hi + kTcBBytes;
   float* park = reinterpret_cast<float*>(tsm);       // D half [128][kRtcDS], over the operands
   int4* sp = reinterpret_cast<int4*>(tsm + kRtcOffInfo);          // (q, cursor, end, -)
-  float* qn = reinterpret_cast<float*>(sp + kRtcN);                // |q - mu|^2 (IP: <mu, q>)
+  float* qn = reinterpret_cast<float*>(sp + kRtcN);
   float* xn = qn + kRtcN;
   uint64_t* bar = reinterpret_cast<uint64_t*>(xn + 128);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
   int* s_min = reinterpret_cast<int*>(tmem_slot + 1);
-  float* mu = reinterpret_cast<float*>(tsm + kRtcOffMu);            // mu_L (16-byte aligned)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bar_a = smem_u32(bar);
-  const int d = ix.d;
-  for (int t = threadIdx.x; t < d; t += kRtcNT) mu[t] = ix.rmu[(size_t)L * d + t];
   if (threadIdx.x == 0) {
     mbar_init(bar_a, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -136,6 +95,7 @@ __global__ void __launch_bounds__(kRtcNT) k_rerank_tc(Batch b, Dev ix, const int
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
   const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo), bh = smem_u32(b_hi), bl = smem_u32(b_lo);
+  const int d = ix.d;
   const long long row0 = ix.loff[L];
   const int nL = (int)(ix.loff[L + 1] - row0);
   const size_t rowb = U8 ? (size_t)d : (size_t)d * 4;
@@ -148,14 +108,17 @@ __global__ void __launch_bounds__(kRtcNT) k_rerank_tc(Batch b, Dev ix, const int
     if (threadIdx.x < np) {
       const int4 g = seg[c0 + threadIdx.x];
       sp[threadIdx.x] = make_int4(g.x, g.y, g.y + g.z, 0);
-      if (IP) {                                        // <mu, q>, sequential FMAs
-        const float* qv = b.Q + (size_t)g.x * d;
+      if (!IP) {
+        const float4* qv = reinterpret_cast<const float4*>(b.Q + (size_t)g.x * d);
         float s = 0.f;
-        for (int t = 0; t < d; ++t) s = fmaf(mu[t], qv[t], s);
+        for (int t = 0; t < d / 4; ++t) {
+          const float4 x = qv[t];
+          s = fmaf(x.x, x.x, s); s = fmaf(x.y, x.y, s); s = fmaf(x.z, x.z, s); s = fmaf(x.w, x.w, s);
+        }
         qn[threadIdx.x] = s;
       }
     }
-    bool have_qn = IP;
+    __syncthreads();
     int t0 = 0;
     while (true) {
       // next tile: the one holding the smallest pending candidate row of the chunk's segments
@@ -169,14 +132,11 @@ __global__ void __launch_bounds__(kRtcNT) k_rerank_tc(Batch b, Dev ix, const int
       const int mn = *s_min;
       if (mn >= nL) break;
       t0 = mn & ~127;
-      float xs[kRtcSlots], qs[kRtcSlots];
-#pragma unroll
-      for (int j = 0; j < kRtcSlots; ++j) xs[j] = qs[j] = 0.f;
       for (int kc = 0; kc < nk; ++kc) {
-        rtc_stage<U8, true>([&](int r) -> const void* { return t0 + r < nL ? raw + (size_t)(t0 + r) * rowb : nullptr; },
-                            d, kc * kTcKC, mu, a_hi, a_lo, xs);
-        rtc_stage<false, !IP>([&](int r) -> const void* { return r < np ? b.Q + (size_t)sp[r].x * d : nullptr; },
-                              d, kc * kTcKC, mu, b_hi, b_lo, qs);
+        rtc_stage<U8>([&](int r) -> const void* { return t0 + r < nL ? raw + (size_t)(t0 + r) * rowb : nullptr; },
+                      d, kc * kTcKC, a_hi, a_lo);
+        rtc_stage<false>([&](int r) -> const void* { return r < np ? b.Q + (size_t)sp[r].x * d : nullptr; },
+                         d, kc * kTcKC, b_hi, b_lo);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -196,12 +156,27 @@ __global__ void __launch_bounds__(kRtcNT) k_rerank_tc(Batch b, Dev ix, const int
         phase ^= 1u;
       }
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      // |x|^2 of the tile's rows (thread = row; sequential FMAs)
       if (!IP) {
-        rtc_norms(xs, xn);
-        if (!have_qn) {                                  // once per chunk (B is the same every tile)
-          rtc_norms(qs, qn);
-          have_qn = true;
+        const int r = threadIdx.x;
+        float s = 0.f;
+        if (t0 + r < nL) {
+          if (U8) {
+            const uint8_t* p = raw + (size_t)(t0 + r) * rowb;
+            for (int t = 0; t < d; t += 4) {
+              const uchar4 u = *reinterpret_cast<const uchar4*>(p + t);
+              s = fmaf((float)u.x, (float)u.x, s); s = fmaf((float)u.y, (float)u.y, s);
+              s = fmaf((float)u.z, (float)u.z, s); s = fmaf((float)u.w, (float)u.w, s);
+            }
+          } else {
+            const float4* p = reinterpret_cast<const float4*>(raw + (size_t)(t0 + r) * rowb);
+            for (int t = 0; t < d / 4; ++t) {
+              const float4 x = __ldg(p + t);
+              s = fmaf(x.x, x.x, s); s = fmaf(x.y, x.y, s); s = fmaf(x.z, x.z, s); s = fmaf(x.w, x.w, s);
+            }
+          }
         }
+        xn[r] = s;
       }
       for (int h = 0; h * 64 < np; ++h) {
         // park columns [64h, 64h + 64) of D: warp w holds rows 32w .. 32w + 31
@@ -224,26 +199,21 @@ __global__ void __launch_bounds__(kRtcNT) k_rerank_tc(Batch b, Dev ix, const int
           for (int e = 0; e < 32; ++e) pr[e] = __uint_as_float(v[e]);
         }
         __syncthreads();
-        // one warp per segment: 32 candidates per step, a prefix of them in this tile
-        for (int pc = warp; pc < 64 && 64 * h + pc < np; pc += kRtcNT / 32) {
-          const int p = 64 * h + pc;
+        // segment threads: the candidates of the tile, in slot order
+        const int p = 64 * h + threadIdx.x;
+        if (threadIdx.x < 64 && p < np) {
           int4 g = sp[p];
           const size_t base = (size_t)g.x * b.cap;
-          const float qq = qn[p];
+          const float qq = IP ? 0.f : qn[p];
           while (g.y < g.z) {
-            const int i = g.y + lane;
-            const int r = i < g.z ? (int)(b.cpos[base + i] - row0) - t0 : 1 << 30;
-            const bool in = r < 128;
-            if (in) {
-              const float dot = park[(size_t)r * kRtcDS + pc];
-              b.val[base + i] = IP ? -(dot + qq) : fmaf(-2.f, dot, xn[r] + qq);
-              b.cid[base + i] = (int)__ldg(ix.ids + row0 + t0 + r);
-            }
-            const int n = __popc(__ballot_sync(0xffffffffu, in));
-            g.y += n;
-            if (n < 32) break;
+            const int r = (int)(b.cpos[base + g.y] - row0) - t0;
+            if (r >= 128) break;
+            const float dot = park[(size_t)r * kRtcDS + threadIdx.x];
+            b.val[base + g.y] = IP ? -dot : fmaf(-2.f, dot, xn[r] + qq);
+            b.cid[base + g.y] = (int)__ldg(ix.ids + row0 + t0 + r);
+            ++g.y;
           }
-          if (lane == 0) sp[p].y = g.y;
+          sp[p].y = g.y;
         }
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncthreads();
@@ -255,14 +225,6 @@ __global__ void __launch_bounds__(kRtcNT) k_rerank_tc(Batch b, Dev ix, const int
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kRtcN));
-}
-
-// rows integer-valued with |x| < 2^11 (fp32 rows): flag stays 1, else cleared
-__global__ void k_raw_is_int(const float* __restrict__ x, long long n, int* flag) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const float v = x[i];
-    if (v != rintf(v) || fabsf(v) >= 2048.f) *flag = 0;
-  }
 }
 
 }  // namespace bbc
