@@ -150,8 +150,8 @@ bbc_status bbc_set_scan_mode(bbc_index index, int32_t mode);
 
 /*
  * bbc_set_rerank_order -- the work order of step a7, the exact re-rank of S* (P:L413).
- * Results are identical in the QUERY, LIST and TILE orders (each candidate's distance is computed
- * by the same lanes in the same arithmetic order); only which rows are read together differs.
+ * Results are identical in both orders (each candidate's distance is computed by the same lanes
+ * in the same arithmetic order); only which rows are read together differs.
  *   BBC_RERANK_QUERY : CTAs walk one query's candidates (rows of one query in flight).
  *   BBC_RERANK_LIST  : the run of candidates a query has in one inverted list is a segment;
  *                      segments are ordered by list, so the rows in flight belong to a few
@@ -160,12 +160,6 @@ bbc_status bbc_set_scan_mode(bbc_index index, int32_t mode);
  *                      consecutive rows per CTA by a bulk copy, every candidate of every query in
  *                      that tile computed from shared memory (fp32 rows of 128, 256, 384 or 512
  *                      bytes; BBC_ERR_ARG otherwise).  Measured slower than LIST.
- *   BBC_RERANK_TC    : list order on the tensor cores: per list, the dense block of its rows x
- *                      the queries of its segments as a 3xTF32 GEMM (tcgen05), candidates picked
- *                      in the epilogue; |x|^2 + |q|^2 - 2<x, q> (IP: -<x, q>).  Exact for
- *                      integer-valued data below 2^11, else within the re-rank's 1e-5 relative
- *                      tolerance rather than bit-identical to the other orders.  Rows with
- *                      d % 4 != 0 fall back to LIST.
  *   BBC_RERANK_AUTO  : (default) LIST when the micro-batch re-ranks each row >= 4 times on
  *                      average (nq * budget / N), else QUERY.
  * BBC_ERR_ARG for a null index or an unknown order.  Must not change while a search on the
@@ -175,7 +169,6 @@ bbc_status bbc_set_scan_mode(bbc_index index, int32_t mode);
 #define BBC_RERANK_LIST 1
 #define BBC_RERANK_AUTO 2
 #define BBC_RERANK_TILE 3
-#define BBC_RERANK_TC 4
 bbc_status bbc_set_rerank_order(bbc_index index, int32_t order);
 
 /*

@@ -369,15 +369,13 @@ class Index:
         Same results in every mode."""
         _check(lib().bbc_set_code_loads(self._h, int(mode)))
 
-    RERANK_QUERY, RERANK_LIST, RERANK_AUTO, RERANK_TILE, RERANK_TC = 0, 1, 2, 3, 4
+    RERANK_QUERY, RERANK_LIST, RERANK_AUTO, RERANK_TILE = 0, 1, 2, 3
 
     def set_rerank_order(self, order: int) -> None:
         """Exact re-rank work order: per query (RERANK_QUERY), per (list, query) segment in list
         order (RERANK_LIST: rows shared by the queries of a list come from L2), list order with
         each list's rows staged in shared memory tile by tile (RERANK_TILE, fp32 rows <= 512 B),
-        list order as tensor-core GEMMs of each list's rows by its queries (RERANK_TC; within
-        the 1e-5 tolerance, exact for small-integer data), or chosen from the data size and
-        reuse (RERANK_AUTO, default)."""
+        or chosen from the data size and reuse (RERANK_AUTO, default)."""
         _check(lib().bbc_set_rerank_order(self._h, int(order)))
 
     def set_timing(self, on: bool) -> None:

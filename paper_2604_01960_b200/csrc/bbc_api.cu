@@ -18,7 +18,6 @@
 #include "bbc_rbq_tc.cuh"
 #include "bbc_pq4.cuh"
 #include "bbc_rerank_tile.cuh"
-#include "bbc_rerank_tc.cuh"
 
 using namespace bbc;
 
@@ -690,8 +689,7 @@ void stage_scan(Shard& s, cudaStream_t st, bool sample_cells) {
 bool rerank_list_order(const bbc_index_s* ix, const Batch& b, int rowb) {
   (void)rowb;
   if (ix->rerank_order != BBC_RERANK_AUTO)
-    return ix->rerank_order == BBC_RERANK_LIST || ix->rerank_order == BBC_RERANK_TILE ||
-           ix->rerank_order == BBC_RERANK_TC;
+    return ix->rerank_order == BBC_RERANK_LIST || ix->rerank_order == BBC_RERANK_TILE;
   const double reuse = (double)b.nq * (double)b.budget / std::max<double>(1.0, (double)ix->n_local);
   return reuse >= 4.0;
 }
@@ -702,13 +700,6 @@ bool rerank_list_order(const bbc_index_s* ix, const Batch& b, int rowb) {
 bool rerank_tile(const bbc_index_s* ix, const Batch& b, int rowb) {
   if (!ix->rt_units || !rerank_list_order(ix, b, rowb)) return false;
   return ix->rerank_order == BBC_RERANK_TILE;
-}
-
-// list-major re-rank on the tensor cores (bbc_rerank_tc.cuh): on request; rows of d % 4 == 0
-bool rerank_tc(const bbc_index_s* ix, const Batch& b, int rowb) {
-  (void)b;
-  (void)rowb;
-  return ix->rerank_order == BBC_RERANK_TC && ix->d % 4 == 0;
 }
 
 void stage_compact(Shard& s, cudaStream_t st) {
@@ -820,23 +811,6 @@ void stage_rerank(Shard& s, cudaStream_t st) {
       else if (rowb == 384) { if (ip) BBC_RT(384, true); else BBC_RT(384, false); }
       else { if (ip) BBC_RT(512, true); else BBC_RT(512, false); }
 #undef BBC_RT
-      g_launches += 4;
-      return;
-    }
-    if (rerank_tc(ix, s.b, rowb)) {
-      // whole segments by list, then one CTA per list
-      cudaMemsetAsync(s.b.rs_cnt, 0, (size_t)(ix->nlist + 1) * 4, st);
-      k_rr_segments<false><<<gp, 256, 0, st>>>(s.b, s.b.rs_cnt, s.b.rseg, 1 << 30);
-      k_inv_scan<<<1, 1024, 0, st>>>(s.b.rs_cnt, s.b.rs_off, s.b.rs_cur, ix->nlist);
-      k_rr_segments<true><<<gp, 256, 0, st>>>(s.b, s.b.rs_cur, s.b.rseg, 1 << 30);
-#define BBC_RTC(U8, IPV)                                                                        \
-  do {                                                                                         \
-    set_smem(k_rerank_tc<U8, IPV>, kRtcSmem);                                                  \
-    k_rerank_tc<U8, IPV><<<ix->nlist, kRtcNT, kRtcSmem, st>>>(s.b, s.dv, s.b.rseg, s.b.rs_off); \
-  } while (0)
-      if (ix->raw_u8) { if (ip) BBC_RTC(true, true); else BBC_RTC(true, false); }
-      else { if (ip) BBC_RTC(false, true); else BBC_RTC(false, false); }
-#undef BBC_RTC
       g_launches += 4;
       return;
     }
@@ -1746,7 +1720,7 @@ bbc_status bbc_set_code_loads(bbc_index ix, int32_t mode) {
 
 bbc_status bbc_set_rerank_order(bbc_index ix, int32_t order) {
   if (!ix) return fail(BBC_ERR_ARG, "null index");
-  if (order != BBC_RERANK_QUERY && order != BBC_RERANK_LIST && order != BBC_RERANK_AUTO && order != BBC_RERANK_TC &&
+  if (order != BBC_RERANK_QUERY && order != BBC_RERANK_LIST && order != BBC_RERANK_AUTO &&
       order != BBC_RERANK_TILE)
     return fail(BBC_ERR_ARG, "unknown re-rank order");
   if (order == BBC_RERANK_TILE && !ix->rt_units)

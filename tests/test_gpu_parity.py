@@ -532,27 +532,6 @@ def test_rerank_orders_identical(name):
                     assert np.array_equal(a[key][i][:n].view(np.uint8), b[key][i][:n].view(np.uint8)), key
 
 
-@pytest.mark.parametrize("name", ["C1t", "C2s", "C4s", "C5s", "C4ip_s"])
-def test_rerank_tensor_core(name):
-    """The tensor-core re-rank (RERANK_TC: per list, 3xTF32 GEMM of its rows by its segments'
-    queries, candidates picked in the epilogue) against the oracle: candidate ids identical, exact
-    distances identical on the integer-valued configs and within 1e-5 relative otherwise, final
-    top-k the (d^2, id) top-k of its own candidates and the oracle's up to ties -- at the config's
-    nprobe and with every list probed (lists with > 128 segments: several query chunks)."""
-    cfg, ix, Q, g = gpu_index(name)
-    g.set_rerank_order(g.RERANK_TC)
-    try:
-        compare(cfg, ix, Q, g, cfg.k, cfg.nprobe, cfg.budget)
-        compare(cfg, ix, Q[:6], g, cfg.k, cfg.nlist, cfg.budget)
-        if name == "C1t":
-            # 300 queries probing all 32 lists: ~300 segments per list, three query chunks
-            from datagen import synth
-            Qm = np.ascontiguousarray(synth.generate_queries(cfg, 300))
-            compare(cfg, ix, Qm, g, cfg.k, cfg.nlist, cfg.budget, sel=[0, 127, 128, 255, 256, 299])
-    finally:
-        g.set_rerank_order(g.RERANK_AUTO)
-
-
 def test_ip_full_probe_unlimited_budget_is_brute_force_mips():
     """Inner-product index (f4): every list probed and budget >= N give the brute-force maximum
     inner product top-k, keys -<q, x> within 1e-5 relative (ids up to key ties)."""

@@ -63,7 +63,7 @@ def test_python_constants_match_header():
              "PROBE_SIMT": "BBC_PROBE_SIMT", "PROBE_TENSOR": "BBC_PROBE_TENSOR",
              "PROBE_AUTO": "BBC_PROBE_AUTO", "RERANK_QUERY": "BBC_RERANK_QUERY",
              "RERANK_LIST": "BBC_RERANK_LIST", "RERANK_AUTO": "BBC_RERANK_AUTO",
-             "RERANK_TILE": "BBC_RERANK_TILE", "RERANK_TC": "BBC_RERANK_TC",
+             "RERANK_TILE": "BBC_RERANK_TILE",
              "CODES_AUTO": "BBC_CODES_AUTO", "CODES_CACHED": "BBC_CODES_CACHED",
              "CODES_STREAM": "BBC_CODES_STREAM"}
     for py, c in pairs.items():

@@ -18,13 +18,13 @@ p.add_argument("--nprobe", type=int, default=768)
 p.add_argument("--budget", type=int, default=20000)
 p.add_argument("--reps", type=int, default=2)
 p.add_argument("--nq", type=int, default=0, help="first nq queries (0: the config's batch)")
-p.add_argument("--rerank", choices=("auto", "query", "list", "tile", "tc"), default="auto")
+p.add_argument("--rerank", choices=("auto", "query", "list", "tile"), default="auto")
 a = p.parse_args()
 cfg = configs.get(a.workload)
 path = datagen.ensure_index(cfg)
 g = Index(path)
 g.set_rerank_order({"auto": g.RERANK_AUTO, "query": g.RERANK_QUERY, "list": g.RERANK_LIST,
-                    "tile": g.RERANK_TILE, "tc": g.RERANK_TC}[a.rerank])
+                    "tile": g.RERANK_TILE}[a.rerank])
 Q = synth.generate_queries(cfg)
 q = torch.from_numpy(Q[:a.nq] if a.nq else Q).contiguous().cuda()
 for _ in range(a.reps):

@@ -25,7 +25,7 @@ p.add_argument("--scan-simt", action="store_true")
 p.add_argument("--probe-tc", action="store_true", help="force the tensor-core probe")
 p.add_argument("--nq", type=int, default=0, help="first nq queries only (0: all)")
 p.add_argument("--ws-gb", type=float, default=48.0, help="workspace cap (GiB)")
-p.add_argument("--rerank", choices=("auto", "query", "list", "tile", "tc"), default="auto", help="re-rank order")
+p.add_argument("--rerank", choices=("auto", "query", "list", "tile"), default="auto", help="re-rank order")
 a = p.parse_args()
 cfg = configs.get(a.workload)
 path = datagen.ensure_index(cfg)
@@ -37,7 +37,7 @@ if a.probe_tc:
 if a.scan_simt:
     g.set_scan_mode(g.SCAN_SIMT)
 g.set_rerank_order({"auto": g.RERANK_AUTO, "query": g.RERANK_QUERY, "list": g.RERANK_LIST,
-                    "tile": g.RERANK_TILE, "tc": g.RERANK_TC}[a.rerank])
+                    "tile": g.RERANK_TILE}[a.rerank])
 q = torch.from_numpy(synth.generate_queries(cfg)).cuda()
 if a.nq:
     q = q[:a.nq].contiguous()
