@@ -1447,8 +1447,18 @@ struct EmitSmem {
   long long s_rb[kEmitWin];
 };
 
+// the thread's 32 cell bytes of chunk c (beyond cap: 0xff, masked by chunk_flags anyway)
+__device__ __forceinline__ Cells32 emit_cells(const Batch& b, int q, int c) {
+  Cells32 cx{make_uint4(~0u, ~0u, ~0u, ~0u), make_uint4(~0u, ~0u, ~0u, ~0u)};
+  const int i0 = c * kChunk + threadIdx.x * kPerThr;
+  const uint4* cl = reinterpret_cast<const uint4*>(b.cells + (size_t)q * b.cap + i0);
+  if (i0 + 16 <= b.cap) cx.a = cl[0];                // cap is a multiple of 16, i0 of 32
+  if (i0 + 32 <= b.cap) cx.b = cl[1];
+  return cx;
+}
+
 __device__ __forceinline__ void emit_chunk(const Batch& b, const Dev& ix, const int* chunk_off, int nchunk, int q,
-                                           int c, EmitSmem& sm) {
+                                           int c, const Cells32& cx, EmitSmem& sm) {
   int* wcnt = sm.wcnt;
   int* s_pre = sm.s_pre;
   unsigned* s_flg = sm.s_flg;
@@ -1468,12 +1478,6 @@ __device__ __forceinline__ void emit_chunk(const Batch& b, const Dev& ix, const 
   const int cnext = c + 1 < nchunk ? chunk_off[cq + 1] : 0;
   const int jc = b.chunkj[cq];
   const int jnext = c + 1 < nchunk ? b.chunkj[cq + 1] : 0;
-  Cells32 cx{make_uint4(~0u, ~0u, ~0u, ~0u), make_uint4(~0u, ~0u, ~0u, ~0u)};
-  {
-    const uint4* cl = reinterpret_cast<const uint4*>(b.cells + (size_t)q * b.cap + i0);
-    if (i0 + 16 <= b.cap) cx.a = cl[0];              // cap is a multiple of 16, i0 of 32
-    if (i0 + 32 <= b.cap) cx.b = cl[1];
-  }
   if (c * kChunk >= n) return;
   const int need = (n + kChunk - 1) / kChunk;        // chunks without candidates exit at once
   const int cend = c + 1 < need ? cnext : ncq;
@@ -1563,9 +1567,12 @@ __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chu
   const int q = blockIdx.y;
   const int n = b.poff[(size_t)q * (b.nprobe + 1) + b.nprobe];
   const int need = (n + kChunk - 1) / kChunk;
+  Cells32 nx = emit_cells(b, q, blockIdx.x);          // the next chunk's cells load ahead
   for (int c = blockIdx.x; c < need; c += gridDim.x) {
     __syncthreads();                                 // shared memory of the previous chunk free
-    emit_chunk(b, ix, chunk_off, nchunk, q, c, sm);
+    const Cells32 cx = nx;
+    if (c + (int)gridDim.x < need) nx = emit_cells(b, q, c + gridDim.x);
+    emit_chunk(b, ix, chunk_off, nchunk, q, c, cx, sm);
   }
 }
 
