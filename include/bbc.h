@@ -186,6 +186,23 @@ bbc_status bbc_set_rerank_order(bbc_index index, int32_t order);
 bbc_status bbc_set_code_loads(bbc_index index, int32_t mode);
 
 /*
+ * bbc_set_scan_order -- the order in which the 8-bit PQ scan (steps a3/a4) visits the probed
+ * objects.  Same results in every order (each object's estimate and bucket id go to its
+ * probe-order position; the histogram is an integer sum); only the L2 reuse of the codes differs.
+ *   BBC_ORDER_PROBE : query after query, each query's lists nearest first (probe order).
+ *   BBC_ORDER_SWEEP : each query's lists by ascending list id, work items issued by the list
+ *                    holding their first object, so the items in flight share a window of lists
+ *                    whose codes stay in L2 (a list's codes come from HBM about once per pass).
+ *   BBC_ORDER_AUTO  : (default) SWEEP when this shard's codes exceed half of the L2 size, PROBE
+ *                    otherwise.
+ * BBC_ERR_ARG for a null index or an unknown order.  Must not change while a search is in flight.
+ */
+#define BBC_ORDER_AUTO 0
+#define BBC_ORDER_PROBE 1
+#define BBC_ORDER_SWEEP 2
+bbc_status bbc_set_scan_order(bbc_index index, int32_t order);
+
+/*
  * bbc_workspace_size -- bytes of device workspace bbc_search needs for (nq, k, nprobe, budget).
  * The workspace holds per-query scratch sized for the nprobe largest lists (cell ids, candidate
  * rows and distances) plus query/output staging used by bbc_search_host.  Queries are processed

@@ -26,7 +26,7 @@ EXPORTS = ("ivf_load", "ivf_free", "bbc_index_info", "bbc_workspace_size", "bbc_
            "bbc_comm_init", "bbc_search_group", "bbc_last_stats2", "bbc_set_probe_mode",
            "bbc_set_scan_mode", "bbc_stats_vector", "bbc_set_buckets", "bbc_set_rerank_order",
            "bbc_measure_l2_read", "bbc_set_remap", "bbc_set_code_loads",
-           "bbc_measure_smem_lookups")
+           "bbc_measure_smem_lookups", "bbc_set_scan_order")
 
 STAGES = ("probe", "tables", "sample", "scan", "compact", "rerank", "select", "comm")
 TAU_INF = 1 << 30
@@ -89,6 +89,7 @@ def lib() -> ctypes.CDLL:
         L.bbc_set_rerank_order.argtypes = [vp, i32]
         L.bbc_set_remap.argtypes = [vp, i32]
         L.bbc_set_code_loads.argtypes = [vp, i32]
+        L.bbc_set_scan_order.argtypes = [vp, i32]
         L.bbc_measure_smem_lookups.argtypes = [i32, i32, ctypes.POINTER(ctypes.c_double)]
         L.bbc_measure_l2_read.argtypes = [i32, ctypes.c_size_t, i32, ctypes.POINTER(ctypes.c_double)]
         L.bbc_stats_vector.argtypes = [vp, ctypes.POINTER(i64), i32]
@@ -108,7 +109,7 @@ def lib() -> ctypes.CDLL:
                    "bbc_comm_init", "bbc_search_group", "bbc_last_stats2", "bbc_set_probe_mode",
                    "bbc_set_scan_mode", "bbc_stats_vector", "bbc_set_buckets",
                    "bbc_set_rerank_order", "bbc_measure_l2_read", "bbc_set_remap",
-                   "bbc_set_code_loads", "bbc_measure_smem_lookups"):
+                   "bbc_set_code_loads", "bbc_measure_smem_lookups", "bbc_set_scan_order"):
             getattr(L, fn).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -368,6 +369,14 @@ class Index:
         (CODES_STREAM) or chosen from the codes' size against the L2 size (CODES_AUTO, default).
         Same results in every mode."""
         _check(lib().bbc_set_code_loads(self._h, int(mode)))
+
+    ORDER_AUTO, ORDER_PROBE, ORDER_SWEEP = 0, 1, 2
+
+    def set_scan_order(self, order: int) -> None:
+        """Visiting order of the 8-bit PQ scan: probe order (ORDER_PROBE), lists by ascending id
+        with work items issued by their first list (ORDER_SWEEP: codes shared through L2), or
+        chosen from the codes' size against the L2 size (ORDER_AUTO, default).  Same results."""
+        _check(lib().bbc_set_scan_order(self._h, int(order)))
 
     RERANK_QUERY, RERANK_LIST, RERANK_AUTO, RERANK_TILE = 0, 1, 2, 3
 

@@ -79,6 +79,7 @@ struct bbc_index_s {
   int rerank_order = BBC_RERANK_AUTO;    // BBC_RERANK_*: work order of the exact re-rank (a7)
   int remap_m = 0;                       // 0 or m equal-depth buckets (bbc_set_remap)
   int code_loads = BBC_CODES_AUTO;       // BBC_CODES_*: L1 policy of the PQ scan's code loads
+  int scan_order = BBC_ORDER_AUTO;        // BBC_SCAN_*: visiting order of the 8-bit PQ scan
   int2* rt_units = nullptr;             // [rt_nunits] (list, tile) of the shared-memory re-rank
   int rt_nunits = 0;                    //   (BBC_RERANK_TILE; fp32 rows of <= 512 bytes)
   int* rt_ubase = nullptr;              // [nlist] first unit of each list
@@ -207,8 +208,11 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1, bool xch
   p.per_query += (size_t)nprobe * 20 + (size_t)(cap / piece) * 16;      // re-rank pieces
   p.per_query += (size_t)nprobe * ix->rt_maxtiles * 16;                   //   + cuts at tile bounds
   p.per_query += kCells;                                                 // remap
+  p.per_query += (size_t)(2 * nprobe + 1) * 4 +                          // sweep order (sperm, spad)
+                 (size_t)((cap + 32LL * nprobe + kItemMin - 1) / kItemMin) * 12;   //   + items_s, ikey
   if (xchg || world > 1) p.per_query += (size_t)k * 16 + (size_t)world * 8;   // result exchange (XBuf)
-  p.fixed = 64 * 256 + (size_t)3 * (std::max(ix->nlist, ix->rt_nunits) + 1) * 4 + 3 * 256;
+  p.fixed = 64 * 256 + (size_t)3 * (std::max(ix->nlist, ix->rt_nunits) + 1) * 4 + 3 * 256 +
+            (size_t)(ix->nlist + 1) * 4 + 512;                          // icnt, ictr
   if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) {            // pair codes + inverted index
     p.per_query += (size_t)nprobe * ((size_t)ix->D + sizeof(RbqPair) + 4);   // codes, records, slots
     p.fixed += (size_t)kRbN * ix->nlist * ((size_t)ix->D + sizeof(RbqPair)) +   // per-list padding
@@ -252,6 +256,11 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nqmax, int nprobe,
   b.qperm = (int*)take((size_t)nqb * 4);
   b.items = (int2*)take((size_t)nqb * ((p.cap + 32LL * nprobe + kItemMin - 1) / kItemMin) * 8);
   b.nitems = (int*)take(4);
+  b.sperm = (int*)take((size_t)nqb * nprobe * 4);
+  b.spad = (int*)take((size_t)nqb * (nprobe + 1) * 4);
+  b.items_s = (int2*)take((size_t)nqb * ((p.cap + 32LL * nprobe + kItemMin - 1) / kItemMin) * 8);
+  b.ikey = (int*)take((size_t)nqb * ((p.cap + 32LL * nprobe + kItemMin - 1) / kItemMin) * 4);
+  b.icnt = (int*)take((size_t)(ix->nlist + 1) * 4);
   b.nsamp = (int*)take((size_t)nqb * 4);
   b.edges = (float*)take((size_t)nqb * 8);
   b.hist = (int*)take((size_t)nqb * kCells * 4);
@@ -316,11 +325,14 @@ __global__ void k_debug_cands(const int* cpos, const float* val, const int* ncan
 
 template <int M>
 void launch_rq(bool est, int grid, cudaStream_t st, const Batch& b, const Dev& dv,
-               const uint8_t* ct, const long long* tb, float* out, long long stride, int mode, bool na) {
+               const uint8_t* ct, const long long* tb, float* out, long long stride, int mode, bool na,
+               bool sweep) {
 #define BBC_RQ_L(E, NA)                                                                                  \
   do {                                                                                                  \
     set_smem(k_pq_scan_rq<M, E, NA>, kRqSmem);                                                          \
-    k_pq_scan_rq<M, E, NA><<<grid, kRqNT, kRqSmem, st>>>(b, dv, ct, tb, out, stride, mode, b.items, b.nitems); \
+    k_pq_scan_rq<M, E, NA><<<grid, kRqNT, kRqSmem, st>>>(b, dv, ct, tb, out, stride, mode,              \
+                                                          sweep ? b.items_s : b.items, b.nitems,        \
+                                                          sweep ? b.sperm : nullptr);                   \
   } while (0)
   if (est) { if (na) BBC_RQ_L(true, true); else BBC_RQ_L(true, false); }
   else { if (na) BBC_RQ_L(false, true); else BBC_RQ_L(false, false); }
@@ -331,17 +343,30 @@ void launch_rq(bool est, int grid, cudaStream_t st, const Batch& b, const Dev& d
 // na: code loads bypass L1 allocation (codes larger than half of L2, or forced by
 // bbc_set_code_loads).
 void rq_scan(int M, bool est, int num_sms, cudaStream_t st, const Batch& b, const Dev& dv,
-             const uint8_t* ct, const long long* tb, float* out, long long stride, int mode, bool na) {
+             const uint8_t* ct, const long long* tb, float* out, long long stride, int mode, bool na,
+             bool sweep) {
   if (b.nq <= 0) return;
+  if (sweep) {                                       // the visiting order of the main pass
+    k_sweep_order<<<b.nq, kSelNT, 0, st>>>(b, dv);
+    g_launches += 1;
+  }
   k_scan_plan<<<1, 1024, 0, st>>>(b, mode, b.items, b.nitems, kRqE);
   g_launches += 1;
+  if (sweep) {
+    const int gi = 4 * num_sms;
+    cudaMemsetAsync(b.icnt, 0, (size_t)(dv.nlist + 1) * 4, st);
+    k_item_count<<<gi, 256, 0, st>>>(b, mode, kRqE);
+    k_item_offsets<<<1, 1024, 0, st>>>(b.icnt, dv.nlist);
+    k_item_scatter<<<gi, 256, 0, st>>>(b);
+    g_launches += 3;
+  }
   switch (M) {
-    case 8: launch_rq<8>(est, num_sms, st, b, dv, ct, tb, out, stride, mode, na); break;
-    case 16: launch_rq<16>(est, num_sms, st, b, dv, ct, tb, out, stride, mode, na); break;
-    case 24: launch_rq<24>(est, num_sms, st, b, dv, ct, tb, out, stride, mode, na); break;
-    case 32: launch_rq<32>(est, num_sms, st, b, dv, ct, tb, out, stride, mode, na); break;
-    case 48: launch_rq<48>(est, num_sms, st, b, dv, ct, tb, out, stride, mode, na); break;
-    case 64: launch_rq<64>(est, num_sms, st, b, dv, ct, tb, out, stride, mode, na); break;
+    case 8: launch_rq<8>(est, num_sms, st, b, dv, ct, tb, out, stride, mode, na, sweep); break;
+    case 16: launch_rq<16>(est, num_sms, st, b, dv, ct, tb, out, stride, mode, na, sweep); break;
+    case 24: launch_rq<24>(est, num_sms, st, b, dv, ct, tb, out, stride, mode, na, sweep); break;
+    case 32: launch_rq<32>(est, num_sms, st, b, dv, ct, tb, out, stride, mode, na, sweep); break;
+    case 48: launch_rq<48>(est, num_sms, st, b, dv, ct, tb, out, stride, mode, na, sweep); break;
+    case 64: launch_rq<64>(est, num_sms, st, b, dv, ct, tb, out, stride, mode, na, sweep); break;
   }
 }
 
@@ -377,9 +402,12 @@ void pq_scan(const bbc_index_s* ix, bool est, cudaStream_t st, const Batch& b, c
     return;
   }
   // codes that do not fit in L2 are streamed past L1 (see k_pq_scan_rq); L2 size queried at load
-  const bool na = ix->code_loads == BBC_CODES_STREAM ||
-                  (ix->code_loads == BBC_CODES_AUTO && (double)ix->n_local * ix->M > 0.5 * (double)ix->l2_bytes);
-  rq_scan(ix->M, est, ix->num_sms, st, b, dv, ix->codes_t, ix->tbase, out, stride, mode, na);
+  const bool big = (double)ix->n_local * ix->M > 0.5 * (double)ix->l2_bytes;
+  const bool na = ix->code_loads == BBC_CODES_STREAM || (ix->code_loads == BBC_CODES_AUTO && big);
+  // sweep order (k_sweep_order) of the main pass for codes that do not fit in L2; the sample
+  // pass (the nearest lists, shared by the queries of a locality region) keeps probe order
+  const bool sweep = mode == 1 && (ix->scan_order == BBC_ORDER_SWEEP || (ix->scan_order == BBC_ORDER_AUTO && big));
+  rq_scan(ix->M, est, ix->num_sms, st, b, dv, ix->codes_t, ix->tbase, out, stride, mode, na, sweep);
 }
 
 bbc_status check_args(bbc_index ix, const void* q, int64_t nq, int32_t k, int32_t nprobe,
@@ -1715,6 +1743,14 @@ bbc_status bbc_set_code_loads(bbc_index ix, int32_t mode) {
   if (mode != BBC_CODES_AUTO && mode != BBC_CODES_CACHED && mode != BBC_CODES_STREAM)
     return fail(BBC_ERR_ARG, "unknown code-load mode");
   ix->code_loads = mode;
+  return BBC_OK;
+}
+
+bbc_status bbc_set_scan_order(bbc_index ix, int32_t order) {
+  if (!ix) return fail(BBC_ERR_ARG, "null index");
+  if (order != BBC_ORDER_AUTO && order != BBC_ORDER_PROBE && order != BBC_ORDER_SWEEP)
+    return fail(BBC_ERR_ARG, "unknown scan order");
+  ix->scan_order = order;
   return BBC_OK;
 }
 

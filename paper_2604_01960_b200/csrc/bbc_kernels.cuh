@@ -51,6 +51,14 @@ struct Batch {
   int* rs_cnt;        // [nlist + 1]    piece counts (rs_off[nlist] = #pieces)
   int* rs_off;        // [nlist + 1]
   int* rs_cur;        // [nlist + 1]
+  // sweep order of the 8-bit PQ scan (k_sweep_order / k_item_*): probe positions sorted by list
+  // id within the sample and the main segment, their padded prefix offsets, and the work items
+  // sorted by the list holding their first object
+  int* sperm;         // [nq x nprobe]      sorted position -> probe position
+  int* spad;          // [nq x (nprobe+1)]  padded offsets in sorted order (spad[ns] = popad[ns])
+  int2* items_s;      // [as items]         items in sweep order
+  int* ikey;          // [as items]         first list of each item
+  int* icnt;          // [nlist + 1]        items per first list -> offsets
 };
 
 // Index arrays on the device.
@@ -636,7 +644,8 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
                                                          const long long* __restrict__ tbase,
                                                          float* out_est, long long est_stride,
                                                          int mode, const int2* __restrict__ items,
-                                                         const int* __restrict__ nitems) {
+                                                         const int* __restrict__ nitems,
+                                                         const int* __restrict__ sperm) {
   constexpr int P = M / kRqMC;                       // chunks
   extern __shared__ __align__(16) uint8_t rsm[];
   float* lut = reinterpret_cast<float*>(rsm);
@@ -646,6 +655,7 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
   int* hist = reinterpret_cast<int*>(rsm + kRqOffHist);
   int* s_popad = reinterpret_cast<int*>(rsm + kRqOffPo);
   // persistent CTAs over the work items of k_scan_plan: (query, pass) in query locality order
+  // (probe order) or sorted by their first list (sweep order)
   const int nit = *nitems;
   for (int it = blockIdx.x; it < nit; it += gridDim.x) {
   __syncthreads();                                   // shared memory of the previous item free
@@ -655,7 +665,9 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
   if (mode != 2 && ns == 0) continue;                // tau = infinity: nothing to bucket
   const int first = mode == 1 ? ns : 0;
   const int lim = mode == 0 ? ns : b.nprobe;
-  const int* popad = b.popad + (size_t)q * (b.nprobe + 1);
+  // padded offsets in visiting order: probe order (sperm == null) or sweep order (k_sweep_order)
+  const int* popad = (sperm ? b.spad : b.popad) + (size_t)q * (b.nprobe + 1);
+  const int* sp = sperm ? sperm + (size_t)q * b.nprobe : nullptr;
   const int nflat = popad[lim];
   const int x0 = popad[first] + wk.y * kRqE;
   if (x0 >= nflat) continue;
@@ -686,12 +698,13 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
         const int mid = (lo + hi + 1) >> 1;
         if (s_popad[mid] <= xg) lo = mid; else hi = mid - 1;
       }
-      const int L = pr[lo];
+      const int j = sp ? sp[lo] : lo;                // probe position of the group's list
+      const int L = pr[j];
       const int nL = (int)(ix.loff[L + 1] - ix.loff[L]);
       const int i0 = xg - s_popad[lo];
       cnt = min(32, nL - i0);
       go = (uint32_t)((tbase[L] + (long long)(i0 >> 5) * M * 32) >> 7);
-      oo = obase + po[lo] + i0;
+      oo = obase + po[j] + i0;
     }
     gofs[G] = go;
     gout[G] = oo;
@@ -842,6 +855,137 @@ __global__ void __launch_bounds__(1024) k_scan_plan(Batch b, int mode, int2* ite
     __syncthreads();
   }
   if (threadIdx.x == 0) *nitems = carry;
+}
+
+// Sweep order of the 8-bit PQ scan (codes larger than L2).  In probe order the CTAs that run
+// at the same time scan unrelated lists of unrelated queries, so every (query, list) pair pulls
+// the list's codes from HBM again (C4: DRAM reads 0.76x the algorithmic code bytes).  In sweep
+// order each query's lists are visited by ascending list id and the work items are issued by the
+// list holding their first object: the ~148 items in flight then cover one window of the list-id
+// space (C4: an item spans ~50 lists, ~1,100 list ids, ~33 MB of codes), which stays in L2 while
+// the other queries' items that start in it pass.  Only the visiting order changes: every
+// object's estimate / bucket id still goes to its probe-order position (poff), so the results are
+// identical bit for bit.
+//
+// k_sweep_order: one CTA (kSelNT threads) per query.  Probe positions sorted by (segment, list
+// id) -- segment 0 = the sample lists [0, ns), 1 = the rest -- and the padded prefix offsets in
+// that order (the segment totals equal popad's: spad[ns] = popad[ns], spad[nprobe] = popad[nprobe]).
+__global__ void __launch_bounds__(kSelNT) k_sweep_order(Batch b, Dev ix) {
+  __shared__ uint64_t keys[kMaxProbe];
+  __shared__ int ws[kSelNT / 32];
+  __shared__ int carry;
+  const int q = blockIdx.x, np = b.nprobe, ns = b.nsamp[q];
+  const int* pr = b.probe + (size_t)q * np;
+  int P2 = 1;
+  while (P2 < np) P2 <<= 1;
+  for (int i = threadIdx.x; i < P2; i += kSelNT)
+    keys[i] = i < np ? ((uint64_t)(i >= ns) << 63) | ((uint64_t)pr[i] << 24) | (uint64_t)i : ~0ull;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  bitonic_sort_keys(keys, P2);
+  __syncthreads();
+  int* sp = b.sperm + (size_t)q * np;
+  int* pd = b.spad + (size_t)q * (np + 1);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int base = 0; base < np; base += kSelNT) {
+    const int t = base + threadIdx.x;
+    int sz = 0, j = 0;
+    if (t < np) {
+      j = (int)(keys[t] & 0xffffffu);
+      const int L = pr[j];
+      sz = ((int)(ix.loff[L + 1] - ix.loff[L]) + 31) & ~31;
+      sp[t] = j;
+    }
+    int x = sz;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      const int v = ws[lane];
+      int y = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int z = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= o) y += z;
+      }
+      ws[lane] = y - v;
+    }
+    __syncthreads();
+    if (t < np) pd[t] = carry + ws[wid] + x - sz;
+    __syncthreads();
+    if (threadIdx.x == kSelNT - 1) carry += ws[wid] + x;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) pd[np] = carry;
+}
+
+// Sweep-ordered work items: a counting sort of k_scan_plan's items by the list holding their
+// first object.  k_item_count: that list per item (binary search of the item's first padded
+// position in spad) and the per-list counts; k_item_offsets: exclusive scan of the counts (one
+// CTA); k_item_scatter: items to their list's slots (order inside a list unspecified -- it changes
+// no result: items write disjoint outputs and add integer counts).
+__global__ void __launch_bounds__(256) k_item_count(Batch b, int mode, int item_objs) {
+  const int nit = *b.nitems;
+  for (int it = blockIdx.x * 256 + threadIdx.x; it < nit; it += gridDim.x * 256) {
+    const int2 wk = b.items[it];
+    const int q = wk.x, ns = b.nsamp[q];
+    const int first = mode == 1 ? ns : 0, lim = mode == 0 ? ns : b.nprobe;
+    const int* pd = b.spad + (size_t)q * (b.nprobe + 1);
+    const int x = pd[first] + wk.y * item_objs;
+    int lo = first, hi = lim - 1;                      // last t with spad[t] <= x
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (pd[mid] <= x) lo = mid; else hi = mid - 1;
+    }
+    const int L = b.probe[(size_t)q * b.nprobe + b.sperm[(size_t)q * b.nprobe + lo]];
+    b.ikey[it] = L;
+    atomicAdd(&b.icnt[L], 1);
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_item_offsets(int* cnt, int n) {
+  __shared__ int ws[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int base = 0; base < n; base += 1024) {
+    const int i = base + threadIdx.x;
+    const int v = i < n ? cnt[i] : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      const int w = ws[lane];
+      int y = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int z = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= o) y += z;
+      }
+      ws[lane] = y - w;
+    }
+    __syncthreads();
+    if (i < n) cnt[i] = carry + ws[wid] + x - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += ws[wid] + x;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_item_scatter(Batch b) {
+  const int nit = *b.nitems;
+  for (int it = blockIdx.x * 256 + threadIdx.x; it < nit; it += gridDim.x * 256)
+    b.items_s[atomicAdd(&b.icnt[b.ikey[it]], 1)] = b.items[it];
 }
 
 // Index-load-time copy of the PQ codes in the group-major order of k_pq_scan_rq.

@@ -173,6 +173,24 @@ def test_parity_code_load_modes(name):
         g.set_code_loads(g.CODES_AUTO)
 
 
+@pytest.mark.parametrize("name,nprobe", [("C2s", None), ("C4s", None), ("C5s", None), ("C4ip_s", None),
+                                         ("C2f", 1500)])
+def test_parity_scan_orders(name, nprobe):
+    """The 8-bit PQ scan in sweep order (BBC_ORDER_SWEEP: each query's lists by ascending id,
+    work items sorted by their first list -- the order full-size C4/C5 take) and in probe order
+    (BBC_ORDER_PROBE): both equal the oracle bit for bit (estimates, histograms, superset, results).
+    C2f at nprobe 1,500 runs the order kernel's two-keys-per-thread sort."""
+    cfg, ix, Q, g = gpu_index(name)
+    npr = nprobe or cfg.nprobe
+    q = Q if nprobe is None else Q[:4]
+    try:
+        for order in (g.ORDER_SWEEP, g.ORDER_PROBE):
+            g.set_scan_order(order)
+            compare(cfg, ix, q, g, cfg.k, npr, cfg.budget)
+    finally:
+        g.set_scan_order(g.ORDER_AUTO)
+
+
 @pytest.mark.parametrize("nprobe", [1025, 1500, 2048])
 def test_parity_probe_sets_past_1024(nprobe):
     """Probe sets of 1,025-2,048 lists (C3's operating point has 2,048): the probe selection's

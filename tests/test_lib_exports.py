@@ -65,7 +65,8 @@ def test_python_constants_match_header():
              "RERANK_LIST": "BBC_RERANK_LIST", "RERANK_AUTO": "BBC_RERANK_AUTO",
              "RERANK_TILE": "BBC_RERANK_TILE",
              "CODES_AUTO": "BBC_CODES_AUTO", "CODES_CACHED": "BBC_CODES_CACHED",
-             "CODES_STREAM": "BBC_CODES_STREAM"}
+             "CODES_STREAM": "BBC_CODES_STREAM", "ORDER_AUTO": "BBC_ORDER_AUTO",
+             "ORDER_PROBE": "BBC_ORDER_PROBE", "ORDER_SWEEP": "BBC_ORDER_SWEEP"}
     for py, c in pairs.items():
         assert c in defs, c
         assert getattr(Index, py) == int(defs[c]), py
@@ -77,5 +78,6 @@ def test_setters_reject_bad_arguments_without_gpu():
     L = bbc.lib()
     for fn, v in (("bbc_set_buckets", 0), ("bbc_set_buckets", 256), ("bbc_set_remap", -1),
                   ("bbc_set_remap", 256), ("bbc_set_rerank_order", 7), ("bbc_set_scan_mode", 9),
-                  ("bbc_set_probe_mode", 5), ("bbc_set_code_loads", 3)):
+                  ("bbc_set_probe_mode", 5), ("bbc_set_code_loads", 3),
+                  ("bbc_set_scan_order", 3)):
         assert getattr(L, fn)(None, v) == 1, fn            # null index first: BBC_ERR_ARG
