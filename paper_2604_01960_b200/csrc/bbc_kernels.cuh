@@ -1179,12 +1179,13 @@ struct Kth32Smem {
   unsigned hist[2048];
   unsigned wsum[32];
   unsigned mn[32], mx[32];
-  unsigned prefix, digit, need;
+  unsigned prefix, digit, need, dcount;
 };
 
+// *eq_out (optional): how many keys equal the returned kth key (its bin in the last pass)
 template <typename KeyF>
 __device__ uint32_t cta_kth32(int n, unsigned kth, KeyF key, unsigned* take, Kth32Smem& sm,
-                              uint32_t* min_out = nullptr) {
+                              uint32_t* min_out = nullptr, unsigned* eq_out = nullptr) {
   constexpr int NT = kSelNT;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   unsigned mn = 0xffffffffu, mx = 0u;
@@ -1209,7 +1210,11 @@ __device__ uint32_t cta_kth32(int n, unsigned kth, KeyF key, unsigned* take, Kth
   if (min_out) *min_out = mn;
   __syncthreads();
   if (mn == mx || kth <= 1) {
-    if (mn == mx) { *take = kth; return mn; }
+    if (mn == mx) {
+      *take = kth;
+      if (eq_out) *eq_out = (unsigned)n;             // (every key valid: the callers' case)
+      return mn;
+    }
   }
   int hi = 31 - __clz(mn ^ mx);                       // highest differing bit
   uint32_t prefix = hi == 31 ? 0u : (mn >> (hi + 1));
@@ -1250,16 +1255,20 @@ __device__ uint32_t cta_kth32(int n, unsigned kth, KeyF key, unsigned* take, Kth
     __syncthreads();
     const unsigned excl = sm.wsum[wid] + x - (h0 + h1);
     if (excl < need && need <= excl + h0) {
-      sm.digit = 2 * threadIdx.x; sm.need = need - excl;
+      sm.digit = 2 * threadIdx.x; sm.need = need - excl; sm.dcount = h0;
     } else if (excl + h0 < need && need <= excl + h0 + h1) {
-      sm.digit = 2 * threadIdx.x + 1; sm.need = need - excl - h0;
+      sm.digit = 2 * threadIdx.x + 1; sm.need = need - excl - h0; sm.dcount = h1;
     }
     __syncthreads();
     need = sm.need;
     prefix = (pshift == 32 ? 0u : (prefix << width)) | sm.digit;
     pshift = shift;
+    const unsigned dc = sm.dcount;
     __syncthreads();
-    if (shift == 0) break;
+    if (shift == 0) {
+      if (eq_out) *eq_out = dc;
+      break;
+    }
   }
   *take = need;
   return prefix;
@@ -1981,15 +1990,20 @@ __global__ void __launch_bounds__(kSelNT) k_final_select(Batch b, Dev ix, long l
     // flight hold ~100 MB of distances: the sampled bracket, cta_kth32_bracket, C4 select 6.7 ->
     // 7.2 ms; gathering the first digit's bin with its ids into 64 KB of shared memory and
     // finishing there, 6.5 -> 7.2 ms)
-    unsigned take;
-    T = cta_kth32(nc, (unsigned)k, [&](int i, bool* ok) { *ok = true; return f2key(vv[i]); }, &take, sm);
-    // elements equal to T: take the `take` smallest ids (ids are unique)
-    unsigned t2;
-    I = cta_kth32(nc, take, [&](int i, bool* ok) {
-          const uint32_t f = f2key(vv[i]);
-          *ok = f == T;
-          return *ok ? (uint32_t)cp[i] : 0u;
-        }, &t2, sm);
+    unsigned take, eq;
+    T = cta_kth32(nc, (unsigned)k, [&](int i, bool* ok) { *ok = true; return f2key(vv[i]); }, &take, sm,
+                  nullptr, &eq);
+    // elements equal to T: take the `take` smallest ids (ids are unique) -- unless all of them
+    // are taken (no tie across the k-th position, the usual case for real-valued data: the id
+    // selection's passes over the candidates are skipped)
+    if (take < eq) {
+      unsigned t2;
+      I = cta_kth32(nc, take, [&](int i, bool* ok) {
+            const uint32_t f = f2key(vv[i]);
+            *ok = f == T;
+            return *ok ? (uint32_t)cp[i] : 0u;
+          }, &t2, sm);
+    }
     all = false;
   }
   int base = 0;
