@@ -734,10 +734,14 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
 #pragma unroll
   for (int e = 0; e < kRqEW; ++e) acc[e] = 0.f;
   const uint32_t lane4 = (uint32_t)lane * 4u;
-  // (warps whose groups all lie past the item's objects still run the lookups: skipping them
-  // under a warp-uniform branch measured slower on C4, 50.2 -> 54.2 ms, from the loop's codegen)
+  // sample pass over L2-resident codes (EST, !NOALLOC): a warp whose groups all lie past the
+  // item's objects (valid groups form a prefix; a query's sample ends in a partly filled item)
+  // only stages and syncs (C2 sample 0.39 -> 0.35 ms).  Elsewhere the loop stays unconditional:
+  // the branch measured slower on the main pass (C4 50.2 -> 54.2 ms) and on C4's streamed sample
+  // pass (14.1 -> 14.8 ms).
+  const bool wact = !(EST && !NOALLOC) || gcnt[wid * 4 * kRqGPL] > 0;
   uint4 cw[kRqDepth];
-  static_for<kRqDepth>([&](auto ic) { cw[decltype(ic)::value] = ldc(ic, 0); });
+  if (wact) static_for<kRqDepth>([&](auto ic) { cw[decltype(ic)::value] = ldc(ic, 0); });
 #pragma unroll 1
   for (int p = 0; p < P; ++p) {
     __syncthreads();                                  // previous chunk fully consumed
@@ -762,7 +766,7 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
     }
     __syncthreads();
     const int pn = p + 1 < P ? p + 1 : p;            // code loads run one chunk ahead at the tail
-    static_for<kRqGPL>([&](auto ic) {
+    if (wact) static_for<kRqGPL>([&](auto ic) {
       constexpr int i = decltype(ic)::value;
       const uint4 c = cw[i % kRqDepth];
       if constexpr (i + kRqDepth < kRqGPL)
