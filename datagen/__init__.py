@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import hashlib
 import os
+import sys
 import time
 
 from . import build_index, configs, index_file, synth  # noqa: F401
@@ -69,5 +70,5 @@ def ensure_index(cfg: Config, verbose: bool = False) -> str:
         idx = build_index.build(cfg, verbose=verbose)
         index_file.write(path, idx)
         if verbose:
-            print(f"[datagen] built {cfg.name} index in {time.time() - t0:.1f}s -> {path}")
+            print(f"[datagen] built {cfg.name} index in {time.time() - t0:.1f}s -> {path}", file=sys.stderr)
     return path

@@ -30,6 +30,7 @@ from __future__ import annotations
 
 import math
 import os
+import sys
 
 import numpy as np
 import torch
@@ -140,7 +141,7 @@ def build(cfg: Config, X: np.ndarray | None = None, verbose: bool = False) -> di
                centroids=cent, list_offsets=offsets, ids=order.astype(np.int64),
                raw=np.ascontiguousarray(X[order]))
     if verbose:
-        print(f"[build] {cfg.name}: lists built, sizes min {sizes.min()} max {sizes.max()}")
+        print(f"[build] {cfg.name}: lists built, sizes min {sizes.min()} max {sizes.max()}", file=sys.stderr)
     if cfg.kind == "pq":
         M, ds = cfg.M, cfg.dsub
         trq = np.sort(gq.choice(N, size=min(N, cfg.pq_train), replace=False))
