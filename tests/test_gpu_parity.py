@@ -438,6 +438,26 @@ def test_sharded_group_equals_single(name, G):
         assert np.array_equal(a[1].view(np.uint32), b[1].view(np.uint32))
 
 
+@pytest.mark.parametrize("name,G", [("C2s", 2), ("C5s", 3)])
+def test_sharded_group_sweep_order(name, G):
+    """The list-sharded group search with every shard's PQ scan in sweep order (each shard sorts
+    its own probed lists and work items): results equal the unsharded search bit for bit."""
+    from paper_2604_01960_b200 import Index
+    from paper_2604_01960_b200.bbc import search_group
+    cfg, ix, Q, g = gpu_index(name)
+    path = _LOAD["f"](name)[3]
+    shards = [Index(path, rank=r, world=G) for r in range(G)]
+    for s in shards:
+        s.set_scan_order(s.ORDER_SWEEP)
+    q = torch.from_numpy(Q).cuda()
+    a_ids, a_d2 = g.search(q, cfg.k, cfg.nprobe, cfg.budget)
+    b_ids, b_d2 = search_group(shards, q, cfg.k, cfg.nprobe, cfg.budget)
+    a = _sorted_by_id(a_ids.cpu().numpy(), a_d2.cpu().numpy())
+    b = _sorted_by_id(b_ids.cpu().numpy(), b_d2.cpu().numpy())
+    assert np.array_equal(a[0], b[0])
+    assert np.array_equal(a[1].view(np.uint32), b[1].view(np.uint32))
+
+
 def test_nccl_path_world1_equals_single():
     """bbc_search through the sharded code path with a real (1-rank) NCCL communicator."""
     from paper_2604_01960_b200 import Index
