@@ -1018,24 +1018,36 @@ __global__ void __launch_bounds__(256) k_sample_cells(Batch b) {
   const int ns = b.nsamp[q];
   if (ns == 0) return;
   const int n = b.poff[(size_t)q * (b.nprobe + 1) + ns];
-  if (blockIdx.x * 256 >= n) return;
+  if (blockIdx.x * 1024 >= n) return;
   for (int i = threadIdx.x; i < kCells; i += 256) hist[i] = 0;
   CellFn cf;
   cf.init(b.edges[2 * q], b.edges[2 * q + 1], b.nbuckets);
   __syncthreads();
   const float* v = b.val + (size_t)q * b.cap;
   uint8_t* cl = b.cells + (size_t)q * b.cap;
-  const int stride = gridDim.x * 256;
-  for (int i0 = blockIdx.x * 256 + threadIdx.x; i0 < n; i0 += 4 * stride) {
-    float x[4];                                       // four loads in flight per thread
+  // four consecutive estimates per thread and step: one 16-byte load, one 4-byte store of their
+  // bucket ids (cap is a multiple of 16, so the query's rows are aligned); two steps in flight
+  const int stride = gridDim.x * 256 * 4;
+  for (int i0 = (blockIdx.x * 256 + threadIdx.x) * 4; i0 < n; i0 += 2 * stride) {
+    float4 x[2];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) x[u] = i0 + u * stride < n ? v[i0 + u * stride] : 0.f;
+    for (int u = 0; u < 2; ++u)
+      x[u] = i0 + u * stride < n ? *reinterpret_cast<const float4*>(v + i0 + u * stride) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (i0 + u * stride >= n) break;
-      const int c = cf(x[u]);
-      cl[i0 + u * stride] = (uint8_t)c;
-      if (c < 255) atomicAdd(&hist[c], 1);
+    for (int u = 0; u < 2; ++u) {
+      const int i = i0 + u * stride;
+      if (i >= n) break;
+      const float e[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+      uint32_t w = 0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int c = i + t < n ? cf(e[t]) : 255;
+        w |= (uint32_t)c << (8 * t);
+        if (c < 255) atomicAdd(&hist[c], 1);
+      }
+      if (i + 4 <= n) *reinterpret_cast<uint32_t*>(cl + i) = w;
+      else
+        for (int t = 0; i + t < n; ++t) cl[i + t] = (uint8_t)(w >> (8 * t));
     }
   }
   __syncthreads();
