@@ -308,15 +308,22 @@ def test_host_api_matches_device_api():
     assert np.array_equal(a_d2.cpu().numpy(), h_d2)
 
 
-def test_host_api_pipelined_microbatches():
+@pytest.mark.parametrize("order", ["auto", "sweep"])
+def test_host_api_pipelined_microbatches(order):
     """Host path with >= 4 micro-batches (device->host copies on a second stream, double-buffered
-    staging) returns the device path's results bit for bit, also on a short last batch."""
+    staging) returns the device path's results bit for bit, also on a short last batch; in the
+    scan's default order and in sweep order (the order the full-size C4/C5 host paths take)."""
     from datagen import configs, synth
     cfg, ix, Q, g = gpu_index("C2s")
     Qm = np.ascontiguousarray(synth.generate_queries(cfg, 1100))
     q = torch.from_numpy(Qm).cuda()
     a_ids, a_d2 = g.search(q, 200, cfg.nprobe, 400)
-    h_ids, h_d2 = g.search_host(Qm, 200, cfg.nprobe, 400)
+    try:
+        if order == "sweep":
+            g.set_scan_order(g.ORDER_SWEEP)
+        h_ids, h_d2 = g.search_host(Qm, 200, cfg.nprobe, 400)
+    finally:
+        g.set_scan_order(g.ORDER_AUTO)
     assert g.last_stats()["microbatches"] >= 4
     assert np.array_equal(a_ids.cpu().numpy(), h_ids)
     assert np.array_equal(a_d2.cpu().numpy(), h_d2)
