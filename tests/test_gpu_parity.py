@@ -223,6 +223,21 @@ def test_full_probe_unlimited_budget_is_brute_force():
         check_final_ids(ids[i], d2[i], gi[i], gd[i].astype(np.float32), cfg.k)
 
 
+def test_edge_cases_sweep_order():
+    """Degenerate passes in the scan's sweep order: a main pass with no lists (nprobe = 1: the
+    sample is every probed list), tau = infinity (no sample), k = budget = 1, a single list after
+    the sample, and every list probed."""
+    cfg, ix, Q, g = gpu_index("C1t")
+    try:
+        g.set_scan_order(g.ORDER_SWEEP)
+        compare(cfg, ix, Q[:3], g, 5000, 1, 5000)
+        compare(cfg, ix, Q[:1], g, 1, 4, 1)
+        compare(cfg, ix, Q[:2], g, 250, 9, 250)
+        compare(cfg, ix, Q[:2], g, 300, cfg.nlist, 600)
+    finally:
+        g.set_scan_order(g.ORDER_AUTO)
+
+
 def test_edge_cases():
     from paper_2604_01960_b200.bbc import BBCError
     cfg, ix, Q, g = gpu_index("C1t")
