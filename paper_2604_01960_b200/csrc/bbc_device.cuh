@@ -125,9 +125,15 @@ struct SelectSmem {
 //   set mode (keys must be unique): returns (prefix, *pshift) such that exactly kth keys satisfy
 //   shr64(key, *pshift) <= prefix.
 // Passes of <= 8 bits from the highest bit where the minimum and maximum keys differ.
+// An upper bound of the kth smallest key: the selection above stopped after `passes` digit
+// passes, returning the largest key of the digit bin that holds the kth smallest (every key below
+// it is in a lower bin).  At least the kth smallest key, at most that bin's last key.
+template <int NT, typename LoadF>
+__device__ uint64_t cta_select_upper(int64_t n, int64_t kth, LoadF load, int passes, SelectSmem& sm);
+
 template <int NT, typename LoadF>
 __device__ uint64_t cta_select(int64_t n, int64_t kth, LoadF load, bool value_mode, int* pshift_out,
-                               SelectSmem& sm) {
+                               SelectSmem& sm, int max_passes = 64) {
   uint64_t mn = ~0ull, mx = 0ull;
   for (int64_t i = threadIdx.x; i < n; i += NT) {
     uint64_t k = load(i);
@@ -187,13 +193,20 @@ __device__ uint64_t cta_select(int64_t n, int64_t kth, LoadF load, bool value_mo
     need = sm.need;
     prefix = (prefix << width) | (uint64_t)sm.digit;
     pshift = shift;
-    const bool fin = (shift == 0) || (!value_mode && (long long)sm.cnt == need);
+    const bool fin = (shift == 0) || (!value_mode && (long long)sm.cnt == need) || --max_passes == 0;
     __syncthreads();
     if (fin) break;
     shift = shift - 8 > 0 ? shift - 8 : 0;
   }
   *pshift_out = pshift;
   return prefix;
+}
+
+template <int NT, typename LoadF>
+__device__ uint64_t cta_select_upper(int64_t n, int64_t kth, LoadF load, int passes, SelectSmem& sm) {
+  int ps = 0;
+  const uint64_t pre = cta_select<NT>(n, kth, load, true, &ps, sm, passes);
+  return ps == 0 ? pre : ((pre << ps) | ((1ull << ps) - 1ull));
 }
 
 }  // namespace bbc

@@ -152,6 +152,9 @@ __global__ void __launch_bounds__(256) k_probe_d2(const float* __restrict__ Q,
 //   sorted, so the probe lists equal the SIMT path's.  A shortlist longer than kMaxShort falls
 //   back to canonical d^2 for every list.
 constexpr int kSelNT = 1024;
+#ifndef BBC_PROBE_PASSES
+#define BBC_PROBE_PASSES 2                  // digit passes of the probe shortlist's threshold
+#endif
 constexpr int kMaxProbe = 2048;
 constexpr int kMaxShort = 4096;
 constexpr int kMaxDimTc = 1024;
@@ -296,8 +299,10 @@ __global__ void __launch_bounds__(kSelNT) k_probe_select(Batch b, Dev ix) {
     qn *= 1.0f + 0x1p-10f;                          // margin for this sum's own rounding
     const float E = 0x1p-12f * sqrtf(qn) * ix.cmax + 0x1p-11f * (qn + ix.cmax * ix.cmax);
     auto load32 = [&](int64_t i) -> uint64_t { return (uint64_t)f2key(d2[i]); };
-    int ps;
-    const float T = key2f((uint32_t)cta_select<kSelNT>(nlist, nprobe, load32, true, &ps, sm));
+    // T~ is only needed as a lower end of the shortlist threshold: an upper bound of the
+    // nprobe-th smallest d~ from two 8-bit digit passes instead of the full selection keeps
+    // every true top-nprobe list in the shortlist (a few more lists are re-scored)
+    const float T = key2f((uint32_t)cta_select_upper<kSelNT>(nlist, nprobe, load32, BBC_PROBE_PASSES, sm));
     float thr = T + 2.0f * E;
     thr = thr + fabsf(thr) * 0x1p-20f + 0x1p-100f;  // round the threshold up
     for (int i = threadIdx.x; i < nlist; i += kSelNT)
