@@ -1049,10 +1049,11 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
                                                            (ix->raw_u8 ? ix->d : 4.0 * ix->d);
   const int tail_div = (double)k * 12.0 * 1000.0 < work_b ? 1 : 4;
   const bool pipe = host && !dist && !dbg && tail_div > 1;
-  // host-path micro-batches of nq/8 queries (at least 512): the copies of one overlap the search
-  // of the next at a fine grain (C4: nq/2 -> nq/8: 140.7 -> 126.4 ms per 10,000 queries; C2's
-  // 1,000 queries keep 512-query batches: smaller ones cost more than they overlap)
-  if (pipe) nqb = std::min<long long>(nqb, std::max<long long>(512, (nq + 7) / 8));
+  // host-path micro-batches of nq/12 queries (at least 512): the copies of one overlap the search
+  // of the next at a fine grain (C4: nq/2 -> nq/8: 140.7 -> 126.4 ms per 10,000 queries; with the
+  // sweep-ordered scan nq/12 128.0 vs nq/8 131.6, nq/16 128.9, nq/6 135.0; C2's 1,000 queries
+  // keep 512-query batches: smaller ones cost more than they overlap)
+  if (pipe) nqb = std::min<long long>(nqb, std::max<long long>(512, (nq + 11) / 12));
   if ((pipe || dist) && !ix->copy_stream) {
     CU(cudaStreamCreateWithFlags(&ix->copy_stream, cudaStreamNonBlocking));
     CU(cudaStreamCreateWithFlags(&ix->copy_stream2, cudaStreamNonBlocking));
