@@ -192,7 +192,9 @@ bbc_status bbc_set_code_loads(bbc_index index, int32_t mode);
  *   BBC_ORDER_PROBE : query after query, each query's lists nearest first (probe order).
  *   BBC_ORDER_SWEEP : each query's lists by ascending list id, work items issued by the list
  *                    holding their first object, so the items in flight share a window of lists
- *                    whose codes stay in L2 (a list's codes come from HBM about once per pass).
+ *                    whose codes stay in L2 (a list's codes come from HBM about once per pass);
+ *                    and the sample pass fills its last work item with the lists that follow the
+ *                    sample in probe order (their bucket ids come from those estimates).
  *   BBC_ORDER_AUTO  : (default) SWEEP when this shard's codes exceed half of the L2 size, PROBE
  *                    otherwise.
  * BBC_ERR_ARG for a null index or an unknown order.  Must not change while a search is in flight.

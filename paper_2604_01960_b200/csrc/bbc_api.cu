@@ -207,7 +207,7 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1, bool xch
   const int piece = rr_piece(ix->raw_u8 ? ix->d : 4 * ix->d);
   p.per_query += (size_t)nprobe * 20 + (size_t)(cap / piece) * 16;      // re-rank pieces
   p.per_query += (size_t)nprobe * ix->rt_maxtiles * 16;                   //   + cuts at tile bounds
-  p.per_query += kCells;                                                 // remap
+  p.per_query += kCells + 4;                                             // remap, nest
   p.per_query += (size_t)(2 * nprobe + 1) * 4 +                          // sweep order (sperm, spad)
                  (size_t)((cap + 32LL * nprobe + kItemMin - 1) / kItemMin) * 12;   //   + items_s, ikey
   if (xchg || world > 1) p.per_query += (size_t)k * 16 + (size_t)world * 8;   // result exchange (XBuf)
@@ -262,6 +262,14 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nqmax, int nprobe,
   b.ikey = (int*)take((size_t)nqb * ((p.cap + 32LL * nprobe + kItemMin - 1) / kItemMin) * 4);
   b.icnt = (int*)take((size_t)(ix->nlist + 1) * 4);
   b.nsamp = (int*)take((size_t)nqb * 4);
+  // with the sweep order (codes streamed from HBM), the 8-bit PQ scan's sample pass fills its
+  // last work item with the following lists (C4 103.4 vs 104.3 ms per step; L2-resident C2,
+  // whose sample pass skips the idle warps of its last item, 5.00 vs 4.96 ms: not there)
+  const bool pq8 = ix->kind == BBC_KIND_PQ && ix->nbits == 8 &&
+                   (ix->scan_order == BBC_ORDER_SWEEP ||
+                    (ix->scan_order == BBC_ORDER_AUTO && (double)ix->n_local * ix->M > 0.5 * (double)ix->l2_bytes));
+  b.nest = pq8 ? (int*)take((size_t)nqb * 4) : b.nsamp;
+  b.nest_item = pq8 ? kRqE : 0;
   b.edges = (float*)take((size_t)nqb * 8);
   b.hist = (int*)take((size_t)nqb * kCells * 4);
   b.tau = (int*)take((size_t)nqb * 4);

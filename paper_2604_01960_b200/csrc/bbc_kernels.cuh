@@ -59,6 +59,9 @@ struct Batch {
   int2* items_s;      // [as items]         items in sweep order
   int* ikey;          // [as items]         first list of each item
   int* icnt;          // [nlist + 1]        items per first list -> offsets
+  int* nest;          // [nq]  lists the PQ sample pass estimates (>= nsamp; == nsamp unless 8-bit
+                      //       PQ: then the same array only when nest_item == 0)
+  int nest_item;      // objects per sample-pass work item (8-bit PQ), 0: nest = nsamp
 };
 
 // Index arrays on the device.
@@ -420,6 +423,7 @@ __global__ void __launch_bounds__(kSelNT) k_probe_select(Batch b, Dev ix) {
     prun += tot_p;
     __syncthreads();
   }
+  __shared__ int s_ns;
   if (threadIdx.x == 0) {
     po[nprobe] = (int)lrun;
     pp[nprobe] = (int)prun;
@@ -430,6 +434,26 @@ __global__ void __launch_bounds__(kSelNT) k_probe_select(Batch b, Dev ix) {
       ns = s + 1 > s0 ? s + 1 : s0;
     }
     b.nsamp[q] = ns;
+    s_ns = ns;
+  }
+  if (b.nest != b.nsamp) {
+    // lists estimated by the 8-bit PQ scan's sample pass (nest >= ns): the sample's last work
+    // item (nest_item objects) is filled up with the whole lists that follow it in probe order,
+    // whose bucket ids k_sample_cells then forms from the stored estimates, so the main pass
+    // starts after them instead of scanning them in a partly filled item of its own.  The edges
+    // come from the first ns lists only (k_select_edges): no result changes.
+    __shared__ int s_more;
+    if (threadIdx.x == 0) s_more = 0;
+    __syncthreads();
+    const int ns = s_ns;
+    if (ns > 0) {
+      const int target = (pp[ns] + b.nest_item - 1) / b.nest_item * b.nest_item;
+      int more = 0;                                  // lists after the sample ending by target
+      for (int j = ns + threadIdx.x; j < nprobe; j += kSelNT) more += pp[j + 1] <= target;
+      if (more) atomicAdd(&s_more, more);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) b.nest[q] = ns + s_more;
   }
 }
 
@@ -666,7 +690,7 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
   __syncthreads();                                   // shared memory of the previous item free
   const int2 wk = items[it];
   const int q = wk.x;
-  const int ns = b.nsamp[q];
+  const int ns = b.nest[q];                          // lists of the sample pass (>= nsamp)
   if (mode != 2 && ns == 0) continue;                // tau = infinity: nothing to bucket
   const int first = mode == 1 ? ns : 0;
   const int lim = mode == 0 ? ns : b.nprobe;
@@ -831,7 +855,7 @@ __global__ void __launch_bounds__(1024) k_scan_plan(Batch b, int mode, int2* ite
     int cnt = 0, q = 0;
     if (r < b.nq) {
       q = b.qperm[r];
-      const int ns = b.nsamp[q];
+      const int ns = b.nest[q];
       if (mode == 2 || ns > 0) {
         const int* pp = b.popad + (size_t)q * (b.nprobe + 1);
         const int first = mode == 1 ? ns : 0, lim = mode == 0 ? ns : b.nprobe;
@@ -883,7 +907,7 @@ __global__ void __launch_bounds__(kSelNT) k_sweep_order(Batch b, Dev ix) {
   __shared__ uint64_t keys[kMaxProbe];
   __shared__ int ws[kSelNT / 32];
   __shared__ int carry;
-  const int q = blockIdx.x, np = b.nprobe, ns = b.nsamp[q];
+  const int q = blockIdx.x, np = b.nprobe, ns = b.nest[q];
   const int* pr = b.probe + (size_t)q * np;
   int P2 = 1;
   while (P2 < np) P2 <<= 1;
@@ -941,7 +965,7 @@ __global__ void __launch_bounds__(256) k_item_count(Batch b, int mode, int item_
   const int nit = *b.nitems;
   for (int it = blockIdx.x * 256 + threadIdx.x; it < nit; it += gridDim.x * 256) {
     const int2 wk = b.items[it];
-    const int q = wk.x, ns = b.nsamp[q];
+    const int q = wk.x, ns = b.nest[q];
     const int first = mode == 1 ? ns : 0, lim = mode == 0 ? ns : b.nprobe;
     const int* pd = b.spad + (size_t)q * (b.nprobe + 1);
     const int x = pd[first] + wk.y * item_objs;
@@ -1020,7 +1044,7 @@ __global__ void k_transpose_codes(const uint8_t* codes, const long long* loff,
 __global__ void __launch_bounds__(256) k_sample_cells(Batch b) {
   __shared__ int hist[kCells];
   const int q = blockIdx.y;
-  const int ns = b.nsamp[q];
+  const int ns = b.nest[q];                          // the sample and its fill-up lists
   if (ns == 0) return;
   const int n = b.poff[(size_t)q * (b.nprobe + 1) + ns];
   if (blockIdx.x * 1024 >= n) return;
