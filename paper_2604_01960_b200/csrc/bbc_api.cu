@@ -1147,7 +1147,8 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
       }
       {
         StageScope sc(s.ix, st, BBC_STAGE_SELECT);
-        k_final_select<<<nb, kSelNT, 0, st>>>(s.b, s.dv, s.oids, s.od2);
+        if (s.b.budget >= 50000) k_final_select<13><<<nb, kSelNT, 0, st>>>(s.b, s.dv, s.oids, s.od2);
+        else k_final_select<11><<<nb, kSelNT, 0, st>>>(s.b, s.dv, s.oids, s.od2);
         g_launches += 1;
       }
       if (pipe) {
