@@ -1664,8 +1664,21 @@ __device__ __forceinline__ Cells32 emit_cells(const Batch& b, int q, int c) {
   return cx;
 }
 
+// the per-chunk values k_emit loads one chunk ahead: candidate offsets of the chunk and of the
+// next one, the probed lists holding their first objects
+struct EmitMeta { int cbeg, cnext, jc, jnext; };
+__device__ __forceinline__ EmitMeta emit_meta(const Batch& b, const int* chunk_off, int nchunk, int q, int c) {
+  const size_t cq = (size_t)q * nchunk + c;
+  EmitMeta m;
+  m.cbeg = chunk_off[cq];
+  m.cnext = c + 1 < nchunk ? chunk_off[cq + 1] : 0;
+  m.jc = b.chunkj[cq];
+  m.jnext = c + 1 < nchunk ? b.chunkj[cq + 1] : 0;
+  return m;
+}
+
 __device__ __forceinline__ void emit_chunk(const Batch& b, const Dev& ix, const int* chunk_off, int nchunk, int q,
-                                           int c, const Cells32& cx, EmitSmem& sm) {
+                                           int c, const Cells32& cx, EmitSmem& sm, const EmitMeta& mt) {
   int* wcnt = sm.wcnt;
   int* s_pre = sm.s_pre;
   unsigned* s_flg = sm.s_flg;
@@ -1677,14 +1690,10 @@ __device__ __forceinline__ void emit_chunk(const Batch& b, const Dev& ix, const 
   const int i0 = c * kChunk + threadIdx.x * kPerThr;
   // Round 1: every load that depends on (q, c) only, issued together (the kernel is bound by
   // dependent-load latency, not bandwidth).  Cell bytes past n are masked by chunk_flags.
-  const size_t cq = (size_t)q * nchunk + c;
   const int n = po[nprobe];
   const int tau = b.tau[q];
   const int ncq = b.ncand[q];
-  const int cbeg = chunk_off[cq];
-  const int cnext = c + 1 < nchunk ? chunk_off[cq + 1] : 0;
-  const int jc = b.chunkj[cq];
-  const int jnext = c + 1 < nchunk ? b.chunkj[cq + 1] : 0;
+  const int cbeg = mt.cbeg, cnext = mt.cnext, jc = mt.jc, jnext = mt.jnext;
   if (c * kChunk >= n) return;
   const int need = (n + kChunk - 1) / kChunk;        // chunks without candidates exit at once
   const int cend = c + 1 < need ? cnext : ncq;
@@ -1774,12 +1783,19 @@ __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chu
   const int q = blockIdx.y;
   const int n = b.poff[(size_t)q * (b.nprobe + 1) + b.nprobe];
   const int need = (n + kChunk - 1) / kChunk;
-  Cells32 nx = emit_cells(b, q, blockIdx.x);          // the next chunk's cells load ahead
+  // the next chunk's cells and offsets load ahead
+  Cells32 nx = emit_cells(b, q, blockIdx.x);
+  EmitMeta nm{0, 0, 0, 0};
+  if ((int)blockIdx.x < need) nm = emit_meta(b, chunk_off, nchunk, q, blockIdx.x);
   for (int c = blockIdx.x; c < need; c += gridDim.x) {
     __syncthreads();                                 // shared memory of the previous chunk free
     const Cells32 cx = nx;
-    if (c + (int)gridDim.x < need) nx = emit_cells(b, q, c + gridDim.x);
-    emit_chunk(b, ix, chunk_off, nchunk, q, c, cx, sm);
+    const EmitMeta mt = nm;
+    if (c + (int)gridDim.x < need) {
+      nx = emit_cells(b, q, c + gridDim.x);
+      nm = emit_meta(b, chunk_off, nchunk, q, c + gridDim.x);
+    }
+    emit_chunk(b, ix, chunk_off, nchunk, q, c, cx, sm, mt);
   }
 }
 
