@@ -445,7 +445,8 @@ def main():
     info = g.info
     code_bytes = info.m if info.kind == 1 else info.dpad // 8 + 8
     row_bytes = info.d * (1 if info.raw_u8 else 4)
-    main_objs = stats["probed"] - stats["sampled"]
+    # (in sweep order the sample pass also estimates the lists filling its last work item)
+    main_objs = stats["probed"] - max(stats["sampled"], stats.get("sample_pass", 0))
     peak, peak_src = peaks()
     scan_ms = stage_ms["scan"] / args.steps
     rr_ms = stage_ms["rerank"] / args.steps

@@ -341,8 +341,9 @@ bbc_status bbc_last_stats2(bbc_index index, int64_t* probed, int64_t* candidates
                            int64_t* microbatches, int64_t* sampled);
 /* Counters of the last search, in order: probed objects, candidates |S*|, sample objects,
  * lists shortlisted by the tensor-core probe (0 in SIMT mode), micro-batches, micro-batches
- * re-ranked in list order.  Copies the first n (<= 6) into out (host memory).  BBC_ERR_ARG for
- * a null index or out with n > 0. */
+ * re-ranked in list order, objects estimated by the PQ sample pass (the sample plus, in sweep
+ * order, the lists that fill its last work item; 0 for RaBitQ).  Copies the first n (<= 7) into
+ * out (host memory).  BBC_ERR_ARG for a null index or out with n > 0. */
 bbc_status bbc_stats_vector(bbc_index index, int64_t* out, int32_t n);
 
 /* Number of CUDA kernels this library has launched in this process. */

@@ -400,7 +400,7 @@ class Index:
         a, b, c, d = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         _check(lib().bbc_last_stats2(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
                                      ctypes.byref(d)))
-        v = (ctypes.c_int64 * 6)()
-        _check(lib().bbc_stats_vector(self._h, v, 6))
+        v = (ctypes.c_int64 * 7)()
+        _check(lib().bbc_stats_vector(self._h, v, 7))
         return dict(probed=a.value, candidates=b.value, microbatches=c.value, sampled=d.value,
-                    shortlisted=v[3], rerank_list_batches=v[5])
+                    shortlisted=v[3], rerank_list_batches=v[5], sample_pass=v[6])

@@ -60,7 +60,7 @@ struct bbc_index_s {
   uint8_t* bits = nullptr;
   float* factors = nullptr;
   void* raw = nullptr;
-  long long* stats = nullptr;           // [4]
+  long long* stats = nullptr;           // [5]
   uint8_t* codes_t = nullptr;           // PQ codes, per-list chunk-major (8-bit: replicated-LUT scan;
                                         // 4-bit: k_pack_codes4 layout)
   long long* tbase = nullptr;           // [nlist] byte offset of each list in codes_t
@@ -1077,7 +1077,7 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
   int mb_index = 0;
   const long long budget_c = std::min<long long>(budget, (long long)1 << 40);
   for (auto& s : sh) {
-    CU(cudaMemsetAsync(s.ix->stats, 0, 4 * sizeof(long long), st));
+    CU(cudaMemsetAsync(s.ix->stats, 0, 5 * sizeof(long long), st));
     s.ix->microbatches = 0;
     s.ix->rr_list_batches = 0;
     if (s.ix->timing) s.ix->timed_calls++;
@@ -1568,7 +1568,7 @@ bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_
     ok = ok && upload_rows(8, 8, (void**)&ix->factors);
   }
   ok = ok && upload_rows(9, rowraw, &ix->raw);
-  ok = ok && dalloc((void**)&ix->stats, 4 * sizeof(long long));
+  ok = ok && dalloc((void**)&ix->stats, 5 * sizeof(long long));
   if (ok) {
     // centroid mean, |c - mu|^2 and max |c - mu| for the tensor-core probe's error bound
     std::vector<float> C((size_t)nlist * d);
@@ -1924,10 +1924,10 @@ bbc_status bbc_last_stats2(bbc_index ix, int64_t* probed, int64_t* candidates, i
 
 bbc_status bbc_stats_vector(bbc_index ix, int64_t* out, int32_t n) {
   if (!ix || (!out && n > 0) || n < 0) return fail(BBC_ERR_ARG, "bad argument");
-  long long h[4];
+  long long h[5];
   CU(cudaMemcpy(h, ix->stats, sizeof(h), cudaMemcpyDeviceToHost));
-  const long long v[6] = {h[0], h[1], h[2], h[3], ix->microbatches, ix->rr_list_batches};
-  for (int i = 0; i < n && i < 6; ++i) out[i] = v[i];
+  const long long v[7] = {h[0], h[1], h[2], h[3], ix->microbatches, ix->rr_list_batches, h[4]};
+  for (int i = 0; i < n && i < 7; ++i) out[i] = v[i];
   return BBC_OK;
 }
 

@@ -36,7 +36,8 @@ struct Batch {
   int* cpos;          // [nq x cap]  candidate rows (list-ordered index of this shard)
   int* cid;           // [nq x cap]  candidate original ids
   float* val;         // [nq x cap]  sample estimates, then exact d^2 of candidates
-  long long* stats;   // [3] sum n_o, sum |S*|, sum sample objects
+  long long* stats;   // [5] sum n_o, sum |S*|, sum sample objects, shortlisted lists, sum
+                      //     objects estimated by the PQ sample pass (k_sample_cells)
   const int* qperm;   // [nq] locality order of the queries (k_qperm): CTA row y -> query qperm[y]
   int2* items;        // [nq x rqg] scan work items (query, pass) of the current pass (k_scan_plan)
   long long* ostage2_ids;  // second output staging buffer (host path, double-buffered copies)
@@ -1047,6 +1048,8 @@ __global__ void __launch_bounds__(256) k_sample_cells(Batch b) {
   const int ns = b.nest[q];                          // the sample and its fill-up lists
   if (ns == 0) return;
   const int n = b.poff[(size_t)q * (b.nprobe + 1) + ns];
+  if (blockIdx.x == 0 && threadIdx.x == 0)          // objects estimated by the sample pass
+    atomicAdd((unsigned long long*)&b.stats[4], (unsigned long long)n);
   if (blockIdx.x * 1024 >= n) return;
   for (int i = threadIdx.x; i < kCells; i += 256) hist[i] = 0;
   CellFn cf;

@@ -187,6 +187,8 @@ def test_parity_scan_orders(name, nprobe):
         for order in (g.ORDER_SWEEP, g.ORDER_PROBE):
             g.set_scan_order(order)
             compare(cfg, ix, q, g, cfg.k, npr, cfg.budget)
+            st = g.last_stats()                      # the sample pass covers the sample (and, in
+            assert st["sample_pass"] >= st["sampled"]   # sweep order, the lists filling its item)
     finally:
         g.set_scan_order(g.ORDER_AUTO)
 
