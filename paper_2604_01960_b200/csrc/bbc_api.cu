@@ -64,6 +64,7 @@ struct bbc_index_s {
   uint8_t* codes_t = nullptr;           // PQ codes, per-list chunk-major (8-bit: replicated-LUT scan;
                                         // 4-bit: k_pack_codes4 layout)
   long long* tbase = nullptr;           // [nlist] byte offset of each list in codes_t
+  long long ct_bytes = 0;               // bytes of codes_t (without the tail pad)
   float* cmu = nullptr;                 // [d] centroid mean (tensor-core probe)
   float* pb_hi = nullptr;               // [nlist_pad x d] centred centroids, tf32 hi part (d <= 128)
   float* pb_lo = nullptr;               //                 and the remainder
@@ -135,6 +136,7 @@ Dev dev_view(const bbc_index_s* ix) {
   v.books = ix->books; v.codes = ix->codes; v.P = ix->P; v.wL = ix->wL; v.bits = ix->bits;
   v.factors = ix->factors; v.raw = ix->raw;
   v.cmu = ix->cmu; v.cnorm = ix->cnorm; v.cmax = ix->cmax; v.probe_tc = 0;
+  v.ct_bytes = ix->ct_bytes;
   return v;
 }
 
@@ -363,7 +365,7 @@ void rq_scan(int M, bool est, int num_sms, cudaStream_t st, const Batch& b, cons
   if (sweep) {
     const int gi = 4 * num_sms;
     cudaMemsetAsync(b.icnt, 0, (size_t)(dv.nlist + 1) * 4, st);
-    k_item_count<<<gi, 256, 0, st>>>(b, mode, kRqE);
+    k_item_count<<<gi, 256, 0, st>>>(b, mode, kRqE, dv.nlist);
     k_item_offsets<<<1, 1024, 0, st>>>(b.icnt, dv.nlist);
     k_item_scatter<<<gi, 256, 0, st>>>(b);
     g_launches += 3;
@@ -1667,6 +1669,7 @@ bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_
       tb[L] = tot;
       tot += (long long)((ix->lsize[L] + 31) / 32) * gbytes;
     }
+    ix->ct_bytes = tot;
     ok = dalloc((void**)&ix->codes_t, (size_t)tot + kCodesTailPad) &&
          dalloc((void**)&ix->tbase, (size_t)nlist * 8) &&
          cudaMemcpy(ix->tbase, tb.data(), (size_t)nlist * 8, cudaMemcpyHostToDevice) == cudaSuccess &&

@@ -3,10 +3,27 @@
 // (d_max) and the final top-k by (exact d^2, id) (Collect l.22-23).
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace bbc {
+
+// BBC_CHECKS=1 (a test build, tests/test_bounds_checks.py): device-side bounds checks on the
+// indices the scan, its ordering kernels, the compaction and the selections compute; a violation
+// traps (the search then fails with a CUDA error).  compute-sanitizer is not available on the
+// GPU pool, so this build plus the parity suite stands in for memcheck on these kernels.
+#ifndef BBC_CHECKS
+#define BBC_CHECKS 0
+#endif
+#define BBC_CHECK(cond)                                                                          \
+  do {                                                                                           \
+    if (BBC_CHECKS && !(cond)) {                                                                 \
+      printf("BBC_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__,      \
+             (int)blockIdx.x, (int)threadIdx.x);                                                 \
+      __trap();                                                                                  \
+    }                                                                                            \
+  } while (0)
 
 constexpr int kCells = 256;          // 255 regular cells + overflow cell 255 (DESIGN R3)
 constexpr int kTauInf = 1 << 30;     // tau = infinity (Alg. 1 l.11)

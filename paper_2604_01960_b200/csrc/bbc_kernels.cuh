@@ -87,6 +87,7 @@ struct Dev {
   const float* cnorm;            // [nlist]
   float cmax;
   int probe_tc;                  // 1: coarse holds d~ (shortlist mode of k_probe_select)
+  long long ct_bytes;            // bytes of the group-major code copy (bounds checks)
 };
 
 // ------------------------------------------------------------------------------------------
@@ -691,6 +692,7 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
   __syncthreads();                                   // shared memory of the previous item free
   const int2 wk = items[it];
   const int q = wk.x;
+  BBC_CHECK(q >= 0 && q < b.nq && wk.y >= 0);
   const int ns = b.nest[q];                          // lists of the sample pass (>= nsamp)
   if (mode != 2 && ns == 0) continue;                // tau = infinity: nothing to bucket
   const int first = mode == 1 ? ns : 0;
@@ -729,12 +731,17 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
         if (s_popad[mid] <= xg) lo = mid; else hi = mid - 1;
       }
       const int j = sp ? sp[lo] : lo;                // probe position of the group's list
+      BBC_CHECK(lo >= first && lo < lim && j >= 0 && j < b.nprobe);
       const int L = pr[j];
+      BBC_CHECK(L >= 0 && L < ix.nlist);
       const int nL = (int)(ix.loff[L + 1] - ix.loff[L]);
       const int i0 = xg - s_popad[lo];
+      BBC_CHECK(i0 >= 0 && i0 < nL && (i0 & 31) == 0);
       cnt = min(32, nL - i0);
       go = (uint32_t)((tbase[L] + (long long)(i0 >> 5) * M * 32) >> 7);
+      BBC_CHECK(((long long)go << 7) + (long long)M * 32 <= ix.ct_bytes);
       oo = obase + po[j] + i0;
+      BBC_CHECK(po[j] + i0 + cnt <= (EST ? est_stride : b.cap));
     }
     gofs[G] = go;
     gout[G] = oo;
@@ -926,6 +933,7 @@ __global__ void __launch_bounds__(kSelNT) k_sweep_order(Batch b, Dev ix) {
     int sz = 0, j = 0;
     if (t < np) {
       j = (int)(keys[t] & 0xffffffu);
+      BBC_CHECK(j < np && (t < ns) == (j < ns));
       const int L = pr[j];
       sz = ((int)(ix.loff[L + 1] - ix.loff[L]) + 31) & ~31;
       sp[t] = j;
@@ -962,7 +970,7 @@ __global__ void __launch_bounds__(kSelNT) k_sweep_order(Batch b, Dev ix) {
 // position in spad) and the per-list counts; k_item_offsets: exclusive scan of the counts (one
 // CTA); k_item_scatter: items to their list's slots (order inside a list unspecified -- it changes
 // no result: items write disjoint outputs and add integer counts).
-__global__ void __launch_bounds__(256) k_item_count(Batch b, int mode, int item_objs) {
+__global__ void __launch_bounds__(256) k_item_count(Batch b, int mode, int item_objs, int ix_nlist) {
   const int nit = *b.nitems;
   for (int it = blockIdx.x * 256 + threadIdx.x; it < nit; it += gridDim.x * 256) {
     const int2 wk = b.items[it];
@@ -976,6 +984,7 @@ __global__ void __launch_bounds__(256) k_item_count(Batch b, int mode, int item_
       if (pd[mid] <= x) lo = mid; else hi = mid - 1;
     }
     const int L = b.probe[(size_t)q * b.nprobe + b.sperm[(size_t)q * b.nprobe + lo]];
+    BBC_CHECK(lo >= first && lo < lim && L >= 0 && L < ix_nlist);
     b.ikey[it] = L;
     atomicAdd(&b.icnt[L], 1);
   }
@@ -1018,8 +1027,11 @@ __global__ void __launch_bounds__(1024) k_item_offsets(int* cnt, int n) {
 
 __global__ void __launch_bounds__(256) k_item_scatter(Batch b) {
   const int nit = *b.nitems;
-  for (int it = blockIdx.x * 256 + threadIdx.x; it < nit; it += gridDim.x * 256)
-    b.items_s[atomicAdd(&b.icnt[b.ikey[it]], 1)] = b.items[it];
+  for (int it = blockIdx.x * 256 + threadIdx.x; it < nit; it += gridDim.x * 256) {
+    const int at = atomicAdd(&b.icnt[b.ikey[it]], 1);
+    BBC_CHECK(at >= 0 && at < nit);
+    b.items_s[at] = b.items[it];
+  }
 }
 
 // Index-load-time copy of the PQ codes in the group-major order of k_pq_scan_rq.
@@ -1048,6 +1060,7 @@ __global__ void __launch_bounds__(256) k_sample_cells(Batch b) {
   const int ns = b.nest[q];                          // the sample and its fill-up lists
   if (ns == 0) return;
   const int n = b.poff[(size_t)q * (b.nprobe + 1) + ns];
+  BBC_CHECK(n <= b.cap);
   if (blockIdx.x == 0 && threadIdx.x == 0)          // objects estimated by the sample pass
     atomicAdd((unsigned long long*)&b.stats[4], (unsigned long long)n);
   if (blockIdx.x * 1024 >= n) return;
@@ -1749,6 +1762,7 @@ __device__ __forceinline__ void emit_chunk(const Batch& b, const Dev& ix, const 
         jend = sp[j + 1];
         rbase = win ? s_rb[j] : rb[jc + j];
       }
+      BBC_CHECK(cbeg + pos < b.cap && rbase + i >= 0 && rbase + i < ix.n_local);
       outp[pos++] = (int)(rbase + i);
     }
   }
@@ -2056,6 +2070,7 @@ __global__ void __launch_bounds__(kSelNT) k_final_select(Batch b, Dev ix, long l
   __shared__ int wcnt[kSelNT / 32 + 1];
   const int q = blockIdx.x;
   const int nc = b.ncand[q];
+  BBC_CHECK(nc >= 0 && nc <= b.cap);
   const int k = b.k;
   const int* cp = b.cid + (size_t)q * b.cap;
   const float* vv = b.val + (size_t)q * b.cap;
