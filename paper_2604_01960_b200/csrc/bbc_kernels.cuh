@@ -1871,6 +1871,7 @@ __device__ __forceinline__ void rr_rows32(const Dev& ix, const RrQuery<U8, LPC, 
   const int sub = lane / LPC, sl = lane % LPC;
   const uint8_t* raw = static_cast<const uint8_t*>(ix.raw);
   const int myrow = lane < n32 ? cp[lane] : 0;
+  BBC_CHECK(n32 <= 32 && myrow >= 0 && myrow < ix.n_local);
   for (int k0 = 0; k0 < n32; k0 += CPW * STEPS) {
     uint4 x[STEPS][MAXV];
     int kk[STEPS];
@@ -2041,6 +2042,7 @@ __global__ void __launch_bounds__(kRrNT, MINB) k_rerank_seg(Batch b, Dev ix, con
       const int q = __shfl_sync(0xffffffffu, mine.x, i);
       if (q < 0) break;
       const int t0 = __shfl_sync(0xffffffffu, mine.y, i), len = __shfl_sync(0xffffffffu, mine.z, i);
+      BBC_CHECK(q < b.nq && t0 >= 0 && len > 0 && t0 + len <= b.ncand[q]);
       if (q != qcur) {
         Q.load(b.Q + (size_t)q * d, sl, per, nv);
         qcur = q;
