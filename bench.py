@@ -71,6 +71,9 @@ def parse():
     p.add_argument("--cpu-workers", type=int, default=0,
                    help="processes of the oracle baseline (0: every host core)")
     p.add_argument("--buckets", type=int, default=255, help="B regular buckets (Eq. 6)")
+    p.add_argument("--bound-rerank", type=float, default=None, metavar="EPS0",
+                   help="RaBitQ: Algorithm 3's bound-aware re-rank with this eps0 (1.9 in the paper) "
+                        "instead of Algorithm 1's superset (f1; measurement, not the headline)")
     p.add_argument("--bucket-sweep", action="store_true",
                    help="QPS, |S*|/budget and recall over B (Table 4 analog) at the operating point")
     return p.parse_args()
@@ -343,6 +346,8 @@ def main():
     else:
         g = Index(path, device=local)
     g.set_buckets(args.buckets)
+    if args.bound_rerank is not None:
+        g.set_bound_rerank(True, args.bound_rerank)
     if args.sweep:
         global args_sweep_nprobe, args_sweep_budget
         if args.sweep_nprobe:
@@ -557,6 +562,8 @@ def main():
                    "budget": budget,
                    "parallelism": (f"list-sharded x{world} (NCCL)" if lists else f"query-sharded x{world}"),
                    "l2": "flushed (256 MB write) between timed steps",
+                   **({} if args.bound_rerank is None else
+                      {"rerank": f"Algorithm 3 (bound-aware, eps0 = {args.bound_rerank})"}),
                    "probed_per_query": stats["probed"] / nq,
                    "candidates_per_query": stats["candidates"] / nq,
                    "microbatches": stats["microbatches"],

@@ -107,6 +107,14 @@ SMALL = {
     # global-search path of k_emit; probe sets of 600 lists
     "C2f": C2.replace(name="C2f", N=40_000, nlist=2_048, nq=8, k=500, nprobe=600, budget=1_000,
                       kmeans_iters=4),
+    # Algorithm 3 (f1) on RaBitQ indexes of integer-valued data (C2's generator as fp32, C5's as
+    # uint8): exact d^2 are integers < 2^24, identical in fp32 and fp64, so the exact distances'
+    # bucket ids that steer Algorithm 3's loop agree on both sides and its re-ranked set is compared
+    # exactly.  40 queries over 12 of 64 lists: tensor-core query tiles per list > 1.
+    "C3a3": C3.replace(name="C3a3", gen="C2", d=128, N=30_000, nlist=64, nq=40, k=300, nprobe=12,
+                       budget=900, kmeans_iters=6),
+    "C3a3u8": C3.replace(name="C3a3u8", gen="C5", raw_dtype="u8", d=128, N=30_000, nlist=64, nq=16,
+                         k=300, nprobe=12, budget=900, kmeans_iters=6),
 }
 
 # Inner-product / cosine variants ("our result buffer

@@ -144,6 +144,24 @@ bbc_status bbc_set_buckets(bbc_index index, int32_t nbuckets);
  */
 bbc_status bbc_set_remap(bbc_index index, int32_t m);
 
+/*
+ * bbc_set_bound_rerank -- Algorithm 3, the bound-aware re-rank of IVF+RaBitQ (
+ * SURVEY 8(f) f1; reading R21), in place of steps a4..a7 of a RaBitQ search.  on = 1:
+ * every probed object's estimate gets the RaBitQ bound lb/ub = est -/+ ((2 r_o) r)(t_o eps),
+ * t_o = sqrt(1 - g_o^2)/g_o, eps = eps0/sqrt(D - 1) (eps0 = 1.9 in the paper,
+ * P:L1440), both bucketed with the sample's codebook (Eq. 6); tau = the first bucket where the
+ * upper-bound counts reach k; objects with a_lb <= tau are the candidates; the marginal-bucket
+ * loop of l.12-21 re-ranks B_l[i] and B_u[j] until i >= j, then B_u[j]'s leftovers (l.22); the
+ * result is the k smallest (exact d^2, id) of the re-ranked objects.  bbc_search_debug reports
+ * the upper-bound histogram in `hist`, tau, the candidates (a_lb <= tau) in cand_ids with exact
+ * d^2 for the re-ranked ones and +inf for the others.  `budget` still sizes the sample (R5).
+ * on = 0 (default): Algorithm 1's superset.  The workspace grows by 8 bytes per probed-object
+ * slot per query (query the size after the change).  BBC_ERR_ARG for a PQ index, a sharded
+ * handle, an active remap, on outside {0, 1} or eps0 outside (0, 1e6); the sharded path
+ * (bbc_search_group, world > 1) returns BBC_ERR_ARG while it is on.
+ */
+bbc_status bbc_set_bound_rerank(bbc_index index, int32_t on, float eps0);
+
 #define BBC_SCAN_SIMT 0
 #define BBC_SCAN_TENSOR 1
 bbc_status bbc_set_scan_mode(bbc_index index, int32_t mode);
@@ -230,6 +248,7 @@ bbc_status bbc_query_capacity(bbc_index index, int32_t nprobe, int64_t* cap);
  *            every probed object is re-ranked (tau = infinity, Alg. 1 l.11)
  *   out_ids  device i64 [nq x k]; out_d2 device f32 [nq x k].  Row i holds the k probed
  *            candidates with the smallest (exact d^2, id), in candidate (probe) order, not sorted.
+ *            (Under bbc_set_bound_rerank the candidate order, and so this order, is unspecified.)
  *            When fewer than k objects are probed the row is padded with (id -1, d^2 +inf).
  *   workspace/workspace_bytes: device scratch of at least the `min_bytes` of bbc_workspace_size.
  *   stream   cudaStream_t (void*), NULL = default stream.

@@ -26,7 +26,7 @@ EXPORTS = ("ivf_load", "ivf_free", "bbc_index_info", "bbc_workspace_size", "bbc_
            "bbc_comm_init", "bbc_search_group", "bbc_last_stats2", "bbc_set_probe_mode",
            "bbc_set_scan_mode", "bbc_stats_vector", "bbc_set_buckets", "bbc_set_rerank_order",
            "bbc_measure_l2_read", "bbc_set_remap", "bbc_set_code_loads",
-           "bbc_measure_smem_lookups", "bbc_set_scan_order")
+           "bbc_measure_smem_lookups", "bbc_set_scan_order", "bbc_set_bound_rerank")
 
 STAGES = ("probe", "tables", "sample", "scan", "compact", "rerank", "select", "comm")
 TAU_INF = 1 << 30
@@ -90,6 +90,7 @@ def lib() -> ctypes.CDLL:
         L.bbc_set_remap.argtypes = [vp, i32]
         L.bbc_set_code_loads.argtypes = [vp, i32]
         L.bbc_set_scan_order.argtypes = [vp, i32]
+        L.bbc_set_bound_rerank.argtypes = [vp, i32, ctypes.c_float]
         L.bbc_measure_smem_lookups.argtypes = [i32, i32, ctypes.POINTER(ctypes.c_double)]
         L.bbc_measure_l2_read.argtypes = [i32, ctypes.c_size_t, i32, ctypes.POINTER(ctypes.c_double)]
         L.bbc_stats_vector.argtypes = [vp, ctypes.POINTER(i64), i32]
@@ -109,7 +110,7 @@ def lib() -> ctypes.CDLL:
                    "bbc_comm_init", "bbc_search_group", "bbc_last_stats2", "bbc_set_probe_mode",
                    "bbc_set_scan_mode", "bbc_stats_vector", "bbc_set_buckets",
                    "bbc_set_rerank_order", "bbc_measure_l2_read", "bbc_set_remap",
-                   "bbc_set_code_loads", "bbc_measure_smem_lookups", "bbc_set_scan_order"):
+                   "bbc_set_code_loads", "bbc_measure_smem_lookups", "bbc_set_scan_order", "bbc_set_bound_rerank"):
             getattr(L, fn).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -361,6 +362,12 @@ class Index:
         """m equal-depth buckets from the sample (the paper's n_ew -> m remap, reading R6); 0
         (default) keeps the equal-width cells as the buckets."""
         _check(lib().bbc_set_remap(self._h, int(m)))
+
+    def set_bound_rerank(self, on: bool, eps0: float = 1.9) -> None:
+        """Algorithm 3 (the bound-aware RaBitQ re-rank) in place of Algorithm 1's
+        superset re-rank: lb/ub buckets from the RaBitQ bound with eps0 (1.9 in the paper), the
+        marginal-bucket loop, exact d^2 of B_exact.  RaBitQ indexes, single shard."""
+        _check(lib().bbc_set_bound_rerank(self._h, int(bool(on)), float(eps0)))
 
     CODES_AUTO, CODES_CACHED, CODES_STREAM = 0, 1, 2
 

@@ -1,0 +1,261 @@
+// f1: Algorithm 3, the bound-aware re-rank of IVF+RaBitQ, on the GPU.
+//
+// Replaces steps a4..a7 of the RaBitQ path when bbc_set_bound_rerank is on.  The codebook is the
+// sample's (d_min, d_max) of Algorithm 1 (the same edges the other path uses), and every
+// probed object's estimate comes from the RaBitQ scan in EST mode (all probed lists).  Then one
+// CTA per query runs, reading R21's one-shot form:
+//   A  lb/ub = est -/+ ((2 r_o) r)(t_o eps), t_o = sqrt(1 - g_o^2)(1/g_o), eps = eps0/sqrt(D - 1)
+//      (the RaBitQ bound, eps0 P:L1440), fp32 with explicit roundings in that order;
+//      their bucket ids a_lb, a_ub (Eq. 6, the canonical CellFn); histograms of both.
+//   B  tau = Update(B_u, k): the first bucket whose cumulative a_ub count reaches k;
+//      candidates {a_lb <= tau} (B_l plus B_u, l.7-11) gathered grouped by a_lb, and the B_u
+//      members (a_ub <= tau) indexed grouped by a_ub.
+//   C  l.12-21: i = first non-empty B_l bucket, j = tau; while i < j: exact d^2 of B_l[i] and
+//      B_u[j] (an object once), He[cell(exact)]++, j = first bucket where B_u + He reach k,
+//      i = next non-empty B_l bucket; then the leftovers of B_u[j] (l.22).
+// Re-ranked candidates keep their exact d^2 in val, the others +inf, so k_final_select returns
+// the k smallest (exact d^2, id) of B_exact (l.22-23).  With tau = infinity (fewer than k upper
+// bounds below d_max) every object with a_lb <= 254 is re-ranked.
+#pragma once
+#include "bbc_kernels.cuh"
+
+namespace bbc {
+
+constexpr int kA3NT = 512;
+
+struct Alg3Smem {
+  int hl[kCells];        // objects not yet re-ranked, by a_lb
+  int hu[kCells];        // objects not yet re-ranked, by a_ub
+  int he[kCells];        // re-ranked objects, by the bucket of their exact d^2
+  int lst[kCells + 1];   // candidate slots grouped by a_lb: bucket c = [lst[c], lst[c+1])
+  int ust[kCells + 1];   // B_u index grouped by a_ub
+  int lcur[kCells], ucur[kCells];
+  int i, j, tau;
+};
+
+// every probed list (warp-strided): f(p, row, rq2) for each probe-order position p of the list
+template <typename F>
+__device__ __forceinline__ void a3_for_probed(const Batch& b, int q, F f) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int* po = b.poff + (size_t)q * (b.nprobe + 1);
+  for (int j = w; j < b.nprobe; j += kA3NT / 32) {
+    const int p0 = po[j], p1 = po[j + 1];
+    const long long rb = b.rbase[(size_t)q * b.nprobe + j];
+    const float rq2 = b.rq2[(size_t)q * b.nprobe + j];
+    for (int p = p0 + lane; p < p1; p += 32) f(p, rb + p, rq2);
+  }
+}
+
+// exact ||q - x||^2 of one row by one warp (all lanes return it); 16-byte (fp32) or 4-byte (u8)
+// loads when d is a multiple of 4, so a 960-d row is 7.5 loads per lane
+template <bool U8>
+__device__ __forceinline__ float a3_exact(const Dev& ix, const float* sq, long long row, int lane) {
+  float acc = 0.f;
+  const int d = ix.d;
+  if (U8) {
+    const uint8_t* r = static_cast<const uint8_t*>(ix.raw) + (size_t)row * d;
+    if ((d & 3) == 0) {
+      for (int t = lane; t < (d >> 2); t += 32) {
+        const uint32_t w4 = __ldg(reinterpret_cast<const uint32_t*>(r) + t);
+        const float4 qv = reinterpret_cast<const float4*>(sq)[t];
+        const float d0 = (float)(w4 & 255u) - qv.x, d1 = (float)((w4 >> 8) & 255u) - qv.y;
+        const float d2 = (float)((w4 >> 16) & 255u) - qv.z, d3 = (float)(w4 >> 24) - qv.w;
+        acc = fmaf(d0, d0, acc); acc = fmaf(d1, d1, acc); acc = fmaf(d2, d2, acc); acc = fmaf(d3, d3, acc);
+      }
+    } else {
+      for (int t = lane; t < d; t += 32) {
+        const float df = (float)__ldg(r + t) - sq[t];
+        acc = fmaf(df, df, acc);
+      }
+    }
+  } else {
+    const float* r = static_cast<const float*>(ix.raw) + (size_t)row * d;
+    if ((d & 3) == 0) {
+#pragma unroll 4
+      for (int t = lane; t < (d >> 2); t += 32) {
+        const float4 x = __ldg(reinterpret_cast<const float4*>(r) + t);
+        const float4 qv = reinterpret_cast<const float4*>(sq)[t];
+        const float d0 = x.x - qv.x, d1 = x.y - qv.y, d2 = x.z - qv.z, d3 = x.w - qv.w;
+        acc = fmaf(d0, d0, acc); acc = fmaf(d1, d1, acc); acc = fmaf(d2, d2, acc); acc = fmaf(d3, d3, acc);
+      }
+    } else {
+      for (int t = lane; t < d; t += 32) {
+        const float df = __ldg(r + t) - sq[t];
+        acc = fmaf(df, df, acc);
+      }
+    }
+  }
+  return warp_sum(acc);
+}
+
+// warp 0: first c in [0, 255) whose cumulative count (hu[c] for c <= tau, + he[c]) reaches k
+__device__ __forceinline__ int a3_threshold(const Alg3Smem& sm, int tau, long long k) {
+  const int lane = threadIdx.x & 31;
+  long long v[8], s = 0;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int c = lane * 8 + e;
+    v[e] = c < 255 ? (long long)(c <= tau ? sm.hu[c] : 0) + sm.he[c] : 0;
+    s += v[e];
+  }
+  long long incl = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  long long c = incl - s;
+  int found = kTauInf;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    c += v[e];
+    if (c >= k && found == kTauInf) found = lane * 8 + e;
+  }
+  return warp_min(found);
+}
+
+// warp 0: first non-empty B_l bucket in [0, tau], kTauInf if none
+__device__ __forceinline__ int a3_first_nonempty(const Alg3Smem& sm, int tau) {
+  const int lane = threadIdx.x & 31;
+  int found = kTauInf;
+  for (int c = lane; c <= tau; c += 32)
+    if (sm.hl[c] > 0) { found = c; break; }
+  return warp_min(found);
+}
+
+template <bool U8>
+__global__ void __launch_bounds__(kA3NT) k_alg3(Batch b, Dev ix, float eps0) {
+  extern __shared__ __align__(16) float sq[];          // the query, [d]
+  __shared__ Alg3Smem sm;
+  const int q = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  constexpr int NW = kA3NT / 32;
+  for (int t = tid; t < ix.d; t += kA3NT) sq[t] = b.Q[(size_t)q * ix.d + t];
+  for (int c = tid; c < kCells; c += kA3NT) { sm.hl[c] = 0; sm.hu[c] = 0; sm.he[c] = 0; }
+  CellFn cf;
+  if (b.nsamp[q] > 0) cf.init(b.edges[2 * q], b.edges[2 * q + 1], b.nbuckets);
+  else cf.init(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), b.nbuckets);   // no sample: all 0
+  const float eps = __fdiv_rn(eps0, __fsqrt_rn((float)(ix.D - 1)));
+  float* val = b.val + (size_t)q * b.cap;
+  uint16_t* lp = b.a3lb + (size_t)q * b.cap;
+  __syncthreads();
+
+  // A: bounds and their bucket ids (est is read from val before anything overwrites it)
+  a3_for_probed(b, q, [&](int p, long long row, float rq2) {
+    const float est = val[p];
+    const float ro = __ldg(ix.factors + 2 * row), g = __ldg(ix.factors + 2 * row + 1);
+    const float r = __fsqrt_rn(rq2);
+    const float t = __fmul_rn(__fsqrt_rn(__fsub_rn(1.f, __fmul_rn(g, g))), __fdiv_rn(1.f, g));
+    const float delta = __fmul_rn(__fmul_rn(__fmul_rn(2.f, ro), r), __fmul_rn(t, eps));
+    const int al = cf(__fsub_rn(est, delta)), au = cf(__fadd_rn(est, delta));
+    lp[p] = (uint16_t)(al | (au << 8));
+    if (al < 255) atomicAdd(&sm.hl[al], 1);
+    if (au < 255) atomicAdd(&sm.hu[au], 1);
+  });
+  __syncthreads();
+  if (w == 0) {
+    const int tau = a3_threshold(sm, 254, b.k);
+    if (lane == 0) sm.tau = tau;
+  }
+  __syncthreads();
+  const int tau = sm.tau;
+  const int tc = tau == kTauInf ? 254 : tau;             // candidates: a_lb <= tc
+  for (int c = tid; c < kCells; c += kA3NT) b.hist[(size_t)q * kCells + c] = c < 255 ? sm.hu[c] : 0;
+  if (tid == 0) {
+    int s = 0, u = 0;
+    for (int c = 0; c <= tc; ++c) {
+      sm.lst[c] = s; sm.lcur[c] = s; s += sm.hl[c];
+      sm.ust[c] = u; sm.ucur[c] = u; u += (tau != kTauInf) ? sm.hu[c] : 0;
+    }
+    sm.lst[tc + 1] = s;
+    sm.ust[tc + 1] = u;
+  }
+  __syncthreads();
+  const int nc = sm.lst[tc + 1];
+
+  // B: gather the candidates grouped by a_lb; index B_u grouped by a_ub
+  int* cpos = b.cpos + (size_t)q * b.cap;
+  int* cid = b.cid + (size_t)q * b.cap;
+  uint16_t* lc = b.a3lc + (size_t)q * b.cap;
+  int* ordu = b.a3ordu + (size_t)q * b.cap;
+  a3_for_probed(b, q, [&](int p, long long row, float) {
+    const int v = lp[p], al = v & 255, au = v >> 8;
+    if (al <= tc) {
+      const int c = atomicAdd(&sm.lcur[al], 1);
+      BBC_CHECK(c < nc && nc <= b.cap);
+      cpos[c] = (int)row;
+      cid[c] = (int)__ldg(ix.ids + row);
+      lc[c] = (uint16_t)v;
+      if (tau != kTauInf && au <= tau) ordu[atomicAdd(&sm.ucur[au], 1)] = c;
+    }
+  });
+  __syncthreads();
+  const float kNaN = __int_as_float(0x7fc00000);
+  for (int c = tid; c < nc; c += kA3NT) val[c] = kNaN;   // NaN: not re-ranked yet
+  __syncthreads();
+
+  // one warp re-ranks candidate c (if not done): exact d^2, counts moved from B_l/B_u to He
+  auto rerank = [&](int c, bool count) {
+    if (!isnan(val[c])) return;                          // warp-uniform
+    const float d2 = a3_exact<U8>(ix, sq, cpos[c], lane);
+    if (lane == 0) {
+      val[c] = d2;
+      if (count) {
+        const int v = lc[c], al = v & 255, au = v >> 8;
+        atomicSub(&sm.hl[al], 1);
+        if (au <= tau) atomicSub(&sm.hu[au], 1);
+        const int ce = cf(d2);
+        if (ce < 255) atomicAdd(&sm.he[ce], 1);
+      }
+    }
+  };
+  if (tau == kTauInf) {
+    for (int c = w; c < nc; c += NW) rerank(c, false);
+  } else {
+    if (w == 0) {
+      const int i0 = a3_first_nonempty(sm, tau);
+      if (lane == 0) { sm.i = i0; sm.j = tau; }
+    }
+    __syncthreads();
+    int i = sm.i, j = sm.j;
+    while (i < j) {
+      for (int x = sm.lst[i] + w; x < sm.lst[i + 1]; x += NW) rerank(x, true);
+      __syncthreads();
+      if (j <= tau)
+        for (int x = sm.ust[j] + w; x < sm.ust[j + 1]; x += NW) rerank(ordu[x], true);
+      __syncthreads();
+      if (w == 0) {
+        const int j2 = a3_threshold(sm, tau, b.k);
+        const int i2 = a3_first_nonempty(sm, tau);
+        if (lane == 0) { sm.i = i2; sm.j = j2; }
+      }
+      __syncthreads();
+      i = sm.i;
+      j = sm.j;
+    }
+    if (j <= tau)                                        // l.22: the threshold bucket's leftovers
+      for (int x = sm.ust[j] + w; x < sm.ust[j + 1]; x += NW) rerank(ordu[x], false);
+  }
+  __syncthreads();
+  int mine = 0;
+  for (int c = tid; c < nc; c += kA3NT) {
+    if (isnan(val[c])) val[c] = __int_as_float(0x7f800000);   // not in B_exact: +inf
+    else ++mine;
+  }
+  mine = warp_sum(mine);
+  if (lane == 0) atomicAdd(&sm.he[255], mine);           // rows re-ranked (he[255] is unused above)
+  __syncthreads();
+  if (tid == 0) {
+    b.ncand[q] = nc;
+    b.tau[q] = tau;
+    const int n_o = b.poff[(size_t)q * (b.nprobe + 1) + b.nprobe];
+    atomicAdd((unsigned long long*)&b.stats[0], (unsigned long long)n_o);
+    atomicAdd((unsigned long long*)&b.stats[1], (unsigned long long)sm.he[255]);
+  }
+}
+
+__global__ void k_fill_int(int* p, int n, int v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+}  // namespace bbc

@@ -18,6 +18,7 @@
 #include "bbc_rbq_tc.cuh"
 #include "bbc_pq4.cuh"
 #include "bbc_rerank_tile.cuh"
+#include "bbc_alg3.cuh"
 
 using namespace bbc;
 
@@ -79,6 +80,8 @@ struct bbc_index_s {
   int rbq_tc = 0;                       // 1: RaBitQ estimates on the tensor cores (bbc_rbq_tc.cuh)
   int rerank_order = BBC_RERANK_AUTO;    // BBC_RERANK_*: work order of the exact re-rank (a7)
   int remap_m = 0;                       // 0 or m equal-depth buckets (bbc_set_remap)
+  int alg3 = 0;                          // 1: Algorithm 3 bound-aware re-rank (bbc_set_bound_rerank)
+  float alg3_eps0 = 1.9f;                // its bound's eps0
   int code_loads = BBC_CODES_AUTO;       // BBC_CODES_*: L1 policy of the PQ scan's code loads
   int scan_order = BBC_ORDER_AUTO;        // BBC_SCAN_*: visiting order of the 8-bit PQ scan
   int2* rt_units = nullptr;             // [rt_nunits] (list, tile) of the shared-memory re-rank
@@ -213,6 +216,7 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1, bool xch
   p.per_query += (size_t)(2 * nprobe + 1) * 4 +                          // sweep order (sperm, spad)
                  (size_t)((cap + 32LL * nprobe + kItemMin - 1) / kItemMin) * 12;   //   + items_s, ikey
   if (xchg || world > 1) p.per_query += (size_t)k * 16 + (size_t)world * 8;   // result exchange (XBuf)
+  if (ix->alg3) p.per_query += (size_t)cap * 8 + 4 + 3 * 256;           // Algorithm 3 (a3lb, a3lc, a3ordu)
   p.fixed = 64 * 256 + (size_t)3 * (std::max(ix->nlist, ix->rt_nunits) + 1) * 4 + 3 * 256 +
             (size_t)(ix->nlist + 1) * 4 + 512;                          // icnt, ictr
   if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) {            // pair codes + inverted index
@@ -292,6 +296,15 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nqmax, int nprobe,
   b.rs_off = (int*)take(nrs * 4);
   b.rs_cur = (int*)take(nrs * 4);
 
+  if (ix->alg3) {
+    b.a3lb = (uint16_t*)take((size_t)nqb * p.cap * 2);
+    b.a3lc = (uint16_t*)take((size_t)nqb * p.cap * 2);
+    b.a3ordu = (int*)take((size_t)nqb * p.cap * 4);
+    b.a3nall = (int*)take((size_t)nqb * 4);
+  } else {
+    b.a3lb = b.a3lc = nullptr;
+    b.a3ordu = b.a3nall = nullptr;
+  }
   db->prefix = (unsigned long long*)take((size_t)nqb * 8);
   db->need = (long long*)take((size_t)nqb * 8);
   db->dh = (int*)take((size_t)nqb * kCells * 4);
@@ -780,6 +793,40 @@ void stage_compact(Shard& s, cudaStream_t st) {
     X(false, 32, 8, 1, 3);                                      \
   }
 
+// f1: Algorithm 3 in place of steps a4..a7 (bbc_alg3.cuh): estimates of every probed object
+// (the RaBitQ scan in EST mode over all probed lists), then one CTA per query for the bounds,
+// the two buffers and the marginal-bucket loop.  Candidates leave with exact d^2 (B_exact) or
+// +inf, ready for k_final_select.
+void stage_alg3(Shard& s, cudaStream_t st) {
+  const bbc_index_s* ix = s.ix;
+  Batch b2 = s.b;
+  b2.nsamp = s.b.a3nall;
+  {
+    StageScope sc(s.ix, st, BBC_STAGE_SCAN);
+    k_fill_int<<<(s.b.nq + 255) / 256, 256, 0, st>>>(b2.nsamp, s.b.nq, s.b.nprobe);
+    g_launches += 1;
+    if (ix->rbq_tc) {
+      rbq_pairs(s, b2, st);
+      rbq_tc_pass(s, b2, st, true);
+    } else {
+      const size_t sm = (size_t)ix->D * 4 + 4 * (ix->D / 32) * 4;
+      set_smem(k_rbq_scan<true>, sm);
+      k_rbq_scan<true><<<dim3(std::min(s.b.nprobe, 64), s.b.nq), kScanNT, sm, st>>>(b2, s.dv, 1);
+      g_launches += 1;
+    }
+  }
+  StageScope sc(s.ix, st, BBC_STAGE_RERANK);
+  const size_t sm = (size_t)ix->d * 4;
+  if (ix->raw_u8) {
+    set_smem(k_alg3<true>, sm);
+    k_alg3<true><<<s.b.nq, kA3NT, sm, st>>>(s.b, s.dv, ix->alg3_eps0);
+  } else {
+    set_smem(k_alg3<false>, sm);
+    k_alg3<false><<<s.b.nq, kA3NT, sm, st>>>(s.b, s.dv, ix->alg3_eps0);
+  }
+  g_launches += 1;
+}
+
 template <bool IP>
 void launch_rerank(Shard& s, dim3 g, cudaStream_t st, int rowb) {
   const bool u8 = s.ix->raw_u8 != 0;
@@ -1029,6 +1076,9 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
     bbc_status st0 = check_args(s.ix, queries, nq, k, nprobe, budget, out_ids, out_d2, s.ws);
     if (st0 != BBC_OK) return st0;
   }
+  if (comm != nullptr)
+    for (auto& s : sh)
+      if (s.ix->alg3) return fail(BBC_ERR_ARG, "Algorithm 3 (bbc_set_bound_rerank) is single-shard only");
   if (nq == 0) return BBC_OK;
   bbc_index_s* ix = sh[0].ix;                       // for CU() error marking
   CU(cudaSetDevice(ix->device));
@@ -1139,9 +1189,13 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
         k_select_edges<<<nb, kSelNT, kFsSmem, st>>>(s.b, s.dv);
         g_launches += 1;
       }
-      stage_scan(s, st, true);
-      stage_compact(s, st);
-      stage_rerank(s, st);
+      if (s.ix->alg3) {
+        stage_alg3(s, st);
+      } else {
+        stage_scan(s, st, true);
+        stage_compact(s, st);
+        stage_rerank(s, st);
+      }
       const int bi = mb_index & 1;
       if (pipe) {
         if (bi == 1) { s.oids = s.b.ostage2_ids; s.od2 = s.b.ostage2_d2; }
@@ -1743,10 +1797,23 @@ bbc_status bbc_set_scan_mode(bbc_index ix, int32_t mode) {
   return BBC_OK;
 }
 
+bbc_status bbc_set_bound_rerank(bbc_index ix, int32_t on, float eps0) {
+  if (!ix) return fail(BBC_ERR_ARG, "null index");
+  if (on != 0 && on != 1) return fail(BBC_ERR_ARG, "on must be 0 or 1");
+  if (on && ix->kind != BBC_KIND_RABITQ) return fail(BBC_ERR_ARG, "Algorithm 3 needs a RaBitQ index");
+  if (on && ix->world > 1) return fail(BBC_ERR_ARG, "Algorithm 3 is single-shard only");
+  if (on && ix->remap_m > 0) return fail(BBC_ERR_ARG, "Algorithm 3 uses the equal-width buckets (remap off)");
+  if (on && !(eps0 > 0.f && eps0 < 1e6f)) return fail(BBC_ERR_ARG, "eps0 must be in (0, 1e6)");
+  ix->alg3 = on;
+  if (on) ix->alg3_eps0 = eps0;
+  return BBC_OK;
+}
+
 bbc_status bbc_set_remap(bbc_index ix, int32_t m) {
   if (!ix) return fail(BBC_ERR_ARG, "null index");
   if (m < 0 || m > 255) return fail(BBC_ERR_ARG, "m must be 0 (off) or in [1, 255]");
   if (m > 0 && ix->world > 1) return fail(BBC_ERR_ARG, "the equal-depth remap is single-shard only");
+  if (m > 0 && ix->alg3) return fail(BBC_ERR_ARG, "the equal-depth remap is off under Algorithm 3");
   ix->remap_m = m;
   return BBC_OK;
 }

@@ -63,6 +63,11 @@ struct Batch {
   int* nest;          // [nq]  lists the PQ sample pass estimates (>= nsamp; == nsamp unless 8-bit
                       //       PQ: then the same array only when nest_item == 0)
   int nest_item;      // objects per sample-pass work item (8-bit PQ), 0: nest = nsamp
+  // Algorithm 3 (bbc_alg3.cuh; allocated only when the bound-aware re-rank is on)
+  uint16_t* a3lb;     // [nq x cap]  (a_lb | a_ub << 8) per probe-order position
+  uint16_t* a3lc;     // [nq x cap]  the same per candidate slot
+  int* a3ordu;        // [nq x cap]  B_u's candidate slots grouped by a_ub
+  int* a3nall;        // [nq]        nprobe (the estimate pass covers every probed list)
 };
 
 // Index arrays on the device.
