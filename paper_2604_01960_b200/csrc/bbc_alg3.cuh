@@ -21,6 +21,15 @@
 
 namespace bbc {
 
+#ifndef BBC_A3_NR
+#define BBC_A3_NR 2      // rows per warp in flight in the marginal-bucket gathers
+#endif
+#ifndef BBC_A3_V
+#define BBC_A3_V 2       // 16-byte vectors per lane per row per load round
+#endif
+#ifndef BBC_A3_MINB
+#define BBC_A3_MINB 2    // CTAs per SM (register cap)
+#endif
 constexpr int kA3NT = 512;
 
 struct Alg3Smem {
@@ -33,59 +42,89 @@ struct Alg3Smem {
   int i, j, tau;
 };
 
-// every probed list (warp-strided): f(p, row, rq2) for each probe-order position p of the list
-template <typename F>
-__device__ __forceinline__ void a3_for_probed(const Batch& b, int q, F f) {
+// every probed list (warp-strided): for each probe-order position p of the list, v = ld(p, row)
+// for U positions per lane first (their loads in flight together), then use(p, row, rq2, v)
+template <int U, typename LdF, typename UseF>
+__device__ __forceinline__ void a3_for_probed(const Batch& b, int q, LdF ld, UseF use) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int* po = b.poff + (size_t)q * (b.nprobe + 1);
   for (int j = w; j < b.nprobe; j += kA3NT / 32) {
     const int p0 = po[j], p1 = po[j + 1];
     const long long rb = b.rbase[(size_t)q * b.nprobe + j];
     const float rq2 = b.rq2[(size_t)q * b.nprobe + j];
-    for (int p = p0 + lane; p < p1; p += 32) f(p, rb + p, rq2);
+    for (int pb = p0 + lane; pb < p1; pb += 32 * U) {
+      decltype(ld(0, 0LL)) v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (pb + 32 * u < p1) v[u] = ld(pb + 32 * u, rb + pb + 32 * u);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (pb + 32 * u < p1) use(pb + 32 * u, rb + pb + 32 * u, rq2, v[u]);
+    }
   }
 }
 
-// exact ||q - x||^2 of one row by one warp (all lanes return it); 16-byte (fp32) or 4-byte (u8)
-// loads when d is a multiple of 4, so a 960-d row is 7.5 loads per lane
-template <bool U8>
-__device__ __forceinline__ float a3_exact(const Dev& ix, const float* sq, long long row, int lane) {
-  float acc = 0.f;
+// exact ||q - x||^2 of NR rows by one warp (rows[r] < 0: skipped, returns 0), all lanes return
+// them; every row's loads are issued before any arithmetic (16-byte loads for fp32 rows, 4-byte
+// for u8, when d is a multiple of 4), so up to NR x 4 loads per lane are in flight -- the
+// gathers are latency-bound (ncu: long-scoreboard stalls on the row loads)
+template <bool U8, int NR>
+__device__ __forceinline__ void a3_exact(const Dev& ix, const float* sq, const long long* rows, int lane,
+                                         float* out) {
   const int d = ix.d;
-  if (U8) {
-    const uint8_t* r = static_cast<const uint8_t*>(ix.raw) + (size_t)row * d;
-    if ((d & 3) == 0) {
-      for (int t = lane; t < (d >> 2); t += 32) {
-        const uint32_t w4 = __ldg(reinterpret_cast<const uint32_t*>(r) + t);
-        const float4 qv = reinterpret_cast<const float4*>(sq)[t];
-        const float d0 = (float)(w4 & 255u) - qv.x, d1 = (float)((w4 >> 8) & 255u) - qv.y;
-        const float d2 = (float)((w4 >> 16) & 255u) - qv.z, d3 = (float)(w4 >> 24) - qv.w;
-        acc = fmaf(d0, d0, acc); acc = fmaf(d1, d1, acc); acc = fmaf(d2, d2, acc); acc = fmaf(d3, d3, acc);
-      }
-    } else {
-      for (int t = lane; t < d; t += 32) {
-        const float df = (float)__ldg(r + t) - sq[t];
-        acc = fmaf(df, df, acc);
+  float acc[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) acc[r] = 0.f;
+  if ((d & 3) == 0) {
+    const int nv = d >> 2;
+    for (int t0 = 0; t0 < nv; t0 += 32 * BBC_A3_V) {     // BBC_A3_V vectors per lane per row per round
+      float4 x[NR][BBC_A3_V];
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+#pragma unroll
+        for (int v = 0; v < BBC_A3_V; ++v) {
+          const int t = t0 + lane + 32 * v;
+          if (rows[r] >= 0 && t < nv) {
+            if (U8) {
+              const uint32_t w4 = __ldg(reinterpret_cast<const uint32_t*>(
+                                            static_cast<const uint8_t*>(ix.raw) + (size_t)rows[r] * d) + t);
+              x[r][v] = make_float4((float)(w4 & 255u), (float)((w4 >> 8) & 255u),
+                                    (float)((w4 >> 16) & 255u), (float)(w4 >> 24));
+            } else {
+              x[r][v] = __ldg(reinterpret_cast<const float4*>(
+                                  static_cast<const float*>(ix.raw) + (size_t)rows[r] * d) + t);
+            }
+          }
+        }
+#pragma unroll
+      for (int v = 0; v < BBC_A3_V; ++v) {
+        const int t = t0 + lane + 32 * v;
+        if (t < nv) {
+          const float4 qv = reinterpret_cast<const float4*>(sq)[t];
+#pragma unroll
+          for (int r = 0; r < NR; ++r)
+            if (rows[r] >= 0) {
+              const float d0 = x[r][v].x - qv.x, d1 = x[r][v].y - qv.y;
+              const float d2 = x[r][v].z - qv.z, d3 = x[r][v].w - qv.w;
+              acc[r] = fmaf(d0, d0, acc[r]); acc[r] = fmaf(d1, d1, acc[r]);
+              acc[r] = fmaf(d2, d2, acc[r]); acc[r] = fmaf(d3, d3, acc[r]);
+            }
+        }
       }
     }
   } else {
-    const float* r = static_cast<const float*>(ix.raw) + (size_t)row * d;
-    if ((d & 3) == 0) {
-#pragma unroll 4
-      for (int t = lane; t < (d >> 2); t += 32) {
-        const float4 x = __ldg(reinterpret_cast<const float4*>(r) + t);
-        const float4 qv = reinterpret_cast<const float4*>(sq)[t];
-        const float d0 = x.x - qv.x, d1 = x.y - qv.y, d2 = x.z - qv.z, d3 = x.w - qv.w;
-        acc = fmaf(d0, d0, acc); acc = fmaf(d1, d1, acc); acc = fmaf(d2, d2, acc); acc = fmaf(d3, d3, acc);
-      }
-    } else {
-      for (int t = lane; t < d; t += 32) {
-        const float df = __ldg(r + t) - sq[t];
-        acc = fmaf(df, df, acc);
-      }
-    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+      if (rows[r] >= 0)
+        for (int t = lane; t < d; t += 32) {
+          const float xv = U8 ? (float)__ldg(static_cast<const uint8_t*>(ix.raw) + (size_t)rows[r] * d + t)
+                              : __ldg(static_cast<const float*>(ix.raw) + (size_t)rows[r] * d + t);
+          const float df = xv - sq[t];
+          acc[r] = fmaf(df, df, acc[r]);
+        }
   }
-  return warp_sum(acc);
+#pragma unroll
+  for (int r = 0; r < NR; ++r) out[r] = warp_sum(acc[r]);
 }
 
 // warp 0: first c in [0, 255) whose cumulative count (hu[c] for c <= tau, + he[c]) reaches k
@@ -124,10 +163,12 @@ __device__ __forceinline__ int a3_first_nonempty(const Alg3Smem& sm, int tau) {
 }
 
 template <bool U8>
-__global__ void __launch_bounds__(kA3NT) k_alg3(Batch b, Dev ix, float eps0) {
+__global__ void __launch_bounds__(kA3NT, BBC_A3_MINB) k_alg3(Batch b, Dev ix, float eps0) {
   extern __shared__ __align__(16) float sq[];          // the query, [d]
   __shared__ Alg3Smem sm;
-  const int q = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  // queries in locality order (k_qperm): CTAs in flight share probed lists, so candidate rows
+  // recur in L2
+  const int q = b.qperm[blockIdx.x], tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   constexpr int NW = kA3NT / 32;
   for (int t = tid; t < ix.d; t += kA3NT) sq[t] = b.Q[(size_t)q * ix.d + t];
   for (int c = tid; c < kCells; c += kA3NT) { sm.hl[c] = 0; sm.hu[c] = 0; sm.he[c] = 0; }
@@ -140,9 +181,11 @@ __global__ void __launch_bounds__(kA3NT) k_alg3(Batch b, Dev ix, float eps0) {
   __syncthreads();
 
   // A: bounds and their bucket ids (est is read from val before anything overwrites it)
-  a3_for_probed(b, q, [&](int p, long long row, float rq2) {
-    const float est = val[p];
-    const float ro = __ldg(ix.factors + 2 * row), g = __ldg(ix.factors + 2 * row + 1);
+  a3_for_probed<2>(b, q, [&](int p, long long row) {
+    const float2 f = __ldg(reinterpret_cast<const float2*>(ix.factors) + row);
+    return make_float3(val[p], f.x, f.y);
+  }, [&](int p, long long row, float rq2, float3 v) {
+    const float est = v.x, ro = v.y, g = v.z;
     const float r = __fsqrt_rn(rq2);
     const float t = __fmul_rn(__fsqrt_rn(__fsub_rn(1.f, __fmul_rn(g, g))), __fdiv_rn(1.f, g));
     const float delta = __fmul_rn(__fmul_rn(__fmul_rn(2.f, ro), r), __fmul_rn(t, eps));
@@ -177,8 +220,9 @@ __global__ void __launch_bounds__(kA3NT) k_alg3(Batch b, Dev ix, float eps0) {
   int* cid = b.cid + (size_t)q * b.cap;
   uint16_t* lc = b.a3lc + (size_t)q * b.cap;
   int* ordu = b.a3ordu + (size_t)q * b.cap;
-  a3_for_probed(b, q, [&](int p, long long row, float) {
-    const int v = lp[p], al = v & 255, au = v >> 8;
+  a3_for_probed<2>(b, q, [&](int p, long long) { return (int)lp[p]; },
+                   [&](int p, long long row, float, int v) {
+    const int al = v & 255, au = v >> 8;
     if (al <= tc) {
       const int c = atomicAdd(&sm.lcur[al], 1);
       BBC_CHECK(c < nc && nc <= b.cap);
@@ -193,23 +237,40 @@ __global__ void __launch_bounds__(kA3NT) k_alg3(Batch b, Dev ix, float eps0) {
   for (int c = tid; c < nc; c += kA3NT) val[c] = kNaN;   // NaN: not re-ranked yet
   __syncthreads();
 
-  // one warp re-ranks candidate c (if not done): exact d^2, counts moved from B_l/B_u to He
-  auto rerank = [&](int c, bool count) {
-    if (!isnan(val[c])) return;                          // warp-uniform
-    const float d2 = a3_exact<U8>(ix, sq, cpos[c], lane);
-    if (lane == 0) {
-      val[c] = d2;
-      if (count) {
-        const int v = lc[c], al = v & 255, au = v >> 8;
-        atomicSub(&sm.hl[al], 1);
-        if (au <= tau) atomicSub(&sm.hu[au], 1);
-        const int ce = cf(d2);
-        if (ce < 255) atomicAdd(&sm.he[ce], 1);
+  // warps re-rank the not-yet-done candidates of a slot range (B_l[i]: slots; B_u[j]: ordu
+  // entries), two rows per warp in flight; counts move from B_l / B_u to He
+  auto rerank_range = [&](int x0, int x1, const int* map, bool count) {
+    constexpr int NR = BBC_A3_NR;
+    for (int x = x0 + NR * w; x < x1; x += NR * NW) {
+      int c[NR];
+      long long rw[NR];
+      bool any = false;
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        c[r] = x + r < x1 ? (map ? map[x + r] : x + r) : -1;
+        rw[r] = (c[r] >= 0 && isnan(val[c[r]])) ? (long long)cpos[c[r]] : -1;   // warp-uniform
+        any |= rw[r] >= 0;
       }
+      if (!any) continue;
+      float d2[NR];
+      a3_exact<U8, NR>(ix, sq, rw, lane, d2);
+      if (lane == 0)
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          if (rw[r] < 0) continue;
+          val[c[r]] = d2[r];
+          if (count) {
+            const int v = lc[c[r]], al = v & 255, au = v >> 8;
+            atomicSub(&sm.hl[al], 1);
+            if (au <= tau) atomicSub(&sm.hu[au], 1);
+            const int ce = cf(d2[r]);
+            if (ce < 255) atomicAdd(&sm.he[ce], 1);
+          }
+        }
     }
   };
   if (tau == kTauInf) {
-    for (int c = w; c < nc; c += NW) rerank(c, false);
+    rerank_range(0, nc, nullptr, false);
   } else {
     if (w == 0) {
       const int i0 = a3_first_nonempty(sm, tau);
@@ -218,10 +279,9 @@ __global__ void __launch_bounds__(kA3NT) k_alg3(Batch b, Dev ix, float eps0) {
     __syncthreads();
     int i = sm.i, j = sm.j;
     while (i < j) {
-      for (int x = sm.lst[i] + w; x < sm.lst[i + 1]; x += NW) rerank(x, true);
+      rerank_range(sm.lst[i], sm.lst[i + 1], nullptr, true);
       __syncthreads();
-      if (j <= tau)
-        for (int x = sm.ust[j] + w; x < sm.ust[j + 1]; x += NW) rerank(ordu[x], true);
+      if (j <= tau) rerank_range(sm.ust[j], sm.ust[j + 1], ordu, true);
       __syncthreads();
       if (w == 0) {
         const int j2 = a3_threshold(sm, tau, b.k);
@@ -232,8 +292,7 @@ __global__ void __launch_bounds__(kA3NT) k_alg3(Batch b, Dev ix, float eps0) {
       i = sm.i;
       j = sm.j;
     }
-    if (j <= tau)                                        // l.22: the threshold bucket's leftovers
-      for (int x = sm.ust[j] + w; x < sm.ust[j + 1]; x += NW) rerank(ordu[x], false);
+    if (j <= tau) rerank_range(sm.ust[j], sm.ust[j + 1], ordu, false);   // l.22: threshold bucket's leftovers
   }
   __syncthreads();
   int mine = 0;

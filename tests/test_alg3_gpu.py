@@ -189,3 +189,47 @@ def test_alg3_argument_errors(load, c1t):
         pq.set_bound_rerank(False)
     finally:
         pq.close()
+
+
+@pytest.mark.slow
+def test_alg3_full_size_c3_sampled(load):
+    """Full-size C3 (1M x 960 fp32) at bench.py's operating point (nprobe 2,048, budget 20,000,
+    k 5,000) with eps0 = 1.3 (Algorithm 3's recall-0.95 point), a batch of 200
+    queries, 3 sampled queries against the oracle.  Everything the exact distances do not decide is
+    bit-exact: tau, the upper-bound histogram, the candidate set {a_lb <= tau}.  fp32 data: the
+    GPU's exact d^2 (fp32, FMA order of the warp split) and the oracle's (fp64 rounded once) differ
+    by ~1e-6 relative, which can move an exact distance across a bucket edge and so steer the loop
+    by a few objects; the re-ranked sets must agree to 0.1 %, the shared distances to 1e-5 relative,
+    and the final ids to 0.1 % of k."""
+    cfg, ix, Q, g = gidx(load, "C3")
+    nprobe, budget, k, eps0 = 2048, 20000, cfg.k, 1.3
+    Q = np.ascontiguousarray(Q[:200])
+    sel = np.array([3, 101, 177])
+    g.set_bound_rerank(True, eps0)
+    try:
+        ids, d2, t = g.search_debug(torch.from_numpy(Q).cuda(), k, nprobe, budget, cand_stride=60000)
+        torch.cuda.synchronize()
+    finally:
+        g.set_bound_rerank(False)
+    si = torch.from_numpy(sel).cuda()
+    t = {a: b[si].cpu().numpy() for a, b in t.items()}
+    ids, d2 = ids[si].cpu().numpy(), d2[si].cpu().numpy()
+    exp = oracle_alg3(ix, np.ascontiguousarray(Q[sel]), k, nprobe, budget, np.float32(eps0))
+    for i, e in enumerate(exp):
+        assert t["tau"][i] == e["tau"] and e["tau"] != (1 << 30), f"q{sel[i]} tau"
+        assert np.array_equal(t["hist"][i][:255], e["hist"]), f"q{sel[i]} ub histogram"
+        nc = int(t["n_cand"][i])
+        assert nc == len(e["cand"]) and nc <= 60000, f"q{sel[i]} n_cand"
+        cids, cd2 = t["cand_ids"][i][:nc], t["cand_d2"][i][:nc]
+        assert np.array_equal(np.sort(cids), e["cand"]), f"q{sel[i]} candidate set"
+        done = np.isfinite(cd2)
+        g_rer = set(cids[done].tolist())
+        o_rer = set(e["rer"].tolist())
+        assert len(g_rer ^ o_rer) <= 0.001 * len(o_rer), f"q{sel[i]} re-ranked sets {len(g_rer ^ o_rer)}"
+        both = [c for c in cids[done].tolist() if c in o_rer]
+        gd = dict(zip(cids[done].tolist(), cd2[done].tolist()))
+        a = np.array([gd[c] for c in both])
+        b = np.array([e["rer_d2"][c] for c in both])
+        assert np.all(np.abs(a - b) <= 1e-5 * np.abs(b)), f"q{sel[i]} exact d2"
+        common = len(set(ids[i].tolist()) & set(e["top_ids"].tolist()))
+        assert common >= k - max(1, k // 1000), f"q{sel[i]} final ids {common}/{k}"
