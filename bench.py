@@ -74,6 +74,8 @@ def parse():
     p.add_argument("--bound-rerank", type=float, default=None, metavar="EPS0",
                    help="RaBitQ: Algorithm 3's bound-aware re-rank with this eps0 (1.9 in the paper) "
                         "instead of Algorithm 1's superset (f1; measurement, not the headline)")
+    p.add_argument("--bound-rerank-gathers", choices=("list", "query"), default="list",
+                   help="Algorithm 3's exact distances: every candidate's in list order, or B_exact's per query")
     p.add_argument("--bucket-sweep", action="store_true",
                    help="QPS, |S*|/budget and recall over B (Table 4 analog) at the operating point")
     return p.parse_args()
@@ -347,7 +349,7 @@ def main():
         g = Index(path, device=local)
     g.set_buckets(args.buckets)
     if args.bound_rerank is not None:
-        g.set_bound_rerank(True, args.bound_rerank)
+        g.set_bound_rerank(True, args.bound_rerank, args.bound_rerank_gathers)
     if args.sweep:
         global args_sweep_nprobe, args_sweep_budget
         if args.sweep_nprobe:
@@ -563,7 +565,8 @@ def main():
                    "parallelism": (f"list-sharded x{world} (NCCL)" if lists else f"query-sharded x{world}"),
                    "l2": "flushed (256 MB write) between timed steps",
                    **({} if args.bound_rerank is None else
-                      {"rerank": f"Algorithm 3 (bound-aware, eps0 = {args.bound_rerank})"}),
+                      {"rerank": f"Algorithm 3 (bound-aware, eps0 = {args.bound_rerank}, "
+                                 f"{args.bound_rerank_gathers}-order gathers)"}),
                    "probed_per_query": stats["probed"] / nq,
                    "candidates_per_query": stats["candidates"] / nq,
                    "microbatches": stats["microbatches"],

@@ -146,7 +146,8 @@ bbc_status bbc_set_remap(bbc_index index, int32_t m);
 
 /*
  * bbc_set_bound_rerank -- Algorithm 3, the bound-aware re-rank of IVF+RaBitQ (
- * SURVEY 8(f) f1; reading R21), in place of steps a4..a7 of a RaBitQ search.  on = 1:
+ * SURVEY 8(f) f1; reading R21), in place of steps a4..a7 of a RaBitQ search.  mode
+ * BBC_ALG3_LIST or BBC_ALG3_QUERY (same results; how the exact distances are gathered, below):
  * every probed object's estimate gets the RaBitQ bound lb/ub = est -/+ ((2 r_o) r)(t_o eps),
  * t_o = sqrt(1 - g_o^2)/g_o, eps = eps0/sqrt(D - 1) (eps0 = 1.9 in the paper,
  * P:L1440), both bucketed with the sample's codebook (Eq. 6); tau = the first bucket where the
@@ -155,12 +156,19 @@ bbc_status bbc_set_remap(bbc_index index, int32_t m);
  * result is the k smallest (exact d^2, id) of the re-ranked objects.  bbc_search_debug reports
  * the upper-bound histogram in `hist`, tau, the candidates (a_lb <= tau) in cand_ids with exact
  * d^2 for the re-ranked ones and +inf for the others.  `budget` still sizes the sample (R5).
- * on = 0 (default): Algorithm 1's superset.  The workspace grows by 8 bytes per probed-object
- * slot per query (query the size after the change).  BBC_ERR_ARG for a PQ index, a sharded
- * handle, an active remap, on outside {0, 1} or eps0 outside (0, 1e6); the sharded path
+ * BBC_ALG3_LIST computes the exact d^2 of every candidate (a_lb <= tau) with the list-order
+ * re-rank (rows shared through L2) and runs the loop on those distances; BBC_ALG3_QUERY gathers
+ * only B_exact's rows, one CTA per query as the loop reaches them (fewer rows, slower on the GPU,
+ * DESIGN.md 8).  The rows gathered are counted in bbc_last_stats' candidates.
+ * BBC_ALG3_OFF (default): Algorithm 1's superset.  The workspace grows by up to 12 bytes per
+ * probed-object slot per query (query the size after the change).  BBC_ERR_ARG for a PQ index,
+ * a sharded handle, an active remap, an unknown mode or eps0 outside (0, 1e6); the sharded path
  * (bbc_search_group, world > 1) returns BBC_ERR_ARG while it is on.
  */
-bbc_status bbc_set_bound_rerank(bbc_index index, int32_t on, float eps0);
+#define BBC_ALG3_OFF 0
+#define BBC_ALG3_LIST 1
+#define BBC_ALG3_QUERY 2
+bbc_status bbc_set_bound_rerank(bbc_index index, int32_t mode, float eps0);
 
 #define BBC_SCAN_SIMT 0
 #define BBC_SCAN_TENSOR 1

@@ -363,11 +363,18 @@ class Index:
         (default) keeps the equal-width cells as the buckets."""
         _check(lib().bbc_set_remap(self._h, int(m)))
 
-    def set_bound_rerank(self, on: bool, eps0: float = 1.9) -> None:
+    ALG3_OFF, ALG3_LIST, ALG3_QUERY = 0, 1, 2
+
+    def set_bound_rerank(self, on: bool, eps0: float = 1.9, gathers: str = "list") -> None:
         """Algorithm 3 (the bound-aware RaBitQ re-rank) in place of Algorithm 1's
         superset re-rank: lb/ub buckets from the RaBitQ bound with eps0 (1.9 in the paper), the
-        marginal-bucket loop, exact d^2 of B_exact.  RaBitQ indexes, single shard."""
-        _check(lib().bbc_set_bound_rerank(self._h, int(bool(on)), float(eps0)))
+        marginal-bucket loop, exact d^2 of B_exact.  gathers="list": every candidate's exact
+        distance by the list-order re-rank, then the loop (faster); "query": only B_exact's rows,
+        gathered per query as the loop reaches them.  Same results.  RaBitQ, single shard."""
+        if gathers not in ("list", "query"):
+            raise BBCError("gathers must be 'list' or 'query'")
+        mode = (self.ALG3_LIST if gathers == "list" else self.ALG3_QUERY) if on else self.ALG3_OFF
+        _check(lib().bbc_set_bound_rerank(self._h, mode, float(eps0)))
 
     CODES_AUTO, CODES_CACHED, CODES_STREAM = 0, 1, 2
 

@@ -162,7 +162,12 @@ __device__ __forceinline__ int a3_first_nonempty(const Alg3Smem& sm, int tau) {
   return warp_min(found);
 }
 
-template <bool U8>
+// MODE 0 (BBC_ALG3_QUERY): the whole algorithm, rows gathered by the query's CTA as the loop
+// reaches them.  MODE 1 (BBC_ALG3_LIST, first kernel): phase A only; writes each position's a_lb
+// to cells, tau to a3tau and the compaction bound (tau, or 254 for tau = infinity) to tau, so
+// that k_count/k_emit gather the candidates {a_lb <= tau} in probe order for the list-order
+// re-rank; k_alg3_loop then runs the loop on those exact distances.
+template <bool U8, int MODE>
 __global__ void __launch_bounds__(kA3NT, BBC_A3_MINB) k_alg3(Batch b, Dev ix, float eps0) {
   extern __shared__ __align__(16) float sq[];          // the query, [d]
   __shared__ Alg3Smem sm;
@@ -170,7 +175,8 @@ __global__ void __launch_bounds__(kA3NT, BBC_A3_MINB) k_alg3(Batch b, Dev ix, fl
   // recur in L2
   const int q = b.qperm[blockIdx.x], tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   constexpr int NW = kA3NT / 32;
-  for (int t = tid; t < ix.d; t += kA3NT) sq[t] = b.Q[(size_t)q * ix.d + t];
+  if (MODE == 0)
+    for (int t = tid; t < ix.d; t += kA3NT) sq[t] = b.Q[(size_t)q * ix.d + t];
   for (int c = tid; c < kCells; c += kA3NT) { sm.hl[c] = 0; sm.hu[c] = 0; sm.he[c] = 0; }
   CellFn cf;
   if (b.nsamp[q] > 0) cf.init(b.edges[2 * q], b.edges[2 * q + 1], b.nbuckets);
@@ -191,6 +197,7 @@ __global__ void __launch_bounds__(kA3NT, BBC_A3_MINB) k_alg3(Batch b, Dev ix, fl
     const float delta = __fmul_rn(__fmul_rn(__fmul_rn(2.f, ro), r), __fmul_rn(t, eps));
     const int al = cf(__fsub_rn(est, delta)), au = cf(__fadd_rn(est, delta));
     lp[p] = (uint16_t)(al | (au << 8));
+    if (MODE == 1) b.cells[(size_t)q * b.cap + p] = (uint8_t)al;
     if (al < 255) atomicAdd(&sm.hl[al], 1);
     if (au < 255) atomicAdd(&sm.hu[au], 1);
   });
@@ -203,6 +210,13 @@ __global__ void __launch_bounds__(kA3NT, BBC_A3_MINB) k_alg3(Batch b, Dev ix, fl
   const int tau = sm.tau;
   const int tc = tau == kTauInf ? 254 : tau;             // candidates: a_lb <= tc
   for (int c = tid; c < kCells; c += kA3NT) b.hist[(size_t)q * kCells + c] = c < 255 ? sm.hu[c] : 0;
+  if (MODE == 1) {
+    if (tid == 0) {
+      b.a3tau[q] = tau;
+      b.tau[q] = tc;
+    }
+    return;
+  }
   if (tid == 0) {
     int s = 0, u = 0;
     for (int c = 0; c <= tc; ++c) {
@@ -248,6 +262,7 @@ __global__ void __launch_bounds__(kA3NT, BBC_A3_MINB) k_alg3(Batch b, Dev ix, fl
 #pragma unroll
       for (int r = 0; r < NR; ++r) {
         c[r] = x + r < x1 ? (map ? map[x + r] : x + r) : -1;
+        BBC_CHECK(c[r] < nc && (c[r] < 0 || (cpos[c[r]] >= 0 && cpos[c[r]] < ix.n_local)));
         rw[r] = (c[r] >= 0 && isnan(val[c[r]])) ? (long long)cpos[c[r]] : -1;   // warp-uniform
         any |= rw[r] >= 0;
       }
@@ -310,6 +325,97 @@ __global__ void __launch_bounds__(kA3NT, BBC_A3_MINB) k_alg3(Batch b, Dev ix, fl
     atomicAdd((unsigned long long*)&b.stats[0], (unsigned long long)n_o);
     atomicAdd((unsigned long long*)&b.stats[1], (unsigned long long)sm.he[255]);
   }
+}
+
+// BBC_ALG3_LIST, second kernel: the loop of l.12-21 over the candidates' exact distances, which
+// the list-order re-rank has computed for every candidate {a_lb <= tau} (val, probe order).  One
+// CTA per query: each candidate's bucket pair from its probe position (a3pos, written by k_emit),
+// the counts B_l / B_u, the candidates grouped by a_lb and B_u's by a_ub, then the loop moving
+// the counts of B_l[i] and B_u[j] to He (a thread per object, no row gathers); the candidates the
+// loop never reaches leave B_exact (+inf), exactly as in MODE 0.
+__global__ void __launch_bounds__(kA3NT) k_alg3_loop(Batch b, Dev ix) {
+  __shared__ Alg3Smem sm;
+  const int q = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int tau = b.a3tau[q];
+  const int tc = tau == kTauInf ? 254 : tau;
+  const int nc = b.ncand[q];
+  if (tid == 0) b.tau[q] = tau;                          // the threshold, as MODE 0 reports it
+  if (tau == kTauInf) return;                            // every candidate is re-ranked
+  for (int c = tid; c < kCells; c += kA3NT) { sm.hl[c] = 0; sm.hu[c] = 0; sm.he[c] = 0; }
+  CellFn cf;
+  if (b.nsamp[q] > 0) cf.init(b.edges[2 * q], b.edges[2 * q + 1], b.nbuckets);
+  else cf.init(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), b.nbuckets);
+  float* val = b.val + (size_t)q * b.cap;
+  int* pos = b.a3pos + (size_t)q * b.cap;                // read, then reused as the B_l index
+  uint16_t* lc = b.a3lc + (size_t)q * b.cap;
+  int* ordu = b.a3ordu + (size_t)q * b.cap;
+  uint8_t* done = b.cells + (size_t)q * b.cap;           // per candidate (the cells are consumed)
+  const uint16_t* lp = b.a3lb + (size_t)q * b.cap;
+  __syncthreads();
+  for (int c = tid; c < nc; c += kA3NT) {
+    BBC_CHECK(pos[c] >= 0 && pos[c] < b.cap);
+    const int v = lp[pos[c]], al = v & 255, au = v >> 8;
+    BBC_CHECK(al <= tc);
+    lc[c] = (uint16_t)v;
+    atomicAdd(&sm.hl[al], 1);
+    if (au <= tau) atomicAdd(&sm.hu[au], 1);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int s = 0, u = 0;
+    for (int c = 0; c <= tc; ++c) {
+      sm.lst[c] = s; sm.lcur[c] = s; s += sm.hl[c];
+      sm.ust[c] = u; sm.ucur[c] = u; u += sm.hu[c];
+    }
+    sm.lst[tc + 1] = s;
+    sm.ust[tc + 1] = u;
+  }
+  __syncthreads();
+  for (int c = tid; c < nc; c += kA3NT) {
+    const int v = lc[c], al = v & 255, au = v >> 8;
+    pos[atomicAdd(&sm.lcur[al], 1)] = c;
+    if (au <= tau) ordu[atomicAdd(&sm.ucur[au], 1)] = c;
+    done[c] = 0;
+  }
+  __syncthreads();
+  auto visit = [&](int x0, int x1, const int* map, bool count) {
+    for (int x = x0 + tid; x < x1; x += kA3NT) {
+      const int c = map[x];
+      if (done[c]) continue;
+      done[c] = 1;
+      if (count) {
+        const int v = lc[c], al = v & 255, au = v >> 8;
+        atomicSub(&sm.hl[al], 1);
+        if (au <= tau) atomicSub(&sm.hu[au], 1);
+        const int ce = cf(val[c]);
+        if (ce < 255) atomicAdd(&sm.he[ce], 1);
+      }
+    }
+  };
+  if (w == 0) {
+    const int i0 = a3_first_nonempty(sm, tau);
+    if (lane == 0) { sm.i = i0; sm.j = tau; }
+  }
+  __syncthreads();
+  int i = sm.i, j = sm.j;
+  while (i < j) {
+    visit(sm.lst[i], sm.lst[i + 1], pos, true);
+    __syncthreads();
+    if (j <= tau) visit(sm.ust[j], sm.ust[j + 1], ordu, true);
+    __syncthreads();
+    if (w == 0) {
+      const int j2 = a3_threshold(sm, tau, b.k);
+      const int i2 = a3_first_nonempty(sm, tau);
+      if (lane == 0) { sm.i = i2; sm.j = j2; }
+    }
+    __syncthreads();
+    i = sm.i;
+    j = sm.j;
+  }
+  if (j <= tau) visit(sm.ust[j], sm.ust[j + 1], ordu, false);   // l.22
+  __syncthreads();
+  for (int c = tid; c < nc; c += kA3NT)
+    if (!done[c]) val[c] = __int_as_float(0x7f800000);          // not in B_exact: +inf
 }
 
 __global__ void k_fill_int(int* p, int n, int v) {

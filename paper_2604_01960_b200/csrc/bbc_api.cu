@@ -216,7 +216,7 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1, bool xch
   p.per_query += (size_t)(2 * nprobe + 1) * 4 +                          // sweep order (sperm, spad)
                  (size_t)((cap + 32LL * nprobe + kItemMin - 1) / kItemMin) * 12;   //   + items_s, ikey
   if (xchg || world > 1) p.per_query += (size_t)k * 16 + (size_t)world * 8;   // result exchange (XBuf)
-  if (ix->alg3) p.per_query += (size_t)cap * 8 + 4 + 3 * 256;           // Algorithm 3 (a3lb, a3lc, a3ordu)
+  if (ix->alg3) p.per_query += (size_t)cap * 12 + 8 + 4 * 256;          // Algorithm 3 (a3lb, a3lc, a3ordu, a3pos)
   p.fixed = 64 * 256 + (size_t)3 * (std::max(ix->nlist, ix->rt_nunits) + 1) * 4 + 3 * 256 +
             (size_t)(ix->nlist + 1) * 4 + 512;                          // icnt, ictr
   if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) {            // pair codes + inverted index
@@ -301,9 +301,11 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nqmax, int nprobe,
     b.a3lc = (uint16_t*)take((size_t)nqb * p.cap * 2);
     b.a3ordu = (int*)take((size_t)nqb * p.cap * 4);
     b.a3nall = (int*)take((size_t)nqb * 4);
+    b.a3pos = ix->alg3 == BBC_ALG3_LIST ? (int*)take((size_t)nqb * p.cap * 4) : nullptr;
+    b.a3tau = (int*)take((size_t)nqb * 4);
   } else {
     b.a3lb = b.a3lc = nullptr;
-    b.a3ordu = b.a3nall = nullptr;
+    b.a3ordu = b.a3nall = b.a3pos = b.a3tau = nullptr;
   }
   db->prefix = (unsigned long long*)take((size_t)nqb * 8);
   db->need = (long long*)take((size_t)nqb * 8);
@@ -797,6 +799,7 @@ void stage_compact(Shard& s, cudaStream_t st) {
 // (the RaBitQ scan in EST mode over all probed lists), then one CTA per query for the bounds,
 // the two buffers and the marginal-bucket loop.  Candidates leave with exact d^2 (B_exact) or
 // +inf, ready for k_final_select.
+void stage_rerank(Shard& s, cudaStream_t st);
 void stage_alg3(Shard& s, cudaStream_t st) {
   const bbc_index_s* ix = s.ix;
   Batch b2 = s.b;
@@ -815,14 +818,41 @@ void stage_alg3(Shard& s, cudaStream_t st) {
       g_launches += 1;
     }
   }
+  if (ix->alg3 == BBC_ALG3_LIST) {
+    // list mode: bounds, tau and the candidates' lower-bound buckets (k_alg3<.., 1>), the
+    // candidates {a_lb <= tau} compacted in probe order and their exact d^2 computed by the
+    // list-order re-rank (a list's rows shared through L2 by its queries), then the loop on
+    // bucket counts over those distances (k_alg3_loop)
+    {
+      StageScope sc(s.ix, st, BBC_STAGE_COMPACT);
+      k_alg3<false, 1><<<s.b.nq, kA3NT, 0, st>>>(s.b, s.dv, ix->alg3_eps0);
+      g_launches += 1;
+    }
+    {
+      StageScope sc(s.ix, st, BBC_STAGE_COMPACT);
+      const int nb = s.b.nq;
+      const int nchunk = (int)((s.p.cap + kChunk - 1) / kChunk);
+      k_count<<<dim3(std::min((nchunk + kCntPer - 1) / kCntPer, 8), nb), kCmpNT, 0, st>>>(s.b, s.b.chunk, nchunk);
+      k_chunk_offsets<<<nb, 256, 0, st>>>(s.b, s.b.chunk, nchunk);
+      Batch be = s.b;
+      if (!rerank_list_order(s.ix, s.b, s.ix->raw_u8 ? s.ix->d : s.ix->d * 4)) be.sstart = nullptr;
+      k_emit<<<dim3(std::min(nchunk, 24), nb), kCmpNT, 0, st>>>(be, s.dv, s.b.chunk, nchunk);
+      g_launches += 3;
+    }
+    stage_rerank(s, st);
+    StageScope sc(s.ix, st, BBC_STAGE_RERANK);
+    k_alg3_loop<<<s.b.nq, kA3NT, 0, st>>>(s.b, s.dv);
+    g_launches += 1;
+    return;
+  }
   StageScope sc(s.ix, st, BBC_STAGE_RERANK);
   const size_t sm = (size_t)ix->d * 4;
   if (ix->raw_u8) {
-    set_smem(k_alg3<true>, sm);
-    k_alg3<true><<<s.b.nq, kA3NT, sm, st>>>(s.b, s.dv, ix->alg3_eps0);
+    set_smem(k_alg3<true, 0>, sm);
+    k_alg3<true, 0><<<s.b.nq, kA3NT, sm, st>>>(s.b, s.dv, ix->alg3_eps0);
   } else {
-    set_smem(k_alg3<false>, sm);
-    k_alg3<false><<<s.b.nq, kA3NT, sm, st>>>(s.b, s.dv, ix->alg3_eps0);
+    set_smem(k_alg3<false, 0>, sm);
+    k_alg3<false, 0><<<s.b.nq, kA3NT, sm, st>>>(s.b, s.dv, ix->alg3_eps0);
   }
   g_launches += 1;
 }
@@ -1799,7 +1829,8 @@ bbc_status bbc_set_scan_mode(bbc_index ix, int32_t mode) {
 
 bbc_status bbc_set_bound_rerank(bbc_index ix, int32_t on, float eps0) {
   if (!ix) return fail(BBC_ERR_ARG, "null index");
-  if (on != 0 && on != 1) return fail(BBC_ERR_ARG, "on must be 0 or 1");
+  if (on != BBC_ALG3_OFF && on != BBC_ALG3_LIST && on != BBC_ALG3_QUERY)
+    return fail(BBC_ERR_ARG, "mode must be BBC_ALG3_OFF, BBC_ALG3_LIST or BBC_ALG3_QUERY");
   if (on && ix->kind != BBC_KIND_RABITQ) return fail(BBC_ERR_ARG, "Algorithm 3 needs a RaBitQ index");
   if (on && ix->world > 1) return fail(BBC_ERR_ARG, "Algorithm 3 is single-shard only");
   if (on && ix->remap_m > 0) return fail(BBC_ERR_ARG, "Algorithm 3 uses the equal-width buckets (remap off)");

@@ -68,6 +68,8 @@ struct Batch {
   uint16_t* a3lc;     // [nq x cap]  the same per candidate slot
   int* a3ordu;        // [nq x cap]  B_u's candidate slots grouped by a_ub
   int* a3nall;        // [nq]        nprobe (the estimate pass covers every probed list)
+  int* a3pos;         // [nq x cap]  probe-order position of each candidate (k_emit, list mode)
+  int* a3tau;         // [nq]        Algorithm 3's tau (b.tau holds the compaction's bound)
 };
 
 // Index arrays on the device.
@@ -1768,6 +1770,7 @@ __device__ __forceinline__ void emit_chunk(const Batch& b, const Dev& ix, const 
         rbase = win ? s_rb[j] : rb[jc + j];
       }
       BBC_CHECK(cbeg + pos < b.cap && rbase + i >= 0 && rbase + i < ix.n_local);
+      if (b.a3pos) b.a3pos[(size_t)q * b.cap + cbeg + pos] = i;   // Algorithm 3 (list mode)
       outp[pos++] = (int)(rbase + i);
     }
   }

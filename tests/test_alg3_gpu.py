@@ -67,7 +67,7 @@ def oracle_alg3(ix, Q, k, nprobe, budget, eps0):
     return out
 
 
-def run_and_compare(load, name, eps0, nprobe=None, budget=None, k=None, scan=None, nq=None):
+def run_and_compare(load, name, eps0, nprobe=None, budget=None, k=None, scan=None, nq=None, gathers="list"):
     cfg, ix, Q, g = gidx(load, name)
     nprobe = cfg.nprobe if nprobe is None else nprobe
     budget = cfg.budget if budget is None else budget
@@ -75,7 +75,7 @@ def run_and_compare(load, name, eps0, nprobe=None, budget=None, k=None, scan=Non
     Q = np.ascontiguousarray(Q[:nq] if nq else Q)
     if scan is not None:
         g.set_scan_mode(scan)
-    g.set_bound_rerank(True, eps0)
+    g.set_bound_rerank(True, eps0, gathers)
     try:
         q = torch.from_numpy(Q).cuda()
         ids, d2, t = g.search_debug(q, k, nprobe, budget)
@@ -87,7 +87,7 @@ def run_and_compare(load, name, eps0, nprobe=None, budget=None, k=None, scan=Non
     ids, d2 = ids.cpu().numpy(), d2.cpu().numpy()
     t = {a: b.cpu().numpy() for a, b in t.items()}
     exp = oracle_alg3(ix, Q, k, nprobe, budget, np.float32(eps0))
-    n_rer = 0
+    n_rer = n_cand = 0
     for i, e in enumerate(exp):
         assert t["tau"][i] == e["tau"], f"q{i} tau {t['tau'][i]} vs {e['tau']}"
         assert np.array_equal(t["hist"][i][:255], e["hist"]) and t["hist"][i][255] == 0, f"q{i} ub histogram"
@@ -104,7 +104,9 @@ def run_and_compare(load, name, eps0, nprobe=None, budget=None, k=None, scan=Non
         assert np.array_equal(ids[i][o], e["top_ids"]), f"q{i} final ids"
         assert np.array_equal(d2[i][o], e["top_d2"]), f"q{i} final d2"
         n_rer += len(e["rer"])
-    assert st["candidates"] == n_rer
+        n_cand += nc
+    # rows gathered: B_exact's (query mode) or every candidate's (list mode)
+    assert st["candidates"] == (n_rer if gathers == "query" else n_cand)
     return t, exp
 
 
@@ -114,39 +116,44 @@ def run_and_compare(load, name, eps0, nprobe=None, budget=None, k=None, scan=Non
 @pytest.mark.parametrize("name,eps0,scan", [
     ("C3a3", 1.9, "tensor"), ("C3a3", 1.2, "simt"), ("C3a3", 1.2, "tensor"), ("C3a3", 0.6, "tensor"),
     ("C3a3u8", 0.6, "tensor"), ("C3a3u8", 1.2, "simt")])
-def test_alg3_parity(load, name, eps0, scan):
+@pytest.mark.parametrize("gathers", ["list", "query"])
+def test_alg3_parity(load, name, eps0, scan, gathers):
     from paper_2604_01960_b200 import Index
     mode = Index.SCAN_TENSOR if scan == "tensor" else Index.SCAN_SIMT
-    t, exp = run_and_compare(load, name, eps0, scan=mode)
+    t, exp = run_and_compare(load, name, eps0, scan=mode, gathers=gathers)
     assert any(e["tau"] != (1 << 30) for e in exp)           # the threshold is finite somewhere
     if eps0 == 1.2:                                            # the loop stopped early somewhere
         assert any(len(e["rer"]) < len(e["cand"]) for e in exp)
 
 
-def test_alg3_tau_infinity(load):
+@pytest.mark.parametrize("gathers", ["list", "query"])
+def test_alg3_tau_infinity(load, gathers):
     """eps0 so wide that fewer than k upper bounds fall below d_max: tau = infinity, every object
     with a_lb <= 254 is re-ranked (R21)."""
-    t, exp = run_and_compare(load, "C3a3", 60.0, nq=8)
+    t, exp = run_and_compare(load, "C3a3", 60.0, nq=8, gathers=gathers)
     assert all(e["tau"] == (1 << 30) for e in exp)
 
 
-def test_alg3_no_sample(load):
+@pytest.mark.parametrize("gathers", ["list", "query"])
+def test_alg3_no_sample(load, gathers):
     """budget >= the probed objects: no sample (Alg. 1 l.11), every bound in bucket 0, tau = 0 and
     all of B_u[0] re-ranked as the threshold bucket's leftovers."""
-    t, exp = run_and_compare(load, "C3a3", 1.9, nprobe=3, budget=10 ** 6, nq=8)
+    t, exp = run_and_compare(load, "C3a3", 1.9, nprobe=3, budget=10 ** 6, nq=8, gathers=gathers)
     assert all(e["tau"] == 0 for e in exp)
 
 
-def test_alg3_narrow_bound(load):
+@pytest.mark.parametrize("gathers", ["list", "query"])
+def test_alg3_narrow_bound(load, gathers):
     """eps0 -> 0: lb = ub = est (up to rounding), Algorithm 3 becomes Algorithm 1 with budget k
     plus the threshold bucket."""
-    run_and_compare(load, "C3a3", 1e-4, nq=12)
+    run_and_compare(load, "C3a3", 1e-4, nq=12, gathers=gathers)
 
 
-def test_alg3_host_path_and_microbatches(load):
+@pytest.mark.parametrize("gathers", ["list", "query"])
+def test_alg3_host_path_and_microbatches(load, gathers):
     """The pipelined host path (micro-batches) gives the device path's results under Algorithm 3."""
     cfg, ix, Q, g = gidx(load, "C3a3")
-    g.set_bound_rerank(True, 1.9)
+    g.set_bound_rerank(True, 1.2, gathers)
     try:
         q = torch.from_numpy(np.ascontiguousarray(Q)).cuda()
         a_ids, a_d2 = g.search(q, cfg.k, cfg.nprobe, cfg.budget)
@@ -176,6 +183,8 @@ def test_alg3_argument_errors(load, c1t):
         g.set_bound_rerank(True, 0.0)
     with pytest.raises(BBCError):
         g.set_bound_rerank(True, float("nan"))
+    with pytest.raises(BBCError):
+        g.set_bound_rerank(True, 1.9, "rows")
     g.set_remap(8)
     try:
         with pytest.raises(BBCError):

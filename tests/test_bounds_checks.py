@@ -1,5 +1,5 @@
 """The bounds-checked build (BBC_CHECKS=1: device-side checks on the indices the PQ scan, its
-sweep-order kernels, the compaction and the selections compute; a violation traps) runs the
+sweep-order kernels, the compaction, the selections and Algorithm 3's kernel compute; a violation traps) runs the
 search paths without a trap and returns the default build's results bit for bit.
 
 compute-sanitizer is closed on the GPU pool, so this stands in for memcheck on those kernels.
@@ -24,7 +24,9 @@ CASES = [("C1t", None, None, None, "probe"), ("C1t", None, None, None, "sweep"),
          ("C1t", 5000, 1, 5000, "sweep"), ("C1t", 300, 32, 600, "sweep"),
          ("C2s", None, None, None, "sweep"), ("C4s", None, None, None, "sweep"),
          ("C4s", None, None, None, "probe"), ("C5s", None, None, None, "sweep"),
-         ("C4ip_s", None, None, None, "sweep"), ("C2s", None, None, None, "group-sweep")]
+         ("C4ip_s", None, None, None, "sweep"), ("C2s", None, None, None, "group-sweep"),
+         ("C3a3", None, None, None, "alg3"), ("C3a3u8", None, None, None, "alg3"),
+         ("C3a3", None, 3, 10 ** 6, "alg3")]    # Algorithm 3 (f1): finite tau, uint8 rows, no sample
 
 SCRIPT = r"""
 import json, sys
@@ -45,6 +47,12 @@ for i, (name, k, nprobe, budget, order) in enumerate(json.loads(sys.argv[2])):
         for s in shards:
             s.set_scan_order(s.ORDER_SWEEP)
         ids, d2 = search_group(shards, q, k, nprobe, budget)
+    elif order == "alg3":
+        g = Index(path)
+        g.set_bound_rerank(True, 1.2)
+        ids, d2 = g.search(q, k, nprobe, budget)
+        o = torch.argsort(ids, dim=1)                 # candidate order unspecified: sort by id
+        ids, d2 = ids.gather(1, o), d2.gather(1, o)
     else:
         g = Index(path)
         g.set_scan_order(g.ORDER_SWEEP if order == "sweep" else g.ORDER_PROBE)

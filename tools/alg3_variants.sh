@@ -6,4 +6,4 @@ mkdir -p build_variants
 [ "$1" = build ] && for v in $V; do IFS=_ read nr vv mb <<< "$v"; BBC_LIB_OUT=build_variants/lib_a3_$v.so BBC_NVCC_DEFS="-DBBC_A3_NR=$nr -DBBC_A3_V=$vv -DBBC_A3_MINB=$mb" python -c "
 import sys; sys.path.insert(0,'.')
 from paper_2604_01960_b200 import build; build.build(force=True)" || exit 1; done
-[ "$1" = run ] && for v in $V; do BBC_LIB=build_variants/lib_a3_$v.so python tools/stage_times.py --workload C3 --nprobe 2048 --budget 20000 --steps 3 --bound-rerank 1.3 --tag a3_$v; done
+[ "$1" = run ] && for v in $V; do BBC_LIB=build_variants/lib_a3_$v.so python tools/stage_times.py --workload C3 --nprobe 2048 --budget 20000 --steps 3 --bound-rerank 1.3 --gathers query --tag a3_$v; done

@@ -27,6 +27,7 @@ p.add_argument("--nq", type=int, default=0, help="first nq queries only (0: all)
 p.add_argument("--ws-gb", type=float, default=48.0, help="workspace cap (GiB)")
 p.add_argument("--rerank", choices=("auto", "query", "list", "tile"), default="auto", help="re-rank order")
 p.add_argument("--bound-rerank", type=float, default=None, help="Algorithm 3 with this eps0 (RaBitQ)")
+p.add_argument("--gathers", choices=("list", "query"), default="list", help="Algorithm 3's gathers")
 p.add_argument("--order", choices=("auto", "probe", "sweep"), default="auto", help="8-bit PQ scan order")
 a = p.parse_args()
 cfg = configs.get(a.workload)
@@ -42,7 +43,7 @@ g.set_rerank_order({"auto": g.RERANK_AUTO, "query": g.RERANK_QUERY, "list": g.RE
                     "tile": g.RERANK_TILE}[a.rerank])
 g.set_scan_order({"auto": g.ORDER_AUTO, "probe": g.ORDER_PROBE, "sweep": g.ORDER_SWEEP}[a.order])
 if a.bound_rerank is not None:
-    g.set_bound_rerank(True, a.bound_rerank)
+    g.set_bound_rerank(True, a.bound_rerank, a.gathers)
 q = torch.from_numpy(synth.generate_queries(cfg)).cuda()
 if a.nq:
     q = q[:a.nq].contiguous()
