@@ -66,7 +66,8 @@ def test_python_constants_match_header():
              "RERANK_TILE": "BBC_RERANK_TILE",
              "CODES_AUTO": "BBC_CODES_AUTO", "CODES_CACHED": "BBC_CODES_CACHED",
              "CODES_STREAM": "BBC_CODES_STREAM", "ORDER_AUTO": "BBC_ORDER_AUTO",
-             "ORDER_PROBE": "BBC_ORDER_PROBE", "ORDER_SWEEP": "BBC_ORDER_SWEEP"}
+             "ORDER_PROBE": "BBC_ORDER_PROBE", "ORDER_SWEEP": "BBC_ORDER_SWEEP",
+             "ALG3_OFF": "BBC_ALG3_OFF", "ALG3_LIST": "BBC_ALG3_LIST", "ALG3_QUERY": "BBC_ALG3_QUERY"}
     for py, c in pairs.items():
         assert c in defs, c
         assert getattr(Index, py) == int(defs[c]), py
@@ -81,3 +82,5 @@ def test_setters_reject_bad_arguments_without_gpu():
                   ("bbc_set_probe_mode", 5), ("bbc_set_code_loads", 3),
                   ("bbc_set_scan_order", 3)):
         assert getattr(L, fn)(None, v) == 1, fn            # null index first: BBC_ERR_ARG
+    for mode, eps0 in ((1, 1.9), (3, 1.9), (1, 0.0)):
+        assert L.bbc_set_bound_rerank(None, mode, eps0) == 1   # null index: BBC_ERR_ARG
