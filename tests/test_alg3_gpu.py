@@ -30,7 +30,7 @@ def gidx(load, name):
     return cfg, ix, Q, _IDX[name]
 
 
-def oracle_alg3(ix, Q, k, nprobe, budget, eps0):
+def oracle_alg3(ix, Q, k, nprobe, budget, eps0, nbuckets=255):
     """Per query: dict(tau, hist, cand (ids of a_lb <= tau), rer (ids of B_exact), rer_d2 by id,
     top ids / d2) from the oracle only."""
     from oracle import bbc_oracle as O
@@ -51,13 +51,13 @@ def oracle_alg3(ix, Q, k, nprobe, budget, eps0):
                                                        np.sqrt(np.float32(g["rq2"][j])), int(ix["D"]),
                                                        eps0)
             o += n
-        a_lb = O.cells(lb, g["d_min"], g["d_max"])
-        a_ub = O.cells(ub, g["d_min"], g["d_max"])
+        a_lb = O.cells(lb, g["d_min"], g["d_max"], nbuckets)
+        a_ub = O.cells(ub, g["d_min"], g["d_max"], nbuckets)
         H = np.bincount(a_ub, minlength=256)
         tau = O.threshold(H[:255], k)
         tc = 254 if tau == O.TAU_INF else tau
         ex = O.exact_d2(Q[i], raw[pos])
-        _, rer, _ = O.bounded_rerank_alg3(lb, ub, lambda t: ex[t], k, g["d_min"], g["d_max"])
+        _, rer, _ = O.bounded_rerank_alg3(lb, ub, lambda t: ex[t], k, g["d_min"], g["d_max"], nbuckets)
         rer = np.array(sorted(rer), dtype=np.int64)
         rid = ids_all[pos[rer]]
         top_ids, top_d2 = O.select_topk(ex[rer], rid, k)
@@ -67,7 +67,8 @@ def oracle_alg3(ix, Q, k, nprobe, budget, eps0):
     return out
 
 
-def run_and_compare(load, name, eps0, nprobe=None, budget=None, k=None, scan=None, nq=None, gathers="list"):
+def run_and_compare(load, name, eps0, nprobe=None, budget=None, k=None, scan=None, nq=None, gathers="list",
+                    nbuckets=255):
     cfg, ix, Q, g = gidx(load, name)
     nprobe = cfg.nprobe if nprobe is None else nprobe
     budget = cfg.budget if budget is None else budget
@@ -76,6 +77,7 @@ def run_and_compare(load, name, eps0, nprobe=None, budget=None, k=None, scan=Non
     if scan is not None:
         g.set_scan_mode(scan)
     g.set_bound_rerank(True, eps0, gathers)
+    g.set_buckets(nbuckets)
     try:
         q = torch.from_numpy(Q).cuda()
         ids, d2, t = g.search_debug(q, k, nprobe, budget)
@@ -84,9 +86,10 @@ def run_and_compare(load, name, eps0, nprobe=None, budget=None, k=None, scan=Non
     finally:
         g.set_bound_rerank(False)
         g.set_scan_mode(g.SCAN_TENSOR)
+        g.set_buckets(255)
     ids, d2 = ids.cpu().numpy(), d2.cpu().numpy()
     t = {a: b.cpu().numpy() for a, b in t.items()}
-    exp = oracle_alg3(ix, Q, k, nprobe, budget, np.float32(eps0))
+    exp = oracle_alg3(ix, Q, k, nprobe, budget, np.float32(eps0), nbuckets)
     n_rer = n_cand = 0
     for i, e in enumerate(exp):
         assert t["tau"][i] == e["tau"], f"q{i} tau {t['tau'][i]} vs {e['tau']}"
@@ -242,3 +245,10 @@ def test_alg3_full_size_c3_sampled(load):
         assert np.all(np.abs(a - b) <= 1e-5 * np.abs(b)), f"q{sel[i]} exact d2"
         common = len(set(ids[i].tolist()) & set(e["top_ids"].tolist()))
         assert common >= k - max(1, k // 1000), f"q{sel[i]} final ids {common}/{k}"
+
+
+@pytest.mark.parametrize("gathers", ["list", "query"])
+@pytest.mark.parametrize("nbuckets", [1, 40, 120])
+def test_alg3_bucket_counts(load, gathers, nbuckets):
+    """B < 255 equal-width buckets (bbc_set_buckets) for both of Algorithm 3's buffers and B_exact."""
+    run_and_compare(load, "C3a3", 1.2, nq=12, gathers=gathers, nbuckets=nbuckets)
