@@ -115,6 +115,10 @@ SMALL = {
                        budget=900, kmeans_iters=6),
     "C3a3u8": C3.replace(name="C3a3u8", gen="C5", raw_dtype="u8", d=128, N=30_000, nlist=64, nq=16,
                          k=300, nprobe=12, budget=900, kmeans_iters=6),
+    # D = 512 uint8 rows (the u8 limit; 8 K blocks of the RaBitQ GEMM): exact d^2 of the
+    # candidates stay integers < 2^24
+    "C3a3u8d512": C3.replace(name="C3a3u8d512", gen="C5", raw_dtype="u8", d=512, N=20_000, nlist=48,
+                             nq=12, k=200, nprobe=10, budget=600, kmeans_iters=6),
 }
 
 # Inner-product / cosine variants ("our result buffer

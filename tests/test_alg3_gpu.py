@@ -118,7 +118,8 @@ def run_and_compare(load, name, eps0, nprobe=None, budget=None, k=None, scan=Non
 # before re-ranking every candidate (B_exact strictly inside {a_lb <= tau})
 @pytest.mark.parametrize("name,eps0,scan", [
     ("C3a3", 1.9, "tensor"), ("C3a3", 1.2, "simt"), ("C3a3", 1.2, "tensor"), ("C3a3", 0.6, "tensor"),
-    ("C3a3u8", 0.6, "tensor"), ("C3a3u8", 1.2, "simt")])
+    ("C3a3u8", 0.6, "tensor"), ("C3a3u8", 1.2, "simt"), ("C3a3u8d512", 0.6, "tensor"),
+    ("C3a3u8d512", 0.6, "simt")])
 @pytest.mark.parametrize("gathers", ["list", "query"])
 def test_alg3_parity(load, name, eps0, scan, gathers):
     from paper_2604_01960_b200 import Index
