@@ -523,6 +523,97 @@ def search(ix: dict, Q: np.ndarray, k: int, nprobe: int, budget: int, want_debug
 
 
 # ----------------------------------------------------------------------------------------------
+# f2  Algorithm 4: early re-ranking of IVF+PQ
+# ----------------------------------------------------------------------------------------------
+def predicted_threshold(sample_est: np.ndarray, n_o: int, budget: int, d_min: F32, d_max: F32,
+                        nbuckets: int = 255) -> int:
+    """Alg. 4 l.2-4: "we use the bucket containing the (|O_sample|/|O| x n_cand)-th
+    quantized distance as the predicted threshold bucket tau_pred".  |O_sample| = objects of the
+    sample lists, |O| = n_o, the objects the query probes (the same sentence's update rule ends
+    at the n_cand-th distance once everything is scanned), n_cand = budget; the rank is the
+    integer floor((budget * |O_sample|) / n_o), at least 1 (reading R22)."""
+    v = np.asarray(sample_est, dtype=F32)
+    r = max(1, (int(budget) * len(v)) // int(n_o))
+    r = min(r, len(v))
+    x = np.partition(v, r - 1)[r - 1]
+    return int(cells(np.array([x], dtype=F32), d_min, d_max, nbuckets)[0])
+
+
+def early_rerank_alg4(est: np.ndarray, n_sample: int, cell: np.ndarray, tau: int, tau_pred: int,
+                      exact_fn, ids: np.ndarray, k: int):
+    """Algorithm 4 for one query, in the one-shot form of readings R17/R22: the
+    codebook (cells), tau and tau_pred are those of the whole pass; objects are visited in probe
+    order, nearest cluster first (l.5).
+      l.8   a_i <= tau ("<" in the listing; "<=" as reading R2): the object enters the buffer B
+      l.9   a_i < tau_pred: its exact distance is computed now (l.10-11, "immediately")
+            -- only for objects scanned after the sample: the sample's estimates (l.2) exist
+            before tau_pred does (l.4)
+      l.13  otherwise its quantized distance is inserted
+      l.15  "Re-rank remaining candidates in B": exact distance of every entry still holding a
+            quantized one
+      l.16  the k smallest (exact d^2, id)
+    exact_fn(i) = exact d^2 (fp32) of probe-order position i.  Returns (ids [k], d2 [k], early)
+    with `early` the probe-order positions whose exact distance was computed at l.10."""
+    B = {}
+    early = []
+    for i in range(len(est)):
+        a = int(cell[i])
+        if a <= tau:
+            if i >= n_sample and a < tau_pred:
+                B[i] = (F32(exact_fn(i)), True)
+                early.append(i)
+            else:
+                B[i] = (F32(est[i]), False)
+    for i in list(B):
+        if not B[i][1]:
+            B[i] = (F32(exact_fn(i)), True)
+    pos = np.fromiter(B.keys(), dtype=np.int64, count=len(B))
+    d2 = np.array([B[int(i)][0] for i in pos], dtype=F32)
+    out_ids, out_d2 = select_topk(d2, np.asarray(ids)[pos], k)
+    return out_ids, out_d2, np.asarray(early, dtype=np.int64)
+
+
+def search_early_alg4(ix: dict, Q: np.ndarray, k: int, nprobe: int, budget: int, nbuckets: int = 255):
+    """IVF+PQ search with Algorithm 4: steps O1-O7 as `search` (probe, LUT, estimates, sample,
+    codebook, Push, Update), then `predicted_threshold` and `early_rerank_alg4` in place of
+    O8-O9.  Returns (ids, d2, per-query dicts with tau_pred, early positions, tau, n_sample)."""
+    if ix["kind"] != "pq" or ix.get("nbits", 8) != 8:
+        raise ValueError("Algorithm 4 is defined for IVF+PQ (8-bit codes here)")
+    Q = np.asarray(Q, dtype=F32)
+    metric = ix.get("metric", "l2")
+    off = np.asarray(ix["list_offsets"])
+    pr, _ = probe(Q, ix["centroids"], nprobe, metric)
+    out_ids = np.empty((len(Q), k), dtype=np.int64)
+    out_d2 = np.empty((len(Q), k), dtype=F32)
+    info = []
+    for i in range(len(Q)):
+        lists = pr[i]
+        sizes = off[lists + 1] - off[lists]
+        pos = np.concatenate([np.arange(off[L], off[L + 1]) for L in lists])
+        est = pq_est(pq_lut(Q[i], ix["codebooks"], metric), np.asarray(ix["codes"][pos]))
+        n_o = len(pos)
+        s = sample_lists(sizes, budget)
+        if s == 0:                                     # no codebook: nothing can be predicted
+            ns, tau, tpred = 0, TAU_INF, 0
+            cell = np.zeros(n_o, dtype=np.int64)
+        else:
+            ns = int(sizes[:s].sum())
+            dmin, dmax = edges(est[:ns], budget)
+            cell = cells(est, dmin, dmax, nbuckets)
+            tau = threshold(np.bincount(cell, minlength=NCELL), budget)
+            tpred = predicted_threshold(est[:ns], n_o, budget, dmin, dmax, nbuckets)
+
+        def exact_fn(j, _q=Q[i], _pos=pos):
+            return exact_d2(_q, np.asarray(ix["raw"][_pos[j]:_pos[j] + 1]), metric)[0]
+
+        out_ids[i], out_d2[i], early = early_rerank_alg4(est, ns, cell, tau, tpred, exact_fn,
+                                                         np.asarray(ix["ids"][pos]), k)
+        info.append(dict(tau=tau, tau_pred=tpred, n_sample=ns, early_pos=early,
+                         early_ids=np.asarray(ix["ids"][pos[early]]) if len(early) else np.zeros(0, np.int64)))
+    return out_ids, out_d2, info
+
+
+# ----------------------------------------------------------------------------------------------
 # paper-literal pieces used as pins
 # ----------------------------------------------------------------------------------------------
 class ResultBuffer:

@@ -662,3 +662,65 @@ def test_alg3_wide_bounds_is_full_rerank_and_zero_width_is_exact(rng):
     assert rer0 <= set(np.flatnonzero(cells <= j0).tolist())
     assert len(rer0) < n // 4
     assert set(top0) == set(np.argsort(ex, kind="stable")[:k].tolist())
+
+
+# ---------------------------------------------------------------- f2: Algorithm 4
+def test_alg4_predicted_threshold_hand_example():
+    """tau_pred by hand: sample estimates 0..99, |O| = 1000, n_cand = 200: rank
+    floor(200 * 100 / 1000) = 20 -> the 20th smallest = 19.0; codebook [0, 51] with 255 cells of
+    width 0.2 -> bucket floor(19 / 0.2) = 95.  Rank below 1 is taken as 1 (the sample minimum:
+    bucket 0); a rank beyond the sample as its last element."""
+    v = np.arange(100, dtype=np.float32)[::-1].copy()
+    assert O.predicted_threshold(v, 1000, 200, np.float32(0), np.float32(51)) == 95
+    assert O.predicted_threshold(v, 100000, 200, np.float32(0), np.float32(51)) == 0
+    assert O.predicted_threshold(v, 100, 200, np.float32(0), np.float32(51)) == 255   # 99 > d_max
+    # the whole set as the sample: the n_cand-th distance's bucket, i.e. Algorithm 1's closed-form tau
+    x = np.random.default_rng(5).uniform(0, 1, 5000).astype(np.float32)
+    dmin, dmax = O.edges(x, 700)
+    c = O.cells(x, dmin, dmax)
+    assert O.predicted_threshold(x, len(x), 700, dmin, dmax) == O.threshold(np.bincount(c, minlength=256), 700)
+
+
+def test_alg4_hand_example():
+    """Ten objects, the first four the sample; cells 0 1 3 2 | 0 1 2 3 4 255, tau = 2, tau_pred = 2:
+    the buffer takes cells <= 2 (positions 0 1 3 4 5 6); of the objects after the sample those with
+    a cell < 2 (positions 4, 5) get their exact distance early, position 6 (cell 2) and the sample's
+    0, 1, 3 at the end; the result is the k smallest exact distances of those six."""
+    cell = np.array([0, 1, 3, 2, 0, 1, 2, 3, 4, 255])
+    est = np.arange(10, dtype=np.float32)
+    exact = np.array([5, 1, 0.5, 7, 3, 9, 2, 0.1, 0.2, 0.3], dtype=np.float32)
+    calls = []
+
+    def fn(i):
+        calls.append(i)
+        return exact[i]
+
+    ids = np.arange(100, 110)
+    out_ids, out_d2, early = O.early_rerank_alg4(est, 4, cell, 2, 2, fn, ids, 3)
+    assert early.tolist() == [4, 5]
+    assert calls == [4, 5, 0, 1, 3, 6]                 # early ones first, each object once
+    assert out_ids.tolist() == [101, 106, 104] and out_d2.tolist() == [1.0, 2.0, 3.0]
+    # tau_pred = 0: nothing early; tau_pred above tau: every candidate after the sample is early
+    assert len(O.early_rerank_alg4(est, 4, cell, 2, 0, fn, ids, 3)[2]) == 0
+    assert O.early_rerank_alg4(est, 4, cell, 2, 200, fn, ids, 3)[2].tolist() == [4, 5, 6]
+
+
+def test_alg4_equals_alg1_and_early_set_invariants(c1t):
+    """Algorithm 4 changes when an exact distance is computed, not which objects are re-ranked
+    ("we cannot reduce the number of objects to be re-ranked"): its result equals
+    Algorithm 1's (`search`) exactly; the early objects lie after the sample, in buckets below
+    tau_pred and at or below tau, and they are all of those."""
+    cfg, ix, Q, _ = c1t
+    k, nprobe, budget = 300, 16, 900
+    ids1, d1, dbg = O.search(ix, Q[:6], k, nprobe, budget, want_debug=True)
+    ids4, d4, info = O.search_early_alg4(ix, Q[:6], k, nprobe, budget)
+    assert np.array_equal(ids1, ids4) and np.array_equal(d1, d4)
+    some = 0
+    for g, f in zip(dbg, info):
+        assert f["tau"] == g["tau"]
+        c = g["cell"]
+        want = np.flatnonzero((np.arange(len(c)) >= f["n_sample"]) & (c < f["tau_pred"]) & (c <= f["tau"]))
+        assert np.array_equal(f["early_pos"], want)
+        assert set(f["early_ids"].tolist()) <= set(g["sup_ids"].tolist())
+        some += len(want)
+    assert some > 0
