@@ -170,6 +170,25 @@ bbc_status bbc_set_remap(bbc_index index, int32_t m);
 #define BBC_ALG3_QUERY 2
 bbc_status bbc_set_bound_rerank(bbc_index index, int32_t mode, float eps0);
 
+/*
+ * bbc_set_early_rerank -- Algorithm 4, the early re-ranking of IVF+PQ (SURVEY 8(f)
+ * f2; reading R22).  on = 1: after the sample stage the predicted threshold bucket
+ * tau_pred is the bucket of the floor(budget * |O_sample| / n_o)-th (at least the first) smallest
+ * sample estimate (l.2-4); the main scan pass computes, right after a work item's
+ * bucket ids, the exact distance of every object in a bucket below tau_pred (l.9-11: "we
+ * immediately compute its exact distance"); the compaction hands those distances to
+ * the candidates among them and the re-rank computes only the remaining candidates' (l.15).
+ * Results are those of Algorithm 1 (same candidates; early distances are rounded in another
+ * order, within the 1e-5 tolerance).  bbc_search_debug reports tau_pred and, per candidate,
+ * whether its distance was computed early; bbc_stats_vector entries 7 and 8 count the objects
+ * given an early distance and the candidates that used one.  The sample is exactly the nsample
+ * lists (the sweep order's sample-pass fill-up is off).  The workspace grows by 4 bytes per
+ * probed-object slot per query (query the size after the change).  on = 0 (default): Algorithm 1.
+ * BBC_ERR_ARG for a RaBitQ or 4-bit PQ index, a sharded handle, an active remap or another
+ * value of on; the sharded paths (bbc_search_group, world > 1) return BBC_ERR_ARG while it is on.
+ */
+bbc_status bbc_set_early_rerank(bbc_index index, int32_t on);
+
 #define BBC_SCAN_SIMT 0
 #define BBC_SCAN_TENSOR 1
 bbc_status bbc_set_scan_mode(bbc_index index, int32_t mode);
@@ -293,6 +312,9 @@ bbc_status bbc_search_host(bbc_index index, const float* queries_host, int64_t n
  *   n_cand  i32 [nq]           |S*|
  *   cand_ids i64 [nq x cand_stride]  ids of S* in probe order
  *   cand_d2  f32 [nq x cand_stride]  exact d^2 of S*
+ *   tau_pred i32 [nq]          Algorithm 4's predicted threshold bucket (0 when it is off)
+ *   cand_early u8 [nq x cand_stride]  1 if the candidate's d^2 was computed early (Algorithm 4)
+ * (the last two may be NULL)
  */
 typedef struct {
   int32_t* probe;
@@ -308,6 +330,8 @@ typedef struct {
   int64_t* cand_ids;
   float* cand_d2;
   int64_t cand_stride;
+  int32_t* tau_pred;
+  uint8_t* cand_early;
 } bbc_debug_bufs;
 
 bbc_status bbc_search_debug(bbc_index index, const float* queries, int64_t nq, int32_t k,
@@ -369,8 +393,9 @@ bbc_status bbc_last_stats2(bbc_index index, int64_t* probed, int64_t* candidates
 /* Counters of the last search, in order: probed objects, candidates |S*|, sample objects,
  * lists shortlisted by the tensor-core probe (0 in SIMT mode), micro-batches, micro-batches
  * re-ranked in list order, objects estimated by the PQ sample pass (the sample plus, in sweep
- * order, the lists that fill its last work item; 0 for RaBitQ).  Copies the first n (<= 7) into
- * out (host memory).  BBC_ERR_ARG for a null index or out with n > 0. */
+ * order, the lists that fill its last work item; 0 for RaBitQ), objects the scan gave an early
+ * exact distance and candidates that used one (Algorithm 4, bbc_set_early_rerank; else 0).
+ * Copies the first n (<= 9) into out (host memory).  BBC_ERR_ARG for a null index or out with n > 0. */
 bbc_status bbc_stats_vector(bbc_index index, int64_t* out, int32_t n);
 
 /* Number of CUDA kernels this library has launched in this process. */

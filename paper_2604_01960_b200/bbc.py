@@ -26,7 +26,8 @@ EXPORTS = ("ivf_load", "ivf_free", "bbc_index_info", "bbc_workspace_size", "bbc_
            "bbc_comm_init", "bbc_search_group", "bbc_last_stats2", "bbc_set_probe_mode",
            "bbc_set_scan_mode", "bbc_stats_vector", "bbc_set_buckets", "bbc_set_rerank_order",
            "bbc_measure_l2_read", "bbc_set_remap", "bbc_set_code_loads",
-           "bbc_measure_smem_lookups", "bbc_set_scan_order", "bbc_set_bound_rerank")
+           "bbc_measure_smem_lookups", "bbc_set_scan_order", "bbc_set_bound_rerank",
+           "bbc_set_early_rerank")
 
 STAGES = ("probe", "tables", "sample", "scan", "compact", "rerank", "select", "comm")
 TAU_INF = 1 << 30
@@ -52,7 +53,8 @@ class DebugBufs(ctypes.Structure):
                 ("n_probed", ctypes.c_void_p), ("est", ctypes.c_void_p),
                 ("est_stride", ctypes.c_int64), ("n_cand", ctypes.c_void_p),
                 ("cand_ids", ctypes.c_void_p), ("cand_d2", ctypes.c_void_p),
-                ("cand_stride", ctypes.c_int64)]
+                ("cand_stride", ctypes.c_int64), ("tau_pred", ctypes.c_void_p),
+                ("cand_early", ctypes.c_void_p)]
 
 
 _lib = None
@@ -91,6 +93,7 @@ def lib() -> ctypes.CDLL:
         L.bbc_set_code_loads.argtypes = [vp, i32]
         L.bbc_set_scan_order.argtypes = [vp, i32]
         L.bbc_set_bound_rerank.argtypes = [vp, i32, ctypes.c_float]
+        L.bbc_set_early_rerank.argtypes = [vp, i32]
         L.bbc_measure_smem_lookups.argtypes = [i32, i32, ctypes.POINTER(ctypes.c_double)]
         L.bbc_measure_l2_read.argtypes = [i32, ctypes.c_size_t, i32, ctypes.POINTER(ctypes.c_double)]
         L.bbc_stats_vector.argtypes = [vp, ctypes.POINTER(i64), i32]
@@ -110,7 +113,8 @@ def lib() -> ctypes.CDLL:
                    "bbc_comm_init", "bbc_search_group", "bbc_last_stats2", "bbc_set_probe_mode",
                    "bbc_set_scan_mode", "bbc_stats_vector", "bbc_set_buckets",
                    "bbc_set_rerank_order", "bbc_measure_l2_read", "bbc_set_remap",
-                   "bbc_set_code_loads", "bbc_measure_smem_lookups", "bbc_set_scan_order", "bbc_set_bound_rerank"):
+                   "bbc_set_code_loads", "bbc_measure_smem_lookups", "bbc_set_scan_order", "bbc_set_bound_rerank",
+                   "bbc_set_early_rerank"):
             getattr(L, fn).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -310,6 +314,8 @@ class Index:
             n_cand=torch.empty(nq, dtype=torch.int32, device=dev),
             cand_ids=torch.full((nq, cs), -1, dtype=torch.int64, device=dev),
             cand_d2=torch.empty((nq, cs), dtype=torch.float32, device=dev),
+            tau_pred=torch.empty(nq, dtype=torch.int32, device=dev),
+            cand_early=torch.zeros((nq, cs), dtype=torch.uint8, device=dev),
         )
         if want_est:
             t["est"] = torch.empty((nq, cap), dtype=torch.float32, device=dev)
@@ -317,7 +323,7 @@ class Index:
                        t["edges"].data_ptr(), t["hist"].data_ptr(), t["tau"].data_ptr(),
                        t["n_probed"].data_ptr(), t["est"].data_ptr() if want_est else None, cap,
                        t["n_cand"].data_ptr(), t["cand_ids"].data_ptr(), t["cand_d2"].data_ptr(),
-                       cs)
+                       cs, t["tau_pred"].data_ptr(), t["cand_early"].data_ptr())
         ids = torch.empty((nq, k), dtype=torch.int64, device=dev)
         d2 = torch.empty((nq, k), dtype=torch.float32, device=dev)
         st = torch.cuda.current_stream(dev).cuda_stream
@@ -376,6 +382,13 @@ class Index:
         mode = (self.ALG3_LIST if gathers == "list" else self.ALG3_QUERY) if on else self.ALG3_OFF
         _check(lib().bbc_set_bound_rerank(self._h, mode, float(eps0)))
 
+    def set_early_rerank(self, on: bool) -> None:
+        """Algorithm 4 (early re-ranking of IVF+PQ): the main scan pass computes the
+        exact distance of every object in a bucket below the predicted threshold tau_pred; the
+        re-rank computes the remaining candidates.  Same results as Algorithm 1.  8-bit PQ,
+        single shard, equal-width buckets."""
+        _check(lib().bbc_set_early_rerank(self._h, int(bool(on))))
+
     CODES_AUTO, CODES_CACHED, CODES_STREAM = 0, 1, 2
 
     def set_code_loads(self, mode: int) -> None:
@@ -414,7 +427,8 @@ class Index:
         a, b, c, d = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         _check(lib().bbc_last_stats2(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
                                      ctypes.byref(d)))
-        v = (ctypes.c_int64 * 7)()
-        _check(lib().bbc_stats_vector(self._h, v, 7))
+        v = (ctypes.c_int64 * 9)()
+        _check(lib().bbc_stats_vector(self._h, v, 9))
         return dict(probed=a.value, candidates=b.value, microbatches=c.value, sampled=d.value,
-                    shortlisted=v[3], rerank_list_batches=v[5], sample_pass=v[6])
+                    shortlisted=v[3], rerank_list_batches=v[5], sample_pass=v[6],
+                    early_objects=v[7], early_candidates=v[8])

@@ -61,7 +61,7 @@ struct bbc_index_s {
   uint8_t* bits = nullptr;
   float* factors = nullptr;
   void* raw = nullptr;
-  long long* stats = nullptr;           // [5]
+  long long* stats = nullptr;           // [kNStats]
   uint8_t* codes_t = nullptr;           // PQ codes, per-list chunk-major (8-bit: replicated-LUT scan;
                                         // 4-bit: k_pack_codes4 layout)
   long long* tbase = nullptr;           // [nlist] byte offset of each list in codes_t
@@ -81,6 +81,7 @@ struct bbc_index_s {
   int rerank_order = BBC_RERANK_AUTO;    // BBC_RERANK_*: work order of the exact re-rank (a7)
   int remap_m = 0;                       // 0 or m equal-depth buckets (bbc_set_remap)
   int alg3 = 0;                          // 1: Algorithm 3 bound-aware re-rank (bbc_set_bound_rerank)
+  int early = 0;                         // 1: Algorithm 4 early re-ranking of IVF+PQ (bbc_set_early_rerank)
   float alg3_eps0 = 1.9f;                // its bound's eps0
   int code_loads = BBC_CODES_AUTO;       // BBC_CODES_*: L1 policy of the PQ scan's code loads
   int scan_order = BBC_ORDER_AUTO;        // BBC_SCAN_*: visiting order of the 8-bit PQ scan
@@ -217,6 +218,7 @@ Plan make_plan(const bbc_index_s* ix, int nprobe, int k, int world = 1, bool xch
                  (size_t)((cap + 32LL * nprobe + kItemMin - 1) / kItemMin) * 12;   //   + items_s, ikey
   if (xchg || world > 1) p.per_query += (size_t)k * 16 + (size_t)world * 8;   // result exchange (XBuf)
   if (ix->alg3) p.per_query += (size_t)cap * 12 + 8 + 4 * 256;          // Algorithm 3 (a3lb, a3lc, a3ordu, a3pos)
+  if (ix->early) p.per_query += (size_t)cap * 4 + 4 + 2 * 256;          // Algorithm 4 (early, tpred)
   p.fixed = 64 * 256 + (size_t)3 * (std::max(ix->nlist, ix->rt_nunits) + 1) * 4 + 3 * 256 +
             (size_t)(ix->nlist + 1) * 4 + 512;                          // icnt, ictr
   if (ix->kind == BBC_KIND_RABITQ && ix->rbq_tc) {            // pair codes + inverted index
@@ -271,7 +273,7 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nqmax, int nprobe,
   // with the sweep order (codes streamed from HBM), the 8-bit PQ scan's sample pass fills its
   // last work item with the following lists (C4 103.4 vs 104.3 ms per step; L2-resident C2,
   // whose sample pass skips the idle warps of its last item, 5.00 vs 4.96 ms: not there)
-  const bool pq8 = ix->kind == BBC_KIND_PQ && ix->nbits == 8 &&
+  const bool pq8 = ix->kind == BBC_KIND_PQ && ix->nbits == 8 && !ix->early &&   // Alg. 4: sample = nsamp
                    (ix->scan_order == BBC_ORDER_SWEEP ||
                     (ix->scan_order == BBC_ORDER_AUTO && (double)ix->n_local * ix->M > 0.5 * (double)ix->l2_bytes));
   b.nest = pq8 ? (int*)take((size_t)nqb * 4) : b.nsamp;
@@ -307,6 +309,13 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nqmax, int nprobe,
     b.a3lb = b.a3lc = nullptr;
     b.a3ordu = b.a3nall = b.a3pos = b.a3tau = nullptr;
   }
+  if (ix->early) {
+    b.early = (float*)take((size_t)nqb * p.cap * 4);
+    b.tpred = (int*)take((size_t)nqb * 4);
+  } else {
+    b.early = nullptr;
+    b.tpred = nullptr;
+  }
   db->prefix = (unsigned long long*)take((size_t)nqb * 8);
   db->need = (long long*)take((size_t)nqb * 8);
   db->dh = (int*)take((size_t)nqb * kCells * 4);
@@ -338,13 +347,15 @@ __global__ void k_iota(int* p, int n) {
 }
 
 __global__ void k_debug_cands(const int* cpos, const float* val, const int* ncand, long long cap,
-                              long long* out_ids, float* out_d2, long long stride) {
+                              long long* out_ids, float* out_d2, long long stride,
+                              const int* rows = nullptr, uint8_t* out_early = nullptr) {
   const int q = blockIdx.y;
   const int n = ncand[q];
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n && i < stride;
        i += (long long)gridDim.x * blockDim.x) {
     if (out_ids) out_ids[q * stride + i] = cpos[q * cap + i];
     if (out_d2) out_d2[q * stride + i] = val[q * cap + i];
+    if (out_early) out_early[q * stride + i] = rows && rows[q * cap + i] < 0;   // Algorithm 4
   }
 }
 
@@ -360,6 +371,17 @@ void launch_rq(bool est, int grid, cudaStream_t st, const Batch& b, const Dev& d
                                                           sweep ? b.sperm : nullptr);                   \
   } while (0)
   if (est) { if (na) BBC_RQ_L(true, true); else BBC_RQ_L(true, false); }
+  else if (b.early && mode == 1) {                   // Algorithm 4: exact distances below tau_pred
+#define BBC_RQ_E(NA)                                                                                     \
+  do {                                                                                                  \
+    set_smem(k_pq_scan_rq<M, false, NA, true>, kRqSmemEarly);                                           \
+    k_pq_scan_rq<M, false, NA, true><<<grid, kRqNT, kRqSmemEarly, st>>>(b, dv, ct, tb, out, stride, mode, \
+                                                                         sweep ? b.items_s : b.items, b.nitems, \
+                                                                         sweep ? b.sperm : nullptr);    \
+  } while (0)
+    if (na) BBC_RQ_E(true); else BBC_RQ_E(false);
+#undef BBC_RQ_E
+  }
   else { if (na) BBC_RQ_L(false, true); else BBC_RQ_L(false, false); }
 #undef BBC_RQ_L
 }
@@ -751,7 +773,7 @@ bool rerank_list_order(const bbc_index_s* ix, const Batch& b, int rowb) {
 // available for fp32 rows of 128-512 bytes, on request only -- measured slower than the L2-fed
 // list order (C4 25.4 -> 37.0 ms, C2 0.90 -> 1.51 ms), so AUTO does not take it
 bool rerank_tile(const bbc_index_s* ix, const Batch& b, int rowb) {
-  if (!ix->rt_units || !rerank_list_order(ix, b, rowb)) return false;
+  if (!ix->rt_units || ix->early || !rerank_list_order(ix, b, rowb)) return false;
   return ix->rerank_order == BBC_RERANK_TILE;
 }
 
@@ -857,10 +879,10 @@ void stage_alg3(Shard& s, cudaStream_t st) {
   g_launches += 1;
 }
 
-template <bool IP>
+template <bool IP, bool ER = false>
 void launch_rerank(Shard& s, dim3 g, cudaStream_t st, int rowb) {
   const bool u8 = s.ix->raw_u8 != 0;
-#define BBC_RR_Q(U8, LPC, MAXV, STEPS, MINB) k_rerank<U8, LPC, MAXV, STEPS, MINB, IP><<<g, kRrNT, 0, st>>>(s.b, s.dv)
+#define BBC_RR_Q(U8, LPC, MAXV, STEPS, MINB) k_rerank<U8, LPC, MAXV, STEPS, MINB, IP, ER><<<g, kRrNT, 0, st>>>(s.b, s.dv)
   BBC_RR_VARIANTS(BBC_RR_Q)
 #undef BBC_RR_Q
 }
@@ -868,7 +890,7 @@ void launch_rerank(Shard& s, dim3 g, cudaStream_t st, int rowb) {
 // Grid: about one warp per kRrSPW pieces.  Pieces <= segments + candidates / piece, segments
 // <= nq * nprobe; candidates are taken as 1.5x the budget (|S*| is the budget plus part of the
 // threshold bucket); the kernel strides by the grid, so an underestimate costs time, not results.
-template <bool IP, int SPW>
+template <bool IP, int SPW, bool ER = false>
 void launch_rerank_seg(Shard& s, cudaStream_t st, int rowb) {
   const bool u8 = s.ix->raw_u8 != 0;
   const long long nq = s.b.nq;
@@ -881,8 +903,8 @@ void launch_rerank_seg(Shard& s, cudaStream_t st, int rowb) {
   const int* nseg = s.b.rs_off + s.ix->nlist;
 #define BBC_RR_S(U8, LPC, MAXV, STEPS, MINB)                                                           \
   do {                                                                                                \
-    k_rerank_seg<U8, LPC, MAXV, STEPS, MINB, IP, SPW, false><<<grid, kRrNT, 0, st>>>(s.b, s.dv, s.b.rseg, nseg, 0); \
-    k_rerank_seg<U8, LPC, MAXV, STEPS, MINB, IP, SPW, true><<<2 * s.ix->num_sms, kRrNT, 0, st>>>(      \
+    k_rerank_seg<U8, LPC, MAXV, STEPS, MINB, IP, SPW, false, ER><<<grid, kRrNT, 0, st>>>(s.b, s.dv, s.b.rseg, nseg, 0); \
+    k_rerank_seg<U8, LPC, MAXV, STEPS, MINB, IP, SPW, true, ER><<<2 * s.ix->num_sms, kRrNT, 0, st>>>(      \
         s.b, s.dv, s.b.rseg, nseg, covered);                                                          \
   } while (0)
   BBC_RR_VARIANTS(BBC_RR_S)
@@ -891,10 +913,10 @@ void launch_rerank_seg(Shard& s, cudaStream_t st, int rowb) {
 
 // segments per warp: 8 for rows >= 1 KB, else 4 (tuned: C3 3840 B rows 8 ~ 16 > 4 > 2 > 1; C4 384 B
 // rows 4 > 8 > 2)
-template <bool IP>
+template <bool IP, bool ER = false>
 void launch_rerank_list(Shard& s, cudaStream_t st, int rowb) {
-  if (rowb >= 1024) launch_rerank_seg<IP, 8>(s, st, rowb);
-  else launch_rerank_seg<IP, 4>(s, st, rowb);
+  if (rowb >= 1024) launch_rerank_seg<IP, 8, ER>(s, st, rowb);
+  else launch_rerank_seg<IP, 4, ER>(s, st, rowb);
 }
 
 
@@ -933,7 +955,10 @@ void stage_rerank(Shard& s, cudaStream_t st) {
     k_rr_segments<false><<<gp, 256, 0, st>>>(s.b, s.b.rs_cnt, s.b.rseg, rr_piece(rowb));
     k_inv_scan<<<1, 1024, 0, st>>>(s.b.rs_cnt, s.b.rs_off, s.b.rs_cur, ix->nlist);
     k_rr_segments<true><<<gp, 256, 0, st>>>(s.b, s.b.rs_cur, s.b.rseg, rr_piece(rowb));
-    if (ip) launch_rerank_list<true>(s, st, rowb);
+    if (s.b.early) {                                 // Algorithm 4: "re-rank remaining candidates"
+      if (ip) launch_rerank_list<true, true>(s, st, rowb);
+      else launch_rerank_list<false, true>(s, st, rowb);
+    } else if (ip) launch_rerank_list<true>(s, st, rowb);
     else launch_rerank_list<false>(s, st, rowb);
     g_launches += 5;
     return;
@@ -941,7 +966,10 @@ void stage_rerank(Shard& s, cudaStream_t st) {
   // ~32 CTAs per SM in total: short CTAs keep every SM busy to the end (tuned on C2)
   const int gy = std::max(1, (32 * ix->num_sms + nb - 1) / nb);
   const dim3 g(gy, nb);
-  if (ip) launch_rerank<true>(s, g, st, rowb);
+  if (s.b.early) {
+    if (ip) launch_rerank<true, true>(s, g, st, rowb);
+    else launch_rerank<false, true>(s, g, st, rowb);
+  } else if (ip) launch_rerank<true>(s, g, st, rowb);
   else launch_rerank<false>(s, g, st, rowb);
   g_launches += 1;
 }
@@ -1107,8 +1135,10 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
     if (st0 != BBC_OK) return st0;
   }
   if (comm != nullptr)
-    for (auto& s : sh)
+    for (auto& s : sh) {
       if (s.ix->alg3) return fail(BBC_ERR_ARG, "Algorithm 3 (bbc_set_bound_rerank) is single-shard only");
+      if (s.ix->early) return fail(BBC_ERR_ARG, "Algorithm 4 (bbc_set_early_rerank) is single-shard only");
+    }
   if (nq == 0) return BBC_OK;
   bbc_index_s* ix = sh[0].ix;                       // for CU() error marking
   CU(cudaSetDevice(ix->device));
@@ -1159,7 +1189,7 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
   int mb_index = 0;
   const long long budget_c = std::min<long long>(budget, (long long)1 << 40);
   for (auto& s : sh) {
-    CU(cudaMemsetAsync(s.ix->stats, 0, 5 * sizeof(long long), st));
+    CU(cudaMemsetAsync(s.ix->stats, 0, kNStats * sizeof(long long), st));
     s.ix->microbatches = 0;
     s.ix->rr_list_batches = 0;
     if (s.ix->timing) s.ix->timed_calls++;
@@ -1218,6 +1248,11 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
         set_smem(k_select_edges, kFsSmem);
         k_select_edges<<<nb, kSelNT, kFsSmem, st>>>(s.b, s.dv);
         g_launches += 1;
+        if (s.b.early) {                              // Algorithm 4 l.4: the predicted threshold bucket
+          set_smem(k_tau_pred, kFsSmem);
+          k_tau_pred<<<nb, kSelNT, kFsSmem, st>>>(s.b, s.dv);
+          g_launches += 1;
+        }
       }
       if (s.ix->alg3) {
         stage_alg3(s, st);
@@ -1292,8 +1327,13 @@ bbc_status run(std::vector<Shard>& sh, Comm* comm, const float* queries, int64_t
                              cudaMemcpyDeviceToDevice, st));
       if (dbg->cand_ids || dbg->cand_d2) {
         k_debug_cands<<<dim3(64, nb), 256, 0, st>>>(b.cid, b.val, b.ncand, s0.p.cap,
-                                                    (long long*)dbg->cand_ids, dbg->cand_d2, dbg->cand_stride);
+                                                    (long long*)dbg->cand_ids, dbg->cand_d2, dbg->cand_stride,
+                                                    b.early ? b.cpos : nullptr, dbg->cand_early);
         g_launches += 1;
+      }
+      if (dbg->tau_pred) {
+        if (b.tpred) CU(cp(dbg->tau_pred, b.tpred, (size_t)nb * 4));
+        else CU(cudaMemsetAsync(dbg->tau_pred, 0, (size_t)nb * 4, st));
       }
       if (dbg->est) {
         // every estimate in probe order, written to the caller's buffer (debug only)
@@ -1654,7 +1694,7 @@ bbc_status ivf_load(const char* path, int rank, int world, int cuda_device, bbc_
     ok = ok && upload_rows(8, 8, (void**)&ix->factors);
   }
   ok = ok && upload_rows(9, rowraw, &ix->raw);
-  ok = ok && dalloc((void**)&ix->stats, 5 * sizeof(long long));
+  ok = ok && dalloc((void**)&ix->stats, kNStats * sizeof(long long));
   if (ok) {
     // centroid mean, |c - mu|^2 and max |c - mu| for the tensor-core probe's error bound
     std::vector<float> C((size_t)nlist * d);
@@ -1840,9 +1880,22 @@ bbc_status bbc_set_bound_rerank(bbc_index ix, int32_t on, float eps0) {
   return BBC_OK;
 }
 
+bbc_status bbc_set_early_rerank(bbc_index ix, int32_t on) {
+  if (!ix) return fail(BBC_ERR_ARG, "null index");
+  if (on != 0 && on != 1) return fail(BBC_ERR_ARG, "on must be 0 or 1");
+  if (on && (ix->kind != BBC_KIND_PQ || ix->nbits != 8))
+    return fail(BBC_ERR_ARG, "Algorithm 4 needs an IVF+PQ index with 8-bit codes");
+  if (on && ix->world > 1) return fail(BBC_ERR_ARG, "Algorithm 4 is single-shard only");
+  if (on && ix->remap_m > 0) return fail(BBC_ERR_ARG, "Algorithm 4 uses the equal-width buckets (remap off)");
+  if (on && (ix->raw_u8 ? ix->d : 4 * ix->d) % 16 != 0) return fail(BBC_ERR_ARG, "Algorithm 4 needs rows of a multiple of 16 bytes");
+  ix->early = on;
+  return BBC_OK;
+}
+
 bbc_status bbc_set_remap(bbc_index ix, int32_t m) {
   if (!ix) return fail(BBC_ERR_ARG, "null index");
   if (m < 0 || m > 255) return fail(BBC_ERR_ARG, "m must be 0 (off) or in [1, 255]");
+  if (m > 0 && ix->early) return fail(BBC_ERR_ARG, "the equal-depth remap is off under Algorithm 4");
   if (m > 0 && ix->world > 1) return fail(BBC_ERR_ARG, "the equal-depth remap is single-shard only");
   if (m > 0 && ix->alg3) return fail(BBC_ERR_ARG, "the equal-depth remap is off under Algorithm 3");
   ix->remap_m = m;
@@ -2025,10 +2078,10 @@ bbc_status bbc_last_stats2(bbc_index ix, int64_t* probed, int64_t* candidates, i
 
 bbc_status bbc_stats_vector(bbc_index ix, int64_t* out, int32_t n) {
   if (!ix || (!out && n > 0) || n < 0) return fail(BBC_ERR_ARG, "bad argument");
-  long long h[5];
+  long long h[kNStats];
   CU(cudaMemcpy(h, ix->stats, sizeof(h), cudaMemcpyDeviceToHost));
-  const long long v[7] = {h[0], h[1], h[2], h[3], ix->microbatches, ix->rr_list_batches, h[4]};
-  for (int i = 0; i < n && i < 7; ++i) out[i] = v[i];
+  const long long v[9] = {h[0], h[1], h[2], h[3], ix->microbatches, ix->rr_list_batches, h[4], h[5], h[6]};
+  for (int i = 0; i < n && i < 9; ++i) out[i] = v[i];
   return BBC_OK;
 }
 

@@ -25,6 +25,7 @@ namespace bbc {
     }                                                                                            \
   } while (0)
 
+constexpr int kNStats = 7;          // device counters of a search (bbc_stats_vector)
 constexpr int kCells = 256;          // 255 regular cells + overflow cell 255 (DESIGN R3)
 constexpr int kTauInf = 1 << 30;     // tau = infinity (Alg. 1 l.11)
 constexpr int kSampleMinLists = 8;   // "5-10 nearest clusters", DESIGN R5

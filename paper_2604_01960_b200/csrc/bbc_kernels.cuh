@@ -70,6 +70,9 @@ struct Batch {
   int* a3nall;        // [nq]        nprobe (the estimate pass covers every probed list)
   int* a3pos;         // [nq x cap]  probe-order position of each candidate (k_emit, list mode)
   int* a3tau;         // [nq]        Algorithm 3's tau (b.tau holds the compaction's bound)
+  // Algorithm 4 (early re-ranking of IVF+PQ, bbc_set_early_rerank; allocated only when it is on)
+  int* tpred;         // [nq]        predicted threshold bucket tau_pred
+  float* early;       // [nq x cap]  exact d^2 the main scan pass computed, per probe-order position
 };
 
 // Index arrays on the device.
@@ -639,6 +642,9 @@ constexpr int kRqOffCnt = kRqOffOut + kRqGroups * 8;
 constexpr int kRqOffHist = kRqOffCnt + kRqGroups * 4;
 constexpr int kRqOffPo = kRqOffHist + kCells * 4;
 constexpr size_t kRqSmem = kRqOffPo + (kMaxProbe + 1) * 4;
+// Algorithm 4 (EARLY): the first row of every group, after the default layout
+constexpr int kRqOffRow = (int)((kRqSmem + 7) / 8 * 8);
+constexpr size_t kRqSmemEarly = kRqOffRow + kRqGroups * 8;
 // The kernel has no static shared memory, so its dynamic buffer starts right after the 1 KB
 // the driver reserves per CTA; the LUT lookups use that offset as an immediate (checked).
 constexpr unsigned kRqSmemBase = 1024;
@@ -677,7 +683,11 @@ __device__ __forceinline__ float rq_lookup4(float a, uint32_t w, uint32_t lane4)
 // 2: all lists -> estimates (debug)
 // NOALLOC: code loads bypass L1 allocation (codes larger than L2 are streamed once from HBM:
 // C4/C5 +1.5 %; L2-resident codes (C2) are faster through L1)
-template <int M, bool EST, bool NOALLOC = false>
+// EARLY (Algorithm 4; main pass only): after a work item's bucket ids are written,
+// every object in a bucket below the query's predicted threshold tau_pred gets its exact distance
+// at once -- one warp per row, 16 bytes per lane, coalesced -- stored at its probe-order position
+// in b.early for the compaction to pick up (emit_chunk).
+template <int M, bool EST, bool NOALLOC = false, bool EARLY = false>
 __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const uint8_t* __restrict__ codes_t,
                                                          const long long* __restrict__ tbase,
                                                          float* out_est, long long est_stride,
@@ -692,6 +702,7 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
   int* gcnt = reinterpret_cast<int*>(rsm + kRqOffCnt);
   int* hist = reinterpret_cast<int*>(rsm + kRqOffHist);
   int* s_popad = reinterpret_cast<int*>(rsm + kRqOffPo);
+  long long* grow = reinterpret_cast<long long*>(rsm + kRqOffRow);   // EARLY only (kRqSmemEarly)
   // persistent CTAs over the work items of k_scan_plan: (query, pass) in query locality order
   // (probe order) or sorted by their first list (sweep order)
   const int nit = *nitems;
@@ -749,6 +760,7 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
       BBC_CHECK(((long long)go << 7) + (long long)M * 32 <= ix.ct_bytes);
       oo = obase + po[j] + i0;
       BBC_CHECK(po[j] + i0 + cnt <= (EST ? est_stride : b.cap));
+      if (EARLY) grow[G] = ix.loff[L] + i0;
     }
     gofs[G] = go;
     gout[G] = oo;
@@ -846,6 +858,65 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
         }
       }
     }
+  }
+  if (EARLY) {
+    // Alg. 4 l.9-11: a_i < tau_pred -> exact distance now.  The lane's early objects are taken
+    // one at a time by the whole warp (ballot, lowest lane first): lane t loads 16 bytes of the
+    // row and of the query (rows of up to 512 bytes: fp32 d <= 128, uint8 d <= 512), warp sum.
+    const int tp = b.tpred[q];
+    const int rowb = ix.raw_u8 ? ix.d : ix.d * 4;
+    const int nv = rowb >> 4;
+    const uint8_t* raw = static_cast<const uint8_t*>(ix.raw);
+    const float* qv = b.Q + (size_t)q * ix.d;
+    const bool ipm = ix.metric == BBC_METRIC_IP;
+    int nearly = 0;
+#pragma unroll 1
+    for (int i = 0; i < kRqGPL; ++i) {
+      const int G = gl0 + 4 * i;
+      const int cnt = gcnt[G];
+      const long long oo = gout[G] + 4 * (lane & 7);
+      const long long r0 = grow[G] + 4 * (lane & 7);
+#pragma unroll 1
+      for (int j = 0; j < 4; ++j) {
+        const bool mine = 4 * (lane & 7) + j < cnt && (int)b.cells[oo + j] < tp;   // the id this lane just wrote
+        unsigned m = __ballot_sync(0xffffffffu, mine);
+        nearly += __popc(m);
+        while (m) {
+          const int src = __ffs(m) - 1;
+          m &= m - 1;
+          const long long row = __shfl_sync(0xffffffffu, r0 + j, src);
+          const long long at = __shfl_sync(0xffffffffu, oo + j, src);
+          BBC_CHECK(row >= 0 && row < ix.n_local);
+          float a = 0.f;
+          for (int t = lane; t < nv; t += 32) {
+            const uint4 x = __ldg(reinterpret_cast<const uint4*>(raw + (size_t)row * rowb) + t);
+            if (ix.raw_u8) {
+              const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+              for (int h = 0; h < 4; ++h)
+#pragma unroll
+                for (int by = 0; by < 4; ++by) {
+                  const float xv = (float)((wv[h] >> (8 * by)) & 255u), qq = __ldg(qv + t * 16 + h * 4 + by);
+                  if (ipm) a = fmaf(xv, qq, a);
+                  else { const float df = xv - qq; a = fmaf(df, df, a); }
+                }
+            } else {
+              const float4 y = __ldg(reinterpret_cast<const float4*>(qv) + t);
+              const float xs[4] = {__uint_as_float(x.x), __uint_as_float(x.y), __uint_as_float(x.z), __uint_as_float(x.w)};
+              const float ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+              for (int h = 0; h < 4; ++h) {
+                if (ipm) a = fmaf(xs[h], ys[h], a);
+                else { const float df = xs[h] - ys[h]; a = fmaf(df, df, a); }
+              }
+            }
+          }
+          a = warp_sum(a);
+          if (lane == 0) b.early[at] = ipm ? -a : a;
+        }
+      }
+    }
+    if (lane == 0 && nearly) atomicAdd((unsigned long long*)&b.stats[5], (unsigned long long)nearly);
   }
   if (!EST) {
     __syncthreads();
@@ -1450,6 +1521,34 @@ __global__ void __launch_bounds__(kSelNT) k_select_edges(Batch b, Dev ix) {
 }
 
 // ------------------------------------------------------------------------------------------
+// f2  Algorithm 4 l.2-4 (reading R22): tau_pred = bucket of the r-th smallest sample
+//     estimate, r = max(1, floor(budget * |O_sample| / n_o)).  0 without a sample (nothing early).
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSelNT) k_tau_pred(Batch b, Dev ix) {
+  __shared__ Kth32Smem sm;
+  extern __shared__ __align__(16) uint8_t fsm[];
+  FastSelSmem& fs = *reinterpret_cast<FastSelSmem*>(fsm);
+  const int q = blockIdx.x;
+  const int ns = b.nsamp[q];
+  if (ns == 0) {
+    if (threadIdx.x == 0) b.tpred[q] = 0;
+    return;
+  }
+  const int* po = b.poff + (size_t)q * (b.nprobe + 1);
+  const int n = po[ns], ntot = po[b.nprobe];
+  const float* v = b.val + (size_t)q * b.cap;
+  const long long r = min((long long)n, max(1LL, (b.budget * (long long)n) / max(1, ntot)));
+  unsigned take;
+  const uint32_t kr = cta_kth32_bracket<false>(n, (unsigned)r, [&](int i) { return f2key(v[i]); },
+                                               [&](int i) { return 0; }, &take, fs, sm, nullptr);
+  if (threadIdx.x == 0) {
+    CellFn cf;
+    cf.init(b.edges[2 * q], b.edges[2 * q + 1], b.nbuckets);
+    b.tpred[q] = cf(key2f(kr));
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // a5  Update: tau = first cell whose cumulative count reaches the budget (Alg. 1 l.5-11).
 //     One warp per query, 8 cells per lane, inclusive scan.  tau = infinity when no sample.
 // ------------------------------------------------------------------------------------------
@@ -1747,6 +1846,12 @@ __device__ __forceinline__ void emit_chunk(const Batch& b, const Dev& ix, const 
   for (int w = 0; w < kCmpNT / 32; ++w) pre += w < wid ? wcnt[w] : 0;
   int pos = pre + incl - mine;
   int* outp = b.cpos + (size_t)q * b.cap + cbeg;     // candidate rows, written in place
+  // Algorithm 4: candidates the main scan pass already gave an exact distance (bucket below
+  // tau_pred, position after the sample) take it from b.early and leave with the row complemented
+  // (negative): the re-rank then only looks up their ids
+  const int tp = b.early ? b.tpred[q] : 0;
+  const int emain = b.early ? po[b.nsamp[q]] : 0;
+  int ntaken = 0;
   s_pre[threadIdx.x] = pos;
   s_flg[threadIdx.x] = f;
   if (f) {
@@ -1771,9 +1876,16 @@ __device__ __forceinline__ void emit_chunk(const Batch& b, const Dev& ix, const 
       }
       BBC_CHECK(cbeg + pos < b.cap && rbase + i >= 0 && rbase + i < ix.n_local);
       if (b.a3pos) b.a3pos[(size_t)q * b.cap + cbeg + pos] = i;   // Algorithm 3 (list mode)
-      outp[pos++] = (int)(rbase + i);
+      int row = (int)(rbase + i);
+      if (b.early && i >= emain && (int)b.cells[(size_t)q * b.cap + i] < tp) {
+        b.val[(size_t)q * b.cap + cbeg + pos] = b.early[(size_t)q * b.cap + i];
+        row = ~row;
+        ++ntaken;
+      }
+      outp[pos++] = row;
     }
   }
+  if (ntaken) atomicAdd((unsigned long long*)&b.stats[6], (unsigned long long)ntaken);
   __syncthreads();
   if (b.sstart) {
     // list-order re-rank: candidates before the start of every pair whose object range starts
@@ -1871,7 +1983,9 @@ struct RrQuery {
 // One warp: exact d^2 (IP: -<q, x>) of up to 32 candidates whose rows are cp[0 .. n32); writes
 // vv[k] and the original id cid[k].  Rows are fetched with one coalesced load and broadcast by
 // shuffle; LPC lanes per row, STEPS rows per lane group in flight.
-template <bool U8, int LPC, int MAXV, int STEPS, bool IP>
+// ER (Algorithm 4): a complemented (negative) row marks a candidate whose exact d^2 is already in
+// vv (computed early by the scan, placed by k_emit): only its id is looked up.
+template <bool U8, int LPC, int MAXV, int STEPS, bool IP, bool ER = false>
 __device__ __forceinline__ void rr_rows32(const Dev& ix, const RrQuery<U8, LPC, MAXV>& Q,
                                           const int* __restrict__ cp, int n32, float* __restrict__ vv,
                                           int* __restrict__ cid, int lane, int per, int nv, int rowb) {
@@ -1879,21 +1993,25 @@ __device__ __forceinline__ void rr_rows32(const Dev& ix, const RrQuery<U8, LPC, 
   const int sub = lane / LPC, sl = lane % LPC;
   const uint8_t* raw = static_cast<const uint8_t*>(ix.raw);
   const int myrow = lane < n32 ? cp[lane] : 0;
-  BBC_CHECK(n32 <= 32 && myrow >= 0 && myrow < ix.n_local);
+  BBC_CHECK(n32 <= 32 && (ER || myrow >= 0) && (myrow < 0 ? ~myrow : myrow) < ix.n_local);
   for (int k0 = 0; k0 < n32; k0 += CPW * STEPS) {
     uint4 x[STEPS][MAXV];
     int kk[STEPS];
     int idr[STEPS];
+    bool done[STEPS];
 #pragma unroll
     for (int s = 0; s < STEPS; ++s) {
       kk[s] = k0 + s * CPW + sub;
-      const int r = __shfl_sync(0xffffffffu, myrow, kk[s] & 31);
+      const int r0 = __shfl_sync(0xffffffffu, myrow, kk[s] & 31);
+      done[s] = ER && r0 < 0;
+      const int r = done[s] ? ~r0 : r0;
       idr[s] = (sl == 0 && kk[s] < n32) ? (int)__ldg(ix.ids + r) : 0;   // original id (final select)
       const uint4* rp = reinterpret_cast<const uint4*>(raw + (size_t)r * rowb);
 #pragma unroll
       for (int v = 0; v < MAXV; ++v) {
         const int t = sl + LPC * v;
-        if (v < per && t < nv) x[s][v] = __ldg(rp + t);
+        if (v < per && t < nv && !done[s]) x[s][v] = __ldg(rp + t);
+        else if (ER) x[s][v] = make_uint4(0u, 0u, 0u, 0u);
       }
     }
 #pragma unroll
@@ -1932,7 +2050,7 @@ __device__ __forceinline__ void rr_rows32(const Dev& ix, const RrQuery<U8, LPC, 
 #pragma unroll
       for (int o = LPC / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (sl == 0 && kk[s] < n32) {
-        vv[kk[s]] = IP ? -acc : acc;
+        if (!done[s]) vv[kk[s]] = IP ? -acc : acc;
         cid[kk[s]] = idr[s];
       }
     }
@@ -1947,7 +2065,7 @@ __device__ __forceinline__ void rr_rows32(const Dev& ix, const RrQuery<U8, LPC, 
 // with one coalesced load and broadcast by shuffle.  Writes exact d^2 to val (fp32, FMA order
 // of the lane split; tolerance 1e-5 relative to the oracle's fp64).
 // ------------------------------------------------------------------------------------------
-template <bool U8, int LPC, int MAXV, int STEPS, int MINB = 1, bool IP = false>
+template <bool U8, int LPC, int MAXV, int STEPS, int MINB = 1, bool IP = false, bool ER = false>
 __global__ void __launch_bounds__(kRrNT, MINB) k_rerank(Batch b, Dev ix) {
   const int q = b.qperm[blockIdx.y];        // neighbours run together: L2 reuse
   const int lane = threadIdx.x & 31, sl = lane % LPC;
@@ -1964,8 +2082,8 @@ __global__ void __launch_bounds__(kRrNT, MINB) k_rerank(Batch b, Dev ix) {
   const int gw = blockIdx.x * (kRrNT / 32) + (threadIdx.x >> 5);
   const int nw = gridDim.x * (kRrNT / 32);
   for (int cb = gw * 32; cb < nc; cb += nw * 32)      // 32 candidates per warp round
-    rr_rows32<U8, LPC, MAXV, STEPS, IP>(ix, Q, cp + cb, min(32, nc - cb), vv + cb, ci + cb, lane, per,
-                                        nv, rowb);
+    rr_rows32<U8, LPC, MAXV, STEPS, IP, ER>(ix, Q, cp + cb, min(32, nc - cb), vv + cb, ci + cb, lane, per,
+                                            nv, rowb);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -2029,7 +2147,7 @@ __global__ void __launch_bounds__(256) k_rr_segments(Batch b, int* __restrict__ 
 // iterations; a global work counter serialises on one address).  The main launch is single-pass
 // (no loop state: no spills at 64 registers); a TAIL launch strides over any pieces beyond its
 // coverage (normally none).  nseg = off[nlist], device-side.
-template <bool U8, int LPC, int MAXV, int STEPS, int MINB, bool IP, int kRrSPW, bool TAIL>
+template <bool U8, int LPC, int MAXV, int STEPS, int MINB, bool IP, int kRrSPW, bool TAIL, bool ER = false>
 __global__ void __launch_bounds__(kRrNT, MINB) k_rerank_seg(Batch b, Dev ix, const int4* __restrict__ seg,
                                                             const int* __restrict__ nseg_p, int first) {
   const int lane = threadIdx.x & 31, sl = lane % LPC;
@@ -2057,8 +2175,8 @@ __global__ void __launch_bounds__(kRrNT, MINB) k_rerank_seg(Batch b, Dev ix, con
       }
       const size_t base = (size_t)q * b.cap + t0;
       for (int cb = 0; cb < len; cb += 32)
-        rr_rows32<U8, LPC, MAXV, STEPS, IP>(ix, Q, b.cpos + base + cb, min(32, len - cb), b.val + base + cb,
-                                            b.cid + base + cb, lane, per, nv, rowb);
+        rr_rows32<U8, LPC, MAXV, STEPS, IP, ER>(ix, Q, b.cpos + base + cb, min(32, len - cb), b.val + base + cb,
+                                                b.cid + base + cb, lane, per, nv, rowb);
     }
   }
 }
