@@ -174,15 +174,15 @@ bbc_status bbc_set_bound_rerank(bbc_index index, int32_t mode, float eps0);
  * bbc_set_early_rerank -- Algorithm 4, the early re-ranking of IVF+PQ (SURVEY 8(f)
  * f2; reading R22).  on = 1: after the sample stage the predicted threshold bucket
  * tau_pred is the bucket of the floor(budget * |O_sample| / n_o)-th (at least the first) smallest
- * sample estimate (l.2-4); the main scan pass computes, right after a work item's
- * bucket ids, the exact distance of every object in a bucket below tau_pred (l.9-11: "we
- * immediately compute its exact distance"); the compaction hands those distances to
- * the candidates among them and the re-rank computes only the remaining candidates' (l.15).
+ * sample estimate (l.2-4); straight after the main scan pass has written the bucket
+ * ids -- before the threshold is known -- every object scanned after the sample whose bucket
+ * lies below tau_pred gets its exact distance (l.9-11: "we immediately compute its exact
+ * distance"; k_early_rows); the compaction hands those distances to the candidates
+ * among them and the re-rank computes only the remaining candidates' (l.15).
  * Results are those of Algorithm 1 (same candidates; early distances are rounded in another
  * order, within the 1e-5 tolerance).  bbc_search_debug reports tau_pred and, per candidate,
  * whether its distance was computed early; bbc_stats_vector entries 7 and 8 count the objects
- * given an early distance and the candidates that used one.  The sample is exactly the nsample
- * lists (the sweep order's sample-pass fill-up is off).  The workspace grows by 4 bytes per
+ * given an early distance and the candidates that used one.  The workspace grows by 4 bytes per
  * probed-object slot per query (query the size after the change).  on = 0 (default): Algorithm 1.
  * BBC_ERR_ARG for a RaBitQ or 4-bit PQ index, a sharded handle, an active remap or another
  * value of on; the sharded paths (bbc_search_group, world > 1) return BBC_ERR_ARG while it is on.

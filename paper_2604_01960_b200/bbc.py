@@ -383,9 +383,9 @@ class Index:
         _check(lib().bbc_set_bound_rerank(self._h, mode, float(eps0)))
 
     def set_early_rerank(self, on: bool) -> None:
-        """Algorithm 4 (early re-ranking of IVF+PQ): the main scan pass computes the
-        exact distance of every object in a bucket below the predicted threshold tau_pred; the
-        re-rank computes the remaining candidates.  Same results as Algorithm 1.  8-bit PQ,
+        """Algorithm 4 (early re-ranking of IVF+PQ): straight after the scan pass,
+        before the threshold is known, every object in a bucket below the predicted threshold
+        tau_pred gets its exact distance; the re-rank computes the remaining candidates.  Same results as Algorithm 1.  8-bit PQ,
         single shard, equal-width buckets."""
         _check(lib().bbc_set_early_rerank(self._h, int(bool(on))))
 

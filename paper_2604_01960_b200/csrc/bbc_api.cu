@@ -273,7 +273,7 @@ void carve(const bbc_index_s* ix, const Plan& p, int nqb, int nqmax, int nprobe,
   // with the sweep order (codes streamed from HBM), the 8-bit PQ scan's sample pass fills its
   // last work item with the following lists (C4 103.4 vs 104.3 ms per step; L2-resident C2,
   // whose sample pass skips the idle warps of its last item, 5.00 vs 4.96 ms: not there)
-  const bool pq8 = ix->kind == BBC_KIND_PQ && ix->nbits == 8 && !ix->early &&   // Alg. 4: sample = nsamp
+  const bool pq8 = ix->kind == BBC_KIND_PQ && ix->nbits == 8 &&
                    (ix->scan_order == BBC_ORDER_SWEEP ||
                     (ix->scan_order == BBC_ORDER_AUTO && (double)ix->n_local * ix->M > 0.5 * (double)ix->l2_bytes));
   b.nest = pq8 ? (int*)take((size_t)nqb * 4) : b.nsamp;
@@ -371,17 +371,6 @@ void launch_rq(bool est, int grid, cudaStream_t st, const Batch& b, const Dev& d
                                                           sweep ? b.sperm : nullptr);                   \
   } while (0)
   if (est) { if (na) BBC_RQ_L(true, true); else BBC_RQ_L(true, false); }
-  else if (b.early && mode == 1) {                   // Algorithm 4: exact distances below tau_pred
-#define BBC_RQ_E(NA)                                                                                     \
-  do {                                                                                                  \
-    set_smem(k_pq_scan_rq<M, false, NA, true>, kRqSmemEarly);                                           \
-    k_pq_scan_rq<M, false, NA, true><<<grid, kRqNT, kRqSmemEarly, st>>>(b, dv, ct, tb, out, stride, mode, \
-                                                                         sweep ? b.items_s : b.items, b.nitems, \
-                                                                         sweep ? b.sperm : nullptr);    \
-  } while (0)
-    if (na) BBC_RQ_E(true); else BBC_RQ_E(false);
-#undef BBC_RQ_E
-  }
   else { if (na) BBC_RQ_L(false, true); else BBC_RQ_L(false, false); }
 #undef BBC_RQ_L
 }
@@ -745,6 +734,13 @@ void stage_scan(Shard& s, cudaStream_t st, bool sample_cells) {
   if (ix->kind == BBC_KIND_PQ) {
     pq_scan(ix, false, st, s.b, s.dv, nullptr, 0, 1);
     g_launches += 1;
+    if (s.b.early) {
+      // Algorithm 4 l.9-11: exact distances of the objects below tau_pred, as soon as the pass
+      // has written the bucket ids and before Update/Collect (timed with the scan stage)
+      const int nchunk = (int)((s.p.cap + kChunk - 1) / kChunk);
+      k_early_rows<<<dim3(std::min(nchunk, 24), nb), kCmpNT, 0, st>>>(s.b, s.dv);
+      g_launches += 1;
+    }
   } else if (ix->rbq_tc) {
     rbq_tc_pass(s, s.b, st, false);
   } else {
@@ -791,7 +787,8 @@ void stage_compact(Shard& s, cudaStream_t st) {
 
   Batch be = s.b;                                   // segment starts only for the list-order re-rank
   if (!rerank_list_order(s.ix, s.b, s.ix->raw_u8 ? s.ix->d : s.ix->d * 4)) be.sstart = nullptr;
-  k_emit<<<dim3(std::min(nchunk, 24), nb), kCmpNT, 0, st>>>(be, s.dv, s.b.chunk, nchunk);
+  if (s.b.early) k_emit<true><<<dim3(std::min(nchunk, 24), nb), kCmpNT, 0, st>>>(be, s.dv, s.b.chunk, nchunk);
+  else k_emit<false><<<dim3(std::min(nchunk, 24), nb), kCmpNT, 0, st>>>(be, s.dv, s.b.chunk, nchunk);
   g_launches += 4;
 }
 
@@ -858,7 +855,7 @@ void stage_alg3(Shard& s, cudaStream_t st) {
       k_chunk_offsets<<<nb, 256, 0, st>>>(s.b, s.b.chunk, nchunk);
       Batch be = s.b;
       if (!rerank_list_order(s.ix, s.b, s.ix->raw_u8 ? s.ix->d : s.ix->d * 4)) be.sstart = nullptr;
-      k_emit<<<dim3(std::min(nchunk, 24), nb), kCmpNT, 0, st>>>(be, s.dv, s.b.chunk, nchunk);
+      k_emit<false><<<dim3(std::min(nchunk, 24), nb), kCmpNT, 0, st>>>(be, s.dv, s.b.chunk, nchunk);
       g_launches += 3;
     }
     stage_rerank(s, st);

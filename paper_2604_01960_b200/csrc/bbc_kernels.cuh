@@ -642,9 +642,6 @@ constexpr int kRqOffCnt = kRqOffOut + kRqGroups * 8;
 constexpr int kRqOffHist = kRqOffCnt + kRqGroups * 4;
 constexpr int kRqOffPo = kRqOffHist + kCells * 4;
 constexpr size_t kRqSmem = kRqOffPo + (kMaxProbe + 1) * 4;
-// Algorithm 4 (EARLY): the first row of every group, after the default layout
-constexpr int kRqOffRow = (int)((kRqSmem + 7) / 8 * 8);
-constexpr size_t kRqSmemEarly = kRqOffRow + kRqGroups * 8;
 // The kernel has no static shared memory, so its dynamic buffer starts right after the 1 KB
 // the driver reserves per CTA; the LUT lookups use that offset as an immediate (checked).
 constexpr unsigned kRqSmemBase = 1024;
@@ -683,11 +680,37 @@ __device__ __forceinline__ float rq_lookup4(float a, uint32_t w, uint32_t lane4)
 // 2: all lists -> estimates (debug)
 // NOALLOC: code loads bypass L1 allocation (codes larger than L2 are streamed once from HBM:
 // C4/C5 +1.5 %; L2-resident codes (C2) are faster through L1)
-// EARLY (Algorithm 4; main pass only): after a work item's bucket ids are written,
-// every object in a bucket below the query's predicted threshold tau_pred gets its exact distance
-// at once -- one warp per row, 16 bytes per lane, coalesced -- stored at its probe-order position
-// in b.early for the compaction to pick up (emit_chunk).
-template <int M, bool EST, bool NOALLOC = false, bool EARLY = false>
+// Algorithm 4: the contribution of 16 row bytes (chunk t) to the exact key: sum (x - q)^2, or
+// sum x q for the inner product; fp32 rows hold 4 values per chunk, uint8 rows 16.
+__device__ __forceinline__ float early_part(float a, const uint4& x, const float* __restrict__ qv, int t,
+                                            bool u8, bool ipm) {
+  if (u8) {
+    const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const float4 y = __ldg(reinterpret_cast<const float4*>(qv) + 4 * t + h);
+      const float ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+      for (int by = 0; by < 4; ++by) {
+        const float xv = (float)((wv[h] >> (8 * by)) & 255u);
+        if (ipm) a = fmaf(xv, ys[by], a);
+        else { const float df = xv - ys[by]; a = fmaf(df, df, a); }
+      }
+    }
+  } else {
+    const float4 y = __ldg(reinterpret_cast<const float4*>(qv) + t);
+    const float xs[4] = {__uint_as_float(x.x), __uint_as_float(x.y), __uint_as_float(x.z), __uint_as_float(x.w)};
+    const float ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      if (ipm) a = fmaf(xs[h], ys[h], a);
+      else { const float df = xs[h] - ys[h]; a = fmaf(df, df, a); }
+    }
+  }
+  return a;
+}
+
+template <int M, bool EST, bool NOALLOC = false>
 __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const uint8_t* __restrict__ codes_t,
                                                          const long long* __restrict__ tbase,
                                                          float* out_est, long long est_stride,
@@ -702,7 +725,6 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
   int* gcnt = reinterpret_cast<int*>(rsm + kRqOffCnt);
   int* hist = reinterpret_cast<int*>(rsm + kRqOffHist);
   int* s_popad = reinterpret_cast<int*>(rsm + kRqOffPo);
-  long long* grow = reinterpret_cast<long long*>(rsm + kRqOffRow);   // EARLY only (kRqSmemEarly)
   // persistent CTAs over the work items of k_scan_plan: (query, pass) in query locality order
   // (probe order) or sorted by their first list (sweep order)
   const int nit = *nitems;
@@ -760,7 +782,6 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
       BBC_CHECK(((long long)go << 7) + (long long)M * 32 <= ix.ct_bytes);
       oo = obase + po[j] + i0;
       BBC_CHECK(po[j] + i0 + cnt <= (EST ? est_stride : b.cap));
-      if (EARLY) grow[G] = ix.loff[L] + i0;
     }
     gofs[G] = go;
     gout[G] = oo;
@@ -858,65 +879,6 @@ __global__ void __launch_bounds__(kRqNT, 1) k_pq_scan_rq(Batch b, Dev ix, const 
         }
       }
     }
-  }
-  if (EARLY) {
-    // Alg. 4 l.9-11: a_i < tau_pred -> exact distance now.  The lane's early objects are taken
-    // one at a time by the whole warp (ballot, lowest lane first): lane t loads 16 bytes of the
-    // row and of the query (rows of up to 512 bytes: fp32 d <= 128, uint8 d <= 512), warp sum.
-    const int tp = b.tpred[q];
-    const int rowb = ix.raw_u8 ? ix.d : ix.d * 4;
-    const int nv = rowb >> 4;
-    const uint8_t* raw = static_cast<const uint8_t*>(ix.raw);
-    const float* qv = b.Q + (size_t)q * ix.d;
-    const bool ipm = ix.metric == BBC_METRIC_IP;
-    int nearly = 0;
-#pragma unroll 1
-    for (int i = 0; i < kRqGPL; ++i) {
-      const int G = gl0 + 4 * i;
-      const int cnt = gcnt[G];
-      const long long oo = gout[G] + 4 * (lane & 7);
-      const long long r0 = grow[G] + 4 * (lane & 7);
-#pragma unroll 1
-      for (int j = 0; j < 4; ++j) {
-        const bool mine = 4 * (lane & 7) + j < cnt && (int)b.cells[oo + j] < tp;   // the id this lane just wrote
-        unsigned m = __ballot_sync(0xffffffffu, mine);
-        nearly += __popc(m);
-        while (m) {
-          const int src = __ffs(m) - 1;
-          m &= m - 1;
-          const long long row = __shfl_sync(0xffffffffu, r0 + j, src);
-          const long long at = __shfl_sync(0xffffffffu, oo + j, src);
-          BBC_CHECK(row >= 0 && row < ix.n_local);
-          float a = 0.f;
-          for (int t = lane; t < nv; t += 32) {
-            const uint4 x = __ldg(reinterpret_cast<const uint4*>(raw + (size_t)row * rowb) + t);
-            if (ix.raw_u8) {
-              const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-              for (int h = 0; h < 4; ++h)
-#pragma unroll
-                for (int by = 0; by < 4; ++by) {
-                  const float xv = (float)((wv[h] >> (8 * by)) & 255u), qq = __ldg(qv + t * 16 + h * 4 + by);
-                  if (ipm) a = fmaf(xv, qq, a);
-                  else { const float df = xv - qq; a = fmaf(df, df, a); }
-                }
-            } else {
-              const float4 y = __ldg(reinterpret_cast<const float4*>(qv) + t);
-              const float xs[4] = {__uint_as_float(x.x), __uint_as_float(x.y), __uint_as_float(x.z), __uint_as_float(x.w)};
-              const float ys[4] = {y.x, y.y, y.z, y.w};
-#pragma unroll
-              for (int h = 0; h < 4; ++h) {
-                if (ipm) a = fmaf(xs[h], ys[h], a);
-                else { const float df = xs[h] - ys[h]; a = fmaf(df, df, a); }
-              }
-            }
-          }
-          a = warp_sum(a);
-          if (lane == 0) b.early[at] = ipm ? -a : a;
-        }
-      }
-    }
-    if (lane == 0 && nearly) atomicAdd((unsigned long long*)&b.stats[5], (unsigned long long)nearly);
   }
   if (!EST) {
     __syncthreads();
@@ -1799,7 +1761,9 @@ __device__ __forceinline__ EmitMeta emit_meta(const Batch& b, const int* chunk_o
   return m;
 }
 
-__device__ __forceinline__ void emit_chunk(const Batch& b, const Dev& ix, const int* chunk_off, int nchunk, int q,
+// returns the number of candidates of the chunk that took an early distance (EARLY; per thread)
+template <bool EARLY>
+__device__ __forceinline__ int emit_chunk(const Batch& b, const Dev& ix, const int* chunk_off, int nchunk, int q,
                                            int c, const Cells32& cx, EmitSmem& sm, const EmitMeta& mt) {
   int* wcnt = sm.wcnt;
   int* s_pre = sm.s_pre;
@@ -1816,10 +1780,10 @@ __device__ __forceinline__ void emit_chunk(const Batch& b, const Dev& ix, const 
   const int tau = b.tau[q];
   const int ncq = b.ncand[q];
   const int cbeg = mt.cbeg, cnext = mt.cnext, jc = mt.jc, jnext = mt.jnext;
-  if (c * kChunk >= n) return;
+  if (c * kChunk >= n) return 0;
   const int need = (n + kChunk - 1) / kChunk;        // chunks without candidates exit at once
   const int cend = c + 1 < need ? cnext : ncq;
-  if (cend == cbeg) return;                           // segment starts here: rr_segment
+  if (cend == cbeg) return 0;                         // segment starts here: rr_segment
   const long long* rb = b.rbase + (size_t)q * nprobe;
   const int jn = (c + 1) * kChunk < n ? jnext : nprobe - 1;
   const int W = jn - jc + 1;                          // lists touching this chunk
@@ -1849,8 +1813,9 @@ __device__ __forceinline__ void emit_chunk(const Batch& b, const Dev& ix, const 
   // Algorithm 4: candidates the main scan pass already gave an exact distance (bucket below
   // tau_pred, position after the sample) take it from b.early and leave with the row complemented
   // (negative): the re-rank then only looks up their ids
-  const int tp = b.early ? b.tpred[q] : 0;
-  const int emain = b.early ? po[b.nsamp[q]] : 0;
+  const int tp = EARLY ? b.tpred[q] : 0;
+  const int emain = EARLY ? po[b.nsamp[q]] : 0;
+  const unsigned fe = EARLY && tp > 0 ? chunk_flags(cx, i0, n, tp - 1) : 0u;   // cell < tau_pred
   int ntaken = 0;
   s_pre[threadIdx.x] = pos;
   s_flg[threadIdx.x] = f;
@@ -1877,7 +1842,7 @@ __device__ __forceinline__ void emit_chunk(const Batch& b, const Dev& ix, const 
       BBC_CHECK(cbeg + pos < b.cap && rbase + i >= 0 && rbase + i < ix.n_local);
       if (b.a3pos) b.a3pos[(size_t)q * b.cap + cbeg + pos] = i;   // Algorithm 3 (list mode)
       int row = (int)(rbase + i);
-      if (b.early && i >= emain && (int)b.cells[(size_t)q * b.cap + i] < tp) {
+      if (EARLY && ((fe >> (i - i0)) & 1u) && i >= emain) {
         b.val[(size_t)q * b.cap + cbeg + pos] = b.early[(size_t)q * b.cap + i];
         row = ~row;
         ++ntaken;
@@ -1885,7 +1850,6 @@ __device__ __forceinline__ void emit_chunk(const Batch& b, const Dev& ix, const 
       outp[pos++] = row;
     }
   }
-  if (ntaken) atomicAdd((unsigned long long*)&b.stats[6], (unsigned long long)ntaken);
   __syncthreads();
   if (b.sstart) {
     // list-order re-rank: candidates before the start of every pair whose object range starts
@@ -1909,17 +1873,117 @@ __device__ __forceinline__ void emit_chunk(const Batch& b, const Dev& ix, const 
       ss[j] = cbeg + s_pre[th] + __popc(s_flg[th] & ((1u << bit) - 1u));
     }
   }
+  return ntaken;
+}
 
+// ------------------------------------------------------------------------------------------
+// f2  Algorithm 4 l.9-11: the exact distance of every object of the main
+// pass whose bucket lies below tau_pred, taken straight after the scan pass has written the
+// bucket ids -- before Update and Collect know tau.  CTA (x, query) walks the query's chunks of
+// bucket ids past the sample (32 ids per thread, two 16-byte loads; flags by chunk_flags against
+// tau_pred - 1); a thread finds the list of its first early object by binary search and walks
+// forward; the warp then takes the lanes' early objects four at a time: lane t loads 16 bytes of
+// each row (all four loads issued before the arithmetic) and of the query, one warp sum per row,
+// stored at the object's probe-order position in b.early for k_emit<EARLY> to hand over.
+// (Computing them inside the scan kernel, at the end of each work item, was measured first: the
+// few warps that chase row latencies hold the whole CTA at the item's barrier and the extra live
+// state spills the lookup loop -- C4 scan 48.7 -> 61.3 ms.)
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kCmpNT) k_early_rows(Batch b, Dev ix) {
+  const int q = blockIdx.y;
+  const int tp = b.tpred[q];
+  if (tp <= 0) return;
+  const int nprobe = b.nprobe;
+  const int* po = b.poff + (size_t)q * (nprobe + 1);
+  const int n = po[nprobe];
+  const int emain = po[b.nsamp[q]];                  // first object after the sample
+  const int need = (n + kChunk - 1) / kChunk;
+  const long long* rb = b.rbase + (size_t)q * nprobe;
+  const int lane = threadIdx.x & 31;
+  const int rowb = ix.raw_u8 ? ix.d : ix.d * 4;
+  const int nv = rowb >> 4;
+  const uint8_t* raw = static_cast<const uint8_t*>(ix.raw);
+  const float* qv = b.Q + (size_t)q * ix.d;
+  const bool ipm = ix.metric == BBC_METRIC_IP, u8 = ix.raw_u8 != 0;
+  float* out = b.early + (size_t)q * b.cap;
+  int cnt = 0;
+  for (int c = emain / kChunk + blockIdx.x; c < need; c += gridDim.x) {
+    const Cells32 cx = emit_cells(b, q, c);
+    const int i0 = c * kChunk + threadIdx.x * kPerThr;
+    unsigned f = chunk_flags(cx, i0, n, tp - 1);      // bucket < tau_pred
+    if (i0 + kPerThr <= emain) f = 0;                 // the sample's objects are not early (R22)
+    else if (i0 < emain) f &= ~((1u << (emain - i0)) - 1u);
+    cnt += __popc(f);
+    int j = 0, jend = 0;
+    long long rbase = 0;
+    if (f) {                                          // list of the first early object
+      const int ifirst = i0 + __ffs(f) - 1;
+      int lo = 0, hi = nprobe - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (po[mid] <= ifirst) lo = mid; else hi = mid - 1;
+      }
+      j = lo;
+      jend = po[j + 1];
+      rbase = rb[j];
+    }
+    while (__any_sync(0xffffffffu, f != 0)) {
+      int pos = -1, myrow = 0;
+      if (f) {
+        pos = i0 + __ffs(f) - 1;
+        f &= f - 1;
+        while (pos >= jend) {                         // next non-empty list containing pos
+          ++j;
+          jend = po[j + 1];
+          rbase = rb[j];
+        }
+        myrow = (int)(rbase + pos);
+        BBC_CHECK(j < nprobe && myrow >= 0 && myrow < ix.n_local && pos < b.cap);
+      }
+      unsigned m = __ballot_sync(0xffffffffu, pos >= 0);
+      while (m) {                                     // four rows in flight per round
+        int src[4], row[4], at[4];
+        float a[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          src[u] = m ? __ffs(m) - 1 : -1;
+          m &= m - 1;                                 // 0 stays 0
+          a[u] = 0.f;
+          row[u] = __shfl_sync(0xffffffffu, myrow, src[u] & 31);
+          at[u] = __shfl_sync(0xffffffffu, pos, src[u] & 31);
+        }
+        for (int t = lane; t - lane < nv; t += 32) {
+          uint4 x[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (src[u] >= 0 && t < nv) x[u] = __ldg(reinterpret_cast<const uint4*>(raw + (size_t)row[u] * rowb) + t);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (src[u] >= 0 && t < nv) a[u] = early_part(a[u], x[u], qv, t, u8, ipm);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (src[u] >= 0) {                          // uniform: m is the same in every lane
+            const float r = warp_sum(a[u]);
+            if (lane == 0) out[at[u]] = ipm ? -r : r;
+          }
+      }
+    }
+  }
+  cnt = warp_sum(cnt);                                // one counter update per warp
+  if (lane == 0 && cnt) atomicAdd((unsigned long long*)&b.stats[5], (unsigned long long)cnt);
 }
 
 // CTA (x, query) takes chunks x, x + gridDim.x, ...: the grid covers the queries' real chunks
 // without one CTA per chunk of the capacity (most of which, past the query's probed objects, had
 // only to exit: C4 ~58 % of 735k CTAs)
+template <bool EARLY = false>
 __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chunk_off, int nchunk) {
   __shared__ EmitSmem sm;
   const int q = blockIdx.y;
   const int n = b.poff[(size_t)q * (b.nprobe + 1) + b.nprobe];
   const int need = (n + kChunk - 1) / kChunk;
+  int taken = 0;
   // the next chunk's cells and offsets load ahead
   Cells32 nx = emit_cells(b, q, blockIdx.x);
   EmitMeta nm{0, 0, 0, 0};
@@ -1932,7 +1996,11 @@ __global__ void __launch_bounds__(kCmpNT) k_emit(Batch b, Dev ix, const int* chu
       nx = emit_cells(b, q, c + gridDim.x);
       nm = emit_meta(b, chunk_off, nchunk, q, c + gridDim.x);
     }
-    emit_chunk(b, ix, chunk_off, nchunk, q, c, cx, sm, mt);
+    taken += emit_chunk<EARLY>(b, ix, chunk_off, nchunk, q, c, cx, sm, mt);
+  }
+  if (EARLY) {                                       // one counter update per warp per CTA
+    taken = warp_sum(taken);
+    if ((threadIdx.x & 31) == 0 && taken) atomicAdd((unsigned long long*)&b.stats[6], (unsigned long long)taken);
   }
 }
 

@@ -26,7 +26,9 @@ CASES = [("C1t", None, None, None, "probe"), ("C1t", None, None, None, "sweep"),
          ("C4s", None, None, None, "probe"), ("C5s", None, None, None, "sweep"),
          ("C4ip_s", None, None, None, "sweep"), ("C2s", None, None, None, "group-sweep"),
          ("C3a3", None, None, None, "alg3"), ("C3a3u8", None, None, None, "alg3"),
-         ("C3a3", None, 3, 10 ** 6, "alg3")]    # Algorithm 3 (f1): finite tau, uint8 rows, no sample
+         ("C3a3", None, 3, 10 ** 6, "alg3"),    # Algorithm 3 (f1): finite tau, uint8 rows, no sample
+         ("C2s", None, 12, 18_000, "alg4"), ("C5s", None, 12, 30_000, "alg4"),   # Algorithm 4 (f2): many
+         ("C4ip_s", None, None, None, "alg4")]                                   # early objects; uint8; IP
 
 SCRIPT = r"""
 import json, sys
@@ -53,6 +55,10 @@ for i, (name, k, nprobe, budget, order) in enumerate(json.loads(sys.argv[2])):
         ids, d2 = g.search(q, k, nprobe, budget)
         o = torch.argsort(ids, dim=1)                 # candidate order unspecified: sort by id
         ids, d2 = ids.gather(1, o), d2.gather(1, o)
+    elif order == "alg4":
+        g = Index(path)
+        g.set_early_rerank(True)
+        ids, d2 = g.search(q, k, nprobe, budget)
     else:
         g = Index(path)
         g.set_scan_order(g.ORDER_SWEEP if order == "sweep" else g.ORDER_PROBE)
