@@ -1907,8 +1907,11 @@ __global__ void __launch_bounds__(kCmpNT) k_early_rows(Batch b, Dev ix) {
   const bool ipm = ix.metric == BBC_METRIC_IP, u8 = ix.raw_u8 != 0;
   float* out = b.early + (size_t)q * b.cap;
   int cnt = 0;
-  for (int c = emain / kChunk + blockIdx.x; c < need; c += gridDim.x) {
-    const Cells32 cx = emit_cells(b, q, c);
+  const int c0 = emain / kChunk + blockIdx.x;
+  Cells32 nx = emit_cells(b, q, c0 < need ? c0 : 0);  // the next chunk's ids load ahead
+  for (int c = c0; c < need; c += gridDim.x) {
+    const Cells32 cx = nx;
+    if (c + (int)gridDim.x < need) nx = emit_cells(b, q, c + gridDim.x);
     const int i0 = c * kChunk + threadIdx.x * kPerThr;
     unsigned f = chunk_flags(cx, i0, n, tp - 1);      // bucket < tau_pred
     if (i0 + kPerThr <= emain) f = 0;                 // the sample's objects are not early (R22)
