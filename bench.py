@@ -75,8 +75,8 @@ def parse():
                    help="RaBitQ: Algorithm 3's bound-aware re-rank with this eps0 (1.9 in the paper) "
                         "instead of Algorithm 1's superset (f1; measurement, not the headline)")
     p.add_argument("--early-rerank", action="store_true",
-                   help="f2: Algorithm 4 (early re-ranking of IVF+PQ, 8-bit codes): the main scan pass "
-                        "computes the exact distance of objects in buckets below tau_pred")
+                   help="f2: Algorithm 4 (early re-ranking of IVF+PQ, 8-bit codes): objects in buckets below "
+                        "tau_pred get their exact distance straight after the scan pass")
     p.add_argument("--bound-rerank-gathers", choices=("list", "query"), default="list",
                    help="Algorithm 3's exact distances: every candidate's in list order, or B_exact's per query")
     p.add_argument("--bucket-sweep", action="store_true",
@@ -572,7 +572,7 @@ def main():
                    **({} if args.bound_rerank is None else
                       {"rerank": f"Algorithm 3 (bound-aware, eps0 = {args.bound_rerank}, "
                                  f"{args.bound_rerank_gathers}-order gathers)"}),
-                   **({"rerank": "Algorithm 4 (early re-ranking in the scan pass)",
+                   **({"rerank": "Algorithm 4 (early re-ranking: exact distances below tau_pred straight after the scan pass)",
                        "early_objects_per_query": stats["early_objects"] / nq,
                        "early_candidates_per_query": stats["early_candidates"] / nq}
                       if args.early_rerank else {}),
